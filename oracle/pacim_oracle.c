@@ -1,0 +1,567 @@
+/*
+ * pacim_oracle.c — plain, slow, single-threaded CPU ORACLE for the PaC-IM hot
+ * path (arXiv 2311.07554).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference leg may load this library.  It
+ * shares no code, header, table or constant generator with the CUDA path in
+ * paper_2311_07554_b200/ and never imports it.
+ *
+ * Citation keys: P:n = /root/reference/PAPER.md line n (section named beside
+ * it); DESIGN.md §"Readings" (R1..R12) lists every choice the paper leaves open.
+ *
+ * Everything is integer; results are defined exactly (no tolerance).
+ *
+ * Functions and what pins them (tests/test_oracle_*.py):
+ *   orc_mix64 ............ published splitmix64 output vectors (pinned)
+ *   orc_t32_const/wic .... closed forms p=0,1/2,1 and 2/(du+dv) (pinned)
+ *   orc_live ............. symmetry, p=0/1 extremes, live fraction ~ p (pinned, statistical)
+ *   orc_sketch_labels .... scipy connected_components on the materialised
+ *                          sampled graph; p=0 / p=1 special cases (pinned)
+ *   orc_greedy ........... brute-force set-union greedy on tiny inputs, closed
+ *                          forms (p=0, p=1, star, path), (1-1/e)*OPT, exact
+ *                          sigma by 2^m world enumeration across hash seeds (pinned)
+ *   orc_compressed_sketch / orc_get_center / orc_greedy_alg3 ....
+ *                          Alg. 3 transcribed; pinned by SPEC-style trivia and
+ *                          by equality with orc_greedy (compression transparency)
+ *   orc_gen_* ............ input generators (not method arithmetic); pinned by
+ *                          structural invariants and exact edge counts.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+
+#define ORC_UNSET 0xFFFFFFFFu
+
+/* ------------------------------------------------------------------------ */
+/* Hash (Implementation notes; reading R1-R3 in DESIGN.md)            */
+/* ------------------------------------------------------------------------ */
+
+/* R1: `hash` is the splitmix64 finalizer (unnamed in P:3). */
+uint64_t orc_mix64(uint64_t z)
+{
+    z ^= z >> 30;
+    z *= 0xBF58476D1CE4E5B9ull;
+    z ^= z >> 27;
+    z *= 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    return z;
+}
+
+/* R2: K = mix64(hash_seed); hash(r) = mix64((2^63 | r) xor K). */
+uint64_t orc_hash_r(uint64_t hash_seed, uint32_t r)
+{
+    uint64_t K = orc_mix64(hash_seed);
+    return orc_mix64(((1ull << 63) | (uint64_t)r) ^ K);
+}
+
+/* R2: hash(min(u,v) << 32 | max(u,v)) keyed by K (P:3). */
+uint64_t orc_hash_e(uint64_t hash_seed, uint32_t u, uint32_t v)
+{
+    uint64_t K = orc_mix64(hash_seed);
+    uint64_t a = u < v ? u : v, b = u < v ? v : u;
+    return orc_mix64(((a << 32) | b) ^ K);
+}
+
+/* P:3: hash_edge(u,v,r) = hash(r) xor hash(min<<32|max). */
+uint64_t orc_hash_edge(uint64_t hash_seed, uint32_t u, uint32_t v, uint32_t r)
+{
+    return orc_hash_r(hash_seed, r) ^ orc_hash_e(hash_seed, u, v);
+}
+
+/* R3: p quantised to T32 = floor(p * 2^32) in IEEE double; p=1 -> 2^32. */
+uint64_t orc_t32_const(double p)
+{
+    if (!(p > 0.0)) return 0;
+    if (p >= 1.0) return 1ull << 32;
+    return (uint64_t)floor(p * 4294967296.0);
+}
+
+/* R4: WIC p(u,v) = 2/(d_u+d_v), capped at 1:
+ *     T32 = min(2^32, floor(2^33 / (d_u + d_v))). */
+uint64_t orc_t32_wic(uint64_t du, uint64_t dv)
+{
+    uint64_t s = du + dv;
+    if (s == 0) return 1ull << 32;
+    uint64_t t = (1ull << 33) / s;
+    return t > (1ull << 32) ? (1ull << 32) : t;
+}
+
+/* P:4: edge (u,v) is in the r-th sampled graph iff hash_edge(u,v,r) < p(u,v);
+ * R3: with p quantised to T32 this is hash_edge < T32 * 2^32. */
+int orc_live(uint64_t hash_seed, uint32_t u, uint32_t v, uint32_t r, uint64_t t32)
+{
+    uint64_t h = orc_hash_edge(hash_seed, u, v, r);
+    if (t32 >= (1ull << 32)) return 1;
+    return h < (t32 << 32);
+}
+
+/* Probability model of an edge of the CSR graph: 0 = constant T32, 1 = WIC. */
+static uint64_t edge_t32(int model, uint64_t t32, const uint64_t *off,
+                         uint32_t u, uint32_t v)
+{
+    if (model == 1)
+        return orc_t32_wic(off[u + 1] - off[u], off[v + 1] - off[v]);
+    return t32;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Sketch(r): connected components of G'_r (Alg. 3)         */
+/* ------------------------------------------------------------------------ */
+
+/*
+ * label[v] = smallest vertex id in v's CC of G'_r (reading R8: canonical
+ * label); if size_of_v != NULL, size_of_v[v] = |C_r(v)|.  Plain BFS from every
+ * unlabelled vertex in ascending id order, testing liveness of each adjacency
+ * entry with the hash rule.  Returns the number of CCs, or -1 on OOM.
+ */
+long orc_sketch_labels(uint32_t n, const uint64_t *off, const uint32_t *nbr,
+                       int model, uint64_t t32, uint64_t hash_seed, uint32_t r,
+                       uint32_t *label, uint32_t *size_of_v)
+{
+    uint32_t *queue = (uint32_t *)malloc((size_t)(n ? n : 1) * sizeof(uint32_t));
+    if (!queue) return -1;
+    for (uint32_t v = 0; v < n; v++) label[v] = ORC_UNSET;
+    long ncc = 0;
+    for (uint32_t v = 0; v < n; v++) {
+        if (label[v] != ORC_UNSET) continue;
+        size_t head = 0, tail = 0;
+        label[v] = v;
+        queue[tail++] = v;
+        while (head < tail) {
+            uint32_t x = queue[head++];
+            for (uint64_t e = off[x]; e < off[x + 1]; e++) {
+                uint32_t w = nbr[e];
+                if (label[w] != ORC_UNSET) continue;
+                if (orc_live(hash_seed, x, w, r, edge_t32(model, t32, off, x, w))) {
+                    label[w] = v;
+                    queue[tail++] = w;
+                }
+            }
+        }
+        if (size_of_v)
+            for (size_t i = 0; i < tail; i++) size_of_v[queue[i]] = (uint32_t)tail;
+        ncc++;
+    }
+    free(queue);
+    return ncc;
+}
+
+/* BFS of C_r(s) over live edges; writes members to out[], returns count.
+ * stamp[] is a caller-owned visited array compared against `tag`. */
+static size_t bfs_component(uint32_t s, const uint64_t *off, const uint32_t *nbr,
+                            int model, uint64_t t32, uint64_t hash_seed,
+                            uint32_t r, uint32_t *stamp, uint32_t tag,
+                            uint32_t *out)
+{
+    size_t head = 0, tail = 0;
+    stamp[s] = tag;
+    out[tail++] = s;
+    while (head < tail) {
+        uint32_t x = out[head++];
+        for (uint64_t e = off[x]; e < off[x + 1]; e++) {
+            uint32_t w = nbr[e];
+            if (stamp[w] == tag) continue;
+            if (orc_live(hash_seed, x, w, r, edge_t32(model, t32, off, x, w))) {
+                stamp[w] = tag;
+                out[tail++] = w;
+            }
+        }
+    }
+    return tail;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Greedy over R fixed sketches (P:396-401 GeneralGreedy;   */
+/* memoised CC influence P:597-601; Alg. 1; tie by id P:2285-2286)  */
+/* ------------------------------------------------------------------------ */
+
+/*
+ * Derive mode.  N(S) = sum_r |reach_{G'_r}(S)|.  gain[v] starts at
+ * sum_r |C_r(v)| (= R * Marginal(empty, v)); each step picks the
+ * smallest-id v not in S with maximal gain (R5, R6), records gain_num =
+ * N(S+s) - N(S) and sigma_num = N(S+s), then for every sketch where C_r(s) is
+ * not yet covered, marks it covered and subtracts |C_r(s)| from the gain of
+ * each of its members (found by BFS over live edges).
+ *
+ * gain0 (optional, n entries) receives the initial gains.  Returns 0, -1 on
+ * OOM, -2 if the per-step cross-check sum_r delta_r == gain[s] fails.
+ */
+int orc_greedy(uint32_t n, const uint64_t *off, const uint32_t *nbr, int model,
+               uint64_t t32, uint32_t R, uint64_t hash_seed, uint32_t k,
+               uint32_t *seeds, int64_t *gain_num, int64_t *sigma_num,
+               int64_t *gain0)
+{
+    int rc = 0;
+    uint32_t *labels = (uint32_t *)malloc((size_t)R * n * sizeof(uint32_t));
+    uint32_t *sizev = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+    int64_t *gain = (int64_t *)calloc(n, sizeof(int64_t));
+    uint8_t *is_seed = (uint8_t *)calloc(n, 1);
+    uint8_t *covered = (uint8_t *)calloc(((size_t)R * n + 7) / 8, 1);
+    uint32_t *stamp = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+    uint32_t *members = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+    if (!labels || !sizev || !gain || !is_seed || !covered || !stamp || !members) {
+        rc = -1;
+        goto done;
+    }
+    /* Step 1 of Alg. 1: every sketch; gain[v] += |C_r(v)|. */
+    for (uint32_t r = 0; r < R; r++) {
+        if (orc_sketch_labels(n, off, nbr, model, t32, hash_seed, r,
+                              labels + (size_t)r * n, sizev) < 0) {
+            rc = -1;
+            goto done;
+        }
+        for (uint32_t v = 0; v < n; v++) gain[v] += sizev[v];
+    }
+    if (gain0) memcpy(gain0, gain, (size_t)n * sizeof(int64_t));
+    for (uint32_t v = 0; v < n; v++) stamp[v] = 0;
+    uint32_t tag = 0;
+    int64_t sigma = 0;
+    /* Step 2 of Alg. 1: k greedy steps. */
+    for (uint32_t i = 0; i < k; i++) {
+        int64_t best = -1;
+        uint32_t s = 0;
+        for (uint32_t v = 0; v < n; v++)
+            if (!is_seed[v] && gain[v] > best) { best = gain[v]; s = v; }
+        int64_t dsum = 0;
+        for (uint32_t r = 0; r < R; r++) {
+            uint32_t c = labels[(size_t)r * n + s];
+            size_t bit = (size_t)r * n + c;
+            if (covered[bit >> 3] & (1u << (bit & 7))) continue; /* delta_r = 0 */
+            covered[bit >> 3] |= (uint8_t)(1u << (bit & 7));
+            if (++tag == 0) { /* wrap: reset stamps */
+                for (uint32_t v = 0; v < n; v++) stamp[v] = 0;
+                tag = 1;
+            }
+            size_t sz = bfs_component(s, off, nbr, model, t32, hash_seed, r,
+                                      stamp, tag, members);
+            dsum += (int64_t)sz;
+            for (size_t j = 0; j < sz; j++) gain[members[j]] -= (int64_t)sz;
+        }
+        if (dsum != best) rc = -2;
+        is_seed[s] = 1;
+        sigma += best;
+        seeds[i] = s;
+        gain_num[i] = best;
+        sigma_num[i] = sigma;
+    }
+done:
+    free(labels); free(sizev); free(gain); free(is_seed); free(covered);
+    free(stamp); free(members);
+    return rc;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Compressed sketches (Alg. 3; §3)       */
+/* ------------------------------------------------------------------------ */
+
+/* R9: v is a center iff hi32(mix64(v xor K_c)) < A32,
+ *     K_c = mix64(hash_seed xor 0x9E3779B97F4A7C15). A32 >= 2^32: all. */
+int orc_is_center(uint64_t hash_seed, uint32_t v, uint64_t a32)
+{
+    if (a32 >= (1ull << 32)) return 1;
+    uint64_t Kc = orc_mix64(hash_seed ^ 0x9E3779B97F4A7C15ull);
+    return (orc_mix64((uint64_t)v ^ Kc) >> 32) < a32;
+}
+
+/* centers c_0 < c_1 < ... in vertex order; returns rho.  center_of[v] = index
+ * or ORC_UNSET.  ("randomly selected centers".) */
+uint32_t orc_centers(uint32_t n, uint64_t hash_seed, uint64_t a32,
+                     uint32_t *centers, uint32_t *center_of)
+{
+    uint32_t rho = 0;
+    for (uint32_t v = 0; v < n; v++) {
+        if (orc_is_center(hash_seed, v, a32)) {
+            if (center_of) center_of[v] = rho;
+            if (centers) centers[rho] = v;
+            rho++;
+        } else if (center_of) {
+            center_of[v] = ORC_UNSET;
+        }
+    }
+    return rho;
+}
+
+/*
+ * Sketch(r) of Alg. 3: CCs of G'_r; for each center c_i,
+ * label[i] = min{ j : c_j in the same CC as c_i };
+ * size[i] = CC size of c_i when label[i] = i, else 0.
+ * Sizes count all vertices of the CC (reading R10).
+ */
+int orc_compressed_sketch(uint32_t n, const uint64_t *off, const uint32_t *nbr,
+                          int model, uint64_t t32, uint64_t hash_seed,
+                          uint32_t r, uint64_t a32, uint32_t *clabel,
+                          uint32_t *csize)
+{
+    uint32_t *label = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+    uint32_t *sizev = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+    uint32_t *first_center = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+    if (!label || !sizev || !first_center) {
+        free(label); free(sizev); free(first_center);
+        return -1;
+    }
+    orc_sketch_labels(n, off, nbr, model, t32, hash_seed, r, label, sizev);
+    for (uint32_t v = 0; v < n; v++) first_center[v] = ORC_UNSET;
+    uint32_t i = 0;
+    for (uint32_t v = 0; v < n; v++) {
+        if (!orc_is_center(hash_seed, v, a32)) continue;
+        uint32_t cc = label[v];
+        if (first_center[cc] == ORC_UNSET) first_center[cc] = i; /* min j */
+        clabel[i] = first_center[cc];
+        csize[i] = (clabel[i] == i) ? sizev[v] : 0;
+        i++;
+    }
+    free(label); free(sizev); free(first_center);
+    return (int)i;
+}
+
+/*
+ * GetCenter(S_r, v, S) of Alg. 3: BFS from v on
+ * G'_r with a local queue.  Each dequeued vertex is first checked for
+ * being a center (-> return <size[label[i]], label[i]>; reading R12/R13), then
+ * for being a seed.  If the BFS exhausts the CC without a center it returns
+ * <0,-1> when a seed was visited, else <n',-1>.  *visits = dequeued count.
+ */
+void orc_get_center(uint32_t n, const uint64_t *off, const uint32_t *nbr,
+                    int model, uint64_t t32, uint64_t hash_seed, uint32_t r,
+                    const uint32_t *center_of, const uint32_t *clabel,
+                    const uint32_t *csize, const uint8_t *is_seed, uint32_t v,
+                    int64_t *delta, int64_t *l, uint64_t *visits)
+{
+    uint32_t *queue = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+    uint8_t *seen = (uint8_t *)calloc(n, 1);
+    size_t head = 0, tail = 0;
+    int seed_seen = 0;
+    *delta = 0; *l = -1;
+    seen[v] = 1;
+    queue[tail++] = v;
+    while (head < tail) {
+        uint32_t x = queue[head++];
+        if (center_of[x] != ORC_UNSET) {
+            uint32_t lab = clabel[center_of[x]];
+            *delta = csize[lab];
+            *l = lab;
+            *visits = head;
+            free(queue); free(seen);
+            return;
+        }
+        if (is_seed && is_seed[x]) seed_seen = 1;
+        for (uint64_t e = off[x]; e < off[x + 1]; e++) {
+            uint32_t w = nbr[e];
+            if (seen[w]) continue;
+            if (orc_live(hash_seed, x, w, r, edge_t32(model, t32, off, x, w))) {
+                seen[w] = 1;
+                queue[tail++] = w;
+            }
+        }
+    }
+    *visits = head;
+    *delta = seed_seen ? 0 : (int64_t)tail;
+    *l = -1;
+    free(queue); free(seen);
+}
+
+/*
+ * Exhaustive greedy literally on Alg. 3's compressed sketches: every step
+ * evaluates Marginal(S, v) = sum_r GetCenter(S_r, v, S).delta for
+ * every v not in S, takes the argmax (smallest id on ties), then MarkSeed
+ * (size[l] <- 0 when l is a valid label, R11).  Tiny inputs only.
+ */
+int orc_greedy_alg3(uint32_t n, const uint64_t *off, const uint32_t *nbr,
+                    int model, uint64_t t32, uint32_t R, uint64_t hash_seed,
+                    uint64_t a32, uint32_t k, uint32_t *seeds,
+                    int64_t *gain_num, int64_t *sigma_num, uint64_t *visits_out)
+{
+    uint32_t *center_of = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+    uint32_t rho = orc_centers(n, hash_seed, a32, NULL, center_of);
+    uint32_t *clabel = (uint32_t *)malloc((size_t)R * (rho ? rho : 1) * sizeof(uint32_t));
+    uint32_t *csize = (uint32_t *)malloc((size_t)R * (rho ? rho : 1) * sizeof(uint32_t));
+    uint8_t *is_seed = (uint8_t *)calloc(n, 1);
+    if (!center_of || !clabel || !csize || !is_seed) return -1;
+    for (uint32_t r = 0; r < R; r++)
+        orc_compressed_sketch(n, off, nbr, model, t32, hash_seed, r, a32,
+                              clabel + (size_t)r * rho, csize + (size_t)r * rho);
+    uint64_t visits = 0;
+    int64_t sigma = 0;
+    for (uint32_t i = 0; i < k; i++) {
+        int64_t best = -1;
+        uint32_t s = 0;
+        for (uint32_t v = 0; v < n; v++) {
+            if (is_seed[v]) continue;
+            int64_t g = 0;
+            for (uint32_t r = 0; r < R; r++) {
+                int64_t d, l;
+                uint64_t vis;
+                orc_get_center(n, off, nbr, model, t32, hash_seed, r, center_of,
+                               clabel + (size_t)r * rho, csize + (size_t)r * rho,
+                               is_seed, v, &d, &l, &vis);
+                g += d;
+                visits += vis;
+            }
+            if (g > best) { best = g; s = v; }
+        }
+        /* MarkSeed(s) */
+        for (uint32_t r = 0; r < R; r++) {
+            int64_t d, l;
+            uint64_t vis;
+            orc_get_center(n, off, nbr, model, t32, hash_seed, r, center_of,
+                           clabel + (size_t)r * rho, csize + (size_t)r * rho,
+                           is_seed, s, &d, &l, &vis);
+            if (l >= 0) csize[(size_t)r * rho + (size_t)l] = 0;
+        }
+        is_seed[s] = 1;
+        sigma += best;
+        seeds[i] = s;
+        gain_num[i] = best;
+        sigma_num[i] = sigma;
+    }
+    if (visits_out) *visits_out = visits;
+    free(center_of); free(clabel); free(csize); free(is_seed);
+    return 0;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Input generators (counter-based; DESIGN.md §"Input recipe").  Not method    */
+/* arithmetic — the oracle's own copy of the recipe, compared bit-exactly      */
+/* against the CUDA generator in the GPU tests.                                */
+/* ------------------------------------------------------------------------ */
+
+static uint64_t gen_key(uint64_t gen_seed)
+{
+    return orc_mix64(gen_seed ^ 0xD1B54A32D192ED03ull);
+}
+
+static int cmp_u64(const void *a, const void *b)
+{
+    uint64_t x = *(const uint64_t *)a, y = *(const uint64_t *)b;
+    return (x > y) - (x < y);
+}
+
+/* ER: draw j = 0,1,2,...: w = mix64(Kg ^ j), u = (lo32(w)*n)>>32,
+ * v = (hi32(w)*n)>>32; skip u == v; keep the first m distinct undirected
+ * pairs.  keys_out (m entries) receives sorted keys min<<32|max.
+ * Returns m, or -1 (OOM / m too large). */
+long orc_gen_er(uint32_t n, uint64_t m, uint64_t gen_seed, uint64_t *keys_out)
+{
+    if (n < 2 || m > (uint64_t)n * (n - 1) / 2) return -1;
+    uint64_t Kg = gen_key(gen_seed);
+    size_t cap = 1;
+    while (cap < 2 * m + 2) cap <<= 1;
+    uint64_t *table = (uint64_t *)malloc(cap * sizeof(uint64_t));
+    if (!table) return -1;
+    for (size_t i = 0; i < cap; i++) table[i] = ~0ull;
+    uint64_t got = 0;
+    for (uint64_t j = 0; got < m; j++) {
+        uint64_t w = orc_mix64(Kg ^ j);
+        uint32_t u = (uint32_t)(((w & 0xFFFFFFFFull) * n) >> 32);
+        uint32_t v = (uint32_t)(((w >> 32) * n) >> 32);
+        if (u == v) continue;
+        uint64_t a = u < v ? u : v, b = u < v ? v : u;
+        uint64_t key = (a << 32) | b;
+        size_t h = (size_t)(orc_mix64(key) & (cap - 1));
+        int dup = 0;
+        while (table[h] != ~0ull) {
+            if (table[h] == key) { dup = 1; break; }
+            h = (h + 1) & (cap - 1);
+        }
+        if (dup) continue;
+        table[h] = key;
+        keys_out[got++] = key;
+    }
+    free(table);
+    qsort(keys_out, (size_t)m, sizeof(uint64_t), cmp_u64);
+    return (long)m;
+}
+
+/* R-MAT permutation pi(x) = h(g2(h(g1(x)))) on [0, 2^s). */
+static uint64_t rmat_perm(uint64_t x, int s)
+{
+    uint64_t mask = (s == 64) ? ~0ull : ((1ull << s) - 1);
+    int sh = (s + 1) / 2;
+    x = (x * 0x9E3779B97F4A7C15ull) & mask;
+    x ^= x >> sh;
+    x = (x * 0xBF58476D1CE4E5B9ull) & mask;
+    x ^= x >> sh;
+    return x;
+}
+
+/* R-MAT: samples i in [0, ef*2^s); level l in [0,s): y = mix64(Kg ^ (i*64+l)) >> 11
+ * (53 bits); y < ta: quadrant a; < tab: b (v bit); < tabc: c (u bit); else d
+ * (both bits); level l sets bit s-1-l.  Optional permutation pi of ids; then
+ * drop loops, dedup.  keys_out capacity ef*2^s.  Returns m (distinct edges). */
+long orc_gen_rmat(int scale, uint32_t ef, uint64_t ta, uint64_t tab,
+                  uint64_t tabc, int permute, uint64_t gen_seed,
+                  uint64_t *keys_out)
+{
+    uint64_t Kg = gen_key(gen_seed);
+    uint64_t ns = (uint64_t)ef << scale;
+    uint64_t cnt = 0;
+    for (uint64_t i = 0; i < ns; i++) {
+        uint64_t u = 0, v = 0;
+        for (int l = 0; l < scale; l++) {
+            uint64_t y = orc_mix64(Kg ^ (i * 64 + (uint64_t)l)) >> 11;
+            uint64_t bit = 1ull << (scale - 1 - l);
+            if (y < ta) {
+            } else if (y < tab) {
+                v |= bit;
+            } else if (y < tabc) {
+                u |= bit;
+            } else {
+                u |= bit;
+                v |= bit;
+            }
+        }
+        if (permute) { u = rmat_perm(u, scale); v = rmat_perm(v, scale); }
+        if (u == v) continue;
+        uint64_t a = u < v ? u : v, b = u < v ? v : u;
+        keys_out[cnt++] = (a << 32) | b;
+    }
+    qsort(keys_out, (size_t)cnt, sizeof(uint64_t), cmp_u64);
+    uint64_t m = 0;
+    for (uint64_t i = 0; i < cnt; i++)
+        if (m == 0 || keys_out[m - 1] != keys_out[i]) keys_out[m++] = keys_out[i];
+    return (long)m;
+}
+
+/* Grid W x H, id = i*W + j: edges (i,j)-(i,j+1), (i,j)-(i+1,j), and the
+ * diagonal (i,j)-(i+1,j+1) iff hi32(mix64(Kg ^ (i*W+j))) < d32.  Keys are
+ * emitted already sorted.  keys_out capacity 3*W*H.  Returns m. */
+long orc_gen_grid(uint32_t W, uint32_t H, uint64_t d32, uint64_t gen_seed,
+                  uint64_t *keys_out)
+{
+    uint64_t Kg = gen_key(gen_seed);
+    uint64_t m = 0;
+    for (uint64_t i = 0; i < H; i++) {
+        for (uint64_t j = 0; j < W; j++) {
+            uint64_t v = i * W + j;
+            if (j + 1 < W) keys_out[m++] = (v << 32) | (v + 1);
+            if (i + 1 < H) keys_out[m++] = (v << 32) | (v + W);
+            if (i + 1 < H && j + 1 < W &&
+                (orc_mix64(Kg ^ v) >> 32) < d32)
+                keys_out[m++] = (v << 32) | (v + W + 1);
+        }
+    }
+    return (long)m;
+}
+
+/* Symmetric CSR from sorted distinct keys (min<<32|max).  off: n+1,
+ * nbr: 2m.  Neighbour lists come out sorted because keys are sorted. */
+void orc_csr_from_keys(uint32_t n, uint64_t m, const uint64_t *keys,
+                       uint64_t *off, uint32_t *nbr)
+{
+    for (uint32_t v = 0; v <= n; v++) off[v] = 0;
+    for (uint64_t e = 0; e < m; e++) {
+        off[(keys[e] >> 32) + 1]++;
+        off[(keys[e] & 0xFFFFFFFFull) + 1]++;
+    }
+    for (uint32_t v = 0; v < n; v++) off[v + 1] += off[v];
+    uint64_t *fill = (uint64_t *)malloc((size_t)n * sizeof(uint64_t));
+    for (uint32_t v = 0; v < n; v++) fill[v] = off[v];
+    for (uint64_t e = 0; e < m; e++) {
+        uint32_t a = (uint32_t)(keys[e] >> 32), b = (uint32_t)keys[e];
+        nbr[fill[a]++] = b;
+        nbr[fill[b]++] = a;
+    }
+    free(fill);
+}
