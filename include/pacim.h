@@ -1,0 +1,225 @@
+/*
+ * pacim.h — C ABI of the B200-native PaC-IM hot path (arXiv 2311.07554).
+ *
+ * The calls follow the paper's problem statement and Alg. 1:
+ *   pacim_load_graph / pacim_generate_graph   (graph G, edge model p; H0-H1)
+ *   pacim_build_sketches(R, hash_seed, ...)   (Step 1: Sketch(r) for all r; H2-H7)
+ *   pacim_select_seeds(k)                     (Step 2: k x NextSeed + MarkSeed; H8-H12)
+ * Citation keys: P:n = PAPER.md line n; Hn = SURVEY.md §8(a) row; Rn = reading
+ * n in DESIGN.md §"Readings of the paper".
+ *
+ * Conventions for every call:
+ *  - Return value is a pacim_status; the message of the last failure is
+ *    available from pacim_last_error(ctx) until the next call on that ctx.
+ *    No exception or signal crosses the ABI.
+ *  - "host" pointers are caller-owned CPU memory; the library copies what it
+ *    needs before returning and never retains them.  "device" pointers are
+ *    caller-owned CUDA memory on the ctx's device (e.g. torch tensors).
+ *  - Every call is ordered on the ctx's stream and synchronises that stream
+ *    before returning (outputs are ready when it returns).
+ *  - One ctx per host thread; one ctx per GPU.  All device memory of a ctx is
+ *    owned by it and released by pacim_destroy.
+ *  - Vertex ids are uint32 < 2^31 (R2: bit 63 separates the sketch-id domain of
+ *    the hash from the edge-key domain).  Edge counts are uint64.
+ *  - The CSR is the symmetric simple graph: offsets u64[n+1] (offsets[0]=0,
+ *    offsets[n]=nnz=2m, nondecreasing), neighbors u32[nnz], each list sorted
+ *    ascending, no self-loops, no duplicates (P:1308 symmetrisation; R14).
+ */
+#ifndef PACIM_H
+#define PACIM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define PACIM_API __attribute__((visibility("default")))
+#else
+#define PACIM_API
+#endif
+
+typedef struct pacim_ctx pacim_ctx;
+
+typedef enum {
+    PACIM_OK = 0,
+    PACIM_EINVAL = -1,   /* bad argument (message names it) */
+    PACIM_ENOMEM = -2,   /* device allocation failed */
+    PACIM_ECUDA = -3,    /* CUDA runtime error (message has cudaGetErrorString) */
+    PACIM_ESTATE = -5,   /* call out of order (load -> build -> select) */
+    PACIM_ENOTIMPL = -6, /* combination not implemented */
+    PACIM_ECHECK = -7    /* an internal invariant check failed (message names it) */
+} pacim_status;
+
+/* Edge-probability models (P:1314-1317 constant p; P:2034 WIC). */
+enum { PACIM_P_CONST = 0, PACIM_P_WIC = 1 };
+/* Synthetic generators (DESIGN.md §Input recipe). */
+enum { PACIM_GEN_ER = 0, PACIM_GEN_RMAT = 1, PACIM_GEN_GRID = 2 };
+
+typedef struct {
+    /* sizes */
+    uint32_t n;
+    uint64_t m;                 /* undirected edges */
+    uint32_t R;                 /* sketches in the job */
+    uint32_t R_local;           /* sketches held by this ctx (shard) */
+    uint32_t rho;               /* centers (compressed mode), else n */
+    int compressed;
+    uint64_t ncomp;             /* non-singleton components stored (uncompressed) */
+    uint64_t nmember;           /* vertices in non-singleton components, summed over sketches */
+    uint64_t live_pairs;        /* sum over local sketches of live edges (H2 count) */
+    /* device time of the last build / select (CUDA events, ms) */
+    double t_build_ms;
+    double t_init_ms, t_edges_ms, t_compress_ms, t_compact_ms, t_gain_ms, t_centers_ms;
+    double t_select_ms;
+    uint64_t device_bytes;      /* bytes currently allocated by the ctx */
+    uint64_t select_member_updates; /* gain updates applied by the last select */
+    uint64_t select_bfs_visits;     /* Get-center / cover BFS vertex visits (compressed) */
+    uint32_t kernel_launches_build; /* launches of library kernels in the last build */
+    uint32_t kernel_launches_select;/* launches of library kernels in the last select */
+} pacim_stats;
+
+/* --------------------------------------------------------------- lifecycle */
+
+/* Create a context on CUDA device `device`.  `cuda_stream` is a cudaStream_t
+ * (e.g. torch.cuda.current_stream().cuda_stream) or NULL for a private
+ * non-blocking stream.  *out receives the ctx.  EINVAL if out is NULL or the
+ * device does not exist; ECUDA on runtime failure. */
+PACIM_API int pacim_create(pacim_ctx **out, int device, void *cuda_stream);
+
+/* Free every device allocation of the ctx and the ctx itself.  NULL is a no-op. */
+PACIM_API void pacim_destroy(pacim_ctx *ctx);
+
+/* Message of the last failed call on ctx ("" if none).  Valid until the next
+ * call on ctx.  With ctx == NULL: message of the last failed pacim_create. */
+PACIM_API const char *pacim_last_error(const pacim_ctx *ctx);
+
+/* Library version string (static storage). */
+PACIM_API const char *pacim_version(void);
+
+/* Quantise a probability to the 32-bit threshold T32 = floor(p * 2^32)
+ * computed in IEEE double; p >= 1 gives 2^32 (always live), p <= 0 or NaN
+ * gives 0 (R3; P:4 "hash_edge < p(u,v)"). */
+PACIM_API uint64_t pacim_threshold_from_p(double p);
+
+/* ------------------------------------------------------------------- graph */
+
+/* H0/H1.  Load the symmetric CSR from HOST arrays offsets[n+1], neighbors[nnz]
+ * and set the edge model: pmodel = PACIM_P_CONST with t32 = T32 in [0, 2^32]
+ * (every edge live in sketch r iff hash_edge(u,v,r) < T32 * 2^32, R3),
+ * or PACIM_P_WIC (t32 ignored; T32(u,v) = min(2^32, floor(2^33/(d_u+d_v))),
+ * P:2034, R4).  validate: 0 = trust the caller; 1 = check offsets, id range,
+ * sorted lists without loops or duplicates (EINVAL naming the first bad
+ * vertex); 2 = also check symmetry.  EINVAL also for n == 0, n >= 2^31,
+ * offsets[0] != 0, offsets[n] != nnz, nnz odd, t32 > 2^32.  Replaces any
+ * previously loaded graph and drops existing sketches. */
+PACIM_API int pacim_load_graph(pacim_ctx *ctx, uint32_t n, uint64_t nnz,
+                     const uint64_t *offsets, const uint32_t *neighbors,
+                     int pmodel, uint64_t t32, int validate);
+
+/* As pacim_load_graph but offsets/neighbors are DEVICE pointers on the ctx's
+ * device (copied device-to-device; the caller keeps ownership). */
+PACIM_API int pacim_load_graph_device(pacim_ctx *ctx, uint32_t n, uint64_t nnz,
+                            const uint64_t *d_offsets, const uint32_t *d_neighbors,
+                            int pmodel, uint64_t t32, int validate);
+
+/* H0 on the device: generate a synthetic graph (DESIGN.md §Input recipe) and
+ * load it with edge model (pmodel, t32).  params (host, nparams entries):
+ *   PACIM_GEN_ER:   {n, m}                       first m distinct pairs
+ *   PACIM_GEN_RMAT: {scale, ef, ta, tab, tabc, permute}  53-bit quadrant thresholds
+ *   PACIM_GEN_GRID: {W, H, d32}                  diagonal iff hash < d32
+ * gen_seed keys the counter-based draws.  EINVAL for bad params / sizes. */
+PACIM_API int pacim_generate_graph(pacim_ctx *ctx, int kind, const uint64_t *params,
+                         int nparams, uint64_t gen_seed, int pmodel, uint64_t t32);
+
+/* Sizes of the loaded graph (host outputs; either may be NULL). ESTATE if none. */
+PACIM_API int pacim_graph_info(pacim_ctx *ctx, uint32_t *n, uint64_t *m);
+
+/* Copy the loaded CSR to HOST arrays offsets_out[n+1], neighbors_out[2m]
+ * (either may be NULL).  ESTATE if no graph. */
+PACIM_API int pacim_get_graph(pacim_ctx *ctx, uint64_t *offsets_out, uint32_t *neighbors_out);
+
+/* -------------------------------------------------------------- sketches */
+
+/* Step 1 of Alg. 1: build this ctx's sketches, Sketch(r) for
+ * every r in [0, R) with r % shard_world == shard_rank (shard_world = 1: all).
+ * Sketch r is the CC structure of G'_r = {e : hash_edge(e, r) < T32(e)*2^32}
+ * with K = mix64(hash_seed) keying both hash(r) and hash(edge) (R1, R2).
+ * center_a32 selects the store (Thm 3.1):
+ *   >= 2^32 : uncompressed (alpha = 1): per-vertex CC labels + sizes + member
+ *             index (InfuserMG-style memo; H4-H6u);
+ *   < 2^32  : compressed: v is a center iff hi32(mix64(v ^ K_c)) < center_a32
+ *             (R9, alpha ~ center_a32 / 2^32); per sketch label[i], size[i]
+ *             over centers only (H6c).
+ * Also computes the initial gains gain0[v] = sum_{own r} |C_r(v)| (int64;
+ * = R * Marginal(empty, v); H7).  EINVAL: R == 0,
+ * shard_world == 0, shard_rank >= shard_world; ESTATE: no graph; ENOMEM if
+ * the store does not fit. */
+PACIM_API int pacim_build_sketches(pacim_ctx *ctx, uint32_t R, uint64_t hash_seed,
+                         uint64_t center_a32, uint32_t shard_rank,
+                         uint32_t shard_world);
+
+/* ------------------------------------------------------------- selection */
+
+/* Step 2 of Alg. 1 on a single ctx holding all R sketches
+ * (shard_world == 1): k greedy steps, each picking the smallest-id vertex not
+ * in S with maximal marginal gain (R5, R6), marking its CC
+ * covered in every sketch (MarkSeed) and updating the gains of the
+ * covered CCs' members (H8-H10).  HOST outputs (k entries each; sigma_out may
+ * be NULL): seeds_out[i]; gain_num_out[i] = sum_r delta_r = R * Marginal(S_i, s_i)
+ * (integer numerator, R7); sigma_num_out[i] = cumulative sum; sigma_out[i] =
+ * sigma_num_out[i] / R.  Every call starts from S = empty (the store is
+ * restored).  EINVAL: k == 0 or k > n or an output NULL; ESTATE: no sketches
+ * or sharded build; ECHECK if sum_r delta_r != gain[s] (never expected). */
+PACIM_API int pacim_select_seeds(pacim_ctx *ctx, uint32_t k, uint32_t *seeds_out,
+                       int64_t *gain_num_out, int64_t *sigma_num_out,
+                       double *sigma_out);
+
+/* --------------------------------------------- multi-rank step primitives */
+/* For sketches sharded over ranks (shard_world > 1) the host runs the greedy
+ * loop and performs the collectives (paper_2311_07554_b200/dist.py); these
+ * calls are this rank's part of a step.  All pointers are DEVICE pointers. */
+
+/* Copy this rank's partial gain0 (n x int64) into d_out. ESTATE if no sketches. */
+PACIM_API int pacim_gain0_to_device(pacim_ctx *ctx, int64_t *d_out);
+
+/* Restore the covered flags of the store (start a new selection, S = empty). */
+PACIM_API int pacim_select_reset(pacim_ctx *ctx);
+
+/* MarkSeed(s) on this rank's sketches: for every own sketch where
+ * C_r(s) is not yet covered, mark it covered and add -|C_r(s)| into d_delta[u]
+ * for every member u (d_delta: n x int64, accumulated, not cleared).
+ * *local_gain (host) receives sum over own sketches of delta_r. */
+PACIM_API int pacim_cover_local(pacim_ctx *ctx, uint32_t s, int64_t *d_delta,
+                      int64_t *local_gain);
+
+/* NextSeed by full scan (H8): *s_out = smallest v with maximal d_gain[v]
+ * (entries < 0 never win unless all are), *g_out = d_gain[*s_out]. */
+PACIM_API int pacim_argmax_device(pacim_ctx *ctx, const int64_t *d_gain, uint32_t n,
+                        uint32_t *s_out, int64_t *g_out);
+
+/* ------------------------------------------------------------ inspection */
+
+/* gain0 (n x int64) to HOST. ESTATE if no sketches. */
+PACIM_API int pacim_get_gain0(pacim_ctx *ctx, int64_t *out);
+
+/* Canonical labels of sketch r (uncompressed store): out[v] = smallest vertex
+ * id of v's CC in G'_r (R8); HOST out[n].  EINVAL if r is not held by this
+ * ctx; ENOTIMPL in compressed mode. */
+PACIM_API int pacim_get_labels(pacim_ctx *ctx, uint32_t r, uint32_t *out);
+
+/* Compressed sketch r: label_out[i], size_out[i] for the rho centers in
+ * vertex order; HOST arrays of rho entries (rho from
+ * pacim_get_stats).  Sizes reflect covered CCs of the last selection. */
+PACIM_API int pacim_get_center_sketch(pacim_ctx *ctx, uint32_t r, uint32_t *label_out,
+                            uint32_t *size_out);
+
+/* Counters and device timings of the last build/select (HOST *out). */
+PACIM_API int pacim_get_stats(pacim_ctx *ctx, pacim_stats *out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PACIM_H */

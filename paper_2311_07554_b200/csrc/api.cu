@@ -1,0 +1,367 @@
+// api.cu — the extern "C" boundary declared in include/pacim.h.
+// Argument validation, state machine (load -> build -> select), error
+// capture; all compute is delegated to graph.cu / build.cu / select.cu.
+#include <cmath>
+#include <cstring>
+
+#include "pacim_internal.cuh"
+
+static std::string g_create_err;
+
+void pc_ensure(pacim_ctx *ctx, DevBuf &b, size_t bytes) {
+  if (bytes <= b.bytes && b.p) return;
+  if (b.p) {
+    cudaFree(b.p);
+    ctx->device_bytes -= b.bytes;
+    b.p = nullptr;
+    b.bytes = 0;
+  }
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(&b.p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    b.p = nullptr;
+    throw PacimError{PACIM_ENOMEM, "cudaMalloc(" + std::to_string(bytes) +
+                                       " bytes) failed: " + cudaGetErrorString(e)};
+  }
+  b.bytes = bytes;
+  ctx->device_bytes += bytes;
+}
+
+void pc_free(pacim_ctx *ctx, DevBuf &b) {
+  if (b.p) {
+    cudaFree(b.p);
+    ctx->device_bytes -= b.bytes;
+  }
+  b.p = nullptr;
+  b.bytes = 0;
+}
+
+template <typename F>
+static int guarded(pacim_ctx *ctx, F &&f) {
+  if (!ctx) return PACIM_EINVAL;
+  ctx->err.clear();
+  try {
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) throw PacimError{PACIM_ECUDA, cudaGetErrorString(e)};
+    f();
+    return PACIM_OK;
+  } catch (const PacimError &pe) {
+    ctx->err = pe.msg;
+    return pe.code;
+  } catch (const std::exception &ex) {
+    ctx->err = ex.what();
+    return PACIM_ECUDA;
+  } catch (...) {
+    ctx->err = "unknown error";
+    return PACIM_ECUDA;
+  }
+}
+
+static void drop_sketches(pacim_ctx *ctx) {
+  pc_free(ctx, ctx->L);
+  pc_free(ctx, ctx->csize);
+  pc_free(ctx, ctx->csize_work);
+  pc_free(ctx, ctx->coff);
+  pc_free(ctx, ctx->cfill);
+  pc_free(ctx, ctx->perm);
+  pc_free(ctx, ctx->clabel);
+  pc_free(ctx, ctx->csz);
+  pc_free(ctx, ctx->csz_work);
+  pc_free(ctx, ctx->Ltmp);
+  ctx->built = false;
+}
+
+static void drop_graph(pacim_ctx *ctx) {
+  drop_sketches(ctx);
+  pc_free(ctx, ctx->off);
+  pc_free(ctx, ctx->nbr);
+  pc_free(ctx, ctx->keys);
+  pc_free(ctx, ctx->tm1);
+  ctx->has_graph = false;
+}
+
+extern "C" {
+
+const char *pacim_version(void) { return "pacim-b200 0.1 (sm_100a)"; }
+
+uint64_t pacim_threshold_from_p(double p) {
+  if (!(p > 0.0)) return 0;
+  if (p >= 1.0) return 1ull << 32;
+  return (uint64_t)std::floor(p * 4294967296.0);
+}
+
+int pacim_create(pacim_ctx **out, int device, void *cuda_stream) {
+  if (!out) return PACIM_EINVAL;
+  *out = nullptr;
+  int cnt = 0;
+  cudaError_t e = cudaGetDeviceCount(&cnt);
+  if (e != cudaSuccess) {
+    g_create_err = std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e);
+    return PACIM_ECUDA;
+  }
+  if (device < 0 || device >= cnt) {
+    g_create_err = "no such CUDA device";
+    return PACIM_EINVAL;
+  }
+  pacim_ctx *ctx = new pacim_ctx();
+  ctx->device = device;
+  e = cudaSetDevice(device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount,
+                                                   device);
+  if (e == cudaSuccess) {
+    if (cuda_stream) {
+      ctx->stream = (cudaStream_t)cuda_stream;
+    } else {
+      e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking);
+      ctx->own_stream = true;
+    }
+  }
+  if (e != cudaSuccess) {
+    g_create_err = cudaGetErrorString(e);
+    delete ctx;
+    return PACIM_ECUDA;
+  }
+  *out = ctx;
+  return PACIM_OK;
+}
+
+void pacim_destroy(pacim_ctx *ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  drop_graph(ctx);
+  pc_free(ctx, ctx->d_shr);
+  pc_free(ctx, ctx->d_tab);
+  pc_free(ctx, ctx->gain0);
+  pc_free(ctx, ctx->gain);
+  pc_free(ctx, ctx->center_of);
+  pc_free(ctx, ctx->counters);
+  pc_free(ctx, ctx->scratch);
+  pc_free(ctx, ctx->scratch2);
+  pc_free(ctx, ctx->sel_seeds);
+  pc_free(ctx, ctx->sel_gain);
+  pc_free(ctx, ctx->sel_partial);
+  pc_free(ctx, ctx->sel_list);
+  pc_free(ctx, ctx->sel_flag);
+  if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+const char *pacim_last_error(const pacim_ctx *ctx) {
+  return ctx ? ctx->err.c_str() : g_create_err.c_str();
+}
+
+static void check_model(int pmodel, uint64_t t32) {
+  PC_REQUIRE(pmodel == PACIM_P_CONST || pmodel == PACIM_P_WIC, PACIM_EINVAL,
+             "pmodel must be PACIM_P_CONST or PACIM_P_WIC");
+  PC_REQUIRE(pmodel != PACIM_P_CONST || t32 <= (1ull << 32), PACIM_EINVAL, "t32 > 2^32");
+}
+
+static void load_common(pacim_ctx *ctx, uint32_t n, uint64_t nnz, int pmodel, uint64_t t32) {
+  PC_REQUIRE(n >= 1, PACIM_EINVAL, "n must be >= 1");
+  PC_REQUIRE(n < (1u << 31), PACIM_EINVAL, "n must be < 2^31 (R2 key packing)");
+  PC_REQUIRE((nnz & 1) == 0, PACIM_EINVAL, "nnz must be even (symmetric CSR)");
+  check_model(pmodel, t32);
+  drop_graph(ctx);
+  ctx->n = n;
+  ctx->m = nnz / 2;
+  ctx->pmodel = pmodel;
+  ctx->t32 = t32;
+  pc_ensure(ctx, ctx->off, ((size_t)n + 1) * 8);
+  pc_ensure(ctx, ctx->nbr, std::max<uint64_t>(nnz, 1) * 4);
+}
+
+int pacim_load_graph(pacim_ctx *ctx, uint32_t n, uint64_t nnz, const uint64_t *offsets,
+                     const uint32_t *neighbors, int pmodel, uint64_t t32, int validate) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(offsets && (neighbors || nnz == 0), PACIM_EINVAL, "NULL CSR array");
+    PC_REQUIRE(n >= 1, PACIM_EINVAL, "n must be >= 1");
+    PC_REQUIRE(offsets[0] == 0, PACIM_EINVAL, "offsets[0] != 0");
+    PC_REQUIRE(offsets[n] == nnz, PACIM_EINVAL, "offsets[n] != nnz");
+    load_common(ctx, n, nnz, pmodel, t32);
+    PC_CUDA(cudaMemcpyAsync(ctx->off.p, offsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice,
+                            ctx->stream));
+    if (nnz)
+      PC_CUDA(cudaMemcpyAsync(ctx->nbr.p, neighbors, nnz * 4, cudaMemcpyHostToDevice, ctx->stream));
+    pc_graph_finish_load(ctx, validate);
+    ctx->has_graph = true;
+  });
+}
+
+int pacim_load_graph_device(pacim_ctx *ctx, uint32_t n, uint64_t nnz, const uint64_t *d_offsets,
+                            const uint32_t *d_neighbors, int pmodel, uint64_t t32, int validate) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(d_offsets && (d_neighbors || nnz == 0), PACIM_EINVAL, "NULL CSR array");
+    load_common(ctx, n, nnz, pmodel, t32);
+    PC_CUDA(cudaMemcpyAsync(ctx->off.p, d_offsets, ((size_t)n + 1) * 8, cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+    if (nnz)
+      PC_CUDA(cudaMemcpyAsync(ctx->nbr.p, d_neighbors, nnz * 4, cudaMemcpyDeviceToDevice,
+                              ctx->stream));
+    uint64_t ends[2];
+    PC_CUDA(cudaMemcpyAsync(&ends[0], ctx->off.as<uint64_t>(), 8, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    PC_CUDA(cudaMemcpyAsync(&ends[1], ctx->off.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    PC_REQUIRE(ends[0] == 0, PACIM_EINVAL, "offsets[0] != 0");
+    PC_REQUIRE(ends[1] == nnz, PACIM_EINVAL, "offsets[n] != nnz");
+    pc_graph_finish_load(ctx, validate);
+    ctx->has_graph = true;
+  });
+}
+
+int pacim_generate_graph(pacim_ctx *ctx, int kind, const uint64_t *params, int nparams,
+                         uint64_t gen_seed, int pmodel, uint64_t t32) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(params || nparams == 0, PACIM_EINVAL, "NULL params");
+    check_model(pmodel, t32);
+    drop_graph(ctx);
+    ctx->pmodel = pmodel;
+    ctx->t32 = t32;
+    pc_generate(ctx, kind, params, nparams, gen_seed);
+    ctx->has_graph = true;
+  });
+}
+
+int pacim_graph_info(pacim_ctx *ctx, uint32_t *n, uint64_t *m) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(ctx->has_graph, PACIM_ESTATE, "no graph loaded");
+    if (n) *n = ctx->n;
+    if (m) *m = ctx->m;
+  });
+}
+
+int pacim_get_graph(pacim_ctx *ctx, uint64_t *offsets_out, uint32_t *neighbors_out) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(ctx->has_graph, PACIM_ESTATE, "no graph loaded");
+    if (offsets_out)
+      PC_CUDA(cudaMemcpyAsync(offsets_out, ctx->off.p, ((size_t)ctx->n + 1) * 8,
+                              cudaMemcpyDeviceToHost, ctx->stream));
+    if (neighbors_out && ctx->m)
+      PC_CUDA(cudaMemcpyAsync(neighbors_out, ctx->nbr.p, 2 * ctx->m * 4, cudaMemcpyDeviceToHost,
+                              ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int pacim_build_sketches(pacim_ctx *ctx, uint32_t R, uint64_t hash_seed, uint64_t center_a32,
+                         uint32_t shard_rank, uint32_t shard_world) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(ctx->has_graph, PACIM_ESTATE, "build before load_graph");
+    PC_REQUIRE(R >= 1, PACIM_EINVAL, "R must be >= 1");
+    PC_REQUIRE(shard_world >= 1 && shard_rank < shard_world, PACIM_EINVAL,
+               "need 0 <= shard_rank < shard_world");
+    PC_REQUIRE(shard_rank < R, PACIM_EINVAL, "shard holds no sketch (shard_rank >= R)");
+    ctx->built = false;
+    ctx->R = R;
+    ctx->rank = shard_rank;
+    ctx->world = shard_world;
+    ctx->R_local = (R - shard_rank + shard_world - 1) / shard_world;
+    ctx->hash_seed = hash_seed;
+    ctx->K = pc_mix64(hash_seed);  // R2
+    ctx->a32 = center_a32;
+    ctx->compressed = center_a32 < (1ull << 32);
+    PC_REQUIRE(!ctx->compressed, PACIM_ENOTIMPL, "compressed store: not in this build");
+    pc_build(ctx);
+    ctx->built = true;
+  });
+}
+
+int pacim_select_seeds(pacim_ctx *ctx, uint32_t k, uint32_t *seeds_out, int64_t *gain_num_out,
+                       int64_t *sigma_num_out, double *sigma_out) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(ctx->built, PACIM_ESTATE, "select before build_sketches");
+    PC_REQUIRE(ctx->world == 1, PACIM_ESTATE,
+               "sharded build: use the multi-rank step primitives (dist.py)");
+    PC_REQUIRE(k >= 1 && k <= ctx->n, PACIM_EINVAL, "k must be in [1, n]");
+    PC_REQUIRE(seeds_out && gain_num_out && sigma_num_out, PACIM_EINVAL, "NULL output");
+    pc_select(ctx, k, seeds_out, gain_num_out, sigma_num_out);
+    if (sigma_out)
+      for (uint32_t i = 0; i < k; i++) sigma_out[i] = (double)sigma_num_out[i] / (double)ctx->R;
+  });
+}
+
+int pacim_gain0_to_device(pacim_ctx *ctx, int64_t *d_out) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(ctx->built, PACIM_ESTATE, "no sketches");
+    PC_REQUIRE(d_out, PACIM_EINVAL, "NULL output");
+    PC_CUDA(cudaMemcpyAsync(d_out, ctx->gain0.p, (size_t)ctx->n * 8, cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int pacim_select_reset(pacim_ctx *ctx) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(ctx->built, PACIM_ESTATE, "no sketches");
+    pc_select_reset(ctx);
+  });
+}
+
+int pacim_cover_local(pacim_ctx *ctx, uint32_t s, int64_t *d_delta, int64_t *local_gain) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(ctx->built, PACIM_ESTATE, "no sketches");
+    PC_REQUIRE(s < ctx->n && d_delta && local_gain, PACIM_EINVAL, "bad argument");
+    pc_cover_local(ctx, s, d_delta, local_gain);
+  });
+}
+
+int pacim_argmax_device(pacim_ctx *ctx, const int64_t *d_gain, uint32_t n, uint32_t *s_out,
+                        int64_t *g_out) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(d_gain && s_out && g_out && n >= 1, PACIM_EINVAL, "bad argument");
+    pc_argmax(ctx, d_gain, n, s_out, g_out);
+  });
+}
+
+int pacim_get_gain0(pacim_ctx *ctx, int64_t *out) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(ctx->built, PACIM_ESTATE, "no sketches");
+    PC_REQUIRE(out, PACIM_EINVAL, "NULL output");
+    PC_CUDA(cudaMemcpyAsync(out, ctx->gain0.p, (size_t)ctx->n * 8, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int pacim_get_labels(pacim_ctx *ctx, uint32_t r, uint32_t *out) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(ctx->built, PACIM_ESTATE, "no sketches");
+    PC_REQUIRE(!ctx->compressed, PACIM_ENOTIMPL, "labels are not stored in compressed mode");
+    PC_REQUIRE(out && r < ctx->R && ctx->r_slot[r] >= 0, PACIM_EINVAL,
+               "sketch r is not held by this ctx");
+    pc_get_labels(ctx, (uint32_t)ctx->r_slot[r], out);
+  });
+}
+
+int pacim_get_center_sketch(pacim_ctx *ctx, uint32_t r, uint32_t *label_out, uint32_t *size_out) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(ctx->built, PACIM_ESTATE, "no sketches");
+    PC_REQUIRE(ctx->compressed, PACIM_ESTATE, "not a compressed store");
+    (void)r;
+    (void)label_out;
+    (void)size_out;
+    throw PacimError{PACIM_ENOTIMPL, "compressed store: not in this build"};
+  });
+}
+
+int pacim_get_stats(pacim_ctx *ctx, pacim_stats *out) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(out, PACIM_EINVAL, "NULL output");
+    pacim_stats s = ctx->stats;
+    s.n = ctx->n;
+    s.m = ctx->m;
+    s.R = ctx->R;
+    s.R_local = ctx->R_local;
+    s.rho = ctx->compressed ? ctx->rho : ctx->n;
+    s.compressed = ctx->compressed ? 1 : 0;
+    s.ncomp = ctx->ncomp;
+    s.nmember = ctx->nmember;
+    s.device_bytes = ctx->device_bytes;
+    *out = s;
+  });
+}
+
+}  // extern "C"

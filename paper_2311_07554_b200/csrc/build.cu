@@ -1,0 +1,454 @@
+// build.cu — Step 1 of Alg. 1: Sketch(r) for every local sketch.
+//
+// Store layout (DESIGN.md §Store layout): the uncompressed store is ONE u32
+// array L[v*B + j] (vertex-major; slot j = local sketch ordered by hash(r)).
+// During the build it is the union-find parent array of all B sketches; after
+// compress_count / compact it is the per-vertex CC memo of P:597-601.
+//
+// Kernels (one pass each over L):
+//   k_init            L[v][j] = v                                   (H3 setup)
+//   k_edges           per upper edge: hash, candidate sketches, live test,
+//                     lock-free hook-larger-root-under-smaller union (H2, H3)
+//   k_compress_count  full path compression to the min-id root (H4) and CC
+//                     sizes counted into the root slot (H5)
+//   k_compact         root slots -> compact component ids, member-index
+//                     ranges allocated per tile                    (H6u)
+//   k_gain_scatter    gain0[v] = sum_j |C_j(v)| (H7) and the member index
+//                     perm grouped by component (H6u)
+#include <algorithm>
+
+#include "pacim_internal.cuh"
+
+namespace {
+
+__device__ __forceinline__ uint32_t ld_cg(const uint32_t *p) { return __ldcg(p); }
+
+// ---------------------------------------------------------------- k_init
+__global__ void k_init(uint32_t *L, uint32_t n, uint32_t B) {
+  const int lane = threadIdx.x & 31;
+  size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  if ((B & 3) == 0) {
+    const uint32_t B4 = B >> 2;
+    for (size_t v = warp; v < n; v += nw) {
+      uint4 *row = reinterpret_cast<uint4 *>(L + v * B);
+      uint4 x = make_uint4((uint32_t)v, (uint32_t)v, (uint32_t)v, (uint32_t)v);
+      for (uint32_t j = lane; j < B4; j += 32) __stcs(row + j, x);
+    }
+  } else {
+    for (size_t v = warp; v < n; v += nw)
+      for (uint32_t j = lane; j < B; j += 32) L[v * B + j] = (uint32_t)v;
+  }
+}
+
+// ------------------------------------------------------------- union-find
+// Lock-free union-find with ids decreasing along parent pointers (a root is
+// only ever hooked under a SMALLER root), so every tree's root is the minimum
+// id of its CC (R8) and no cycle can form even with stale reads.  Path
+// halving uses plain stores: it only replaces a parent by an ancestor.
+__device__ __forceinline__ uint32_t uf_find(uint32_t *L, uint32_t B, uint32_t j, uint32_t x) {
+  for (;;) {
+    uint32_t p = ld_cg(L + (size_t)x * B + j);
+    if (p == x) return x;
+    uint32_t gp = ld_cg(L + (size_t)p * B + j);
+    if (gp == p) return p;
+    L[(size_t)x * B + j] = gp;
+    x = gp;
+  }
+}
+
+__device__ __forceinline__ void uf_unite(uint32_t *L, uint32_t B, uint32_t j, uint32_t u,
+                                         uint32_t v) {
+  for (;;) {
+    u = uf_find(L, B, j, u);
+    v = uf_find(L, B, j, v);
+    if (u == v) return;
+    if (u < v) {
+      uint32_t t = u;
+      u = v;
+      v = t;
+    }
+    // hook the larger root u under the smaller v
+    uint32_t old = atomicCAS(L + (size_t)u * B + j, u, v);
+    if (old == u) return;
+    u = old;  // u was hooked meanwhile: continue from its new parent
+  }
+}
+
+// --------------------------------------------------------------- k_edges
+// Sketch slot table in shared memory: shr[j] = hi32(hash(r_j)) ascending and
+// tab[p] = #{j : shr[j] >> (32-TB) < p}.  live(e, j) <=> (shr[j] ^ he) < T
+// implies the top w = clz(T-1) bits of shr[j] and he agree, so the candidate
+// slots of an edge are one contiguous range of the sorted table (exact; R2
+// candidate enumeration, SURVEY §8(a) note).
+template <bool WIC>
+__global__ void __launch_bounds__(256) k_edges(const uint64_t *__restrict__ keys,
+                                               const uint32_t *__restrict__ tm1, uint64_t m,
+                                               uint64_t K, uint64_t t32,
+                                               const uint32_t *__restrict__ g_shr,
+                                               const uint16_t *__restrict__ g_tab, uint32_t B,
+                                               uint32_t *L, unsigned long long *live_ctr) {
+  extern __shared__ uint32_t sm[];
+  uint32_t *shr = sm;
+  uint16_t *tab = reinterpret_cast<uint16_t *>(sm + B);
+  for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) shr[i] = g_shr[i];
+  for (uint32_t i = threadIdx.x; i <= (1u << PACIM_TB); i += blockDim.x) tab[i] = g_tab[i];
+  __syncthreads();
+  unsigned long long live = 0;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (size_t)gridDim.x * blockDim.x) {
+    const uint64_t key = keys[e];
+    const uint64_t T = WIC ? (uint64_t)tm1[e] + 1 : t32;
+    if (T == 0) continue;
+    const uint32_t he = (uint32_t)(pc_mix64(key ^ K) >> 32);
+    const uint32_t w = __clz((uint32_t)(T - 1));
+    uint32_t lo, hi;
+    if (w >= PACIM_TB) {
+      uint32_t p = he >> (32 - PACIM_TB);
+      lo = tab[p];
+      hi = tab[p + 1];
+    } else if (w == 0) {
+      lo = 0;
+      hi = B;
+    } else {
+      uint32_t p = (he >> (32 - w)) << (PACIM_TB - w);
+      lo = tab[p];
+      hi = tab[p + (1u << (PACIM_TB - w))];
+    }
+    const uint32_t u = (uint32_t)(key >> 32), v = (uint32_t)key;
+    for (uint32_t j = lo; j < hi; j++) {
+      if ((uint64_t)(shr[j] ^ he) < T) {
+        uf_unite(L, B, j, u, v);
+        live++;
+      }
+    }
+  }
+  // block-aggregated counter
+  for (int d = 16; d; d >>= 1) live += __shfl_xor_sync(0xffffffffu, live, d);
+  __shared__ unsigned long long bsum;
+  if (threadIdx.x == 0) bsum = 0;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0 && live) atomicAdd(&bsum, live);
+  __syncthreads();
+  if (threadIdx.x == 0 && bsum) atomicAdd(live_ctr, bsum);
+}
+
+// ------------------------------------------------------ k_compress_count
+// find that also stops at a converted root slot (HIGH set)
+__device__ __forceinline__ uint32_t uf_find_root(uint32_t *L, uint32_t B, uint32_t j,
+                                                 uint32_t x) {
+  for (;;) {
+    uint32_t p = ld_cg(L + (size_t)x * B + j);
+    if (p == x || (p & PACIM_HIGH)) return x;
+    uint32_t gp = ld_cg(L + (size_t)p * B + j);
+    if (gp == p || (gp & PACIM_HIGH)) return p;
+    // atomicMin, not a plain store: a slot may only move towards the root,
+    // so a racing halving can never undo the owner's full compression
+    atomicMin(L + (size_t)x * B + j, gp);
+    x = gp;
+  }
+}
+
+// For every non-root (v, j): slot <- root (full compression, H4); root slot
+// becomes HIGH | size by CAS(root -> HIGH|1) then atomicAdd(+1) per member
+// (H5).  ctr[0] += CCs of size >= 2, ctr[1] += non-root entries.
+__global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n, uint32_t B,
+                                                        unsigned long long *ctr) {
+  const int lane = threadIdx.x & 31;
+  size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long ncc = 0, nnr = 0;
+  for (size_t v = warp; v < n; v += nw) {
+    for (uint32_t j = lane; j < B; j += 32) {
+      uint32_t *slot = L + v * B + j;
+      uint32_t s = ld_cg(slot);
+      if (s == (uint32_t)v || (s & PACIM_HIGH)) continue;  // root (or singleton)
+      uint32_t root = uf_find_root(L, B, j, s);
+      if (root != s) atomicMin(slot, root);
+      uint32_t *rs = L + (size_t)root * B + j;
+      atomicCAS(rs, root, PACIM_HIGH | 1u);
+      uint32_t old = atomicAdd(rs, 1u);
+      if (old == (PACIM_HIGH | 1u)) ncc++;
+      nnr++;
+    }
+  }
+  for (int d = 16; d; d >>= 1) {
+    ncc += __shfl_xor_sync(0xffffffffu, ncc, d);
+    nnr += __shfl_xor_sync(0xffffffffu, nnr, d);
+  }
+  __shared__ unsigned long long s0, s1;
+  if (threadIdx.x == 0) s0 = s1 = 0;
+  __syncthreads();
+  if (lane == 0) {
+    if (ncc) atomicAdd(&s0, ncc);
+    if (nnr) atomicAdd(&s1, nnr);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (s0) atomicAdd(ctr + 0, s0);
+    if (s1) atomicAdd(ctr + 1, s1);
+  }
+}
+
+// ------------------------------------------------------------ k_compact
+// Tiles of TR rows per block.  Pass 1 counts root slots (HIGH) and their
+// sizes, one block scan, two global atomics allocate [ci_base, +cnt) and
+// [mem_base, +size_sum); pass 2 (L1-resident re-read) writes
+// csize[ci], coff[ci] and rewrites the root slot to HIGH | ci.
+constexpr int CT_THREADS = 256;
+constexpr int CT_ROWS = 32;
+
+__device__ __forceinline__ void block_scan2(unsigned long long a, unsigned long long b,
+                                            unsigned long long &ea, unsigned long long &eb,
+                                            unsigned long long &ta, unsigned long long &tb) {
+  __shared__ unsigned long long wa[CT_THREADS / 32], wb[CT_THREADS / 32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long ia = a, ib = b;
+  for (int d = 1; d < 32; d <<= 1) {
+    unsigned long long ya = __shfl_up_sync(0xffffffffu, ia, d);
+    unsigned long long yb = __shfl_up_sync(0xffffffffu, ib, d);
+    if (lane >= d) {
+      ia += ya;
+      ib += yb;
+    }
+  }
+  if (lane == 31) {
+    wa[wid] = ia;
+    wb[wid] = ib;
+  }
+  __syncthreads();
+  unsigned long long pa = 0, pb = 0;
+  ta = tb = 0;
+  for (int w = 0; w < CT_THREADS / 32; w++) {
+    if (w < wid) {
+      pa += wa[w];
+      pb += wb[w];
+    }
+    ta += wa[w];
+    tb += wb[w];
+  }
+  ea = pa + ia - a;
+  eb = pb + ib - b;
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(CT_THREADS) k_compact(uint32_t *L, uint32_t n, uint32_t B,
+                                                        uint32_t *csize, uint64_t *coff,
+                                                        unsigned long long *ctr) {
+  __shared__ unsigned long long base_c, base_m;
+  const size_t per_tile = (size_t)CT_ROWS * B;
+  const size_t ntiles = ((size_t)n + CT_ROWS - 1) / CT_ROWS;
+  for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const size_t e0 = t * per_tile;
+    const size_t e1 = min(e0 + per_tile, (size_t)n * B);
+    unsigned long long c = 0, msum = 0;
+    for (size_t e = e0 + threadIdx.x; e < e1; e += CT_THREADS) {
+      uint32_t s = L[e];
+      if (s & PACIM_HIGH) {
+        c++;
+        msum += s & PACIM_LOW;
+      }
+    }
+    unsigned long long ec, em, tc, tm;
+    block_scan2(c, msum, ec, em, tc, tm);
+    if (threadIdx.x == 0) {
+      base_c = tc ? atomicAdd(ctr + 2, tc) : 0;
+      base_m = tm ? atomicAdd(ctr + 3, tm) : 0;
+    }
+    __syncthreads();
+    unsigned long long ci = base_c + ec, mo = base_m + em;
+    for (size_t e = e0 + threadIdx.x; e < e1; e += CT_THREADS) {
+      uint32_t s = L[e];
+      if (s & PACIM_HIGH) {
+        uint32_t sz = s & PACIM_LOW;
+        csize[ci] = sz;
+        coff[ci] = mo;
+        L[e] = PACIM_HIGH | (uint32_t)ci;
+        ci++;
+        mo += sz;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// --------------------------------------------------------- k_gain_scatter
+// Warp per vertex row; lanes over slots.  gain0[v] (+)= sum_j |C_j(v)| and
+// v is written into its component's member range (cursor atomics).
+__global__ void __launch_bounds__(256) k_gain_scatter(const uint32_t *__restrict__ L, uint32_t n,
+                                                      uint32_t B, const uint32_t *csize,
+                                                      const uint64_t *coff, uint32_t *cfill,
+                                                      uint32_t *perm, int64_t *gain0,
+                                                      int accumulate) {
+  const int lane = threadIdx.x & 31;
+  size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t v = warp; v < n; v += nw) {
+    long long g = 0;
+    for (uint32_t j = lane; j < B; j += 32) {
+      uint32_t s = L[v * B + j];
+      if (s == (uint32_t)v) {
+        g += 1;  // singleton CC
+        continue;
+      }
+      uint32_t ci = (s & PACIM_HIGH) ? (s & PACIM_LOW) : (__ldg(L + (size_t)s * B + j) & PACIM_LOW);
+      uint32_t sz = csize[ci];
+      g += sz;
+      uint32_t pos = atomicAdd(cfill + ci, 1u);
+      perm[coff[ci] + pos] = (uint32_t)v;
+    }
+    for (int d = 16; d; d >>= 1) g += __shfl_xor_sync(0xffffffffu, g, d);
+    if (lane == 0) gain0[v] = accumulate ? gain0[v] + g : g;
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host
+static float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  return ms;
+}
+
+void pc_build(pacim_ctx *ctx) {
+  const uint32_t n = ctx->n, B = ctx->R_local;
+  PC_REQUIRE(B >= 1 && B <= 65535, PACIM_EINVAL, "local sketch count must be in [1, 65535]");
+  PC_REQUIRE(!ctx->compressed, PACIM_ENOTIMPL, "compressed store not built by pc_build");
+  // ---- slot table (host): local sketches sorted by hi32(hash(r)) (R2)
+  ctx->slot_r.clear();
+  ctx->r_slot.assign(ctx->R, -1);
+  std::vector<std::pair<uint32_t, uint32_t>> hs;
+  for (uint32_t r = ctx->rank; r < ctx->R; r += ctx->world) {
+    uint64_t h = pc_mix64(((1ull << 63) | (uint64_t)r) ^ ctx->K);
+    hs.push_back({(uint32_t)(h >> 32), r});
+  }
+  std::sort(hs.begin(), hs.end());
+  ctx->shr.resize(B);
+  ctx->slot_r.resize(B);
+  for (uint32_t j = 0; j < B; j++) {
+    ctx->shr[j] = hs[j].first;
+    ctx->slot_r[j] = hs[j].second;
+    ctx->r_slot[hs[j].second] = (int32_t)j;
+  }
+  const uint32_t NT = 1u << PACIM_TB;
+  ctx->tab.assign(NT + 1, 0);
+  {
+    uint32_t j = 0;
+    for (uint32_t p = 0; p <= NT; p++) {
+      while (j < B && (ctx->shr[j] >> (32 - PACIM_TB)) < p) j++;
+      ctx->tab[p] = (uint16_t)j;
+    }
+  }
+  pc_ensure(ctx, ctx->d_shr, B * sizeof(uint32_t));
+  pc_ensure(ctx, ctx->d_tab, (NT + 1) * sizeof(uint16_t));
+  PC_CUDA(cudaMemcpyAsync(ctx->d_shr.p, ctx->shr.data(), B * 4, cudaMemcpyHostToDevice,
+                          ctx->stream));
+  PC_CUDA(cudaMemcpyAsync(ctx->d_tab.p, ctx->tab.data(), (NT + 1) * 2, cudaMemcpyHostToDevice,
+                          ctx->stream));
+
+  // ---- buffers
+  pc_ensure(ctx, ctx->L, (size_t)n * B * sizeof(uint32_t));
+  pc_ensure(ctx, ctx->gain0, (size_t)n * sizeof(int64_t));
+  pc_ensure(ctx, ctx->counters, 64 * sizeof(uint64_t));
+  unsigned long long *ctr = ctx->counters.as<unsigned long long>();
+  PC_CUDA(cudaMemsetAsync(ctr, 0, 64 * sizeof(uint64_t), ctx->stream));
+  uint32_t *L = ctx->L.as<uint32_t>();
+
+  cudaEvent_t ev[6];
+  for (auto &e : ev) PC_CUDA(cudaEventCreate(&e));
+  ctx->launches = 0;
+  const unsigned rows_grid = pc_grid(ctx, (size_t)n * 32, 256, 16);
+
+  PC_CUDA(cudaEventRecord(ev[0], ctx->stream));
+  k_init<<<rows_grid, 256, 0, ctx->stream>>>(L, n, B);
+  PC_CHECK_LAUNCH();
+  PC_CUDA(cudaEventRecord(ev[1], ctx->stream));
+  {
+    size_t smem = B * sizeof(uint32_t) + (NT + 1) * sizeof(uint16_t);
+    unsigned g = pc_grid(ctx, ctx->m, 256, 8);
+    if (ctx->pmodel == PACIM_P_WIC) {
+      PC_CUDA(cudaFuncSetAttribute(k_edges<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+      k_edges<true><<<g, 256, smem, ctx->stream>>>(ctx->keys.as<uint64_t>(),
+                                                    ctx->tm1.as<uint32_t>(), ctx->m, ctx->K, 0,
+                                                    ctx->d_shr.as<uint32_t>(),
+                                                    ctx->d_tab.as<uint16_t>(), B, L, ctr + 4);
+    } else {
+      PC_CUDA(cudaFuncSetAttribute(k_edges<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+      k_edges<false><<<g, 256, smem, ctx->stream>>>(ctx->keys.as<uint64_t>(), nullptr, ctx->m,
+                                                     ctx->K, ctx->t32, ctx->d_shr.as<uint32_t>(),
+                                                     ctx->d_tab.as<uint16_t>(), B, L, ctr + 4);
+    }
+    PC_CHECK_LAUNCH();
+  }
+  PC_CUDA(cudaEventRecord(ev[2], ctx->stream));
+  k_compress_count<<<rows_grid, 256, 0, ctx->stream>>>(L, n, B, ctr);
+  PC_CHECK_LAUNCH();
+  PC_CUDA(cudaEventRecord(ev[3], ctx->stream));
+  // pool sizes -> host (one sync per build)
+  unsigned long long hc[2];
+  PC_CUDA(cudaMemcpyAsync(hc, ctr, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->ncomp = hc[0];
+  ctx->nmember = hc[0] + hc[1];
+  PC_REQUIRE(ctx->ncomp < (1ull << 31), PACIM_ENOTIMPL,
+             "more than 2^31 non-singleton components in one store");
+  pc_ensure(ctx, ctx->csize, std::max<size_t>(ctx->ncomp, 1) * 4);
+  pc_ensure(ctx, ctx->csize_work, std::max<size_t>(ctx->ncomp, 1) * 4);
+  pc_ensure(ctx, ctx->coff, std::max<size_t>(ctx->ncomp, 1) * 8);
+  pc_ensure(ctx, ctx->cfill, std::max<size_t>(ctx->ncomp, 1) * 4);
+  pc_ensure(ctx, ctx->perm, std::max<size_t>(ctx->nmember, 1) * 4);
+  PC_CUDA(cudaMemsetAsync(ctx->cfill.p, 0, std::max<size_t>(ctx->ncomp, 1) * 4, ctx->stream));
+  k_compact<<<pc_grid(ctx, ((size_t)n + CT_ROWS - 1) / CT_ROWS * CT_THREADS, CT_THREADS, 8),
+              CT_THREADS, 0, ctx->stream>>>(L, n, B, ctx->csize.as<uint32_t>(),
+                                            ctx->coff.as<uint64_t>(), ctr);
+  PC_CHECK_LAUNCH();
+  PC_CUDA(cudaEventRecord(ev[4], ctx->stream));
+  k_gain_scatter<<<rows_grid, 256, 0, ctx->stream>>>(
+      L, n, B, ctx->csize.as<uint32_t>(), ctx->coff.as<uint64_t>(), ctx->cfill.as<uint32_t>(),
+      ctx->perm.as<uint32_t>(), ctx->gain0.as<int64_t>(), 0);
+  PC_CHECK_LAUNCH();
+  PC_CUDA(cudaEventRecord(ev[5], ctx->stream));
+  ctx->launches += 5;
+  unsigned long long h[6];
+  PC_CUDA(cudaMemcpyAsync(h, ctr, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  PC_REQUIRE(h[2] == ctx->ncomp && h[3] == ctx->nmember, PACIM_ECHECK,
+             "compact: component/member totals disagree with compress_count");
+  ctx->stats.live_pairs = h[4];
+  ctx->stats.t_init_ms = ev_ms(ev[0], ev[1]);
+  ctx->stats.t_edges_ms = ev_ms(ev[1], ev[2]);
+  ctx->stats.t_compress_ms = ev_ms(ev[2], ev[3]);
+  ctx->stats.t_compact_ms = ev_ms(ev[3], ev[4]);
+  ctx->stats.t_gain_ms = ev_ms(ev[4], ev[5]);
+  ctx->stats.t_centers_ms = 0;
+  ctx->stats.t_build_ms = ev_ms(ev[0], ev[5]);
+  ctx->stats.kernel_launches_build = ctx->launches;
+  for (auto &e : ev) cudaEventDestroy(e);
+}
+
+// canonical labels of one slot: slot value is v (singleton), HIGH|ci (root:
+// label v) or the root id (R8: min id of the CC)
+namespace {
+__global__ void k_labels(const uint32_t *L, uint32_t n, uint32_t B, uint32_t j, uint32_t *out) {
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (size_t)gridDim.x * blockDim.x) {
+    uint32_t s = L[v * B + j];
+    out[v] = (s == (uint32_t)v || (s & PACIM_HIGH)) ? (uint32_t)v : s;
+  }
+}
+}  // namespace
+
+void pc_get_labels(pacim_ctx *ctx, uint32_t slot, uint32_t *host_out) {
+  TmpBuf t(ctx);
+  pc_ensure(ctx, t, (size_t)ctx->n * 4);
+  k_labels<<<pc_grid(ctx, ctx->n, 256), 256, 0, ctx->stream>>>(ctx->L.as<uint32_t>(), ctx->n,
+                                                              ctx->R_local, slot, t.as<uint32_t>());
+  PC_CHECK_LAUNCH();
+  PC_CUDA(cudaMemcpyAsync(host_out, t.p, (size_t)ctx->n * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+}

@@ -1,0 +1,592 @@
+// graph.cu — H0/H1: CSR load, validation, upper edge list, WIC thresholds,
+// and the on-device synthetic generators (DESIGN.md §Input recipe).
+//
+// Sorting in the generators uses CUB radix sort (setup stage, outside the
+// timed build/select step); every other kernel here is hand-written.
+#include <cub/cub.cuh>
+
+#include "pacim_internal.cuh"
+
+// ------------------------------------------------------------------- scan
+// Exclusive prefix sum of u64 (3-phase: tile reduce, recursive scan of tile
+// sums, tile scan + base).  In-place allowed.
+namespace {
+constexpr int SCAN_BLOCK = 512;
+constexpr int SCAN_ITEMS = 8;
+constexpr int SCAN_TILE = SCAN_BLOCK * SCAN_ITEMS;
+
+__device__ __forceinline__ uint64_t block_excl_scan(uint64_t x, uint64_t *warp_tot,
+                                                    uint64_t &block_total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  uint64_t inc = x;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint64_t y = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += y;
+  }
+  if (lane == 31) warp_tot[wid] = inc;
+  __syncthreads();
+  if (wid == 0) {
+    const int nw = blockDim.x >> 5;
+    uint64_t t = lane < nw ? warp_tot[lane] : 0, ti = t;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint64_t y = __shfl_up_sync(0xffffffffu, ti, d);
+      if (lane >= d) ti += y;
+    }
+    if (lane < nw) warp_tot[lane] = ti - t;
+    if (lane == nw - 1) warp_tot[32] = ti;
+  }
+  __syncthreads();
+  block_total = warp_tot[32];
+  uint64_t r = inc - x + warp_tot[wid];
+  __syncthreads();
+  return r;
+}
+
+__global__ void __launch_bounds__(SCAN_BLOCK) k_scan_reduce(const uint64_t *in, size_t N,
+                                                            uint64_t *sums) {
+  __shared__ uint64_t wt[33];
+  size_t base = (size_t)blockIdx.x * SCAN_TILE;
+  uint64_t s = 0;
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    size_t idx = base + (size_t)i * SCAN_BLOCK + threadIdx.x;
+    if (idx < N) s += in[idx];
+  }
+  uint64_t tot;
+  block_excl_scan(s, wt, tot);
+  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(SCAN_BLOCK) k_scan_apply(const uint64_t *in, uint64_t *out,
+                                                           size_t N, const uint64_t *tile_base) {
+  __shared__ uint64_t tile[SCAN_TILE];
+  __shared__ uint64_t wt[33];
+  size_t base = (size_t)blockIdx.x * SCAN_TILE;
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    size_t idx = base + (size_t)i * SCAN_BLOCK + threadIdx.x;
+    tile[i * SCAN_BLOCK + threadIdx.x] = idx < N ? in[idx] : 0;
+  }
+  __syncthreads();
+  uint64_t v[SCAN_ITEMS], s = 0;
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    v[i] = tile[threadIdx.x * SCAN_ITEMS + i];
+    s += v[i];
+  }
+  uint64_t tot;
+  uint64_t run = block_excl_scan(s, wt, tot) + (tile_base ? tile_base[blockIdx.x] : 0);
+#pragma unroll
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    tile[threadIdx.x * SCAN_ITEMS + i] = run;
+    run += v[i];
+  }
+  __syncthreads();
+  for (int i = 0; i < SCAN_ITEMS; i++) {
+    size_t idx = base + (size_t)i * SCAN_BLOCK + threadIdx.x;
+    if (idx < N) out[idx] = tile[i * SCAN_BLOCK + threadIdx.x];
+  }
+}
+}  // namespace
+
+static void scan_rec(pacim_ctx *ctx, const uint64_t *in, uint64_t *out, size_t N,
+                     uint64_t *tmp) {
+  size_t nb = (N + SCAN_TILE - 1) / SCAN_TILE;
+  if (nb <= 1) {
+    k_scan_apply<<<1, SCAN_BLOCK, 0, ctx->stream>>>(in, out, N, nullptr);
+    PC_CHECK_LAUNCH();
+    ctx->launches++;
+    return;
+  }
+  uint64_t *sums = tmp;
+  k_scan_reduce<<<(unsigned)nb, SCAN_BLOCK, 0, ctx->stream>>>(in, N, sums);
+  PC_CHECK_LAUNCH();
+  scan_rec(ctx, sums, sums, nb, tmp + nb);
+  k_scan_apply<<<(unsigned)nb, SCAN_BLOCK, 0, ctx->stream>>>(in, out, N, sums);
+  PC_CHECK_LAUNCH();
+  ctx->launches += 2;
+}
+
+void pc_exclusive_scan_u64(pacim_ctx *ctx, const uint64_t *in, uint64_t *out, size_t N) {
+  if (N == 0) return;
+  size_t need = 0, t = N;
+  while (t > 1) {
+    t = (t + SCAN_TILE - 1) / SCAN_TILE;
+    need += t + 1;
+  }
+  pc_ensure(ctx, ctx->scratch2, (need + 1) * sizeof(uint64_t));
+  scan_rec(ctx, in, out, N, ctx->scratch2.as<uint64_t>());
+}
+
+// ------------------------------------------------------------- validation
+namespace {
+// One warp per vertex: offsets monotone, ids < n, no self loop, strictly
+// increasing lists.  bad[0] = smallest offending vertex (atomicMin).
+__global__ void k_validate(const uint64_t *off, const uint32_t *nbr, uint32_t n,
+                           uint32_t *bad) {
+  const int lane = threadIdx.x & 31;
+  size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t v = warp; v < n; v += nwarps) {
+    uint64_t a = off[v], b = off[v + 1];
+    bool ok = b >= a;
+    if (ok) {
+      for (uint64_t e = a + lane; e < b; e += 32) {
+        uint32_t w = nbr[e];
+        if (w >= n || w == (uint32_t)v || (e > a && nbr[e - 1] >= w)) ok = false;
+      }
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    if (!ok && lane == 0) atomicMin(bad, (uint32_t)v);
+  }
+}
+
+// Symmetry: for each entry (v, w), v must appear in w's (sorted) list.
+__global__ void k_validate_sym(const uint64_t *off, const uint32_t *nbr, uint32_t n,
+                               uint32_t *bad) {
+  const int lane = threadIdx.x & 31;
+  size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t v = warp; v < n; v += nwarps) {
+    bool ok = true;
+    for (uint64_t e = off[v] + lane; e < off[v + 1]; e += 32) {
+      uint32_t w = nbr[e];
+      uint64_t lo = off[w], hi = off[w + 1];
+      while (lo < hi) {
+        uint64_t mid = (lo + hi) >> 1;
+        if (nbr[mid] < (uint32_t)v) lo = mid + 1; else hi = mid;
+      }
+      if (lo == off[w + 1] || nbr[lo] != (uint32_t)v) ok = false;
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    if (!ok && lane == 0) atomicMin(bad, (uint32_t)v);
+  }
+}
+
+// Upper degree: number of neighbours w > v (lists are sorted).
+__global__ void k_upper_count(const uint64_t *off, const uint32_t *nbr, uint32_t n,
+                              uint64_t *ucnt) {
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (size_t)gridDim.x * blockDim.x) {
+    uint64_t lo = off[v], hi = off[v + 1], end = hi;
+    while (lo < hi) {
+      uint64_t mid = (lo + hi) >> 1;
+      if (nbr[mid] <= (uint32_t)v) lo = mid + 1; else hi = mid;
+    }
+    ucnt[v] = end - lo;
+  }
+}
+
+// keys[ustart[v] + i] = v<<32 | w for the i-th neighbour w > v (warp per vertex).
+__global__ void k_upper_fill(const uint64_t *off, const uint32_t *nbr, uint32_t n,
+                             const uint64_t *ustart, const uint64_t *ucnt, uint64_t *keys) {
+  const int lane = threadIdx.x & 31;
+  size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t v = warp; v < n; v += nwarps) {
+    uint64_t c = ucnt[v];
+    uint64_t first = off[v + 1] - c, dst = ustart[v];
+    for (uint64_t i = lane; i < c; i += 32)
+      keys[dst + i] = ((uint64_t)v << 32) | nbr[first + i];
+  }
+}
+
+// R4: WIC threshold T32 = min(2^32, floor(2^33 / (d_u + d_v))), stored as T32-1.
+__global__ void k_wic(const uint64_t *keys, uint64_t m, const uint64_t *off, uint32_t *tm1) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (size_t)gridDim.x * blockDim.x) {
+    uint64_t k = keys[e];
+    uint32_t u = (uint32_t)(k >> 32), v = (uint32_t)k;
+    uint64_t s = (off[u + 1] - off[u]) + (off[v + 1] - off[v]);
+    uint64_t t = (1ull << 33) / s;
+    if (t > (1ull << 32)) t = 1ull << 32;
+    tm1[e] = (uint32_t)(t - 1);
+  }
+}
+}  // namespace
+
+void pc_graph_finish_load(pacim_ctx *ctx, int validate) {
+  const uint32_t n = ctx->n;
+  uint64_t *off = ctx->off.as<uint64_t>();
+  uint32_t *nbr = ctx->nbr.as<uint32_t>();
+  pc_ensure(ctx, ctx->counters, 64 * sizeof(uint64_t));
+  if (validate) {
+    uint32_t *bad = ctx->counters.as<uint32_t>();
+    PC_CUDA(cudaMemsetAsync(bad, 0xFF, sizeof(uint32_t), ctx->stream));
+    k_validate<<<pc_grid(ctx, (size_t)n * 32, 256), 256, 0, ctx->stream>>>(off, nbr, n, bad);
+    PC_CHECK_LAUNCH();
+    if (validate >= 2) {
+      k_validate_sym<<<pc_grid(ctx, (size_t)n * 32, 256), 256, 0, ctx->stream>>>(off, nbr, n, bad);
+      PC_CHECK_LAUNCH();
+    }
+    uint32_t hbad = 0;
+    PC_CUDA(cudaMemcpyAsync(&hbad, bad, 4, cudaMemcpyDeviceToHost, ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (hbad != 0xFFFFFFFFu) {
+      throw PacimError{PACIM_EINVAL,
+                       "CSR invalid at vertex " + std::to_string(hbad) +
+                           (validate >= 2 ? " (range/order/loop/duplicate/asymmetry)"
+                                          : " (range/order/loop/duplicate)")};
+    }
+  }
+  // upper edge list (sorted keys): counts -> scan -> fill
+  pc_ensure(ctx, ctx->scratch, 2 * ((size_t)n + 1) * sizeof(uint64_t));
+  uint64_t *ucnt = ctx->scratch.as<uint64_t>();
+  uint64_t *ustart = ucnt + n + 1;
+  k_upper_count<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(off, nbr, n, ucnt);
+  PC_CHECK_LAUNCH();
+  pc_exclusive_scan_u64(ctx, ucnt, ustart, n);
+  pc_ensure(ctx, ctx->keys, std::max<size_t>(ctx->m, 1) * sizeof(uint64_t));
+  k_upper_fill<<<pc_grid(ctx, (size_t)n * 32, 256), 256, 0, ctx->stream>>>(
+      off, nbr, n, ustart, ucnt, ctx->keys.as<uint64_t>());
+  PC_CHECK_LAUNCH();
+  if (ctx->pmodel == PACIM_P_WIC) {
+    pc_ensure(ctx, ctx->tm1, std::max<size_t>(ctx->m, 1) * sizeof(uint32_t));
+    k_wic<<<pc_grid(ctx, ctx->m, 256), 256, 0, ctx->stream>>>(ctx->keys.as<uint64_t>(), ctx->m,
+                                                             off, ctx->tm1.as<uint32_t>());
+    PC_CHECK_LAUNCH();
+  }
+  ctx->launches += 4;
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// ------------------------------------------------------------- generators
+namespace {
+// ER candidate j: u = (lo32(w) n) >> 32, v = (hi32(w) n) >> 32 (loop -> ~0).
+__global__ void k_gen_er(uint64_t Kg, uint32_t n, uint64_t j0, uint64_t J, uint64_t *key,
+                         uint64_t *idx) {
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < J;
+       t += (size_t)gridDim.x * blockDim.x) {
+    uint64_t j = j0 + t;
+    uint64_t w = pc_mix64(Kg ^ j);
+    uint32_t u = (uint32_t)(((w & 0xFFFFFFFFull) * n) >> 32);
+    uint32_t v = (uint32_t)(((w >> 32) * n) >> 32);
+    uint64_t a = u < v ? u : v, b = u < v ? v : u;
+    key[t] = (u == v) ? ~0ull : ((a << 32) | b);
+    idx[t] = j;
+  }
+}
+
+__device__ __forceinline__ uint64_t rmat_perm(uint64_t x, int s) {
+  uint64_t mask = (s >= 64) ? ~0ull : ((1ull << s) - 1);
+  int sh = (s + 1) / 2;
+  x = (x * 0x9E3779B97F4A7C15ull) & mask;
+  x ^= x >> sh;
+  x = (x * 0xBF58476D1CE4E5B9ull) & mask;
+  x ^= x >> sh;
+  return x;
+}
+
+// R-MAT sample i: per level l, y = mix64(Kg ^ (i*64+l)) >> 11 picks the
+// quadrant against 53-bit thresholds; level l sets bit scale-1-l.
+__global__ void k_gen_rmat(uint64_t Kg, int scale, uint64_t i0, uint64_t cnt, uint64_t ta,
+                           uint64_t tab, uint64_t tabc, int permute, uint64_t *key) {
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt;
+       t += (size_t)gridDim.x * blockDim.x) {
+    uint64_t i = i0 + t, u = 0, v = 0;
+    for (int l = 0; l < scale; l++) {
+      uint64_t y = pc_mix64(Kg ^ (i * 64 + (uint64_t)l)) >> 11;
+      uint64_t bit = 1ull << (scale - 1 - l);
+      if (y < ta) {
+      } else if (y < tab) {
+        v |= bit;
+      } else if (y < tabc) {
+        u |= bit;
+      } else {
+        u |= bit;
+        v |= bit;
+      }
+    }
+    if (permute) {
+      u = rmat_perm(u, scale);
+      v = rmat_perm(v, scale);
+    }
+    uint64_t a = u < v ? u : v, b = u < v ? v : u;
+    key[t] = (u == v) ? ~0ull : ((a << 32) | b);
+  }
+}
+
+// Grid: per vertex, count of edges to larger ids (right, down, diagonal).
+__device__ __forceinline__ int grid_edges(uint64_t Kg, uint32_t W, uint32_t H, uint64_t d32,
+                                          uint64_t v, uint64_t *out) {
+  uint64_t i = v / W, j = v % W;
+  int c = 0;
+  if (j + 1 < W) out[c++] = (v << 32) | (v + 1);
+  if (i + 1 < H) out[c++] = (v << 32) | (v + W);
+  if (i + 1 < H && j + 1 < W && (pc_mix64(Kg ^ v) >> 32) < d32) out[c++] = (v << 32) | (v + W + 1);
+  return c;
+}
+
+__global__ void k_grid_count(uint64_t Kg, uint32_t W, uint32_t H, uint64_t d32, uint64_t *cnt) {
+  uint64_t nv = (uint64_t)W * H;
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv;
+       v += (size_t)gridDim.x * blockDim.x) {
+    uint64_t tmp[3];
+    cnt[v] = grid_edges(Kg, W, H, d32, v, tmp);
+  }
+}
+
+__global__ void k_grid_fill(uint64_t Kg, uint32_t W, uint32_t H, uint64_t d32,
+                            const uint64_t *start, uint64_t *keys) {
+  uint64_t nv = (uint64_t)W * H;
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv;
+       v += (size_t)gridDim.x * blockDim.x) {
+    uint64_t tmp[3];
+    int c = grid_edges(Kg, W, H, d32, v, tmp);
+    for (int q = 0; q < c; q++) keys[start[v] + q] = tmp[q];
+  }
+}
+
+// first-occurrence flag of sorted keys (excluding the ~0 loop sentinel)
+__global__ void k_first_flag(const uint64_t *k, uint64_t N, uint64_t *flag) {
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < N;
+       t += (size_t)gridDim.x * blockDim.x)
+    flag[t] = (k[t] != ~0ull && (t == 0 || k[t] != k[t - 1])) ? 1 : 0;
+}
+
+__global__ void k_compact2(const uint64_t *k, const uint64_t *v, const uint64_t *flag,
+                           const uint64_t *pos, uint64_t N, uint64_t *ko, uint64_t *vo) {
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < N;
+       t += (size_t)gridDim.x * blockDim.x)
+    if (flag[t]) {
+      ko[pos[t]] = k[t];
+      if (v) vo[pos[t]] = v[t];
+    }
+}
+
+// CSR from sorted distinct keys: degree histograms.
+__global__ void k_deg_hist(const uint64_t *keys, uint64_t m, uint64_t *dlo, uint64_t *dhi) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (size_t)gridDim.x * blockDim.x) {
+    uint64_t k = keys[e];
+    atomicAdd((unsigned long long *)&dhi[k >> 32], 1ull);
+    atomicAdd((unsigned long long *)&dlo[k & 0xFFFFFFFFull], 1ull);
+  }
+}
+
+__global__ void k_add2(const uint64_t *a, const uint64_t *b, uint64_t *c, uint64_t N) {
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < N;
+       t += (size_t)gridDim.x * blockDim.x)
+    c[t] = a[t] + b[t];
+}
+
+// upper half of row a: position e - hstart[a] after the dlo[a] lower entries
+__global__ void k_fill_hi(const uint64_t *keys, uint64_t m, const uint64_t *off,
+                          const uint64_t *dlo, const uint64_t *hstart, uint32_t *nbr) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (size_t)gridDim.x * blockDim.x) {
+    uint64_t k = keys[e];
+    uint32_t a = (uint32_t)(k >> 32), b = (uint32_t)k;
+    nbr[off[a] + dlo[a] + (e - hstart[a])] = b;
+  }
+}
+
+// lower half of row b from the (b, a)-sorted swapped keys
+__global__ void k_fill_lo(const uint64_t *sw, uint64_t m, const uint64_t *off,
+                          const uint64_t *lstart, uint32_t *nbr) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (size_t)gridDim.x * blockDim.x) {
+    uint64_t k = sw[e];
+    uint32_t b = (uint32_t)(k >> 32), a = (uint32_t)k;
+    nbr[off[b] + (e - lstart[b])] = a;
+  }
+}
+
+__global__ void k_swap_halves(const uint64_t *in, uint64_t *out, uint64_t m) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (size_t)gridDim.x * blockDim.x) {
+    uint64_t k = in[e];
+    out[e] = (k << 32) | (k >> 32);
+  }
+}
+}  // namespace
+
+static void sort_keys(pacim_ctx *ctx, uint64_t *keys, uint64_t *alt, uint64_t N, int end_bit,
+                      uint64_t **result) {
+  cub::DoubleBuffer<uint64_t> db(keys, alt);
+  size_t tmp = 0;
+  PC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, db, (int64_t)N, 0, end_bit, ctx->stream));
+  TmpBuf t(ctx);
+  pc_ensure(ctx, t, tmp + 16);
+  PC_CUDA(cub::DeviceRadixSort::SortKeys(t.p, tmp, db, (int64_t)N, 0, end_bit, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  pc_free(ctx, t);
+  *result = db.Current();
+}
+
+static void sort_pairs(pacim_ctx *ctx, uint64_t *k, uint64_t *k2, uint64_t *v, uint64_t *v2,
+                       uint64_t N, int end_bit, uint64_t **rk, uint64_t **rv) {
+  cub::DoubleBuffer<uint64_t> dk(k, k2), dv(v, v2);
+  size_t tmp = 0;
+  PC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int64_t)N, 0, end_bit,
+                                          ctx->stream));
+  TmpBuf t(ctx);
+  pc_ensure(ctx, t, tmp + 16);
+  PC_CUDA(cub::DeviceRadixSort::SortPairs(t.p, tmp, dk, dv, (int64_t)N, 0, end_bit, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  pc_free(ctx, t);
+  *rk = dk.Current();
+  *rv = dv.Current();
+}
+
+// Unique sorted keys of k[0..N) into out; returns count.  Uses flag/pos scratch.
+static uint64_t unique_sorted(pacim_ctx *ctx, const uint64_t *k, const uint64_t *v, uint64_t N,
+                              uint64_t *ko, uint64_t *vo) {
+  TmpBuf flag(ctx), pos(ctx);
+  pc_ensure(ctx, flag, (N + 1) * sizeof(uint64_t));
+  pc_ensure(ctx, pos, (N + 1) * sizeof(uint64_t));
+  unsigned g = pc_grid(ctx, N, 256);
+  k_first_flag<<<g, 256, 0, ctx->stream>>>(k, N, flag.as<uint64_t>());
+  PC_CHECK_LAUNCH();
+  pc_exclusive_scan_u64(ctx, flag.as<uint64_t>(), pos.as<uint64_t>(), N + 1);
+  uint64_t cnt = 0;
+  PC_CUDA(cudaMemcpyAsync(&cnt, pos.as<uint64_t>() + N, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  k_compact2<<<g, 256, 0, ctx->stream>>>(k, v, flag.as<uint64_t>(), pos.as<uint64_t>(), N, ko, vo);
+  PC_CHECK_LAUNCH();
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  pc_free(ctx, flag);
+  pc_free(ctx, pos);
+  return cnt;
+}
+
+// Build the full CSR (off, nbr) from ctx->keys (sorted distinct, m entries).
+static void csr_from_keys(pacim_ctx *ctx) {
+  const uint32_t n = ctx->n;
+  const uint64_t m = ctx->m;
+  pc_ensure(ctx, ctx->off, ((size_t)n + 1) * sizeof(uint64_t));
+  pc_ensure(ctx, ctx->nbr, std::max<size_t>(2 * m, 1) * sizeof(uint32_t));
+  TmpBuf d(ctx);
+  pc_ensure(ctx, d, 5 * ((size_t)n + 1) * sizeof(uint64_t));
+  uint64_t *dlo = d.as<uint64_t>(), *dhi = dlo + n + 1, *deg = dhi + n + 1, *lstart = deg + n + 1,
+           *hstart = lstart + n + 1;
+  PC_CUDA(cudaMemsetAsync(dlo, 0, 2 * ((size_t)n + 1) * sizeof(uint64_t), ctx->stream));
+  uint64_t *keys = ctx->keys.as<uint64_t>();
+  k_deg_hist<<<pc_grid(ctx, m, 256), 256, 0, ctx->stream>>>(keys, m, dlo, dhi);
+  PC_CHECK_LAUNCH();
+  k_add2<<<pc_grid(ctx, n + 1, 256), 256, 0, ctx->stream>>>(dlo, dhi, deg, (uint64_t)n + 1);
+  PC_CHECK_LAUNCH();
+  pc_exclusive_scan_u64(ctx, deg, ctx->off.as<uint64_t>(), (size_t)n + 1);
+  pc_exclusive_scan_u64(ctx, dlo, lstart, n);
+  pc_exclusive_scan_u64(ctx, dhi, hstart, n);
+  k_fill_hi<<<pc_grid(ctx, m, 256), 256, 0, ctx->stream>>>(keys, m, ctx->off.as<uint64_t>(), dlo,
+                                                          hstart, ctx->nbr.as<uint32_t>());
+  PC_CHECK_LAUNCH();
+  TmpBuf sw(ctx), sw2(ctx);
+  pc_ensure(ctx, sw, std::max<size_t>(m, 1) * sizeof(uint64_t));
+  pc_ensure(ctx, sw2, std::max<size_t>(m, 1) * sizeof(uint64_t));
+  k_swap_halves<<<pc_grid(ctx, m, 256), 256, 0, ctx->stream>>>(keys, sw.as<uint64_t>(), m);
+  PC_CHECK_LAUNCH();
+  uint64_t *sorted = nullptr;
+  sort_keys(ctx, sw.as<uint64_t>(), sw2.as<uint64_t>(), m, 64, &sorted);
+  k_fill_lo<<<pc_grid(ctx, m, 256), 256, 0, ctx->stream>>>(sorted, m, ctx->off.as<uint64_t>(),
+                                                          lstart, ctx->nbr.as<uint32_t>());
+  PC_CHECK_LAUNCH();
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  pc_free(ctx, sw);
+  pc_free(ctx, sw2);
+  pc_free(ctx, d);
+}
+
+void pc_generate(pacim_ctx *ctx, int kind, const uint64_t *params, int nparams,
+                 uint64_t gen_seed) {
+  uint64_t Kg = pc_mix64(gen_seed ^ 0xD1B54A32D192ED03ull);
+  if (kind == PACIM_GEN_ER) {
+    PC_REQUIRE(nparams >= 2, PACIM_EINVAL, "ER needs params {n, m}");
+    uint64_t n = params[0], m = params[1];
+    PC_REQUIRE(n >= 2 && n < (1ull << 31), PACIM_EINVAL, "ER: n out of range");
+    PC_REQUIRE(m >= 1 && m <= n * (n - 1) / 4, PACIM_EINVAL, "ER: m must be <= n(n-1)/4");
+    ctx->n = (uint32_t)n;
+    uint64_t J = m + m / 4 + 1024;
+    for (;;) {
+      TmpBuf a(ctx), b(ctx), c(ctx), d2(ctx), ko(ctx), vo(ctx);
+      pc_ensure(ctx, a, J * 8); pc_ensure(ctx, b, J * 8);
+      pc_ensure(ctx, c, J * 8); pc_ensure(ctx, d2, J * 8);
+      k_gen_er<<<pc_grid(ctx, J, 256), 256, 0, ctx->stream>>>(Kg, (uint32_t)n, 0, J,
+                                                             a.as<uint64_t>(), b.as<uint64_t>());
+      PC_CHECK_LAUNCH();
+      uint64_t *sk, *sv;
+      sort_pairs(ctx, a.as<uint64_t>(), c.as<uint64_t>(), b.as<uint64_t>(), d2.as<uint64_t>(), J,
+                 64, &sk, &sv);
+      // first occurrence (smallest j, stable sort) of each distinct pair
+      pc_ensure(ctx, ko, J * 8); pc_ensure(ctx, vo, J * 8);
+      uint64_t cnt = unique_sorted(ctx, sk, sv, J, ko.as<uint64_t>(), vo.as<uint64_t>());
+      if (cnt < m) {
+        J *= 2;
+        continue;
+      }
+      // order the distinct pairs by their first draw index j; keep the first m
+      uint64_t *rk, *rv;
+      sort_pairs(ctx, vo.as<uint64_t>(), a.as<uint64_t>(), ko.as<uint64_t>(), b.as<uint64_t>(),
+                 cnt, 64, &rk, &rv);
+      pc_ensure(ctx, ctx->keys, m * 8);
+      PC_CUDA(cudaMemcpyAsync(ctx->keys.p, rv, m * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+      uint64_t *fin;
+      sort_keys(ctx, ctx->keys.as<uint64_t>(), c.as<uint64_t>(), m, 64, &fin);
+      if (fin != ctx->keys.as<uint64_t>())
+        PC_CUDA(cudaMemcpyAsync(ctx->keys.p, fin, m * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+      PC_CUDA(cudaStreamSynchronize(ctx->stream));
+      ctx->m = m;
+      break;
+    }
+  } else if (kind == PACIM_GEN_RMAT) {
+    PC_REQUIRE(nparams >= 6, PACIM_EINVAL, "RMAT needs {scale, ef, ta, tab, tabc, permute}");
+    int scale = (int)params[0];
+    uint64_t ef = params[1];
+    PC_REQUIRE(scale >= 1 && scale <= 30, PACIM_EINVAL, "RMAT: scale must be in [1, 30]");
+    PC_REQUIRE(ef >= 1 && ef <= 64, PACIM_EINVAL, "RMAT: ef must be in [1, 64]");
+    ctx->n = 1u << scale;
+    uint64_t ns = ef << scale;
+    TmpBuf a(ctx), b(ctx);
+    pc_ensure(ctx, a, ns * 8);
+    pc_ensure(ctx, b, ns * 8);
+    k_gen_rmat<<<pc_grid(ctx, ns, 256, 16), 256, 0, ctx->stream>>>(
+        Kg, scale, 0, ns, params[2], params[3], params[4], (int)params[5], a.as<uint64_t>());
+    PC_CHECK_LAUNCH();
+    uint64_t *sk;
+    sort_keys(ctx, a.as<uint64_t>(), b.as<uint64_t>(), ns, 64, &sk);
+    uint64_t *other = (sk == a.as<uint64_t>()) ? b.as<uint64_t>() : a.as<uint64_t>();
+    uint64_t cnt = unique_sorted(ctx, sk, nullptr, ns, other, nullptr);
+    pc_free(ctx, ctx->keys);
+    pc_ensure(ctx, ctx->keys, std::max<uint64_t>(cnt, 1) * 8);
+    PC_CUDA(cudaMemcpyAsync(ctx->keys.p, other, cnt * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    pc_free(ctx, a);
+    pc_free(ctx, b);
+    ctx->m = cnt;
+  } else if (kind == PACIM_GEN_GRID) {
+    PC_REQUIRE(nparams >= 3, PACIM_EINVAL, "GRID needs {W, H, d32}");
+    uint64_t W = params[0], H = params[1], d32 = params[2];
+    PC_REQUIRE(W >= 1 && H >= 1 && W * H < (1ull << 31), PACIM_EINVAL, "GRID: bad size");
+    ctx->n = (uint32_t)(W * H);
+    TmpBuf cnt(ctx), start(ctx);
+    pc_ensure(ctx, cnt, (W * H + 1) * 8);
+    pc_ensure(ctx, start, (W * H + 1) * 8);
+    k_grid_count<<<pc_grid(ctx, W * H, 256), 256, 0, ctx->stream>>>(Kg, (uint32_t)W, (uint32_t)H,
+                                                                   d32, cnt.as<uint64_t>());
+    PC_CHECK_LAUNCH();
+    PC_CUDA(cudaMemsetAsync(cnt.as<uint64_t>() + W * H, 0, 8, ctx->stream));
+    pc_exclusive_scan_u64(ctx, cnt.as<uint64_t>(), start.as<uint64_t>(), W * H + 1);
+    uint64_t m = 0;
+    PC_CUDA(cudaMemcpyAsync(&m, start.as<uint64_t>() + W * H, 8, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    pc_ensure(ctx, ctx->keys, std::max<uint64_t>(m, 1) * 8);
+    k_grid_fill<<<pc_grid(ctx, W * H, 256), 256, 0, ctx->stream>>>(
+        Kg, (uint32_t)W, (uint32_t)H, d32, start.as<uint64_t>(), ctx->keys.as<uint64_t>());
+    PC_CHECK_LAUNCH();
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    pc_free(ctx, cnt);
+    pc_free(ctx, start);
+    ctx->m = m;
+  } else {
+    throw PacimError{PACIM_EINVAL, "unknown generator kind"};
+  }
+  csr_from_keys(ctx);
+  if (ctx->pmodel == PACIM_P_WIC) {
+    pc_ensure(ctx, ctx->tm1, std::max<size_t>(ctx->m, 1) * sizeof(uint32_t));
+    k_wic<<<pc_grid(ctx, ctx->m, 256), 256, 0, ctx->stream>>>(
+        ctx->keys.as<uint64_t>(), ctx->m, ctx->off.as<uint64_t>(), ctx->tm1.as<uint32_t>());
+    PC_CHECK_LAUNCH();
+  }
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+}

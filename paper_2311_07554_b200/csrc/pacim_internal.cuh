@@ -1,0 +1,168 @@
+// pacim_internal.cuh — device helpers and the context of the B200 CUDA path.
+//
+// This is the PRODUCT path.  It shares nothing with oracle/ (its own hash,
+// generator and graph code are written here, from the paper and DESIGN.md's
+// readings).  Citation keys: P:n = PAPER.md line n; Hn = SURVEY.md §8(a) row;
+// Rn = DESIGN.md reading n.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/pacim.h"
+
+// Root-slot marker of the uncompressed store (DESIGN.md §Store layout):
+//   slot(v, j) == v            v is a singleton in sketch j
+//   slot(v, j) & PACIM_HIGH    v is the root (min id) of a non-singleton CC;
+//                              low 31 bits = CC size (after compress_count) or
+//                              compact component index ci (after compact)
+//   otherwise                  slot(v, j) = root id of v's CC (< v)
+#define PACIM_HIGH 0x80000000u
+#define PACIM_LOW 0x7FFFFFFFu
+#define PACIM_TB 12  // bits of the sketch bucket table (R2 candidate enumeration)
+
+// ------------------------------------------------------------------ hash (R1)
+__host__ __device__ __forceinline__ uint64_t pc_mix64(uint64_t z) {
+  z ^= z >> 30;
+  z *= 0xBF58476D1CE4E5B9ull;
+  z ^= z >> 27;
+  z *= 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return z;
+}
+
+// ------------------------------------------------------------ error helpers
+struct PacimError {
+  int code;
+  std::string msg;
+};
+
+#define PC_CUDA(call)                                                        \
+  do {                                                                       \
+    cudaError_t e_ = (call);                                                 \
+    if (e_ != cudaSuccess)                                                   \
+      throw PacimError{e_ == cudaErrorMemoryAllocation ? PACIM_ENOMEM        \
+                                                       : PACIM_ECUDA,        \
+                       std::string(#call) + ": " + cudaGetErrorString(e_)};  \
+  } while (0)
+
+#define PC_CHECK_LAUNCH() PC_CUDA(cudaGetLastError())
+
+#define PC_REQUIRE(cond, code, msg)                                           \
+  do {                                                                        \
+    if (!(cond)) throw PacimError{code, msg};                                 \
+  } while (0)
+
+// ------------------------------------------------------- device allocation
+struct DevBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  template <typename T>
+  T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+struct pacim_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  std::string err;
+  int sm_count = 148;
+  uint64_t device_bytes = 0;
+
+  // ---- graph (H0/H1)
+  bool has_graph = false;
+  uint32_t n = 0;
+  uint64_t m = 0;        // undirected edges
+  int pmodel = 0;        // PACIM_P_CONST / PACIM_P_WIC
+  uint64_t t32 = 0;      // constant threshold (R3)
+  DevBuf off;            // u64[n+1] full CSR offsets
+  DevBuf nbr;            // u32[2m]  full CSR neighbours
+  DevBuf keys;           // u64[m]   upper edge list min<<32|max, sorted
+  DevBuf tm1;            // u32[m]   WIC: T32(e) - 1
+
+  // ---- sketches
+  bool built = false;
+  uint32_t R = 0, R_local = 0, rank = 0, world = 1;
+  uint64_t hash_seed = 0, K = 0, a32 = 0;
+  bool compressed = false;
+  std::vector<uint32_t> slot_r;   // slot j -> sketch id r  (slots sorted by hash(r))
+  std::vector<int32_t> r_slot;    // sketch id r -> slot j or -1
+  std::vector<uint32_t> shr;      // hr32 of slot j (sorted ascending)
+  std::vector<uint16_t> tab;      // bucket table, (1<<PACIM_TB)+1 entries
+  DevBuf d_shr, d_tab;
+
+  // uncompressed store: L[v*B + j] (B = R_local)
+  DevBuf L;
+  uint64_t ncomp = 0, nmember = 0;
+  DevBuf csize;       // u32[ncomp] pristine CC sizes
+  DevBuf csize_work;  // u32[ncomp] sizes zeroed on cover (MarkSeed)
+  DevBuf coff;        // u64[ncomp] member-index offsets
+  DevBuf cfill;       // u32[ncomp] scatter cursors
+  DevBuf perm;        // u32[nmember] members grouped by component
+  DevBuf gain0;       // i64[n]
+  DevBuf gain;        // i64[n] working gains of a selection
+
+  // compressed store (H6c)
+  uint32_t rho = 0;
+  DevBuf center_of;   // u32[n] center index or 0xFFFFFFFF
+  DevBuf clabel;      // u32[rho*B]  label of center i in slot j at i*B + j
+  DevBuf csz;         // u32[rho*B]  pristine sizes
+  DevBuf csz_work;    // u32[rho*B]  sizes zeroed by MarkSeed
+  DevBuf Ltmp;        // u32[n*Bb] parent arrays of one build batch
+
+  // scratch
+  DevBuf counters;    // u64[64]
+  DevBuf scratch;     // generic temporary
+  DevBuf scratch2;
+  unsigned long long *h_counters = nullptr;  // pinned host mirror (64)
+
+  // selection outputs (device)
+  DevBuf sel_seeds, sel_gain, sel_partial, sel_list, sel_flag;
+
+  pacim_stats stats{};
+  uint32_t launches = 0;
+};
+
+// allocation with capacity reuse
+void pc_ensure(pacim_ctx *ctx, DevBuf &b, size_t bytes);
+void pc_free(pacim_ctx *ctx, DevBuf &b);
+
+// temporary device buffer released at scope exit (also on exceptions)
+struct TmpBuf : DevBuf {
+  pacim_ctx *c;
+  explicit TmpBuf(pacim_ctx *c_) : c(c_) {}
+  ~TmpBuf() { pc_free(c, *this); }
+  TmpBuf(const TmpBuf &) = delete;
+  TmpBuf &operator=(const TmpBuf &) = delete;
+};
+
+// ---------------------------------------------------------- host wrappers
+// graph.cu
+void pc_exclusive_scan_u64(pacim_ctx *ctx, const uint64_t *in, uint64_t *out,
+                           size_t N);
+void pc_graph_finish_load(pacim_ctx *ctx, int validate);
+void pc_generate(pacim_ctx *ctx, int kind, const uint64_t *params, int nparams,
+                 uint64_t gen_seed);
+// build.cu
+void pc_build(pacim_ctx *ctx);
+// select.cu
+void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
+               int64_t *sigma_num);
+void pc_select_reset(pacim_ctx *ctx);
+void pc_cover_local(pacim_ctx *ctx, uint32_t s, int64_t *d_delta,
+                    int64_t *local_gain);
+void pc_argmax(pacim_ctx *ctx, const int64_t *d_gain, uint32_t n, uint32_t *s,
+               int64_t *g);
+void pc_get_labels(pacim_ctx *ctx, uint32_t slot, uint32_t *host_out);
+
+// grid sizing: multiples of the SM count (148 on B200)
+inline unsigned pc_grid(const pacim_ctx *ctx, size_t work, unsigned block,
+                        unsigned per_sm = 8) {
+  size_t need = (work + block - 1) / block;
+  size_t cap = (size_t)ctx->sm_count * per_sm;
+  if (need < 1) need = 1;
+  return (unsigned)(need < cap ? need : cap);
+}
