@@ -58,27 +58,23 @@ static int guarded(pacim_ctx *ctx, F &&f) {
   }
 }
 
-static void drop_sketches(pacim_ctx *ctx) {
-  pc_free(ctx, ctx->L);
-  pc_free(ctx, ctx->csize);
-  pc_free(ctx, ctx->csize_work);
-  pc_free(ctx, ctx->coff);
-  pc_free(ctx, ctx->cfill);
-  pc_free(ctx, ctx->perm);
-  pc_free(ctx, ctx->clabel);
-  pc_free(ctx, ctx->csz);
-  pc_free(ctx, ctx->csz_work);
-  pc_free(ctx, ctx->Ltmp);
-  ctx->built = false;
-}
+// Dropping keeps the device buffers as capacity for the next load/build
+// (pc_ensure reuses them); they are released by pacim_destroy.
+static void drop_sketches(pacim_ctx *ctx) { ctx->built = false; }
 
 static void drop_graph(pacim_ctx *ctx) {
   drop_sketches(ctx);
-  pc_free(ctx, ctx->off);
-  pc_free(ctx, ctx->nbr);
-  pc_free(ctx, ctx->keys);
-  pc_free(ctx, ctx->tm1);
   ctx->has_graph = false;
+}
+
+static void free_all(pacim_ctx *ctx) {
+  DevBuf *bufs[] = {&ctx->off,   &ctx->nbr,        &ctx->keys,     &ctx->tm1,      &ctx->L,
+                    &ctx->csize, &ctx->csize_work, &ctx->coff,     &ctx->cfill,    &ctx->perm,
+                    &ctx->clabel, &ctx->csz,       &ctx->csz_work, &ctx->Ltmp,     &ctx->d_shr,
+                    &ctx->d_tab, &ctx->gain0,      &ctx->gain,     &ctx->center_of, &ctx->counters,
+                    &ctx->scratch, &ctx->scratch2, &ctx->sel_seeds, &ctx->sel_gain,
+                    &ctx->sel_partial, &ctx->sel_list, &ctx->sel_flag};
+  for (DevBuf *b : bufs) pc_free(ctx, *b);
 }
 
 extern "C" {
@@ -130,20 +126,7 @@ void pacim_destroy(pacim_ctx *ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
-  drop_graph(ctx);
-  pc_free(ctx, ctx->d_shr);
-  pc_free(ctx, ctx->d_tab);
-  pc_free(ctx, ctx->gain0);
-  pc_free(ctx, ctx->gain);
-  pc_free(ctx, ctx->center_of);
-  pc_free(ctx, ctx->counters);
-  pc_free(ctx, ctx->scratch);
-  pc_free(ctx, ctx->scratch2);
-  pc_free(ctx, ctx->sel_seeds);
-  pc_free(ctx, ctx->sel_gain);
-  pc_free(ctx, ctx->sel_partial);
-  pc_free(ctx, ctx->sel_list);
-  pc_free(ctx, ctx->sel_flag);
+  free_all(ctx);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }
