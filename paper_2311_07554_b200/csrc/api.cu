@@ -71,6 +71,7 @@ static void free_all(pacim_ctx *ctx) {
   DevBuf *bufs[] = {&ctx->off,   &ctx->nbr,        &ctx->keys,     &ctx->tm1,      &ctx->L,
                     &ctx->csize, &ctx->csize_work, &ctx->coff,     &ctx->cfill,    &ctx->perm,
                     &ctx->clabel, &ctx->csz,       &ctx->csz_work, &ctx->Ltmp,     &ctx->d_shr,
+                    &ctx->d_hot,
                     &ctx->d_tab, &ctx->gain0,      &ctx->gain,     &ctx->center_of, &ctx->counters,
                     &ctx->scratch, &ctx->scratch2, &ctx->sel_seeds, &ctx->sel_gain,
                     &ctx->sel_partial, &ctx->sel_list, &ctx->sel_flag};

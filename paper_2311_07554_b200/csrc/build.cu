@@ -1,25 +1,35 @@
 // build.cu — Step 1 of Alg. 1: Sketch(r) for every local sketch.
 //
 // Store layout (DESIGN.md §Store layout): the uncompressed store is ONE u32
-// array L[v*B + j] (vertex-major; slot j = local sketch ordered by hash(r)).
+// array L[v*B + j] (vertex-major; slot j = local sketch, slots sorted by
+// hash(r) so that correlated sketches are adjacent in a row).
 // During the build it is the union-find parent array of all B sketches; after
 // compress_count / compact it is the per-vertex CC memo of P:597-601.
 //
 // Kernels (one pass each over L):
 //   k_init            L[v][j] = v                                   (H3 setup)
 //   k_edges           per upper edge: hash, candidate sketches, live test,
-//                     lock-free hook-larger-root-under-smaller union (H2, H3)
+//                     lock-free hook-larger-root-under-smaller union (H2, H3);
+//                     a warp flattens the candidate (edge, slot) pairs of 32
+//                     edges and unites 32 pairs per round (adjacent slots of
+//                     one edge -> coalesced row accesses, no idle lanes)
+//   k_hot_roots       per slot the root of the hub vertex (hot component)
 //   k_compress_count  full path compression to the min-id root (H4) and CC
-//                     sizes counted into the root slot (H5)
+//                     sizes counted into the root slot (H5); the hot root's
+//                     count is aggregated per block in shared memory
 //   k_compact         root slots -> compact component ids, member-index
 //                     ranges allocated per tile                    (H6u)
 //   k_gain_scatter    gain0[v] = sum_j |C_j(v)| (H7) and the member index
-//                     perm grouped by component (H6u)
+//                     perm grouped by component (H6u); hot-component cursor
+//                     reservations aggregated per tile in shared memory
 #include <algorithm>
 
 #include "pacim_internal.cuh"
 
 namespace {
+
+constexpr uint32_t HOT_MAX = 1024;  // slots with a shared-memory hot-root cache
+constexpr uint32_t NONE = 0xFFFFFFFFu;
 
 __device__ __forceinline__ uint32_t ld_cg(const uint32_t *p) { return __ldcg(p); }
 
@@ -33,7 +43,7 @@ __global__ void k_init(uint32_t *L, uint32_t n, uint32_t B) {
     for (size_t v = warp; v < n; v += nw) {
       uint4 *row = reinterpret_cast<uint4 *>(L + v * B);
       uint4 x = make_uint4((uint32_t)v, (uint32_t)v, (uint32_t)v, (uint32_t)v);
-      for (uint32_t j = lane; j < B4; j += 32) __stcs(row + j, x);
+      for (uint32_t j = lane; j < B4; j += 32) row[j] = x;
     }
   } else {
     for (size_t v = warp; v < n; v += nw)
@@ -81,79 +91,141 @@ __device__ __forceinline__ void uf_unite(uint32_t *L, uint32_t B, uint32_t j, ui
 // implies the top w = clz(T-1) bits of shr[j] and he agree, so the candidate
 // slots of an edge are one contiguous range of the sorted table (exact; R2
 // candidate enumeration, SURVEY §8(a) note).
+constexpr int EDGE_THREADS = 256;
+constexpr int EDGE_WARPS = EDGE_THREADS / 32;
+
 template <bool WIC>
-__global__ void __launch_bounds__(256) k_edges(const uint64_t *__restrict__ keys,
-                                               const uint32_t *__restrict__ tm1, uint64_t m,
-                                               uint64_t K, uint64_t t32,
-                                               const uint32_t *__restrict__ g_shr,
-                                               const uint16_t *__restrict__ g_tab, uint32_t B,
-                                               uint32_t *L, unsigned long long *live_ctr) {
+__global__ void __launch_bounds__(EDGE_THREADS) k_edges(const uint64_t *__restrict__ keys,
+                                                        const uint32_t *__restrict__ tm1,
+                                                        uint64_t m, uint64_t K, uint64_t t32,
+                                                        const uint32_t *__restrict__ g_shr,
+                                                        const uint16_t *__restrict__ g_tab,
+                                                        uint32_t B, uint32_t *L,
+                                                        unsigned long long *live_ctr) {
   extern __shared__ uint32_t sm[];
   uint32_t *shr = sm;
   uint16_t *tab = reinterpret_cast<uint16_t *>(sm + B);
+  __shared__ uint32_t w_u[EDGE_WARPS][32], w_v[EDGE_WARPS][32], w_he[EDGE_WARPS][32];
+  __shared__ uint32_t w_lo[EDGE_WARPS][32], w_pre[EDGE_WARPS][33];
+  __shared__ uint64_t w_T[EDGE_WARPS][32];
   for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) shr[i] = g_shr[i];
   for (uint32_t i = threadIdx.x; i <= (1u << PACIM_TB); i += blockDim.x) tab[i] = g_tab[i];
   __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const size_t gw = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long live = 0;
-  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
-       e += (size_t)gridDim.x * blockDim.x) {
-    const uint64_t key = keys[e];
-    const uint64_t T = WIC ? (uint64_t)tm1[e] + 1 : t32;
-    if (T == 0) continue;
-    const uint32_t he = (uint32_t)(pc_mix64(key ^ K) >> 32);
-    const uint32_t w = __clz((uint32_t)(T - 1));
-    uint32_t lo, hi;
-    if (w >= PACIM_TB) {
-      uint32_t p = he >> (32 - PACIM_TB);
-      lo = tab[p];
-      hi = tab[p + 1];
-    } else if (w == 0) {
-      lo = 0;
-      hi = B;
-    } else {
-      uint32_t p = (he >> (32 - w)) << (PACIM_TB - w);
-      lo = tab[p];
-      hi = tab[p + (1u << (PACIM_TB - w))];
+  for (size_t base = gw * 32; base < m; base += nw * 32) {
+    // ---- one edge per lane: hash and candidate slot range
+    const size_t e = base + lane;
+    uint32_t cnt = 0;
+    if (e < m) {
+      const uint64_t key = keys[e];
+      const uint64_t T = WIC ? (uint64_t)tm1[e] + 1 : t32;
+      const uint32_t he = (uint32_t)(pc_mix64(key ^ K) >> 32);
+      uint32_t lo = 0, hi = 0;
+      if (T != 0) {
+        const uint32_t w = __clz((uint32_t)(T - 1));
+        if (w >= PACIM_TB) {
+          uint32_t p = he >> (32 - PACIM_TB);
+          lo = tab[p];
+          hi = tab[p + 1];
+        } else if (w == 0) {
+          lo = 0;
+          hi = B;
+        } else {
+          uint32_t p = (he >> (32 - w)) << (PACIM_TB - w);
+          lo = tab[p];
+          hi = tab[p + (1u << (PACIM_TB - w))];
+        }
+      }
+      cnt = hi - lo;
+      w_u[wid][lane] = (uint32_t)(key >> 32);
+      w_v[wid][lane] = (uint32_t)key;
+      w_he[wid][lane] = he;
+      w_T[wid][lane] = T;
+      w_lo[wid][lane] = lo;
     }
-    const uint32_t u = (uint32_t)(key >> 32), v = (uint32_t)key;
-    for (uint32_t j = lo; j < hi; j++) {
-      if ((uint64_t)(shr[j] ^ he) < T) {
-        uf_unite(L, B, j, u, v);
-        live++;
+    // ---- exclusive prefix of candidate counts across the warp
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+      if (lane >= d) inc += y;
+    }
+    w_pre[wid][lane] = inc - cnt;
+    const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
+    if (lane == 31) w_pre[wid][32] = total;
+    __syncwarp();
+    // ---- 32 (edge, slot) candidate pairs per round
+    for (uint32_t c0 = 0; c0 < total; c0 += 32) {
+      const uint32_t idx = c0 + lane;
+      if (idx < total) {
+        uint32_t a = 0, b = 32;  // largest i with pre[i] <= idx
+        while (b - a > 1) {
+          uint32_t mid = (a + b) >> 1;
+          if (w_pre[wid][mid] <= idx) a = mid; else b = mid;
+        }
+        const uint32_t j = w_lo[wid][a] + (idx - w_pre[wid][a]);
+        if ((uint64_t)(shr[j] ^ w_he[wid][a]) < w_T[wid][a]) {
+          uf_unite(L, B, j, w_u[wid][a], w_v[wid][a]);
+          live++;
+        }
       }
     }
+    __syncwarp();
   }
   // block-aggregated counter
   for (int d = 16; d; d >>= 1) live += __shfl_xor_sync(0xffffffffu, live, d);
   __shared__ unsigned long long bsum;
   if (threadIdx.x == 0) bsum = 0;
   __syncthreads();
-  if ((threadIdx.x & 31) == 0 && live) atomicAdd(&bsum, live);
+  if (lane == 0 && live) atomicAdd(&bsum, live);
   __syncthreads();
   if (threadIdx.x == 0 && bsum) atomicAdd(live_ctr, bsum);
 }
 
-// ------------------------------------------------------ k_compress_count
-// find that also stops at a converted root slot (HIGH set)
-__device__ __forceinline__ uint32_t uf_find_root(uint32_t *L, uint32_t B, uint32_t j,
-                                                 uint32_t x) {
+// ---------------------------------------------------------- hot roots
+// read-only find that also stops at a converted root slot (HIGH set)
+__device__ __forceinline__ uint32_t find_ro(const uint32_t *L, uint32_t B, uint32_t j,
+                                            uint32_t x) {
   for (;;) {
     uint32_t p = ld_cg(L + (size_t)x * B + j);
     if (p == x || (p & PACIM_HIGH)) return x;
-    uint32_t gp = ld_cg(L + (size_t)p * B + j);
-    if (gp == p || (gp & PACIM_HIGH)) return p;
-    // atomicMin, not a plain store: a slot may only move towards the root,
-    // so a racing halving can never undo the owner's full compression
-    atomicMin(L + (size_t)x * B + j, gp);
-    x = gp;
+    x = p;
   }
 }
 
-// For every non-root (v, j): slot <- root (full compression, H4); root slot
-// becomes HIGH | size by CAS(root -> HIGH|1) then atomicAdd(+1) per member
-// (H5).  ctr[0] += CCs of size >= 2, ctr[1] += non-root entries.
+__global__ void k_hot_roots(const uint32_t *L, uint32_t B, uint32_t hub, uint32_t *hot) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < B; j += gridDim.x * blockDim.x)
+    hot[j] = find_ro(L, B, j, hub);
+}
+
+// ------------------------------------------------------ k_compress_count
+// For every non-root (v, j): slot <- root (full compression, H4; only the
+// owner writes its slot, finds are read-only, so the result is final); the
+// root slot becomes HIGH | size by CAS(root -> HIGH|1) then atomicAdd per
+// member (H5).  Members of the slot's hot root are counted in shared memory
+// and added once per block.  ctr[0] += CCs of size >= 2, ctr[1] += non-roots.
+__device__ __forceinline__ bool add_to_root(uint32_t *L, uint32_t B, uint32_t j, uint32_t root,
+                                            uint32_t cnt) {
+  uint32_t *rs = L + (size_t)root * B + j;
+  if (!(ld_cg(rs) & PACIM_HIGH)) atomicCAS(rs, root, PACIM_HIGH | 1u);
+  uint32_t old = atomicAdd(rs, cnt);
+  return old == (PACIM_HIGH | 1u);  // the first add after conversion: a new CC
+}
+
 __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n, uint32_t B,
+                                                        const uint32_t *hot,
                                                         unsigned long long *ctr) {
+  extern __shared__ uint32_t hsm[];
+  const uint32_t H = min(B, HOT_MAX);
+  uint32_t *hroot = hsm, *hcnt = hsm + H;
+  for (uint32_t j = threadIdx.x; j < H; j += blockDim.x) {
+    hroot[j] = hot[j];
+    hcnt[j] = 0;
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
   size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
@@ -163,15 +235,19 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
       uint32_t *slot = L + v * B + j;
       uint32_t s = ld_cg(slot);
       if (s == (uint32_t)v || (s & PACIM_HIGH)) continue;  // root (or singleton)
-      uint32_t root = uf_find_root(L, B, j, s);
-      if (root != s) atomicMin(slot, root);
-      uint32_t *rs = L + (size_t)root * B + j;
-      atomicCAS(rs, root, PACIM_HIGH | 1u);
-      uint32_t old = atomicAdd(rs, 1u);
-      if (old == (PACIM_HIGH | 1u)) ncc++;
+      uint32_t root = find_ro(L, B, j, s);
+      if (root != s) *slot = root;
       nnr++;
+      if (j < H && root == hroot[j]) {
+        atomicAdd(hcnt + j, 1u);
+      } else if (add_to_root(L, B, j, root, 1u)) {
+        ncc++;
+      }
     }
   }
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < H; j += blockDim.x)
+    if (hcnt[j] && add_to_root(L, B, j, hroot[j], hcnt[j])) ncc++;
   for (int d = 16; d; d >>= 1) {
     ncc += __shfl_xor_sync(0xffffffffu, ncc, d);
     nnr += __shfl_xor_sync(0xffffffffu, nnr, d);
@@ -191,10 +267,10 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
 }
 
 // ------------------------------------------------------------ k_compact
-// Tiles of TR rows per block.  Pass 1 counts root slots (HIGH) and their
+// Tiles of CT_ROWS rows per block.  Pass 1 counts root slots (HIGH) and their
 // sizes, one block scan, two global atomics allocate [ci_base, +cnt) and
-// [mem_base, +size_sum); pass 2 (L1-resident re-read) writes
-// csize[ci], coff[ci] and rewrites the root slot to HIGH | ci.
+// [mem_base, +size_sum); pass 2 (cache-resident re-read) writes csize[ci],
+// coff[ci] and rewrites the root slot to HIGH | ci.
 constexpr int CT_THREADS = 256;
 constexpr int CT_ROWS = 32;
 
@@ -272,33 +348,91 @@ __global__ void __launch_bounds__(CT_THREADS) k_compact(uint32_t *L, uint32_t n,
   }
 }
 
+// hot component id per slot: the compacted id of the hub's root (or NONE)
+__global__ void k_hot_ci(const uint32_t *L, uint32_t B, const uint32_t *hot_root,
+                         uint32_t *hot_ci) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < B; j += gridDim.x * blockDim.x) {
+    uint32_t s = L[(size_t)hot_root[j] * B + j];
+    hot_ci[j] = (s & PACIM_HIGH) ? (s & PACIM_LOW) : NONE;
+  }
+}
+
 // --------------------------------------------------------- k_gain_scatter
-// Warp per vertex row; lanes over slots.  gain0[v] (+)= sum_j |C_j(v)| and
-// v is written into its component's member range (cursor atomics).
-__global__ void __launch_bounds__(256) k_gain_scatter(const uint32_t *__restrict__ L, uint32_t n,
-                                                      uint32_t B, const uint32_t *csize,
-                                                      const uint64_t *coff, uint32_t *cfill,
-                                                      uint32_t *perm, int64_t *gain0,
-                                                      int accumulate) {
-  const int lane = threadIdx.x & 31;
-  size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
-  for (size_t v = warp; v < n; v += nw) {
-    long long g = 0;
-    for (uint32_t j = lane; j < B; j += 32) {
-      uint32_t s = L[v * B + j];
-      if (s == (uint32_t)v) {
-        g += 1;  // singleton CC
-        continue;
+// Tiles of GS_ROWS rows; warp per row, lanes over slots.  gain0[v] (+)=
+// sum_j |C_j(v)| and v is written into its component's member range.
+// Members of the slot's hot component are counted per tile in shared memory
+// (bit flags remember which), one global cursor reservation per slot and
+// tile, then placed from shared-memory cursors.
+constexpr int GS_THREADS = 256;
+constexpr int GS_ROWS = 64;
+
+__global__ void __launch_bounds__(GS_THREADS) k_gain_scatter(
+    const uint32_t *__restrict__ L, uint32_t n, uint32_t B, const uint32_t *csize,
+    const uint64_t *coff, uint32_t *cfill, uint32_t *perm, int64_t *gain0, int accumulate,
+    const uint32_t *g_hot_ci) {
+  extern __shared__ uint32_t gsm[];
+  const uint32_t H = min(B, HOT_MAX);
+  const uint32_t HW = (H + 31) / 32;  // flag words per row
+  uint32_t *hci = gsm, *hcnt = gsm + H, *hcur = gsm + 2 * H;
+  uint32_t *flags = gsm + 3 * H;                                        // GS_ROWS * HW
+  unsigned long long *hbase = reinterpret_cast<unsigned long long *>(
+      gsm + ((3 * H + GS_ROWS * HW + 1) & ~1u));                        // H entries
+  for (uint32_t j = threadIdx.x; j < H; j += blockDim.x) {
+    hci[j] = g_hot_ci[j];
+    hcnt[j] = 0;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const size_t ntiles = ((size_t)n + GS_ROWS - 1) / GS_ROWS;
+  for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    for (uint32_t i = threadIdx.x; i < GS_ROWS * HW; i += blockDim.x) flags[i] = 0;
+    __syncthreads();
+    // ---- pass 1
+    for (uint32_t r = wid; r < GS_ROWS; r += GS_THREADS / 32) {
+      const size_t v = t * GS_ROWS + r;
+      if (v >= n) break;
+      long long g = 0;
+      for (uint32_t j = lane; j < B; j += 32) {
+        uint32_t s = L[v * B + j];
+        if (s == (uint32_t)v) {
+          g += 1;  // singleton CC
+          continue;
+        }
+        uint32_t ci = (s & PACIM_HIGH) ? (s & PACIM_LOW) : (__ldg(L + (size_t)s * B + j) & PACIM_LOW);
+        g += csize[ci];
+        if (j < H && ci == hci[j]) {
+          atomicAdd(hcnt + j, 1u);
+          atomicOr(flags + r * HW + (j >> 5), 1u << (j & 31));
+        } else {
+          uint32_t pos = atomicAdd(cfill + ci, 1u);
+          perm[coff[ci] + pos] = (uint32_t)v;
+        }
       }
-      uint32_t ci = (s & PACIM_HIGH) ? (s & PACIM_LOW) : (__ldg(L + (size_t)s * B + j) & PACIM_LOW);
-      uint32_t sz = csize[ci];
-      g += sz;
-      uint32_t pos = atomicAdd(cfill + ci, 1u);
-      perm[coff[ci] + pos] = (uint32_t)v;
+      for (int d = 16; d; d >>= 1) g += __shfl_xor_sync(0xffffffffu, g, d);
+      if (lane == 0) gain0[v] = accumulate ? gain0[v] + g : g;
     }
-    for (int d = 16; d; d >>= 1) g += __shfl_xor_sync(0xffffffffu, g, d);
-    if (lane == 0) gain0[v] = accumulate ? gain0[v] + g : g;
+    __syncthreads();
+    // ---- one reservation per hot component and tile
+    for (uint32_t j = threadIdx.x; j < H; j += blockDim.x) {
+      uint32_t c = hcnt[j];
+      if (c) {
+        hbase[j] = coff[hci[j]] + atomicAdd(cfill + hci[j], c);
+        hcur[j] = 0;
+      }
+    }
+    __syncthreads();
+    // ---- pass 2: place the flagged hot members
+    for (uint32_t r = wid; r < GS_ROWS; r += GS_THREADS / 32) {
+      const size_t v = t * GS_ROWS + r;
+      if (v >= n) break;
+      for (uint32_t j = lane; j < H; j += 32) {
+        if (flags[r * HW + (j >> 5)] & (1u << (j & 31))) {
+          uint32_t pos = atomicAdd(hcur + j, 1u);
+          perm[hbase[j] + pos] = (uint32_t)v;
+        }
+      }
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < H; j += blockDim.x) hcnt[j] = 0;
   }
 }
 
@@ -342,6 +476,7 @@ void pc_build(pacim_ctx *ctx) {
   }
   pc_ensure(ctx, ctx->d_shr, B * sizeof(uint32_t));
   pc_ensure(ctx, ctx->d_tab, (NT + 1) * sizeof(uint16_t));
+  pc_ensure(ctx, ctx->d_hot, 2 * (size_t)B * sizeof(uint32_t));
   PC_CUDA(cudaMemcpyAsync(ctx->d_shr.p, ctx->shr.data(), B * 4, cudaMemcpyHostToDevice,
                           ctx->stream));
   PC_CUDA(cudaMemcpyAsync(ctx->d_tab.p, ctx->tab.data(), (NT + 1) * 2, cudaMemcpyHostToDevice,
@@ -354,6 +489,8 @@ void pc_build(pacim_ctx *ctx) {
   unsigned long long *ctr = ctx->counters.as<unsigned long long>();
   PC_CUDA(cudaMemsetAsync(ctr, 0, 64 * sizeof(uint64_t), ctx->stream));
   uint32_t *L = ctx->L.as<uint32_t>();
+  uint32_t *hot_root = ctx->d_hot.as<uint32_t>(), *hot_ci = hot_root + B;
+  const uint32_t H = std::min<uint32_t>(B, HOT_MAX);
 
   cudaEvent_t ev[6];
   for (auto &e : ev) PC_CUDA(cudaEventCreate(&e));
@@ -366,25 +503,27 @@ void pc_build(pacim_ctx *ctx) {
   PC_CUDA(cudaEventRecord(ev[1], ctx->stream));
   {
     size_t smem = B * sizeof(uint32_t) + (NT + 1) * sizeof(uint16_t);
-    unsigned g = pc_grid(ctx, ctx->m, 256, 8);
+    unsigned g = pc_grid(ctx, (ctx->m + 31) / 32 * 32, EDGE_THREADS, 8);
     if (ctx->pmodel == PACIM_P_WIC) {
       PC_CUDA(cudaFuncSetAttribute(k_edges<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
-      k_edges<true><<<g, 256, smem, ctx->stream>>>(ctx->keys.as<uint64_t>(),
-                                                    ctx->tm1.as<uint32_t>(), ctx->m, ctx->K, 0,
-                                                    ctx->d_shr.as<uint32_t>(),
-                                                    ctx->d_tab.as<uint16_t>(), B, L, ctr + 4);
+      k_edges<true><<<g, EDGE_THREADS, smem, ctx->stream>>>(
+          ctx->keys.as<uint64_t>(), ctx->tm1.as<uint32_t>(), ctx->m, ctx->K, 0,
+          ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, L, ctr + 4);
     } else {
       PC_CUDA(cudaFuncSetAttribute(k_edges<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
-      k_edges<false><<<g, 256, smem, ctx->stream>>>(ctx->keys.as<uint64_t>(), nullptr, ctx->m,
-                                                     ctx->K, ctx->t32, ctx->d_shr.as<uint32_t>(),
-                                                     ctx->d_tab.as<uint16_t>(), B, L, ctr + 4);
+      k_edges<false><<<g, EDGE_THREADS, smem, ctx->stream>>>(
+          ctx->keys.as<uint64_t>(), nullptr, ctx->m, ctx->K, ctx->t32, ctx->d_shr.as<uint32_t>(),
+          ctx->d_tab.as<uint16_t>(), B, L, ctr + 4);
     }
     PC_CHECK_LAUNCH();
   }
   PC_CUDA(cudaEventRecord(ev[2], ctx->stream));
-  k_compress_count<<<rows_grid, 256, 0, ctx->stream>>>(L, n, B, ctr);
+  k_hot_roots<<<(B + 255) / 256, 256, 0, ctx->stream>>>(L, B, ctx->hub, hot_root);
+  PC_CHECK_LAUNCH();
+  k_compress_count<<<rows_grid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(L, n, B, hot_root,
+                                                                              ctr);
   PC_CHECK_LAUNCH();
   PC_CUDA(cudaEventRecord(ev[3], ctx->stream));
   // pool sizes -> host (one sync per build)
@@ -406,13 +545,22 @@ void pc_build(pacim_ctx *ctx) {
               CT_THREADS, 0, ctx->stream>>>(L, n, B, ctx->csize.as<uint32_t>(),
                                             ctx->coff.as<uint64_t>(), ctr);
   PC_CHECK_LAUNCH();
-  PC_CUDA(cudaEventRecord(ev[4], ctx->stream));
-  k_gain_scatter<<<rows_grid, 256, 0, ctx->stream>>>(
-      L, n, B, ctx->csize.as<uint32_t>(), ctx->coff.as<uint64_t>(), ctx->cfill.as<uint32_t>(),
-      ctx->perm.as<uint32_t>(), ctx->gain0.as<int64_t>(), 0);
+  k_hot_ci<<<(B + 255) / 256, 256, 0, ctx->stream>>>(L, B, hot_root, hot_ci);
   PC_CHECK_LAUNCH();
+  PC_CUDA(cudaEventRecord(ev[4], ctx->stream));
+  {
+    const uint32_t HW = (H + 31) / 32;
+    size_t smem = ((3 * H + GS_ROWS * HW + 1) & ~1u) * 4 + (size_t)H * 8;
+    PC_CUDA(cudaFuncSetAttribute(k_gain_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    k_gain_scatter<<<pc_grid(ctx, ((size_t)n + GS_ROWS - 1) / GS_ROWS * GS_THREADS, GS_THREADS, 8),
+                     GS_THREADS, smem, ctx->stream>>>(
+        L, n, B, ctx->csize.as<uint32_t>(), ctx->coff.as<uint64_t>(), ctx->cfill.as<uint32_t>(),
+        ctx->perm.as<uint32_t>(), ctx->gain0.as<int64_t>(), 0, hot_ci);
+    PC_CHECK_LAUNCH();
+  }
   PC_CUDA(cudaEventRecord(ev[5], ctx->stream));
-  ctx->launches += 5;
+  ctx->launches += 8;
   unsigned long long h[6];
   PC_CUDA(cudaMemcpyAsync(h, ctr, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                           ctx->stream));

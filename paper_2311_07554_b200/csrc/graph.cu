@@ -205,6 +205,39 @@ __global__ void k_wic(const uint64_t *keys, uint64_t m, const uint64_t *off, uin
 }
 }  // namespace
 
+// ------------------------------------------------------------------ hub
+namespace {
+// packed (degree << 32 | ~v) max: the largest degree, smallest id on ties
+__global__ void k_max_deg(const uint64_t *off, uint32_t n, unsigned long long *best) {
+  unsigned long long b = 0;
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (size_t)gridDim.x * blockDim.x) {
+    unsigned long long d = off[v + 1] - off[v];
+    unsigned long long key = (d << 32) | (0xFFFFFFFFull - v);
+    if (key > b) b = key;
+  }
+  for (int s = 16; s; s >>= 1) {
+    unsigned long long o = __shfl_xor_sync(0xffffffffu, b, s);
+    if (o > b) b = o;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(best, b);
+}
+}  // namespace
+
+static void find_hub(pacim_ctx *ctx) {
+  TmpBuf t(ctx);
+  pc_ensure(ctx, t, 8);
+  PC_CUDA(cudaMemsetAsync(t.p, 0, 8, ctx->stream));
+  k_max_deg<<<pc_grid(ctx, ctx->n, 256), 256, 0, ctx->stream>>>(ctx->off.as<uint64_t>(), ctx->n,
+                                                               t.as<unsigned long long>());
+  PC_CHECK_LAUNCH();
+  unsigned long long h = 0;
+  PC_CUDA(cudaMemcpyAsync(&h, t.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->hub = (uint32_t)(0xFFFFFFFFull - (h & 0xFFFFFFFFull));
+  if (ctx->hub >= ctx->n) ctx->hub = 0;
+}
+
 void pc_graph_finish_load(pacim_ctx *ctx, int validate) {
   const uint32_t n = ctx->n;
   uint64_t *off = ctx->off.as<uint64_t>();
@@ -247,6 +280,7 @@ void pc_graph_finish_load(pacim_ctx *ctx, int validate) {
     PC_CHECK_LAUNCH();
   }
   ctx->launches += 4;
+  find_hub(ctx);
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
@@ -582,6 +616,7 @@ void pc_generate(pacim_ctx *ctx, int kind, const uint64_t *params, int nparams,
     throw PacimError{PACIM_EINVAL, "unknown generator kind"};
   }
   csr_from_keys(ctx);
+  find_hub(ctx);
   if (ctx->pmodel == PACIM_P_WIC) {
     pc_ensure(ctx, ctx->tm1, std::max<size_t>(ctx->m, 1) * sizeof(uint32_t));
     k_wic<<<pc_grid(ctx, ctx->m, 256), 256, 0, ctx->stream>>>(

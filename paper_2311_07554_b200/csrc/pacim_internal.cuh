@@ -93,6 +93,8 @@ struct pacim_ctx {
   std::vector<uint32_t> shr;      // hr32 of slot j (sorted ascending)
   std::vector<uint16_t> tab;      // bucket table, (1<<PACIM_TB)+1 entries
   DevBuf d_shr, d_tab;
+  DevBuf d_hot;        // u32[2*B]: per slot the hub's root and its component id
+  uint32_t hub = 0;    // a maximum-degree vertex (most likely in the giant CC)
 
   // uncompressed store: L[v*B + j] (B = R_local)
   DevBuf L;
