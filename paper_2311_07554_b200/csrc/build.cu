@@ -52,36 +52,35 @@ __global__ void k_init(uint32_t *L, uint32_t n, uint32_t B) {
 }
 
 // ------------------------------------------------------------- union-find
-// Lock-free union-find with ids decreasing along parent pointers (a root is
-// only ever hooked under a SMALLER root), so every tree's root is the minimum
-// id of its CC (R8) and no cycle can form even with stale reads.  Path
-// halving uses plain stores: it only replaces a parent by an ancestor.
-__device__ __forceinline__ uint32_t uf_find(uint32_t *L, uint32_t B, uint32_t j, uint32_t x) {
-  for (;;) {
-    uint32_t p = ld_cg(L + (size_t)x * B + j);
-    if (p == x) return x;
-    uint32_t gp = ld_cg(L + (size_t)p * B + j);
-    if (gp == p) return p;
-    L[(size_t)x * B + j] = gp;
-    x = gp;
-  }
-}
-
+// Rem's union with splicing, lock-free (the UniteRemCAS variant of ConnectIt
+// the paper uses, P:8 / P:1328): walk both paths one step at a time from the
+// side with the larger parent; hook a root under the other side's parent, or
+// splice the non-root's pointer over to the other side's (smaller) parent.
+// Parents stay strictly smaller than children, so the final root of every
+// CC is its minimum id (R8).  Two independent loads per step; the walk stops
+// as soon as the two paths meet.
 __device__ __forceinline__ void uf_unite(uint32_t *L, uint32_t B, uint32_t j, uint32_t u,
                                          uint32_t v) {
+  uint32_t *Lj = L + j;
   for (;;) {
-    u = uf_find(L, B, j, u);
-    v = uf_find(L, B, j, v);
-    if (u == v) return;
-    if (u < v) {
+    uint32_t pu = ld_cg(Lj + (size_t)u * B);
+    uint32_t pv = ld_cg(Lj + (size_t)v * B);
+    if (pu == pv) return;
+    if (pu < pv) {
       uint32_t t = u;
       u = v;
       v = t;
+      t = pu;
+      pu = pv;
+      pv = t;
     }
-    // hook the larger root u under the smaller v
-    uint32_t old = atomicCAS(L + (size_t)u * B + j, u, v);
-    if (old == u) return;
-    u = old;  // u was hooked meanwhile: continue from its new parent
+    // now pu > pv
+    if (u == pu) {
+      if (atomicCAS(Lj + (size_t)u * B, u, pv) == u) return;  // hook root u under pv
+    } else {
+      atomicCAS(Lj + (size_t)u * B, pu, pv);  // splice (may lose a race harmlessly)
+      u = pu;
+    }
   }
 }
 
@@ -231,17 +230,26 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
   size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long ncc = 0, nnr = 0;
   for (size_t v = warp; v < n; v += nw) {
-    for (uint32_t j = lane; j < B; j += 32) {
-      uint32_t *slot = L + v * B + j;
-      uint32_t s = ld_cg(slot);
-      if (s == (uint32_t)v || (s & PACIM_HIGH)) continue;  // root (or singleton)
-      uint32_t root = find_ro(L, B, j, s);
-      if (root != s) *slot = root;
-      nnr++;
-      if (j < H && root == hroot[j]) {
-        atomicAdd(hcnt + j, 1u);
-      } else if (add_to_root(L, B, j, root, 1u)) {
-        ncc++;
+    for (uint32_t j0 = 0; j0 < B; j0 += 256) {
+      uint32_t sv[8];  // prefetch up to 8 slots per lane (independent loads)
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        uint32_t j = j0 + lane + 32 * i;
+        sv[i] = j < B ? ld_cg(L + v * B + j) : (uint32_t)v;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const uint32_t j = j0 + lane + 32 * i;
+        const uint32_t s = sv[i];
+        if (s == (uint32_t)v || (s & PACIM_HIGH)) continue;  // root (or singleton)
+        uint32_t root = find_ro(L, B, j, s);
+        if (root != s) L[v * B + j] = root;
+        nnr++;
+        if (j < H && root == hroot[j]) {
+          atomicAdd(hcnt + j, 1u);
+        } else if (add_to_root(L, B, j, root, 1u)) {
+          ncc++;
+        }
       }
     }
   }
