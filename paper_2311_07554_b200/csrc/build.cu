@@ -23,6 +23,7 @@
 //                     perm grouped by component (H6u); hot-component cursor
 //                     reservations aggregated per tile in shared memory
 #include <algorithm>
+#include <cstdlib>
 
 #include "pacim_internal.cuh"
 
@@ -195,14 +196,28 @@ __device__ __forceinline__ uint32_t find_ro(const uint32_t *L, uint32_t B, uint3
   }
 }
 
+// find with path halving for compress_count: every write is an atomicMin, so
+// a slot only ever moves towards its root (ids decrease along parent
+// pointers) and racing halvings can never undo an owner's full compression.
+__device__ __forceinline__ uint32_t find_halve(uint32_t *L, uint32_t B, uint32_t j, uint32_t x) {
+  for (;;) {
+    uint32_t p = ld_cg(L + (size_t)x * B + j);
+    if (p == x || (p & PACIM_HIGH)) return x;
+    uint32_t gp = ld_cg(L + (size_t)p * B + j);
+    if (gp == p || (gp & PACIM_HIGH)) return p;
+    atomicMin(L + (size_t)x * B + j, gp);
+    x = gp;
+  }
+}
+
 __global__ void k_hot_roots(const uint32_t *L, uint32_t B, uint32_t hub, uint32_t *hot) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < B; j += gridDim.x * blockDim.x)
     hot[j] = find_ro(L, B, j, hub);
 }
 
 // ------------------------------------------------------ k_compress_count
-// For every non-root (v, j): slot <- root (full compression, H4; only the
-// owner writes its slot, finds are read-only, so the result is final); the
+// For every non-root (v, j): slot <- root (full compression, H4; halving and
+// the owner's write are atomicMin, so the final slot is the root); the
 // root slot becomes HIGH | size by CAS(root -> HIGH|1) then atomicAdd per
 // member (H5).  Members of the slot's hot root are counted in shared memory
 // and added once per block.  ctr[0] += CCs of size >= 2, ctr[1] += non-roots.
@@ -242,8 +257,8 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
         const uint32_t j = j0 + lane + 32 * i;
         const uint32_t s = sv[i];
         if (s == (uint32_t)v || (s & PACIM_HIGH)) continue;  // root (or singleton)
-        uint32_t root = find_ro(L, B, j, s);
-        if (root != s) L[v * B + j] = root;
+        uint32_t root = find_halve(L, B, j, s);
+        if (root != s) atomicMin(L + v * B + j, root);
         nnr++;
         if (j < H && root == hroot[j]) {
           atomicAdd(hcnt + j, 1u);
@@ -317,8 +332,8 @@ __device__ __forceinline__ void block_scan2(unsigned long long a, unsigned long 
 }
 
 __global__ void __launch_bounds__(CT_THREADS) k_compact(uint32_t *L, uint32_t n, uint32_t B,
-                                                        uint32_t *csize, uint64_t *coff,
-                                                        unsigned long long *ctr) {
+                                                        uint32_t big_t, uint32_t *csize,
+                                                        uint64_t *coff, unsigned long long *ctr) {
   __shared__ unsigned long long base_c, base_m;
   const size_t per_tile = (size_t)CT_ROWS * B;
   const size_t ntiles = ((size_t)n + CT_ROWS - 1) / CT_ROWS;
@@ -326,11 +341,13 @@ __global__ void __launch_bounds__(CT_THREADS) k_compact(uint32_t *L, uint32_t n,
     const size_t e0 = t * per_tile;
     const size_t e1 = min(e0 + per_tile, (size_t)n * B);
     unsigned long long c = 0, msum = 0;
+#pragma unroll 8
     for (size_t e = e0 + threadIdx.x; e < e1; e += CT_THREADS) {
       uint32_t s = L[e];
       if (s & PACIM_HIGH) {
+        uint32_t sz = s & PACIM_LOW;
         c++;
-        msum += s & PACIM_LOW;
+        if (sz < big_t) msum += sz;
       }
     }
     unsigned long long ec, em, tc, tm;
@@ -341,106 +358,67 @@ __global__ void __launch_bounds__(CT_THREADS) k_compact(uint32_t *L, uint32_t n,
     }
     __syncthreads();
     unsigned long long ci = base_c + ec, mo = base_m + em;
+#pragma unroll 8
     for (size_t e = e0 + threadIdx.x; e < e1; e += CT_THREADS) {
       uint32_t s = L[e];
       if (s & PACIM_HIGH) {
         uint32_t sz = s & PACIM_LOW;
         csize[ci] = sz;
-        coff[ci] = mo;
+        if (sz < big_t) {
+          coff[ci] = mo;
+          mo += sz;
+        } else {
+          coff[ci] = PACIM_BIG;  // covered by a dense pass, not indexed
+        }
         L[e] = PACIM_HIGH | (uint32_t)ci;
         ci++;
-        mo += sz;
       }
     }
     __syncthreads();
   }
 }
 
-// hot component id per slot: the compacted id of the hub's root (or NONE)
-__global__ void k_hot_ci(const uint32_t *L, uint32_t B, const uint32_t *hot_root,
-                         uint32_t *hot_ci) {
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < B; j += gridDim.x * blockDim.x) {
-    uint32_t s = L[(size_t)hot_root[j] * B + j];
-    hot_ci[j] = (s & PACIM_HIGH) ? (s & PACIM_LOW) : NONE;
-  }
-}
-
 // --------------------------------------------------------- k_gain_scatter
-// Tiles of GS_ROWS rows; warp per row, lanes over slots.  gain0[v] (+)=
-// sum_j |C_j(v)| and v is written into its component's member range.
-// Members of the slot's hot component are counted per tile in shared memory
-// (bit flags remember which), one global cursor reservation per slot and
-// tile, then placed from shared-memory cursors.
-constexpr int GS_THREADS = 256;
-constexpr int GS_ROWS = 64;
-
-__global__ void __launch_bounds__(GS_THREADS) k_gain_scatter(
-    const uint32_t *__restrict__ L, uint32_t n, uint32_t B, const uint32_t *csize,
-    const uint64_t *coff, uint32_t *cfill, uint32_t *perm, int64_t *gain0, int accumulate,
-    const uint32_t *g_hot_ci) {
-  extern __shared__ uint32_t gsm[];
-  const uint32_t H = min(B, HOT_MAX);
-  const uint32_t HW = (H + 31) / 32;  // flag words per row
-  uint32_t *hci = gsm, *hcnt = gsm + H, *hcur = gsm + 2 * H;
-  uint32_t *flags = gsm + 3 * H;                                        // GS_ROWS * HW
-  unsigned long long *hbase = reinterpret_cast<unsigned long long *>(
-      gsm + ((3 * H + GS_ROWS * HW + 1) & ~1u));                        // H entries
-  for (uint32_t j = threadIdx.x; j < H; j += blockDim.x) {
-    hci[j] = g_hot_ci[j];
-    hcnt[j] = 0;
-  }
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const size_t ntiles = ((size_t)n + GS_ROWS - 1) / GS_ROWS;
-  for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    for (uint32_t i = threadIdx.x; i < GS_ROWS * HW; i += blockDim.x) flags[i] = 0;
-    __syncthreads();
-    // ---- pass 1
-    for (uint32_t r = wid; r < GS_ROWS; r += GS_THREADS / 32) {
-      const size_t v = t * GS_ROWS + r;
-      if (v >= n) break;
-      long long g = 0;
-      for (uint32_t j = lane; j < B; j += 32) {
-        uint32_t s = L[v * B + j];
+// Warp per vertex row, lanes over slots (8 slots prefetched per lane).
+// gain0[v] (+)= sum_j |C_j(v)| (H7); v is written into the member range of
+// each of its indexed (non-big) components (H6u).
+__global__ void __launch_bounds__(256) k_gain_scatter(const uint32_t *__restrict__ L, uint32_t n,
+                                                      uint32_t B, const uint32_t *csize,
+                                                      const uint64_t *coff, uint32_t *cfill,
+                                                      uint32_t *perm, int64_t *gain0,
+                                                      int accumulate) {
+  const int lane = threadIdx.x & 31;
+  size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t v = warp; v < n; v += nw) {
+    long long g = 0;
+    for (uint32_t j0 = 0; j0 < B; j0 += 256) {
+      uint32_t sv[8];
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        uint32_t j = j0 + lane + 32 * i;
+        sv[i] = j < B ? L[v * B + j] : NONE;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const uint32_t j = j0 + lane + 32 * i;
+        const uint32_t s = sv[i];
+        if (s == NONE) continue;
         if (s == (uint32_t)v) {
           g += 1;  // singleton CC
           continue;
         }
         uint32_t ci = (s & PACIM_HIGH) ? (s & PACIM_LOW) : (__ldg(L + (size_t)s * B + j) & PACIM_LOW);
         g += csize[ci];
-        if (j < H && ci == hci[j]) {
-          atomicAdd(hcnt + j, 1u);
-          atomicOr(flags + r * HW + (j >> 5), 1u << (j & 31));
-        } else {
+        const uint64_t off = coff[ci];
+        if (off != PACIM_BIG) {
           uint32_t pos = atomicAdd(cfill + ci, 1u);
-          perm[coff[ci] + pos] = (uint32_t)v;
-        }
-      }
-      for (int d = 16; d; d >>= 1) g += __shfl_xor_sync(0xffffffffu, g, d);
-      if (lane == 0) gain0[v] = accumulate ? gain0[v] + g : g;
-    }
-    __syncthreads();
-    // ---- one reservation per hot component and tile
-    for (uint32_t j = threadIdx.x; j < H; j += blockDim.x) {
-      uint32_t c = hcnt[j];
-      if (c) {
-        hbase[j] = coff[hci[j]] + atomicAdd(cfill + hci[j], c);
-        hcur[j] = 0;
-      }
-    }
-    __syncthreads();
-    // ---- pass 2: place the flagged hot members
-    for (uint32_t r = wid; r < GS_ROWS; r += GS_THREADS / 32) {
-      const size_t v = t * GS_ROWS + r;
-      if (v >= n) break;
-      for (uint32_t j = lane; j < H; j += 32) {
-        if (flags[r * HW + (j >> 5)] & (1u << (j & 31))) {
-          uint32_t pos = atomicAdd(hcur + j, 1u);
-          perm[hbase[j] + pos] = (uint32_t)v;
+          perm[off + pos] = (uint32_t)v;
         }
       }
     }
-    __syncthreads();
-    for (uint32_t j = threadIdx.x; j < H; j += blockDim.x) hcnt[j] = 0;
+    for (int d = 16; d; d >>= 1) g += __shfl_xor_sync(0xffffffffu, g, d);
+    if (lane == 0) gain0[v] = accumulate ? gain0[v] + g : g;
   }
 }
 
@@ -497,7 +475,7 @@ void pc_build(pacim_ctx *ctx) {
   unsigned long long *ctr = ctx->counters.as<unsigned long long>();
   PC_CUDA(cudaMemsetAsync(ctr, 0, 64 * sizeof(uint64_t), ctx->stream));
   uint32_t *L = ctx->L.as<uint32_t>();
-  uint32_t *hot_root = ctx->d_hot.as<uint32_t>(), *hot_ci = hot_root + B;
+  uint32_t *hot_root = ctx->d_hot.as<uint32_t>();
   const uint32_t H = std::min<uint32_t>(B, HOT_MAX);
 
   cudaEvent_t ev[6];
@@ -534,47 +512,46 @@ void pc_build(pacim_ctx *ctx) {
                                                                               ctr);
   PC_CHECK_LAUNCH();
   PC_CUDA(cudaEventRecord(ev[3], ctx->stream));
-  // pool sizes -> host (one sync per build)
+  // component count -> host (sync 1 of 2 per build)
   unsigned long long hc[2];
   PC_CUDA(cudaMemcpyAsync(hc, ctr, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                           ctx->stream));
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->ncomp = hc[0];
-  ctx->nmember = hc[0] + hc[1];
+  ctx->nnonsingle = hc[0] + hc[1];
   PC_REQUIRE(ctx->ncomp < (1ull << 31), PACIM_ENOTIMPL,
              "more than 2^31 non-singleton components in one store");
   pc_ensure(ctx, ctx->csize, std::max<size_t>(ctx->ncomp, 1) * 4);
   pc_ensure(ctx, ctx->csize_work, std::max<size_t>(ctx->ncomp, 1) * 4);
   pc_ensure(ctx, ctx->coff, std::max<size_t>(ctx->ncomp, 1) * 8);
   pc_ensure(ctx, ctx->cfill, std::max<size_t>(ctx->ncomp, 1) * 4);
-  pc_ensure(ctx, ctx->perm, std::max<size_t>(ctx->nmember, 1) * 4);
   PC_CUDA(cudaMemsetAsync(ctx->cfill.p, 0, std::max<size_t>(ctx->ncomp, 1) * 4, ctx->stream));
+  ctx->big_t = std::max<uint32_t>(PACIM_BIG_MIN, n / PACIM_BIG_DIV);
+  if (const char *e = getenv("PACIM_BIG_T")) ctx->big_t = (uint32_t)std::max(2L, atol(e));  // tests
   k_compact<<<pc_grid(ctx, ((size_t)n + CT_ROWS - 1) / CT_ROWS * CT_THREADS, CT_THREADS, 8),
-              CT_THREADS, 0, ctx->stream>>>(L, n, B, ctx->csize.as<uint32_t>(),
+              CT_THREADS, 0, ctx->stream>>>(L, n, B, ctx->big_t, ctx->csize.as<uint32_t>(),
                                             ctx->coff.as<uint64_t>(), ctr);
   PC_CHECK_LAUNCH();
-  k_hot_ci<<<(B + 255) / 256, 256, 0, ctx->stream>>>(L, B, hot_root, hot_ci);
-  PC_CHECK_LAUNCH();
   PC_CUDA(cudaEventRecord(ev[4], ctx->stream));
-  {
-    const uint32_t HW = (H + 31) / 32;
-    size_t smem = ((3 * H + GS_ROWS * HW + 1) & ~1u) * 4 + (size_t)H * 8;
-    PC_CUDA(cudaFuncSetAttribute(k_gain_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem));
-    k_gain_scatter<<<pc_grid(ctx, ((size_t)n + GS_ROWS - 1) / GS_ROWS * GS_THREADS, GS_THREADS, 8),
-                     GS_THREADS, smem, ctx->stream>>>(
-        L, n, B, ctx->csize.as<uint32_t>(), ctx->coff.as<uint64_t>(), ctx->cfill.as<uint32_t>(),
-        ctx->perm.as<uint32_t>(), ctx->gain0.as<int64_t>(), 0, hot_ci);
-    PC_CHECK_LAUNCH();
-  }
+  // indexed member count -> host (sync 2 of 2)
+  unsigned long long hm[4];
+  PC_CUDA(cudaMemcpyAsync(hm, ctr, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  PC_REQUIRE(hm[2] == ctx->ncomp, PACIM_ECHECK,
+             "compact: component total disagrees with compress_count");
+  ctx->nmember = hm[3];
+  pc_ensure(ctx, ctx->perm, std::max<size_t>(ctx->nmember, 1) * 4);
+  k_gain_scatter<<<rows_grid, 256, 0, ctx->stream>>>(
+      L, n, B, ctx->csize.as<uint32_t>(), ctx->coff.as<uint64_t>(), ctx->cfill.as<uint32_t>(),
+      ctx->perm.as<uint32_t>(), ctx->gain0.as<int64_t>(), 0);
+  PC_CHECK_LAUNCH();
   PC_CUDA(cudaEventRecord(ev[5], ctx->stream));
-  ctx->launches += 8;
+  ctx->launches += 6;
   unsigned long long h[6];
   PC_CUDA(cudaMemcpyAsync(h, ctr, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                           ctx->stream));
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
-  PC_REQUIRE(h[2] == ctx->ncomp && h[3] == ctx->nmember, PACIM_ECHECK,
-             "compact: component/member totals disagree with compress_count");
   ctx->stats.live_pairs = h[4];
   ctx->stats.t_init_ms = ev_ms(ev[0], ev[1]);
   ctx->stats.t_edges_ms = ev_ms(ev[1], ev[2]);

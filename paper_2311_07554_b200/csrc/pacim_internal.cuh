@@ -23,6 +23,12 @@
 #define PACIM_HIGH 0x80000000u
 #define PACIM_LOW 0x7FFFFFFFu
 #define PACIM_TB 12  // bits of the sketch bucket table (R2 candidate enumeration)
+// Components of at least max(PACIM_BIG_MIN, n / PACIM_BIG_DIV) vertices are
+// not put in the member index; MarkSeed covers them with one dense pass over
+// the store (coff = PACIM_BIG marks them).
+#define PACIM_BIG_MIN 4096u
+#define PACIM_BIG_DIV 256u
+#define PACIM_BIG 0xFFFFFFFFFFFFFFFFull
 
 // ------------------------------------------------------------------ hash (R1)
 __host__ __device__ __forceinline__ uint64_t pc_mix64(uint64_t z) {
@@ -98,7 +104,8 @@ struct pacim_ctx {
 
   // uncompressed store: L[v*B + j] (B = R_local)
   DevBuf L;
-  uint64_t ncomp = 0, nmember = 0;
+  uint64_t ncomp = 0, nmember = 0, nnonsingle = 0;
+  uint32_t big_t = 0;
   DevBuf csize;       // u32[ncomp] pristine CC sizes
   DevBuf csize_work;  // u32[ncomp] sizes zeroed on cover (MarkSeed)
   DevBuf coff;        // u64[ncomp] member-index offsets

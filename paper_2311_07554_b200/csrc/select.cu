@@ -4,10 +4,15 @@
 //   A  argmax over v of (gain desc, id asc); seeds hold gain -1 (R5, R6)
 //   B  MarkSeed: per sketch slot j, the seed's component
 //      c = comp(s, j); delta_j = size_work[c]; size_work[c] <- 0      (H9)
-//   C  incremental gain update: every member u != s of each newly covered
-//      component loses delta_j (H10); gain[s] <- -1
+//   C  incremental gain update (H10): every member u != s of each newly
+//      covered component loses delta_j — indexed components through the
+//      member index, big components (coff = PACIM_BIG) through one dense
+//      pass over the store comparing slots with the covered root;
+//      gain[s] <- -1
 // separated by grid-wide barriers.  gain_num[i] = sum_j delta_j is checked
 // against the argmax gain (the two must agree exactly).
+// The multi-rank primitives (pacim_cover_local / pacim_argmax_device) reuse
+// the same device phases as ordinary launches.
 #include <cooperative_groups.h>
 
 #include "pacim_internal.cuh"
@@ -17,6 +22,7 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr int SEL_THREADS = 512;
+constexpr uint32_t NONE = 0xFFFFFFFFu;
 
 struct Best {
   long long g;
@@ -55,16 +61,131 @@ __device__ Best block_best(Best b, Best *sh) {
   return sh[32];
 }
 
-struct SelParams {
+// Per-step cover state (device, B entries each).
+struct CoverState {
   const uint32_t *L;
   uint32_t n, B;
   const uint64_t *coff;
   const uint32_t *perm;
-  uint32_t *csw;          // working sizes (zeroed on cover)
+  uint32_t *csw;       // working sizes, zeroed on cover
+  uint64_t *list_off;  // indexed member range of slot j's covered CC
+  uint32_t *list_len;  // its length (0: none)
+  uint32_t *cov_root;  // root of slot j's covered big CC, or NONE
+  uint32_t *cov_delta; // its size
+  int *dense;          // set when some big CC was covered this step
+};
+
+// Phase B for slot j: returns delta_j.
+__device__ __forceinline__ uint32_t cover_slot(const CoverState &C, uint32_t s, uint32_t j) {
+  const uint32_t sl = __ldcg(C.L + (size_t)s * C.B + j);
+  uint32_t delta = 1, len = 0, croot = NONE;
+  uint64_t off = 0;
+  if (sl != s) {
+    const uint32_t root = (sl & PACIM_HIGH) ? s : sl;
+    const uint32_t ci = (sl & PACIM_HIGH) ? (sl & PACIM_LOW)
+                                          : (__ldcg(C.L + (size_t)root * C.B + j) & PACIM_LOW);
+    delta = __ldcg(C.csw + ci);
+    if (delta) {
+      C.csw[ci] = 0;
+      off = C.coff[ci];
+      if (off == PACIM_BIG) {
+        croot = root;
+        *C.dense = 1;
+      } else {
+        len = delta;
+      }
+    }
+  }  // else: singleton {s}, covered now, no other member
+  C.list_len[j] = len;
+  C.list_off[j] = off;
+  C.cov_root[j] = croot;
+  C.cov_delta[j] = delta;
+  return delta;
+}
+
+// Phase C1: target[u] -= delta_j for the members u != s of the indexed CCs,
+// threads [tid, +nth) over the concatenated ranges; pre[] is per-block smem.
+__device__ unsigned long long apply_members(const CoverState &C, uint32_t s, long long *target,
+                                            uint32_t *pre, size_t tid, size_t nth) {
+  unsigned long long upd = 0;
+  for (uint32_t j0 = 0; j0 < C.B; j0 += 1024) {
+    const uint32_t cnt = min(1024u, C.B - j0);
+    __syncthreads();
+    if (threadIdx.x < 32) {  // warp-parallel exclusive prefix over cnt slots
+      uint32_t carry = 0;
+      for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
+        uint32_t q = q0 + threadIdx.x;
+        uint32_t x = q < cnt ? __ldcg(C.list_len + j0 + q) : 0, inc = x;
+        for (int d = 1; d < 32; d <<= 1) {
+          uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
+          if ((int)threadIdx.x >= d) inc += y;
+        }
+        if (q < cnt) pre[q] = carry + inc - x;
+        carry += __shfl_sync(0xffffffffu, inc, 31);
+      }
+      if (threadIdx.x == 0) pre[cnt] = carry;
+    }
+    __syncthreads();
+    const uint32_t W = pre[cnt];
+    for (size_t idx = tid; idx < W; idx += nth) {
+      uint32_t lo = 0, hi = cnt;  // slot q with pre[q] <= idx < pre[q+1]
+      while (hi - lo > 1) {
+        uint32_t mid = (lo + hi) >> 1;
+        if (pre[mid] <= idx) lo = mid; else hi = mid;
+      }
+      const uint32_t u = C.perm[__ldcg(C.list_off + j0 + lo) + (idx - pre[lo])];
+      if (u != s) {
+        atomicAdd((unsigned long long *)&target[u],
+                  (unsigned long long)(-(long long)__ldcg(C.list_len + j0 + lo)));
+        upd++;
+      }
+    }
+  }
+  return upd;
+}
+
+// Phase C2: dense pass over the store for the covered big CCs: v is a member
+// of slot j's covered CC iff its slot holds that root, or v is the root.
+// Each lane keeps the covered roots of its 8 slots of a 256-slot chunk in
+// registers and streams the rows.
+__device__ unsigned long long apply_dense(const CoverState &C, uint32_t s, long long *target,
+                                          size_t warp0, size_t nwarps) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long upd = 0;
+  for (uint32_t j0 = 0; j0 < C.B; j0 += 256) {
+    uint32_t cr[8], cd[8];
+    bool any = false;
+#pragma unroll
+    for (int i = 0; i < 8; i++) {
+      const uint32_t j = j0 + lane + 32 * i;
+      cr[i] = j < C.B ? __ldcg(C.cov_root + j) : NONE;
+      cd[i] = j < C.B ? __ldcg(C.cov_delta + j) : 0;
+      any |= cr[i] != NONE;
+    }
+    if (!__any_sync(0xffffffffu, any)) continue;
+    for (size_t v = warp0; v < C.n; v += nwarps) {
+      uint32_t x[8];
+#pragma unroll
+      for (int i = 0; i < 8; i++)
+        x[i] = cr[i] != NONE ? __ldcs(C.L + v * C.B + j0 + lane + 32 * i) : NONE;
+      long long d = 0;
+#pragma unroll
+      for (int i = 0; i < 8; i++)
+        if (cr[i] != NONE && (x[i] == cr[i] || (uint32_t)v == cr[i])) d += cd[i];
+      for (int q = 16; q; q >>= 1) d += __shfl_xor_sync(0xffffffffu, d, q);
+      if (lane == 0 && d && (uint32_t)v != s) {
+        atomicAdd((unsigned long long *)&target[v], (unsigned long long)(-d));
+        upd++;
+      }
+    }
+  }
+  return upd;
+}
+
+struct SelParams {
+  CoverState C;
   long long *gain;        // working gains
   Best *partial;          // gridDim entries
-  uint64_t *list_off;     // B entries
-  uint32_t *list_len;     // B entries
   uint32_t k;
   uint32_t *seeds;
   long long *gain_num;    // k, zeroed
@@ -80,12 +201,13 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(SelParams P) {
   __shared__ Best chosen;
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t nth = (size_t)gridDim.x * blockDim.x;
+  const CoverState &C = P.C;
   unsigned long long upd = 0;
   for (uint32_t step = 0; step < P.k; step++) {
     // ---- A: argmax (gain desc, id asc)
     Best b{LLONG_MIN, 0xFFFFFFFFu};
-    for (size_t v = tid; v < P.n; v += nth) {
-      long long g = P.gain[v];
+    for (size_t v = tid; v < C.n; v += nth) {
+      long long g = __ldcg(P.gain + v);
       if (better(g, (uint32_t)v, b.g, b.v)) {
         b.g = g;
         b.v = (uint32_t)v;
@@ -93,10 +215,13 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(SelParams P) {
     }
     b = block_best(b, sh);
     if (threadIdx.x == 0) P.partial[blockIdx.x] = b;
+    if (tid == 0) *C.dense = 0;
     grid.sync();
     Best c{LLONG_MIN, 0xFFFFFFFFu};
     for (uint32_t i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
-      Best x = P.partial[i];
+      Best x;
+      x.g = __ldcg(&P.partial[i].g);
+      x.v = __ldcg(&P.partial[i].v);
       if (better(x.g, x.v, c.g, c.v)) c = x;
     }
     c = block_best(c, sh);
@@ -104,62 +229,18 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(SelParams P) {
     __syncthreads();
     const uint32_t s = chosen.v;
     // ---- B: MarkSeed on every slot
-    for (size_t j = tid; j < P.B; j += nth) {
-      uint32_t sl = P.L[(size_t)s * P.B + j];
-      uint32_t delta, len = 0;
-      uint64_t off = 0;
-      if (sl == s) {
-        delta = 1;  // singleton {s}: covered now, no other member
-      } else {
-        uint32_t ci = (sl & PACIM_HIGH) ? (sl & PACIM_LOW)
-                                        : (P.L[(size_t)sl * P.B + j] & PACIM_LOW);
-        delta = P.csw[ci];
-        if (delta) {
-          P.csw[ci] = 0;
-          len = delta;
-          off = P.coff[ci];
-        }
-      }
-      P.list_len[j] = len;
-      P.list_off[j] = off;
+    for (size_t j = tid; j < C.B; j += nth) {
+      uint32_t delta = cover_slot(C, s, (uint32_t)j);
       atomicAdd((unsigned long long *)&P.gain_num[step], (unsigned long long)delta);
     }
     grid.sync();
-    // ---- C: gain updates over the concatenated member ranges
-    // per block: exclusive prefix of list_len in chunks of 1024 slots
-    for (uint32_t j0 = 0; j0 < P.B; j0 += 1024) {
-      const uint32_t cnt = min(1024u, P.B - j0);
-      if (threadIdx.x == 0) {
-        uint32_t run = 0;
-        for (uint32_t q = 0; q < cnt; q++) {
-          pre[q] = run;
-          run += P.list_len[j0 + q];
-        }
-        pre[cnt] = run;
-      }
-      __syncthreads();
-      const uint32_t W = pre[cnt];
-      for (size_t idx = tid; idx < W; idx += nth) {
-        // slot q with pre[q] <= idx < pre[q+1]
-        uint32_t lo = 0, hi = cnt;
-        while (hi - lo > 1) {
-          uint32_t mid = (lo + hi) >> 1;
-          if (pre[mid] <= idx) lo = mid; else hi = mid;
-        }
-        const uint32_t q = lo;
-        const uint32_t u = P.perm[P.list_off[j0 + q] + (idx - pre[q])];
-        if (u != s) {
-          atomicAdd((unsigned long long *)&P.gain[u],
-                    (unsigned long long)(-(long long)P.list_len[j0 + q]));
-          upd++;
-        }
-      }
-      __syncthreads();
-    }
+    // ---- C: gain updates
+    upd += apply_members(C, s, P.gain, pre, tid, nth);
+    if (__ldcg(C.dense)) upd += apply_dense(C, s, P.gain, tid >> 5, nth >> 5);
     if (tid == 0) {
       P.seeds[step] = s;
       P.arg_gain[step] = chosen.g;
-      if (P.gain_num[step] != chosen.g) *P.flag = 1;
+      if (__ldcg(P.gain_num + step) != chosen.g) *P.flag = 1;
       P.gain[s] = -1;
     }
     grid.sync();
@@ -168,7 +249,25 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(SelParams P) {
   if ((threadIdx.x & 31) == 0 && upd) atomicAdd(P.updates, upd);
 }
 
-// standalone argmax for the multi-rank loop
+// ------------------------------------------------ multi-rank step kernels
+__global__ void k_cover_slots(CoverState C, uint32_t s, unsigned long long *sum) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < C.B; j += gridDim.x * blockDim.x)
+    atomicAdd(sum, (unsigned long long)cover_slot(C, s, j));
+}
+
+__global__ void __launch_bounds__(SEL_THREADS) k_apply_members(CoverState C, uint32_t s,
+                                                               long long *target) {
+  __shared__ uint32_t pre[1025];
+  apply_members(C, s, target, pre, (size_t)blockIdx.x * blockDim.x + threadIdx.x,
+                (size_t)gridDim.x * blockDim.x);
+}
+
+__global__ void __launch_bounds__(256) k_apply_dense(CoverState C, uint32_t s, long long *target) {
+  if (!__ldcg(C.dense)) return;
+  apply_dense(C, s, target, ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5,
+              ((size_t)gridDim.x * blockDim.x) >> 5);
+}
+
 __global__ void __launch_bounds__(SEL_THREADS) k_argmax_part(const long long *gain, uint32_t n,
                                                              Best *partial) {
   __shared__ Best sh[33];
@@ -197,38 +296,25 @@ __global__ void __launch_bounds__(SEL_THREADS) k_argmax_final(const Best *partia
   if (threadIdx.x == 0) *out = c;
 }
 
-// MarkSeed on this rank's slots, member deltas accumulated into delta[]
-__global__ void k_cover_local(const uint32_t *L, uint32_t B, uint32_t s, uint32_t *csw,
-                              const uint64_t *coff, const uint32_t *perm, long long *delta,
-                              unsigned long long *sum) {
-  // one block per slot j
-  for (uint32_t j = blockIdx.x; j < B; j += gridDim.x) {
-    uint32_t sl = L[(size_t)s * B + j];
-    uint32_t d;
-    uint64_t off = 0;
-    bool members = false;
-    if (sl == s) {
-      d = 1;
-    } else {
-      uint32_t ci = (sl & PACIM_HIGH) ? (sl & PACIM_LOW) : (L[(size_t)sl * B + j] & PACIM_LOW);
-      d = csw[ci];
-      off = coff[ci];
-      members = d > 0;
-    }
-    __syncthreads();
-    if (members && threadIdx.x == 0) {
-      uint32_t ci = (sl & PACIM_HIGH) ? (sl & PACIM_LOW) : (L[(size_t)sl * B + j] & PACIM_LOW);
-      csw[ci] = 0;
-    }
-    if (threadIdx.x == 0) atomicAdd(sum, (unsigned long long)d);
-    if (members)
-      for (uint32_t i = threadIdx.x; i < d; i += blockDim.x)
-        atomicAdd((unsigned long long *)&delta[perm[off + i]], (unsigned long long)(-(long long)d));
-    __syncthreads();
-  }
-}
-
 }  // namespace
+
+static CoverState make_cover_state(pacim_ctx *ctx) {
+  const uint32_t B = ctx->R_local;
+  pc_ensure(ctx, ctx->sel_list, (size_t)B * 20 + 64);
+  CoverState C;
+  C.L = ctx->L.as<uint32_t>();
+  C.n = ctx->n;
+  C.B = B;
+  C.coff = ctx->coff.as<uint64_t>();
+  C.perm = ctx->perm.as<uint32_t>();
+  C.csw = ctx->csize_work.as<uint32_t>();
+  C.list_off = ctx->sel_list.as<uint64_t>();
+  C.list_len = reinterpret_cast<uint32_t *>(C.list_off + B);
+  C.cov_root = C.list_len + B;
+  C.cov_delta = C.cov_root + B;
+  C.dense = reinterpret_cast<int *>(C.cov_delta + B);
+  return C;
+}
 
 void pc_select_reset(pacim_ctx *ctx) {
   PC_CUDA(cudaMemcpyAsync(ctx->csize_work.p, ctx->csize.p, std::max<size_t>(ctx->ncomp, 1) * 4,
@@ -238,17 +324,18 @@ void pc_select_reset(pacim_ctx *ctx) {
 
 void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
                int64_t *sigma_num) {
-  const uint32_t n = ctx->n, B = ctx->R_local;
+  const uint32_t n = ctx->n;
   int occ = 0;
   PC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_select, SEL_THREADS, 0));
   PC_REQUIRE(occ >= 1, PACIM_ECUDA, "k_select cannot be resident");
   unsigned grid = (unsigned)ctx->sm_count * (unsigned)std::min(occ, 2);
   pc_ensure(ctx, ctx->gain, (size_t)n * 8);
   pc_ensure(ctx, ctx->sel_partial, (size_t)grid * sizeof(Best));
-  pc_ensure(ctx, ctx->sel_list, (size_t)B * 12 + 16);
   pc_ensure(ctx, ctx->sel_seeds, (size_t)k * 4);
   pc_ensure(ctx, ctx->sel_gain, (size_t)k * 16 + 64);
   pc_ensure(ctx, ctx->sel_flag, 64);
+  SelParams P;
+  P.C = make_cover_state(ctx);
   cudaEvent_t e0, e1;
   PC_CUDA(cudaEventCreate(&e0));
   PC_CUDA(cudaEventCreate(&e1));
@@ -259,17 +346,8 @@ void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
                           cudaMemcpyDeviceToDevice, ctx->stream));
   PC_CUDA(cudaMemsetAsync(ctx->sel_gain.p, 0, (size_t)k * 16 + 64, ctx->stream));
   PC_CUDA(cudaMemsetAsync(ctx->sel_flag.p, 0, 64, ctx->stream));
-  SelParams P;
-  P.L = ctx->L.as<uint32_t>();
-  P.n = n;
-  P.B = B;
-  P.coff = ctx->coff.as<uint64_t>();
-  P.perm = ctx->perm.as<uint32_t>();
-  P.csw = ctx->csize_work.as<uint32_t>();
   P.gain = ctx->gain.as<long long>();
   P.partial = ctx->sel_partial.as<Best>();
-  P.list_off = ctx->sel_list.as<uint64_t>();
-  P.list_len = reinterpret_cast<uint32_t *>(P.list_off + B);
   P.k = k;
   P.seeds = ctx->sel_seeds.as<uint32_t>();
   P.gain_num = ctx->sel_gain.as<long long>();
@@ -303,14 +381,19 @@ void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
 }
 
 void pc_cover_local(pacim_ctx *ctx, uint32_t s, int64_t *d_delta, int64_t *local_gain) {
+  CoverState C = make_cover_state(ctx);
   pc_ensure(ctx, ctx->sel_flag, 64);
   unsigned long long *sum = ctx->sel_flag.as<unsigned long long>();
   PC_CUDA(cudaMemsetAsync(sum, 0, 8, ctx->stream));
-  unsigned g = std::min<unsigned>(ctx->R_local, (unsigned)ctx->sm_count * 8);
-  k_cover_local<<<g, 256, 0, ctx->stream>>>(ctx->L.as<uint32_t>(), ctx->R_local, s,
-                                           ctx->csize_work.as<uint32_t>(),
-                                           ctx->coff.as<uint64_t>(), ctx->perm.as<uint32_t>(),
-                                           reinterpret_cast<long long *>(d_delta), sum);
+  PC_CUDA(cudaMemsetAsync(C.dense, 0, 4, ctx->stream));
+  const uint32_t B = ctx->R_local;
+  k_cover_slots<<<(B + 255) / 256, 256, 0, ctx->stream>>>(C, s, sum);
+  PC_CHECK_LAUNCH();
+  long long *t = reinterpret_cast<long long *>(d_delta);
+  k_apply_members<<<pc_grid(ctx, (size_t)1 << 22, SEL_THREADS, 2), SEL_THREADS, 0, ctx->stream>>>(
+      C, s, t);
+  PC_CHECK_LAUNCH();
+  k_apply_dense<<<pc_grid(ctx, (size_t)ctx->n * 32, 256, 8), 256, 0, ctx->stream>>>(C, s, t);
   PC_CHECK_LAUNCH();
   unsigned long long h = 0;
   PC_CUDA(cudaMemcpyAsync(&h, sum, 8, cudaMemcpyDeviceToHost, ctx->stream));

@@ -83,6 +83,15 @@ def test_tiny_corpus_parity(orc, ctx, i):
     full_parity(orc, ctx, g, model, t32, R, 1000 + i, min(k, g.n))
 
 
+@pytest.mark.parametrize("i", [0, 2, 3, 5, 7, 9])
+def test_dense_cover_path(orc, ctx, i, monkeypatch):
+    """Force components of >= 8 vertices out of the member index so MarkSeed
+    covers them with the dense pass over the store (the path big components
+    take at full scale)."""
+    monkeypatch.setenv("PACIM_BIG_T", "8")
+    test_tiny_corpus_parity(orc, ctx, i)
+
+
 def test_edge_cases(orc, ctx, pc):
     from oracle.oracle import Graph
     # single vertex, no edges, k = n = 1
@@ -189,11 +198,13 @@ def test_config_golden(ctx, name):
 
 
 # ------------------------------------------------ multi-rank primitives
-def test_rank_emulation_matches_single(orc, pc):
+@pytest.mark.parametrize("big_t", [None, "6"])
+def test_rank_emulation_matches_single(orc, pc, big_t, monkeypatch):
     """Sketch sharding r = rank mod P with the per-step primitives, ranks run
     one after another on one GPU (no waiting kernels), the collective replaced
     by a host sum: identical to the single-ctx greedy."""
-    import torch
+    if big_t:
+        monkeypatch.setenv("PACIM_BIG_T", big_t)
     from oracle.oracle import Graph
     from paper_2311_07554_b200 import dist
     off, nbr = inputs.random_powerlaw_graph(3000, 15000, 21)
