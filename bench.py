@@ -102,15 +102,15 @@ class ClockSampler:
 # ------------------------------------------------------------ roofline model
 def kernel_bytes(st: dict, cfg: dict, k: int) -> dict:
     """Algorithmic bytes per launch of each kernel."""
-    n, m, B = st["n"], st["m"], st["R_local"]
-    L = 4 * n * B
+    n, m, B, rows = st["n"], st["m"], st["R_local"], st["rows"]
+    L = 4 * rows * B                      # the store: one u32 slot per (row, sketch)
     wic = 4 * m if cfg["pmodel"] == 1 else 0
-    nonroot = st["nmember"] - st["ncomp"]
+    nonroot = st["nnonsingle"] - st["ncomp"]
     return {
         "k_init": L,                                        # write every slot
-        "k_edges": 8 * m + wic + 8 * st["live_pairs"],      # keys (+T32) + 2 slot reads per live pair
+        "k_edges": 16 * m + wic + 8 * st["live_pairs"],     # key + row pair (+T32), 2 slot reads per live pair
         "k_compress_count": L + 8 * nonroot,                # read slots; write root + count per non-root
-        "k_compact": L + 16 * st["ncomp"],                  # read slots; csize+coff per CC
+        "k_compact": L + 12 * st["ncomp"],                  # read slots; csize+coff per CC
         "k_gain_scatter": L + 8 * n + 4 * st["nmember"] + 4 * nonroot,  # slots, gain0, perm, root slots
         "k_select": k * 8 * n + 8 * st["select_member_updates"],  # argmax scans + member updates
     }
@@ -118,10 +118,10 @@ def kernel_bytes(st: dict, cfg: dict, k: int) -> dict:
 
 def build_bytes(st: dict, cfg: dict) -> int:
     """CSR_upper * ceil(R_g/B) + 16 n R_g (one pass, B = R_g)."""
-    csr_upper = 8 * st["m"]  # sorted u64 key list = the upper edge list read by k_edges
+    csr_upper = 16 * st["m"]  # u64 hash key + u64 row pair per upper edge read by k_edges
     if cfg["pmodel"] == 1:
         csr_upper += 4 * st["m"]
-    return csr_upper + 16 * st["n"] * st["R_local"]
+    return csr_upper + 16 * st["rows"] * st["R_local"]
 
 
 def load_peaks():
@@ -318,7 +318,7 @@ def main():
                 "kernel_ms": {kk: round(v, 4) for kk, v in dur.items()},
                 "build": {"bytes": bb, "ms": round(avg["t_build_ms"], 4),
                           "achieved": round(build_gbs, 1), "frac": round(build_gbs / hbm, 4),
-                          "model": "SURVEY 8(d): CSR_upper*ceil(R_g/B) + 16*n*R_g, B=R_g"}}
+                          "model": "SURVEY 8(d): CSR_upper*ceil(R_g/B) + 16*rows*R_g, B=R_g (rows = non-isolated vertices)"}}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -336,8 +336,8 @@ def main():
         "gpu_launches": launches,
         "roofline": roofline,
         "clocks": clk,
-        "stats": {kk: st[kk] for kk in ("ncomp", "nmember", "live_pairs", "device_bytes",
-                                        "select_member_updates")},
+        "stats": {kk: st[kk] for kk in ("rows", "ncomp", "nmember", "nnonsingle", "live_pairs",
+                                        "device_bytes", "select_member_updates")},
         "seeds_head": [int(x) for x in out[0][:8]],
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

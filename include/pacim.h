@@ -78,6 +78,9 @@ typedef struct {
     uint64_t select_bfs_visits;     /* Get-center / cover BFS vertex visits (compressed) */
     uint32_t kernel_launches_build; /* launches of library kernels in the last build */
     uint32_t kernel_launches_select;/* launches of library kernels in the last select */
+    uint32_t rows;                  /* store rows = non-isolated vertices (isolated
+                                       vertices are singletons in every sketch) */
+    uint64_t nnonsingle;            /* (vertex, sketch) pairs in non-singleton CCs */
 } pacim_stats;
 
 /* --------------------------------------------------------------- lifecycle */

@@ -42,7 +42,7 @@ class Stats(C.Structure):
         ("t_centers_ms", C.c_double), ("t_select_ms", C.c_double),
         ("device_bytes", C.c_uint64), ("select_member_updates", C.c_uint64),
         ("select_bfs_visits", C.c_uint64), ("kernel_launches_build", C.c_uint32),
-        ("kernel_launches_select", C.c_uint32),
+        ("kernel_launches_select", C.c_uint32), ("rows", C.c_uint32), ("nnonsingle", C.c_uint64),
     ]
 
     def asdict(self):

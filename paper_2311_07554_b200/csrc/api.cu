@@ -68,7 +68,7 @@ static void drop_graph(pacim_ctx *ctx) {
 }
 
 static void free_all(pacim_ctx *ctx) {
-  DevBuf *bufs[] = {&ctx->off,   &ctx->nbr,        &ctx->keys,     &ctx->tm1,      &ctx->L,
+  DevBuf *bufs[] = {&ctx->off,   &ctx->nbr,        &ctx->keys,     &ctx->tm1, &ctx->ckeys, &ctx->cid, &ctx->rmap,      &ctx->L,
                     &ctx->csize, &ctx->csize_work, &ctx->coff,     &ctx->cfill,    &ctx->perm,
                     &ctx->clabel, &ctx->csz,       &ctx->csz_work, &ctx->Ltmp,     &ctx->d_shr,
                     &ctx->d_hot,
@@ -343,6 +343,8 @@ int pacim_get_stats(pacim_ctx *ctx, pacim_stats *out) {
     s.compressed = ctx->compressed ? 1 : 0;
     s.ncomp = ctx->ncomp;
     s.nmember = ctx->nmember;
+    s.rows = ctx->nr;
+    s.nnonsingle = ctx->nnonsingle;
     s.device_bytes = ctx->device_bytes;
     *out = s;
   });

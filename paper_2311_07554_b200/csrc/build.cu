@@ -96,6 +96,7 @@ constexpr int EDGE_WARPS = EDGE_THREADS / 32;
 
 template <bool WIC>
 __global__ void __launch_bounds__(EDGE_THREADS) k_edges(const uint64_t *__restrict__ keys,
+                                                        const uint64_t *__restrict__ ckeys,
                                                         const uint32_t *__restrict__ tm1,
                                                         uint64_t m, uint64_t K, uint64_t t32,
                                                         const uint32_t *__restrict__ g_shr,
@@ -140,8 +141,9 @@ __global__ void __launch_bounds__(EDGE_THREADS) k_edges(const uint64_t *__restri
         }
       }
       cnt = hi - lo;
-      w_u[wid][lane] = (uint32_t)(key >> 32);
-      w_v[wid][lane] = (uint32_t)key;
+      const uint64_t ck = ckeys[e];  // the endpoints' store rows
+      w_u[wid][lane] = (uint32_t)(ck >> 32);
+      w_v[wid][lane] = (uint32_t)ck;
       w_he[wid][lane] = he;
       w_T[wid][lane] = T;
       w_lo[wid][lane] = lo;
@@ -210,9 +212,10 @@ __device__ __forceinline__ uint32_t find_halve(uint32_t *L, uint32_t B, uint32_t
   }
 }
 
-__global__ void k_hot_roots(const uint32_t *L, uint32_t B, uint32_t hub, uint32_t *hot) {
+__global__ void k_hot_roots(const uint32_t *L, uint32_t nr, uint32_t B, uint32_t hub,
+                            uint32_t *hot) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < B; j += gridDim.x * blockDim.x)
-    hot[j] = find_ro(L, B, j, hub);
+    hot[j] = hub < nr ? find_ro(L, B, j, hub) : NONE;
 }
 
 // ------------------------------------------------------ k_compress_count
@@ -257,7 +260,9 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
         const uint32_t j = j0 + lane + 32 * i;
         const uint32_t s = sv[i];
         if (s == (uint32_t)v || (s & PACIM_HIGH)) continue;  // root (or singleton)
-        uint32_t root = find_halve(L, B, j, s);
+        // parent already the hot root: no walk (the common case for members
+        // of the giant CC)
+        uint32_t root = (j < H && s == hroot[j]) ? s : find_halve(L, B, j, s);
         if (root != s) atomicMin(L + v * B + j, root);
         nnr++;
         if (j < H && root == hroot[j]) {
@@ -386,7 +391,7 @@ __global__ void __launch_bounds__(256) k_gain_scatter(const uint32_t *__restrict
                                                       uint32_t B, const uint32_t *csize,
                                                       const uint64_t *coff, uint32_t *cfill,
                                                       uint32_t *perm, int64_t *gain0,
-                                                      int accumulate) {
+                                                      const uint32_t *rmap, int accumulate) {
   const int lane = threadIdx.x & 31;
   size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
@@ -413,13 +418,23 @@ __global__ void __launch_bounds__(256) k_gain_scatter(const uint32_t *__restrict
         const uint64_t off = coff[ci];
         if (off != PACIM_BIG) {
           uint32_t pos = atomicAdd(cfill + ci, 1u);
-          perm[off + pos] = (uint32_t)v;
+          perm[off + pos] = rmap[v];
         }
       }
     }
     for (int d = 16; d; d >>= 1) g += __shfl_xor_sync(0xffffffffu, g, d);
-    if (lane == 0) gain0[v] = accumulate ? gain0[v] + g : g;
+    if (lane == 0) {
+      const uint32_t vid = rmap[v];
+      gain0[vid] = accumulate ? gain0[vid] + g : g;
+    }
   }
+}
+
+// isolated vertices are singletons in every sketch: gain0 = B
+__global__ void k_fill_i64(int64_t *a, uint32_t n, int64_t x) {
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (size_t)gridDim.x * blockDim.x)
+    a[v] = x;
 }
 
 }  // namespace
@@ -432,7 +447,7 @@ static float ev_ms(cudaEvent_t a, cudaEvent_t b) {
 }
 
 void pc_build(pacim_ctx *ctx) {
-  const uint32_t n = ctx->n, B = ctx->R_local;
+  const uint32_t n = ctx->nr, B = ctx->R_local;  // store rows = non-isolated vertices
   PC_REQUIRE(B >= 1 && B <= 65535, PACIM_EINVAL, "local sketch count must be in [1, 65535]");
   PC_REQUIRE(!ctx->compressed, PACIM_ENOTIMPL, "compressed store not built by pc_build");
   // ---- slot table (host): local sketches sorted by hi32(hash(r)) (R2)
@@ -470,7 +485,7 @@ void pc_build(pacim_ctx *ctx) {
 
   // ---- buffers
   pc_ensure(ctx, ctx->L, (size_t)n * B * sizeof(uint32_t));
-  pc_ensure(ctx, ctx->gain0, (size_t)n * sizeof(int64_t));
+  pc_ensure(ctx, ctx->gain0, (size_t)ctx->n * sizeof(int64_t));
   pc_ensure(ctx, ctx->counters, 64 * sizeof(uint64_t));
   unsigned long long *ctr = ctx->counters.as<unsigned long long>();
   PC_CUDA(cudaMemsetAsync(ctr, 0, 64 * sizeof(uint64_t), ctx->stream));
@@ -494,19 +509,21 @@ void pc_build(pacim_ctx *ctx) {
       PC_CUDA(cudaFuncSetAttribute(k_edges<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
       k_edges<true><<<g, EDGE_THREADS, smem, ctx->stream>>>(
-          ctx->keys.as<uint64_t>(), ctx->tm1.as<uint32_t>(), ctx->m, ctx->K, 0,
+          ctx->keys.as<uint64_t>(), ctx->ckeys.as<uint64_t>(), ctx->tm1.as<uint32_t>(), ctx->m,
+          ctx->K, 0,
           ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, L, ctr + 4);
     } else {
       PC_CUDA(cudaFuncSetAttribute(k_edges<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
       k_edges<false><<<g, EDGE_THREADS, smem, ctx->stream>>>(
-          ctx->keys.as<uint64_t>(), nullptr, ctx->m, ctx->K, ctx->t32, ctx->d_shr.as<uint32_t>(),
+          ctx->keys.as<uint64_t>(), ctx->ckeys.as<uint64_t>(), nullptr, ctx->m, ctx->K, ctx->t32,
+          ctx->d_shr.as<uint32_t>(),
           ctx->d_tab.as<uint16_t>(), B, L, ctr + 4);
     }
     PC_CHECK_LAUNCH();
   }
   PC_CUDA(cudaEventRecord(ev[2], ctx->stream));
-  k_hot_roots<<<(B + 255) / 256, 256, 0, ctx->stream>>>(L, B, ctx->hub, hot_root);
+  k_hot_roots<<<(B + 255) / 256, 256, 0, ctx->stream>>>(L, n, B, ctx->hub_row, hot_root);
   PC_CHECK_LAUNCH();
   k_compress_count<<<rows_grid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(L, n, B, hot_root,
                                                                               ctr);
@@ -542,9 +559,12 @@ void pc_build(pacim_ctx *ctx) {
              "compact: component total disagrees with compress_count");
   ctx->nmember = hm[3];
   pc_ensure(ctx, ctx->perm, std::max<size_t>(ctx->nmember, 1) * 4);
+  k_fill_i64<<<pc_grid(ctx, ctx->n, 256), 256, 0, ctx->stream>>>(ctx->gain0.as<int64_t>(), ctx->n,
+                                                                (int64_t)B);
+  PC_CHECK_LAUNCH();
   k_gain_scatter<<<rows_grid, 256, 0, ctx->stream>>>(
       L, n, B, ctx->csize.as<uint32_t>(), ctx->coff.as<uint64_t>(), ctx->cfill.as<uint32_t>(),
-      ctx->perm.as<uint32_t>(), ctx->gain0.as<int64_t>(), 0);
+      ctx->perm.as<uint32_t>(), ctx->gain0.as<int64_t>(), ctx->rmap.as<uint32_t>(), 0);
   PC_CHECK_LAUNCH();
   PC_CUDA(cudaEventRecord(ev[5], ctx->stream));
   ctx->launches += 6;
@@ -567,11 +587,17 @@ void pc_build(pacim_ctx *ctx) {
 // canonical labels of one slot: slot value is v (singleton), HIGH|ci (root:
 // label v) or the root id (R8: min id of the CC)
 namespace {
-__global__ void k_labels(const uint32_t *L, uint32_t n, uint32_t B, uint32_t j, uint32_t *out) {
+__global__ void k_labels(const uint32_t *L, uint32_t n, uint32_t B, uint32_t j,
+                         const uint32_t *cid, const uint32_t *rmap, uint32_t *out) {
   for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (size_t)gridDim.x * blockDim.x) {
-    uint32_t s = L[v * B + j];
-    out[v] = (s == (uint32_t)v || (s & PACIM_HIGH)) ? (uint32_t)v : s;
+    const uint32_t c = cid[v];
+    if (c == 0xFFFFFFFFu) {  // isolated vertex: singleton
+      out[v] = (uint32_t)v;
+      continue;
+    }
+    uint32_t s = L[(size_t)c * B + j];
+    out[v] = (s == c || (s & PACIM_HIGH)) ? (uint32_t)v : rmap[s];
   }
 }
 }  // namespace
@@ -580,7 +606,10 @@ void pc_get_labels(pacim_ctx *ctx, uint32_t slot, uint32_t *host_out) {
   TmpBuf t(ctx);
   pc_ensure(ctx, t, (size_t)ctx->n * 4);
   k_labels<<<pc_grid(ctx, ctx->n, 256), 256, 0, ctx->stream>>>(ctx->L.as<uint32_t>(), ctx->n,
-                                                              ctx->R_local, slot, t.as<uint32_t>());
+                                                              ctx->R_local, slot,
+                                                              ctx->cid.as<uint32_t>(),
+                                                              ctx->rmap.as<uint32_t>(),
+                                                              t.as<uint32_t>());
   PC_CHECK_LAUNCH();
   PC_CUDA(cudaMemcpyAsync(host_out, t.p, (size_t)ctx->n * 4, cudaMemcpyDeviceToHost, ctx->stream));
   PC_CUDA(cudaStreamSynchronize(ctx->stream));

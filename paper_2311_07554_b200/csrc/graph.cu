@@ -224,18 +224,92 @@ __global__ void k_max_deg(const uint64_t *off, uint32_t n, unsigned long long *b
 }
 }  // namespace
 
-static void find_hub(pacim_ctx *ctx) {
-  TmpBuf t(ctx);
-  pc_ensure(ctx, t, 8);
-  PC_CUDA(cudaMemsetAsync(t.p, 0, 8, ctx->stream));
-  k_max_deg<<<pc_grid(ctx, ctx->n, 256), 256, 0, ctx->stream>>>(ctx->off.as<uint64_t>(), ctx->n,
-                                                               t.as<unsigned long long>());
+namespace {
+__global__ void k_nonisolated(const uint64_t *off, uint32_t n, uint64_t *flag) {
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (size_t)gridDim.x * blockDim.x)
+    flag[v] = off[v + 1] > off[v] ? 1 : 0;
+}
+
+__global__ void k_rowmap(const uint64_t *flag, const uint64_t *pos, uint32_t n, uint32_t *cid,
+                         uint32_t *rmap) {
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (size_t)gridDim.x * blockDim.x) {
+    if (flag[v]) {
+      cid[v] = (uint32_t)pos[v];
+      rmap[pos[v]] = (uint32_t)v;
+    } else {
+      cid[v] = 0xFFFFFFFFu;
+    }
+  }
+}
+
+__global__ void k_ckeys(const uint64_t *keys, uint64_t m, const uint32_t *cid, uint64_t *ckeys) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (size_t)gridDim.x * blockDim.x) {
+    uint64_t k = keys[e];
+    ckeys[e] = ((uint64_t)cid[k >> 32] << 32) | cid[k & 0xFFFFFFFFull];
+  }
+}
+}  // namespace
+
+// Everything derived from (off, nbr, keys): hub vertex, the store's row map
+// (isolated vertices are singletons in every sketch and get no row; rows keep
+// the vertex order, so min row = min id), compact edge endpoints, WIC T32.
+static void derive_common(pacim_ctx *ctx) {
+  const uint32_t n = ctx->n;
+  const uint64_t m = ctx->m;
+  uint64_t *off = ctx->off.as<uint64_t>();
+  {
+    pc_ensure(ctx, ctx->counters, 64 * 8);
+    unsigned long long *t = ctx->counters.as<unsigned long long>();
+    PC_CUDA(cudaMemsetAsync(t, 0, 8, ctx->stream));
+    k_max_deg<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(off, n, t);
+    PC_CHECK_LAUNCH();
+    unsigned long long h = 0;
+    PC_CUDA(cudaMemcpyAsync(&h, t, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->hub = (uint32_t)(0xFFFFFFFFull - (h & 0xFFFFFFFFull));
+    if (ctx->hub >= n) ctx->hub = 0;
+  }
+  {
+    // persistent scratch (capacity reused across loads: no cudaMalloc/cudaFree)
+    pc_ensure(ctx, ctx->scratch, 2 * ((size_t)n + 1) * 8);
+    DevBuf flag, pos;
+    flag.p = ctx->scratch.p;
+    pos.p = ctx->scratch.as<uint64_t>() + n + 1;
+
+    k_nonisolated<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(off, n, flag.as<uint64_t>());
+    PC_CHECK_LAUNCH();
+    PC_CUDA(cudaMemsetAsync(flag.as<uint64_t>() + n, 0, 8, ctx->stream));
+    pc_exclusive_scan_u64(ctx, flag.as<uint64_t>(), pos.as<uint64_t>(), (size_t)n + 1);
+    uint64_t nr = 0;
+    PC_CUDA(cudaMemcpyAsync(&nr, pos.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->nr = (uint32_t)nr;
+    pc_ensure(ctx, ctx->cid, (size_t)n * 4);
+    pc_ensure(ctx, ctx->rmap, std::max<size_t>(nr, 1) * 4);
+    k_rowmap<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(flag.as<uint64_t>(), pos.as<uint64_t>(),
+                                                           n, ctx->cid.as<uint32_t>(),
+                                                           ctx->rmap.as<uint32_t>());
+    PC_CHECK_LAUNCH();
+    PC_CUDA(cudaMemcpyAsync(&ctx->hub_row, ctx->cid.as<uint32_t>() + ctx->hub, 4,
+                            cudaMemcpyDeviceToHost, ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  pc_ensure(ctx, ctx->ckeys, std::max<size_t>(m, 1) * 8);
+  k_ckeys<<<pc_grid(ctx, m, 256), 256, 0, ctx->stream>>>(ctx->keys.as<uint64_t>(), m,
+                                                        ctx->cid.as<uint32_t>(),
+                                                        ctx->ckeys.as<uint64_t>());
   PC_CHECK_LAUNCH();
-  unsigned long long h = 0;
-  PC_CUDA(cudaMemcpyAsync(&h, t.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  if (ctx->pmodel == PACIM_P_WIC) {
+    pc_ensure(ctx, ctx->tm1, std::max<size_t>(m, 1) * sizeof(uint32_t));
+    k_wic<<<pc_grid(ctx, m, 256), 256, 0, ctx->stream>>>(ctx->keys.as<uint64_t>(), m, off,
+                                                        ctx->tm1.as<uint32_t>());
+    PC_CHECK_LAUNCH();
+  }
+  ctx->launches += 5;
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
-  ctx->hub = (uint32_t)(0xFFFFFFFFull - (h & 0xFFFFFFFFull));
-  if (ctx->hub >= ctx->n) ctx->hub = 0;
 }
 
 void pc_graph_finish_load(pacim_ctx *ctx, int validate) {
@@ -273,15 +347,8 @@ void pc_graph_finish_load(pacim_ctx *ctx, int validate) {
   k_upper_fill<<<pc_grid(ctx, (size_t)n * 32, 256), 256, 0, ctx->stream>>>(
       off, nbr, n, ustart, ucnt, ctx->keys.as<uint64_t>());
   PC_CHECK_LAUNCH();
-  if (ctx->pmodel == PACIM_P_WIC) {
-    pc_ensure(ctx, ctx->tm1, std::max<size_t>(ctx->m, 1) * sizeof(uint32_t));
-    k_wic<<<pc_grid(ctx, ctx->m, 256), 256, 0, ctx->stream>>>(ctx->keys.as<uint64_t>(), ctx->m,
-                                                             off, ctx->tm1.as<uint32_t>());
-    PC_CHECK_LAUNCH();
-  }
-  ctx->launches += 4;
-  find_hub(ctx);
-  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->launches += 3;
+  derive_common(ctx);
 }
 
 // ------------------------------------------------------------- generators
@@ -616,12 +683,5 @@ void pc_generate(pacim_ctx *ctx, int kind, const uint64_t *params, int nparams,
     throw PacimError{PACIM_EINVAL, "unknown generator kind"};
   }
   csr_from_keys(ctx);
-  find_hub(ctx);
-  if (ctx->pmodel == PACIM_P_WIC) {
-    pc_ensure(ctx, ctx->tm1, std::max<size_t>(ctx->m, 1) * sizeof(uint32_t));
-    k_wic<<<pc_grid(ctx, ctx->m, 256), 256, 0, ctx->stream>>>(
-        ctx->keys.as<uint64_t>(), ctx->m, ctx->off.as<uint64_t>(), ctx->tm1.as<uint32_t>());
-    PC_CHECK_LAUNCH();
-  }
-  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  derive_common(ctx);
 }

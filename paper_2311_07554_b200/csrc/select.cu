@@ -15,6 +15,8 @@
 // the same device phases as ordinary launches.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "pacim_internal.cuh"
 
 namespace cg = cooperative_groups;
@@ -63,8 +65,10 @@ __device__ Best block_best(Best b, Best *sh) {
 
 // Per-step cover state (device, B entries each).
 struct CoverState {
-  const uint32_t *L;
-  uint32_t n, B;
+  const uint32_t *L;      // store rows (non-isolated vertices) x B slots
+  uint32_t n, B;          // n = store rows
+  const uint32_t *cid;    // vertex -> row (0xFFFFFFFF: isolated)
+  const uint32_t *rmap;   // row -> vertex
   const uint64_t *coff;
   const uint32_t *perm;
   uint32_t *csw;       // working sizes, zeroed on cover
@@ -77,11 +81,12 @@ struct CoverState {
 
 // Phase B for slot j: returns delta_j.
 __device__ __forceinline__ uint32_t cover_slot(const CoverState &C, uint32_t s, uint32_t j) {
-  const uint32_t sl = __ldcg(C.L + (size_t)s * C.B + j);
+  const uint32_t cs = C.cid[s];  // the seed's row
+  const uint32_t sl = cs == NONE ? NONE : __ldcg(C.L + (size_t)cs * C.B + j);
   uint32_t delta = 1, len = 0, croot = NONE;
   uint64_t off = 0;
-  if (sl != s) {
-    const uint32_t root = (sl & PACIM_HIGH) ? s : sl;
+  if (cs != NONE && sl != cs) {
+    const uint32_t root = (sl & PACIM_HIGH) ? cs : sl;
     const uint32_t ci = (sl & PACIM_HIGH) ? (sl & PACIM_LOW)
                                           : (__ldcg(C.L + (size_t)root * C.B + j) & PACIM_LOW);
     delta = __ldcg(C.csw + ci);
@@ -105,6 +110,9 @@ __device__ __forceinline__ uint32_t cover_slot(const CoverState &C, uint32_t s, 
 
 // Phase C1: target[u] -= delta_j for the members u != s of the indexed CCs,
 // threads [tid, +nth) over the concatenated ranges; pre[] is per-block smem.
+// The list arrays may live in global memory (written by an earlier launch or
+// before a grid barrier) or in shared memory (plain loads either way).
+
 __device__ unsigned long long apply_members(const CoverState &C, uint32_t s, long long *target,
                                             uint32_t *pre, size_t tid, size_t nth) {
   unsigned long long upd = 0;
@@ -115,7 +123,7 @@ __device__ unsigned long long apply_members(const CoverState &C, uint32_t s, lon
       uint32_t carry = 0;
       for (uint32_t q0 = 0; q0 < cnt; q0 += 32) {
         uint32_t q = q0 + threadIdx.x;
-        uint32_t x = q < cnt ? __ldcg(C.list_len + j0 + q) : 0, inc = x;
+        uint32_t x = q < cnt ? C.list_len[j0 + q] : 0, inc = x;
         for (int d = 1; d < 32; d <<= 1) {
           uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
           if ((int)threadIdx.x >= d) inc += y;
@@ -133,10 +141,10 @@ __device__ unsigned long long apply_members(const CoverState &C, uint32_t s, lon
         uint32_t mid = (lo + hi) >> 1;
         if (pre[mid] <= idx) lo = mid; else hi = mid;
       }
-      const uint32_t u = C.perm[__ldcg(C.list_off + j0 + lo) + (idx - pre[lo])];
+      const uint32_t u = C.perm[C.list_off[j0 + lo] + (idx - pre[lo])];
       if (u != s) {
         atomicAdd((unsigned long long *)&target[u],
-                  (unsigned long long)(-(long long)__ldcg(C.list_len + j0 + lo)));
+                  (unsigned long long)(-(long long)C.list_len[j0 + lo]));
         upd++;
       }
     }
@@ -158,8 +166,8 @@ __device__ unsigned long long apply_dense(const CoverState &C, uint32_t s, long 
 #pragma unroll
     for (int i = 0; i < 8; i++) {
       const uint32_t j = j0 + lane + 32 * i;
-      cr[i] = j < C.B ? __ldcg(C.cov_root + j) : NONE;
-      cd[i] = j < C.B ? __ldcg(C.cov_delta + j) : 0;
+      cr[i] = j < C.B ? C.cov_root[j] : NONE;
+      cd[i] = j < C.B ? C.cov_delta[j] : 0;
       any |= cr[i] != NONE;
     }
     if (!__any_sync(0xffffffffu, any)) continue;
@@ -173,9 +181,12 @@ __device__ unsigned long long apply_dense(const CoverState &C, uint32_t s, long 
       for (int i = 0; i < 8; i++)
         if (cr[i] != NONE && (x[i] == cr[i] || (uint32_t)v == cr[i])) d += cd[i];
       for (int q = 16; q; q >>= 1) d += __shfl_xor_sync(0xffffffffu, d, q);
-      if (lane == 0 && d && (uint32_t)v != s) {
-        atomicAdd((unsigned long long *)&target[v], (unsigned long long)(-d));
-        upd++;
+      if (lane == 0 && d) {
+        const uint32_t vid = C.rmap[v];
+        if (vid != s) {
+          atomicAdd((unsigned long long *)&target[vid], (unsigned long long)(-d));
+          upd++;
+        }
       }
     }
   }
@@ -184,6 +195,7 @@ __device__ unsigned long long apply_dense(const CoverState &C, uint32_t s, long 
 
 struct SelParams {
   CoverState C;
+  uint32_t nv;            // vertices (gain vector length)
   long long *gain;        // working gains
   Best *partial;          // gridDim entries
   uint32_t k;
@@ -206,7 +218,7 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(SelParams P) {
   for (uint32_t step = 0; step < P.k; step++) {
     // ---- A: argmax (gain desc, id asc)
     Best b{LLONG_MIN, 0xFFFFFFFFu};
-    for (size_t v = tid; v < C.n; v += nth) {
+    for (size_t v = tid; v < P.nv; v += nth) {
       long long g = __ldcg(P.gain + v);
       if (better(g, (uint32_t)v, b.g, b.v)) {
         b.g = g;
@@ -241,6 +253,129 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(SelParams P) {
       P.seeds[step] = s;
       P.arg_gain[step] = chosen.g;
       if (__ldcg(P.gain_num + step) != chosen.g) *P.flag = 1;
+      P.gain[s] = -1;
+    }
+    grid.sync();
+  }
+  for (int d = 16; d; d >>= 1) upd += __shfl_xor_sync(0xffffffffu, upd, d);
+  if ((threadIdx.x & 31) == 0 && upd) atomicAdd(P.updates, upd);
+}
+
+// Two barriers per step (B <= SEL_FUSED_B): every block redundantly computes
+// the seed's per-slot cover list (B cheap lookups) into shared memory, so the
+// MarkSeed phase needs no barrier of its own.  The zeroing of the covered
+// sizes is deferred to block 0 in the next step's argmax phase, i.e. after
+// every block has read them (the cover of step i reads sizes as of step i-1).
+constexpr uint32_t SEL_FUSED_B = 1024;
+
+struct Sel2Params {
+  CoverState C;           // list arrays unused (kept in shared memory)
+  uint32_t nv;
+  long long *gain;
+  Best *partial;
+  uint32_t *pending_ci;   // B: component covered in slot j by the previous step, or NONE
+  uint32_t k;
+  uint32_t *seeds;
+  long long *gain_num;
+  long long *arg_gain;
+  int *flag;
+  unsigned long long *updates;
+};
+
+__global__ void __launch_bounds__(SEL_THREADS) k_select2(Sel2Params P) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ uint64_t s2[];
+  const uint32_t B = P.C.B;
+  uint64_t *l_off = s2;                                          // B
+  uint32_t *l_len = reinterpret_cast<uint32_t *>(l_off + B);     // B
+  uint32_t *c_root = l_len + B;                                  // B
+  uint32_t *c_delta = c_root + B;                                // B
+  uint32_t *pre = c_delta + B;                                   // 1025
+  __shared__ Best sh[33];
+  __shared__ Best chosen;
+  __shared__ int dense;
+  __shared__ unsigned long long dsum;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t nth = (size_t)gridDim.x * blockDim.x;
+  CoverState C = P.C;
+  C.list_off = l_off;
+  C.list_len = l_len;
+  C.cov_root = c_root;
+  C.cov_delta = c_delta;
+  unsigned long long upd = 0;
+  for (uint32_t step = 0; step < P.k; step++) {
+    // ---- A: argmax partials; block 0 applies the previous step's zeroing
+    Best b{LLONG_MIN, 0xFFFFFFFFu};
+    for (size_t v = tid; v < P.nv; v += nth) {
+      long long g = __ldcg(P.gain + v);
+      if (better(g, (uint32_t)v, b.g, b.v)) {
+        b.g = g;
+        b.v = (uint32_t)v;
+      }
+    }
+    b = block_best(b, sh);
+    if (threadIdx.x == 0) P.partial[blockIdx.x] = b;
+    if (blockIdx.x == 0)
+      for (uint32_t j = threadIdx.x; j < B; j += blockDim.x) {
+        const uint32_t ci = P.pending_ci[j];
+        if (ci != NONE) C.csw[ci] = 0;
+      }
+    grid.sync();
+    // ---- every block: s, and the cover list of all slots
+    Best c{LLONG_MIN, 0xFFFFFFFFu};
+    for (uint32_t i = threadIdx.x; i < gridDim.x; i += blockDim.x) {
+      Best x;
+      x.g = __ldcg(&P.partial[i].g);
+      x.v = __ldcg(&P.partial[i].v);
+      if (better(x.g, x.v, c.g, c.v)) c = x;
+    }
+    c = block_best(c, sh);
+    if (threadIdx.x == 0) {
+      chosen = c;
+      dense = 0;
+      dsum = 0;
+    }
+    __syncthreads();
+    const uint32_t s = chosen.v;
+    const uint32_t cs = C.cid[s];
+    unsigned long long mysum = 0;
+    for (uint32_t j = threadIdx.x; j < B; j += blockDim.x) {
+      uint32_t delta = 1, len = 0, croot = NONE, ci = NONE;
+      uint64_t off = 0;
+      const uint32_t sl = cs == NONE ? NONE : __ldcg(C.L + (size_t)cs * B + j);
+      if (cs != NONE && sl != cs) {
+        const uint32_t root = (sl & PACIM_HIGH) ? cs : sl;
+        ci = (sl & PACIM_HIGH) ? (sl & PACIM_LOW) : (__ldcg(C.L + (size_t)root * B + j) & PACIM_LOW);
+        delta = __ldcg(C.csw + ci);
+        if (delta) {
+          off = C.coff[ci];
+          if (off == PACIM_BIG) {
+            croot = root;
+            dense = 1;
+          } else {
+            len = delta;
+          }
+        } else {
+          ci = NONE;  // already covered: nothing to zero
+        }
+      }
+      l_off[j] = off;
+      l_len[j] = len;
+      c_root[j] = croot;
+      c_delta[j] = delta;
+      mysum += delta;
+      if (blockIdx.x == 0) P.pending_ci[j] = ci;
+    }
+    for (int d = 16; d; d >>= 1) mysum += __shfl_xor_sync(0xffffffffu, mysum, d);
+    if ((threadIdx.x & 31) == 0 && mysum) atomicAdd(&dsum, mysum);
+    // ---- C: gain updates (apply_members starts with a block barrier)
+    upd += apply_members(C, s, P.gain, pre, tid, nth);
+    if (dense) upd += apply_dense(C, s, P.gain, tid >> 5, nth >> 5);
+    if (tid == 0) {
+      P.seeds[step] = s;
+      P.arg_gain[step] = chosen.g;
+      P.gain_num[step] = (long long)dsum;
+      if ((long long)dsum != chosen.g) *P.flag = 1;
       P.gain[s] = -1;
     }
     grid.sync();
@@ -303,7 +438,9 @@ static CoverState make_cover_state(pacim_ctx *ctx) {
   pc_ensure(ctx, ctx->sel_list, (size_t)B * 20 + 64);
   CoverState C;
   C.L = ctx->L.as<uint32_t>();
-  C.n = ctx->n;
+  C.n = ctx->nr;
+  C.cid = ctx->cid.as<uint32_t>();
+  C.rmap = ctx->rmap.as<uint32_t>();
   C.B = B;
   C.coff = ctx->coff.as<uint64_t>();
   C.perm = ctx->perm.as<uint32_t>();
@@ -336,6 +473,7 @@ void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
   pc_ensure(ctx, ctx->sel_flag, 64);
   SelParams P;
   P.C = make_cover_state(ctx);
+  P.nv = n;
   cudaEvent_t e0, e1;
   PC_CUDA(cudaEventCreate(&e0));
   PC_CUDA(cudaEventCreate(&e1));
@@ -354,8 +492,38 @@ void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
   P.arg_gain = P.gain_num + k;
   P.flag = ctx->sel_flag.as<int>();
   P.updates = reinterpret_cast<unsigned long long *>(P.gain_num + 2 * k);
-  void *args[] = {&P};
-  PC_CUDA(cudaLaunchCooperativeKernel((void *)k_select, grid, SEL_THREADS, args, 0, ctx->stream));
+  const uint32_t B = ctx->R_local;
+  if (B <= SEL_FUSED_B && !getenv("PACIM_SELECT_3SYNC")) {
+    // two grid barriers per step (the cover list is computed in every block)
+    const size_t smem = (size_t)B * 20 + 1025 * 4;
+    PC_CUDA(cudaFuncSetAttribute(k_select2, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem));
+    int occ2 = 0;
+    PC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, k_select2, SEL_THREADS, smem));
+    PC_REQUIRE(occ2 >= 1, PACIM_ECUDA, "k_select2 cannot be resident");
+    const unsigned grid2 = (unsigned)ctx->sm_count * (unsigned)std::min(occ2, 2);
+    pc_ensure(ctx, ctx->sel_partial, (size_t)grid2 * sizeof(Best) + (size_t)B * 4);
+    Sel2Params Q;
+    Q.C = P.C;
+    Q.nv = n;
+    Q.gain = P.gain;
+    Q.partial = ctx->sel_partial.as<Best>();
+    Q.pending_ci = reinterpret_cast<uint32_t *>(Q.partial + grid2);
+    PC_CUDA(cudaMemsetAsync(Q.pending_ci, 0xFF, (size_t)B * 4, ctx->stream));
+    Q.k = k;
+    Q.seeds = P.seeds;
+    Q.gain_num = P.gain_num;
+    Q.arg_gain = P.arg_gain;
+    Q.flag = P.flag;
+    Q.updates = P.updates;
+    void *args2[] = {&Q};
+    PC_CUDA(cudaLaunchCooperativeKernel((void *)k_select2, grid2, SEL_THREADS, args2, smem,
+                                        ctx->stream));
+  } else {
+    void *args[] = {&P};
+    PC_CUDA(cudaLaunchCooperativeKernel((void *)k_select, grid, SEL_THREADS, args, 0, ctx->stream));
+  }
+
   PC_CUDA(cudaEventRecord(e1, ctx->stream));
   std::vector<long long> hg(2 * k + 1);
   int flag = 0;
@@ -403,8 +571,9 @@ void pc_cover_local(pacim_ctx *ctx, uint32_t s, int64_t *d_delta, int64_t *local
 
 void pc_argmax(pacim_ctx *ctx, const int64_t *d_gain, uint32_t n, uint32_t *s, int64_t *g) {
   unsigned grid = pc_grid(ctx, n, SEL_THREADS, 2);
-  TmpBuf part(ctx);
+  DevBuf &part = ctx->sel_partial;  // persistent: no allocation per step
   pc_ensure(ctx, part, (size_t)(grid + 1) * sizeof(Best));
+
   k_argmax_part<<<grid, SEL_THREADS, 0, ctx->stream>>>(reinterpret_cast<const long long *>(d_gain),
                                                        n, part.as<Best>());
   PC_CHECK_LAUNCH();
