@@ -193,6 +193,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2")
     ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--alpha", type=float, default=None,
+                    help="override the config's alpha (< 1: compressed store)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-sketches", type=int, default=2)
@@ -200,7 +202,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     cfg = inputs.config(args.config)
+    if args.alpha is not None:
+        cfg["alpha"] = args.alpha
     if args.impl == "reference":
+
         run_reference(args, cfg)
         return
     k = args.k or cfg["k"]

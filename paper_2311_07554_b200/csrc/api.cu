@@ -71,7 +71,8 @@ static void free_all(pacim_ctx *ctx) {
   DevBuf *bufs[] = {&ctx->off,   &ctx->nbr,        &ctx->keys,     &ctx->tm1, &ctx->ckeys, &ctx->cid, &ctx->rmap,      &ctx->L,
                     &ctx->csize, &ctx->csize_work, &ctx->coff,     &ctx->cfill,    &ctx->perm,
                     &ctx->clabel, &ctx->csz,       &ctx->csz_work, &ctx->Ltmp,     &ctx->d_shr,
-                    &ctx->d_hot,
+                    &ctx->d_hot, &ctx->centers, &ctx->is_seed, &ctx->cwork,
+
                     &ctx->d_tab, &ctx->gain0,      &ctx->gain,     &ctx->center_of, &ctx->counters,
                     &ctx->scratch, &ctx->scratch2, &ctx->sel_seeds, &ctx->sel_gain,
                     &ctx->sel_partial, &ctx->sel_list, &ctx->sel_flag};
@@ -247,8 +248,10 @@ int pacim_build_sketches(pacim_ctx *ctx, uint32_t R, uint64_t hash_seed, uint64_
     ctx->K = pc_mix64(hash_seed);  // R2
     ctx->a32 = center_a32;
     ctx->compressed = center_a32 < (1ull << 32);
-    PC_REQUIRE(!ctx->compressed, PACIM_ENOTIMPL, "compressed store: not in this build");
-    pc_build(ctx);
+    if (ctx->compressed)
+      pc_build_compressed(ctx);
+    else
+      pc_build(ctx);
     ctx->built = true;
   });
 }
@@ -261,7 +264,10 @@ int pacim_select_seeds(pacim_ctx *ctx, uint32_t k, uint32_t *seeds_out, int64_t 
                "sharded build: use the multi-rank step primitives (dist.py)");
     PC_REQUIRE(k >= 1 && k <= ctx->n, PACIM_EINVAL, "k must be in [1, n]");
     PC_REQUIRE(seeds_out && gain_num_out && sigma_num_out, PACIM_EINVAL, "NULL output");
-    pc_select(ctx, k, seeds_out, gain_num_out, sigma_num_out);
+    if (ctx->compressed)
+      pc_select_compressed(ctx, k, seeds_out, gain_num_out, sigma_num_out);
+    else
+      pc_select(ctx, k, seeds_out, gain_num_out, sigma_num_out);
     if (sigma_out)
       for (uint32_t i = 0; i < k; i++) sigma_out[i] = (double)sigma_num_out[i] / (double)ctx->R;
   });
@@ -280,7 +286,10 @@ int pacim_gain0_to_device(pacim_ctx *ctx, int64_t *d_out) {
 int pacim_select_reset(pacim_ctx *ctx) {
   return guarded(ctx, [&] {
     PC_REQUIRE(ctx->built, PACIM_ESTATE, "no sketches");
-    pc_select_reset(ctx);
+    if (ctx->compressed)
+      pc_select_reset_compressed(ctx);
+    else
+      pc_select_reset(ctx);
   });
 }
 
@@ -288,7 +297,12 @@ int pacim_cover_local(pacim_ctx *ctx, uint32_t s, int64_t *d_delta, int64_t *loc
   return guarded(ctx, [&] {
     PC_REQUIRE(ctx->built, PACIM_ESTATE, "no sketches");
     PC_REQUIRE(s < ctx->n && d_delta && local_gain, PACIM_EINVAL, "bad argument");
-    pc_cover_local(ctx, s, d_delta, local_gain);
+    if (ctx->compressed) {
+      pc_cover_compressed(ctx, s, d_delta, local_gain);
+      PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    } else {
+      pc_cover_local(ctx, s, d_delta, local_gain);
+    }
   });
 }
 
@@ -327,7 +341,9 @@ int pacim_get_center_sketch(pacim_ctx *ctx, uint32_t r, uint32_t *label_out, uin
     (void)r;
     (void)label_out;
     (void)size_out;
-    throw PacimError{PACIM_ENOTIMPL, "compressed store: not in this build"};
+    PC_REQUIRE(label_out && size_out && r < ctx->R && ctx->r_slot[r] >= 0, PACIM_EINVAL,
+               "sketch r is not held by this ctx");
+    pc_get_center_sketch(ctx, (uint32_t)ctx->r_slot[r], label_out, size_out);
   });
 }
 

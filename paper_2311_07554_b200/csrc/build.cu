@@ -101,8 +101,10 @@ __global__ void __launch_bounds__(EDGE_THREADS) k_edges(const uint64_t *__restri
                                                         uint64_t m, uint64_t K, uint64_t t32,
                                                         const uint32_t *__restrict__ g_shr,
                                                         const uint16_t *__restrict__ g_tab,
-                                                        uint32_t B, uint32_t *L,
+                                                        uint32_t B, uint32_t j0, uint32_t Bb,
+                                                        uint32_t *L,
                                                         unsigned long long *live_ctr) {
+  // slots [j0, j0 + Bb) of the B sorted slots go to L (row stride Bb)
   extern __shared__ uint32_t sm[];
   uint32_t *shr = sm;
   uint16_t *tab = reinterpret_cast<uint16_t *>(sm + B);
@@ -140,6 +142,9 @@ __global__ void __launch_bounds__(EDGE_THREADS) k_edges(const uint64_t *__restri
           hi = tab[p + (1u << (PACIM_TB - w))];
         }
       }
+      lo = max(lo, j0);  // clip to the batch window
+      hi = min(hi, j0 + Bb);
+      if (hi < lo) hi = lo;
       cnt = hi - lo;
       const uint64_t ck = ckeys[e];  // the endpoints' store rows
       w_u[wid][lane] = (uint32_t)(ck >> 32);
@@ -170,7 +175,8 @@ __global__ void __launch_bounds__(EDGE_THREADS) k_edges(const uint64_t *__restri
         }
         const uint32_t j = w_lo[wid][a] + (idx - w_pre[wid][a]);
         if ((uint64_t)(shr[j] ^ w_he[wid][a]) < w_T[wid][a]) {
-          uf_unite(L, B, j, w_u[wid][a], w_v[wid][a]);
+          uf_unite(L, Bb, j - j0, w_u[wid][a], w_v[wid][a]);
+
           live++;
         }
       }
@@ -446,11 +452,10 @@ static float ev_ms(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
-void pc_build(pacim_ctx *ctx) {
-  const uint32_t n = ctx->nr, B = ctx->R_local;  // store rows = non-isolated vertices
-  PC_REQUIRE(B >= 1 && B <= 65535, PACIM_EINVAL, "local sketch count must be in [1, 65535]");
-  PC_REQUIRE(!ctx->compressed, PACIM_ENOTIMPL, "compressed store not built by pc_build");
-  // ---- slot table (host): local sketches sorted by hi32(hash(r)) (R2)
+// Host slot table: this ctx's sketches sorted by hi32(hash(r)) (R2) and the
+// candidate bucket table of k_edges; uploaded once per build.
+void pc_slot_table(pacim_ctx *ctx) {
+  const uint32_t B = ctx->R_local;
   ctx->slot_r.clear();
   ctx->r_slot.assign(ctx->R, -1);
   std::vector<std::pair<uint32_t, uint32_t>> hs;
@@ -468,40 +473,34 @@ void pc_build(pacim_ctx *ctx) {
   }
   const uint32_t NT = 1u << PACIM_TB;
   ctx->tab.assign(NT + 1, 0);
-  {
-    uint32_t j = 0;
-    for (uint32_t p = 0; p <= NT; p++) {
-      while (j < B && (ctx->shr[j] >> (32 - PACIM_TB)) < p) j++;
-      ctx->tab[p] = (uint16_t)j;
-    }
+  uint32_t j = 0;
+  for (uint32_t p = 0; p <= NT; p++) {
+    while (j < B && (ctx->shr[j] >> (32 - PACIM_TB)) < p) j++;
+    ctx->tab[p] = (uint16_t)j;
   }
   pc_ensure(ctx, ctx->d_shr, B * sizeof(uint32_t));
   pc_ensure(ctx, ctx->d_tab, (NT + 1) * sizeof(uint16_t));
-  pc_ensure(ctx, ctx->d_hot, 2 * (size_t)B * sizeof(uint32_t));
   PC_CUDA(cudaMemcpyAsync(ctx->d_shr.p, ctx->shr.data(), B * 4, cudaMemcpyHostToDevice,
                           ctx->stream));
   PC_CUDA(cudaMemcpyAsync(ctx->d_tab.p, ctx->tab.data(), (NT + 1) * 2, cudaMemcpyHostToDevice,
                           ctx->stream));
+}
 
-  // ---- buffers
-  pc_ensure(ctx, ctx->L, (size_t)n * B * sizeof(uint32_t));
-  pc_ensure(ctx, ctx->gain0, (size_t)ctx->n * sizeof(int64_t));
-  pc_ensure(ctx, ctx->counters, 64 * sizeof(uint64_t));
-  unsigned long long *ctr = ctx->counters.as<unsigned long long>();
-  PC_CUDA(cudaMemsetAsync(ctr, 0, 64 * sizeof(uint64_t), ctx->stream));
-  uint32_t *L = ctx->L.as<uint32_t>();
+// One sketch pass over the edge list for slots [j0, j0+Bb): parent arrays in
+// Lb (rows x Bb), unions, full compression and CC sizes (root slot HIGH|size).
+// ctr[0] += non-singleton CCs, ctr[1] += non-roots, ctr[4] += live pairs.
+// ev (optional, 3 events) is recorded after init, edges and compress.
+void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
+                    unsigned long long *ctr, cudaEvent_t *ev) {
+  const uint32_t n = ctx->nr, B = ctx->R_local;
+  const uint32_t NT = 1u << PACIM_TB;
+  pc_ensure(ctx, ctx->d_hot, 2 * (size_t)B * sizeof(uint32_t));
   uint32_t *hot_root = ctx->d_hot.as<uint32_t>();
-  const uint32_t H = std::min<uint32_t>(B, HOT_MAX);
-
-  cudaEvent_t ev[6];
-  for (auto &e : ev) PC_CUDA(cudaEventCreate(&e));
-  ctx->launches = 0;
+  const uint32_t H = std::min<uint32_t>(Bb, HOT_MAX);
   const unsigned rows_grid = pc_grid(ctx, (size_t)n * 32, 256, 16);
-
-  PC_CUDA(cudaEventRecord(ev[0], ctx->stream));
-  k_init<<<rows_grid, 256, 0, ctx->stream>>>(L, n, B);
+  k_init<<<rows_grid, 256, 0, ctx->stream>>>(Lb, n, Bb);
   PC_CHECK_LAUNCH();
-  PC_CUDA(cudaEventRecord(ev[1], ctx->stream));
+  if (ev) PC_CUDA(cudaEventRecord(ev[0], ctx->stream));
   {
     size_t smem = B * sizeof(uint32_t) + (NT + 1) * sizeof(uint16_t);
     unsigned g = pc_grid(ctx, (ctx->m + 31) / 32 * 32, EDGE_THREADS, 8);
@@ -510,25 +509,43 @@ void pc_build(pacim_ctx *ctx) {
                                    (int)smem));
       k_edges<true><<<g, EDGE_THREADS, smem, ctx->stream>>>(
           ctx->keys.as<uint64_t>(), ctx->ckeys.as<uint64_t>(), ctx->tm1.as<uint32_t>(), ctx->m,
-          ctx->K, 0,
-          ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, L, ctr + 4);
+          ctx->K, 0, ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4);
     } else {
       PC_CUDA(cudaFuncSetAttribute(k_edges<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
       k_edges<false><<<g, EDGE_THREADS, smem, ctx->stream>>>(
           ctx->keys.as<uint64_t>(), ctx->ckeys.as<uint64_t>(), nullptr, ctx->m, ctx->K, ctx->t32,
-          ctx->d_shr.as<uint32_t>(),
-          ctx->d_tab.as<uint16_t>(), B, L, ctr + 4);
+          ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4);
     }
     PC_CHECK_LAUNCH();
   }
-  PC_CUDA(cudaEventRecord(ev[2], ctx->stream));
-  k_hot_roots<<<(B + 255) / 256, 256, 0, ctx->stream>>>(L, n, B, ctx->hub_row, hot_root);
+  if (ev) PC_CUDA(cudaEventRecord(ev[1], ctx->stream));
+  k_hot_roots<<<(Bb + 255) / 256, 256, 0, ctx->stream>>>(Lb, n, Bb, ctx->hub_row, hot_root);
   PC_CHECK_LAUNCH();
-  k_compress_count<<<rows_grid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(L, n, B, hot_root,
+  k_compress_count<<<rows_grid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(Lb, n, Bb, hot_root,
                                                                               ctr);
   PC_CHECK_LAUNCH();
-  PC_CUDA(cudaEventRecord(ev[3], ctx->stream));
+  if (ev) PC_CUDA(cudaEventRecord(ev[2], ctx->stream));
+  ctx->launches += 4;
+}
+
+void pc_build(pacim_ctx *ctx) {
+  const uint32_t n = ctx->nr, B = ctx->R_local;  // store rows = non-isolated vertices
+  PC_REQUIRE(B >= 1 && B <= 65535, PACIM_EINVAL, "local sketch count must be in [1, 65535]");
+  PC_REQUIRE(!ctx->compressed, PACIM_ENOTIMPL, "compressed store not built by pc_build");
+  pc_slot_table(ctx);
+  pc_ensure(ctx, ctx->L, (size_t)n * B * sizeof(uint32_t));
+  pc_ensure(ctx, ctx->gain0, (size_t)ctx->n * sizeof(int64_t));
+  pc_ensure(ctx, ctx->counters, 64 * sizeof(uint64_t));
+  unsigned long long *ctr = ctx->counters.as<unsigned long long>();
+  PC_CUDA(cudaMemsetAsync(ctr, 0, 64 * sizeof(uint64_t), ctx->stream));
+  uint32_t *L = ctx->L.as<uint32_t>();
+  cudaEvent_t ev[6];
+  for (auto &e : ev) PC_CUDA(cudaEventCreate(&e));
+  ctx->launches = 0;
+  const unsigned rows_grid = pc_grid(ctx, (size_t)n * 32, 256, 16);
+  PC_CUDA(cudaEventRecord(ev[0], ctx->stream));
+  pc_sketch_pass(ctx, L, 0, B, ctr, ev + 1);
   // component count -> host (sync 1 of 2 per build)
   unsigned long long hc[2];
   PC_CUDA(cudaMemcpyAsync(hc, ctr, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
@@ -567,7 +584,8 @@ void pc_build(pacim_ctx *ctx) {
       ctx->perm.as<uint32_t>(), ctx->gain0.as<int64_t>(), ctx->rmap.as<uint32_t>(), 0);
   PC_CHECK_LAUNCH();
   PC_CUDA(cudaEventRecord(ev[5], ctx->stream));
-  ctx->launches += 6;
+  ctx->launches += 3;  // compact, fill, gain_scatter
+
   unsigned long long h[6];
   PC_CUDA(cudaMemcpyAsync(h, ctr, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                           ctx->stream));

@@ -1,0 +1,584 @@
+// compressed.cu — the paper's compressed sketches (Alg. 3; §3
+// P:1104-1253): H6c (center store) and H11 (warp-cooperative Get-center).
+//
+// Build: the R_g sketches are processed in batches of Bb slots.  Each batch
+// runs the same union-find pass as the uncompressed store into a temporary
+// parent array, adds its CC sizes to gain0 (H7), and keeps only, for each
+// center c_i (R9: hi32(mix64(v ^ K_c)) < A32, index = rank in vertex order),
+//   label[i][j] = min{ j' : c_j' in the same CC as c_i }
+//   size[i][j]  = CC size if label[i][j] = i, else 0
+// Total space O((1 + alpha R) n) (Thm 3.1).
+//
+// Select: per greedy step and slot, GetCenter(s) is a BFS from
+// the seed s over the live edges of G'_r run by one warp with a local queue
+// and visited set in shared memory ("Get-center allocates a local
+// queue").  The first center met gives <size[label], label>; a CC without a
+// center gives <0,-1> if a seed was visited, else <n', -1>.  MarkSeed
+// zeroes size[label].  The members of a newly covered CC lose
+// delta from their gain (incremental update, R17): small CCs are
+// enumerated by the same warp BFS; CCs larger than the queue are handled by
+// re-running the sketch pass for their batch and one dense pass (the only
+// place the full labels are rebuilt).
+#include <algorithm>
+#include <cstdlib>
+
+#include "pacim_internal.cuh"
+
+namespace {
+
+constexpr uint32_t NONE = 0xFFFFFFFFu;
+constexpr int PROBE_WARPS = 4;     // warps per block in k_probe
+constexpr uint32_t QCAP = 512;     // Get-center local queue capacity
+constexpr uint32_t HCAP = 1024;    // its visited hash set (power of two)
+
+// probe outcomes
+constexpr uint32_t ST_DONE = 0;       // delta known and applied (or zero)
+constexpr uint32_t ST_BIG_KNOWN = 1;  // uncovered CC with a center, too big to enumerate
+constexpr uint32_t ST_BIG_UNKNOWN = 2;// no center within QCAP visits: needs the dense analysis
+
+// ------------------------------------------------------------- centers
+__global__ void k_center_flag(uint32_t n, uint64_t Kc, uint64_t a32, uint64_t *flag) {
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (size_t)gridDim.x * blockDim.x)
+    flag[v] = (a32 >= (1ull << 32) || (pc_mix64((uint64_t)v ^ Kc) >> 32) < a32) ? 1 : 0;
+}
+
+__global__ void k_center_index(const uint64_t *flag, const uint64_t *pos, uint32_t n,
+                               uint32_t *center_of, uint32_t *centers) {
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (size_t)gridDim.x * blockDim.x) {
+    if (flag[v]) {
+      center_of[v] = (uint32_t)pos[v];
+      centers[pos[v]] = (uint32_t)v;
+    } else {
+      center_of[v] = NONE;
+    }
+  }
+}
+
+// ------------------------------------------------------- batch outputs
+// gain0[v] += sum over the batch's slots of (|C_j(v)| - 1) (gain0 starts at B)
+__global__ void k_gain_sizes(const uint32_t *Lb, uint32_t nr, uint32_t Bb, const uint32_t *rmap,
+                             int64_t *gain0) {
+  const int lane = threadIdx.x & 31;
+  size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t v = warp; v < nr; v += nw) {
+    long long g = 0;
+    for (uint32_t j = lane; j < Bb; j += 32) {
+      uint32_t s = Lb[v * Bb + j];
+      if (s == (uint32_t)v) continue;  // singleton: size 1, already counted
+      uint32_t sz = (s & PACIM_HIGH) ? (s & PACIM_LOW) : (Lb[(size_t)s * Bb + j] & PACIM_LOW);
+      g += (long long)sz - 1;
+    }
+    for (int d = 16; d; d >>= 1) g += __shfl_xor_sync(0xffffffffu, g, d);
+    if (lane == 0 && g) gain0[rmap[v]] += g;
+  }
+}
+
+// center i, batch slot jj: its CC's root row (NONE: singleton) and CC size
+__global__ void k_center_a(const uint32_t *Lb, uint32_t Bb, uint32_t rho, const uint32_t *centers,
+                           const uint32_t *cid, uint32_t *croot, uint32_t *csz, uint32_t B,
+                           uint32_t j0) {
+  const size_t tot = (size_t)rho * Bb;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t i = (uint32_t)(t / Bb), jj = (uint32_t)(t % Bb);
+    const uint32_t r = cid[centers[i]];
+    uint32_t root = NONE, size = 1;
+    if (r != NONE) {
+      const uint32_t s = Lb[(size_t)r * Bb + jj];
+      if (s & PACIM_HIGH) {
+        root = r;
+        size = s & PACIM_LOW;
+      } else if (s != r) {
+        root = s;
+        size = Lb[(size_t)s * Bb + jj] & PACIM_LOW;
+      }
+    }
+    croot[t] = root;
+    csz[(size_t)i * B + j0 + jj] = size;
+  }
+}
+
+// the root slot (HIGH|size > any center index) takes the minimum center index
+__global__ void k_center_b(uint32_t *Lb, uint32_t Bb, uint32_t rho, const uint32_t *croot) {
+  const size_t tot = (size_t)rho * Bb;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t root = croot[t];
+    if (root != NONE) atomicMin(Lb + (size_t)root * Bb + (t % Bb), (uint32_t)(t / Bb));
+  }
+}
+
+__global__ void k_center_c(const uint32_t *Lb, uint32_t Bb, uint32_t rho, const uint32_t *croot,
+                           uint32_t *clabel, uint32_t *csz, uint32_t B, uint32_t j0) {
+  const size_t tot = (size_t)rho * Bb;
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < tot;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t i = (uint32_t)(t / Bb), jj = (uint32_t)(t % Bb);
+    const uint32_t root = croot[t];
+    const uint32_t label = root == NONE ? i : Lb[(size_t)root * Bb + jj];
+    clabel[(size_t)i * B + j0 + jj] = label;
+    if (label != i) csz[(size_t)i * B + j0 + jj] = 0;  // size kept at the label only
+  }
+}
+
+__global__ void k_fill_i64c(int64_t *a, uint32_t n, int64_t x) {
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (size_t)gridDim.x * blockDim.x)
+    a[v] = x;
+}
+
+// --------------------------------------------------------- Get-center
+struct ProbeParams {
+  const uint64_t *off;
+  const uint32_t *nbr;
+  uint64_t K, t32;
+  int wic;
+  const uint32_t *shr;      // hi32(hash(r)) per slot
+  uint32_t B;
+  const uint32_t *center_of;
+  const uint32_t *clabel;   // [rho][B]
+  uint32_t *csw;            // [rho][B] working sizes
+  const uint8_t *is_seed;
+  long long *target;        // gain (or delta) vector, n entries
+  uint32_t *st;             // per slot: outcome
+  uint32_t *lab;            // per slot: label (BIG_KNOWN)
+  uint32_t *dl;             // per slot: delta
+  unsigned long long *sum;  // [0] sum of DONE deltas, [1] number of BIG slots, [2] visits
+};
+
+__device__ __forceinline__ bool live_edge(const ProbeParams &P, uint32_t x, uint32_t w,
+                                          uint32_t hr) {
+  const uint64_t a = x < w ? x : w, b = x < w ? w : x;
+  const uint32_t he = (uint32_t)(pc_mix64(((a << 32) | b) ^ P.K) >> 32);
+  uint64_t T = P.t32;
+  if (P.wic) {  // R4
+    const uint64_t s = (P.off[x + 1] - P.off[x]) + (P.off[w + 1] - P.off[w]);
+    T = (1ull << 33) / s;
+    if (T > (1ull << 32)) T = 1ull << 32;
+  }
+  return (uint64_t)(hr ^ he) < T;  // R3
+}
+
+// one warp per slot: BFS from s with a shared-memory queue and visited set
+__global__ void __launch_bounds__(PROBE_WARPS * 32) k_probe(ProbeParams P, uint32_t s) {
+  __shared__ uint32_t q[PROBE_WARPS][QCAP];
+  __shared__ uint32_t hs[PROBE_WARPS][HCAP];
+  __shared__ uint32_t tail[PROBE_WARPS], ovf[PROBE_WARPS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned long long mysum = 0, nbig = 0, visits = 0;
+  for (uint32_t j = blockIdx.x * PROBE_WARPS + w; j < P.B; j += gridDim.x * PROBE_WARPS) {
+    const uint32_t hr = P.shr[j];
+    for (uint32_t i = lane; i < HCAP; i += 32) hs[w][i] = NONE;
+    __syncwarp();
+    if (lane == 0) {
+      q[w][0] = s;
+      hs[w][(s * 2654435761u) & (HCAP - 1)] = s;
+      tail[w] = 1;
+      ovf[w] = 0;
+    }
+    __syncwarp();
+    uint32_t head = 0, label = NONE, delta = 0;
+    bool seed_seen = false, enumerate = false;
+    while (head < tail[w]) {
+      const uint32_t x = q[w][head++];
+      if (!enumerate) {
+        const uint32_t ci = P.center_of[x];  // R12: center check first
+        if (ci != NONE) {
+          label = P.clabel[(size_t)ci * P.B + j];
+          delta = P.csw[(size_t)label * P.B + j];
+          if (delta == 0 || delta > QCAP) break;  // covered, or too big to enumerate here
+          enumerate = true;  // uncovered CC of delta <= QCAP vertices: list its members
+        }
+        if (P.is_seed[x]) seed_seen = true;
+      }
+      for (uint64_t e = P.off[x] + lane; e < P.off[x + 1]; e += 32) {
+        const uint32_t v = P.nbr[e];
+        if (!live_edge(P, x, v, hr)) continue;
+        uint32_t h = (v * 2654435761u) & (HCAP - 1);
+        for (;;) {
+          const uint32_t old = atomicCAS(&hs[w][h], NONE, v);
+          if (old == NONE) {  // newly visited
+            const uint32_t pos = atomicAdd(&tail[w], 1u);
+            if (pos < QCAP) q[w][pos] = v; else ovf[w] = 1;
+            break;
+          }
+          if (old == v) break;
+          h = (h + 1) & (HCAP - 1);
+        }
+      }
+      __syncwarp();
+      if (ovf[w]) break;
+    }
+    const uint32_t nvis = min(tail[w], QCAP);
+    visits += head;
+    uint32_t status = ST_DONE;
+    if (label != NONE) {
+      if (delta > QCAP) {
+        status = ST_BIG_KNOWN;
+      } else if (delta > 0) {
+        // enumerated: q[0..delta) are exactly the CC's members
+        for (uint32_t i = lane; i < nvis; i += 32) {
+          const uint32_t u = q[w][i];
+          if (u != s) atomicAdd((unsigned long long *)&P.target[u], (unsigned long long)(-(long long)delta));
+        }
+      }
+      if (lane == 0 && delta > 0) P.csw[(size_t)label * P.B + j] = 0;  // MarkSeed
+    } else if (ovf[w]) {
+      status = ST_BIG_UNKNOWN;  // no center among the first QCAP vertices
+    } else {
+      // BFS exhausted the CC without a center
+      delta = seed_seen ? 0 : nvis;
+      if (delta)
+        for (uint32_t i = lane; i < nvis; i += 32) {
+          const uint32_t u = q[w][i];
+          if (u != s) atomicAdd((unsigned long long *)&P.target[u], (unsigned long long)(-(long long)delta));
+        }
+    }
+    if (lane == 0) {
+      P.st[j] = status;
+      P.lab[j] = label;
+      P.dl[j] = delta;
+      if (status == ST_DONE) mysum += delta; else nbig++;
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    if (mysum) atomicAdd(P.sum + 0, mysum);
+    if (nbig) atomicAdd(P.sum + 1, nbig);
+    if (visits) atomicAdd(P.sum + 2, visits);
+  }
+}
+
+// ------------------------------------------- dense path for big components
+// root row of row v in batch slot jj of the rebuilt parent array
+__device__ __forceinline__ uint32_t root_of(const uint32_t *Lb, uint32_t Bb, uint32_t v,
+                                            uint32_t jj) {
+  const uint32_t s = Lb[(size_t)v * Bb + jj];
+  return (s == v || (s & PACIM_HIGH)) ? v : s;
+}
+
+// per big slot: size of the seed's CC, any center's label in it, seed present
+__global__ void k_big_analyze(const uint32_t *Lb, uint32_t nr, uint32_t Bb, uint32_t j0,
+                             uint32_t B, const uint32_t *st, const uint32_t *sroot,
+                             const uint32_t *rmap, const uint32_t *center_of,
+                             const uint32_t *clabel, const uint8_t *is_seed,
+                             unsigned long long *cnt, uint32_t *clab, uint32_t *seedf) {
+  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < (size_t)nr * Bb;
+       t += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t v = (uint32_t)(t / Bb), jj = (uint32_t)(t % Bb);
+    if (st[j0 + jj] != ST_BIG_UNKNOWN) continue;
+    if (root_of(Lb, Bb, v, jj) != sroot[jj]) continue;
+    atomicAdd(cnt + jj, 1ull);
+    const uint32_t vid = rmap[v];
+    const uint32_t ci = center_of[vid];
+    if (ci != NONE) atomicMin(clab + jj, clabel[(size_t)ci * B + j0 + jj]);
+    if (is_seed[vid]) seedf[jj] = 1;
+  }
+}
+
+__global__ void k_big_decide(uint32_t Bb, uint32_t j0, uint32_t B, uint32_t *st, uint32_t *dl,
+                             const uint32_t *lab, const unsigned long long *cnt,
+                             const uint32_t *clab, const uint32_t *seedf, uint32_t *csw,
+                             unsigned long long *sum) {
+  for (uint32_t jj = blockIdx.x * blockDim.x + threadIdx.x; jj < Bb; jj += gridDim.x * blockDim.x) {
+    const uint32_t j = j0 + jj;
+    uint32_t d = 0;
+    if (st[j] == ST_BIG_KNOWN) {
+      d = dl[j];
+      csw[(size_t)lab[j] * B + j] = 0;
+    } else if (st[j] == ST_BIG_UNKNOWN) {
+      if (clab[jj] != NONE) {
+        d = csw[(size_t)clab[jj] * B + j];
+        csw[(size_t)clab[jj] * B + j] = 0;
+      } else {
+        d = seedf[jj] ? 0 : (uint32_t)cnt[jj];
+      }
+    } else {
+      continue;
+    }
+    dl[j] = d;
+    atomicAdd(sum, (unsigned long long)d);
+  }
+}
+
+__global__ void k_big_apply(const uint32_t *Lb, uint32_t nr, uint32_t Bb, uint32_t j0,
+                            const uint32_t *st, const uint32_t *dl, const uint32_t *sroot,
+                            const uint32_t *rmap, uint32_t s, long long *target) {
+  const int lane = threadIdx.x & 31;
+  size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t v = warp; v < nr; v += nw) {
+    long long d = 0;
+    for (uint32_t jj = lane; jj < Bb; jj += 32) {
+      const uint32_t stt = st[j0 + jj];
+      if (stt == ST_DONE || dl[j0 + jj] == 0) continue;
+      if (root_of(Lb, Bb, (uint32_t)v, jj) == sroot[jj]) d += dl[j0 + jj];
+    }
+    for (int q = 16; q; q >>= 1) d += __shfl_xor_sync(0xffffffffu, d, q);
+    if (lane == 0 && d) {
+      const uint32_t vid = rmap[v];
+      if (vid != s) atomicAdd((unsigned long long *)&target[vid], (unsigned long long)(-d));
+    }
+  }
+}
+
+__global__ void k_seed_roots(const uint32_t *Lb, uint32_t Bb, uint32_t srow, uint32_t *sroot) {
+  for (uint32_t jj = blockIdx.x * blockDim.x + threadIdx.x; jj < Bb; jj += gridDim.x * blockDim.x)
+    sroot[jj] = root_of(Lb, Bb, srow, jj);
+}
+
+__global__ void k_set_seed(long long *gain, uint8_t *is_seed, uint32_t s, int set_gain) {
+  if (set_gain) gain[s] = -1;
+  is_seed[s] = 1;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host
+static uint32_t choose_batch(pacim_ctx *ctx) {
+  const uint32_t B = ctx->R_local;
+  if (const char *e = getenv("PACIM_BATCH")) return std::max<uint32_t>(1, std::min<uint32_t>(B, atoi(e)));
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  size_t budget = std::min<size_t>(fr / 3, (size_t)24 << 30);
+  size_t per = (size_t)std::max<uint32_t>(ctx->nr, 1) * 4;
+  size_t bb = budget / per;
+  return (uint32_t)std::max<size_t>(1, std::min<size_t>(B, bb));
+}
+
+void pc_build_compressed(pacim_ctx *ctx) {
+  const uint32_t n = ctx->n, nr = ctx->nr, B = ctx->R_local;
+  PC_REQUIRE(B >= 1 && B <= 65535, PACIM_EINVAL, "local sketch count must be in [1, 65535]");
+  pc_slot_table(ctx);
+  pc_ensure(ctx, ctx->counters, 64 * sizeof(uint64_t));
+  unsigned long long *ctr = ctx->counters.as<unsigned long long>();
+  PC_CUDA(cudaMemsetAsync(ctr, 0, 64 * sizeof(uint64_t), ctx->stream));
+  cudaEvent_t e0, e1, e2;
+  PC_CUDA(cudaEventCreate(&e0));
+  PC_CUDA(cudaEventCreate(&e1));
+  PC_CUDA(cudaEventCreate(&e2));
+  ctx->launches = 0;
+  PC_CUDA(cudaEventRecord(e0, ctx->stream));
+  // ---- centers (R9)
+  const uint64_t Kc = pc_mix64(ctx->hash_seed ^ 0x9E3779B97F4A7C15ull);
+  pc_ensure(ctx, ctx->scratch, 2 * ((size_t)n + 1) * 8);
+  uint64_t *flag = ctx->scratch.as<uint64_t>(), *pos = flag + n + 1;
+  k_center_flag<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(n, Kc, ctx->a32, flag);
+  PC_CHECK_LAUNCH();
+  PC_CUDA(cudaMemsetAsync(flag + n, 0, 8, ctx->stream));
+  pc_exclusive_scan_u64(ctx, flag, pos, (size_t)n + 1);
+  uint64_t rho = 0;
+  PC_CUDA(cudaMemcpyAsync(&rho, pos + n, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->rho = (uint32_t)rho;
+  pc_ensure(ctx, ctx->center_of, (size_t)n * 4);
+  pc_ensure(ctx, ctx->centers, std::max<size_t>(rho, 1) * 4);
+  k_center_index<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(
+      flag, pos, n, ctx->center_of.as<uint32_t>(), ctx->centers.as<uint32_t>());
+  PC_CHECK_LAUNCH();
+  const size_t cs = std::max<size_t>((size_t)rho * B, 1) * 4;
+  pc_ensure(ctx, ctx->clabel, cs);
+  pc_ensure(ctx, ctx->csz, cs);
+  pc_ensure(ctx, ctx->csz_work, cs);
+  pc_ensure(ctx, ctx->gain0, (size_t)n * 8);
+  k_fill_i64c<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(ctx->gain0.as<int64_t>(), n,
+                                                            (int64_t)B);
+  PC_CHECK_LAUNCH();
+  // ---- batches of Bb slots
+  ctx->Bb = choose_batch(ctx);
+  const uint32_t Bb = ctx->Bb;
+  pc_ensure(ctx, ctx->Ltmp, std::max<size_t>((size_t)nr * Bb, 1) * 4);
+  pc_ensure(ctx, ctx->cwork, std::max<size_t>((size_t)rho * Bb, 1) * 4 + 64);
+  uint32_t *Lb = ctx->Ltmp.as<uint32_t>();
+  uint32_t *croot = ctx->cwork.as<uint32_t>();
+  PC_CUDA(cudaEventRecord(e1, ctx->stream));
+  for (uint32_t j0 = 0; j0 < B; j0 += Bb) {
+    const uint32_t bb = std::min(Bb, B - j0);
+    pc_sketch_pass(ctx, Lb, j0, bb, ctr, nullptr);
+    k_gain_sizes<<<pc_grid(ctx, (size_t)nr * 32, 256, 16), 256, 0, ctx->stream>>>(
+        Lb, nr, bb, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>());
+    PC_CHECK_LAUNCH();
+    const size_t tot = (size_t)rho * bb;
+    if (tot) {
+      k_center_a<<<pc_grid(ctx, tot, 256), 256, 0, ctx->stream>>>(
+          Lb, bb, (uint32_t)rho, ctx->centers.as<uint32_t>(), ctx->cid.as<uint32_t>(), croot,
+          ctx->csz.as<uint32_t>(), B, j0);
+      PC_CHECK_LAUNCH();
+      k_center_b<<<pc_grid(ctx, tot, 256), 256, 0, ctx->stream>>>(Lb, bb, (uint32_t)rho, croot);
+      PC_CHECK_LAUNCH();
+      k_center_c<<<pc_grid(ctx, tot, 256), 256, 0, ctx->stream>>>(
+          Lb, bb, (uint32_t)rho, croot, ctx->clabel.as<uint32_t>(), ctx->csz.as<uint32_t>(), B,
+          j0);
+      PC_CHECK_LAUNCH();
+      ctx->launches += 3;
+    }
+    ctx->launches += 1;
+  }
+  PC_CUDA(cudaMemcpyAsync(ctx->csz_work.p, ctx->csz.p, cs, cudaMemcpyDeviceToDevice, ctx->stream));
+  PC_CUDA(cudaEventRecord(e2, ctx->stream));
+  unsigned long long h[6];
+  PC_CUDA(cudaMemcpyAsync(h, ctr, 6 * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  float ms_all = 0, ms_pre = 0;
+  cudaEventElapsedTime(&ms_all, e0, e2);
+  cudaEventElapsedTime(&ms_pre, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(e2);
+  ctx->ncomp = h[0];
+  ctx->nnonsingle = h[0] + h[1];
+  ctx->nmember = 0;
+  ctx->stats.live_pairs = h[4];
+  ctx->stats.t_build_ms = ms_all;
+  ctx->stats.t_centers_ms = ms_pre;
+  ctx->stats.t_init_ms = ctx->stats.t_edges_ms = ctx->stats.t_compress_ms = 0;
+  ctx->stats.t_compact_ms = ctx->stats.t_gain_ms = 0;
+  ctx->stats.kernel_launches_build = ctx->launches;
+}
+
+void pc_select_reset_compressed(pacim_ctx *ctx) {
+  const size_t cs = std::max<size_t>((size_t)ctx->rho * ctx->R_local, 1) * 4;
+  PC_CUDA(cudaMemcpyAsync(ctx->csz_work.p, ctx->csz.p, cs, cudaMemcpyDeviceToDevice, ctx->stream));
+  pc_ensure(ctx, ctx->is_seed, ctx->n);
+  PC_CUDA(cudaMemsetAsync(ctx->is_seed.p, 0, ctx->n, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// MarkSeed(s) on this ctx's compressed sketches; member gains in target
+// decrease by delta_r.  Returns sum_r delta_r.  Marks s as a seed.
+void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *local_gain) {
+  const uint32_t B = ctx->R_local, nr = ctx->nr;
+  pc_ensure(ctx, ctx->sel_list, (size_t)B * 16 + 64);
+  uint32_t *st = ctx->sel_list.as<uint32_t>(), *lab = st + B, *dl = lab + B;
+  unsigned long long *sum = reinterpret_cast<unsigned long long *>(dl + B + (B & 1));
+  PC_CUDA(cudaMemsetAsync(sum, 0, 3 * 8, ctx->stream));
+  ProbeParams P;
+  P.off = ctx->off.as<uint64_t>();
+  P.nbr = ctx->nbr.as<uint32_t>();
+  P.K = ctx->K;
+  P.t32 = ctx->t32;
+  P.wic = ctx->pmodel == PACIM_P_WIC;
+  P.shr = ctx->d_shr.as<uint32_t>();
+  P.B = B;
+  P.center_of = ctx->center_of.as<uint32_t>();
+  P.clabel = ctx->clabel.as<uint32_t>();
+  P.csw = ctx->csz_work.as<uint32_t>();
+  P.is_seed = ctx->is_seed.as<uint8_t>();
+  P.target = reinterpret_cast<long long *>(target);
+  P.st = st;
+  P.lab = lab;
+  P.dl = dl;
+  P.sum = sum;
+  k_probe<<<std::min<unsigned>((B + PROBE_WARPS - 1) / PROBE_WARPS, ctx->sm_count * 8),
+            PROBE_WARPS * 32, 0, ctx->stream>>>(P, s);
+  PC_CHECK_LAUNCH();
+  ctx->launches++;
+  unsigned long long hs[3];
+  PC_CUDA(cudaMemcpyAsync(hs, sum, 24, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->stats.select_bfs_visits += hs[2];
+  unsigned long long total = hs[0];
+  if (hs[1]) {
+    // big CCs: rebuild the labels of the affected batches, then dense passes
+    std::vector<uint32_t> hst(B);
+    PC_CUDA(cudaMemcpyAsync(hst.data(), st, (size_t)B * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    uint32_t srow = 0;
+    PC_CUDA(cudaMemcpyAsync(&srow, ctx->cid.as<uint32_t>() + s, 4, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    const uint32_t Bb = ctx->Bb;
+    uint32_t *Lb = ctx->Ltmp.as<uint32_t>();
+    pc_ensure(ctx, ctx->scratch2, (size_t)Bb * 24 + 64);
+    unsigned long long *cnt = ctx->scratch2.as<unsigned long long>();
+    uint32_t *sroot = reinterpret_cast<uint32_t *>(cnt + Bb), *clab = sroot + Bb, *seedf = clab + Bb;
+    unsigned long long *ctr = ctx->counters.as<unsigned long long>();
+    for (uint32_t j0 = 0; j0 < B; j0 += Bb) {
+      const uint32_t bb = std::min(Bb, B - j0);
+      bool any = false;
+      for (uint32_t j = j0; j < j0 + bb; j++) any |= hst[j] != ST_DONE;
+      if (!any) continue;
+      pc_sketch_pass(ctx, Lb, j0, bb, ctr, nullptr);
+      k_seed_roots<<<(bb + 255) / 256, 256, 0, ctx->stream>>>(Lb, bb, srow, sroot);
+      PC_CUDA(cudaMemsetAsync(cnt, 0, (size_t)bb * 8, ctx->stream));
+      PC_CUDA(cudaMemsetAsync(clab, 0xFF, (size_t)bb * 4, ctx->stream));
+      PC_CUDA(cudaMemsetAsync(seedf, 0, (size_t)bb * 4, ctx->stream));
+      k_big_analyze<<<pc_grid(ctx, (size_t)nr * bb, 256, 16), 256, 0, ctx->stream>>>(
+          Lb, nr, bb, j0, B, st, sroot, ctx->rmap.as<uint32_t>(), ctx->center_of.as<uint32_t>(),
+          ctx->clabel.as<uint32_t>(), ctx->is_seed.as<uint8_t>(), cnt, clab, seedf);
+      k_big_decide<<<(bb + 255) / 256, 256, 0, ctx->stream>>>(bb, j0, B, st, dl, lab, cnt, clab,
+                                                             seedf, ctx->csz_work.as<uint32_t>(),
+                                                             sum);
+      k_big_apply<<<pc_grid(ctx, (size_t)nr * 32, 256, 16), 256, 0, ctx->stream>>>(
+          Lb, nr, bb, j0, st, dl, sroot, ctx->rmap.as<uint32_t>(), s,
+          reinterpret_cast<long long *>(target));
+      PC_CHECK_LAUNCH();
+      ctx->launches += 4;
+    }
+    PC_CUDA(cudaMemcpyAsync(&total, sum, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  k_set_seed<<<1, 1, 0, ctx->stream>>>(reinterpret_cast<long long *>(target), ctx->is_seed.as<uint8_t>(),
+                                       s, 0);
+  PC_CHECK_LAUNCH();
+  *local_gain = (int64_t)total;
+}
+
+void pc_select_compressed(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
+                          int64_t *sigma_num) {
+  const uint32_t n = ctx->n;
+  cudaEvent_t e0, e1;
+  PC_CUDA(cudaEventCreate(&e0));
+  PC_CUDA(cudaEventCreate(&e1));
+  PC_CUDA(cudaEventRecord(e0, ctx->stream));
+  pc_ensure(ctx, ctx->gain, (size_t)n * 8);
+  PC_CUDA(cudaMemcpyAsync(ctx->gain.p, ctx->gain0.p, (size_t)n * 8, cudaMemcpyDeviceToDevice,
+                          ctx->stream));
+  pc_select_reset_compressed(ctx);
+  ctx->stats.select_bfs_visits = 0;
+  ctx->launches = 0;
+  long long run = 0;
+  for (uint32_t i = 0; i < k; i++) {
+    uint32_t s;
+    int64_t g;
+    pc_argmax(ctx, ctx->gain.as<int64_t>(), n, &s, &g);
+    int64_t got = 0;
+    pc_cover_compressed(ctx, s, ctx->gain.as<int64_t>(), &got);
+    k_set_seed<<<1, 1, 0, ctx->stream>>>(ctx->gain.as<long long>(), ctx->is_seed.as<uint8_t>(), s,
+                                         1);
+    PC_CHECK_LAUNCH();
+    ctx->launches += 3;
+    PC_REQUIRE(got == g, PACIM_ECHECK,
+               "compressed select: sum_r delta_r = " + std::to_string(got) +
+                   " differs from the argmax gain " + std::to_string(g));
+    seeds[i] = s;
+    gain_num[i] = g;
+    run += g;
+    sigma_num[i] = run;
+  }
+  PC_CUDA(cudaEventRecord(e1, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  ctx->stats.t_select_ms = ms;
+  ctx->stats.kernel_launches_select = ctx->launches;
+}
+
+void pc_get_center_sketch(pacim_ctx *ctx, uint32_t slot, uint32_t *label, uint32_t *size) {
+  const uint32_t rho = ctx->rho, B = ctx->R_local;
+  if (!rho) return;
+  std::vector<uint32_t> a((size_t)rho * B), b((size_t)rho * B);
+  PC_CUDA(cudaMemcpyAsync(a.data(), ctx->clabel.p, (size_t)rho * B * 4, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  PC_CUDA(cudaMemcpyAsync(b.data(), ctx->csz_work.p, (size_t)rho * B * 4, cudaMemcpyDeviceToHost,
+                          ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (uint32_t i = 0; i < rho; i++) {
+    label[i] = a[(size_t)i * B + slot];
+    size[i] = b[(size_t)i * B + slot];
+  }
+}

@@ -122,10 +122,14 @@ struct pacim_ctx {
   // compressed store (H6c)
   uint32_t rho = 0;
   DevBuf center_of;   // u32[n] center index or 0xFFFFFFFF
+  DevBuf centers;     // u32[rho] center vertex ids in increasing order
   DevBuf clabel;      // u32[rho*B]  label of center i in slot j at i*B + j
   DevBuf csz;         // u32[rho*B]  pristine sizes
   DevBuf csz_work;    // u32[rho*B]  sizes zeroed by MarkSeed
-  DevBuf Ltmp;        // u32[n*Bb] parent arrays of one build batch
+  DevBuf Ltmp;        // u32[rows*Bb] parent arrays of one build batch
+  uint32_t Bb = 0;    // slots per compressed build batch
+  DevBuf is_seed;     // u8[n] seeds of the current selection (Get-center seed test)
+  DevBuf cwork;       // per-step compressed cover scratch
 
   // scratch
   DevBuf counters;    // u64[64]
@@ -162,6 +166,16 @@ void pc_generate(pacim_ctx *ctx, int kind, const uint64_t *params, int nparams,
                  uint64_t gen_seed);
 // build.cu
 void pc_build(pacim_ctx *ctx);
+void pc_slot_table(pacim_ctx *ctx);
+void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
+                    unsigned long long *ctr, cudaEvent_t *ev);
+// compressed.cu (H6c, H11)
+void pc_build_compressed(pacim_ctx *ctx);
+void pc_select_compressed(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
+                          int64_t *sigma_num);
+void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *local_gain);
+void pc_select_reset_compressed(pacim_ctx *ctx);
+void pc_get_center_sketch(pacim_ctx *ctx, uint32_t slot, uint32_t *label, uint32_t *size);
 // select.cu
 void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
                int64_t *sigma_num);

@@ -1,0 +1,107 @@
+"""GPU parity of the compressed store (H6c) and Get-center selection (H11)
+against the oracle's Alg. 3 transcription and its greedy."""
+import numpy as np
+import pytest
+
+import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pc():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2311_07554_b200 import build
+    build.build()
+    import paper_2311_07554_b200 as P
+    return P
+
+
+@pytest.fixture(scope="module")
+def ctx(pc):
+    c = pc.Context(0)
+    yield c
+    c.close()
+
+
+CASES = [
+    # graph, p, R, k, a32
+    (lambda: inputs.random_graph(300, 900, 41), 0.2, 16, 8, 1 << 28),
+    (lambda: inputs.random_powerlaw_graph(2000, 8000, 42), 0.05, 64, 12, 1 << 28),
+    (lambda: inputs.random_graph(3000, 9000, 43), 0.5, 8, 6, 1 << 28),      # giant CC > queue
+    (lambda: inputs.random_graph(3000, 9000, 44), 0.5, 8, 6, 1 << 20),      # few centers: overflow
+    (lambda: inputs.random_powerlaw_graph(1500, 9000, 45), "wic", 24, 10, 1 << 30),
+    (lambda: inputs.random_graph(500, 1500, 46), 0.3, 12, 10, 0),           # alpha = 0: no centers
+    (lambda: inputs.path_graph(700), 1.0, 4, 3, 1 << 27),
+    (lambda: inputs.random_graph(400, 800, 47), 0.0, 5, 4, 1 << 29),
+]
+
+
+def run_case(orc, ctx, i, check_sketches=True):
+    from oracle.oracle import Graph
+    build_fn, p, R, k, a32 = CASES[i]
+    off, nbr = build_fn()
+    g = Graph(len(off) - 1, off, nbr)
+    model, t32 = (1, 0) if p == "wic" else (0, orc.t32_const(p))
+    seed = 500 + i
+    ctx.pacim_load_graph(g.off, g.nbr, model, t32, 2)
+    ctx.pacim_build_sketches(R, seed, a32)
+    st = ctx.pacim_get_stats()
+    cs, _ = orc.centers(g.n, seed, a32)
+    assert st["compressed"] == 1 and st["rho"] == len(cs)
+    if check_sketches:
+        for r in range(R):
+            lab, sz = ctx.pacim_get_center_sketch(r)
+            elab, esz = orc.compressed_sketch(g, model, t32, seed, r, a32)
+            assert np.array_equal(lab, elab), r
+            assert np.array_equal(sz, esz), r
+    s, gn, sg, _ = ctx.pacim_select_seeds(k)
+    es, egn, esg, eg0 = orc.greedy(g, model, t32, R, seed, k, want_gain0=True)
+    assert np.array_equal(ctx.pacim_get_gain0(), eg0)
+    assert list(s) == list(es)
+    assert list(gn) == list(egn)
+    assert list(sg) == list(esg)
+
+
+@pytest.mark.parametrize("i", range(len(CASES)))
+def test_compressed_parity(orc, ctx, i):
+    run_case(orc, ctx, i)
+
+
+@pytest.mark.parametrize("i", [1, 2, 4])
+def test_compressed_multibatch(orc, ctx, i, monkeypatch):
+    monkeypatch.setenv("PACIM_BATCH", "3")  # 3 slots per build batch
+    run_case(orc, ctx, i)
+
+
+def test_compressed_equals_uncompressed_c1(ctx):
+    from paper_2311_07554_b200 import pipeline
+    cfg = inputs.config("c1")
+    pipeline.generate(ctx, cfg)
+    ctx.pacim_build_sketches(cfg["R"], cfg["hash_seed"])
+    a = ctx.pacim_select_seeds(cfg["k"])
+    ctx.pacim_build_sketches(cfg["R"], cfg["hash_seed"], 1 << 28)
+    b = ctx.pacim_select_seeds(cfg["k"])
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+
+
+def test_compressed_rank_emulation(orc, pc):
+    from oracle.oracle import Graph
+    from paper_2311_07554_b200 import dist
+    off, nbr = inputs.random_powerlaw_graph(2500, 12000, 48)
+    g = Graph(2500, off, nbr)
+    t32 = orc.t32_const(0.08)
+    R, seed, k = 20, 9, 10
+    es, egn, esg, _ = orc.greedy(g, 0, t32, R, seed, k)
+    ctxs = []
+    for rank in range(2):
+        c = pc.Context(0)
+        c.pacim_load_graph(off, nbr, 0, t32, 1)
+        c.pacim_build_sketches(R, seed, 1 << 28, rank, 2)
+        ctxs.append(c)
+    seeds, gains, sig = dist.emulated_select(ctxs, g.n, k, device="cuda")
+    assert list(seeds) == list(es) and list(gains) == list(egn)
+    for c in ctxs:
+        c.close()
