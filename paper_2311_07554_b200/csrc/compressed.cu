@@ -166,7 +166,7 @@ __device__ __forceinline__ bool live_edge(const ProbeParams &P, uint32_t x, uint
 __global__ void __launch_bounds__(PROBE_WARPS * 32) k_probe(ProbeParams P, uint32_t s) {
   __shared__ uint32_t q[PROBE_WARPS][QCAP];
   __shared__ uint32_t hs[PROBE_WARPS][HCAP];
-  __shared__ uint32_t tail[PROBE_WARPS], ovf[PROBE_WARPS];
+  __shared__ uint32_t tail[PROBE_WARPS], ovf[PROBE_WARPS], found[PROBE_WARPS];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   unsigned long long mysum = 0, nbig = 0, visits = 0;
   for (uint32_t j = blockIdx.x * PROBE_WARPS + w; j < P.B; j += gridDim.x * PROBE_WARPS) {
@@ -182,34 +182,65 @@ __global__ void __launch_bounds__(PROBE_WARPS * 32) k_probe(ProbeParams P, uint3
     __syncwarp();
     uint32_t head = 0, label = NONE, delta = 0;
     bool seed_seen = false, enumerate = false;
+    if (lane == 0) found[w] = NONE;
+    {  // the start vertex itself (R12: center check first)
+      const uint32_t ci = P.center_of[s];
+      if (ci != NONE && lane == 0) found[w] = P.clabel[(size_t)ci * P.B + j];
+    }
+    __syncwarp();
     while (head < tail[w]) {
-      const uint32_t x = q[w][head++];
-      if (!enumerate) {
-        const uint32_t ci = P.center_of[x];  // R12: center check first
-        if (ci != NONE) {
-          label = P.clabel[(size_t)ci * P.B + j];
-          delta = P.csw[(size_t)label * P.B + j];
-          if (delta == 0 || delta > QCAP) break;  // covered, or too big to enumerate here
-          enumerate = true;  // uncovered CC of delta <= QCAP vertices: list its members
-        }
-        if (P.is_seed[x]) seed_seen = true;
+      // A center met anywhere in the CC gives the same <size, label> (all
+      // centers of a CC share the label), so centers are recognised when
+      // discovered, not only when dequeued: a hub seed finds one among its
+      // live neighbours without filling the queue.
+      if (!enumerate && found[w] != NONE) {
+        label = found[w];
+        delta = P.csw[(size_t)label * P.B + j];
+        if (delta == 0 || delta > QCAP) break;  // covered, or too big to enumerate here
+        enumerate = true;  // uncovered CC of delta <= QCAP vertices: list its members
       }
-      for (uint64_t e = P.off[x] + lane; e < P.off[x + 1]; e += 32) {
-        const uint32_t v = P.nbr[e];
-        if (!live_edge(P, x, v, hr)) continue;
-        uint32_t h = (v * 2654435761u) & (HCAP - 1);
-        for (;;) {
-          const uint32_t old = atomicCAS(&hs[w][h], NONE, v);
-          if (old == NONE) {  // newly visited
-            const uint32_t pos = atomicAdd(&tail[w], 1u);
-            if (pos < QCAP) q[w][pos] = v; else ovf[w] = 1;
-            break;
+      const uint32_t x = q[w][head++];
+      if (!enumerate && P.is_seed[x]) seed_seen = true;
+      const uint64_t e1 = P.off[x + 1];
+      for (uint64_t e0 = P.off[x]; e0 < e1; e0 += 32) {
+        const uint64_t e = e0 + lane;
+        // the set never holds more than QCAP + 31 < HCAP vertices: lanes stop
+        // inserting once the queue is full, so probing always terminates
+        if (e < e1 && tail[w] < QCAP) {
+          const uint32_t v = P.nbr[e];
+          if (live_edge(P, x, v, hr)) {
+            uint32_t h = (v * 2654435761u) & (HCAP - 1);
+            for (;;) {
+              const uint32_t old = atomicCAS(&hs[w][h], NONE, v);
+              if (old == NONE) {  // newly visited
+                const uint32_t pos = atomicAdd(&tail[w], 1u);
+                if (pos < QCAP) q[w][pos] = v; else ovf[w] = 1;
+                const uint32_t ci = P.center_of[v];
+                if (ci != NONE && !enumerate) found[w] = P.clabel[(size_t)ci * P.B + j];
+                break;
+              }
+              if (old == v) break;
+              h = (h + 1) & (HCAP - 1);
+            }
           }
-          if (old == v) break;
-          h = (h + 1) & (HCAP - 1);
+        } else if (e < e1) {
+          ovf[w] = 1;  // queue full with adjacency left
         }
+        __syncwarp();
+        if (ovf[w] || (!enumerate && found[w] != NONE)) break;
       }
       __syncwarp();
+      if (!enumerate && found[w] != NONE) {
+        label = found[w];
+        delta = P.csw[(size_t)label * P.B + j];
+        if (delta == 0 || delta > QCAP) break;
+        // uncovered and small: restart the walk from the queue head to list
+        // every member (the queue already holds the visited part of the CC;
+        // the current vertex's remaining adjacency is rescanned below)
+        enumerate = true;
+        head--;  // re-expand x fully
+        continue;
+      }
       if (ovf[w]) break;
     }
     const uint32_t nvis = min(tail[w], QCAP);

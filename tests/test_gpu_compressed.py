@@ -35,6 +35,8 @@ CASES = [
     (lambda: inputs.random_graph(500, 1500, 46), 0.3, 12, 10, 0),           # alpha = 0: no centers
     (lambda: inputs.path_graph(700), 1.0, 4, 3, 1 << 27),
     (lambda: inputs.random_graph(400, 800, 47), 0.0, 5, 4, 1 << 29),
+    (lambda: inputs.star_graph(5000), 0.5, 6, 3, 1 << 28),                   # hub: queue overflow
+    (lambda: inputs.random_powerlaw_graph(20000, 60000, 49), 0.3, 8, 5, 1 << 24),
 ]
 
 
