@@ -60,7 +60,10 @@ static int guarded(pacim_ctx *ctx, F &&f) {
 
 // Dropping keeps the device buffers as capacity for the next load/build
 // (pc_ensure reuses them); they are released by pacim_destroy.
-static void drop_sketches(pacim_ctx *ctx) { ctx->built = false; }
+static void drop_sketches(pacim_ctx *ctx) {
+  ctx->built = false;
+  ctx->sel_list_valid = false;  // the covered list refers to the old store
+}
 
 static void drop_graph(pacim_ctx *ctx) {
   drop_sketches(ctx);
@@ -75,7 +78,7 @@ static void free_all(pacim_ctx *ctx) {
 
                     &ctx->d_tab, &ctx->gain0,      &ctx->gain,     &ctx->center_of, &ctx->counters,
                     &ctx->scratch, &ctx->scratch2, &ctx->sel_seeds, &ctx->sel_gain,
-                    &ctx->sel_partial, &ctx->sel_list, &ctx->sel_flag};
+                    &ctx->sel_partial, &ctx->sel_list, &ctx->sel_flag, &ctx->argmax_part, &ctx->bfs};
   for (DevBuf *b : bufs) pc_free(ctx, *b);
 }
 
@@ -239,7 +242,8 @@ int pacim_build_sketches(pacim_ctx *ctx, uint32_t R, uint64_t hash_seed, uint64_
     PC_REQUIRE(shard_world >= 1 && shard_rank < shard_world, PACIM_EINVAL,
                "need 0 <= shard_rank < shard_world");
     PC_REQUIRE(shard_rank < R, PACIM_EINVAL, "shard holds no sketch (shard_rank >= R)");
-    ctx->built = false;
+    drop_sketches(ctx);
+
     ctx->R = R;
     ctx->rank = shard_rank;
     ctx->world = shard_world;

@@ -300,104 +300,11 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
   }
 }
 
-// ------------------------------------------------------------ k_compact
-// Tiles of CT_ROWS rows per block.  Pass 1 counts root slots (HIGH) and their
-// sizes, one block scan, two global atomics allocate [ci_base, +cnt) and
-// [mem_base, +size_sum); pass 2 (cache-resident re-read) writes csize[ci],
-// coff[ci] and rewrites the root slot to HIGH | ci.
-constexpr int CT_THREADS = 256;
-constexpr int CT_ROWS = 32;
-
-__device__ __forceinline__ void block_scan2(unsigned long long a, unsigned long long b,
-                                            unsigned long long &ea, unsigned long long &eb,
-                                            unsigned long long &ta, unsigned long long &tb) {
-  __shared__ unsigned long long wa[CT_THREADS / 32], wb[CT_THREADS / 32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  unsigned long long ia = a, ib = b;
-  for (int d = 1; d < 32; d <<= 1) {
-    unsigned long long ya = __shfl_up_sync(0xffffffffu, ia, d);
-    unsigned long long yb = __shfl_up_sync(0xffffffffu, ib, d);
-    if (lane >= d) {
-      ia += ya;
-      ib += yb;
-    }
-  }
-  if (lane == 31) {
-    wa[wid] = ia;
-    wb[wid] = ib;
-  }
-  __syncthreads();
-  unsigned long long pa = 0, pb = 0;
-  ta = tb = 0;
-  for (int w = 0; w < CT_THREADS / 32; w++) {
-    if (w < wid) {
-      pa += wa[w];
-      pb += wb[w];
-    }
-    ta += wa[w];
-    tb += wb[w];
-  }
-  ea = pa + ia - a;
-  eb = pb + ib - b;
-  __syncthreads();
-}
-
-__global__ void __launch_bounds__(CT_THREADS) k_compact(uint32_t *L, uint32_t n, uint32_t B,
-                                                        uint32_t big_t, uint32_t *csize,
-                                                        uint64_t *coff, unsigned long long *ctr) {
-  __shared__ unsigned long long base_c, base_m;
-  const size_t per_tile = (size_t)CT_ROWS * B;
-  const size_t ntiles = ((size_t)n + CT_ROWS - 1) / CT_ROWS;
-  for (size_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const size_t e0 = t * per_tile;
-    const size_t e1 = min(e0 + per_tile, (size_t)n * B);
-    unsigned long long c = 0, msum = 0;
-#pragma unroll 8
-    for (size_t e = e0 + threadIdx.x; e < e1; e += CT_THREADS) {
-      uint32_t s = L[e];
-      if (s & PACIM_HIGH) {
-        uint32_t sz = s & PACIM_LOW;
-        c++;
-        if (sz < big_t) msum += sz;
-      }
-    }
-    unsigned long long ec, em, tc, tm;
-    block_scan2(c, msum, ec, em, tc, tm);
-    if (threadIdx.x == 0) {
-      base_c = tc ? atomicAdd(ctr + 2, tc) : 0;
-      base_m = tm ? atomicAdd(ctr + 3, tm) : 0;
-    }
-    __syncthreads();
-    unsigned long long ci = base_c + ec, mo = base_m + em;
-#pragma unroll 8
-    for (size_t e = e0 + threadIdx.x; e < e1; e += CT_THREADS) {
-      uint32_t s = L[e];
-      if (s & PACIM_HIGH) {
-        uint32_t sz = s & PACIM_LOW;
-        csize[ci] = sz;
-        if (sz < big_t) {
-          coff[ci] = mo;
-          mo += sz;
-        } else {
-          coff[ci] = PACIM_BIG;  // covered by a dense pass, not indexed
-        }
-        L[e] = PACIM_HIGH | (uint32_t)ci;
-        ci++;
-      }
-    }
-    __syncthreads();
-  }
-}
-
-// --------------------------------------------------------- k_gain_scatter
-// Warp per vertex row, lanes over slots (8 slots prefetched per lane).
-// gain0[v] (+)= sum_j |C_j(v)| (H7); v is written into the member range of
-// each of its indexed (non-big) components (H6u).
-__global__ void __launch_bounds__(256) k_gain_scatter(const uint32_t *__restrict__ L, uint32_t n,
-                                                      uint32_t B, const uint32_t *csize,
-                                                      const uint64_t *coff, uint32_t *cfill,
-                                                      uint32_t *perm, int64_t *gain0,
-                                                      const uint32_t *rmap, int accumulate) {
+// ---------------------------------------------------------------- k_gain0
+// Warp per store row, 8 slots prefetched per lane: gain0[v] = sum_j |C_j(v)|
+// (H7), the CC size read from the root slot (HIGH | size).
+__global__ void __launch_bounds__(256) k_gain0(const uint32_t *__restrict__ L, uint32_t n,
+                                               uint32_t B, const uint32_t *rmap, int64_t *gain0) {
   const int lane = threadIdx.x & 31;
   size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
@@ -417,22 +324,15 @@ __global__ void __launch_bounds__(256) k_gain_scatter(const uint32_t *__restrict
         if (s == NONE) continue;
         if (s == (uint32_t)v) {
           g += 1;  // singleton CC
-          continue;
-        }
-        uint32_t ci = (s & PACIM_HIGH) ? (s & PACIM_LOW) : (__ldg(L + (size_t)s * B + j) & PACIM_LOW);
-        g += csize[ci];
-        const uint64_t off = coff[ci];
-        if (off != PACIM_BIG) {
-          uint32_t pos = atomicAdd(cfill + ci, 1u);
-          perm[off + pos] = rmap[v];
+        } else if (s & PACIM_HIGH) {
+          g += s & PACIM_LOW;
+        } else {
+          g += __ldg(L + (size_t)s * B + j) & PACIM_LOW;
         }
       }
     }
     for (int d = 16; d; d >>= 1) g += __shfl_xor_sync(0xffffffffu, g, d);
-    if (lane == 0) {
-      const uint32_t vid = rmap[v];
-      gain0[vid] = accumulate ? gain0[vid] + g : g;
-    }
+    if (lane == 0) gain0[rmap[v]] = g;
   }
 }
 
@@ -546,50 +446,24 @@ void pc_build(pacim_ctx *ctx) {
   const unsigned rows_grid = pc_grid(ctx, (size_t)n * 32, 256, 16);
   PC_CUDA(cudaEventRecord(ev[0], ctx->stream));
   pc_sketch_pass(ctx, L, 0, B, ctr, ev + 1);
-  // component count -> host (sync 1 of 2 per build)
-  unsigned long long hc[2];
-  PC_CUDA(cudaMemcpyAsync(hc, ctr, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                          ctx->stream));
-  PC_CUDA(cudaStreamSynchronize(ctx->stream));
-  ctx->ncomp = hc[0];
-  ctx->nnonsingle = hc[0] + hc[1];
-  PC_REQUIRE(ctx->ncomp < (1ull << 31), PACIM_ENOTIMPL,
-             "more than 2^31 non-singleton components in one store");
-  pc_ensure(ctx, ctx->csize, std::max<size_t>(ctx->ncomp, 1) * 4);
-  pc_ensure(ctx, ctx->csize_work, std::max<size_t>(ctx->ncomp, 1) * 4);
-  pc_ensure(ctx, ctx->coff, std::max<size_t>(ctx->ncomp, 1) * 8);
-  pc_ensure(ctx, ctx->cfill, std::max<size_t>(ctx->ncomp, 1) * 4);
-  PC_CUDA(cudaMemsetAsync(ctx->cfill.p, 0, std::max<size_t>(ctx->ncomp, 1) * 4, ctx->stream));
-  ctx->big_t = std::max<uint32_t>(PACIM_BIG_MIN, n / PACIM_BIG_DIV);
-  if (const char *e = getenv("PACIM_BIG_T")) ctx->big_t = (uint32_t)std::max(2L, atol(e));  // tests
-  k_compact<<<pc_grid(ctx, ((size_t)n + CT_ROWS - 1) / CT_ROWS * CT_THREADS, CT_THREADS, 8),
-              CT_THREADS, 0, ctx->stream>>>(L, n, B, ctx->big_t, ctx->csize.as<uint32_t>(),
-                                            ctx->coff.as<uint64_t>(), ctr);
-  PC_CHECK_LAUNCH();
   PC_CUDA(cudaEventRecord(ev[4], ctx->stream));
-  // indexed member count -> host (sync 2 of 2)
-  unsigned long long hm[4];
-  PC_CUDA(cudaMemcpyAsync(hm, ctr, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
-                          ctx->stream));
-  PC_CUDA(cudaStreamSynchronize(ctx->stream));
-  PC_REQUIRE(hm[2] == ctx->ncomp, PACIM_ECHECK,
-             "compact: component total disagrees with compress_count");
-  ctx->nmember = hm[3];
-  pc_ensure(ctx, ctx->perm, std::max<size_t>(ctx->nmember, 1) * 4);
+  // gain0 (H7): isolated vertices are singletons everywhere (gain B); every
+  // store row sums its CC sizes read from the root slots (HIGH | size)
   k_fill_i64<<<pc_grid(ctx, ctx->n, 256), 256, 0, ctx->stream>>>(ctx->gain0.as<int64_t>(), ctx->n,
                                                                 (int64_t)B);
   PC_CHECK_LAUNCH();
-  k_gain_scatter<<<rows_grid, 256, 0, ctx->stream>>>(
-      L, n, B, ctx->csize.as<uint32_t>(), ctx->coff.as<uint64_t>(), ctx->cfill.as<uint32_t>(),
-      ctx->perm.as<uint32_t>(), ctx->gain0.as<int64_t>(), ctx->rmap.as<uint32_t>(), 0);
+  k_gain0<<<rows_grid, 256, 0, ctx->stream>>>(L, n, B, ctx->rmap.as<uint32_t>(),
+                                             ctx->gain0.as<int64_t>());
   PC_CHECK_LAUNCH();
   PC_CUDA(cudaEventRecord(ev[5], ctx->stream));
-  ctx->launches += 3;  // compact, fill, gain_scatter
-
+  ctx->launches += 2;  // fill, gain0
   unsigned long long h[6];
   PC_CUDA(cudaMemcpyAsync(h, ctr, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                           ctx->stream));
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->ncomp = h[0];
+  ctx->nnonsingle = h[0] + h[1];
+  ctx->nmember = 0;
   ctx->stats.live_pairs = h[4];
   ctx->stats.t_init_ms = ev_ms(ev[0], ev[1]);
   ctx->stats.t_edges_ms = ev_ms(ev[1], ev[2]);

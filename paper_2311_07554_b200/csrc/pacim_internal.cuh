@@ -138,7 +138,11 @@ struct pacim_ctx {
   unsigned long long *h_counters = nullptr;  // pinned host mirror (64)
 
   // selection outputs (device)
-  DevBuf sel_seeds, sel_gain, sel_partial, sel_list, sel_flag;
+  DevBuf sel_seeds, sel_gain, sel_partial, sel_list, sel_flag, argmax_part;
+  DevBuf bfs;                   // multi-slot BFS state of the cover step
+  uint32_t bfs_nr = 0, bfs_bw = 0;  // its layout (rows, bitmap words per row)
+  uint32_t sel_k_cap = 128;     // covered-CC list capacity, in steps
+  bool sel_list_valid = false;  // sel_list holds the covered list of this store
 
   pacim_stats stats{};
   uint32_t launches = 0;

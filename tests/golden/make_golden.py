@@ -65,6 +65,41 @@ def make(name: str):
     print(name, "done", out["oracle_seconds"], flush=True)
 
 
+def make_partial(name: str, sketches):
+    """Full-size configs whose greedy is out of single-thread reach (c4):
+    graph digests plus the canonical labels / CC-size histogram of a few
+    sketches, each by the oracle's BFS labelling."""
+    cfg = inputs.config(name)
+    t0 = time.time()
+    g = O.gen_config(cfg)
+    t_gen = time.time() - t0
+    model, t32 = O.model_args(cfg)
+    hs = cfg["hash_seed"]
+    labels, hist = {}, {}
+    t0 = time.time()
+    for r in sketches:
+        lab, size = O.sketch_labels(g, model, t32, hs, r)
+        labels[str(r)] = sha(lab)
+        roots = lab == np.arange(g.n, dtype=np.uint32)
+        sz = size[roots].astype(np.int64)
+        hist[str(r)] = dict(ncc=int(roots.sum()), nonsingleton=int((size > 1).sum()),
+                            max=int(sz.max()), sum_sq=int((sz * sz).sum()))
+    t_lab = time.time() - t0
+    out = dict(config=name, partial=True,
+               source="oracle/pacim_oracle.c via tests/golden/make_golden.py --partial",
+               n=g.n, m=g.m, model=model, t32=t32, R=cfg["R"], hash_seed=hs,
+               keys_sha256=sha(g.keys), off_sha256=sha(g.off), nbr_sha256=sha(g.nbr),
+               label_sha256=labels, cc_stats=hist,
+               oracle_seconds=dict(generate=round(t_gen, 2), label=round(t_lab, 2)))
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), f"{name}.json")
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
+    print(name, "partial done", out["oracle_seconds"], flush=True)
+
+
 if __name__ == "__main__":
-    for nm in sys.argv[1:]:
-        make(nm)
+    if sys.argv[1] == "--partial":
+        make_partial(sys.argv[2], [int(x) for x in sys.argv[3].split(",")])
+    else:
+        for nm in sys.argv[1:]:
+            make(nm)
