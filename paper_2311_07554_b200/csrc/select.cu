@@ -103,9 +103,10 @@ struct Sel {
   uint32_t *inl;           // [2][rows]: row is in the frontier list
   uint32_t *flist;         // [2][rows] light frontier rows
   uint32_t *hlist;         // [2][rows] heavy frontier rows
-  uint32_t *fcnt;          // [0..2] light sizes by level % 3, [3] touched, [4..6] heavy sizes
-  uint32_t *touched;       // rows visited this step (each once)
-  uint32_t *tflag;         // [rows]: row is in touched
+  uint32_t *fcnt;          // [0..2] light / [4..6] heavy list sizes by level % 3,
+                           // [8 + par] touched count of a step of parity par
+  uint32_t *touched;       // [2][rows]: rows visited in a step of parity par (each once)
+  uint32_t *tflag;         // [rows]: row is in a touched list
   uint64_t heavy_deg;      // rows of higher degree are expanded by the whole grid
   // argmax cache (single rank): marks of step i go to buffer i & 1, consumed
   // by step i + 1 which resets buffer i - 1 (no reset races with a mark)
@@ -120,6 +121,12 @@ __device__ __forceinline__ void mark_dirty(const Sel &S, uint32_t u) {
   const uint32_t c = u >> S.csh;
   if (atomicExch(S.cdirty + c, 1u) == 0u)
     S.dlist[(size_t)S.par * S.nchunks + atomicAdd(S.dcnt + S.par, 1u)] = c;
+}
+
+// remember a row whose visited bits must be cleared before the next step
+__device__ __forceinline__ void touch(const Sel &S, uint32_t row) {
+  if (atomicExch(S.tflag + row, 1u) == 0u)
+    S.touched[(size_t)S.par * S.nr + atomicAdd(S.fcnt + 8 + S.par, 1u)] = row;
 }
 
 __device__ __forceinline__ void sub_gain(const Sel &S, uint32_t u, long long d) {
@@ -149,9 +156,86 @@ __device__ __forceinline__ uint32_t cover_slot(const Sel &S, uint32_t srow, uint
   } else {
     S.dl[j] = delta;
     atomicOr(S.vis + (size_t)srow * S.BW + (j >> 5), 1u << (j & 31));
-    atomicOr(S.fmask + (size_t)srow * S.BW + (j >> 5), 1u << (j & 31));
+    touch(S, srow);
   }
   return delta;
+}
+
+// hand slot j of the seed's small CC to the grid-wide multi-slot BFS
+__device__ __forceinline__ void defer_slot(const Sel &S, uint32_t s, uint32_t srow, uint32_t j) {
+  atomicOr(S.fmask + (size_t)srow * S.BW + (j >> 5), 1u << (j & 31));
+  if (atomicExch(S.inl + srow, 1u) == 0u) {  // level-0 list (parity 0)
+    if (S.off[s + 1] - S.off[s] > S.heavy_deg)
+      S.hlist[atomicAdd(S.fcnt + 4, 1u)] = srow;
+    else
+      S.flist[atomicAdd(S.fcnt + 0, 1u)] = srow;
+  }
+}
+
+// Warp-local BFS of the seed's CC in slot j (<= QCAP vertices) with a
+// shared-memory queue and visited set; applies the gain updates.  Returns
+// false, before updating anything, if it meets a vertex of degree > WARP_DEG
+// (the grid-wide BFS then takes the slot and reads that adjacency once for
+// all slots).
+constexpr uint32_t QCAP = 512;
+constexpr uint32_t HCAP = 1024;
+constexpr uint64_t WARP_DEG = 1024;
+constexpr uint32_t WARP_WORDS = QCAP + HCAP + 1;
+
+// shared-memory words of the slot tables (shr[B] + tab[2^TB + 1] u16), 16-B aligned
+__host__ __device__ __forceinline__ uint32_t table_words(uint32_t B) {
+  return (((uint32_t)B * 4 + ((1u << PACIM_TB) + 1) * 2 + 15) & ~15u) / 4;
+}
+
+__device__ bool warp_bfs(const Sel &S, uint32_t s, uint32_t j, uint32_t delta, uint32_t *q,
+                         uint32_t *hs, uint32_t *tail, const uint32_t *shr) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t hr = shr[j];
+  for (uint32_t i = lane; i < HCAP; i += 32) hs[i] = NONE;
+  __syncwarp();
+  if (lane == 0) {
+    q[0] = s;
+    hs[(s * 2654435761u) & (HCAP - 1)] = s;
+    *tail = 1;
+  }
+  __syncwarp();
+  for (uint32_t head = 0; head < *tail;) {
+    const uint32_t x = q[head++];
+    const uint64_t e0 = S.off[x], e1 = S.off[x + 1];
+    if (e1 - e0 > WARP_DEG) return false;  // uniform: same x in every lane
+    for (uint64_t e = e0 + lane; e < e1; e += 32) {
+      const uint32_t w = S.nbr[e];
+      const uint64_t a = x < w ? x : w, b = x < w ? w : x;
+      const uint32_t he = (uint32_t)(pc_mix64(((a << 32) | b) ^ S.K) >> 32);
+      uint64_t T = S.t32;
+      if (S.wic) {  // R4
+        const uint64_t sd = (e1 - e0) + (S.off[w + 1] - S.off[w]);
+        T = (1ull << 33) / sd;
+        if (T > (1ull << 32)) T = 1ull << 32;
+      }
+      if ((uint64_t)(hr ^ he) >= T) continue;  // R3
+      uint32_t h = (w * 2654435761u) & (HCAP - 1);
+      for (;;) {
+        const uint32_t old = atomicCAS(hs + h, NONE, w);
+        if (old == NONE) {
+          const uint32_t pos = atomicAdd(tail, 1u);
+          if (pos < QCAP) q[pos] = w;
+          break;
+        }
+        if (old == w) break;
+        h = (h + 1) & (HCAP - 1);
+      }
+    }
+    __syncwarp();
+    if (*tail > QCAP) return false;  // cannot happen for a CC of delta <= QCAP
+  }
+  const uint32_t cnt = *tail;
+  for (uint32_t i = lane; i < cnt; i += 32) {
+    const uint32_t u = q[i];
+    if (u != s) sub_gain(S, u, delta);
+  }
+  __syncwarp();
+  return true;
 }
 
 // One BFS level: every frontier row is expanded by one block; its adjacency
@@ -216,7 +300,7 @@ __device__ void expand_row(const Sel &S, uint32_t lvl, uint32_t u, const uint32_
         }
         // a row can enter several levels' lists (reached at different depths
         // in different slots) but is listed for the vis clean-up only once
-        if (atomicExch(S.tflag + wr, 1u) == 0u) S.touched[atomicAdd(S.fcnt + 3, 1u)] = wr;
+        touch(S, wr);
       }
     }
   }
@@ -314,6 +398,9 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(Sel S0, SelOut O) {
   Sel S = S0;
   uint32_t *shr = dsm;
   uint16_t *tab = reinterpret_cast<uint16_t *>(dsm + S.B);
+  // per-warp queue / visited set / tail of warp_bfs, after the tables
+  uint32_t *wbase = dsm + (table_words(S.B)) + (size_t)(threadIdx.x >> 5) * WARP_WORDS;
+  uint32_t *wq = wbase, *whs = wbase + QCAP, *wtail = wbase + QCAP + HCAP;
   __shared__ Best sh[33];
   load_tables(S, shr, tab);
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -344,15 +431,17 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(Sel S0, SelOut O) {
         S.cdirty[c] = 0;
       }
     }
-    {
-      const uint32_t nt = ((volatile uint32_t *)S.fcnt)[3];
-      for (size_t t = tid; t < (size_t)nt * S.BW; t += nth)
-      {
-        const uint32_t r = __ldcg(S.touched + t / S.BW);
+    {  // rows visited by the previous step: clear their visited bits and flags
+      const uint32_t nt = ((volatile uint32_t *)S.fcnt)[8 + prev];
+      for (size_t t = tid; t < (size_t)nt * S.BW; t += nth) {
+        const uint32_t r = __ldcg(S.touched + (size_t)prev * S.nr + t / S.BW);
         S.vis[(size_t)r * S.BW + (t % S.BW)] = 0;
         if (t % S.BW == 0) S.tflag[r] = 0;
       }
     }
+    // level-0/1 list sizes for this step's BFS (nobody reads them before the
+    // barrier; the previous step's loop exit only read zero ones)
+    if (tid == 0) S.fcnt[0] = S.fcnt[1] = S.fcnt[4] = S.fcnt[5] = 0;
     grid.sync();
     // ---- A2: every block reduces the chunk maxima -> s
     Best c{LLONG_MIN, 0xFFFFFFFFu};
@@ -369,31 +458,35 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(Sel S0, SelOut O) {
       S.alldirty[prev] = 0;
       S.dcnt[prev] = 0;
       S.dense[prev] = 0;
-      S.fcnt[3] = 0;  // touched rows: cleared above
+      S.fcnt[8 + prev] = 0;  // the previous step's touched rows were cleared in A1
       O.seeds[step] = s;
       O.arg_gain[step] = c.g;
       S.target[s] = -1;  // s leaves the candidate set (R6)
       mark_dirty(S, s);
-      S.fcnt[0] = S.fcnt[1] = S.fcnt[4] = S.fcnt[5] = 0;
-      if (srow != NONE) {  // BFS starts at the seed's row
-        if (S.off[s + 1] - S.off[s] > S.heavy_deg) {
-          S.hlist[0] = srow;
-          S.fcnt[4] = 1;
-        } else {
-          S.flist[0] = srow;
-          S.fcnt[0] = 1;
-        }
-        S.inl[srow] = 1;
-        S.touched[0] = srow;
-        S.tflag[srow] = 1;
-        S.fcnt[3] = 1;
-      }
     }
-    // ---- B: MarkSeed, one thread per slot
-    unsigned long long dsum = 0;
-    for (size_t j = tid; j < S.B; j += nth) dsum += cover_slot(S, srow, (uint32_t)j);
-    for (int d = 16; d; d >>= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, d);
-    if ((threadIdx.x & 31) == 0 && dsum) atomicAdd((unsigned long long *)&O.gain_num[step], dsum);
+    // ---- B: MarkSeed, one warp per slot; small newly covered CCs are
+    //          enumerated right here by the warp (warp_bfs) unless they are
+    //          larger than its queue or reach a high-degree vertex, which
+    //          defers them to the grid-wide BFS below
+    {
+      const int lane = threadIdx.x & 31;
+      unsigned long long dsum = 0;
+      for (size_t j = gwarp; j < S.B; j += nwarps) {
+        uint32_t d = 0;
+        if (lane == 0) d = cover_slot(S, srow, (uint32_t)j);
+        d = __shfl_sync(0xffffffffu, d, 0);
+        __syncwarp();
+        dsum += d;
+        const uint32_t small = __shfl_sync(0xffffffffu, lane == 0 ? __ldcg(S.dl + j) : 0u, 0);
+        if (small) {
+          bool done = false;
+          if (small <= QCAP) done = warp_bfs(S, s, (uint32_t)j, small, wq, whs, wtail, shr);
+          if (!done && lane == 0) defer_slot(S, s, srow, (uint32_t)j);
+          __syncwarp();
+        }
+      }
+      if (lane == 0 && dsum) atomicAdd((unsigned long long *)&O.gain_num[step], dsum);
+    }
     grid.sync();
     // ---- C1: multi-slot BFS over the small newly covered CCs
     for (uint32_t lvl = 0;; lvl++) {
@@ -423,8 +516,10 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(Sel S0, SelOut O) {
 __global__ void k_cover_slots(Sel S, uint32_t s, unsigned long long *sum) {
   const uint32_t srow = S.cid[s];
   unsigned long long d = 0;
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < S.B; j += gridDim.x * blockDim.x)
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < S.B; j += gridDim.x * blockDim.x) {
     d += cover_slot(S, srow, j);
+    if (S.dl[j]) defer_slot(S, s, srow, j);  // all small CCs: grid BFS
+  }
   if (d) atomicAdd(sum, d);
 }
 
@@ -447,8 +542,8 @@ __global__ void k_clear_heavy(Sel S, uint32_t lvl) {
               (uint64_t)gridDim.x * blockDim.x);
 }
 
-__global__ void k_clear_touched(Sel S) {
-  const uint32_t nt = S.fcnt[3];
+__global__ void k_clear_touched(Sel S) {  // multi-rank calls use parity 0
+  const uint32_t nt = S.fcnt[8];
   for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < (size_t)nt * S.BW;
        t += (size_t)gridDim.x * blockDim.x)
   {
@@ -548,8 +643,8 @@ static Sel make_sel(pacim_ctx *ctx, long long *target) {
   S.alldirty = reinterpret_cast<int *>(S.dcnt + 2);
   // BFS state: vis, fmask[2], inl[2], flist[2], touched, fcnt[3]
   const size_t bw = (size_t)nr * S.BW;
-  // words: vis, fmask[2], inl[2], flist[2], hlist[2], touched, fcnt[8]
-  const size_t words = 3 * bw + 8 * (size_t)nr + 8;
+  // words: vis, fmask[2], inl[2], flist[2], hlist[2], touched[2], tflag, fcnt[16]
+  const size_t words = 3 * bw + 9 * (size_t)nr + 16;
   if (ctx->bfs.bytes < words * 4 || ctx->bfs_nr != nr || ctx->bfs_bw != S.BW) {
     // new layout: every mask, flag and counter starts at zero
     pc_ensure(ctx, ctx->bfs, words * 4);
@@ -564,7 +659,7 @@ static Sel make_sel(pacim_ctx *ctx, long long *target) {
   S.flist = S.inl + 2 * (size_t)nr;
   S.hlist = S.flist + 2 * (size_t)nr;
   S.touched = S.hlist + 2 * (size_t)nr;
-  S.tflag = S.touched + nr;
+  S.tflag = S.touched + 2 * (size_t)nr;
   S.fcnt = S.tflag + nr;
   S.heavy_deg = 4096;
   S.par = 0;
@@ -587,7 +682,7 @@ static void uncover(pacim_ctx *ctx, const Sel &S) {
   PC_CUDA(cudaMemsetAsync(S.cov_root, 0xFF, (size_t)S.B * 4, ctx->stream));
   PC_CUDA(cudaMemsetAsync(S.vis, 0, (size_t)S.nr * S.BW * 4, ctx->stream));
   PC_CUDA(cudaMemsetAsync(S.tflag, 0, (size_t)S.nr * 4, ctx->stream));
-  PC_CUDA(cudaMemsetAsync(S.fcnt, 0, 32, ctx->stream));
+  PC_CUDA(cudaMemsetAsync(S.fcnt, 0, 64, ctx->stream));
   ctx->sel_list_valid = true;
 }
 
@@ -620,7 +715,8 @@ void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
   O.gain_num = ctx->sel_gain.as<long long>();
   O.arg_gain = O.gain_num + k;
   O.levels = reinterpret_cast<unsigned long long *>(O.gain_num + 2 * k);
-  const size_t smem = table_smem(S.B);
+  const size_t smem = (size_t)table_words(S.B) * 4 + (SEL_THREADS / 32) * WARP_WORDS * 4;
+  PC_REQUIRE(smem <= 200 * 1024, PACIM_ENOTIMPL, "too many sketch slots for k_select");
   PC_CUDA(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int occ = 0;
   PC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_select, SEL_THREADS, smem));
@@ -674,24 +770,9 @@ void pc_cover_local(pacim_ctx *ctx, uint32_t s, int64_t *d_delta, int64_t *local
   PC_CUDA(cudaMemsetAsync(S.dense, 0, 8, ctx->stream));
   // previous call's visited rows, then the seed's row as the BFS start
   k_clear_touched<<<pc_grid(ctx, (size_t)S.nr, 256), 256, 0, ctx->stream>>>(S);
-  uint32_t srow = NONE;
-  PC_CUDA(cudaMemcpyAsync(&srow, S.cid + s, 4, cudaMemcpyDeviceToHost, ctx->stream));
-  PC_CUDA(cudaStreamSynchronize(ctx->stream));
-  uint64_t so[2] = {0, 0};
-  PC_CUDA(cudaMemcpyAsync(so, S.off + s, 16, cudaMemcpyDeviceToHost, ctx->stream));
-  PC_CUDA(cudaStreamSynchronize(ctx->stream));
-  const bool heavy = so[1] - so[0] > S.heavy_deg;
-  const uint32_t has = srow != NONE ? 1u : 0u;
-  uint32_t init[7] = {heavy ? 0u : has, 0u, 0u, has, heavy ? has : 0u, 0u, 0u};
-  PC_CUDA(cudaMemcpyAsync(S.fcnt, init, 28, cudaMemcpyHostToDevice, ctx->stream));
-  if (srow != NONE) {
-    const uint32_t one = 1;
-    PC_CUDA(cudaMemcpyAsync(heavy ? S.hlist : S.flist, &srow, 4, cudaMemcpyHostToDevice,
-                            ctx->stream));
-    PC_CUDA(cudaMemcpyAsync(S.touched, &srow, 4, cudaMemcpyHostToDevice, ctx->stream));
-    PC_CUDA(cudaMemcpyAsync(S.tflag + srow, &one, 4, cudaMemcpyHostToDevice, ctx->stream));
-    PC_CUDA(cudaMemcpyAsync(S.inl + srow, &one, 4, cudaMemcpyHostToDevice, ctx->stream));
-  }
+  // list and touched counters start empty; k_cover_slots defers the small
+  // CCs (seed row into the level-0 list) and records touched rows
+  PC_CUDA(cudaMemsetAsync(S.fcnt, 0, 64, ctx->stream));
   k_cover_slots<<<(S.B + 255) / 256, 256, 0, ctx->stream>>>(S, s, sum);
   PC_CHECK_LAUNCH();
   const size_t smem = table_smem(S.B);
