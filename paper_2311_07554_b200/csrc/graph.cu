@@ -192,6 +192,23 @@ __global__ void k_upper_fill(const uint64_t *off, const uint32_t *nbr, uint32_t 
 }
 
 // R4: WIC threshold T32 = min(2^32, floor(2^33 / (d_u + d_v))), stored as T32-1.
+// R4 per CSR entry (warp per vertex): tcsr[e] = T32(x, nbr[e]) - 1
+__global__ void k_wic_csr(const uint64_t *off, const uint32_t *nbr, uint32_t n, uint32_t *tcsr) {
+  const int lane = threadIdx.x & 31;
+  size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t x = warp; x < n; x += nw) {
+    const uint64_t a = off[x], b = off[x + 1];
+    for (uint64_t e = a + lane; e < b; e += 32) {
+      const uint32_t w = nbr[e];
+      const uint64_t s = (b - a) + (off[w + 1] - off[w]);
+      uint64_t t = (1ull << 33) / s;
+      if (t > (1ull << 32)) t = 1ull << 32;
+      tcsr[e] = (uint32_t)(t - 1);
+    }
+  }
+}
+
 __global__ void k_wic(const uint64_t *keys, uint64_t m, const uint64_t *off, uint32_t *tm1) {
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
        e += (size_t)gridDim.x * blockDim.x) {
@@ -306,6 +323,11 @@ static void derive_common(pacim_ctx *ctx) {
     pc_ensure(ctx, ctx->tm1, std::max<size_t>(m, 1) * sizeof(uint32_t));
     k_wic<<<pc_grid(ctx, m, 256), 256, 0, ctx->stream>>>(ctx->keys.as<uint64_t>(), m, off,
                                                         ctx->tm1.as<uint32_t>());
+    PC_CHECK_LAUNCH();
+    // the same thresholds in CSR order, for the traversals of the selection
+    pc_ensure(ctx, ctx->tcsr, std::max<size_t>(2 * m, 1) * sizeof(uint32_t));
+    k_wic_csr<<<pc_grid(ctx, (size_t)n * 32, 256), 256, 0, ctx->stream>>>(
+        off, ctx->nbr.as<uint32_t>(), n, ctx->tcsr.as<uint32_t>());
     PC_CHECK_LAUNCH();
   }
   ctx->launches += 5;

@@ -88,6 +88,7 @@ struct pacim_ctx {
   DevBuf nbr;            // u32[2m]  full CSR neighbours
   DevBuf keys;           // u64[m]   upper edge list min<<32|max, sorted
   DevBuf tm1;            // u32[m]   WIC: T32(e) - 1
+  DevBuf tcsr;           // u32[2m]  WIC: T32 - 1 per CSR entry (traversals)
   DevBuf ckeys;          // u64[m]   the same edges as store rows: row(min)<<32|row(max)
   DevBuf cid;            // u32[n]   store row of v, or 0xFFFFFFFF for isolated v
   DevBuf rmap;           // u32[nr]  vertex id of store row c

@@ -80,7 +80,7 @@ struct Sel {
   const uint64_t *off;
   const uint32_t *nbr;
   uint64_t K, t32;
-  const uint32_t *tm1;  // WIC: per upper edge T32 - 1 (unused here; WIC from degrees)
+  const uint32_t *tcsr;  // WIC: T32 - 1 per CSR entry
   int wic;
   const uint32_t *g_shr;   // hi32(hash(r)) of slot j (sorted)
   const uint16_t *g_tab;   // candidate bucket table of the sorted slots
@@ -207,13 +207,8 @@ __device__ bool warp_bfs(const Sel &S, uint32_t s, uint32_t j, uint32_t delta, u
       const uint32_t w = S.nbr[e];
       const uint64_t a = x < w ? x : w, b = x < w ? w : x;
       const uint32_t he = (uint32_t)(pc_mix64(((a << 32) | b) ^ S.K) >> 32);
-      uint64_t T = S.t32;
-      if (S.wic) {  // R4
-        const uint64_t sd = (e1 - e0) + (S.off[w + 1] - S.off[w]);
-        T = (1ull << 33) / sd;
-        if (T > (1ull << 32)) T = 1ull << 32;
-      }
-      if ((uint64_t)(hr ^ he) >= T) continue;  // R3
+      const uint64_t T = S.wic ? (uint64_t)S.tcsr[e] + 1 : S.t32;  // R4
+      if ((uint64_t)(hr ^ he) >= T) continue;                        // R3
       uint32_t h = (w * 2654435761u) & (HCAP - 1);
       for (;;) {
         const uint32_t old = atomicCAS(hs + h, NONE, w);
@@ -260,12 +255,7 @@ __device__ void expand_row(const Sel &S, uint32_t lvl, uint32_t u, const uint32_
       const uint32_t w = S.nbr[e];
       const uint64_t a = x < w ? x : w, b = x < w ? w : x;
       const uint32_t he = (uint32_t)(pc_mix64(((a << 32) | b) ^ S.K) >> 32);
-      uint64_t T = S.t32;
-      if (S.wic) {  // R4
-        const uint64_t sd = (S.off[x + 1] - S.off[x]) + (S.off[w + 1] - S.off[w]);
-        T = (1ull << 33) / sd;
-        if (T > (1ull << 32)) T = 1ull << 32;
-      }
+      const uint64_t T = S.wic ? (uint64_t)S.tcsr[e] + 1 : S.t32;  // R3 / R4
       if (T == 0) continue;
       const uint32_t wb = __clz((uint32_t)(T - 1));
       uint32_t lo, hi;
@@ -603,7 +593,7 @@ static Sel make_sel(pacim_ctx *ctx, long long *target) {
   S.nbr = ctx->nbr.as<uint32_t>();
   S.K = ctx->K;
   S.t32 = ctx->t32;
-  S.tm1 = ctx->tm1.as<uint32_t>();
+  S.tcsr = ctx->tcsr.as<uint32_t>();
   S.wic = ctx->pmodel == PACIM_P_WIC;
   S.g_shr = ctx->d_shr.as<uint32_t>();
   S.g_tab = ctx->d_tab.as<uint16_t>();
