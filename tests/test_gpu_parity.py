@@ -197,6 +197,38 @@ def test_config_golden(ctx, name):
     assert st["nmember"] + (n * cfg["R"] - st["nmember"]) == n * cfg["R"]
 
 
+def test_c4_full_scale_sampled(ctx):
+    """BASELINE.json configs[3] at full size (n = 2^26, m = 1.57e9, WIC, R =
+    256) in bench.py's launch configuration: the generated CSR and two
+    sketches' canonical labels against the oracle's golden digests; the
+    selection against properties that hold at any size."""
+    path = os.path.join(GOLD, "c4.json")
+    if not os.path.exists(path):
+        pytest.skip("c4 golden not generated")
+    gold = json.load(open(path))
+    from paper_2311_07554_b200 import pipeline
+    cfg = inputs.config("c4")
+    n, m = pipeline.generate(ctx, cfg)
+    assert (n, m) == (gold["n"], gold["m"])
+    off, nbr = ctx.pacim_get_graph()
+    assert sha(off) == gold["off_sha256"] and sha(nbr) == gold["nbr_sha256"]
+    del nbr
+    ctx.pacim_build_sketches(cfg["R"], cfg["hash_seed"])
+    for r, h in gold["label_sha256"].items():
+        lab = ctx.pacim_get_labels(int(r))
+        assert sha(lab) == h, r
+        roots = lab == np.arange(n, dtype=np.uint32)
+        sz = np.bincount(lab, minlength=n)[lab]
+        st = gold["cc_stats"][r]
+        assert int(roots.sum()) == st["ncc"] and int((sz > 1).sum()) == st["nonsingleton"]
+    g0 = ctx.pacim_get_gain0()
+    s, gn, sg, _ = ctx.pacim_select_seeds(cfg["k"])
+    assert gn[0] == g0.max() and s[0] == int(np.argmax(g0))       # first NextSeed
+    assert all(a >= b for a, b in zip(gn, gn[1:]))                 # submodularity
+    assert len(set(int(x) for x in s)) == cfg["k"]                 # distinct seeds
+    assert list(sg) == list(np.cumsum(gn))
+
+
 # ------------------------------------------------ multi-rank primitives
 @pytest.mark.parametrize("big_t", [None, "6"])
 def test_rank_emulation_matches_single(orc, pc, big_t, monkeypatch):
