@@ -81,6 +81,13 @@ typedef struct {
     uint32_t rows;                  /* store rows = non-isolated vertices (isolated
                                        vertices are singletons in every sketch) */
     uint64_t nnonsingle;            /* (vertex, sketch) pairs in non-singleton CCs */
+    /* cover-step diagnostics of the last select (uncompressed store) */
+    uint64_t select_dense_steps;    /* steps that ran the dense pass (big CCs) */
+    uint64_t select_warp_slots;     /* (step, slot) CCs enumerated by a warp-local BFS */
+    uint64_t select_deferred_slots; /* (step, slot) CCs handed to the shared traversal */
+    uint64_t select_row_items;      /* row expansions of the shared traversal */
+    uint64_t select_chunk_items;    /* chunk items (CH-edge slices of long rows) */
+    uint64_t select_inline_rows;    /* rows expanded without queueing (queue guard) */
 } pacim_stats;
 
 /* --------------------------------------------------------------- lifecycle */

@@ -43,6 +43,9 @@ class Stats(C.Structure):
         ("device_bytes", C.c_uint64), ("select_member_updates", C.c_uint64),
         ("select_bfs_visits", C.c_uint64), ("kernel_launches_build", C.c_uint32),
         ("kernel_launches_select", C.c_uint32), ("rows", C.c_uint32), ("nnonsingle", C.c_uint64),
+        ("select_dense_steps", C.c_uint64), ("select_warp_slots", C.c_uint64),
+        ("select_deferred_slots", C.c_uint64), ("select_row_items", C.c_uint64),
+        ("select_chunk_items", C.c_uint64), ("select_inline_rows", C.c_uint64),
     ]
 
     def asdict(self):

@@ -62,6 +62,7 @@ static int guarded(pacim_ctx *ctx, F &&f) {
 // (pc_ensure reuses them); they are released by pacim_destroy.
 static void drop_sketches(pacim_ctx *ctx) {
   ctx->built = false;
+  ctx->hla_ok = false;
   ctx->sel_list_valid = false;  // the covered list refers to the old store
 }
 
@@ -78,7 +79,7 @@ static void free_all(pacim_ctx *ctx) {
 
                     &ctx->d_tab, &ctx->gain0,      &ctx->gain,     &ctx->center_of, &ctx->counters,
                     &ctx->scratch, &ctx->scratch2, &ctx->sel_seeds, &ctx->sel_gain,
-                    &ctx->sel_partial, &ctx->sel_list, &ctx->sel_flag, &ctx->argmax_part, &ctx->bfs, &ctx->tcsr};
+                    &ctx->sel_partial, &ctx->sel_list, &ctx->sel_flag, &ctx->argmax_part, &ctx->bfs, &ctx->tcsr, &ctx->hidx, &ctx->hla_off, &ctx->hla_row, &ctx->hla_raw};
   for (DevBuf *b : bufs) pc_free(ctx, *b);
 }
 

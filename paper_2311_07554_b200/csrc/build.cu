@@ -94,8 +94,8 @@ __device__ __forceinline__ void uf_unite(uint32_t *L, uint32_t B, uint32_t j, ui
 constexpr int EDGE_THREADS = 256;
 constexpr int EDGE_WARPS = EDGE_THREADS / 32;
 
-template <bool WIC>
-__global__ void __launch_bounds__(EDGE_THREADS) k_edges(const uint64_t *__restrict__ keys,
+template <bool WIC, bool REC>
+__global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__restrict__ keys,
                                                         const uint64_t *__restrict__ ckeys,
                                                         const uint32_t *__restrict__ tm1,
                                                         uint64_t m, uint64_t K, uint64_t t32,
@@ -103,7 +103,7 @@ __global__ void __launch_bounds__(EDGE_THREADS) k_edges(const uint64_t *__restri
                                                         const uint16_t *__restrict__ g_tab,
                                                         uint32_t B, uint32_t j0, uint32_t Bb,
                                                         uint32_t *L,
-                                                        unsigned long long *live_ctr) {
+                                                        unsigned long long *live_ctr, Hla hla) {
   // slots [j0, j0 + Bb) of the B sorted slots go to L (row stride Bb)
   extern __shared__ uint32_t sm[];
   uint32_t *shr = sm;
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(EDGE_THREADS) k_edges(const uint64_t *__restri
       hi = min(hi, j0 + Bb);
       if (hi < lo) hi = lo;
       cnt = hi - lo;
-      const uint64_t ck = ckeys[e];  // the endpoints' store rows
+      const uint64_t ck = ckeys[e];  // the endpoints' store rows (+ hub flags)
       w_u[wid][lane] = (uint32_t)(ck >> 32);
       w_v[wid][lane] = (uint32_t)ck;
       w_he[wid][lane] = he;
@@ -167,19 +167,26 @@ __global__ void __launch_bounds__(EDGE_THREADS) k_edges(const uint64_t *__restri
     // ---- 32 (edge, slot) candidate pairs per round
     for (uint32_t c0 = 0; c0 < total; c0 += 32) {
       const uint32_t idx = c0 + lane;
+      uint32_t j = 0, u = 0, v = 0;
+      bool lv = false;
       if (idx < total) {
         uint32_t a = 0, b = 32;  // largest i with pre[i] <= idx
         while (b - a > 1) {
           uint32_t mid = (a + b) >> 1;
           if (w_pre[wid][mid] <= idx) a = mid; else b = mid;
         }
-        const uint32_t j = w_lo[wid][a] + (idx - w_pre[wid][a]);
-        if ((uint64_t)(shr[j] ^ w_he[wid][a]) < w_T[wid][a]) {
-          uf_unite(L, Bb, j - j0, w_u[wid][a], w_v[wid][a]);
-
+        j = w_lo[wid][a] + (idx - w_pre[wid][a]);
+        lv = (uint64_t)(shr[j] ^ w_he[wid][a]) < w_T[wid][a];
+        u = w_u[wid][a];
+        v = w_v[wid][a];
+        if (lv) {
+          uf_unite(L, Bb, j - j0, u & ~PACIM_HUBF, v & ~PACIM_HUBF);
           live++;
         }
       }
+      if (REC)  // live edges of hubs, appended with one counter update per warp
+        hla.add_warp(u & ~PACIM_HUBF, v & ~PACIM_HUBF, j, (lv && (u & PACIM_HUBF)) ? 1u : 0u,
+                     (lv && (v & PACIM_HUBF)) ? 1u : 0u);
     }
     __syncwarp();
   }
@@ -336,6 +343,16 @@ __global__ void __launch_bounds__(256) k_gain0(const uint32_t *__restrict__ L, u
   }
 }
 
+// HLA: raw entries -> rows grouped by (hub, slot); cur = a copy of the offsets
+__global__ void k_hla_scatter(const unsigned long long *raw, unsigned long long n,
+                              unsigned long long *cur, uint32_t *rows) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const unsigned long long r = raw[i];
+    rows[atomicAdd(cur + (r >> 32), 1ull)] = (uint32_t)r;
+  }
+}
+
 // isolated vertices are singletons in every sketch: gain0 = B
 __global__ void k_fill_i64(int64_t *a, uint32_t n, int64_t x) {
   for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
@@ -391,7 +408,9 @@ void pc_slot_table(pacim_ctx *ctx) {
 // ctr[0] += non-singleton CCs, ctr[1] += non-roots, ctr[4] += live pairs.
 // ev (optional, 3 events) is recorded after init, edges and compress.
 void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
-                    unsigned long long *ctr, cudaEvent_t *ev) {
+                    unsigned long long *ctr, cudaEvent_t *ev, const Hla *hla_in) {
+  Hla hla{};
+  if (hla_in) hla = *hla_in;
   const uint32_t n = ctx->nr, B = ctx->R_local;
   const uint32_t NT = 1u << PACIM_TB;
   pc_ensure(ctx, ctx->d_hot, 2 * (size_t)B * sizeof(uint32_t));
@@ -405,17 +424,17 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
     size_t smem = B * sizeof(uint32_t) + (NT + 1) * sizeof(uint16_t);
     unsigned g = pc_grid(ctx, (ctx->m + 31) / 32 * 32, EDGE_THREADS, 8);
     if (ctx->pmodel == PACIM_P_WIC) {
-      PC_CUDA(cudaFuncSetAttribute(k_edges<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-      k_edges<true><<<g, EDGE_THREADS, smem, ctx->stream>>>(
+      auto kern = hla.cnt ? k_edges<true, true> : k_edges<true, false>;
+      PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
           ctx->keys.as<uint64_t>(), ctx->ckeys.as<uint64_t>(), ctx->tm1.as<uint32_t>(), ctx->m,
-          ctx->K, 0, ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4);
+          ctx->K, 0, ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla);
     } else {
-      PC_CUDA(cudaFuncSetAttribute(k_edges<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
-      k_edges<false><<<g, EDGE_THREADS, smem, ctx->stream>>>(
+      auto kern = hla.cnt ? k_edges<false, true> : k_edges<false, false>;
+      PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
           ctx->keys.as<uint64_t>(), ctx->ckeys.as<uint64_t>(), nullptr, ctx->m, ctx->K, ctx->t32,
-          ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4);
+          ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla);
     }
     PC_CHECK_LAUNCH();
   }
@@ -444,8 +463,28 @@ void pc_build(pacim_ctx *ctx) {
   for (auto &e : ev) PC_CUDA(cudaEventCreate(&e));
   ctx->launches = 0;
   const unsigned rows_grid = pc_grid(ctx, (size_t)n * 32, 256, 16);
+  // live hub adjacency (HLA) of the hub rows: opt-in (PACIM_HLA=1): on c4 recording costs more build time than the
+  // selection saves (its traversal is bound by hop latency, not edge work)
+  const bool want_hla = ctx->nhub > 0 && (getenv("PACIM_HLA") != nullptr ||
+                                          getenv("PACIM_FORCE_HLA") != nullptr);
+  ctx->hla_ok = false;
+  Hla hla{};
+  if (want_hla) {
+    const size_t keys = (size_t)ctx->nhub * B + 1;
+    const unsigned long long cap = std::max<unsigned long long>(1ull << 20, (ctx->m / 16));
+    pc_ensure(ctx, ctx->hla_off, keys * 8);
+    pc_ensure(ctx, ctx->hla_raw, (cap + 1) * 8);
+    PC_CUDA(cudaMemsetAsync(ctx->hla_off.p, 0, keys * 8, ctx->stream));
+    PC_CUDA(cudaMemsetAsync(ctx->hla_raw.p, 0, 8, ctx->stream));
+    hla.hidx = ctx->hidx.as<uint32_t>();
+    hla.cnt = ctx->hla_off.as<unsigned long long>();
+    hla.n = ctx->hla_raw.as<unsigned long long>();
+    hla.raw = hla.n + 1;
+    hla.cap = cap;
+    hla.B = B;
+  }
   PC_CUDA(cudaEventRecord(ev[0], ctx->stream));
-  pc_sketch_pass(ctx, L, 0, B, ctr, ev + 1);
+  pc_sketch_pass(ctx, L, 0, B, ctr, ev + 1, want_hla ? &hla : nullptr);
   PC_CUDA(cudaEventRecord(ev[4], ctx->stream));
   // gain0 (H7): isolated vertices are singletons everywhere (gain B); every
   // store row sums its CC sizes read from the root slots (HIGH | size)
@@ -455,6 +494,27 @@ void pc_build(pacim_ctx *ctx) {
   k_gain0<<<rows_grid, 256, 0, ctx->stream>>>(L, n, B, ctx->rmap.as<uint32_t>(),
                                              ctx->gain0.as<int64_t>());
   PC_CHECK_LAUNCH();
+  if (want_hla) {
+    // counts -> offsets (in place via scratch), then rows grouped by key
+    const size_t keys = (size_t)ctx->nhub * B + 1;
+    unsigned long long nraw = 0;
+    PC_CUDA(cudaMemcpyAsync(&nraw, hla.n, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (nraw <= hla.cap) {
+      TmpBuf cur(ctx);
+      pc_ensure(ctx, cur, keys * 8);
+      pc_exclusive_scan_u64(ctx, reinterpret_cast<const uint64_t *>(hla.cnt), cur.as<uint64_t>(), keys);
+      PC_CUDA(cudaMemcpyAsync(hla.cnt, cur.p, keys * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+      pc_ensure(ctx, ctx->hla_row, std::max<size_t>(nraw, 1) * 4);
+      k_hla_scatter<<<pc_grid(ctx, nraw, 256), 256, 0, ctx->stream>>>(
+          hla.raw, nraw, cur.as<unsigned long long>(), ctx->hla_row.as<uint32_t>());
+      PC_CHECK_LAUNCH();
+      PC_CUDA(cudaStreamSynchronize(ctx->stream));
+      ctx->hla_ok = true;
+      ctx->hla_n = nraw;
+      ctx->launches += 2;
+    }
+  }
   PC_CUDA(cudaEventRecord(ev[5], ctx->stream));
   ctx->launches += 2;  // fill, gain0
   unsigned long long h[6];

@@ -5,6 +5,8 @@
 // timed build/select step); every other kernel here is hand-written.
 #include <cub/cub.cuh>
 
+#include <cstdlib>
+
 #include "pacim_internal.cuh"
 
 // ------------------------------------------------------------------- scan
@@ -261,11 +263,25 @@ __global__ void k_rowmap(const uint64_t *flag, const uint64_t *pos, uint32_t n, 
   }
 }
 
-__global__ void k_ckeys(const uint64_t *keys, uint64_t m, const uint32_t *cid, uint64_t *ckeys) {
+__global__ void k_ckeys(const uint64_t *keys, uint64_t m, const uint32_t *cid, const uint32_t *hidx,
+                        uint64_t *ckeys) {
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
        e += (size_t)gridDim.x * blockDim.x) {
     uint64_t k = keys[e];
-    ckeys[e] = ((uint64_t)cid[k >> 32] << 32) | cid[k & 0xFFFFFFFFull];
+    uint32_t a = cid[k >> 32], b = cid[k & 0xFFFFFFFFull];
+    if (hidx[a] != 0xFFFFFFFFu) a |= PACIM_HUBF;
+    if (hidx[b] != 0xFFFFFFFFu) b |= PACIM_HUBF;
+    ckeys[e] = ((uint64_t)a << 32) | b;
+  }
+}
+
+// hub index of the store rows: degree > hub_deg
+__global__ void k_hub_index(const uint64_t *off, const uint32_t *rmap, uint32_t nr,
+                            uint64_t hub_deg, uint32_t *hidx, unsigned long long *cnt) {
+  for (size_t u = (size_t)blockIdx.x * blockDim.x + threadIdx.x; u < nr;
+       u += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t x = rmap[u];
+    hidx[u] = off[x + 1] - off[x] > hub_deg ? (uint32_t)atomicAdd(cnt, 1ull) : 0xFFFFFFFFu;
   }
 }
 }  // namespace
@@ -314,9 +330,24 @@ static void derive_common(pacim_ctx *ctx) {
                             cudaMemcpyDeviceToHost, ctx->stream));
     PC_CUDA(cudaStreamSynchronize(ctx->stream));
   }
+  {
+    // hub rows (degree > hub_deg): their live edges are recorded by the build
+    if (const char *e = getenv("PACIM_HUB_DEG")) ctx->hub_deg = (uint64_t)std::max(1LL, atoll(e));
+    pc_ensure(ctx, ctx->hidx, std::max<size_t>(ctx->nr, 1) * 4);
+    unsigned long long *t = ctx->counters.as<unsigned long long>();
+    PC_CUDA(cudaMemsetAsync(t, 0, 8, ctx->stream));
+    k_hub_index<<<pc_grid(ctx, ctx->nr, 256), 256, 0, ctx->stream>>>(
+        off, ctx->rmap.as<uint32_t>(), ctx->nr, ctx->hub_deg, ctx->hidx.as<uint32_t>(), t);
+    PC_CHECK_LAUNCH();
+    unsigned long long h = 0;
+    PC_CUDA(cudaMemcpyAsync(&h, t, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->nhub = (uint32_t)h;
+  }
   pc_ensure(ctx, ctx->ckeys, std::max<size_t>(m, 1) * 8);
   k_ckeys<<<pc_grid(ctx, m, 256), 256, 0, ctx->stream>>>(ctx->keys.as<uint64_t>(), m,
                                                         ctx->cid.as<uint32_t>(),
+                                                        ctx->hidx.as<uint32_t>(),
                                                         ctx->ckeys.as<uint64_t>());
   PC_CHECK_LAUNCH();
   if (ctx->pmodel == PACIM_P_WIC) {

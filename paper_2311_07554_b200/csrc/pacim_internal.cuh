@@ -23,6 +23,7 @@
 #define PACIM_HIGH 0x80000000u
 #define PACIM_LOW 0x7FFFFFFFu
 #define PACIM_TB 12  // bits of the sketch bucket table (R2 candidate enumeration)
+#define PACIM_HUBF 0x80000000u  // hub flag of a row in ckeys
 // Components of at least max(PACIM_BIG_MIN, n / PACIM_BIG_DIV) vertices are
 // not put in the member index; MarkSeed covers them with one dense pass over
 // the store (coff = PACIM_BIG marks them).
@@ -89,11 +90,25 @@ struct pacim_ctx {
   DevBuf keys;           // u64[m]   upper edge list min<<32|max, sorted
   DevBuf tm1;            // u32[m]   WIC: T32(e) - 1
   DevBuf tcsr;           // u32[2m]  WIC: T32 - 1 per CSR entry (traversals)
-  DevBuf ckeys;          // u64[m]   the same edges as store rows: row(min)<<32|row(max)
+  DevBuf ckeys;          // u64[m]   the same edges as store rows: row(min)<<32|row(max);
+                         //          bit 31 of a half flags a hub row (PACIM_HUBF)
   DevBuf cid;            // u32[n]   store row of v, or 0xFFFFFFFF for isolated v
   DevBuf rmap;           // u32[nr]  vertex id of store row c
   uint32_t nr = 0;       // store rows = non-isolated vertices (order kept)
   uint32_t hub_row = 0xFFFFFFFFu;  // store row of the hub vertex
+
+  // hub rows (degree > hub_deg): index per row and the live hub adjacency of
+  // the last build (HLA: per (hub, slot) the rows joined to the hub by a live
+  // edge), used by the cover traversal instead of hashing the
+  // hub's whole adjacency
+  uint64_t hub_deg = 2048;
+  uint32_t nhub = 0;
+  DevBuf hidx;           // u32[nr] hub index of a row or 0xFFFFFFFF
+  bool hla_ok = false;   // HLA built for the current store
+  uint64_t hla_n = 0;    // live (hub, slot, row) entries
+  DevBuf hla_off;        // u64[nhub * B + 1] segment offsets by (hub, slot)
+  DevBuf hla_row;        // u32[hla_n] the other rows
+  DevBuf hla_raw;        // u64 scratch: unsorted (key << 32 | row)
 
   // ---- sketches
   bool built = false;
@@ -140,8 +155,10 @@ struct pacim_ctx {
 
   // selection outputs (device)
   DevBuf sel_seeds, sel_gain, sel_partial, sel_list, sel_flag, argmax_part;
-  DevBuf bfs;                   // multi-slot BFS state of the cover step
-  uint32_t bfs_nr = 0, bfs_bw = 0;  // its layout (rows, bitmap words per row)
+  DevBuf bfs;                   // traversal state of the cover step (select.cu)
+  uint32_t bfs_nr = 0, bfs_bw = 0;  // its layout (rows, mask words per row)
+  bool bfs_ring_reset = false;  // the work-queue rings must be (re)initialised
+  uint32_t sel_par = 0;         // parity of the next selection step (touched lists)
   uint32_t sel_k_cap = 128;     // covered-CC list capacity, in steps
   bool sel_list_valid = false;  // sel_list holds the covered list of this store
 
@@ -172,8 +189,48 @@ void pc_generate(pacim_ctx *ctx, int kind, const uint64_t *params, int nparams,
 // build.cu
 void pc_build(pacim_ctx *ctx);
 void pc_slot_table(pacim_ctx *ctx);
+// Live hub adjacency (HLA) being recorded: raw (key << 32 | other row) with
+// key = hub index * B + slot, counted per key.  Entries past cap are dropped
+// (the build then flags the HLA invalid and the selection hashes hubs' edges).
+struct Hla {
+  const uint32_t *hidx;
+  unsigned long long *cnt;   // [nhub * B + 1]
+  unsigned long long *raw;   // [cap]
+  unsigned long long *n;     // entries appended
+  unsigned long long cap;
+  uint32_t B;
+  // all 32 lanes call this together; lane i appends nu entries for hub row u
+  // and nv for hub row v (live edge (u, v) in slot j): one counter update per warp
+  __device__ __forceinline__ void add_warp(uint32_t u, uint32_t v, uint32_t j, uint32_t nu,
+                                           uint32_t nv) const {
+    const uint32_t mine = nu + nv;
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t pre = mine;
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, pre, d);
+      if (lane >= (uint32_t)d) pre += y;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, pre, 31);
+    if (!tot) return;
+    unsigned long long base = 0;
+    if (lane == 31) base = atomicAdd(n, (unsigned long long)tot);
+    base = __shfl_sync(0xffffffffu, base, 31) + (pre - mine);
+    if (nu) {
+      const unsigned long long key = (unsigned long long)hidx[u] * B + j;
+      atomicAdd(cnt + key, 1ull);
+      if (base < cap) raw[base] = (key << 32) | v;
+      base++;
+    }
+    if (nv) {
+      const unsigned long long key = (unsigned long long)hidx[v] * B + j;
+      atomicAdd(cnt + key, 1ull);
+      if (base < cap) raw[base] = (key << 32) | u;
+    }
+  }
+};
+
 void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
-                    unsigned long long *ctr, cudaEvent_t *ev);
+                    unsigned long long *ctr, cudaEvent_t *ev, const Hla *hla = nullptr);
 // compressed.cu (H6c, H11)
 void pc_build_compressed(pacim_ctx *ctx);
 void pc_select_compressed(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,

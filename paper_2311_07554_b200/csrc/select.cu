@@ -4,25 +4,32 @@
 // One persistent cooperative kernel runs all k steps:
 //   A  NextSeed: argmax of (gain desc, id asc) over v (R5, R6) through a
 //      two-level tournament array (the Win-Tree layout of P:2658-2664,
-//      flattened): per-chunk maxima, recomputed only for chunks whose gains
-//      changed, reduced by every block.
+//      flattened): per-chunk maxima; a chunk is rescanned only when the
+//      vertex holding its maximum lost gain (gains only decrease, so a drop
+//      anywhere else cannot change the chunk's (max, argmax)).
 //   B  MarkSeed: one warp per sketch slot j reads the seed's CC
 //      from its root slot (HIGH | size): delta_j = size unless the CC is
 //      already covered (bit 30), then marks it covered.
 //   C  incremental gain update (R17): the members of every newly covered CC
-//      lose delta_j.  Small CCs (<= big_t vertices) are enumerated by ONE
-//      breadth-first search over the live edges shared by all slots: a
-//      frontier vertex carries the set of slots it was reached in, its
-//      adjacency is read once and each edge's hash is computed once, and only
-//      the candidate slots of the edge (the same bucket table as the build)
-//      are tested — hubs are expanded once, not once per sketch.  Big CCs are
-//      handled by one dense pass over the store (slot == covered root).
+//      lose delta_j.  Small CCs are enumerated by the slot's warp with a
+//      shared-memory queue (warp_bfs).  The others are enumerated by ONE
+//      asynchronous traversal shared by all slots: a row carries the set of
+//      slots it was newly reached in (a bitmask), its adjacency is read and
+//      each edge hashed once, and only the edge's candidate slots (the bucket
+//      table of the build) that are in the mask are tested, a 32-slot word at
+//      a time.  Work items sit in a queue served by every warp of the grid —
+//      no barrier per BFS level; the traversal ends at quiescence (every
+//      pushed item expanded, no producer left).  A row of degree > CH splits
+//      its adjacency into CH-edge chunk items (carrying one 32-slot mask word
+//      each), so hubs are expanded by many warps at once.  CCs larger than
+//      big_t are covered by one dense pass over the store.
 // The covered bits are cleared before the next selection (the list of
 // covered root slots is kept).  gain_num[i] = sum_j delta_j; the host checks
 // it against the argmax gain.
 #include <cooperative_groups.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "pacim_internal.cuh"
@@ -32,11 +39,14 @@ namespace cg = cooperative_groups;
 namespace {
 
 constexpr int SEL_THREADS = 512;
+constexpr int SEL_WARPS = SEL_THREADS / 32;
 constexpr uint32_t NONE = 0xFFFFFFFFu;
 constexpr uint32_t COV = 0x40000000u;   // covered bit of a root slot
 constexpr uint32_t SIZE = 0x3FFFFFFFu;  // CC size bits of a root slot
-constexpr uint32_t MAX_CHUNKS = 4096;   // argmax cache: chunk maxima per step
-constexpr uint32_t BIG_DEFAULT = 4096;  // CCs larger than this: dense pass
+constexpr uint32_t MAX_CHUNKS = 4096;   // argmax cache: chunk maxima
+constexpr uint32_t MAX_BW = 32;         // slot-mask words per row: select supports B <= 1024
+constexpr uint32_t CH_DEFAULT = 256;    // edges per chunk item
+constexpr unsigned long long FULL = 0xffffffffu;
 
 struct Best {
   long long g;
@@ -75,8 +85,63 @@ __device__ Best block_best(Best b, Best *sh) {
   return sh[32];
 }
 
+__device__ __forceinline__ unsigned long long ld_acq(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_acq32(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_rlx(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t exch_release(uint32_t *p, uint32_t x) {
+  uint32_t v;
+  asm volatile("atom.release.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "r"(x) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t exch_acq_rel(uint32_t *p, uint32_t x) {
+  uint32_t v;
+  asm volatile("atom.acq_rel.gpu.global.exch.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "r"(x) : "memory");
+  return v;
+}
+__device__ __forceinline__ void add_release(unsigned long long *p, unsigned long long x) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(x) : "memory");
+}
+
+// queue control words (u64 tickets, each in its own 128-B line)
+// Queue tickets (tail / head / done) in their own 128-B lines.  QC_PROD + 16
+// * parity: producers of B still running in a step of that parity.
+enum { QC_TAIL = 0, QC_HEAD = 16, QC_DONE = 32, QC_PROD = 48, QC_WORDS = 80 };
+// diagnostics (u64): steps, dense steps, warp-BFS slots, deferred slots,
+// row items, chunk items, chunks expanded inline (queue guard)
+enum { DG_STEPS = 0, DG_DENSE, DG_WARP, DG_DEFER, DG_ROWS, DG_CHUNKS, DG_INLINE, DG_ABORT,
+       DG_WORDS = 8 };
+constexpr unsigned long long WATCHDOG_NS = 4000000000ull;  // a wait this long is a bug: abort
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Work-queue slot (bounded MPMC ring with per-slot sequence numbers): the
+// producer of ticket t waits for seq == t, writes, sets seq = t + 1; the
+// consumer of ticket t waits for seq == t + 1, reads, sets seq = t + Q.
+// cw = chunk << 6 | mask word; chunk == CW_ROW marks a row item (its slots
+// are taken from the row's pending mask).
+struct Item {
+  uint32_t seq, row, cw, bits;
+};
+constexpr uint32_t CW_ROW = 0xFFFFFFFFu;
+
 struct Sel {
-  // graph (BFS over live edges)
+  // graph (traversals over live edges)
   const uint64_t *off;
   const uint32_t *nbr;
   uint64_t K, t32;
@@ -86,39 +151,56 @@ struct Sel {
   const uint16_t *g_tab;   // candidate bucket table of the sorted slots
   // store
   uint32_t *L;
-  uint32_t nr, B, BW, nv;  // rows, slots, bitmap words per row, vertices
+  uint32_t nr, B, BW, nv;  // rows, slots, mask words per row, vertices
   const uint32_t *cid, *rmap;
   // per step
   long long *target;       // gain vector (single rank) or delta vector (multi-rank)
-  uint32_t *dl;            // B: delta_j of a CC to enumerate by BFS (0: none)
+  uint32_t *dl;            // B: delta_j of a CC enumerated by traversal (0: none)
   uint32_t *cov_root;      // B: root row of a big CC covered in slot j, or NONE
   uint32_t *cov_delta;     // B
   int *dense;              // [2] by step parity: a big CC was covered
   unsigned long long *cov_list, *cov_cnt;  // covered root-slot indices (restored later)
   unsigned long long cov_cap;
   uint32_t big_t;
-  // multi-slot BFS
-  uint32_t *vis;           // rows x BW: slot bits of visited (row, slot)
-  uint32_t *fmask;         // [2][rows x BW]: slots a frontier row was newly reached in
-  uint32_t *inl;           // [2][rows]: row is in the frontier list
-  uint32_t *flist;         // [2][rows] light frontier rows
-  uint32_t *hlist;         // [2][rows] heavy frontier rows
-  uint32_t *fcnt;          // [0..2] light / [4..6] heavy list sizes by level % 3,
-                           // [8 + par] touched count of a step of parity par
+  int warp_ok;             // small CCs may use warp_bfs
+  // asynchronous traversal
+  uint32_t *vis;           // rows x BW: slots in which the row was visited this step
+  uint32_t *pend;          // rows x BW: slots reached but not yet expanded (light rows)
+  uint32_t *inq;           // rows: row is in the queue
+  Item *ring;              // work queue (rows, chunk items), Q = qmask + 1 slots
+  unsigned long long qmask, qguard;  // chunk items are queued only below qguard outstanding
+  unsigned long long *qc;  // QC_* words
+  const uint32_t *hidx;    // rows: hub index or NONE (HLA valid iff hla_off != nullptr)
+  const unsigned long long *hla_off;  // [nhub * B + 1] segment offsets by (hub, slot)
+  const uint32_t *hla_row; // the rows joined to the hub by an edge live in the slot
+  uint32_t ch;             // edges per chunk item
+  uint32_t lkeep;          // rows a warp keeps for itself (local continuation), <= LCAP
+  uint32_t max_sleep;      // ns: backoff cap of idle queue pollers
   uint32_t *touched;       // [2][rows]: rows visited in a step of parity par (each once)
   uint32_t *tflag;         // [rows]: row is in a touched list
-  uint64_t heavy_deg;      // rows of higher degree are expanded by the whole grid
-  // argmax cache (single rank): marks of step i go to buffer i & 1, consumed
-  // by step i + 1 which resets buffer i - 1 (no reset races with a mark)
+  uint32_t *tcnt;          // [2]
+  // argmax cache (single rank): marks of step i go to dlist[i & 1], consumed
+  // at the end of step i; the buffer is re-armed at the end of step i + 1
   Best *cmax;
   uint32_t *cdirty, *dlist, *dcnt;  // dlist[2][nchunks], dcnt[2]
-  int *alldirty;                    // [2]
   uint32_t par, csh, nchunks;
   int track;
+  unsigned long long *diag;
+  uint32_t tlstep;
+  unsigned long long *ilog;  // optional item log: [0] count, then {start, end, step, edges} x cap
+  unsigned long long ilog_cap;
+  unsigned long long *tl;  // optional timeline: 8 %globaltimer stamps per step (block 0, thread 0)
 };
 
-__device__ __forceinline__ void mark_dirty(const Sel &S, uint32_t u) {
-  const uint32_t c = u >> S.csh;
+__device__ __forceinline__ void stamp(const Sel &S, uint32_t step, int i) {
+  if (S.tl && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    S.tl[(size_t)step * 8 + i] = t;
+  }
+}
+
+__device__ __forceinline__ void mark_dirty(const Sel &S, uint32_t c) {
   if (atomicExch(S.cdirty + c, 1u) == 0u)
     S.dlist[(size_t)S.par * S.nchunks + atomicAdd(S.dcnt + S.par, 1u)] = c;
 }
@@ -126,12 +208,55 @@ __device__ __forceinline__ void mark_dirty(const Sel &S, uint32_t u) {
 // remember a row whose visited bits must be cleared before the next step
 __device__ __forceinline__ void touch(const Sel &S, uint32_t row) {
   if (atomicExch(S.tflag + row, 1u) == 0u)
-    S.touched[(size_t)S.par * S.nr + atomicAdd(S.fcnt + 8 + S.par, 1u)] = row;
+    S.touched[(size_t)S.par * S.nr + atomicAdd(S.tcnt + S.par, 1u)] = row;
 }
 
 __device__ __forceinline__ void sub_gain(const Sel &S, uint32_t u, long long d) {
   atomicAdd((unsigned long long *)&S.target[u], (unsigned long long)(-d));
-  if (S.track) mark_dirty(S, u);
+  if (S.track) {
+    const uint32_t c = u >> S.csh;
+    if (__ldcg(&S.cmax[c].v) == u) mark_dirty(S, c);  // only the chunk's argmax matters
+  }
+}
+
+__device__ __forceinline__ void q_write(Item *ring, unsigned long long mask, unsigned long long t,
+                                        uint32_t row, uint32_t cw, uint32_t bits) {
+  Item *it = ring + (t & mask);
+  while (ld_acq32(&it->seq) != (uint32_t)t) __nanosleep(32);  // freed by its last consumer
+  it->row = row;
+  it->cw = cw;
+  it->bits = bits;
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&it->seq), "r"((uint32_t)(t + 1))
+               : "memory");
+}
+
+// The warp's local stack of rows it discovered and expands itself (no queue
+// hand-off); rows beyond the first `lkeep` go to the shared queue.
+struct LStack {
+  uint32_t *row, *x, *cnt;  // shared memory of the warp
+  uint32_t keep;
+};
+constexpr uint32_t LCAP = 16;
+
+// (row wr of vertex w, mask word wd) newly reached in the slots nb: schedule
+// its expansion (one queue entry per row at a time; bits arriving meanwhile
+// merge into it)
+__device__ __forceinline__ void reach(const Sel &S, uint32_t wr, uint32_t w, uint32_t wd,
+                                      uint32_t nb, const LStack *ls) {
+  atomicOr(S.pend + (size_t)wr * S.BW + wd, nb);
+  // release: a consumer that clears the flag after this exchange (acq_rel)
+  // sees the bits
+  if (exch_release(S.inq + wr, 1u) == 0u) {
+    if (ls) {
+      const uint32_t at = atomicAdd(ls->cnt, 1u);
+      if (at < ls->keep) {
+        ls->row[at] = wr;
+        ls->x[at] = w;
+        return;
+      }
+    }
+    q_write(S.ring, S.qmask, atomicAdd(S.qc + QC_TAIL, 1ull), wr, CW_ROW, 0);
+  }
 }
 
 // Phase B for slot j (one thread): MarkSeed and classification.
@@ -161,26 +286,16 @@ __device__ __forceinline__ uint32_t cover_slot(const Sel &S, uint32_t srow, uint
   return delta;
 }
 
-// hand slot j of the seed's small CC to the grid-wide multi-slot BFS
-__device__ __forceinline__ void defer_slot(const Sel &S, uint32_t s, uint32_t srow, uint32_t j) {
-  atomicOr(S.fmask + (size_t)srow * S.BW + (j >> 5), 1u << (j & 31));
-  if (atomicExch(S.inl + srow, 1u) == 0u) {  // level-0 list (parity 0)
-    if (S.off[s + 1] - S.off[s] > S.heavy_deg)
-      S.hlist[atomicAdd(S.fcnt + 4, 1u)] = srow;
-    else
-      S.flist[atomicAdd(S.fcnt + 0, 1u)] = srow;
-  }
-}
-
 // Warp-local BFS of the seed's CC in slot j (<= QCAP vertices) with a
 // shared-memory queue and visited set; applies the gain updates.  Returns
 // false, before updating anything, if it meets a vertex of degree > WARP_DEG
-// (the grid-wide BFS then takes the slot and reads that adjacency once for
-// all slots).
+// (the shared traversal then takes the slot and reads that adjacency once
+// for all slots).
 constexpr uint32_t QCAP = 512;
 constexpr uint32_t HCAP = 1024;
 constexpr uint64_t WARP_DEG = 1024;
-constexpr uint32_t WARP_WORDS = QCAP + HCAP + 1;
+// + mask, nonzero-word list (u8), local stack (rows, vertices, count)
+constexpr uint32_t WARP_WORDS = QCAP + HCAP + 1 + MAX_BW + MAX_BW / 4 + 2 * 16 + 1;
 
 // shared-memory words of the slot tables (shr[B] + tab[2^TB + 1] u16), 16-B aligned
 __host__ __device__ __forceinline__ uint32_t table_words(uint32_t B) {
@@ -199,29 +314,61 @@ __device__ bool warp_bfs(const Sel &S, uint32_t s, uint32_t j, uint32_t delta, u
     *tail = 1;
   }
   __syncwarp();
+  // level-synchronous within the warp: the (vertex, edge) pairs of up to 32
+  // queued vertices are spread over the lanes, so the latency is the CC's
+  // depth, not its size
   for (uint32_t head = 0; head < *tail;) {
-    const uint32_t x = q[head++];
-    const uint64_t e0 = S.off[x], e1 = S.off[x + 1];
-    if (e1 - e0 > WARP_DEG) return false;  // uniform: same x in every lane
-    for (uint64_t e = e0 + lane; e < e1; e += 32) {
-      const uint32_t w = S.nbr[e];
-      const uint64_t a = x < w ? x : w, b = x < w ? w : x;
-      const uint32_t he = (uint32_t)(pc_mix64(((a << 32) | b) ^ S.K) >> 32);
-      const uint64_t T = S.wic ? (uint64_t)S.tcsr[e] + 1 : S.t32;  // R4
-      if ((uint64_t)(hr ^ he) >= T) continue;                        // R3
-      uint32_t h = (w * 2654435761u) & (HCAP - 1);
-      for (;;) {
-        const uint32_t old = atomicCAS(hs + h, NONE, w);
-        if (old == NONE) {
-          const uint32_t pos = atomicAdd(tail, 1u);
-          if (pos < QCAP) q[pos] = w;
-          break;
-        }
-        if (old == w) break;
-        h = (h + 1) & (HCAP - 1);
+    const uint32_t lvl_end = *tail;
+    for (uint32_t base = head; base < lvl_end; base += 32) {
+      const uint32_t idx = base + lane;
+      const uint32_t x = idx < lvl_end ? q[idx] : 0u;
+      uint64_t e0 = 0, deg = 0;
+      if (idx < lvl_end) {
+        e0 = S.off[x];
+        deg = S.off[x + 1] - e0;
       }
+      if (__any_sync(FULL, deg > WARP_DEG)) return false;  // a hub: the shared traversal
+      uint32_t pre = (uint32_t)deg;  // inclusive scan of the degrees
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, pre, d);
+        if (lane >= d) pre += y;
+      }
+      const uint32_t total = __shfl_sync(FULL, pre, 31);
+      pre -= (uint32_t)deg;  // exclusive
+      for (uint32_t c = 0; c < total; c += 32) {
+        const uint32_t t = c + lane;
+        uint32_t a = 0;  // the lane (vertex) owning pair t: largest a with pre[a] <= t
+#pragma unroll
+        for (int b = 16; b; b >>= 1) {
+          const uint32_t pa = __shfl_sync(FULL, pre, a + b);
+          if (pa <= t) a += b;
+        }
+        const uint32_t xa = __shfl_sync(FULL, x, a);
+        const uint64_t ea = __shfl_sync(FULL, e0, a);
+        const uint32_t pra = __shfl_sync(FULL, pre, a);
+        if (t >= total) continue;
+        const uint64_t e = ea + (t - pra);
+        const uint32_t w = S.nbr[e];
+        const uint64_t lo = xa < w ? xa : w, hi = xa < w ? w : xa;
+        const uint32_t he = (uint32_t)(pc_mix64(((lo << 32) | hi) ^ S.K) >> 32);
+        const uint64_t T = S.wic ? (uint64_t)S.tcsr[e] + 1 : S.t32;  // R4
+        if ((uint64_t)(hr ^ he) >= T) continue;                        // R3
+        uint32_t h = (w * 2654435761u) & (HCAP - 1);
+        for (;;) {
+          const uint32_t old = atomicCAS(hs + h, NONE, w);
+          if (old == NONE) {
+            const uint32_t pos = atomicAdd(tail, 1u);
+            if (pos < QCAP) q[pos] = w;
+            break;
+          }
+          if (old == w) break;
+          h = (h + 1) & (HCAP - 1);
+        }
+      }
+      __syncwarp();
     }
-    __syncwarp();
+    head = lvl_end;
     if (*tail > QCAP) return false;  // cannot happen for a CC of delta <= QCAP
   }
   const uint32_t cnt = *tail;
@@ -233,110 +380,359 @@ __device__ bool warp_bfs(const Sel &S, uint32_t s, uint32_t j, uint32_t delta, u
   return true;
 }
 
-// One BFS level: every frontier row is expanded by one block; its adjacency
-// is read once, each edge hashed once, and only the edge's candidate slots
-// that the row was newly reached in are tested (R3 live test).
-// Frontier lists alternate by level parity; their sizes live in fcnt[lvl % 3]
-// so that the counter of level + 2 can be reset during level (nobody reads
-// or appends to it then).
-// Expand frontier row u (vertex x) over adjacency entries [e0, e1) taken with
-// stride `stride` from offset `first` (a block or the whole grid).
-__device__ void expand_row(const Sel &S, uint32_t lvl, uint32_t u, const uint32_t *shr,
-                           const uint16_t *tab, uint32_t s, uint64_t first, uint64_t stride) {
-  const uint32_t cur = lvl & 1, nxt = cur ^ 1;
-  uint32_t *ncnt = S.fcnt + (lvl + 1) % 3;      // light list of level + 1
-  uint32_t *nhcnt = S.fcnt + 4 + (lvl + 1) % 3; // heavy list of level + 1
-  const uint32_t *M = S.fmask + ((size_t)cur * S.nr + u) * S.BW;
-  uint32_t *fm_nxt = S.fmask + (size_t)nxt * S.nr * S.BW;
-  const uint32_t x = S.rmap[u];
-  const uint64_t e1 = S.off[x + 1];
-  {
-    for (uint64_t e = S.off[x] + first; e < e1; e += stride) {
-      const uint32_t w = S.nbr[e];
-      const uint64_t a = x < w ? x : w, b = x < w ? w : x;
-      const uint32_t he = (uint32_t)(pc_mix64(((a << 32) | b) ^ S.K) >> 32);
-      const uint64_t T = S.wic ? (uint64_t)S.tcsr[e] + 1 : S.t32;  // R3 / R4
-      if (T == 0) continue;
-      const uint32_t wb = __clz((uint32_t)(T - 1));
-      uint32_t lo, hi;
-      if (wb >= PACIM_TB) {
-        const uint32_t p = he >> (32 - PACIM_TB);
-        lo = tab[p];
-        hi = tab[p + 1];
-      } else if (wb == 0) {
-        lo = 0;
-        hi = S.B;
-      } else {
-        const uint32_t p = (he >> (32 - wb)) << (PACIM_TB - wb);
-        lo = tab[p];
-        hi = tab[p + (1u << (PACIM_TB - wb))];
+// Expand CSR entry e of vertex x for the slots in mask M (BW words): hash
+// the edge once (R2), enumerate its candidate slots from the bucket table
+// (exact: the top clz(T-1) bits of hash(r) and hash(e) must agree), test
+// the masked candidates 32 at a time (R3 live test), and for the slots in
+// which the neighbour is new: one gain update with the sum of their deltas
+// and one scheduling of its expansion.
+__device__ __forceinline__ void expand_edge(const Sel &S, uint32_t x, uint32_t w, uint64_t T,
+                                            const uint32_t *M, uint32_t s, const uint32_t *shr,
+                                            const uint16_t *tab, const uint32_t *sdl,
+                                            const LStack *ls) {
+  const uint64_t a = x < w ? x : w, b = x < w ? w : x;
+  if (T == 0) return;
+  const uint32_t he = (uint32_t)(pc_mix64(((a << 32) | b) ^ S.K) >> 32);
+  const uint32_t wb = __clz((uint32_t)(T - 1));
+  uint32_t lo, hi;
+  if (wb >= PACIM_TB) {
+    const uint32_t p = he >> (32 - PACIM_TB);
+    lo = tab[p];
+    hi = tab[p + 1];
+  } else if (wb == 0) {
+    lo = 0;
+    hi = S.B;
+  } else {
+    const uint32_t p = (he >> (32 - wb)) << (PACIM_TB - wb);
+    lo = tab[p];
+    hi = tab[p + (1u << (PACIM_TB - wb))];
+  }
+  if (lo >= hi) return;
+  // every candidate is live when T is the full bucket width 2^(32 - wb) and
+  // the table resolves all wb bits
+  const bool all_live = wb <= PACIM_TB && T == (1ull << (32 - wb));
+  uint32_t wr = NONE;
+  const uint32_t w0 = lo >> 5, w1 = (hi - 1) >> 5;
+  for (uint32_t wd = w0; wd <= w1; wd++) {
+    uint32_t rb = 0xFFFFFFFFu;
+    if (wd == w0) rb &= 0xFFFFFFFFu << (lo & 31);
+    if (wd == w1) rb &= 0xFFFFFFFFu >> (31 - ((hi - 1) & 31));
+    const uint32_t bits = M[wd] & rb;
+    if (!bits) continue;
+    uint32_t live = bits;
+    if (!all_live) {
+      live = 0;
+      for (uint32_t t = bits; t; t &= t - 1) {
+        const uint32_t bit = __ffs(t) - 1;
+        if ((uint64_t)(shr[wd * 32 + bit] ^ he) < T) live |= 1u << bit;
       }
-      uint32_t wr = NONE;
-      for (uint32_t j = lo; j < hi; j++) {
-        if (!((__ldcg(M + (j >> 5)) >> (j & 31)) & 1u)) continue;
-        if ((uint64_t)(shr[j] ^ he) >= T) continue;
-        if (wr == NONE) wr = S.cid[w];
-        const uint32_t bit = 1u << (j & 31);
-        const uint32_t old = atomicOr(S.vis + (size_t)wr * S.BW + (j >> 5), bit);
-        if (old & bit) continue;  // already in this slot's CC walk
-        if (w != s) sub_gain(S, w, __ldcg(S.dl + j));
-        atomicOr(fm_nxt + (size_t)wr * S.BW + (j >> 5), bit);
-        if (atomicExch(S.inl + (size_t)nxt * S.nr + wr, 1u) == 0u) {
-          const bool heavy = S.off[w + 1] - S.off[w] > S.heavy_deg;
-          if (heavy)
-            S.hlist[(size_t)nxt * S.nr + atomicAdd(nhcnt, 1u)] = wr;
-          else
-            S.flist[(size_t)nxt * S.nr + atomicAdd(ncnt, 1u)] = wr;
-        }
-        // a row can enter several levels' lists (reached at different depths
-        // in different slots) but is listed for the vis clean-up only once
-        touch(S, wr);
+      if (!live) continue;
+    }
+    uint32_t cm = NONE;
+    if (wr == NONE) {
+      wr = S.cid[w];
+      if (S.track) cm = __ldcg(&S.cmax[w >> S.csh].v);  // in flight with the row lookup
+    }
+    const uint32_t old = atomicOr(S.vis + (size_t)wr * S.BW + wd, live);
+    const uint32_t nb = live & ~old;
+    if (!nb) continue;
+    long long d = 0;
+    for (uint32_t t = nb; t; t &= t - 1) d += sdl[wd * 32 + __ffs(t) - 1];
+    if (w != s) {
+      atomicAdd((unsigned long long *)&S.target[w], (unsigned long long)(-d));
+      if (S.track) {  // only the chunk's argmax matters (gains only decrease)
+        if (cm == NONE) cm = __ldcg(&S.cmax[w >> S.csh].v);
+        if (cm == w) mark_dirty(S, w >> S.csh);
       }
+    }
+    reach(S, wr, w, wd, nb, ls);  // the row is touched when it is expanded
+  }
+}
+
+// Expand CSR entries [ea, eb) of vertex x (lanes strided): the neighbour and
+// threshold loads of EU entries per lane are issued before any of them is
+// tested, so a 256-entry chunk costs about one memory latency, not eight.
+constexpr int EU = 8;
+__device__ __forceinline__ void expand_range(const Sel &S, uint32_t x, uint64_t ea, uint64_t eb,
+                                             const uint32_t *M, uint32_t s, const uint32_t *shr,
+                                             const uint16_t *tab, const uint32_t *sdl,
+                                             const LStack *ls) {
+  const int lane = threadIdx.x & 31;
+  for (uint64_t base = ea; base < eb; base += 32 * EU) {
+    uint32_t w[EU], tm[EU];
+#pragma unroll
+    for (int u = 0; u < EU; u++) {
+      const uint64_t e = base + lane + 32 * u;
+      w[u] = e < eb ? __ldcs(S.nbr + e) : NONE;
+      tm[u] = (e < eb && S.wic) ? __ldcs(S.tcsr + e) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < EU; u++) {
+      if (w[u] == NONE) continue;
+      const uint64_t T = S.wic ? (uint64_t)tm[u] + 1 : S.t32;  // R3 / R4
+      expand_edge(S, x, w[u], T, M, s, shr, tab, sdl, ls);
     }
   }
 }
 
-// One BFS level.  Light frontier rows are expanded by one block each (which
-// then clears the row's frontier mask and list flag); heavy rows (degree >
-// heavy_deg, e.g. hubs) by the whole grid, their masks cleared after the
-// level barrier (clear_heavy).  Frontier lists alternate by level parity;
-// their sizes live in fcnt[lvl % 3] (light) and fcnt[4 + lvl % 3] (heavy) so
-// that the counters of level + 2 can be reset during the level.
-__device__ void bfs_level(const Sel &S, uint32_t lvl, const uint32_t *shr, const uint16_t *tab,
-                          uint32_t s) {
-  const uint32_t cur = lvl & 1;
-  const uint32_t cnt = __ldcg(S.fcnt + lvl % 3);
-  const uint32_t hcnt = __ldcg(S.fcnt + 4 + lvl % 3);
-  for (uint32_t i = blockIdx.x; i < cnt; i += gridDim.x) {
-    const uint32_t u = __ldcg(S.flist + (size_t)cur * S.nr + i);
-    expand_row(S, lvl, u, shr, tab, s, threadIdx.x, blockDim.x);
-    __syncthreads();
-    uint32_t *fm = S.fmask + ((size_t)cur * S.nr + u) * S.BW;
-    for (uint32_t q = threadIdx.x; q < S.BW; q += blockDim.x) fm[q] = 0;
-    if (threadIdx.x == 0) S.inl[(size_t)cur * S.nr + u] = 0;
-  }
-  const uint64_t gt = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const uint64_t gn = (uint64_t)gridDim.x * blockDim.x;
-  for (uint32_t i = 0; i < hcnt; i++) {
-    const uint32_t u = __ldcg(S.hlist + (size_t)cur * S.nr + i);
-    expand_row(S, lvl, u, shr, tab, s, gt, gn);
+// row r newly reached from a hub in slot j (mask word wd, bit)
+__device__ __forceinline__ void hub_visit(const Sel &S, uint32_t r, uint32_t j, uint32_t s,
+                                          const uint32_t *sdl, const LStack *ls) {
+  const uint32_t wd = j >> 5, bit = 1u << (j & 31);
+  const uint32_t old = atomicOr(S.vis + (size_t)r * S.BW + wd, bit);
+  if (old & bit) return;
+  const uint32_t w = S.rmap[r];
+  if (w != s) sub_gain(S, w, sdl[j]);
+  reach(S, r, w, wd, bit, ls);
+}
+
+// Expand hub h for the pending slots in wm through the live hub adjacency:
+// lane l takes slot 32 * wd + l of each nonzero mask word; segments longer
+// than 32 rows are walked by the whole warp.
+__device__ void expand_hub(const Sel &S, uint32_t h, const uint32_t *wm, uint32_t s,
+                           const uint32_t *sdl, const LStack *ls) {
+  const int lane = threadIdx.x & 31;
+  for (uint32_t wd = 0; wd < S.BW; wd++) {
+    const uint32_t m = wm[wd];
+    if (!m) continue;
+    const uint32_t j = wd * 32 + lane;
+    unsigned long long a = 0, z = 0;
+    if ((m >> lane) & 1u) {
+      const unsigned long long key = (unsigned long long)h * S.B + j;
+      a = __ldg(S.hla_off + key);
+      z = __ldg(S.hla_off + key + 1);
+    }
+    const bool longseg = z - a > 32;
+    if (!longseg)
+      for (unsigned long long i = a; i < z; i++) hub_visit(S, __ldg(S.hla_row + i), j, s, sdl, ls);
+    for (uint32_t lm = __ballot_sync(FULL, longseg); lm; lm &= lm - 1) {
+      const int src = __ffs(lm) - 1;
+      const unsigned long long la = __shfl_sync(FULL, a, src), lz = __shfl_sync(FULL, z, src);
+      const uint32_t lj = wd * 32 + src;
+      for (unsigned long long i = la + lane; i < lz; i += 32)
+        hub_visit(S, __ldg(S.hla_row + i), lj, s, sdl, ls);
+    }
   }
 }
 
-// after the level barrier: clear the heavy rows' frontier masks and flags
-__device__ void clear_heavy(const Sel &S, uint32_t lvl, uint64_t gt, uint64_t gn) {
-  const uint32_t cur = lvl & 1;
-  const uint32_t hcnt = __ldcg(S.fcnt + 4 + lvl % 3);
-  for (uint64_t t = gt; t < (uint64_t)hcnt * S.BW; t += gn) {
-    const uint32_t u = __ldcg(S.hlist + (size_t)cur * S.nr + t / S.BW);
-    S.fmask[((size_t)cur * S.nr + u) * S.BW + t % S.BW] = 0;
-    if (t % S.BW == 0) S.inl[(size_t)cur * S.nr + u] = 0;
+// Expand one item: a row (its pending slots taken; rows of degree > CH also
+// queue their chunks 1.. as chunk items) or a chunk item.  Returns the CSR
+// entries tested.
+__device__ uint64_t process_item(const Sel &S, uint32_t s, uint32_t row, uint32_t x, uint32_t cw,
+                                 uint32_t bits, uint32_t *wm, uint8_t *wl, const uint32_t *shr,
+                                 const uint16_t *tab, const uint32_t *sdl, const LStack *ls,
+                                 unsigned long long &nrow, unsigned long long &nchunk,
+                                 unsigned long long &ninl) {
+  const int lane = threadIdx.x & 31;
+  uint64_t c_lo, c_hi;  // chunks expanded by this warp
+  uint64_t e0, e1, nch;
+  if (cw == CW_ROW) {
+    nrow++;
+    e0 = S.off[x];  // issued before the flag exchange (independent)
+    e1 = S.off[x + 1];
+    // take the row's pending slots (clear the queue flag first: bits added
+    // after this point re-queue the row)
+    if (lane == 0) exch_acq_rel(S.inq + row, 0u);
+    __syncwarp();
+    const uint32_t m = lane < S.BW ? atomicExch(S.pend + (size_t)row * S.BW + lane, 0u) : 0u;
+    if (lane < S.BW) wm[lane] = m;
+    const uint32_t nzb = __ballot_sync(FULL, m != 0);
+    const uint32_t nnz = __popc(nzb);
+    if (m) wl[__popc(nzb & ((1u << lane) - 1))] = lane;
+    if (lane == 0) touch(S, row);  // its visited bits are cleared before the next step
+    __syncwarp();
+    nch = (e1 - e0 + S.ch - 1) / S.ch;
+    c_lo = 0;
+    c_hi = nnz ? nch : 0;
+    if (S.hla_off && nnz) {
+      const uint32_t h = S.hidx[row];
+      if (h != NONE) {  // a hub: its live edges from the build, no hashing
+        expand_hub(S, h, wm, s, sdl, ls);
+        return 0;
+      }
+    }
+    // chunks 1..nch-1: one item per (chunk, nonzero word), queued in batches
+    // of 32 while the queue has room, else expanded here
+    const uint64_t nitems = nch > 1 ? (nch - 1) * nnz : 0;
+    uint64_t done_items = 0;
+    while (done_items < nitems) {
+      unsigned long long t0 = 0;
+      const uint32_t nb = (uint32_t)(nitems - done_items < 32 ? nitems - done_items : 32);
+      int ok = 0;
+      if (lane == 0) {
+        const unsigned long long out = ld_acq(S.qc + QC_TAIL) - ld_acq(S.qc + QC_DONE);
+        if (out + nb < S.qguard) {
+          ok = 1;
+          t0 = atomicAdd(S.qc + QC_TAIL, (unsigned long long)nb);
+        }
+      }
+      if (!__shfl_sync(FULL, ok, 0)) break;
+      t0 = __shfl_sync(FULL, t0, 0);
+      if (lane < nb) {
+        const uint64_t it = done_items + lane;
+        const uint32_t wd = wl[it % nnz];
+        q_write(S.ring, S.qmask, t0 + lane, row, (uint32_t)((1 + it / nnz) << 6) | wd, wm[wd]);
+      }
+      done_items += nb;
+    }
+    if (nitems) {
+      if (done_items < nitems) {
+        ninl++;  // the queue is full: expand the rest here (with the full mask;
+                 // repeated tests of already visited slots are no-ops)
+        expand_range(S, x, e0, min(e1, e0 + S.ch), wm, s, shr, tab, sdl, ls);
+        c_lo = 1 + done_items / nnz;
+        c_hi = nch;
+      } else {
+        c_hi = 1;
+      }
+    }
+  } else {
+    nchunk++;
+    x = S.rmap[row];
+    e0 = S.off[x];
+    e1 = S.off[x + 1];
+    for (uint32_t q = lane; q < S.BW; q += 32) wm[q] = 0;
+    __syncwarp();
+    if (lane == 0) wm[cw & 63] = bits;
+    __syncwarp();
+    c_lo = cw >> 6;
+    c_hi = c_lo + 1;
+  }
+  const uint64_t ea = min(e1, e0 + c_lo * S.ch), eb = min(e1, e0 + c_hi * S.ch);
+  expand_range(S, x, ea, eb, wm, s, shr, tab, sdl, ls);
+  return eb > ea ? eb - ea : 0;
+}
+
+// Queue phase: every warp pops items and expands them until quiescence.
+// Returns the final tail (identical in every warp).  wm / wl: the warp's
+// shared words for the item's mask and the list of its nonzero words; sdl:
+// the block's copy of the slots' deltas (final once every B is done).
+__device__ unsigned long long queue_phase(const Sel &S, uint32_t s, uint32_t *wm, uint8_t *wl,
+                                          const uint32_t *shr, const uint16_t *tab,
+                                          uint32_t *sdl, const unsigned long long *prod,
+                                          const LStack *ls) {
+  const int lane = threadIdx.x & 31;
+  // wait for every producer of B; if nothing was queued the traversal is
+  // already over (quiescent: no producer, nothing queued), else snapshot the
+  // deltas
+  __shared__ unsigned long long quiet_tail;
+  if (threadIdx.x == 0) {
+    unsigned ns = 32;
+    const unsigned long long t0 = gtime();
+    while (ld_acq(prod) != 0) {
+      __nanosleep(ns);
+      ns = ns < 256 ? ns * 2 : 256;
+      if (gtime() - t0 > WATCHDOG_NS) {
+        atomicExch(S.diag + DG_ABORT, 1ull);
+        break;
+      }
+    }
+    const unsigned long long done = ld_acq(S.qc + QC_DONE);
+    const unsigned long long tail = ld_acq(S.qc + QC_TAIL);
+    quiet_tail = done == tail ? tail : ~0ull;
+  }
+  __syncthreads();
+  if (S.tl && blockIdx.x == 0 && threadIdx.x == 0) S.tl[(size_t)S.tlstep * 8 + 3] = gtime();
+  const unsigned long long qt = quiet_tail;
+  if (qt != ~0ull) return qt;
+  for (uint32_t j = threadIdx.x; j < S.B; j += blockDim.x) sdl[j] = __ldcg(S.dl + j);
+  __syncthreads();
+  unsigned long long nrow = 0, nchunk = 0, ninl = 0;
+  for (;;) {
+    unsigned long long i = 0, tend = 0;
+    uint32_t row = NONE, cw = 0, bits = 0;
+    int fin = 0;
+    if (lane == 0) {
+      unsigned ns = 32;
+      bool have = false;
+      const unsigned long long t0 = gtime();
+      for (;;) {
+        const unsigned long long tail = ld_acq(S.qc + QC_TAIL);
+        if (!have && ld_rlx(S.qc + QC_HEAD) < tail) {  // reserve only when work is queued
+          i = atomicAdd(S.qc + QC_HEAD, 1ull);
+          have = true;
+          ns = 32;
+        }
+        if (have) {
+          Item *it = S.ring + (i & S.qmask);
+          if (ld_acq32(&it->seq) == (uint32_t)(i + 1)) {  // item i is written
+            row = it->row;
+            cw = it->cw;
+            bits = it->bits;
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&it->seq),
+                         "r"((uint32_t)(i + S.qmask + 1))
+                         : "memory");
+            break;
+          }
+        }
+        if (!have || i >= tail) {
+          const unsigned long long done = ld_acq(S.qc + QC_DONE);
+          const unsigned long long t2 = ld_acq(S.qc + QC_TAIL);
+          if (done == t2 && (!have || i >= t2)) {  // quiescent: nothing queued, nobody expanding
+            fin = 1;
+            tend = t2;
+            break;
+          }
+        }
+        if (gtime() - t0 > WATCHDOG_NS || ld_rlx(S.diag + DG_ABORT)) {
+          atomicExch(S.diag + DG_ABORT, 1ull);
+          fin = 1;  // the host reports the abort
+          break;
+        }
+        __nanosleep(ns);
+        ns = ns < S.max_sleep ? ns * 2 : S.max_sleep;  // idle pollers stay off the hot lines
+      }
+    }
+    fin = __shfl_sync(FULL, fin, 0);
+    if (fin) {
+      if (lane == 0 && S.diag) {
+        atomicAdd(S.diag + DG_ROWS, nrow);
+        atomicAdd(S.diag + DG_CHUNKS, nchunk);
+        atomicAdd(S.diag + DG_INLINE, ninl);
+      }
+      return __shfl_sync(FULL, tend, 0);
+    }
+    row = __shfl_sync(FULL, row, 0);
+    cw = __shfl_sync(FULL, cw, 0);
+    bits = __shfl_sync(FULL, bits, 0);
+    const unsigned long long it_t0 = S.ilog ? gtime() : 0;
+    // the popped item, then the rows this warp discovered and kept (local
+    // continuation: no queue hand-off); the item is done when both are
+    if (lane == 0) *ls->cnt = 0;
+    __syncwarp();
+    uint32_t xr = cw == CW_ROW ? S.rmap[row] : NONE;  // chunk items look up x below
+    uint64_t nedges = 0;
+    for (int first = 1;; first = 0) {
+      nedges += process_item(S, s, row, xr, cw, bits, wm, wl, shr, tab, sdl, ls, nrow, nchunk, ninl);
+      __syncwarp();
+      const uint32_t n = min(*ls->cnt, ls->keep);
+      __syncwarp();
+      if (n == 0) break;
+      row = ls->row[n - 1];
+      xr = ls->x[n - 1];
+      cw = CW_ROW;
+      __syncwarp();
+      if (lane == 0) *ls->cnt = n - 1;
+      __syncwarp();
+    }
+    if (lane == 0 && S.ilog) {
+      const unsigned long long at = atomicAdd(S.ilog, 1ull);
+      if (at < S.ilog_cap) {
+        unsigned long long *r = S.ilog + 4 + at * 4;
+        r[0] = it_t0;
+        r[1] = gtime();
+        r[2] = S.tlstep;
+        r[3] = nedges;
+      }
+    }
+    if (lane == 0) add_release(S.qc + QC_DONE, 1ull);  // after this item's pushes
   }
 }
 
 // dense pass for the big CCs covered this step: v is a member of slot j's
 // covered CC iff its slot holds that root, or v is the root.  8 slots per
-// lane kept in registers, rows streamed.
+// lane kept in registers; DR rows in flight per warp.
+constexpr int DR = 4;
 __device__ void apply_dense(const Sel &S, uint32_t s, size_t warp0, size_t nwarps) {
   const int lane = threadIdx.x & 31;
   for (uint32_t j0 = 0; j0 < S.B; j0 += 256) {
@@ -350,19 +746,28 @@ __device__ void apply_dense(const Sel &S, uint32_t s, size_t warp0, size_t nwarp
       any |= cr[i] != NONE;
     }
     if (!__any_sync(0xffffffffu, any)) continue;
-    for (size_t v = warp0; v < S.nr; v += nwarps) {
-      uint32_t x[8];
+    for (size_t v0 = warp0 * DR; v0 < S.nr; v0 += nwarps * DR) {
+      uint32_t x[DR][8];
 #pragma unroll
-      for (int i = 0; i < 8; i++)
-        x[i] = cr[i] != NONE ? __ldcs(S.L + v * S.B + j0 + lane + 32 * i) : NONE;
-      long long d = 0;
+      for (int r = 0; r < DR; r++)
 #pragma unroll
-      for (int i = 0; i < 8; i++)
-        if (cr[i] != NONE && (x[i] == cr[i] || (uint32_t)v == cr[i])) d += cd[i];
-      for (int q = 16; q; q >>= 1) d += __shfl_xor_sync(0xffffffffu, d, q);
-      if (lane == 0 && d) {
-        const uint32_t vid = S.rmap[v];
-        if (vid != s) atomicAdd((unsigned long long *)&S.target[vid], (unsigned long long)(-d));
+        for (int i = 0; i < 8; i++)
+          x[r][i] = (cr[i] != NONE && v0 + r < S.nr)
+                        ? __ldcs(S.L + (v0 + r) * S.B + j0 + lane + 32 * i)
+                        : NONE;
+#pragma unroll
+      for (int r = 0; r < DR; r++) {
+        const uint32_t v = (uint32_t)(v0 + r);
+        long long d = 0;
+#pragma unroll
+        for (int i = 0; i < 8; i++)
+          if (cr[i] != NONE && (x[r][i] == cr[i] || v == cr[i])) d += cd[i];
+        if (!__any_sync(0xffffffffu, d != 0)) continue;
+        for (int q = 16; q; q >>= 1) d += __shfl_xor_sync(0xffffffffu, d, q);
+        if (lane == 0 && d) {
+          const uint32_t vid = S.rmap[v];
+          if (vid != s) atomicAdd((unsigned long long *)&S.target[vid], (unsigned long long)(-d));
+        }
       }
     }
   }
@@ -376,91 +781,126 @@ __device__ void load_tables(const Sel &S, uint32_t *shr, uint16_t *tab) {
 
 struct SelOut {
   uint32_t k;
+  uint32_t given;          // NONE: argmax over the gains; else the seed of a single
+                           // multi-rank step (no argmax, target = delta vector)
   uint32_t *seeds;
-  long long *gain_num;   // k, zeroed
-  long long *arg_gain;   // k
-  unsigned long long *levels;
+  long long *gain_num;     // k, zeroed
+  long long *arg_gain;     // k
 };
 
-__global__ void __launch_bounds__(SEL_THREADS) k_select(Sel S0, SelOut O) {
+// refresh the chunk maxima whose argmax lost gain in step parity par (all
+// chunks if `all`); block-strided over chunks
+__device__ void refresh_chunks(const Sel &S, uint32_t par, bool all, Best *sh) {
+  const uint32_t nd = all ? S.nchunks : __ldcg(S.dcnt + par);
+  for (uint32_t t = blockIdx.x; t < nd; t += gridDim.x) {
+    const uint32_t c = all ? t : __ldcg(S.dlist + (size_t)par * S.nchunks + t);
+    const size_t v0 = (size_t)c << S.csh, v1 = min((size_t)S.nv, v0 + ((size_t)1 << S.csh));
+    Best b{LLONG_MIN, 0xFFFFFFFFu};
+    for (size_t v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+      const long long g = __ldcg(S.target + v);
+      if (better(g, (uint32_t)v, b.g, b.v)) {
+        b.g = g;
+        b.v = (uint32_t)v;
+      }
+    }
+    b = block_best(b, sh);
+    if (threadIdx.x == 0) {
+      S.cmax[c] = b;
+      S.cdirty[c] = 0;
+    }
+  }
+}
+
+// clear the visited bits and touched flags of the rows in touched list par
+__device__ void clear_touched(const Sel &S, uint32_t par, size_t tid, size_t nth) {
+  const uint32_t nt = __ldcg(S.tcnt + par);
+  for (size_t t = tid; t < (size_t)nt * S.BW; t += nth) {
+    const uint32_t r = __ldcg(S.touched + (size_t)par * S.nr + t / S.BW);
+    S.vis[(size_t)r * S.BW + (t % S.BW)] = 0;
+    if (t % S.BW == 0) S.tflag[r] = 0;
+  }
+}
+
+// Step i (parity par): A argmax -> B MarkSeed + small CCs -> C shared
+// traversal (until quiescence) -> D dense pass (big CCs) -> E refresh of the
+// chunk maxima and clean-up, then ONE grid barrier.  At quiescence every
+// update of B and C is complete (release/acquire on the producer and done
+// counters), so E needs no barrier of its own; counters of parity par ^ 1
+// (read during step i - 1) are re-armed in E of step i.
+__global__ void __launch_bounds__(SEL_THREADS, 1) k_select(Sel S0, SelOut O, uint32_t par0) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ uint32_t dsm[];
   Sel S = S0;
   uint32_t *shr = dsm;
   uint16_t *tab = reinterpret_cast<uint16_t *>(dsm + S.B);
-  // per-warp queue / visited set / tail of warp_bfs, after the tables
+  // per-warp queue / visited set / tail of warp_bfs and the popped row's mask
   uint32_t *wbase = dsm + (table_words(S.B)) + (size_t)(threadIdx.x >> 5) * WARP_WORDS;
   uint32_t *wq = wbase, *whs = wbase + QCAP, *wtail = wbase + QCAP + HCAP;
+  uint32_t *wm = wbase + QCAP + HCAP + 1;
+  uint8_t *wl = reinterpret_cast<uint8_t *>(wm + MAX_BW);
+  LStack lst;
+  lst.row = wm + MAX_BW + MAX_BW / 4;
+  lst.x = lst.row + LCAP;
+  lst.cnt = lst.x + LCAP;
+  lst.keep = S.lkeep;
+  uint32_t *sdl = dsm + table_words(S.B) + SEL_WARPS * WARP_WORDS;  // block's copy of dl[B]
   __shared__ Best sh[33];
   load_tables(S, shr, tab);
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t nth = (size_t)gridDim.x * blockDim.x;
   const size_t gwarp = tid >> 5, nwarps = nth >> 5;
-  unsigned long long lvls = 0;
+  const int lane = threadIdx.x & 31;
+  // ---- prologue: every chunk maximum; arm the first step
+  if (S.track) refresh_chunks(S, 0, true, sh);
+  if (tid == 0) {
+    S.qc[QC_PROD + 16 * (par0 & 1)] = nwarps;  // every warp produces in B
+    S.dcnt[par0 & 1] = 0;
+    S.tcnt[par0 & 1] = 0;
+    S.dense[par0 & 1] = 0;
+  }
+  grid.sync();
+  unsigned long long tstart = ld_acq(S.qc + QC_TAIL);  // stable: no traversal running
   for (uint32_t step = 0; step < O.k; step++) {
-    S.par = step & 1;
-    const uint32_t prev = S.par ^ 1;
-    // ---- A1: refresh the chunk maxima whose gains changed; clear the
-    //          previous step's visited bits
-    const bool all = ((volatile int *)S.alldirty)[prev];
-    const uint32_t nd = all ? S.nchunks : ((volatile uint32_t *)S.dcnt)[prev];
-    for (uint32_t t = blockIdx.x; t < nd; t += gridDim.x) {
-      const uint32_t c = all ? t : __ldcg(S.dlist + (size_t)prev * S.nchunks + t);
-      const size_t v0 = (size_t)c << S.csh, v1 = min((size_t)S.nv, v0 + ((size_t)1 << S.csh));
-      Best b{LLONG_MIN, 0xFFFFFFFFu};
-      for (size_t v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
-        const long long g = __ldcg(S.target + v);
-        if (better(g, (uint32_t)v, b.g, b.v)) {
-          b.g = g;
-          b.v = (uint32_t)v;
-        }
+    if (__ldcg(S.diag + DG_ABORT)) break;  // uniform: read after a barrier
+    S.par = (par0 + step) & 1;
+    S.tlstep = step;
+    const uint32_t nxt = S.par ^ 1;
+    stamp(S, step, 0);
+    // ---- A: every block reduces the chunk maxima -> s
+    uint32_t s;
+    long long sg = 0;
+    if (O.given == NONE) {
+      Best c{LLONG_MIN, 0xFFFFFFFFu};
+      for (uint32_t i = threadIdx.x; i < S.nchunks; i += blockDim.x) {
+        Best x;
+        x.g = __ldcg(&S.cmax[i].g);
+        x.v = __ldcg(&S.cmax[i].v);
+        if (better(x.g, x.v, c.g, c.v)) c = x;
       }
-      b = block_best(b, sh);
-      if (threadIdx.x == 0) {
-        S.cmax[c] = b;
-        S.cdirty[c] = 0;
-      }
+      c = block_best(c, sh);
+      s = c.v;
+      sg = c.g;
+    } else {
+      s = O.given;
     }
-    {  // rows visited by the previous step: clear their visited bits and flags
-      const uint32_t nt = ((volatile uint32_t *)S.fcnt)[8 + prev];
-      for (size_t t = tid; t < (size_t)nt * S.BW; t += nth) {
-        const uint32_t r = __ldcg(S.touched + (size_t)prev * S.nr + t / S.BW);
-        S.vis[(size_t)r * S.BW + (t % S.BW)] = 0;
-        if (t % S.BW == 0) S.tflag[r] = 0;
-      }
-    }
-    // level-0/1 list sizes for this step's BFS (nobody reads them before the
-    // barrier; the previous step's loop exit only read zero ones)
-    if (tid == 0) S.fcnt[0] = S.fcnt[1] = S.fcnt[4] = S.fcnt[5] = 0;
-    grid.sync();
-    // ---- A2: every block reduces the chunk maxima -> s
-    Best c{LLONG_MIN, 0xFFFFFFFFu};
-    for (uint32_t i = threadIdx.x; i < S.nchunks; i += blockDim.x) {
-      Best x;
-      x.g = __ldcg(&S.cmax[i].g);
-      x.v = __ldcg(&S.cmax[i].v);
-      if (better(x.g, x.v, c.g, c.v)) c = x;
-    }
-    c = block_best(c, sh);
-    const uint32_t s = c.v;
     const uint32_t srow = S.cid[s];
+    stamp(S, step, 1);
     if (tid == 0) {
-      S.alldirty[prev] = 0;
-      S.dcnt[prev] = 0;
-      S.dense[prev] = 0;
-      S.fcnt[8 + prev] = 0;  // the previous step's touched rows were cleared in A1
+      // reservations past the end of the previous traversal are void (every
+      // consumer reserves only after all of B, including this warp's, is done)
+      S.qc[QC_HEAD] = tstart;
       O.seeds[step] = s;
-      O.arg_gain[step] = c.g;
-      S.target[s] = -1;  // s leaves the candidate set (R6)
-      mark_dirty(S, s);
+      O.arg_gain[step] = sg;
+      if (O.given == NONE) {
+        S.target[s] = -1;  // s leaves the candidate set (R6)
+        mark_dirty(S, s >> S.csh);
+      }
     }
     // ---- B: MarkSeed, one warp per slot; small newly covered CCs are
-    //          enumerated right here by the warp (warp_bfs) unless they are
-    //          larger than its queue or reach a high-degree vertex, which
-    //          defers them to the grid-wide BFS below
+    //          enumerated right here by the warp (warp_bfs); the others are
+    //          handed to the shared traversal through the seed row's mask
     {
-      const int lane = threadIdx.x & 31;
-      unsigned long long dsum = 0;
+      unsigned long long dsum = 0, nwarp = 0, ndef = 0;
       for (size_t j = gwarp; j < S.B; j += nwarps) {
         uint32_t d = 0;
         if (lane == 0) d = cover_slot(S, srow, (uint32_t)j);
@@ -470,76 +910,53 @@ __global__ void __launch_bounds__(SEL_THREADS) k_select(Sel S0, SelOut O) {
         const uint32_t small = __shfl_sync(0xffffffffu, lane == 0 ? __ldcg(S.dl + j) : 0u, 0);
         if (small) {
           bool done = false;
-          if (small <= QCAP) done = warp_bfs(S, s, (uint32_t)j, small, wq, whs, wtail, shr);
-          if (!done && lane == 0) defer_slot(S, s, srow, (uint32_t)j);
+          if (S.warp_ok && small <= QCAP)
+            done = warp_bfs(S, s, (uint32_t)j, small, wq, whs, wtail, shr);
+          if (done) {
+            nwarp++;
+          } else {
+            ndef++;
+            if (lane == 0) reach(S, srow, s, (uint32_t)j >> 5, 1u << (j & 31), nullptr);
+          }
           __syncwarp();
         }
       }
-      if (lane == 0 && dsum) atomicAdd((unsigned long long *)&O.gain_num[step], dsum);
-    }
-    grid.sync();
-    // ---- C1: multi-slot BFS over the small newly covered CCs
-    for (uint32_t lvl = 0;; lvl++) {
-      // uniform decisions: counts read after a barrier
-      const uint32_t nl = __ldcg(S.fcnt + lvl % 3), nh = __ldcg(S.fcnt + 4 + lvl % 3);
-      if (nl == 0 && nh == 0) break;
-      if (tid == 0) S.fcnt[(lvl + 2) % 3] = S.fcnt[4 + (lvl + 2) % 3] = 0;  // level + 2
-      bfs_level(S, lvl, shr, tab, s);
-      grid.sync();
-      if (nh) {
-        clear_heavy(S, lvl, tid, nth);
-        grid.sync();
+      if (lane == 0) {
+        if (dsum) atomicAdd((unsigned long long *)&O.gain_num[step], dsum);
+        if (S.diag && (nwarp | ndef)) {
+          atomicAdd(S.diag + DG_WARP, nwarp);
+          atomicAdd(S.diag + DG_DEFER, ndef);
+        }
+        add_release(S.qc + QC_PROD + 16 * S.par, ~0ull);  // -1, after this warp's updates
       }
-      lvls++;
     }
-    // ---- C2: dense pass for big CCs (uniform decision after the barrier)
-    if (__ldcg(S.dense + S.par)) {
+    stamp(S, step, 2);
+    // ---- C: the shared traversal, until quiescence
+    const unsigned long long tend =
+        queue_phase(S, s, wm, wl, shr, tab, sdl, S.qc + QC_PROD + 16 * S.par, &lst);
+    stamp(S, step, 4);
+    // ---- D: dense pass for big CCs (the flag is final: every B is done)
+    const bool dense = __ldcg(S.dense + S.par) != 0;
+    if (dense) {
       apply_dense(S, s, gwarp, nwarps);
-      if (tid == 0) S.alldirty[S.par] = 1;
+      if (tid == 0 && S.diag) atomicAdd(S.diag + DG_DENSE, 1ull);
       grid.sync();
     }
-  }
-  if (tid == 0) *O.levels = lvls;
-}
-
-// ------------------------------------------------ multi-rank step kernels
-__global__ void k_cover_slots(Sel S, uint32_t s, unsigned long long *sum) {
-  const uint32_t srow = S.cid[s];
-  unsigned long long d = 0;
-  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < S.B; j += gridDim.x * blockDim.x) {
-    d += cover_slot(S, srow, j);
-    if (S.dl[j]) defer_slot(S, s, srow, j);  // all small CCs: grid BFS
-  }
-  if (d) atomicAdd(sum, d);
-}
-
-__global__ void __launch_bounds__(SEL_THREADS) k_bfs_level(Sel S, uint32_t lvl, uint32_t s) {
-  extern __shared__ uint32_t dsm[];
-  uint32_t *shr = dsm;
-  uint16_t *tab = reinterpret_cast<uint16_t *>(dsm + S.B);
-  load_tables(S, shr, tab);
-  bfs_level(S, lvl, shr, tab, s);
-}
-
-__global__ void __launch_bounds__(256) k_dense(Sel S, uint32_t s) {
-  if (!((volatile int *)S.dense)[S.par]) return;
-  apply_dense(S, s, ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5,
-              ((size_t)gridDim.x * blockDim.x) >> 5);
-}
-
-__global__ void k_clear_heavy(Sel S, uint32_t lvl) {
-  clear_heavy(S, lvl, (uint64_t)blockIdx.x * blockDim.x + threadIdx.x,
-              (uint64_t)gridDim.x * blockDim.x);
-}
-
-__global__ void k_clear_touched(Sel S) {  // multi-rank calls use parity 0
-  const uint32_t nt = S.fcnt[8];
-  for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < (size_t)nt * S.BW;
-       t += (size_t)gridDim.x * blockDim.x)
-  {
-    const uint32_t r = S.touched[t / S.BW];
-    S.vis[(size_t)r * S.BW + (t % S.BW)] = 0;
-    if (t % S.BW == 0) S.tflag[r] = 0;
+    stamp(S, step, 5);
+    // ---- E: chunk maxima of this step, clean-up, re-arm parity nxt
+    if (S.track) refresh_chunks(S, S.par, dense, sh);
+    clear_touched(S, S.par, tid, nth);
+    if (tid == 0) {
+      S.qc[QC_PROD + 16 * nxt] = nwarps;
+      S.dcnt[nxt] = 0;
+      S.tcnt[nxt] = 0;
+      S.dense[nxt] = 0;
+      if (S.diag) atomicAdd(S.diag + DG_STEPS, 1ull);
+    }
+    stamp(S, step, 6);
+    grid.sync();
+    stamp(S, step, 7);
+    tstart = tend;
   }
 }
 
@@ -578,16 +995,26 @@ __global__ void __launch_bounds__(SEL_THREADS) k_argmax_final(const Best *partia
   if (threadIdx.x == 0) *out = c;
 }
 
+// empty ring: slot i expects ticket i
+__global__ void k_ring_init(Item *ring, unsigned long long Q) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < Q;
+       i += (size_t)gridDim.x * blockDim.x)
+    ring[i] = Item{(uint32_t)i, NONE, 0, 0};
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ host
-static size_t table_smem(uint32_t B) {
-  return ((size_t)B * 4 + ((1u << PACIM_TB) + 1) * 2 + 15) & ~(size_t)15;
+static uint64_t env_u64(const char *name, uint64_t dflt) {
+  const char *e = getenv(name);
+  return e ? (uint64_t)std::max(1LL, atoll(e)) : dflt;
 }
 
-// Device state shared by the single-rank kernel and the multi-rank calls.
+// Device state shared by the single-rank selection and the multi-rank steps.
 static Sel make_sel(pacim_ctx *ctx, long long *target) {
   const uint32_t B = ctx->R_local, n = ctx->n, nr = ctx->nr;
+  PC_REQUIRE((B + 31) / 32 <= MAX_BW, PACIM_ENOTIMPL,
+             "selection supports at most 1024 local sketches per context");
   Sel S;
   S.off = ctx->off.as<uint64_t>();
   S.nbr = ctx->nbr.as<uint32_t>();
@@ -605,11 +1032,18 @@ static Sel make_sel(pacim_ctx *ctx, long long *target) {
   S.cid = ctx->cid.as<uint32_t>();
   S.rmap = ctx->rmap.as<uint32_t>();
   S.target = target;
-  S.big_t = BIG_DEFAULT;
-  if (const char *e = getenv("PACIM_BIG_T"))  // tests: force the dense path
-    S.big_t = (uint32_t)std::max(1L, atol(e));
+  // dense pass only for CCs whose traversal would cost more than streaming
+  // the store (tests force it down with PACIM_BIG_T)
+  S.big_t = (uint32_t)env_u64("PACIM_BIG_T", std::max<uint64_t>(65536, nr / 8));
+  S.warp_ok = getenv("PACIM_NO_WARP_BFS") == nullptr;
+  S.ch = (uint32_t)env_u64("PACIM_CHUNK", CH_DEFAULT);
+  S.lkeep = (uint32_t)std::min<uint64_t>(16, getenv("PACIM_LKEEP") ? atoll(getenv("PACIM_LKEEP")) : 2);
+  S.hidx = ctx->hidx.as<uint32_t>();
+  S.hla_off = ctx->hla_ok ? ctx->hla_off.as<unsigned long long>() : nullptr;
+  S.hla_row = ctx->hla_row.as<uint32_t>();
+  S.max_sleep = (uint32_t)env_u64("PACIM_MAX_SLEEP", 4096);
   // argmax cache geometry: <= MAX_CHUNKS chunks of 2^csh vertices
-  uint32_t csh = 12;
+  uint32_t csh = 10;
   while (((uint64_t)n + (1ull << csh) - 1) >> csh > MAX_CHUNKS) csh++;
   S.csh = csh;
   S.nchunks = (uint32_t)(((uint64_t)n + (1ull << csh) - 1) >> csh);
@@ -624,40 +1058,72 @@ static Sel make_sel(pacim_ctx *ctx, long long *target) {
   S.dense = reinterpret_cast<int *>(base + 3 * (size_t)B);
   S.cov_cnt = reinterpret_cast<unsigned long long *>(base + head_words);
   S.cov_list = S.cov_cnt + 1;
-  // argmax cache: cmax[nchunks], cdirty[nchunks], dlist[2][nchunks], dcnt[2], alldirty[2]
+  // argmax cache: cmax[nchunks], cdirty[nchunks], dlist[2][nchunks], dcnt[2]
   pc_ensure(ctx, ctx->sel_partial, (size_t)S.nchunks * (sizeof(Best) + 12) + 64);
   S.cmax = ctx->sel_partial.as<Best>();
   S.cdirty = reinterpret_cast<uint32_t *>(S.cmax + S.nchunks);
   S.dlist = S.cdirty + S.nchunks;
   S.dcnt = S.dlist + 2 * (size_t)S.nchunks;
-  S.alldirty = reinterpret_cast<int *>(S.dcnt + 2);
-  // BFS state: vis, fmask[2], inl[2], flist[2], touched, fcnt[3]
+  // traversal state (words): qc[QC_WORDS] u64, diag[DG_WORDS] u64, tcnt[4],
+  // vis, pend (rows x BW each), inq, tflag, touched[2] (rows each), ring (Q
+  // items of 4 words).  Outstanding row items <= rows (one per row at a
+  // time); chunk items are queued only while fewer than Q/2 items are
+  // outstanding, so Q >= 2 (rows + 2^18) never blocks a producer for good.
+  uint64_t qcap = 1024;
+  while (qcap < 2ull * ((uint64_t)nr + (1ull << 18))) qcap <<= 1;
   const size_t bw = (size_t)nr * S.BW;
-  // words: vis, fmask[2], inl[2], flist[2], hlist[2], touched[2], tflag, fcnt[16]
-  const size_t words = 3 * bw + 9 * (size_t)nr + 16;
+  const size_t head = 2 * QC_WORDS + 2 * DG_WORDS + 4;
+  const size_t words = head + 2 * bw + 4 * (size_t)nr + 4 * qcap + 4;
   if (ctx->bfs.bytes < words * 4 || ctx->bfs_nr != nr || ctx->bfs_bw != S.BW) {
-    // new layout: every mask, flag and counter starts at zero
+    // new layout: every mask, flag and counter starts at zero, the ring empty
     pc_ensure(ctx, ctx->bfs, words * 4);
     PC_CUDA(cudaMemsetAsync(ctx->bfs.p, 0, words * 4, ctx->stream));
     ctx->bfs_nr = nr;
     ctx->bfs_bw = S.BW;
+    ctx->bfs_ring_reset = true;
+    ctx->sel_par = 0;
   }
   uint32_t *q = ctx->bfs.as<uint32_t>();
-  S.vis = q;
-  S.fmask = q + bw;
-  S.inl = q + 3 * bw;
-  S.flist = S.inl + 2 * (size_t)nr;
-  S.hlist = S.flist + 2 * (size_t)nr;
-  S.touched = S.hlist + 2 * (size_t)nr;
-  S.tflag = S.touched + 2 * (size_t)nr;
-  S.fcnt = S.tflag + nr;
-  S.heavy_deg = 4096;
+  S.qc = reinterpret_cast<unsigned long long *>(q);
+  S.diag = S.qc + QC_WORDS;
+  S.tcnt = q + 2 * QC_WORDS + 2 * DG_WORDS;
+  S.vis = q + head;
+  S.pend = S.vis + bw;
+  S.inq = S.pend + bw;
+  S.tflag = S.inq + nr;
+  S.touched = S.tflag + nr;
+  S.ring = reinterpret_cast<Item *>(S.touched + 2 * (size_t)nr + ((4 - (head + 2 * bw) % 4) % 4));
+  S.qmask = qcap - 1;
+  S.qguard = qcap / 2;
+  if (ctx->bfs_ring_reset) {
+    k_ring_init<<<pc_grid(ctx, qcap, 256), 256, 0, ctx->stream>>>(S.ring, qcap);
+    PC_CHECK_LAUNCH();
+    ctx->bfs_ring_reset = false;
+  }
   S.par = 0;
   S.track = 0;
+  S.tl = nullptr;
+  S.tlstep = 0;
+  S.ilog = nullptr;
+  S.ilog_cap = 0;
   return S;
 }
 
-// clear covered bits of the previous selection and the BFS bookkeeping
+static size_t sel_smem(uint32_t B) {
+  return (size_t)table_words(B) * 4 + (size_t)SEL_WARPS * WARP_WORDS * 4 + (size_t)B * 4;
+}
+
+static unsigned sel_grid(pacim_ctx *ctx, size_t smem) {
+  PC_REQUIRE(smem <= 200 * 1024, PACIM_ENOTIMPL, "too many sketch slots for k_select");
+  PC_CUDA(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0;
+  PC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_select, SEL_THREADS, smem));
+  PC_REQUIRE(occ >= 1, PACIM_ECUDA, "k_select cannot be resident");
+  const int bps = (int)env_u64("PACIM_SEL_BPS", 1);  // resident blocks per SM
+  return (unsigned)ctx->sm_count * (unsigned)std::min(occ, bps);
+}
+
+// clear covered bits of the previous selection and the traversal bookkeeping
 static void uncover(pacim_ctx *ctx, const Sel &S) {
   unsigned long long cnt = 0;
   if (ctx->sel_list_valid) {
@@ -670,9 +1136,10 @@ static void uncover(pacim_ctx *ctx, const Sel &S) {
   PC_CUDA(cudaMemsetAsync(S.cov_cnt, 0, 8, ctx->stream));
   PC_CUDA(cudaMemsetAsync(S.dense, 0, 8, ctx->stream));
   PC_CUDA(cudaMemsetAsync(S.cov_root, 0xFF, (size_t)S.B * 4, ctx->stream));
-  PC_CUDA(cudaMemsetAsync(S.vis, 0, (size_t)S.nr * S.BW * 4, ctx->stream));
-  PC_CUDA(cudaMemsetAsync(S.tflag, 0, (size_t)S.nr * 4, ctx->stream));
-  PC_CUDA(cudaMemsetAsync(S.fcnt, 0, 64, ctx->stream));
+  // diagnostics.  Queue tickets keep counting (the ring's sequence numbers
+  // follow them); visited bits, touched flags, pending bits and queue flags
+  // are all clear after every completed step.
+  PC_CUDA(cudaMemsetAsync(S.diag, 0, DG_WORDS * 8, ctx->stream));
   ctx->sel_list_valid = true;
 }
 
@@ -680,6 +1147,21 @@ void pc_select_reset(pacim_ctx *ctx) {
   Sel S = make_sel(ctx, nullptr);
   uncover(ctx, S);
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+static void read_diag(pacim_ctx *ctx, const Sel &S) {
+  unsigned long long d[DG_WORDS];
+  PC_CUDA(cudaMemcpyAsync(d, S.diag, sizeof(d), cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->stats.select_member_updates = 0;
+  ctx->stats.select_bfs_visits = d[DG_ROWS] + d[DG_CHUNKS];
+  ctx->stats.select_dense_steps = d[DG_DENSE];
+  ctx->stats.select_warp_slots = d[DG_WARP];
+  ctx->stats.select_deferred_slots = d[DG_DEFER];
+  ctx->stats.select_row_items = d[DG_ROWS];
+  ctx->stats.select_chunk_items = d[DG_CHUNKS];
+  ctx->stats.select_inline_rows = d[DG_INLINE];
+  PC_REQUIRE(!d[DG_ABORT], PACIM_ECHECK, "select: traversal watchdog expired (internal error)");
 }
 
 void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
@@ -701,17 +1183,12 @@ void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
   pc_ensure(ctx, ctx->sel_seeds, (size_t)k * 4);
   SelOut O;
   O.k = k;
+  O.given = NONE;
   O.seeds = ctx->sel_seeds.as<uint32_t>();
   O.gain_num = ctx->sel_gain.as<long long>();
   O.arg_gain = O.gain_num + k;
-  O.levels = reinterpret_cast<unsigned long long *>(O.gain_num + 2 * k);
-  const size_t smem = (size_t)table_words(S.B) * 4 + (SEL_THREADS / 32) * WARP_WORDS * 4;
-  PC_REQUIRE(smem <= 200 * 1024, PACIM_ENOTIMPL, "too many sketch slots for k_select");
-  PC_CUDA(cudaFuncSetAttribute(k_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  int occ = 0;
-  PC_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_select, SEL_THREADS, smem));
-  PC_REQUIRE(occ >= 1, PACIM_ECUDA, "k_select cannot be resident");
-  const unsigned grid = (unsigned)ctx->sm_count * (unsigned)std::min(occ, 2);
+  const size_t smem = sel_smem(S.B);
+  const unsigned grid = sel_grid(ctx, smem);
   cudaEvent_t e0, e1;
   PC_CUDA(cudaEventCreate(&e0));
   PC_CUDA(cudaEventCreate(&e1));
@@ -722,15 +1199,52 @@ void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
   PC_CUDA(cudaMemsetAsync(ctx->sel_gain.p, 0, (size_t)k * 16 + 64, ctx->stream));
   PC_CUDA(cudaMemsetAsync(S.cdirty, 0, (size_t)S.nchunks * 4, ctx->stream));
   PC_CUDA(cudaMemsetAsync(S.dcnt, 0, 8, ctx->stream));
-  // step 0 reads the buffer of "step -1" (parity 1): everything dirty
-  static const int init_all[2] = {0, 1};
-  PC_CUDA(cudaMemcpyAsync(S.alldirty, init_all, 8, cudaMemcpyHostToDevice, ctx->stream));
-  void *args[] = {&S, &O};
+  uint32_t par0 = ctx->sel_par;
+  TmpBuf tlb(ctx);
+  const bool timeline = getenv("PACIM_TIMELINE") != nullptr;
+  if (timeline) {
+    pc_ensure(ctx, tlb, (size_t)k * 64);
+    S.tl = tlb.as<unsigned long long>();
+  }
+  TmpBuf ilb(ctx);
+  const char *ilog_path = getenv("PACIM_ITEMLOG");
+  if (ilog_path) {
+    S.ilog_cap = 4u << 20;
+    pc_ensure(ctx, ilb, (S.ilog_cap * 4 + 4) * 8);
+    PC_CUDA(cudaMemsetAsync(ilb.p, 0, 32, ctx->stream));
+    S.ilog = ilb.as<unsigned long long>();
+  }
+  void *args[] = {&S, &O, &par0};
   PC_CUDA(cudaLaunchCooperativeKernel((void *)k_select, grid, SEL_THREADS, args, smem, ctx->stream));
   PC_CUDA(cudaEventRecord(e1, ctx->stream));
-  std::vector<long long> hg(2 * (size_t)k + 1);
+  if (ilog_path) {  // raw item log -> file (u64 count, then 4 x u64 per item)
+    unsigned long long cnt = 0;
+    PC_CUDA(cudaMemcpyAsync(&cnt, S.ilog, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    cnt = std::min(cnt, S.ilog_cap);
+    std::vector<unsigned long long> h(cnt * 4 + 4);
+    PC_CUDA(cudaMemcpyAsync(h.data(), S.ilog, (cnt * 4 + 4) * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    h[0] = cnt;
+    if (FILE *f = fopen(ilog_path, "wb")) {
+      fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
+    }
+  }
+  if (timeline) {  // mean ns per phase over the steps, on stderr
+    std::vector<unsigned long long> h((size_t)k * 8);
+    PC_CUDA(cudaMemcpyAsync(h.data(), S.tl, (size_t)k * 64, cudaMemcpyDeviceToHost, ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    double acc[8] = {0};
+    for (uint32_t i = 0; i < k; i++)
+      for (int p = 1; p < 8; p++) acc[p] += (double)(h[i * 8 + p] - h[i * 8 + p - 1]);
+    fprintf(stderr, "timeline us/step: A %.2f B %.2f waitB %.2f queue %.2f dense %.2f E %.2f sync %.2f\n",
+            acc[1] / k / 1e3, acc[2] / k / 1e3, acc[3] / k / 1e3, acc[4] / k / 1e3, acc[5] / k / 1e3,
+            acc[6] / k / 1e3, acc[7] / k / 1e3);
+  }
+  std::vector<long long> hg(2 * (size_t)k);
   PC_CUDA(cudaMemcpyAsync(seeds, O.seeds, (size_t)k * 4, cudaMemcpyDeviceToHost, ctx->stream));
-  PC_CUDA(cudaMemcpyAsync(hg.data(), O.gain_num, (2 * (size_t)k + 1) * 8, cudaMemcpyDeviceToHost,
+  PC_CUDA(cudaMemcpyAsync(hg.data(), O.gain_num, (2 * (size_t)k) * 8, cudaMemcpyDeviceToHost,
                           ctx->stream));
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
   float ms = 0;
@@ -739,7 +1253,8 @@ void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
   cudaEventDestroy(e1);
   ctx->stats.t_select_ms = ms;
   ctx->stats.kernel_launches_select = 2;
-  ctx->stats.select_member_updates = (uint64_t)hg[2 * (size_t)k];  // BFS levels run
+  read_diag(ctx, S);
+  ctx->sel_par = (par0 + k) & 1;
   long long run = 0;
   bool ok = true;
   for (uint32_t i = 0; i < k; i++) {
@@ -751,43 +1266,32 @@ void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
   PC_REQUIRE(ok, PACIM_ECHECK, "select: sum_r delta_r differs from the argmax gain");
 }
 
+// One multi-rank step: MarkSeed of the given seed s on this ctx's sketches and
+// the member deltas (-delta per member) accumulated into d_delta.
 void pc_cover_local(pacim_ctx *ctx, uint32_t s, int64_t *d_delta, int64_t *local_gain) {
   PC_REQUIRE(ctx->sel_list_valid, PACIM_ESTATE, "pacim_select_reset first");
   Sel S = make_sel(ctx, reinterpret_cast<long long *>(d_delta));
-  pc_ensure(ctx, ctx->sel_flag, 64);
-  unsigned long long *sum = ctx->sel_flag.as<unsigned long long>();
-  PC_CUDA(cudaMemsetAsync(sum, 0, 8, ctx->stream));
-  PC_CUDA(cudaMemsetAsync(S.dense, 0, 8, ctx->stream));
-  // previous call's visited rows, then the seed's row as the BFS start
-  k_clear_touched<<<pc_grid(ctx, (size_t)S.nr, 256), 256, 0, ctx->stream>>>(S);
-  // list and touched counters start empty; k_cover_slots defers the small
-  // CCs (seed row into the level-0 list) and records touched rows
-  PC_CUDA(cudaMemsetAsync(S.fcnt, 0, 64, ctx->stream));
-  k_cover_slots<<<(S.B + 255) / 256, 256, 0, ctx->stream>>>(S, s, sum);
-  PC_CHECK_LAUNCH();
-  const size_t smem = table_smem(S.B);
-  PC_CUDA(cudaFuncSetAttribute(k_bfs_level, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  for (uint32_t lvl = 0;; lvl++) {
-    uint32_t c[7];
-    PC_CUDA(cudaMemcpyAsync(c, S.fcnt, 28, cudaMemcpyDeviceToHost, ctx->stream));
-    PC_CUDA(cudaStreamSynchronize(ctx->stream));
-    const uint32_t nl = c[lvl % 3], nh = c[4 + lvl % 3];
-    if (!nl && !nh) break;
-    PC_CUDA(cudaMemsetAsync(S.fcnt + (lvl + 2) % 3, 0, 4, ctx->stream));
-    PC_CUDA(cudaMemsetAsync(S.fcnt + 4 + (lvl + 2) % 3, 0, 4, ctx->stream));
-    k_bfs_level<<<ctx->sm_count * 2, SEL_THREADS, smem, ctx->stream>>>(S, lvl, s);
-    PC_CHECK_LAUNCH();
-    if (nh) {
-      k_clear_heavy<<<pc_grid(ctx, (size_t)nh * S.BW, 256), 256, 0, ctx->stream>>>(S, lvl);
-      PC_CHECK_LAUNCH();
-    }
-
-  }
-  k_dense<<<pc_grid(ctx, (size_t)S.nr * 32, 256, 8), 256, 0, ctx->stream>>>(S, s);
-  PC_CHECK_LAUNCH();
-  unsigned long long h = 0;
-  PC_CUDA(cudaMemcpyAsync(&h, sum, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  pc_ensure(ctx, ctx->sel_gain, 64);
+  pc_ensure(ctx, ctx->sel_seeds, 16);
+  SelOut O;
+  O.k = 1;
+  O.given = s;
+  O.seeds = ctx->sel_seeds.as<uint32_t>();
+  O.gain_num = ctx->sel_gain.as<long long>();
+  O.arg_gain = O.gain_num + 1;
+  PC_CUDA(cudaMemsetAsync(O.gain_num, 0, 16, ctx->stream));
+  const size_t smem = sel_smem(S.B);
+  const unsigned grid = sel_grid(ctx, smem);
+  uint32_t par0 = ctx->sel_par;
+  void *args[] = {&S, &O, &par0};
+  PC_CUDA(cudaLaunchCooperativeKernel((void *)k_select, grid, SEL_THREADS, args, smem, ctx->stream));
+  ctx->sel_par ^= 1;
+  long long h = 0;
+  unsigned long long abort_flag = 0;
+  PC_CUDA(cudaMemcpyAsync(&h, O.gain_num, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaMemcpyAsync(&abort_flag, S.diag + DG_ABORT, 8, cudaMemcpyDeviceToHost, ctx->stream));
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  PC_REQUIRE(!abort_flag, PACIM_ECHECK, "cover: traversal watchdog expired (internal error)");
   *local_gain = (int64_t)h;
 }
 

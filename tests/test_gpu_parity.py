@@ -92,6 +92,23 @@ def test_dense_cover_path(orc, ctx, i, monkeypatch):
     test_tiny_corpus_parity(orc, ctx, i)
 
 
+@pytest.mark.parametrize("env", [
+    {"PACIM_NO_WARP_BFS": "1"},                        # every CC through the queue
+    {"PACIM_NO_WARP_BFS": "1", "PACIM_CHUNK": "2"},    # rows split into 2-edge chunk items
+    {"PACIM_CHUNK": "3", "PACIM_BIG_T": "40"},         # all three cover paths mixed
+    {"PACIM_NO_WARP_BFS": "1", "PACIM_HUB_DEG": "4", "PACIM_FORCE_HLA": "1"},  # hubs via live lists
+    {"PACIM_HUB_DEG": "2", "PACIM_FORCE_HLA": "1", "PACIM_CHUNK": "5"},
+])
+@pytest.mark.parametrize("i", [0, 2, 3, 7, 8, 9])
+def test_traversal_paths(orc, ctx, i, env, monkeypatch):
+    """The shared traversal of the cover step (row items and chunk items of
+    the work queue), forced on the tiny corpus by shrinking the chunk size and
+    disabling the warp-local BFS; must give the oracle's greedy."""
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    test_tiny_corpus_parity(orc, ctx, i)
+
+
 def test_edge_cases(orc, ctx, pc):
     from oracle.oracle import Graph
     # single vertex, no edges, k = n = 1
@@ -230,13 +247,18 @@ def test_c4_full_scale_sampled(ctx):
 
 
 # ------------------------------------------------ multi-rank primitives
-@pytest.mark.parametrize("big_t", [None, "6"])
-def test_rank_emulation_matches_single(orc, pc, big_t, monkeypatch):
+@pytest.mark.parametrize("big_t,chunk", [(None, None), ("6", None), (None, "3")])
+def test_rank_emulation_matches_single(orc, pc, big_t, chunk, monkeypatch):
     """Sketch sharding r = rank mod P with the per-step primitives, ranks run
     one after another on one GPU (no waiting kernels), the collective replaced
     by a host sum: identical to the single-ctx greedy."""
     if big_t:
         monkeypatch.setenv("PACIM_BIG_T", big_t)
+    if chunk:
+        monkeypatch.setenv("PACIM_CHUNK", chunk)
+        monkeypatch.setenv("PACIM_HUB_DEG", "6")
+        monkeypatch.setenv("PACIM_FORCE_HLA", "1")
+        monkeypatch.setenv("PACIM_NO_WARP_BFS", "1")
     from oracle.oracle import Graph
     from paper_2311_07554_b200 import dist
     off, nbr = inputs.random_powerlaw_graph(3000, 15000, 21)
