@@ -3,8 +3,8 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
 
 One step = one pass of the whole hot path over the resident synthetic graph:
-pacim_build_sketches (hash + live test, union-find, compression, CC sizes,
-member index, gain0) followed by pacim_select_seeds (k
+pacim_build_sketches (hash + live test, union-find, compression, CC sizes in
+the root slots, gain0) followed by pacim_select_seeds (k
 greedy steps, H8-H12).  value = R*m / t_step summed over the job (m =
 undirected edges; every logical (edge, sketch) test counted).  e2e repeats the
 step through pacim_load_graph from pinned HOST buffers (H2D inside the timed
@@ -110,9 +110,11 @@ def kernel_bytes(st: dict, cfg: dict, k: int) -> dict:
         "k_init": L,                                        # write every slot
         "k_edges": 16 * m + wic + 8 * st["live_pairs"],     # key + row pair (+T32), 2 slot reads per live pair
         "k_compress_count": L + 8 * nonroot,                # read slots; write root + count per non-root
-        "k_compact": L + 12 * st["ncomp"],                  # read slots; csize+coff per CC
-        "k_gain_scatter": L + 8 * n + 4 * st["nmember"] + 4 * nonroot,  # slots, gain0, perm, root slots
-        "k_select": k * 8 * n + 8 * st["select_member_updates"],  # argmax scans + member updates
+        "k_gain0": L + 8 * n + 4 * nonroot,                 # slots, gain0, root-size reads
+        # traversal reads (CSR entry + WIC threshold) + the dense passes over the
+        # store + one read of the gains per step for the chunk maxima (upper bound)
+        "k_select": (4 + (4 if cfg["pmodel"] == 1 else 0)) * st["select_edges"]
+                    + L * st["select_dense_steps"] + k * 16 * 4096,
     }
 
 
@@ -240,8 +242,7 @@ def main():
     for _ in range(max(3, args.warmup)):
         step()
     # ---------------- device-resident timed region
-    keys = ["t_build_ms", "t_init_ms", "t_edges_ms", "t_compress_ms", "t_compact_ms",
-            "t_gain_ms", "t_select_ms"]
+    keys = ["t_build_ms", "t_init_ms", "t_edges_ms", "t_compress_ms", "t_gain_ms", "t_select_ms"]
     acc = {kk: 0.0 for kk in keys}
     launches = 0
     clocks = ClockSampler(local)
@@ -309,8 +310,8 @@ def main():
     hbm = hbm or 6650.0
     kb = kernel_bytes(st, cfg, k)
     dur = {"k_init": avg["t_init_ms"], "k_edges": avg["t_edges_ms"],
-           "k_compress_count": avg["t_compress_ms"], "k_compact": avg["t_compact_ms"],
-           "k_gain_scatter": avg["t_gain_ms"], "k_select": avg["t_select_ms"]}
+           "k_compress_count": avg["t_compress_ms"], "k_gain0": avg["t_gain_ms"],
+           "k_select": avg["t_select_ms"]}
     dom = max(dur, key=lambda x: dur[x])
     achieved = kb[dom] / (dur[dom] / 1000.0) / 1e9
     traffic = load_traffic().get(args.config, {}).get(dom)
@@ -341,8 +342,10 @@ def main():
         "gpu_launches": launches,
         "roofline": roofline,
         "clocks": clk,
-        "stats": {kk: st[kk] for kk in ("rows", "ncomp", "nmember", "nnonsingle", "live_pairs",
-                                        "device_bytes", "select_member_updates")},
+        "stats": {kk: st[kk] for kk in ("rows", "ncomp", "nnonsingle", "live_pairs", "device_bytes",
+                                        "select_dense_steps", "select_warp_slots",
+                                        "select_deferred_slots", "select_row_items",
+                                        "select_chunk_items", "select_edges")},
         "seeds_head": [int(x) for x in out[0][:8]],
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -88,6 +88,7 @@ typedef struct {
     uint64_t select_row_items;      /* row expansions of the shared traversal */
     uint64_t select_chunk_items;    /* chunk items (CH-edge slices of long rows) */
     uint64_t select_inline_rows;    /* rows expanded without queueing (queue guard) */
+    uint64_t select_edges;          /* CSR entries tested by the shared traversal */
 } pacim_stats;
 
 /* --------------------------------------------------------------- lifecycle */

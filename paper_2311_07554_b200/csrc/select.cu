@@ -121,7 +121,7 @@ enum { QC_TAIL = 0, QC_HEAD = 16, QC_DONE = 32, QC_PROD = 48, QC_WORDS = 80 };
 // diagnostics (u64): steps, dense steps, warp-BFS slots, deferred slots,
 // row items, chunk items, chunks expanded inline (queue guard)
 enum { DG_STEPS = 0, DG_DENSE, DG_WARP, DG_DEFER, DG_ROWS, DG_CHUNKS, DG_INLINE, DG_ABORT,
-       DG_WORDS = 8 };
+       DG_EDGES, DG_WORDS = 10 };
 constexpr unsigned long long WATCHDOG_NS = 4000000000ull;  // a wait this long is a bug: abort
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -637,7 +637,7 @@ __device__ unsigned long long queue_phase(const Sel &S, uint32_t s, uint32_t *wm
   if (qt != ~0ull) return qt;
   for (uint32_t j = threadIdx.x; j < S.B; j += blockDim.x) sdl[j] = __ldcg(S.dl + j);
   __syncthreads();
-  unsigned long long nrow = 0, nchunk = 0, ninl = 0;
+  unsigned long long nrow = 0, nchunk = 0, ninl = 0, nedg = 0;
   for (;;) {
     unsigned long long i = 0, tend = 0;
     uint32_t row = NONE, cw = 0, bits = 0;
@@ -689,6 +689,7 @@ __device__ unsigned long long queue_phase(const Sel &S, uint32_t s, uint32_t *wm
         atomicAdd(S.diag + DG_ROWS, nrow);
         atomicAdd(S.diag + DG_CHUNKS, nchunk);
         atomicAdd(S.diag + DG_INLINE, ninl);
+        atomicAdd(S.diag + DG_EDGES, nedg);
       }
       return __shfl_sync(FULL, tend, 0);
     }
@@ -715,6 +716,7 @@ __device__ unsigned long long queue_phase(const Sel &S, uint32_t s, uint32_t *wm
       if (lane == 0) *ls->cnt = n - 1;
       __syncwarp();
     }
+    nedg += nedges;
     if (lane == 0 && S.ilog) {
       const unsigned long long at = atomicAdd(S.ilog, 1ull);
       if (at < S.ilog_cap) {
@@ -1161,6 +1163,7 @@ static void read_diag(pacim_ctx *ctx, const Sel &S) {
   ctx->stats.select_row_items = d[DG_ROWS];
   ctx->stats.select_chunk_items = d[DG_CHUNKS];
   ctx->stats.select_inline_rows = d[DG_INLINE];
+  ctx->stats.select_edges = d[DG_EDGES];
   PC_REQUIRE(!d[DG_ABORT], PACIM_ECHECK, "select: traversal watchdog expired (internal error)");
 }
 
