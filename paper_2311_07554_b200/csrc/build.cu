@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__res
   uint32_t *shr = sm;
   uint16_t *tab = reinterpret_cast<uint16_t *>(sm + B);
   __shared__ uint32_t w_u[EDGE_WARPS][32], w_v[EDGE_WARPS][32], w_he[EDGE_WARPS][32];
-  __shared__ uint32_t w_lo[EDGE_WARPS][32], w_pre[EDGE_WARPS][33];
+  __shared__ uint32_t w_lo[EDGE_WARPS][32];
   __shared__ uint64_t w_T[EDGE_WARPS][32];
   for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) shr[i] = g_shr[i];
   for (uint32_t i = threadIdx.x; i <= (1u << PACIM_TB); i += blockDim.x) tab[i] = g_tab[i];
@@ -121,7 +121,8 @@ __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__res
   for (size_t base = gw * 32; base < m; base += nw * 32) {
     // ---- one edge per lane: hash and candidate slot range
     const size_t e = base + lane;
-    uint32_t cnt = 0;
+    uint32_t cnt = 0, eu = 0, ev = 0, ehe = 0, elo = 0;
+    uint64_t eT = 0;
     if (e < m) {
       const uint64_t key = keys[e];
       const uint64_t T = WIC ? (uint64_t)tm1[e] + 1 : t32;
@@ -147,36 +148,46 @@ __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__res
       if (hi < lo) hi = lo;
       cnt = hi - lo;
       const uint64_t ck = ckeys[e];  // the endpoints' store rows (+ hub flags)
-      w_u[wid][lane] = (uint32_t)(ck >> 32);
-      w_v[wid][lane] = (uint32_t)ck;
-      w_he[wid][lane] = he;
-      w_T[wid][lane] = T;
-      w_lo[wid][lane] = lo;
+      eu = (uint32_t)(ck >> 32);
+      ev = (uint32_t)ck;
+      ehe = he;
+      eT = T;
+      elo = lo;
     }
-    // ---- exclusive prefix of candidate counts across the warp
+    // ---- compact the edges that have candidates; exclusive prefix of counts
+    const uint32_t nz = __ballot_sync(0xffffffffu, cnt > 0);
     uint32_t inc = cnt;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       uint32_t y = __shfl_up_sync(0xffffffffu, inc, d);
       if (lane >= d) inc += y;
     }
-    w_pre[wid][lane] = inc - cnt;
+    const uint32_t pre = inc - cnt;
     const uint32_t total = __shfl_sync(0xffffffffu, inc, 31);
-    if (lane == 31) w_pre[wid][32] = total;
+    if (cnt) {
+      const uint32_t k = __popc(nz & ((1u << lane) - 1));
+      w_u[wid][k] = eu;
+      w_v[wid][k] = ev;
+      w_he[wid][k] = ehe;
+      if (WIC) w_T[wid][k] = eT;
+      w_lo[wid][k] = elo - pre;  // slot of candidate position idx: w_lo + idx
+    }
     __syncwarp();
-    // ---- 32 (edge, slot) candidate pairs per round
+    // ---- 32 (edge, slot) candidate pairs per round; lane -> edge by the
+    //      start positions of this round (no search): rank = edges started
+    //      before the round + starts at or below the lane, minus one
     for (uint32_t c0 = 0; c0 < total; c0 += 32) {
       const uint32_t idx = c0 + lane;
+      const uint32_t smask =
+          __reduce_or_sync(0xffffffffu, (cnt && pre >= c0 && pre < c0 + 32) ? 1u << (pre - c0) : 0u);
+      const uint32_t before = __popc(__ballot_sync(0xffffffffu, cnt && pre < c0));
       uint32_t j = 0, u = 0, v = 0;
       bool lv = false;
       if (idx < total) {
-        uint32_t a = 0, b = 32;  // largest i with pre[i] <= idx
-        while (b - a > 1) {
-          uint32_t mid = (a + b) >> 1;
-          if (w_pre[wid][mid] <= idx) a = mid; else b = mid;
-        }
-        j = w_lo[wid][a] + (idx - w_pre[wid][a]);
-        lv = (uint64_t)(shr[j] ^ w_he[wid][a]) < w_T[wid][a];
+        const uint32_t a = before + __popc(smask & (0xffffffffu >> (31 - lane))) - 1;
+        j = w_lo[wid][a] + idx;
+        const uint64_t T = WIC ? w_T[wid][a] : t32;
+        lv = (uint64_t)(shr[j] ^ w_he[wid][a]) < T;
         u = w_u[wid][a];
         v = w_v[wid][a];
         if (lv) {
