@@ -205,6 +205,31 @@ PACIM_API int pacim_select_reset(pacim_ctx *ctx);
 PACIM_API int pacim_cover_local(pacim_ctx *ctx, uint32_t s, int64_t *d_delta,
                       int64_t *local_gain);
 
+/* pacim_cover_local plus the same updates as a sparse list (SURVEY §8(e)
+ * sparse per-step deltas): every update d_delta[u] += -delta is also written
+ * as d_list_v[i] = u, d_list_d[i] = -delta (u32 / int64 DEVICE arrays of
+ * `cap` entries; duplicates of u are allowed and add up).  *count (host)
+ * receives the number of updates; when *count > cap the list is incomplete
+ * and the caller must use d_delta (dense fallback).  *local_gain as above. */
+PACIM_API int pacim_cover_local_sparse(pacim_ctx *ctx, uint32_t s, int64_t *d_delta,
+                                       uint32_t *d_list_v, int64_t *d_list_d, uint64_t cap,
+                                       uint64_t *count, int64_t *local_gain);
+
+/* d_gain[v[i]] += d[i] for i < count (the gathered lists of all ranks,
+ * duplicates add up), then d_gain[s] = -1 (the seed leaves the candidates,
+ * R6) unless s == 0xFFFFFFFF.  DEVICE arrays. */
+PACIM_API int pacim_apply_deltas(pacim_ctx *ctx, int64_t *d_gain, const uint32_t *d_v,
+                                 const int64_t *d_d, uint64_t count, uint32_t s);
+
+/* Dense fallback: d_gain += d_delta, d_delta = 0 (n entries), then
+ * d_gain[s] = -1 unless s == 0xFFFFFFFF.  DEVICE arrays. */
+PACIM_API int pacim_apply_dense(pacim_ctx *ctx, int64_t *d_gain, int64_t *d_delta, uint32_t n,
+                                uint32_t s);
+
+/* d_delta[v[i]] = 0 for i < count: clears the dense delta after a sparse step. */
+PACIM_API int pacim_clear_deltas(pacim_ctx *ctx, int64_t *d_delta, const uint32_t *d_v,
+                                 uint64_t count);
+
 /* NextSeed by full scan (H8): *s_out = smallest v with maximal d_gain[v]
  * (entries < 0 never win unless all are), *g_out = d_gain[*s_out]. */
 PACIM_API int pacim_argmax_device(pacim_ctx *ctx, const int64_t *d_gain, uint32_t n,

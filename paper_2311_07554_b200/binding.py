@@ -20,7 +20,8 @@ EXPORTS = [
     "pacim_threshold_from_p", "pacim_load_graph", "pacim_load_graph_device",
     "pacim_generate_graph", "pacim_graph_info", "pacim_get_graph",
     "pacim_build_sketches", "pacim_select_seeds", "pacim_gain0_to_device",
-    "pacim_select_reset", "pacim_cover_local", "pacim_argmax_device",
+    "pacim_select_reset", "pacim_cover_local", "pacim_cover_local_sparse",
+    "pacim_apply_deltas", "pacim_apply_dense", "pacim_clear_deltas", "pacim_argmax_device",
     "pacim_get_gain0", "pacim_get_labels", "pacim_get_center_sketch",
     "pacim_get_stats",
 ]
@@ -84,6 +85,10 @@ def lib():
             "pacim_gain0_to_device": (i32, [P, P]),
             "pacim_select_reset": (i32, [P]),
             "pacim_cover_local": (i32, [P, u32, P, P]),
+            "pacim_cover_local_sparse": (i32, [P, u32, P, P, P, u64, P, P]),
+            "pacim_apply_deltas": (i32, [P, P, P, P, u64, u32]),
+            "pacim_apply_dense": (i32, [P, P, P, u32, u32]),
+            "pacim_clear_deltas": (i32, [P, P, P, u64]),
             "pacim_argmax_device": (i32, [P, P, u32, P, P]),
             "pacim_get_gain0": (i32, [P, P]),
             "pacim_get_labels": (i32, [P, u32, P]),
@@ -200,6 +205,23 @@ class Context:
         g = C.c_int64()
         self._check(self._L.pacim_cover_local(self._h, s, _dptr(d_delta), C.byref(g)))
         return g.value
+
+    def pacim_cover_local_sparse(self, s: int, d_delta, d_list_v, d_list_d, cap: int):
+        """-> (count, local_gain); count > cap means the list is incomplete."""
+        g, c = C.c_int64(), C.c_uint64()
+        self._check(self._L.pacim_cover_local_sparse(self._h, s, _dptr(d_delta), _dptr(d_list_v),
+                                                     _dptr(d_list_d), cap, C.byref(c), C.byref(g)))
+        return c.value, g.value
+
+    def pacim_apply_deltas(self, d_gain, d_v, d_d, count: int, s: int = 0xFFFFFFFF):
+        self._check(self._L.pacim_apply_deltas(self._h, _dptr(d_gain), _dptr(d_v), _dptr(d_d),
+                                               count, s))
+
+    def pacim_apply_dense(self, d_gain, d_delta, n: int, s: int = 0xFFFFFFFF):
+        self._check(self._L.pacim_apply_dense(self._h, _dptr(d_gain), _dptr(d_delta), n, s))
+
+    def pacim_clear_deltas(self, d_delta, d_v, count: int):
+        self._check(self._L.pacim_clear_deltas(self._h, _dptr(d_delta), _dptr(d_v), count))
 
     def pacim_argmax_device(self, d_gain, n: int):
         s, g = C.c_uint32(), C.c_int64()

@@ -311,6 +311,62 @@ int pacim_cover_local(pacim_ctx *ctx, uint32_t s, int64_t *d_delta, int64_t *loc
   });
 }
 
+int pacim_cover_local_sparse(pacim_ctx *ctx, uint32_t s, int64_t *d_delta, uint32_t *d_list_v,
+                             int64_t *d_list_d, uint64_t cap, uint64_t *count,
+                             int64_t *local_gain) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(ctx->built, PACIM_ESTATE, "no sketches");
+    PC_REQUIRE(s < ctx->n && d_delta && local_gain && count && d_list_v && d_list_d,
+               PACIM_EINVAL, "bad argument");
+    // the list counter lives in the ctx (reset per call)
+    pc_ensure(ctx, ctx->sel_flag, 64);
+    unsigned long long *cnt = ctx->sel_flag.as<unsigned long long>() + 4;
+    PC_CUDA(cudaMemsetAsync(cnt, 0, 8, ctx->stream));
+    ctx->dlist.v = d_list_v;
+    ctx->dlist.d = reinterpret_cast<long long *>(d_list_d);
+    ctx->dlist.cnt = cnt;
+    ctx->dlist.cap = cap;
+    try {
+      if (ctx->compressed) {
+        pc_cover_compressed(ctx, s, d_delta, local_gain);
+        PC_CUDA(cudaStreamSynchronize(ctx->stream));
+      } else {
+        pc_cover_local(ctx, s, d_delta, local_gain);
+      }
+    } catch (...) {
+      ctx->dlist = DeltaList{};
+      throw;
+    }
+    ctx->dlist = DeltaList{};
+    unsigned long long h = 0;
+    PC_CUDA(cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    *count = h;
+  });
+}
+
+int pacim_apply_deltas(pacim_ctx *ctx, int64_t *d_gain, const uint32_t *d_v, const int64_t *d_d,
+                       uint64_t count, uint32_t s) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(d_gain && (count == 0 || (d_v && d_d)), PACIM_EINVAL, "bad argument");
+    pc_apply_deltas(ctx, d_gain, d_v, d_d, count, s);
+  });
+}
+
+int pacim_apply_dense(pacim_ctx *ctx, int64_t *d_gain, int64_t *d_delta, uint32_t n, uint32_t s) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(d_gain && d_delta && n >= 1, PACIM_EINVAL, "bad argument");
+    pc_apply_dense(ctx, d_gain, d_delta, n, s);
+  });
+}
+
+int pacim_clear_deltas(pacim_ctx *ctx, int64_t *d_delta, const uint32_t *d_v, uint64_t count) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(d_delta && (count == 0 || d_v), PACIM_EINVAL, "bad argument");
+    pc_clear_deltas(ctx, d_delta, d_v, count);
+  });
+}
+
 int pacim_argmax_device(pacim_ctx *ctx, const int64_t *d_gain, uint32_t n, uint32_t *s_out,
                         int64_t *g_out) {
   return guarded(ctx, [&] {

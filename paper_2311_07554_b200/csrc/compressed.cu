@@ -143,6 +143,7 @@ struct ProbeParams {
   uint32_t *csw;            // [rho][B] working sizes
   const uint8_t *is_seed;
   long long *target;        // gain (or delta) vector, n entries
+  DeltaList dlst;           // multi-rank sparse deltas (v == nullptr: off)
   uint32_t *st;             // per slot: outcome
   uint32_t *lab;            // per slot: label (BIG_KNOWN)
   uint32_t *dl;             // per slot: delta
@@ -253,7 +254,10 @@ __global__ void __launch_bounds__(PROBE_WARPS * 32) k_probe(ProbeParams P, uint3
         // enumerated: q[0..delta) are exactly the CC's members
         for (uint32_t i = lane; i < nvis; i += 32) {
           const uint32_t u = q[w][i];
-          if (u != s) atomicAdd((unsigned long long *)&P.target[u], (unsigned long long)(-(long long)delta));
+          if (u != s) {
+            atomicAdd((unsigned long long *)&P.target[u], (unsigned long long)(-(long long)delta));
+            P.dlst.add(u, -(long long)delta);
+          }
         }
       }
       if (lane == 0 && delta > 0) P.csw[(size_t)label * P.B + j] = 0;  // MarkSeed
@@ -265,7 +269,10 @@ __global__ void __launch_bounds__(PROBE_WARPS * 32) k_probe(ProbeParams P, uint3
       if (delta)
         for (uint32_t i = lane; i < nvis; i += 32) {
           const uint32_t u = q[w][i];
-          if (u != s) atomicAdd((unsigned long long *)&P.target[u], (unsigned long long)(-(long long)delta));
+          if (u != s) {
+            atomicAdd((unsigned long long *)&P.target[u], (unsigned long long)(-(long long)delta));
+            P.dlst.add(u, -(long long)delta);
+          }
         }
     }
     if (lane == 0) {
@@ -337,7 +344,8 @@ __global__ void k_big_decide(uint32_t Bb, uint32_t j0, uint32_t B, uint32_t *st,
 
 __global__ void k_big_apply(const uint32_t *Lb, uint32_t nr, uint32_t Bb, uint32_t j0,
                             const uint32_t *st, const uint32_t *dl, const uint32_t *sroot,
-                            const uint32_t *rmap, uint32_t s, long long *target) {
+                            const uint32_t *rmap, uint32_t s, long long *target,
+                            DeltaList dlst) {
   const int lane = threadIdx.x & 31;
   size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
@@ -351,7 +359,10 @@ __global__ void k_big_apply(const uint32_t *Lb, uint32_t nr, uint32_t Bb, uint32
     for (int q = 16; q; q >>= 1) d += __shfl_xor_sync(0xffffffffu, d, q);
     if (lane == 0 && d) {
       const uint32_t vid = rmap[v];
-      if (vid != s) atomicAdd((unsigned long long *)&target[vid], (unsigned long long)(-d));
+      if (vid != s) {
+        atomicAdd((unsigned long long *)&target[vid], (unsigned long long)(-d));
+        dlst.add(vid, -d);
+      }
     }
   }
 }
@@ -499,6 +510,7 @@ void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *l
   P.csw = ctx->csz_work.as<uint32_t>();
   P.is_seed = ctx->is_seed.as<uint8_t>();
   P.target = reinterpret_cast<long long *>(target);
+  P.dlst = ctx->dlist;
   P.st = st;
   P.lab = lab;
   P.dl = dl;
@@ -544,7 +556,7 @@ void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *l
                                                              sum);
       k_big_apply<<<pc_grid(ctx, (size_t)nr * 32, 256, 16), 256, 0, ctx->stream>>>(
           Lb, nr, bb, j0, st, dl, sroot, ctx->rmap.as<uint32_t>(), s,
-          reinterpret_cast<long long *>(target));
+          reinterpret_cast<long long *>(target), ctx->dlist);
       PC_CHECK_LAUNCH();
       ctx->launches += 4;
     }

@@ -71,6 +71,25 @@ struct DevBuf {
   T *as() const { return reinterpret_cast<T *>(p); }
 };
 
+// Sparse per-step deltas of a multi-rank greedy step: every
+// gain update u -= delta of a cover step is also appended as (u, -delta)
+// (duplicates allowed; their sum is the dense delta).  Entries past cap are
+// dropped and counted, so cnt > cap tells the caller to use the dense vector.
+struct DeltaList {
+  uint32_t *v = nullptr;
+  long long *d = nullptr;
+  unsigned long long *cnt = nullptr;
+  unsigned long long cap = 0;
+  __device__ __forceinline__ void add(uint32_t u, long long delta) const {
+    if (!v) return;
+    const unsigned long long at = atomicAdd(cnt, 1ull);
+    if (at < cap) {
+      v[at] = u;
+      d[at] = delta;
+    }
+  }
+};
+
 struct pacim_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -162,6 +181,8 @@ struct pacim_ctx {
   uint32_t sel_k_cap = 128;     // covered-CC list capacity, in steps
   bool sel_list_valid = false;  // sel_list holds the covered list of this store
 
+  DeltaList dlist;              // set only during pacim_cover_local_sparse
+
   pacim_stats stats{};
   uint32_t launches = 0;
 };
@@ -246,6 +267,10 @@ void pc_cover_local(pacim_ctx *ctx, uint32_t s, int64_t *d_delta,
                     int64_t *local_gain);
 void pc_argmax(pacim_ctx *ctx, const int64_t *d_gain, uint32_t n, uint32_t *s,
                int64_t *g);
+void pc_apply_deltas(pacim_ctx *ctx, int64_t *d_gain, const uint32_t *v, const int64_t *d,
+                     uint64_t count, uint32_t s);
+void pc_apply_dense(pacim_ctx *ctx, int64_t *d_gain, int64_t *d_delta, uint32_t n, uint32_t s);
+void pc_clear_deltas(pacim_ctx *ctx, int64_t *d_delta, const uint32_t *v, uint64_t count);
 void pc_get_labels(pacim_ctx *ctx, uint32_t slot, uint32_t *host_out);
 
 // grid sizing: multiples of the SM count (148 on B200)

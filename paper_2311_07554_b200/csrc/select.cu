@@ -186,6 +186,7 @@ struct Sel {
   uint32_t par, csh, nchunks;
   int track;
   unsigned long long *diag;
+  DeltaList dlst;          // multi-rank sparse deltas (v == nullptr: off)
   uint32_t tlstep;
   unsigned long long *ilog;  // optional item log: [0] count, then {start, end, step, edges} x cap
   unsigned long long ilog_cap;
@@ -213,6 +214,7 @@ __device__ __forceinline__ void touch(const Sel &S, uint32_t row) {
 
 __device__ __forceinline__ void sub_gain(const Sel &S, uint32_t u, long long d) {
   atomicAdd((unsigned long long *)&S.target[u], (unsigned long long)(-d));
+  S.dlst.add(u, -d);
   if (S.track) {
     const uint32_t c = u >> S.csh;
     if (__ldcg(&S.cmax[c].v) == u) mark_dirty(S, c);  // only the chunk's argmax matters
@@ -440,6 +442,7 @@ __device__ __forceinline__ void expand_edge(const Sel &S, uint32_t x, uint32_t w
     for (uint32_t t = nb; t; t &= t - 1) d += sdl[wd * 32 + __ffs(t) - 1];
     if (w != s) {
       atomicAdd((unsigned long long *)&S.target[w], (unsigned long long)(-d));
+      S.dlst.add(w, -d);
       if (S.track) {  // only the chunk's argmax matters (gains only decrease)
         if (cm == NONE) cm = __ldcg(&S.cmax[w >> S.csh].v);
         if (cm == w) mark_dirty(S, w >> S.csh);
@@ -768,7 +771,10 @@ __device__ void apply_dense(const Sel &S, uint32_t s, size_t warp0, size_t nwarp
         for (int q = 16; q; q >>= 1) d += __shfl_xor_sync(0xffffffffu, d, q);
         if (lane == 0 && d) {
           const uint32_t vid = S.rmap[v];
-          if (vid != s) atomicAdd((unsigned long long *)&S.target[vid], (unsigned long long)(-d));
+          if (vid != s) {
+            atomicAdd((unsigned long long *)&S.target[vid], (unsigned long long)(-d));
+            S.dlst.add(vid, -d);
+          }
         }
       }
     }
@@ -997,6 +1003,30 @@ __global__ void __launch_bounds__(SEL_THREADS) k_argmax_final(const Best *partia
   if (threadIdx.x == 0) *out = c;
 }
 
+// gain[v[i]] += d[i] (duplicates add up), then gain[s] = -1 (R6)
+__global__ void k_apply_deltas(long long *gain, const uint32_t *v, const long long *d,
+                               unsigned long long count) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x)
+    if (d[i]) atomicAdd((unsigned long long *)&gain[v[i]], (unsigned long long)d[i]);
+}
+__global__ void k_apply_dense(long long *gain, long long *delta, uint32_t n) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const long long x = delta[i];
+    if (x) {
+      gain[i] += x;
+      delta[i] = 0;
+    }
+  }
+}
+__global__ void k_clear_deltas(long long *delta, const uint32_t *v, unsigned long long count) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (size_t)gridDim.x * blockDim.x)
+    delta[v[i]] = 0;
+}
+__global__ void k_set_gain(long long *gain, uint32_t s, long long x) { gain[s] = x; }
+
 // empty ring: slot i expects ticket i
 __global__ void k_ring_init(Item *ring, unsigned long long Q) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < Q;
@@ -1108,6 +1138,7 @@ static Sel make_sel(pacim_ctx *ctx, long long *target) {
   S.tlstep = 0;
   S.ilog = nullptr;
   S.ilog_cap = 0;
+  S.dlst = ctx->dlist;
   return S;
 }
 
@@ -1314,4 +1345,38 @@ void pc_argmax(pacim_ctx *ctx, const int64_t *d_gain, uint32_t n, uint32_t *s, i
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
   *s = h.v;
   *g = h.g;
+}
+
+void pc_apply_deltas(pacim_ctx *ctx, int64_t *d_gain, const uint32_t *v, const int64_t *d,
+                     uint64_t count, uint32_t s) {
+  if (count) {
+    k_apply_deltas<<<pc_grid(ctx, count, 256), 256, 0, ctx->stream>>>(
+        reinterpret_cast<long long *>(d_gain), v, reinterpret_cast<const long long *>(d), count);
+    PC_CHECK_LAUNCH();
+  }
+  if (s != NONE) {
+    k_set_gain<<<1, 1, 0, ctx->stream>>>(reinterpret_cast<long long *>(d_gain), s, -1);
+    PC_CHECK_LAUNCH();
+  }
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void pc_apply_dense(pacim_ctx *ctx, int64_t *d_gain, int64_t *d_delta, uint32_t n, uint32_t s) {
+  k_apply_dense<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(
+      reinterpret_cast<long long *>(d_gain), reinterpret_cast<long long *>(d_delta), n);
+  PC_CHECK_LAUNCH();
+  if (s != NONE) {
+    k_set_gain<<<1, 1, 0, ctx->stream>>>(reinterpret_cast<long long *>(d_gain), s, -1);
+    PC_CHECK_LAUNCH();
+  }
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void pc_clear_deltas(pacim_ctx *ctx, int64_t *d_delta, const uint32_t *v, uint64_t count) {
+  if (count) {
+    k_clear_deltas<<<pc_grid(ctx, count, 256), 256, 0, ctx->stream>>>(
+        reinterpret_cast<long long *>(d_delta), v, count);
+    PC_CHECK_LAUNCH();
+  }
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
 }

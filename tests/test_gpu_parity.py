@@ -273,7 +273,12 @@ def test_rank_emulation_matches_single(orc, pc, big_t, chunk, monkeypatch):
             c.pacim_load_graph(off, nbr, 0, t32, 1)
             c.pacim_build_sketches(R, seed, 1 << 32, rank, P)
             ctxs.append(c)
-        seeds, gains, sig = dist.emulated_select(ctxs, g.n, k, device="cuda")
-        assert list(seeds) == list(es) and list(gains) == list(egn) and list(sig) == list(esg)
+        for mode, cap in (("sparse", None), ("dense", None), ("sparse", 40)):
+            for c in ctxs:
+                c.pacim_select_reset()
+            seeds, gains, sig = dist.emulated_select(ctxs, g.n, k, device="cuda", cap=cap,
+                                                     mode=mode)
+            assert list(seeds) == list(es) and list(gains) == list(egn), (mode, cap)
+            assert list(sig) == list(esg)
         for c in ctxs:
             c.close()
