@@ -30,6 +30,7 @@
 namespace {
 
 constexpr uint32_t HOT_MAX = 1024;  // slots with a shared-memory hot-root cache
+constexpr uint32_t NARROW_W = 128;  // windows narrower than this use the (row, slot) lane map
 constexpr uint32_t NONE = 0xFFFFFFFFu;
 
 __device__ __forceinline__ uint32_t ld_cg(const uint32_t *p) { return __ldcg(p); }
@@ -39,7 +40,7 @@ __global__ void k_init(uint32_t *L, uint32_t n, uint32_t B) {
   const int lane = threadIdx.x & 31;
   size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
-  if ((B & 3) == 0) {
+  if ((B & 3) == 0 && (reinterpret_cast<uintptr_t>(L) & 15) == 0) {
     const uint32_t B4 = B >> 2;
     for (size_t v = warp; v < n; v += nw) {
       uint4 *row = reinterpret_cast<uint4 *>(L + v * B);
@@ -321,8 +322,11 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
 // ---------------------------------------------------------------- k_gain0
 // Warp per store row, 8 slots prefetched per lane: gain0[v] = sum_j |C_j(v)|
 // (H7), the CC size read from the root slot (HIGH | size).
+// acc: window of a multi-window store, gain0[v] += sum (|C| - 1) over its
+// slots (gain0 starts at B); else gain0[v] = the sum over all B slots
 __global__ void __launch_bounds__(256) k_gain0(const uint32_t *__restrict__ L, uint32_t n,
-                                               uint32_t B, const uint32_t *rmap, int64_t *gain0) {
+                                               uint32_t B, const uint32_t *rmap, int64_t *gain0,
+                                               int acc) {
   const int lane = threadIdx.x & 31;
   size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
@@ -350,7 +354,13 @@ __global__ void __launch_bounds__(256) k_gain0(const uint32_t *__restrict__ L, u
       }
     }
     for (int d = 16; d; d >>= 1) g += __shfl_xor_sync(0xffffffffu, g, d);
-    if (lane == 0) gain0[rmap[v]] = g;
+    if (lane == 0) {
+      if (acc) {
+        if (g != (long long)B) gain0[rmap[v]] += g - (long long)B;
+      } else {
+        gain0[rmap[v]] = g;
+      }
+    }
   }
 }
 
@@ -361,6 +371,163 @@ __global__ void k_hla_scatter(const unsigned long long *raw, unsigned long long 
        i += (size_t)gridDim.x * blockDim.x) {
     const unsigned long long r = raw[i];
     rows[atomicAdd(cur + (r >> 32), 1ull)] = (uint32_t)r;
+  }
+}
+
+// ------------------------------------------------ narrow-window kernels
+// A window of c slots is a contiguous nr x c block.  A warp covers 32 / c
+// rows per iteration (lane -> (row offset, column), computed once), so all
+// lanes stream consecutive words; c >= 32: one row per iteration, lanes
+// striding the columns.
+struct WLanes {
+  uint32_t rpw, r, jj;
+  bool act;
+  __device__ __forceinline__ explicit WLanes(uint32_t c) {
+    const uint32_t lane = threadIdx.x & 31;
+    if (c >= 32) {
+      rpw = 1;
+      r = 0;
+      jj = lane;
+      act = true;
+    } else {
+      rpw = 32 / c;
+      r = lane / c;
+      jj = lane % c;
+      act = r < rpw;
+    }
+  }
+};
+
+__global__ void __launch_bounds__(256) k_init_w(uint32_t *L, uint32_t nr, uint32_t c) {
+  const WLanes wl(c);
+  const size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t row0 = warp * wl.rpw; row0 < nr; row0 += nw * wl.rpw) {
+    const size_t row = row0 + wl.r;
+    if (!wl.act || row >= nr) continue;
+    for (uint32_t j = wl.jj; j < c; j += 32) L[row * c + j] = (uint32_t)row;
+  }
+}
+
+// compress_count for a narrow window (same contract as k_compress_count)
+__global__ void __launch_bounds__(256) k_compress_w(uint32_t *L, uint32_t nr, uint32_t c,
+                                                    const uint32_t *hot, unsigned long long *ctr) {
+  extern __shared__ uint32_t hsm[];
+  const uint32_t H = min(c, HOT_MAX);
+  uint32_t *hroot = hsm, *hcnt = hsm + H;
+  for (uint32_t j = threadIdx.x; j < H; j += blockDim.x) {
+    hroot[j] = hot[j];
+    hcnt[j] = 0;
+  }
+  __syncthreads();
+  const WLanes wl(c);
+  const size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long ncc = 0, nnr = 0;
+  for (size_t row0 = warp * wl.rpw; row0 < nr; row0 += nw * wl.rpw) {
+    const size_t v = row0 + wl.r;
+    if (!wl.act || v >= nr) continue;
+    for (uint32_t j = wl.jj; j < c; j += 32) {
+      const uint32_t s = ld_cg(L + v * c + j);
+      if (s == (uint32_t)v || (s & PACIM_HIGH)) continue;  // root (or singleton)
+      const uint32_t root = (j < H && s == hroot[j]) ? s : find_halve(L, c, j, s);
+      if (root != s) atomicMin(L + v * c + j, root);
+      nnr++;
+      if (j < H && root == hroot[j]) atomicAdd(hcnt + j, 1u);
+      else if (add_to_root(L, c, j, root, 1u)) ncc++;
+    }
+  }
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < H; j += blockDim.x)
+    if (hcnt[j] && add_to_root(L, c, j, hroot[j], hcnt[j])) ncc++;
+  for (int d = 16; d; d >>= 1) {
+    ncc += __shfl_xor_sync(0xffffffffu, ncc, d);
+    nnr += __shfl_xor_sync(0xffffffffu, nnr, d);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (ncc) atomicAdd(ctr + 0, ncc);
+    if (nnr) atomicAdd(ctr + 1, nnr);
+  }
+}
+
+// gain0[v] += sum over the window's slots of (|C| - 1) (gain0 starts at B);
+// the lanes of one row are consecutive: segmented sum by shuffles
+__global__ void __launch_bounds__(256) k_gain_w(const uint32_t *__restrict__ L, uint32_t nr,
+                                                uint32_t c, const uint32_t *rmap, int64_t *gain0) {
+  const WLanes wl(c);
+  const int lane = threadIdx.x & 31;
+  const size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t seg = c >= 32 ? 32 : c;  // lanes per row
+  for (size_t row0 = warp * wl.rpw; row0 < nr; row0 += nw * wl.rpw) {
+    const size_t v = row0 + wl.r;
+    long long g = 0;
+    if (wl.act && v < nr) {
+      for (uint32_t j = wl.jj; j < c; j += 32) {
+        const uint32_t s = L[v * c + j];
+        if (s == (uint32_t)v) continue;  // singleton: |C| - 1 = 0
+        const uint32_t sz = (s & PACIM_HIGH) ? (s & PACIM_LOW) : (__ldg(L + (size_t)s * c + j) & PACIM_LOW);
+        g += (long long)sz - 1;
+      }
+    }
+    // sum the lanes of each row segment [r * seg, r * seg + seg)
+    for (uint32_t d = 1; d < seg; d <<= 1) {
+      const long long y = __shfl_down_sync(0xffffffffu, g, d);
+      if (wl.jj + d < seg) g += y;
+    }
+    if (wl.act && wl.jj == 0 && v < nr && g) gain0[rmap[v]] += g;
+  }
+}
+
+// ------------------------------------------------------ edge partition
+// Per build: the upper edges grouped by the top W bits of hash(e) (their
+// candidate sketches all lie in the slot bucket with the same top bits of
+// hash(r); R2 candidate enumeration).  Counting pass + scatter pass; the
+// order inside a bucket is arbitrary (union-find is order-independent).
+__global__ void k_bucket_count(const uint64_t *keys, uint64_t m, uint64_t K, uint32_t W,
+                               unsigned long long *cnt) {
+  extern __shared__ unsigned long long hcnt_s[];
+  const uint32_t NB = 1u << W;
+  for (uint32_t i = threadIdx.x; i < NB; i += blockDim.x) hcnt_s[i] = 0;
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  for (size_t base = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(size_t)31; base < m;
+       base += (size_t)gridDim.x * blockDim.x) {
+    const size_t e = base + lane;
+    const uint32_t b = e < m ? (uint32_t)(pc_mix64(keys[e] ^ K) >> 32) >> (32 - W) : 0xFFFFFFFFu;
+    const uint32_t peers = __match_any_sync(0xffffffffu, b);  // one shared add per bucket
+    if (b != 0xFFFFFFFFu && lane == __ffs(peers) - 1) atomicAdd(hcnt_s + b, (unsigned long long)__popc(peers));
+  }
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < NB; i += blockDim.x)
+    if (hcnt_s[i]) atomicAdd(cnt + i, hcnt_s[i]);
+}
+
+__global__ void k_bucket_scatter(const uint64_t *keys, const uint64_t *ckeys, uint64_t m,
+                                 uint64_t K, uint32_t W, unsigned long long *cur, uint64_t *okeys,
+                                 uint64_t *ockeys) {
+  const int lane = threadIdx.x & 31;
+  for (size_t base = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(size_t)31; base < m;
+       base += (size_t)gridDim.x * blockDim.x) {
+    const size_t e = base + lane;
+    const bool ok = e < m;
+    uint64_t k = 0, ck = 0;
+    uint32_t b = 0xFFFFFFFFu;
+    if (ok) {
+      k = keys[e];
+      ck = ckeys[e];
+      b = (uint32_t)(pc_mix64(k ^ K) >> 32) >> (32 - W);
+    }
+    // one cursor update per bucket present in the warp
+    const uint32_t peers = __match_any_sync(0xffffffffu, b);
+    const int leader = __ffs(peers) - 1;
+    unsigned long long pos = 0;
+    if (ok && lane == leader) pos = atomicAdd(cur + b, (unsigned long long)__popc(peers));
+    pos = __shfl_sync(peers, pos, leader) + __popc(peers & ((1u << lane) - 1));
+    if (ok) {
+      okeys[pos] = k;
+      ockeys[pos] = ck;
+    }
   }
 }
 
@@ -419,32 +586,46 @@ void pc_slot_table(pacim_ctx *ctx) {
 // ctr[0] += non-singleton CCs, ctr[1] += non-roots, ctr[4] += live pairs.
 // ev (optional, 3 events) is recorded after init, edges and compress.
 void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
-                    unsigned long long *ctr, cudaEvent_t *ev, const Hla *hla_in) {
+                    unsigned long long *ctr, cudaEvent_t *ev, const Hla *hla_in,
+                    const EdgeSet *es_in) {
   Hla hla{};
   if (hla_in) hla = *hla_in;
+  EdgeSet es;
+  if (es_in) {
+    es = *es_in;
+  } else {
+    es.keys = ctx->keys.as<uint64_t>();
+    es.ckeys = ctx->ckeys.as<uint64_t>();
+    es.m = ctx->m;
+  }
   const uint32_t n = ctx->nr, B = ctx->R_local;
   const uint32_t NT = 1u << PACIM_TB;
   pc_ensure(ctx, ctx->d_hot, 2 * (size_t)B * sizeof(uint32_t));
   uint32_t *hot_root = ctx->d_hot.as<uint32_t>();
   const uint32_t H = std::min<uint32_t>(Bb, HOT_MAX);
   const unsigned rows_grid = pc_grid(ctx, (size_t)n * 32, 256, 16);
-  k_init<<<rows_grid, 256, 0, ctx->stream>>>(Lb, n, Bb);
+  const bool narrow = Bb < NARROW_W;  // lanes over (row, slot) pairs
+  const unsigned wgrid = pc_grid(ctx, (size_t)n * Bb, 256, 16);
+  if (narrow)
+    k_init_w<<<wgrid, 256, 0, ctx->stream>>>(Lb, n, Bb);
+  else
+    k_init<<<rows_grid, 256, 0, ctx->stream>>>(Lb, n, Bb);
   PC_CHECK_LAUNCH();
   if (ev) PC_CUDA(cudaEventRecord(ev[0], ctx->stream));
   {
     size_t smem = B * sizeof(uint32_t) + (NT + 1) * sizeof(uint16_t);
-    unsigned g = pc_grid(ctx, (ctx->m + 31) / 32 * 32, EDGE_THREADS, 8);
+    unsigned g = pc_grid(ctx, (es.m + 31) / 32 * 32, EDGE_THREADS, 8);
     if (ctx->pmodel == PACIM_P_WIC) {
       auto kern = hla.cnt ? k_edges<true, true> : k_edges<true, false>;
       PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
-          ctx->keys.as<uint64_t>(), ctx->ckeys.as<uint64_t>(), ctx->tm1.as<uint32_t>(), ctx->m,
+          es.keys, es.ckeys, ctx->tm1.as<uint32_t>(), es.m,
           ctx->K, 0, ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla);
     } else {
       auto kern = hla.cnt ? k_edges<false, true> : k_edges<false, false>;
       PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
-          ctx->keys.as<uint64_t>(), ctx->ckeys.as<uint64_t>(), nullptr, ctx->m, ctx->K, ctx->t32,
+          es.keys, es.ckeys, nullptr, es.m, ctx->K, ctx->t32,
           ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla);
     }
     PC_CHECK_LAUNCH();
@@ -452,11 +633,62 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
   if (ev) PC_CUDA(cudaEventRecord(ev[1], ctx->stream));
   k_hot_roots<<<(Bb + 255) / 256, 256, 0, ctx->stream>>>(Lb, n, Bb, ctx->hub_row, hot_root);
   PC_CHECK_LAUNCH();
-  k_compress_count<<<rows_grid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(Lb, n, Bb, hot_root,
-                                                                              ctr);
+  if (narrow)
+    k_compress_w<<<wgrid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(Lb, n, Bb, hot_root, ctr);
+  else
+    k_compress_count<<<rows_grid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(Lb, n, Bb,
+                                                                                hot_root, ctr);
   PC_CHECK_LAUNCH();
   if (ev) PC_CUDA(cudaEventRecord(ev[2], ctx->stream));
   ctx->launches += 4;
+}
+
+// Slot windows of the store for this build.  With a constant
+// threshold the live sketches of an edge all lie in the bucket of slots whose
+// top w = clz(T - 1) bits of hash(r) equal those of hash(e); the slots are
+// sorted by hash(r), so every bucket is a contiguous slot range.  When a
+// bucket's parent arrays (rows x slots x 4 B) fit the L2 budget, the build
+// runs one window (a bucket, or a slice of an oversized one) at a time over
+// that bucket's edges only: the unions, compression and CC counting of a
+// window hit L2 instead of HBM.  Otherwise (WIC thresholds, or rows too
+// many) one window [0, B) over all edges.  Returns the bucket bits W (0: one
+// window).
+static uint32_t plan_windows(pacim_ctx *ctx) {
+  const uint32_t B = ctx->R_local, nr = ctx->nr;
+  ctx->win_first.assign({0u, B});
+  // opt-in (PACIM_L2_BUDGET = bytes of parent arrays per window): measured on
+  // c2 (profiles/r01_v7_windows.md) the windows do not stay L2-resident and
+  // 35 windows x 4 short kernels cost more than they save, so the default is
+  // the single window [0, B)
+  uint64_t budget = 0;
+  if (const char *e = getenv("PACIM_L2_BUDGET")) budget = (uint64_t)atoll(e);
+  if (ctx->pmodel != PACIM_P_CONST || ctx->t32 < 2 || ctx->t32 >= (1ull << 32) || nr == 0 ||
+      budget == 0 || ctx->compressed)
+    return 0;
+  const uint32_t w = __builtin_clz((uint32_t)(ctx->t32 - 1));
+  const uint64_t g = budget / ((uint64_t)nr * 4);  // slots per window that fit the budget
+  if (g >= B || g < 1) return 0;                   // everything fits, or nothing does
+  uint32_t W = std::min<uint32_t>(w, 10);
+  if (W == 0) return 0;
+  // windows: each bucket split into slices of <= g slots
+  std::vector<uint32_t> wf;
+  uint32_t j = 0;
+  for (uint32_t b = 0; b < (1u << W); b++) {
+    uint32_t e = j;
+    while (e < B && (ctx->shr[e] >> (32 - W)) == b) e++;
+    for (uint32_t f = j; f < e; f += (uint32_t)g) wf.push_back(f);
+    j = e;
+  }
+  wf.push_back(B);
+  if (wf.size() <= 2) return 0;
+  ctx->win_first = wf;
+  return W;
+}
+
+__global__ void k_fill_smap(const uint32_t *wf, uint32_t nw, uint32_t *smap) {
+  for (uint32_t w = blockIdx.x; w < nw; w += gridDim.x)
+    for (uint32_t j = wf[w] + threadIdx.x; j < wf[w + 1]; j += blockDim.x)
+      smap[j] = (wf[w] << 16) | (wf[w + 1] - wf[w]);
 }
 
 void pc_build(pacim_ctx *ctx) {
@@ -470,12 +702,11 @@ void pc_build(pacim_ctx *ctx) {
   unsigned long long *ctr = ctx->counters.as<unsigned long long>();
   PC_CUDA(cudaMemsetAsync(ctr, 0, 64 * sizeof(uint64_t), ctx->stream));
   uint32_t *L = ctx->L.as<uint32_t>();
-  cudaEvent_t ev[6];
-  for (auto &e : ev) PC_CUDA(cudaEventCreate(&e));
   ctx->launches = 0;
   const unsigned rows_grid = pc_grid(ctx, (size_t)n * 32, 256, 16);
-  // live hub adjacency (HLA) of the hub rows: opt-in (PACIM_HLA=1): on c4 recording costs more build time than the
-  // selection saves (its traversal is bound by hop latency, not edge work)
+  // live hub adjacency (HLA) of the hub rows: opt-in (PACIM_HLA=1): on c4
+  // recording costs more build time than the selection saves (its traversal
+  // is bound by hop latency, not edge work)
   const bool want_hla = ctx->nhub > 0 && (getenv("PACIM_HLA") != nullptr ||
                                           getenv("PACIM_FORCE_HLA") != nullptr);
   ctx->hla_ok = false;
@@ -494,17 +725,76 @@ void pc_build(pacim_ctx *ctx) {
     hla.cap = cap;
     hla.B = B;
   }
+  const uint32_t W = plan_windows(ctx);
+  const uint32_t nwin = (uint32_t)ctx->win_first.size() - 1;
+  {  // per-slot window table (select / labels address the store through it)
+    pc_ensure(ctx, ctx->d_smap, (size_t)B * 4);
+    TmpBuf wf(ctx);
+    pc_ensure(ctx, wf, ctx->win_first.size() * 4);
+    PC_CUDA(cudaMemcpyAsync(wf.p, ctx->win_first.data(), ctx->win_first.size() * 4,
+                            cudaMemcpyHostToDevice, ctx->stream));
+    k_fill_smap<<<std::min<uint32_t>(nwin, 1024), 256, 0, ctx->stream>>>(wf.as<uint32_t>(), nwin,
+                                                                         ctx->d_smap.as<uint32_t>());
+    PC_CHECK_LAUNCH();
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  // events: start, then per window init / edges / compress / gain done
+  std::vector<cudaEvent_t> ev(2 + 4 * (size_t)nwin);
+  for (auto &e : ev) PC_CUDA(cudaEventCreate(&e));
   PC_CUDA(cudaEventRecord(ev[0], ctx->stream));
-  pc_sketch_pass(ctx, L, 0, B, ctr, ev + 1, want_hla ? &hla : nullptr);
-  PC_CUDA(cudaEventRecord(ev[4], ctx->stream));
-  // gain0 (H7): isolated vertices are singletons everywhere (gain B); every
-  // store row sums its CC sizes read from the root slots (HIGH | size)
+  // gain0 (H7): isolated vertices are singletons everywhere (gain B)
   k_fill_i64<<<pc_grid(ctx, ctx->n, 256), 256, 0, ctx->stream>>>(ctx->gain0.as<int64_t>(), ctx->n,
                                                                 (int64_t)B);
   PC_CHECK_LAUNCH();
-  k_gain0<<<rows_grid, 256, 0, ctx->stream>>>(L, n, B, ctx->rmap.as<uint32_t>(),
-                                             ctx->gain0.as<int64_t>());
-  PC_CHECK_LAUNCH();
+  // partition of the edges by bucket (W > 0)
+  std::vector<unsigned long long> boff;
+  if (W) {
+    const uint32_t NB = 1u << W;
+    const uint64_t m = ctx->m;
+    pc_ensure(ctx, ctx->pkeys, std::max<uint64_t>(m, 1) * 16 + (NB + 1) * 16);
+    uint64_t *pk = ctx->pkeys.as<uint64_t>(), *pck = pk + m;
+    unsigned long long *cnt = reinterpret_cast<unsigned long long *>(pck + m);
+    unsigned long long *cur = cnt + NB;
+    PC_CUDA(cudaMemsetAsync(cnt, 0, NB * 8, ctx->stream));
+    k_bucket_count<<<pc_grid(ctx, m, 256, 4), 256, NB * 8, ctx->stream>>>(ctx->keys.as<uint64_t>(),
+                                                                         m, ctx->K, W, cnt);
+    PC_CHECK_LAUNCH();
+    std::vector<unsigned long long> hc(NB);
+    PC_CUDA(cudaMemcpyAsync(hc.data(), cnt, NB * 8, cudaMemcpyDeviceToHost, ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    boff.assign(NB + 1, 0);
+    for (uint32_t b = 0; b < NB; b++) boff[b + 1] = boff[b] + hc[b];
+    PC_CUDA(cudaMemcpyAsync(cur, boff.data(), NB * 8, cudaMemcpyHostToDevice, ctx->stream));
+    k_bucket_scatter<<<pc_grid(ctx, m, 256, 8), 256, 0, ctx->stream>>>(
+        ctx->keys.as<uint64_t>(), ctx->ckeys.as<uint64_t>(), m, ctx->K, W, cur, pk, pck);
+    PC_CHECK_LAUNCH();
+    ctx->launches += 2;
+  }
+  for (uint32_t w = 0; w < nwin; w++) {
+    const uint32_t f = ctx->win_first[w], c = ctx->win_first[w + 1] - f;
+    uint32_t *Lw = L + (size_t)n * f;
+    EdgeSet es;
+    if (W) {
+      const uint32_t b = ctx->shr[f] >> (32 - W);
+      const uint64_t *pk = ctx->pkeys.as<uint64_t>();
+      es.keys = pk + boff[b];
+      es.ckeys = pk + ctx->m + boff[b];
+      es.m = boff[b + 1] - boff[b];
+    }
+    PC_CUDA(cudaEventRecord(ev[1 + 4 * w], ctx->stream));
+    pc_sketch_pass(ctx, Lw, f, c, ctr, ev.data() + 2 + 4 * w, want_hla ? &hla : nullptr,
+                   W ? &es : nullptr);
+    // CC sizes of the window into gain0 while it is still cached
+    if (nwin > 1 && c < NARROW_W)
+      k_gain_w<<<pc_grid(ctx, (size_t)n * c, 256, 16), 256, 0, ctx->stream>>>(
+          Lw, n, c, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>());
+    else
+      k_gain0<<<rows_grid, 256, 0, ctx->stream>>>(Lw, n, c, ctx->rmap.as<uint32_t>(),
+                                                 ctx->gain0.as<int64_t>(), nwin > 1);
+    PC_CHECK_LAUNCH();
+    ctx->launches++;
+  }
+  PC_CUDA(cudaEventRecord(ev.back(), ctx->stream));
   if (want_hla) {
     // counts -> offsets (in place via scratch), then rows grouped by key
     const size_t keys = (size_t)ctx->nhub * B + 1;
@@ -526,8 +816,7 @@ void pc_build(pacim_ctx *ctx) {
       ctx->launches += 2;
     }
   }
-  PC_CUDA(cudaEventRecord(ev[5], ctx->stream));
-  ctx->launches += 2;  // fill, gain0
+  ctx->launches += 1;  // fill
   unsigned long long h[6];
   PC_CUDA(cudaMemcpyAsync(h, ctr, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                           ctx->stream));
@@ -536,13 +825,21 @@ void pc_build(pacim_ctx *ctx) {
   ctx->nnonsingle = h[0] + h[1];
   ctx->nmember = 0;
   ctx->stats.live_pairs = h[4];
-  ctx->stats.t_init_ms = ev_ms(ev[0], ev[1]);
-  ctx->stats.t_edges_ms = ev_ms(ev[1], ev[2]);
-  ctx->stats.t_compress_ms = ev_ms(ev[2], ev[3]);
-  ctx->stats.t_compact_ms = ev_ms(ev[3], ev[4]);
-  ctx->stats.t_gain_ms = ev_ms(ev[4], ev[5]);
+  double ti = 0, te = 0, tc = 0, tg = 0;
+  for (uint32_t w = 0; w < nwin; w++) {
+    cudaEvent_t *e = ev.data() + 1 + 4 * w;  // window start, init, edges, compress
+    ti += ev_ms(e[0], e[1]);
+    te += ev_ms(e[1], e[2]);
+    tc += ev_ms(e[2], e[3]);
+    tg += ev_ms(e[3], w + 1 < nwin ? e[4] : ev.back());  // gain0 of the window
+  }
+  ctx->stats.t_init_ms = ti;
+  ctx->stats.t_edges_ms = te;
+  ctx->stats.t_compress_ms = tc;
+  ctx->stats.t_gain_ms = tg;
+  ctx->stats.t_compact_ms = ev_ms(ev[0], ev[1]);  // gain fill + edge partition
   ctx->stats.t_centers_ms = 0;
-  ctx->stats.t_build_ms = ev_ms(ev[0], ev[5]);
+  ctx->stats.t_build_ms = ev_ms(ev[0], ev.back());
   ctx->stats.kernel_launches_build = ctx->launches;
   for (auto &e : ev) cudaEventDestroy(e);
 }
@@ -550,7 +847,7 @@ void pc_build(pacim_ctx *ctx) {
 // canonical labels of one slot: slot value is v (singleton), HIGH|ci (root:
 // label v) or the root id (R8: min id of the CC)
 namespace {
-__global__ void k_labels(const uint32_t *L, uint32_t n, uint32_t B, uint32_t j,
+__global__ void k_labels(const uint32_t *L, uint32_t n, uint32_t nr, const uint32_t *smap, uint32_t j,
                          const uint32_t *cid, const uint32_t *rmap, uint32_t *out) {
   for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (size_t)gridDim.x * blockDim.x) {
@@ -559,7 +856,7 @@ __global__ void k_labels(const uint32_t *L, uint32_t n, uint32_t B, uint32_t j,
       out[v] = (uint32_t)v;
       continue;
     }
-    uint32_t s = L[(size_t)c * B + j];
+    uint32_t s = L[pc_addr(smap, nr, c, j)];
     out[v] = (s == c || (s & PACIM_HIGH)) ? (uint32_t)v : rmap[s];
   }
 }
@@ -569,7 +866,7 @@ void pc_get_labels(pacim_ctx *ctx, uint32_t slot, uint32_t *host_out) {
   TmpBuf t(ctx);
   pc_ensure(ctx, t, (size_t)ctx->n * 4);
   k_labels<<<pc_grid(ctx, ctx->n, 256), 256, 0, ctx->stream>>>(ctx->L.as<uint32_t>(), ctx->n,
-                                                              ctx->R_local, slot,
+                                                              ctx->nr, ctx->d_smap.as<uint32_t>(), slot,
                                                               ctx->cid.as<uint32_t>(),
                                                               ctx->rmap.as<uint32_t>(),
                                                               t.as<uint32_t>());

@@ -63,6 +63,13 @@ struct PacimError {
     if (!(cond)) throw PacimError{code, msg};                                 \
   } while (0)
 
+// store address of (row, slot j) under the window layout (smap = d_smap)
+__device__ __forceinline__ size_t pc_addr(const uint32_t *smap, uint32_t nr, uint32_t row,
+                                          uint32_t j) {
+  const uint32_t fc = smap[j], f = fc >> 16, c = fc & 0xFFFFu;
+  return (size_t)nr * f + (size_t)row * c + (j - f);
+}
+
 // ------------------------------------------------------- device allocation
 struct DevBuf {
   void *p = nullptr;
@@ -142,8 +149,14 @@ struct pacim_ctx {
   DevBuf d_hot;        // u32[2*B]: per slot the hub's root and its component id
   uint32_t hub = 0;    // a maximum-degree vertex (most likely in the giant CC)
 
-  // uncompressed store: L[v*B + j] (B = R_local)
+  // uncompressed store: slot windows: window w holds slots
+  // [f_w, f_w + c_w) of every row at L + nr * f_w, row stride c_w, so
+  // (row, j) lives at nr * f + row * c + (j - f).  One window [0, B) is the
+  // plain vertex-major layout.  d_smap[j] = f << 16 | c of j's window.
   DevBuf L;
+  std::vector<uint32_t> win_first;  // window starts, + B at the end
+  DevBuf d_smap;
+  DevBuf pkeys;          // per-build edge partition by bucket: keys, ckeys, counts
   uint64_t ncomp = 0, nmember = 0, nnonsingle = 0;
   uint32_t big_t = 0;
   DevBuf csize;       // u32[ncomp] pristine CC sizes
@@ -250,8 +263,15 @@ struct Hla {
   }
 };
 
+// edges of one sketch pass: the whole upper edge list (default) or one
+// bucket of the per-build partition
+struct EdgeSet {
+  const uint64_t *keys = nullptr, *ckeys = nullptr;
+  uint64_t m = 0;
+};
 void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
-                    unsigned long long *ctr, cudaEvent_t *ev, const Hla *hla = nullptr);
+                    unsigned long long *ctr, cudaEvent_t *ev, const Hla *hla = nullptr,
+                    const EdgeSet *es = nullptr);
 // compressed.cu (H6c, H11)
 void pc_build_compressed(pacim_ctx *ctx);
 void pc_select_compressed(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,

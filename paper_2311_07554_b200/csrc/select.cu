@@ -151,6 +151,7 @@ struct Sel {
   const uint16_t *g_tab;   // candidate bucket table of the sorted slots
   // store
   uint32_t *L;
+  const uint32_t *smap;    // slot -> f << 16 | c of its store window (pc_addr)
   uint32_t nr, B, BW, nv;  // rows, slots, mask words per row, vertices
   const uint32_t *cid, *rmap;
   // per step
@@ -267,15 +268,16 @@ __device__ __forceinline__ uint32_t cover_slot(const Sel &S, uint32_t srow, uint
   S.dl[j] = 0;
   S.cov_root[j] = NONE;
   if (srow == NONE) return delta;  // isolated seed: singleton in every sketch
-  const uint32_t sl = S.L[(size_t)srow * S.B + j];
+  const uint32_t sl = S.L[pc_addr(S.smap, S.nr, srow, j)];
   if (sl == srow) return delta;    // singleton {s}
   const uint32_t root = (sl & PACIM_HIGH) ? srow : sl;
-  uint32_t *rs = S.L + (size_t)root * S.B + j;
+  const size_t ra = pc_addr(S.smap, S.nr, root, j);
+  uint32_t *rs = S.L + ra;
   const uint32_t x = atomicOr(rs, COV);  // covered from now on
   if (x & COV) return 0;                 // covered by an earlier seed
   delta = x & SIZE;
   const unsigned long long at = atomicAdd(S.cov_cnt, 1ull);
-  if (at < S.cov_cap) S.cov_list[at] = (size_t)root * S.B + j;
+  if (at < S.cov_cap) S.cov_list[at] = ra;
   if (delta > S.big_t) {
     S.cov_root[j] = root;
     S.cov_delta[j] = delta;
@@ -758,7 +760,7 @@ __device__ void apply_dense(const Sel &S, uint32_t s, size_t warp0, size_t nwarp
 #pragma unroll
         for (int i = 0; i < 8; i++)
           x[r][i] = (cr[i] != NONE && v0 + r < S.nr)
-                        ? __ldcs(S.L + (v0 + r) * S.B + j0 + lane + 32 * i)
+                        ? __ldcs(S.L + pc_addr(S.smap, S.nr, (uint32_t)(v0 + r), j0 + lane + 32 * i))
                         : NONE;
 #pragma unroll
       for (int r = 0; r < DR; r++) {
@@ -1057,6 +1059,7 @@ static Sel make_sel(pacim_ctx *ctx, long long *target) {
   S.g_shr = ctx->d_shr.as<uint32_t>();
   S.g_tab = ctx->d_tab.as<uint16_t>();
   S.L = ctx->L.as<uint32_t>();
+  S.smap = ctx->d_smap.as<uint32_t>();
   S.nr = nr;
   S.B = B;
   S.BW = (B + 31) / 32;

@@ -109,6 +109,19 @@ def test_traversal_paths(orc, ctx, i, env, monkeypatch):
     test_tiny_corpus_parity(orc, ctx, i)
 
 
+@pytest.mark.parametrize("budget", ["1000", "6000", "40000"])
+@pytest.mark.parametrize("i", [0, 1, 2, 5, 7, 9])
+def test_window_layout(orc, ctx, i, budget, monkeypatch):
+    """Store split into slot windows (one bucket of sketches, or a slice of
+    one, at a time over the bucket's edges) -- the layout the L2-resident
+    build uses at c2 -- forced on the tiny corpus with a small budget: labels,
+    gain0 and the greedy must equal the oracle's, also with the dense pass."""
+    monkeypatch.setenv("PACIM_L2_BUDGET", budget)
+    test_tiny_corpus_parity(orc, ctx, i)
+    monkeypatch.setenv("PACIM_BIG_T", "10")
+    test_tiny_corpus_parity(orc, ctx, i)
+
+
 def test_edge_cases(orc, ctx, pc):
     from oracle.oracle import Graph
     # single vertex, no edges, k = n = 1
