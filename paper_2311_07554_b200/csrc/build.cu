@@ -409,7 +409,9 @@ __global__ void __launch_bounds__(256) k_init_w(uint32_t *L, uint32_t nr, uint32
   }
 }
 
-// compress_count for a narrow window (same contract as k_compress_count)
+// compress_count for a narrow window (same contract as k_compress_count);
+// WU row groups per lane loaded before any find (loads in flight together)
+constexpr int WU = 4;
 __global__ void __launch_bounds__(256) k_compress_w(uint32_t *L, uint32_t nr, uint32_t c,
                                                     const uint32_t *hot, unsigned long long *ctr) {
   extern __shared__ uint32_t hsm[];
@@ -424,17 +426,26 @@ __global__ void __launch_bounds__(256) k_compress_w(uint32_t *L, uint32_t nr, ui
   const size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long ncc = 0, nnr = 0;
-  for (size_t row0 = warp * wl.rpw; row0 < nr; row0 += nw * wl.rpw) {
-    const size_t v = row0 + wl.r;
-    if (!wl.act || v >= nr) continue;
+  const size_t step = (size_t)wl.rpw * WU;
+  for (size_t row0 = warp * step; row0 < nr; row0 += nw * step) {
     for (uint32_t j = wl.jj; j < c; j += 32) {
-      const uint32_t s = ld_cg(L + v * c + j);
-      if (s == (uint32_t)v || (s & PACIM_HIGH)) continue;  // root (or singleton)
-      const uint32_t root = (j < H && s == hroot[j]) ? s : find_halve(L, c, j, s);
-      if (root != s) atomicMin(L + v * c + j, root);
-      nnr++;
-      if (j < H && root == hroot[j]) atomicAdd(hcnt + j, 1u);
-      else if (add_to_root(L, c, j, root, 1u)) ncc++;
+      uint32_t sv[WU];
+#pragma unroll
+      for (int u = 0; u < WU; u++) {
+        const size_t v = row0 + (size_t)u * wl.rpw + wl.r;
+        sv[u] = (wl.act && v < nr) ? ld_cg(L + v * c + j) : NONE;
+      }
+#pragma unroll
+      for (int u = 0; u < WU; u++) {
+        const size_t v = row0 + (size_t)u * wl.rpw + wl.r;
+        const uint32_t s = sv[u];
+        if (s == NONE || s == (uint32_t)v || (s & PACIM_HIGH)) continue;  // root (or singleton)
+        const uint32_t root = (j < H && s == hroot[j]) ? s : find_halve(L, c, j, s);
+        if (root != s) atomicMin(L + v * c + j, root);
+        nnr++;
+        if (j < H && root == hroot[j]) atomicAdd(hcnt + j, 1u);
+        else if (add_to_root(L, c, j, root, 1u)) ncc++;
+      }
     }
   }
   __syncthreads();
@@ -450,32 +461,60 @@ __global__ void __launch_bounds__(256) k_compress_w(uint32_t *L, uint32_t nr, ui
   }
 }
 
-// gain0[v] += sum over the window's slots of (|C| - 1) (gain0 starts at B);
-// the lanes of one row are consecutive: segmented sum by shuffles
+// gain0 over a narrow window: acc ? gain0[v] += sum (|C| - 1) (gain0 starts
+// at B) : gain0[v] = sum |C| over the window (= all slots); the lanes of one
+// row are consecutive: segmented sum by shuffles; WU row groups in flight
 __global__ void __launch_bounds__(256) k_gain_w(const uint32_t *__restrict__ L, uint32_t nr,
-                                                uint32_t c, const uint32_t *rmap, int64_t *gain0) {
+                                                uint32_t c, const uint32_t *rmap, int64_t *gain0,
+                                                int acc) {
   const WLanes wl(c);
-  const int lane = threadIdx.x & 31;
   const size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
   const uint32_t seg = c >= 32 ? 32 : c;  // lanes per row
-  for (size_t row0 = warp * wl.rpw; row0 < nr; row0 += nw * wl.rpw) {
-    const size_t v = row0 + wl.r;
-    long long g = 0;
-    if (wl.act && v < nr) {
-      for (uint32_t j = wl.jj; j < c; j += 32) {
-        const uint32_t s = L[v * c + j];
-        if (s == (uint32_t)v) continue;  // singleton: |C| - 1 = 0
-        const uint32_t sz = (s & PACIM_HIGH) ? (s & PACIM_LOW) : (__ldg(L + (size_t)s * c + j) & PACIM_LOW);
-        g += (long long)sz - 1;
+  const size_t step = (size_t)wl.rpw * WU;
+  for (size_t row0 = warp * step; row0 < nr; row0 += nw * step) {
+    long long g[WU];
+#pragma unroll
+    for (int u = 0; u < WU; u++) g[u] = 0;
+    for (uint32_t j = wl.jj; j < c; j += 32) {
+      uint32_t sv[WU], sz[WU];
+#pragma unroll
+      for (int u = 0; u < WU; u++) {
+        const size_t v = row0 + (size_t)u * wl.rpw + wl.r;
+        sv[u] = (wl.act && v < nr) ? __ldcs(L + v * c + j) : NONE;
+      }
+#pragma unroll
+      for (int u = 0; u < WU; u++) {  // root sizes of the non-roots, in flight together
+        const size_t v = row0 + (size_t)u * wl.rpw + wl.r;
+        const uint32_t s = sv[u];
+        sz[u] = (s != NONE && s != (uint32_t)v && !(s & PACIM_HIGH))
+                    ? (__ldg(L + (size_t)s * c + j) & PACIM_LOW) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < WU; u++) {
+        const size_t v = row0 + (size_t)u * wl.rpw + wl.r;
+        const uint32_t s = sv[u];
+        if (s == NONE) continue;
+        const uint32_t size = s == (uint32_t)v ? 1u : (s & PACIM_HIGH) ? (s & PACIM_LOW) : sz[u];
+        g[u] += acc ? (long long)size - 1 : (long long)size;
       }
     }
-    // sum the lanes of each row segment [r * seg, r * seg + seg)
-    for (uint32_t d = 1; d < seg; d <<= 1) {
-      const long long y = __shfl_down_sync(0xffffffffu, g, d);
-      if (wl.jj + d < seg) g += y;
+#pragma unroll
+    for (int u = 0; u < WU; u++) {
+      long long t = g[u];
+      for (uint32_t d = 1; d < seg; d <<= 1) {
+        const long long y = __shfl_down_sync(0xffffffffu, t, d);
+        if (wl.jj + d < seg) t += y;
+      }
+      const size_t v = row0 + (size_t)u * wl.rpw + wl.r;
+      if (wl.act && wl.jj == 0 && v < nr) {
+        if (acc) {
+          if (t) gain0[rmap[v]] += t;
+        } else {
+          gain0[rmap[v]] = t;
+        }
+      }
     }
-    if (wl.act && wl.jj == 0 && v < nr && g) gain0[rmap[v]] += g;
   }
 }
 
@@ -785,9 +824,9 @@ void pc_build(pacim_ctx *ctx) {
     pc_sketch_pass(ctx, Lw, f, c, ctr, ev.data() + 2 + 4 * w, want_hla ? &hla : nullptr,
                    W ? &es : nullptr);
     // CC sizes of the window into gain0 while it is still cached
-    if (nwin > 1 && c < NARROW_W)
+    if (c < NARROW_W)
       k_gain_w<<<pc_grid(ctx, (size_t)n * c, 256, 16), 256, 0, ctx->stream>>>(
-          Lw, n, c, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>());
+          Lw, n, c, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>(), nwin > 1);
     else
       k_gain0<<<rows_grid, 256, 0, ctx->stream>>>(Lw, n, c, ctx->rmap.as<uint32_t>(),
                                                  ctx->gain0.as<int64_t>(), nwin > 1);
