@@ -197,13 +197,15 @@ def main():
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--alpha", type=float, default=None,
                     help="override the config's alpha (< 1: compressed store)")
+    ap.add_argument("--scale", type=int, default=None,
+                    help="override the R-MAT scale (c5 at full scale needs 8 GPUs)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--ref-sketches", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
-    cfg = inputs.config(args.config)
+    cfg = inputs.config(args.config, **({"scale": args.scale} if args.scale else {}))
     if args.alpha is not None:
         cfg["alpha"] = args.alpha
     if args.impl == "reference":
@@ -331,7 +333,9 @@ def main():
         "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (counter-based generator, DESIGN.md §Input recipe)",
-        "config": {"workload": cfg["name"], "config": args.config, "n": n, "m": m, "R": R, "k": k,
+        "config": {"workload": cfg["name"] + (f"-scale{args.scale}" if args.scale else ""),
+                   "config": args.config, "n": n, "m": m, "R": R, "k": k,
+                   "alpha": cfg.get("alpha"),
                    "sketches_per_pass": st["R_local"], "parallelism": f"sketch-shard x{world}",
                    "l2": "inputs larger than L2 (store 4*n*R bytes, keys 8*m bytes)",
                    "arith": "u64 hash, u32 labels, i64 gains"},

@@ -107,3 +107,21 @@ def test_compressed_rank_emulation(orc, pc):
     assert list(seeds) == list(es) and list(gains) == list(egn)
     for c in ctxs:
         c.close()
+
+
+def test_c5_shape_scale16(orc, ctx):
+    """BASELINE.json configs[4]'s shape (web R-MAT a,b,c,d = .6/.15/.15/.1, ef
+    32, p = 0.01, R = 256, alpha = 1/16 compressed) at scale 16, generated on
+    the GPU: seeds and gains equal the oracle's greedy (compression is
+    transparent, R17), the generated CSR equals the oracle's."""
+    from paper_2311_07554_b200 import pipeline
+    cfg = inputs.config("c5", scale=16, k=20)
+    n, m = pipeline.generate(ctx, cfg)
+    g = orc.gen_config(cfg)
+    assert (n, m) == (g.n, g.m)
+    s, gn, sg, _ = pipeline.run(ctx, cfg)
+    st = ctx.pacim_get_stats()
+    assert st["compressed"] == 1 and st["rho"] < n // 8
+    model, t32 = orc.model_args(cfg)
+    es, egn, esg, _ = orc.greedy(g, model, t32, cfg["R"], cfg["hash_seed"], cfg["k"])
+    assert list(s) == list(es) and list(gn) == list(egn) and list(sg) == list(esg)
