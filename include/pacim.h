@@ -89,6 +89,11 @@ typedef struct {
     uint64_t select_chunk_items;    /* chunk items (CH-edge slices of long rows) */
     uint64_t select_inline_rows;    /* rows expanded without queueing (queue guard) */
     uint64_t select_edges;          /* CSR entries tested by the shared traversal */
+    uint64_t select_center_visits;  /* compressed: Get-center vertices dequeued before a
+                                       center was met, summed over probes (Thm 3.1) */
+    uint64_t select_center_found;   /* compressed: probes that met a center */
+    uint32_t batch_slots;           /* compressed: sketches per build batch (parent arrays
+                                       rows x batch_slots u32 of scratch) */
 } pacim_stats;
 
 /* --------------------------------------------------------------- lifecycle */

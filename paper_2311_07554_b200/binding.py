@@ -47,7 +47,8 @@ class Stats(C.Structure):
         ("select_dense_steps", C.c_uint64), ("select_warp_slots", C.c_uint64),
         ("select_deferred_slots", C.c_uint64), ("select_row_items", C.c_uint64),
         ("select_chunk_items", C.c_uint64), ("select_inline_rows", C.c_uint64),
-        ("select_edges", C.c_uint64),
+        ("select_edges", C.c_uint64), ("select_center_visits", C.c_uint64),
+        ("select_center_found", C.c_uint64), ("batch_slots", C.c_uint32),
     ]
 
     def asdict(self):

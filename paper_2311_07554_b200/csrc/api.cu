@@ -79,7 +79,7 @@ static void free_all(pacim_ctx *ctx) {
 
                     &ctx->d_tab, &ctx->gain0,      &ctx->gain,     &ctx->center_of, &ctx->counters,
                     &ctx->scratch, &ctx->scratch2, &ctx->sel_seeds, &ctx->sel_gain,
-                    &ctx->sel_partial, &ctx->sel_list, &ctx->sel_flag, &ctx->argmax_part, &ctx->bfs, &ctx->tcsr, &ctx->hidx, &ctx->hla_off, &ctx->hla_row, &ctx->hla_raw, &ctx->d_smap, &ctx->pkeys};
+                    &ctx->sel_partial, &ctx->sel_list, &ctx->sel_flag, &ctx->argmax_part, &ctx->bfs, &ctx->tcsr, &ctx->hidx, &ctx->hla_off, &ctx->hla_row, &ctx->hla_raw, &ctx->d_smap, &ctx->pkeys, &ctx->cprobe, &ctx->cseed};
   for (DevBuf *b : bufs) pc_free(ctx, *b);
 }
 
@@ -421,6 +421,7 @@ int pacim_get_stats(pacim_ctx *ctx, pacim_stats *out) {
     s.ncomp = ctx->ncomp;
     s.nmember = ctx->nmember;
     s.rows = ctx->nr;
+    s.batch_slots = ctx->compressed ? ctx->Bb : 0;
     s.nnonsingle = ctx->nnonsingle;
     s.device_bytes = ctx->device_bytes;
     *out = s;

@@ -30,7 +30,9 @@
 namespace {
 
 constexpr uint32_t HOT_MAX = 1024;  // slots with a shared-memory hot-root cache
-constexpr uint32_t NARROW_W = 128;  // windows narrower than this use the (row, slot) lane map
+// windows narrower than this use the (row, slot) lane map (measured: the
+// warp-per-row kernels win from ~16 slots up, e.g. c4's 23-slot batch)
+constexpr uint32_t NARROW_W = 16;
 constexpr uint32_t NONE = 0xFFFFFFFFu;
 
 __device__ __forceinline__ uint32_t ld_cg(const uint32_t *p) { return __ldcg(p); }
@@ -735,6 +737,10 @@ void pc_build(pacim_ctx *ctx) {
   PC_REQUIRE(B >= 1 && B <= 65535, PACIM_EINVAL, "local sketch count must be in [1, 65535]");
   PC_REQUIRE(!ctx->compressed, PACIM_ENOTIMPL, "compressed store not built by pc_build");
   pc_slot_table(ctx);
+  // a compressed store of an earlier build is released first (capacity for
+  // this one: at c4 the two do not fit together)
+  for (DevBuf *d : {&ctx->clabel, &ctx->csz, &ctx->csz_work, &ctx->Ltmp, &ctx->cwork})
+    pc_free(ctx, *d);
   pc_ensure(ctx, ctx->L, (size_t)n * B * sizeof(uint32_t));
   pc_ensure(ctx, ctx->gain0, (size_t)ctx->n * sizeof(int64_t));
   pc_ensure(ctx, ctx->counters, 64 * sizeof(uint64_t));

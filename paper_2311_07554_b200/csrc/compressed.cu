@@ -148,6 +148,9 @@ struct ProbeParams {
   uint32_t *lab;            // per slot: label (BIG_KNOWN)
   uint32_t *dl;             // per slot: delta
   unsigned long long *sum;  // [0] sum of DONE deltas, [1] number of BIG slots, [2] visits
+  const uint16_t *tab;      // candidate bucket table of the sorted slots
+  const uint32_t *slive;    // [B][QCAP] live neighbours of the seed per slot (pre-expansion)
+  const uint32_t *scnt;     // [B] their number (> QCAP - 1: overflow, expand s in the probe)
 };
 
 __device__ __forceinline__ bool live_edge(const ProbeParams &P, uint32_t x, uint32_t w,
@@ -163,13 +166,53 @@ __device__ __forceinline__ bool live_edge(const ProbeParams &P, uint32_t x, uint
   return (uint64_t)(hr ^ he) < T;  // R3
 }
 
+// The seed's live neighbours for every slot, its adjacency read and each
+// edge hashed once by the whole grid (a hub seed would otherwise be scanned
+// by every slot's probe warp).  Candidate slots from the bucket table (R2),
+// live test R3 / R4.
+__global__ void k_seed_live(ProbeParams P, uint32_t s, uint32_t *slive, uint32_t *scnt) {
+  const uint64_t e0 = P.off[s], e1 = P.off[s + 1];
+  for (uint64_t e = e0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e1;
+       e += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t w = P.nbr[e];
+    const uint64_t a = s < w ? s : w, b = s < w ? w : s;
+    const uint32_t he = (uint32_t)(pc_mix64(((a << 32) | b) ^ P.K) >> 32);
+    uint64_t T = P.t32;
+    if (P.wic) {
+      const uint64_t sd = (e1 - e0) + (P.off[w + 1] - P.off[w]);
+      T = (1ull << 33) / sd;
+      if (T > (1ull << 32)) T = 1ull << 32;
+    }
+    if (T == 0) continue;
+    const uint32_t wb = __clz((uint32_t)(T - 1));
+    uint32_t lo, hi;
+    if (wb >= PACIM_TB) {
+      const uint32_t p = he >> (32 - PACIM_TB);
+      lo = P.tab[p];
+      hi = P.tab[p + 1];
+    } else if (wb == 0) {
+      lo = 0;
+      hi = P.B;
+    } else {
+      const uint32_t p = (he >> (32 - wb)) << (PACIM_TB - wb);
+      lo = P.tab[p];
+      hi = P.tab[p + (1u << (PACIM_TB - wb))];
+    }
+    for (uint32_t j = lo; j < hi; j++) {
+      if ((uint64_t)(P.shr[j] ^ he) >= T) continue;
+      const uint32_t at = atomicAdd(scnt + j, 1u);
+      if (at < QCAP - 1) slive[(size_t)j * QCAP + at] = w;
+    }
+  }
+}
+
 // one warp per slot: BFS from s with a shared-memory queue and visited set
 __global__ void __launch_bounds__(PROBE_WARPS * 32) k_probe(ProbeParams P, uint32_t s) {
   __shared__ uint32_t q[PROBE_WARPS][QCAP];
   __shared__ uint32_t hs[PROBE_WARPS][HCAP];
   __shared__ uint32_t tail[PROBE_WARPS], ovf[PROBE_WARPS], found[PROBE_WARPS];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  unsigned long long mysum = 0, nbig = 0, visits = 0;
+  unsigned long long mysum = 0, nbig = 0, visits = 0, cvis = 0, nfound = 0;
   for (uint32_t j = blockIdx.x * PROBE_WARPS + w; j < P.B; j += gridDim.x * PROBE_WARPS) {
     const uint32_t hr = P.shr[j];
     for (uint32_t i = lane; i < HCAP; i += 32) hs[w][i] = NONE;
@@ -189,6 +232,27 @@ __global__ void __launch_bounds__(PROBE_WARPS * 32) k_probe(ProbeParams P, uint3
       if (ci != NONE && lane == 0) found[w] = P.clabel[(size_t)ci * P.B + j];
     }
     __syncwarp();
+    const uint32_t nsl = P.slive ? P.scnt[j] : QCAP;
+    if (nsl < QCAP - 1) {
+      // the seed was expanded by k_seed_live: its live neighbours are the
+      // next queue entries (distinct: one CSR entry per neighbour), centers
+      // among them recognised at discovery
+      for (uint32_t i = lane; i < nsl; i += 32) {
+        const uint32_t v = P.slive[(size_t)j * QCAP + i];
+        q[w][1 + i] = v;
+        uint32_t h = (v * 2654435761u) & (HCAP - 1);
+        while (atomicCAS(&hs[w][h], NONE, v) != NONE) h = (h + 1) & (HCAP - 1);
+        const uint32_t ci = P.center_of[v];
+        if (ci != NONE) found[w] = P.clabel[(size_t)ci * P.B + j];
+      }
+      if (lane == 0) {
+        tail[w] = 1 + nsl;
+        if (P.is_seed[s]) seed_seen = true;
+      }
+      seed_seen = __shfl_sync(0xffffffffu, seed_seen, 0);
+      head = 1;
+      __syncwarp();
+    }
     while (head < tail[w]) {
       // A center met anywhere in the CC gives the same <size, label> (all
       // centers of a CC share the label), so centers are recognised when
@@ -196,6 +260,8 @@ __global__ void __launch_bounds__(PROBE_WARPS * 32) k_probe(ProbeParams P, uint3
       // live neighbours without filling the queue.
       if (!enumerate && found[w] != NONE) {
         label = found[w];
+        cvis += head;  // Get-center visits until a center was met (Thm 3.1)
+        nfound++;
         delta = P.csw[(size_t)label * P.B + j];
         if (delta == 0 || delta > QCAP) break;  // covered, or too big to enumerate here
         enumerate = true;  // uncovered CC of delta <= QCAP vertices: list its members
@@ -233,6 +299,8 @@ __global__ void __launch_bounds__(PROBE_WARPS * 32) k_probe(ProbeParams P, uint3
       __syncwarp();
       if (!enumerate && found[w] != NONE) {
         label = found[w];
+        cvis += head;
+        nfound++;
         delta = P.csw[(size_t)label * P.B + j];
         if (delta == 0 || delta > QCAP) break;
         // uncovered and small: restart the walk from the queue head to list
@@ -287,6 +355,8 @@ __global__ void __launch_bounds__(PROBE_WARPS * 32) k_probe(ProbeParams P, uint3
     if (mysum) atomicAdd(P.sum + 0, mysum);
     if (nbig) atomicAdd(P.sum + 1, nbig);
     if (visits) atomicAdd(P.sum + 2, visits);
+    if (cvis) atomicAdd(P.sum + 3, cvis);
+    if (nfound) atomicAdd(P.sum + 4, nfound);
   }
 }
 
@@ -395,6 +465,11 @@ void pc_build_compressed(pacim_ctx *ctx) {
   const uint32_t n = ctx->n, nr = ctx->nr, B = ctx->R_local;
   PC_REQUIRE(B >= 1 && B <= 65535, PACIM_EINVAL, "local sketch count must be in [1, 65535]");
   pc_slot_table(ctx);
+  // the uncompressed store and its selection state of an earlier build are
+  // released first (the point of the compressed mode is not to hold them)
+  for (DevBuf *d : {&ctx->L, &ctx->bfs, &ctx->pkeys}) pc_free(ctx, *d);
+  ctx->bfs_nr = 0;
+  ctx->sel_list_valid = false;
   pc_ensure(ctx, ctx->counters, 64 * sizeof(uint64_t));
   unsigned long long *ctr = ctx->counters.as<unsigned long long>();
   PC_CUDA(cudaMemsetAsync(ctr, 0, 64 * sizeof(uint64_t), ctx->stream));
@@ -493,10 +568,10 @@ void pc_select_reset_compressed(pacim_ctx *ctx) {
 // decrease by delta_r.  Returns sum_r delta_r.  Marks s as a seed.
 void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *local_gain) {
   const uint32_t B = ctx->R_local, nr = ctx->nr;
-  pc_ensure(ctx, ctx->sel_list, (size_t)B * 16 + 64);
-  uint32_t *st = ctx->sel_list.as<uint32_t>(), *lab = st + B, *dl = lab + B;
+  pc_ensure(ctx, ctx->cprobe, (size_t)B * 16 + 64);
+  uint32_t *st = ctx->cprobe.as<uint32_t>(), *lab = st + B, *dl = lab + B;
   unsigned long long *sum = reinterpret_cast<unsigned long long *>(dl + B + (B & 1));
-  PC_CUDA(cudaMemsetAsync(sum, 0, 3 * 8, ctx->stream));
+  PC_CUDA(cudaMemsetAsync(sum, 0, 5 * 8, ctx->stream));
   ProbeParams P;
   P.off = ctx->off.as<uint64_t>();
   P.nbr = ctx->nbr.as<uint32_t>();
@@ -511,6 +586,19 @@ void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *l
   P.is_seed = ctx->is_seed.as<uint8_t>();
   P.target = reinterpret_cast<long long *>(target);
   P.dlst = ctx->dlist;
+  P.tab = ctx->d_tab.as<uint16_t>();
+  {  // seed pre-expansion (one grid pass over its adjacency for all slots)
+    pc_ensure(ctx, ctx->cseed, ((size_t)B * QCAP + B) * 4);
+    uint32_t *slive = ctx->cseed.as<uint32_t>(), *scnt = slive + (size_t)B * QCAP;
+    PC_CUDA(cudaMemsetAsync(scnt, 0, (size_t)B * 4, ctx->stream));
+    P.slive = nullptr;
+    P.scnt = nullptr;
+    k_seed_live<<<ctx->sm_count * 4, 256, 0, ctx->stream>>>(P, s, slive, scnt);
+    PC_CHECK_LAUNCH();
+    P.slive = slive;
+    P.scnt = scnt;
+    ctx->launches++;
+  }
   P.st = st;
   P.lab = lab;
   P.dl = dl;
@@ -519,13 +607,42 @@ void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *l
             PROBE_WARPS * 32, 0, ctx->stream>>>(P, s);
   PC_CHECK_LAUNCH();
   ctx->launches++;
-  unsigned long long hs[3];
-  PC_CUDA(cudaMemcpyAsync(hs, sum, 24, cudaMemcpyDeviceToHost, ctx->stream));
+  unsigned long long hs[5];
+  PC_CUDA(cudaMemcpyAsync(hs, sum, 40, cudaMemcpyDeviceToHost, ctx->stream));
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->stats.select_bfs_visits += hs[2];
-  unsigned long long total = hs[0];
+  ctx->stats.select_center_visits += hs[3];
+  ctx->stats.select_center_found += hs[4];
+  unsigned long long total = hs[0], known = 0;
   if (hs[1]) {
-    // big CCs: rebuild the labels of the affected batches, then dense passes
+    std::vector<uint32_t> hst(B), hdl(B);
+    PC_CUDA(cudaMemcpyAsync(hst.data(), st, (size_t)B * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    PC_CUDA(cudaMemcpyAsync(hdl.data(), dl, (size_t)B * 4, cudaMemcpyDeviceToHost, ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    // big CCs with a center (MarkSeed done by the probe, delta = its size):
+    // members enumerated by the store-less cover traversal of select.cu
+    bool unknown = false;
+    std::vector<uint32_t> tdl(B, 0);
+    // giant CCs stay with the batch rebuild + dense pass (a queue traversal of
+    // a giant is slower)
+    const uint64_t big_t = std::max<uint64_t>(65536, nr / 8);
+    for (uint32_t j = 0; j < B; j++) {
+      if (hst[j] == ST_BIG_KNOWN && hdl[j] <= big_t) {
+        tdl[j] = hdl[j];
+        known += hdl[j];
+        hst[j] = ST_DONE;
+      }
+      unknown |= hst[j] == ST_BIG_UNKNOWN;
+    }
+    if (known) {
+      pc_traverse_slots(ctx, s, target, tdl.data());
+      PC_CUDA(cudaMemcpyAsync(st, hst.data(), (size_t)B * 4, cudaMemcpyHostToDevice, ctx->stream));
+    }
+    total += known;
+  }
+  if (hs[1]) {
+    // big CCs without a center among the first QCAP vertices: rebuild the
+    // labels of the affected batches, then dense passes
     std::vector<uint32_t> hst(B);
     PC_CUDA(cudaMemcpyAsync(hst.data(), st, (size_t)B * 4, cudaMemcpyDeviceToHost, ctx->stream));
     uint32_t srow = 0;
@@ -562,6 +679,7 @@ void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *l
     }
     PC_CUDA(cudaMemcpyAsync(&total, sum, 8, cudaMemcpyDeviceToHost, ctx->stream));
     PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    total += known;  // sum[0] holds the probe's and the rebuild's deltas
   }
   k_set_seed<<<1, 1, 0, ctx->stream>>>(reinterpret_cast<long long *>(target), ctx->is_seed.as<uint8_t>(),
                                        s, 0);
@@ -581,6 +699,8 @@ void pc_select_compressed(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *
                           ctx->stream));
   pc_select_reset_compressed(ctx);
   ctx->stats.select_bfs_visits = 0;
+  ctx->stats.select_center_visits = 0;
+  ctx->stats.select_center_found = 0;
   ctx->launches = 0;
   long long run = 0;
   for (uint32_t i = 0; i < k; i++) {

@@ -178,6 +178,8 @@ struct pacim_ctx {
   uint32_t Bb = 0;    // slots per compressed build batch
   DevBuf is_seed;     // u8[n] seeds of the current selection (Get-center seed test)
   DevBuf cwork;       // per-step compressed cover scratch
+  DevBuf cprobe;      // compressed cover: per-slot status / label / delta + sums
+  DevBuf cseed;       // compressed cover: the seed's live neighbours per slot
 
   // scratch
   DevBuf counters;    // u64[64]
@@ -292,6 +294,9 @@ void pc_apply_deltas(pacim_ctx *ctx, int64_t *d_gain, const uint32_t *v, const i
 void pc_apply_dense(pacim_ctx *ctx, int64_t *d_gain, int64_t *d_delta, uint32_t n, uint32_t s);
 void pc_clear_deltas(pacim_ctx *ctx, int64_t *d_delta, const uint32_t *v, uint64_t count);
 void pc_get_labels(pacim_ctx *ctx, uint32_t slot, uint32_t *host_out);
+// the cover traversal alone (no store): for every slot j with delta[j] > 0
+// (HOST array of R_local), the members of C_j(s) lose delta[j] in target
+void pc_traverse_slots(pacim_ctx *ctx, uint32_t s, int64_t *target, const uint32_t *delta);
 
 // grid sizing: multiples of the SM count (148 on B200)
 inline unsigned pc_grid(const pacim_ctx *ctx, size_t work, unsigned block,

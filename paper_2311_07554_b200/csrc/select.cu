@@ -164,6 +164,7 @@ struct Sel {
   unsigned long long cov_cap;
   uint32_t big_t;
   int warp_ok;             // small CCs may use warp_bfs
+  int trav_only;           // no store: dl[] preset per slot, only the member traversal
   // asynchronous traversal
   uint32_t *vis;           // rows x BW: slots in which the row was visited this step
   uint32_t *pend;          // rows x BW: slots reached but not yet expanded (light rows)
@@ -913,7 +914,14 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) k_select(Sel S0, SelOut O, uin
       unsigned long long dsum = 0, nwarp = 0, ndef = 0;
       for (size_t j = gwarp; j < S.B; j += nwarps) {
         uint32_t d = 0;
-        if (lane == 0) d = cover_slot(S, srow, (uint32_t)j);
+        if (S.trav_only) {  // compressed store: MarkSeed done by the Get-center probe
+          if (lane == 0 && __ldcg(S.dl + j)) {
+            atomicOr(S.vis + (size_t)srow * S.BW + (j >> 5), 1u << (j & 31));
+            touch(S, srow);
+          }
+        } else if (lane == 0) {
+          d = cover_slot(S, srow, (uint32_t)j);
+        }
         d = __shfl_sync(0xffffffffu, d, 0);
         __syncwarp();
         dsum += d;
@@ -1137,6 +1145,7 @@ static Sel make_sel(pacim_ctx *ctx, long long *target) {
   }
   S.par = 0;
   S.track = 0;
+  S.trav_only = 0;
   S.tl = nullptr;
   S.tlstep = 0;
   S.ilog = nullptr;
@@ -1382,4 +1391,31 @@ void pc_clear_deltas(pacim_ctx *ctx, int64_t *d_delta, const uint32_t *v, uint64
     PC_CHECK_LAUNCH();
   }
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// Store-less member traversal for the compressed store's big CCs (H10 with
+// H6c): slot j's members of C_j(s) lose delta[j] (HOST, R_local entries).
+void pc_traverse_slots(pacim_ctx *ctx, uint32_t s, int64_t *target, const uint32_t *delta) {
+  Sel S = make_sel(ctx, reinterpret_cast<long long *>(target));
+  S.trav_only = 1;
+  S.warp_ok = 0;  // these CCs are larger than the probe's queue
+  PC_CUDA(cudaMemcpyAsync(S.dl, delta, (size_t)S.B * 4, cudaMemcpyHostToDevice, ctx->stream));
+  pc_ensure(ctx, ctx->sel_gain, 64);
+  pc_ensure(ctx, ctx->sel_seeds, 16);
+  SelOut O;
+  O.k = 1;
+  O.given = s;
+  O.seeds = ctx->sel_seeds.as<uint32_t>();
+  O.gain_num = ctx->sel_gain.as<long long>();
+  O.arg_gain = O.gain_num + 1;
+  const size_t smem = sel_smem(S.B);
+  const unsigned grid = sel_grid(ctx, smem);
+  uint32_t par0 = ctx->sel_par;
+  void *args[] = {&S, &O, &par0};
+  PC_CUDA(cudaLaunchCooperativeKernel((void *)k_select, grid, SEL_THREADS, args, smem, ctx->stream));
+  ctx->sel_par ^= 1;
+  unsigned long long abort_flag = 0;
+  PC_CUDA(cudaMemcpyAsync(&abort_flag, S.diag + DG_ABORT, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  PC_REQUIRE(!abort_flag, PACIM_ECHECK, "compressed cover: traversal watchdog expired");
 }
