@@ -44,6 +44,7 @@ def lib():
             "orc_hash_edge": (u64, [u64, u32, u32, u32]),
             "orc_t32_const": (u64, [dbl]),
             "orc_t32_wic": (u64, [u64, u64]),
+            "orc_t32_uniform": (u64, [u64, u32, u32]),
             "orc_live": (i32, [u64, u32, u32, u32, u64]),
             "orc_sketch_labels": (C.c_long, [u32, P, P, i32, u64, u64, u32, P, P]),
             "orc_greedy": (i32, [u32, P, P, i32, u64, u32, u64, u32, P, P, P, P]),
@@ -85,6 +86,18 @@ def t32_const(p: float) -> int:
 
 def t32_wic(du: int, dv: int) -> int:
     return lib().orc_t32_wic(du, dv)
+
+
+def uniform_param(lo: float, hi: float) -> int:
+    """R19: the Uniform model's packed parameter H << 32 | L (IEEE double floors)."""
+    L = t32_const(lo)
+    H = min(t32_const(hi), (1 << 32) - 1)
+    L = min(L, H)
+    return (H << 32) | L
+
+
+def t32_uniform(packed: int, u: int, v: int) -> int:
+    return lib().orc_t32_uniform(packed, u, v)
 
 
 def live(seed: int, u: int, v: int, r: int, t32: int) -> bool:

@@ -15,6 +15,9 @@
  * Functions and what pins them (tests/test_oracle_*.py):
  *   orc_mix64 ............ published splitmix64 output vectors (pinned)
  *   orc_t32_const/wic .... closed forms p=0,1/2,1 and 2/(du+dv) (pinned)
+ *   orc_t32_uniform ...... R19, U(lo, hi) per edge from the edge key: lo = hi
+ *                          reduces to the constant; range, mean and
+ *                          uniformity checked statistically (pinned)
  *   orc_live ............. symmetry, p=0/1 extremes, live fraction ~ p (pinned, statistical)
  *   orc_sketch_labels .... scipy connected_components on the materialised
  *                          sampled graph; p=0 / p=1 special cases (pinned)
@@ -88,6 +91,24 @@ uint64_t orc_t32_wic(uint64_t du, uint64_t dv)
     return t > (1ull << 32) ? (1ull << 32) : t;
 }
 
+/* R19 (NEXT f4): Uniform p(u,v) ~ U(lo, hi) ("draw a uniform random
+ * number from x to y" per edge), drawn deterministically from the edge key
+ * with a fixed key K_U (a graph property, independent of the
+ * sketch hash seed):
+ *     L = floor(lo 2^32), H = min(floor(hi 2^32), 2^32 - 1)   (IEEE double)
+ *     u = hi32(mix64((min<<32 | max) xor K_U))                 uniform on [0, 2^32)
+ *     T32(u,v) = L + floor((H - L) u / 2^32)                   in [L, H]
+ * The model's parameter packs both bounds: t32 = H << 32 | L. */
+#define ORC_K_U_SEED 0x5EED0F0DDBA11E55ull
+
+uint64_t orc_t32_uniform(uint64_t packed, uint32_t u, uint32_t v)
+{
+    uint64_t L = packed & 0xFFFFFFFFull, H = packed >> 32;
+    uint64_t a = u < v ? u : v, b = u < v ? v : u;
+    uint64_t x = orc_mix64(((a << 32) | b) ^ orc_mix64(ORC_K_U_SEED)) >> 32;
+    return L + (((H - L) * x) >> 32);
+}
+
 /* P:4: edge (u,v) is in the r-th sampled graph iff hash_edge(u,v,r) < p(u,v);
  * R3: with p quantised to T32 this is hash_edge < T32 * 2^32. */
 int orc_live(uint64_t hash_seed, uint32_t u, uint32_t v, uint32_t r, uint64_t t32)
@@ -97,12 +118,15 @@ int orc_live(uint64_t hash_seed, uint32_t u, uint32_t v, uint32_t r, uint64_t t3
     return h < (t32 << 32);
 }
 
-/* Probability model of an edge of the CSR graph: 0 = constant T32, 1 = WIC. */
+/* Probability model of an edge of the CSR graph: 0 = constant T32, 1 = WIC,
+ * 2 = Uniform U(lo, hi) (R19; t32 = H << 32 | L). */
 static uint64_t edge_t32(int model, uint64_t t32, const uint64_t *off,
                          uint32_t u, uint32_t v)
 {
     if (model == 1)
         return orc_t32_wic(off[u + 1] - off[u], off[v + 1] - off[v]);
+    if (model == 2)
+        return orc_t32_uniform(t32, u, v);
     return t32;
 }
 

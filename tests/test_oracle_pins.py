@@ -53,6 +53,35 @@ def test_t32_wic_matches_paper_formula(orc):
     assert orc.t32_wic(1, 2) == (1 << 33) // 3  # path 0-1-2, edge (0,1): p = 2/3
 
 
+def test_t32_uniform_pins(orc):
+    """R19 (P:2032 'draw a uniform random number from x to y'; SPEC S:31 'per-edge
+    value drawn deterministically from the edge key'): lo = hi reduces to the
+    constant threshold; every value lies in [L, H]; symmetric in (u, v); over
+    2e5 edges the mean is (L + H) / 2 within 5 sigma of a uniform law and a
+    20-bin histogram passes chi-square at 1e-4."""
+    rng = np.random.default_rng(7)
+    us = rng.integers(0, 1 << 31, 200000)
+    vs = rng.integers(0, 1 << 31, 200000)
+    for p in (0.0, 0.02, 0.5):
+        P = orc.uniform_param(p, p)
+        assert all(orc.t32_uniform(P, int(u), int(v)) == orc.t32_const(p)
+                   for u, v in zip(us[:200], vs[:200]))
+    lo, hi = 0.1, 0.3
+    P = orc.uniform_param(lo, hi)
+    L, H = P & 0xFFFFFFFF, P >> 32
+    assert L == orc.t32_const(lo) and H == orc.t32_const(hi)
+    t = np.array([orc.t32_uniform(P, int(u), int(v)) for u, v in zip(us, vs)], np.float64)
+    assert t.min() >= L and t.max() <= H
+    assert all(orc.t32_uniform(P, int(u), int(v)) == orc.t32_uniform(P, int(v), int(u))
+               for u, v in zip(us[:500], vs[:500]))
+    x = (t - L) / (H - L)
+    assert abs(x.mean() - 0.5) < 5 * math.sqrt(1 / 12 / len(x))
+    cnt = np.histogram(x, bins=20, range=(0, 1))[0]
+    chi2 = ((cnt - len(x) / 20) ** 2 / (len(x) / 20)).sum()
+    assert chi2 < 53.0  # chi-square 19 dof, p = 1e-4
+    assert orc.uniform_param(0.5, 1.0) >> 32 == (1 << 32) - 1  # hi = 1: H capped below 2^32
+
+
 def test_live_symmetry_and_extremes(orc):
     rng = np.random.default_rng(1)
     for _ in range(500):
@@ -92,7 +121,8 @@ def materialise(orc, g, model, t32, seed, r):
             v = int(g.nbr[e])
             if v <= u:
                 continue
-            t = orc.t32_wic(int(deg[u]), int(deg[v])) if model == 1 else t32
+            t = (orc.t32_wic(int(deg[u]), int(deg[v])) if model == 1 else
+                 orc.t32_uniform(t32, u, v) if model == 2 else t32)
             if orc.live(seed, u, v, r, t):
                 out.append((u, v))
     return out
@@ -123,14 +153,23 @@ def tiny_graph(i):
     return Graph(n, off, nbr)
 
 
-PS = [0.0, 0.05, 0.2, 0.5, 1.0, "wic"]
+PS = [0.0, 0.05, 0.2, 0.5, 1.0, "wic", ("unif", 0.0, 0.1), ("unif", 0.1, 0.3), ("unif", 0.3, 0.9)]
 
 
-@pytest.mark.parametrize("i", range(12))
+def model_of(orc, p):
+    """(model, t32): constant, WIC (R4) or Uniform U(lo, hi) (R19)."""
+    if p == "wic":
+        return 1, 0
+    if isinstance(p, tuple):
+        return 2, orc.uniform_param(p[1], p[2])
+    return 0, orc.t32_const(p)
+
+
+@pytest.mark.parametrize("i", range(18))
 def test_sketch_labels_equal_scipy_on_materialised_graph(orc, i):
     g = tiny_graph(i)
     p = PS[i % len(PS)]
-    model, t32 = (1, 0) if p == "wic" else (0, orc.t32_const(p))
+    model, t32 = model_of(orc, p)
     for r in (0, 3, 17):
         seed = 11 + i
         lab, sz = orc.sketch_labels(g, model, t32, seed, r)
@@ -178,13 +217,13 @@ def brute_greedy(n, labs, k):
     return S, gains, sig
 
 
-@pytest.mark.parametrize("i", range(10))
+@pytest.mark.parametrize("i", range(14))
 def test_greedy_equals_brute_force(orc, i):
     g = tiny_graph(i)
     if g.n > 60:
         return
     p = PS[(i + 1) % len(PS)]
-    model, t32 = (1, 0) if p == "wic" else (0, orc.t32_const(p))
+    model, t32 = model_of(orc, p)
     R, k, seed = [4, 16][i % 2], min(6, g.n), 40 + i
     seeds, gain, sigma, gain0 = orc.greedy(g, model, t32, R, seed, k, want_gain0=True)
     labs = [scipy_labels(g.n, materialise(orc, g, model, t32, seed, r))[0] for r in range(R)]
@@ -230,7 +269,7 @@ def test_greedy_one_minus_inv_e_of_brute_force_opt(orc, i):
     # greedy achieves (1-1/e) OPT of the (coverage) estimator.
     g = tiny_graph(i * 4)  # n = 12
     p = [0.2, 0.5, "wic"][i % 3]
-    model, t32 = (1, 0) if p == "wic" else (0, orc.t32_const(p))
+    model, t32 = model_of(orc, p)
     R, seed = 8, 70 + i
     labs = [scipy_labels(g.n, materialise(orc, g, model, t32, seed, r))[0] for r in range(R)]
     sizes = [np.bincount(l, minlength=g.n) for l in labs]
@@ -267,7 +306,7 @@ def exact_sigma(n, edges, probs, S):
     return tot
 
 
-@pytest.mark.parametrize("case", ["star", "path", "er8", "wic"])
+@pytest.mark.parametrize("case", ["star", "path", "er8", "wic", "unif"])
 def test_sigma_hat_unbiased_across_hash_seeds(orc, case):
     """Mean over hash seeds of sigma_hat(S) = gain0/R equals exact sigma(S)
     within 4.5 empirical standard errors (F1: the literal rule correlates
@@ -281,14 +320,19 @@ def test_sigma_hat_unbiased_across_hash_seeds(orc, case):
         off, nbr = inputs.random_graph(8, 11, seed=3)
         edges = [(u, int(v)) for u in range(8) for v in nbr[off[u]:off[u + 1]] if v > u]
         n, p = 8, 0.3
-    else:
+    elif case == "wic":
         n, edges, p = 7, [(0, 1), (1, 2), (2, 3), (0, 3), (3, 4), (4, 5), (5, 6)], "wic"
+    else:
+        n, edges, p = 7, [(0, 1), (1, 2), (2, 3), (0, 3), (3, 4), (4, 5), (5, 6)], ("unif", 0.1, 0.6)
     off, nbr = inputs.csr_from_edges(n, edges)
     g = Graph(n, off, nbr)
     deg = np.diff(off.astype(np.int64))
     if p == "wic":
         model, t32 = 1, 0
         probs = [orc.t32_wic(int(deg[u]), int(deg[v])) / 2**32 for u, v in edges]
+    elif isinstance(p, tuple):
+        model, t32 = 2, orc.uniform_param(p[1], p[2])
+        probs = [orc.t32_uniform(t32, u, v) / 2**32 for u, v in edges]
     else:
         model, t32 = 0, orc.t32_const(p)
         probs = [t32 / 2**32] * len(edges)
