@@ -104,7 +104,7 @@ def kernel_bytes(st: dict, cfg: dict, k: int) -> dict:
     """Algorithmic bytes per launch of each kernel."""
     n, m, B, rows = st["n"], st["m"], st["R_local"], st["rows"]
     L = 4 * rows * B                      # the store: one u32 slot per (row, sketch)
-    wic = 4 * m if cfg["pmodel"] == 1 else 0
+    wic = 4 * m if cfg["pmodel"] != 0 else 0  # per-edge thresholds (WIC, Uniform)
     nonroot = st["nnonsingle"] - st["ncomp"]
     return {
         "k_init": L,                                        # write every slot
@@ -113,7 +113,7 @@ def kernel_bytes(st: dict, cfg: dict, k: int) -> dict:
         "k_gain0": L + 8 * n + 4 * nonroot,                 # slots, gain0, root-size reads
         # traversal reads (CSR entry + WIC threshold) + the dense passes over the
         # store + one read of the gains per step for the chunk maxima (upper bound)
-        "k_select": (4 + (4 if cfg["pmodel"] == 1 else 0)) * st["select_edges"]
+        "k_select": (4 + (4 if cfg["pmodel"] != 0 else 0)) * st["select_edges"]
                     + L * st["select_dense_steps"] + k * 16 * 4096,
     }
 
@@ -121,7 +121,7 @@ def kernel_bytes(st: dict, cfg: dict, k: int) -> dict:
 def build_bytes(st: dict, cfg: dict) -> int:
     """CSR_upper * ceil(R_g/B) + 16 n R_g (one pass, B = R_g)."""
     csr_upper = 16 * st["m"]  # u64 hash key + u64 row pair per upper edge read by k_edges
-    if cfg["pmodel"] == 1:
+    if cfg["pmodel"] != 0:
         csr_upper += 4 * st["m"]
     return csr_upper + 16 * st["rows"] * st["R_local"]
 

@@ -54,7 +54,7 @@ typedef enum {
 } pacim_status;
 
 /* Edge-probability models (P:1314-1317 constant p; P:2034 WIC). */
-enum { PACIM_P_CONST = 0, PACIM_P_WIC = 1 };
+enum { PACIM_P_CONST = 0, PACIM_P_WIC = 1, PACIM_P_UNIFORM = 2 };
 /* Synthetic generators (DESIGN.md §Input recipe). */
 enum { PACIM_GEN_ER = 0, PACIM_GEN_RMAT = 1, PACIM_GEN_GRID = 2 };
 
@@ -119,13 +119,20 @@ PACIM_API const char *pacim_version(void);
  * gives 0 (R3; P:4 "hash_edge < p(u,v)"). */
 PACIM_API uint64_t pacim_threshold_from_p(double p);
 
+/* The Uniform model's parameter (R19): L = floor(lo 2^32), H = min(floor(hi
+ * 2^32), 2^32 - 1) in IEEE double, returned packed as H << 32 | L (L <= H);
+ * lo, hi are clamped to [0, 1] and swapped if lo > hi. */
+PACIM_API uint64_t pacim_threshold_uniform(double lo, double hi);
+
 /* ------------------------------------------------------------------- graph */
 
 /* H0/H1.  Load the symmetric CSR from HOST arrays offsets[n+1], neighbors[nnz]
  * and set the edge model: pmodel = PACIM_P_CONST with t32 = T32 in [0, 2^32]
  * (every edge live in sketch r iff hash_edge(u,v,r) < T32 * 2^32, R3),
  * or PACIM_P_WIC (t32 ignored; T32(u,v) = min(2^32, floor(2^33/(d_u+d_v))),
- * P:2034, R4).  validate: 0 = trust the caller; 1 = check offsets, id range,
+ * P:2034, R4), or PACIM_P_UNIFORM (p(u,v) ~ U(lo, hi) drawn from the edge key,
+ * P:2032, R19: t32 = H << 32 | L from pacim_threshold_uniform, T32(u,v) =
+ * L + ((H - L) * hi32(mix64((min<<32|max) ^ K_U))) >> 32).  validate: 0 = trust the caller; 1 = check offsets, id range,
  * sorted lists without loops or duplicates (EINVAL naming the first bad
  * vertex); 2 = also check symmetry.  EINVAL also for n == 0, n >= 2^31,
  * offsets[0] != 0, offsets[n] != nnz, nnz odd, t32 > 2^32.  Replaces any

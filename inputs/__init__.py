@@ -20,7 +20,7 @@ import numpy as np
 # ---------------------------------------------------------------------------
 
 GEN_ER, GEN_RMAT, GEN_GRID = 0, 1, 2
-P_CONST, P_WIC = 0, 1
+P_CONST, P_WIC, P_UNIFORM = 0, 1, 2  # P_UNIFORM: p ~ U(lo, hi), cfg['p_range'] (R19)
 
 
 def rmat_thresholds(a: float, b: float, c: float) -> tuple[int, int, int]:

@@ -165,6 +165,8 @@ def model_args(cfg: dict):
     """(model, t32) for a config: the oracle quantises p itself."""
     if cfg["pmodel"] == 1:
         return 1, 0
+    if cfg["pmodel"] == 2:
+        return 2, uniform_param(*cfg["p_range"])
     return 0, t32_const(cfg["p"])
 
 

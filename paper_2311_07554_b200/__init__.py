@@ -12,10 +12,12 @@ from .binding import (  # noqa: F401
     PACIM_GEN_RMAT,
     PACIM_P_CONST,
     PACIM_P_WIC,
+    PACIM_P_UNIFORM,
     Context,
     PacimError,
     lib,
     lib_path,
     pacim_threshold_from_p,
+    pacim_threshold_uniform,
     pacim_version,
 )

@@ -9,7 +9,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(HERE, "libpacim.so")
 
-PACIM_P_CONST, PACIM_P_WIC = 0, 1
+PACIM_P_CONST, PACIM_P_WIC, PACIM_P_UNIFORM = 0, 1, 2
 PACIM_GEN_ER, PACIM_GEN_RMAT, PACIM_GEN_GRID = 0, 1, 2
 STATUS = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -5: "ESTATE",
           -6: "ENOTIMPL", -7: "ECHECK"}
@@ -17,7 +17,7 @@ STATUS = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -5: "ESTATE",
 # Every function declared in include/pacim.h (tests check the .so exports them).
 EXPORTS = [
     "pacim_create", "pacim_destroy", "pacim_last_error", "pacim_version",
-    "pacim_threshold_from_p", "pacim_load_graph", "pacim_load_graph_device",
+    "pacim_threshold_from_p", "pacim_threshold_uniform", "pacim_load_graph", "pacim_load_graph_device",
     "pacim_generate_graph", "pacim_graph_info", "pacim_get_graph",
     "pacim_build_sketches", "pacim_select_seeds", "pacim_gain0_to_device",
     "pacim_select_reset", "pacim_cover_local", "pacim_cover_local_sparse",
@@ -76,6 +76,7 @@ def lib():
             "pacim_last_error": (C.c_char_p, [P]),
             "pacim_version": (C.c_char_p, []),
             "pacim_threshold_from_p": (u64, [C.c_double]),
+            "pacim_threshold_uniform": (u64, [C.c_double, C.c_double]),
             "pacim_load_graph": (i32, [P, u32, u64, P, P, i32, u64, i32]),
             "pacim_load_graph_device": (i32, [P, u32, u64, P, P, i32, u64, i32]),
             "pacim_generate_graph": (i32, [P, i32, P, i32, u64, i32, u64]),
@@ -106,6 +107,10 @@ def lib():
 
 def pacim_threshold_from_p(p: float) -> int:
     return int(lib().pacim_threshold_from_p(float(p)))
+
+
+def pacim_threshold_uniform(lo: float, hi: float) -> int:
+    return int(lib().pacim_threshold_uniform(float(lo), float(hi)))
 
 
 def pacim_version() -> str:

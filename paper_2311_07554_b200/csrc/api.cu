@@ -87,6 +87,15 @@ extern "C" {
 
 const char *pacim_version(void) { return "pacim-b200 0.1 (sm_100a)"; }
 
+uint64_t pacim_threshold_uniform(double lo, double hi) {
+  lo = std::isnan(lo) ? 0.0 : std::min(1.0, std::max(0.0, lo));
+  hi = std::isnan(hi) ? 0.0 : std::min(1.0, std::max(0.0, hi));
+  if (lo > hi) std::swap(lo, hi);
+  const uint64_t H = std::min<uint64_t>(pacim_threshold_from_p(hi), 0xFFFFFFFFull);
+  const uint64_t L = std::min<uint64_t>(pacim_threshold_from_p(lo), H);
+  return (H << 32) | L;
+}
+
 uint64_t pacim_threshold_from_p(double p) {
   if (!(p > 0.0)) return 0;
   if (p >= 1.0) return 1ull << 32;
@@ -142,9 +151,11 @@ const char *pacim_last_error(const pacim_ctx *ctx) {
 }
 
 static void check_model(int pmodel, uint64_t t32) {
-  PC_REQUIRE(pmodel == PACIM_P_CONST || pmodel == PACIM_P_WIC, PACIM_EINVAL,
-             "pmodel must be PACIM_P_CONST or PACIM_P_WIC");
+  PC_REQUIRE(pmodel == PACIM_P_CONST || pmodel == PACIM_P_WIC || pmodel == PACIM_P_UNIFORM,
+             PACIM_EINVAL, "pmodel must be PACIM_P_CONST, PACIM_P_WIC or PACIM_P_UNIFORM");
   PC_REQUIRE(pmodel != PACIM_P_CONST || t32 <= (1ull << 32), PACIM_EINVAL, "t32 > 2^32");
+  PC_REQUIRE(pmodel != PACIM_P_UNIFORM || (t32 & 0xFFFFFFFFull) <= (t32 >> 32), PACIM_EINVAL,
+             "uniform model: L > H in t32 = H << 32 | L");
 }
 
 static void load_common(pacim_ctx *ctx, uint32_t n, uint64_t nnz, int pmodel, uint64_t t32) {

@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__res
     uint64_t eT = 0;
     if (e < m) {
       const uint64_t key = keys[e];
-      const uint64_t T = WIC ? (uint64_t)tm1[e] + 1 : t32;
+      const uint64_t T = WIC ? (uint64_t)tm1[e] + t32 : t32;  // per-edge: t32 = toff
       const uint32_t he = (uint32_t)(pc_mix64(key ^ K) >> 32);
       uint32_t lo = 0, hi = 0;
       if (T != 0) {
@@ -656,12 +656,12 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
   {
     size_t smem = B * sizeof(uint32_t) + (NT + 1) * sizeof(uint16_t);
     unsigned g = pc_grid(ctx, (es.m + 31) / 32 * 32, EDGE_THREADS, 8);
-    if (ctx->pmodel == PACIM_P_WIC) {
+    if (ctx->pmodel != PACIM_P_CONST) {  // per-edge thresholds (WIC, Uniform)
       auto kern = hla.cnt ? k_edges<true, true> : k_edges<true, false>;
       PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
           es.keys, es.ckeys, ctx->tm1.as<uint32_t>(), es.m,
-          ctx->K, 0, ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla);
+          ctx->K, ctx->toff(), ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla);
     } else {
       auto kern = hla.cnt ? k_edges<false, true> : k_edges<false, false>;
       PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -136,6 +136,7 @@ struct ProbeParams {
   const uint32_t *nbr;
   uint64_t K, t32;
   int wic;
+  int unif;                 // R19: T32 from the edge key (t32 = H << 32 | L)
   const uint32_t *shr;      // hi32(hash(r)) per slot
   uint32_t B;
   const uint32_t *center_of;
@@ -162,6 +163,8 @@ __device__ __forceinline__ bool live_edge(const ProbeParams &P, uint32_t x, uint
     const uint64_t s = (P.off[x + 1] - P.off[x]) + (P.off[w + 1] - P.off[w]);
     T = (1ull << 33) / s;
     if (T > (1ull << 32)) T = 1ull << 32;
+  } else if (P.unif) {  // R19
+    T = pc_t32_uniform(P.t32, (a << 32) | b);
   }
   return (uint64_t)(hr ^ he) < T;  // R3
 }
@@ -182,6 +185,8 @@ __global__ void k_seed_live(ProbeParams P, uint32_t s, uint32_t *slive, uint32_t
       const uint64_t sd = (e1 - e0) + (P.off[w + 1] - P.off[w]);
       T = (1ull << 33) / sd;
       if (T > (1ull << 32)) T = 1ull << 32;
+    } else if (P.unif) {
+      T = pc_t32_uniform(P.t32, (a << 32) | b);
     }
     if (T == 0) continue;
     const uint32_t wb = __clz((uint32_t)(T - 1));
@@ -578,6 +583,7 @@ void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *l
   P.K = ctx->K;
   P.t32 = ctx->t32;
   P.wic = ctx->pmodel == PACIM_P_WIC;
+  P.unif = ctx->pmodel == PACIM_P_UNIFORM;
   P.shr = ctx->d_shr.as<uint32_t>();
   P.B = B;
   P.center_of = ctx->center_of.as<uint32_t>();

@@ -211,6 +211,26 @@ __global__ void k_wic_csr(const uint64_t *off, const uint32_t *nbr, uint32_t n, 
   }
 }
 
+// R19 Uniform thresholds per upper edge / per CSR entry (stored as T32, toff 0)
+__global__ void k_unif(const uint64_t *keys, uint64_t m, uint64_t packed, uint32_t *tm1) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (size_t)gridDim.x * blockDim.x)
+    tm1[e] = (uint32_t)pc_t32_uniform(packed, keys[e]);
+}
+__global__ void k_unif_csr(const uint64_t *off, const uint32_t *nbr, uint32_t n, uint64_t packed,
+                           uint32_t *tcsr) {
+  const int lane = threadIdx.x & 31;
+  size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t x = warp; x < n; x += nw) {
+    for (uint64_t e = off[x] + lane; e < off[x + 1]; e += 32) {
+      const uint64_t w = nbr[e];
+      const uint64_t key = x < w ? ((uint64_t)x << 32) | w : (w << 32) | x;
+      tcsr[e] = (uint32_t)pc_t32_uniform(packed, key);
+    }
+  }
+}
+
 __global__ void k_wic(const uint64_t *keys, uint64_t m, const uint64_t *off, uint32_t *tm1) {
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
        e += (size_t)gridDim.x * blockDim.x) {
@@ -350,6 +370,16 @@ static void derive_common(pacim_ctx *ctx) {
                                                         ctx->hidx.as<uint32_t>(),
                                                         ctx->ckeys.as<uint64_t>());
   PC_CHECK_LAUNCH();
+  if (ctx->pmodel == PACIM_P_UNIFORM) {
+    pc_ensure(ctx, ctx->tm1, std::max<size_t>(m, 1) * sizeof(uint32_t));
+    k_unif<<<pc_grid(ctx, m, 256), 256, 0, ctx->stream>>>(ctx->keys.as<uint64_t>(), m, ctx->t32,
+                                                         ctx->tm1.as<uint32_t>());
+    PC_CHECK_LAUNCH();
+    pc_ensure(ctx, ctx->tcsr, std::max<size_t>(2 * m, 1) * sizeof(uint32_t));
+    k_unif_csr<<<pc_grid(ctx, (size_t)n * 32, 256), 256, 0, ctx->stream>>>(
+        off, ctx->nbr.as<uint32_t>(), n, ctx->t32, ctx->tcsr.as<uint32_t>());
+    PC_CHECK_LAUNCH();
+  }
   if (ctx->pmodel == PACIM_P_WIC) {
     pc_ensure(ctx, ctx->tm1, std::max<size_t>(m, 1) * sizeof(uint32_t));
     k_wic<<<pc_grid(ctx, m, 256), 256, 0, ctx->stream>>>(ctx->keys.as<uint64_t>(), m, off,

@@ -41,6 +41,14 @@ __host__ __device__ __forceinline__ uint64_t pc_mix64(uint64_t z) {
   return z;
 }
 
+// R19: Uniform U(lo, hi) threshold of edge key (min<<32 | max), packed = H<<32|L
+#define PACIM_K_U_SEED 0x5EED0F0DDBA11E55ull
+__host__ __device__ __forceinline__ uint64_t pc_t32_uniform(uint64_t packed, uint64_t key) {
+  const uint64_t L = packed & 0xFFFFFFFFull, H = packed >> 32;
+  const uint64_t x = pc_mix64(key ^ pc_mix64(PACIM_K_U_SEED)) >> 32;
+  return L + (((H - L) * x) >> 32);
+}
+
 // ------------------------------------------------------------ error helpers
 struct PacimError {
   int code;
@@ -109,13 +117,16 @@ struct pacim_ctx {
   bool has_graph = false;
   uint32_t n = 0;
   uint64_t m = 0;        // undirected edges
-  int pmodel = 0;        // PACIM_P_CONST / PACIM_P_WIC
+  int pmodel = 0;        // PACIM_P_CONST / PACIM_P_WIC / PACIM_P_UNIFORM
+  // per-edge thresholds (WIC, Uniform) are stored as T32 - toff in u32
+  // (WIC: T32 in [1, 2^32], toff = 1; Uniform: T32 in [0, 2^32 - 1], toff = 0)
+  uint32_t toff() const { return pmodel == PACIM_P_WIC ? 1u : 0u; }
   uint64_t t32 = 0;      // constant threshold (R3)
   DevBuf off;            // u64[n+1] full CSR offsets
   DevBuf nbr;            // u32[2m]  full CSR neighbours
   DevBuf keys;           // u64[m]   upper edge list min<<32|max, sorted
-  DevBuf tm1;            // u32[m]   WIC: T32(e) - 1
-  DevBuf tcsr;           // u32[2m]  WIC: T32 - 1 per CSR entry (traversals)
+  DevBuf tm1;            // u32[m]   per-edge models: T32(e) - toff()
+  DevBuf tcsr;           // u32[2m]  per-edge models: T32 - toff() per CSR entry (traversals)
   DevBuf ckeys;          // u64[m]   the same edges as store rows: row(min)<<32|row(max);
                          //          bit 31 of a half flags a hub row (PACIM_HUBF)
   DevBuf cid;            // u32[n]   store row of v, or 0xFFFFFFFF for isolated v

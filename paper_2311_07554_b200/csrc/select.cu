@@ -145,8 +145,9 @@ struct Sel {
   const uint64_t *off;
   const uint32_t *nbr;
   uint64_t K, t32;
-  const uint32_t *tcsr;  // WIC: T32 - 1 per CSR entry
-  int wic;
+  const uint32_t *tcsr;  // per-edge models: T32 - toff per CSR entry
+  int wic;                // per-edge thresholds (WIC or Uniform)
+  uint32_t toff;
   const uint32_t *g_shr;   // hi32(hash(r)) of slot j (sorted)
   const uint16_t *g_tab;   // candidate bucket table of the sorted slots
   // store
@@ -357,7 +358,7 @@ __device__ bool warp_bfs(const Sel &S, uint32_t s, uint32_t j, uint32_t delta, u
         const uint32_t w = S.nbr[e];
         const uint64_t lo = xa < w ? xa : w, hi = xa < w ? w : xa;
         const uint32_t he = (uint32_t)(pc_mix64(((lo << 32) | hi) ^ S.K) >> 32);
-        const uint64_t T = S.wic ? (uint64_t)S.tcsr[e] + 1 : S.t32;  // R4
+        const uint64_t T = S.wic ? (uint64_t)S.tcsr[e] + S.toff : S.t32;  // R4 / R19
         if ((uint64_t)(hr ^ he) >= T) continue;                        // R3
         uint32_t h = (w * 2654435761u) & (HCAP - 1);
         for (;;) {
@@ -475,7 +476,7 @@ __device__ __forceinline__ void expand_range(const Sel &S, uint32_t x, uint64_t 
 #pragma unroll
     for (int u = 0; u < EU; u++) {
       if (w[u] == NONE) continue;
-      const uint64_t T = S.wic ? (uint64_t)tm[u] + 1 : S.t32;  // R3 / R4
+      const uint64_t T = S.wic ? (uint64_t)tm[u] + S.toff : S.t32;  // R3 / R4 / R19
       expand_edge(S, x, w[u], T, M, s, shr, tab, sdl, ls);
     }
   }
@@ -1063,7 +1064,8 @@ static Sel make_sel(pacim_ctx *ctx, long long *target) {
   S.K = ctx->K;
   S.t32 = ctx->t32;
   S.tcsr = ctx->tcsr.as<uint32_t>();
-  S.wic = ctx->pmodel == PACIM_P_WIC;
+  S.wic = ctx->pmodel != PACIM_P_CONST;  // per-edge thresholds in tcsr
+  S.toff = ctx->toff();
   S.g_shr = ctx->d_shr.as<uint32_t>();
   S.g_tab = ctx->d_tab.as<uint16_t>();
   S.L = ctx->L.as<uint32_t>();

@@ -3,6 +3,7 @@ the device, build the sketches, select seeds.  Argument marshalling only."""
 from __future__ import annotations
 
 from .binding import (PACIM_GEN_ER, PACIM_GEN_GRID, PACIM_GEN_RMAT, PACIM_P_CONST, PACIM_P_WIC,
+                      PACIM_P_UNIFORM, pacim_threshold_uniform,
                       Context, pacim_threshold_from_p)
 
 
@@ -10,6 +11,8 @@ def model_of(cfg: dict) -> tuple[int, int]:
     """(pmodel, t32) of a config dict (see inputs.CONFIGS)."""
     if cfg["pmodel"] == PACIM_P_WIC:
         return PACIM_P_WIC, 0
+    if cfg["pmodel"] == PACIM_P_UNIFORM:  # R19: p ~ U(lo, hi) per edge
+        return PACIM_P_UNIFORM, pacim_threshold_uniform(*cfg["p_range"])
     return PACIM_P_CONST, pacim_threshold_from_p(cfg["p"])
 
 

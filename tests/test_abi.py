@@ -39,7 +39,7 @@ def test_binding_names_match_header(libpath):
     assert sorted(binding.EXPORTS) == header_symbols()
     for s in header_symbols():
         if s in ("pacim_create", "pacim_destroy", "pacim_last_error", "pacim_version",
-                 "pacim_threshold_from_p"):
+                 "pacim_threshold_from_p", "pacim_threshold_uniform"):
             continue
         assert hasattr(binding.Context, s), s
 

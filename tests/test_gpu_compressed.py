@@ -37,6 +37,8 @@ CASES = [
     (lambda: inputs.random_graph(400, 800, 47), 0.0, 5, 4, 1 << 29),
     (lambda: inputs.star_graph(5000), 0.5, 6, 3, 1 << 28),                   # hub: queue overflow
     (lambda: inputs.random_powerlaw_graph(20000, 60000, 49), 0.3, 8, 5, 1 << 24),
+    (lambda: inputs.random_powerlaw_graph(3000, 15000, 50), ("unif", 0.0, 0.1), 32, 8, 1 << 28),
+    (lambda: inputs.random_graph(2000, 8000, 51), ("unif", 0.1, 0.3), 16, 6, 1 << 28),
 ]
 
 
@@ -45,7 +47,12 @@ def run_case(orc, ctx, i, check_sketches=True):
     build_fn, p, R, k, a32 = CASES[i]
     off, nbr = build_fn()
     g = Graph(len(off) - 1, off, nbr)
-    model, t32 = (1, 0) if p == "wic" else (0, orc.t32_const(p))
+    if p == "wic":
+        model, t32 = 1, 0
+    elif isinstance(p, tuple):  # R19 Uniform U(lo, hi)
+        model, t32 = 2, orc.uniform_param(p[1], p[2])
+    else:
+        model, t32 = 0, orc.t32_const(p)
     seed = 500 + i
     ctx.pacim_load_graph(g.off, g.nbr, model, t32, 2)
     ctx.pacim_build_sketches(R, seed, a32)

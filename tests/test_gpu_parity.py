@@ -70,7 +70,23 @@ CASES = [
     (lambda: inputs.random_powerlaw_graph(4000, 30000, 8), 0.05, 256, 30),
     (lambda: inputs.star_graph(50), 0.3, 64, 4),
     (lambda: inputs.path_graph(257), 0.9, 40, 7),
+    (lambda: inputs.random_powerlaw_graph(3000, 20000, 12), ("unif", 0.0, 0.1), 64, 12),
+    (lambda: inputs.random_graph(2000, 8000, 13), ("unif", 0.1, 0.3), 32, 10),
 ]
+
+
+def model_of(orc, p):
+    """(model, t32) for the oracle and the library alike: constant, WIC, or
+    Uniform U(lo, hi) (R19; the library's own pacim_threshold_uniform must
+    give the oracle's packed parameter)."""
+    if p == "wic":
+        return 1, 0
+    if isinstance(p, tuple):
+        from paper_2311_07554_b200 import pacim_threshold_uniform
+        t = orc.uniform_param(p[1], p[2])
+        assert pacim_threshold_uniform(p[1], p[2]) == t
+        return 2, t
+    return 0, orc.t32_const(p)
 
 
 @pytest.mark.parametrize("i", range(len(CASES)))
@@ -79,11 +95,11 @@ def test_tiny_corpus_parity(orc, ctx, i):
     build_fn, p, R, k = CASES[i]
     off, nbr = build_fn()
     g = Graph(len(off) - 1, off, nbr)
-    model, t32 = (1, 0) if p == "wic" else (0, orc.t32_const(p))
+    model, t32 = model_of(orc, p)
     full_parity(orc, ctx, g, model, t32, R, 1000 + i, min(k, g.n))
 
 
-@pytest.mark.parametrize("i", [0, 2, 3, 5, 7, 9])
+@pytest.mark.parametrize("i", [0, 2, 3, 5, 7, 9, 10])
 def test_dense_cover_path(orc, ctx, i, monkeypatch):
     """Force components of >= 8 vertices out of the member index so MarkSeed
     covers them with the dense pass over the store (the path big components
@@ -99,7 +115,7 @@ def test_dense_cover_path(orc, ctx, i, monkeypatch):
     {"PACIM_NO_WARP_BFS": "1", "PACIM_HUB_DEG": "4", "PACIM_FORCE_HLA": "1"},  # hubs via live lists
     {"PACIM_HUB_DEG": "2", "PACIM_FORCE_HLA": "1", "PACIM_CHUNK": "5"},
 ])
-@pytest.mark.parametrize("i", [0, 2, 3, 7, 8, 9])
+@pytest.mark.parametrize("i", [0, 2, 3, 7, 8, 9, 11])
 def test_traversal_paths(orc, ctx, i, env, monkeypatch):
     """The shared traversal of the cover step (row items and chunk items of
     the work queue), forced on the tiny corpus by shrinking the chunk size and
