@@ -45,6 +45,8 @@ def lib():
             "orc_t32_const": (u64, [dbl]),
             "orc_t32_wic": (u64, [u64, u64]),
             "orc_t32_uniform": (u64, [u64, u32, u32]),
+            "orc_live_decor": (i32, [u64, u32, u32, u32, u64]),
+            "orc_simulate_ic": (u64, [u32, P, P, i32, u64, P, u32, u32, u64]),
             "orc_live": (i32, [u64, u32, u32, u32, u64]),
             "orc_sketch_labels": (C.c_long, [u32, P, P, i32, u64, u64, u32, P, P]),
             "orc_greedy": (i32, [u32, P, P, i32, u64, u32, u64, u32, P, P, P, P]),
@@ -98,6 +100,10 @@ def uniform_param(lo: float, hi: float) -> int:
 
 def t32_uniform(packed: int, u: int, v: int) -> int:
     return lib().orc_t32_uniform(packed, u, v)
+
+
+def hash_r(seed: int, r: int) -> int:
+    return int(lib().orc_hash_r(seed, r))
 
 
 def live(seed: int, u: int, v: int, r: int, t32: int) -> bool:
@@ -232,3 +238,18 @@ def greedy_alg3(g: Graph, model, t32, R, seed, a32, k):
     if rc != 0:
         raise RuntimeError(rc)
     return seeds, gain, sigma, visits.value
+
+
+# ----------------------------------------------------------- NEXT f3
+DECOR = 1 << 8  # model word bit: the decorrelated hash rule (R20)
+
+
+def live_decor(seed: int, u: int, v: int, r: int, t32: int) -> bool:
+    return bool(lib().orc_live_decor(seed, u, v, r, t32))
+
+
+def simulate_ic(g: Graph, model: int, t32: int, seeds, nsims: int, mc_seed: int) -> int:
+    """R21: total vertices reached from `seeds` over nsims Monte-Carlo worlds."""
+    s = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint32))
+    return int(lib().orc_simulate_ic(g.n, _p(g.off), _p(g.nbr), model, t32, _p(s), len(s), nsims,
+                                     mc_seed))

@@ -19,6 +19,10 @@
  *                          reduces to the constant; range, mean and
  *                          uniformity checked statistically (pinned)
  *   orc_live ............. symmetry, p=0/1 extremes, live fraction ~ p (pinned, statistical)
+ *   orc_live_decor ....... R20 decorrelated rule: live fraction ~ p, co-liveness of two
+ *                          sketches ~ p^2 (pinned, statistical)
+ *   orc_simulate_ic ...... R21 Monte-Carlo sigma(S): p = 0 / 1 closed forms, exact sigma by
+ *                          world enumeration within 5 standard errors (pinned)
  *   orc_sketch_labels .... scipy connected_components on the materialised
  *                          sampled graph; p=0 / p=1 special cases (pinned)
  *   orc_greedy ........... brute-force set-union greedy on tiny inputs, closed
@@ -118,11 +122,30 @@ int orc_live(uint64_t hash_seed, uint32_t u, uint32_t v, uint32_t r, uint64_t t3
     return h < (t32 << 32);
 }
 
-/* Probability model of an edge of the CSR graph: 0 = constant T32, 1 = WIC,
- * 2 = Uniform U(lo, hi) (R19; t32 = H << 32 | L). */
+/* R20 (NEXT f3): the decorrelated rule, an option beside the literal P:3-4:
+ *     live'(u,v,r) <=> hi32(mix64(hash(r) xor hash(min<<32|max))) < T32
+ * (the literal rule only compares leading bits, so sketches whose
+ * hash(r) share those bits sample nearly the same edges). */
+int orc_live_decor(uint64_t hash_seed, uint32_t u, uint32_t v, uint32_t r, uint64_t t32)
+{
+    if (t32 >= (1ull << 32)) return 1;
+    return (orc_mix64(orc_hash_edge(hash_seed, u, v, r)) >> 32) < t32;
+}
+
+/* The oracle's model word: bits 0-7 the probability model (0 = constant T32,
+ * 1 = WIC, 2 = Uniform U(lo, hi), R19, t32 = H << 32 | L), bits 8-15 the hash
+ * rule (0 = literal P:3-4, 1 = decorrelated R20). */
+static int live_m(int model, uint64_t hash_seed, uint32_t u, uint32_t v, uint32_t r,
+                  uint64_t t32)
+{
+    return (model >> 8) == 1 ? orc_live_decor(hash_seed, u, v, r, t32)
+                             : orc_live(hash_seed, u, v, r, t32);
+}
+
 static uint64_t edge_t32(int model, uint64_t t32, const uint64_t *off,
                          uint32_t u, uint32_t v)
 {
+    model &= 0xFF;
     if (model == 1)
         return orc_t32_wic(off[u + 1] - off[u], off[v + 1] - off[v]);
     if (model == 2)
@@ -158,7 +181,7 @@ long orc_sketch_labels(uint32_t n, const uint64_t *off, const uint32_t *nbr,
             for (uint64_t e = off[x]; e < off[x + 1]; e++) {
                 uint32_t w = nbr[e];
                 if (label[w] != ORC_UNSET) continue;
-                if (orc_live(hash_seed, x, w, r, edge_t32(model, t32, off, x, w))) {
+                if (live_m(model, hash_seed, x, w, r, edge_t32(model, t32, off, x, w))) {
                     label[w] = v;
                     queue[tail++] = w;
                 }
@@ -187,7 +210,7 @@ static size_t bfs_component(uint32_t s, const uint64_t *off, const uint32_t *nbr
         for (uint64_t e = off[x]; e < off[x + 1]; e++) {
             uint32_t w = nbr[e];
             if (stamp[w] == tag) continue;
-            if (orc_live(hash_seed, x, w, r, edge_t32(model, t32, off, x, w))) {
+            if (live_m(model, hash_seed, x, w, r, edge_t32(model, t32, off, x, w))) {
                 stamp[w] = tag;
                 out[tail++] = w;
             }
@@ -374,7 +397,7 @@ void orc_get_center(uint32_t n, const uint64_t *off, const uint32_t *nbr,
         for (uint64_t e = off[x]; e < off[x + 1]; e++) {
             uint32_t w = nbr[e];
             if (seen[w]) continue;
-            if (orc_live(hash_seed, x, w, r, edge_t32(model, t32, off, x, w))) {
+            if (live_m(model, hash_seed, x, w, r, edge_t32(model, t32, off, x, w))) {
                 seen[w] = 1;
                 queue[tail++] = w;
             }
@@ -588,4 +611,57 @@ void orc_csr_from_keys(uint32_t n, uint64_t m, const uint64_t *keys,
         nbr[fill[b]++] = a;
     }
     free(fill);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Monte-Carlo sigma(S) (NEXT f3; IC simulation P:375-377, the paper's        */
+/* "Influence ... 20000 simulations" column P:1335)           */
+/* ------------------------------------------------------------------------ */
+/*
+ * R21: simulation i draws a fresh world: edge e = (u,v) is live iff
+ *     hi32(mix64(mix64(K_mc xor i) xor (min<<32|max))) < T32(e)
+ * with K_mc = mix64(mc_seed xor 0x4D435349434D4353) (T32 = 2^32: always).
+ * Returns the total number of vertices reached from S over the nsims worlds
+ * (sigma_hat(S) = total / nsims), or UINT64_MAX on OOM.
+ */
+uint64_t orc_simulate_ic(uint32_t n, const uint64_t *off, const uint32_t *nbr, int model,
+                         uint64_t t32, const uint32_t *seeds, uint32_t ns, uint32_t nsims,
+                         uint64_t mc_seed)
+{
+    uint32_t *stamp = (uint32_t *)calloc(n ? n : 1, sizeof(uint32_t));
+    uint32_t *queue = (uint32_t *)malloc((size_t)(n ? n : 1) * sizeof(uint32_t));
+    if (!stamp || !queue) {
+        free(stamp);
+        free(queue);
+        return UINT64_MAX;
+    }
+    const uint64_t Kmc = orc_mix64(mc_seed ^ 0x4D435349434D4353ull);
+    uint64_t total = 0;
+    for (uint32_t i = 0; i < nsims; i++) {
+        const uint32_t tag = i + 1;
+        const uint64_t Ki = orc_mix64(Kmc ^ (uint64_t)i);
+        size_t head = 0, tail = 0;
+        for (uint32_t k = 0; k < ns; k++)
+            if (stamp[seeds[k]] != tag) {
+                stamp[seeds[k]] = tag;
+                queue[tail++] = seeds[k];
+            }
+        while (head < tail) {
+            uint32_t x = queue[head++];
+            for (uint64_t e = off[x]; e < off[x + 1]; e++) {
+                uint32_t w = nbr[e];
+                if (stamp[w] == tag) continue;
+                uint64_t T = edge_t32(model, t32, off, x, w);
+                uint64_t a = x < w ? x : w, b = x < w ? w : x;
+                if (T >= (1ull << 32) || (orc_mix64(Ki ^ ((a << 32) | b)) >> 32) < T) {
+                    stamp[w] = tag;
+                    queue[tail++] = w;
+                }
+            }
+        }
+        total += tail;
+    }
+    free(stamp);
+    free(queue);
+    return total;
 }
