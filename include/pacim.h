@@ -119,6 +119,24 @@ PACIM_API const char *pacim_version(void);
  * gives 0 (R3; P:4 "hash_edge < p(u,v)"). */
 PACIM_API uint64_t pacim_threshold_from_p(double p);
 
+/* NEXT f3, R21: Monte-Carlo influence of the seed set S = seeds[0..ns) (HOST
+ * array; repeated ids count once) under the IC model of the loaded graph
+ * (its probability model): nsims independent worlds, simulation
+ * i's edge e live iff hi32(mix64(mix64(K_mc ^ i) ^ key(e))) < T32(e),
+ * K_mc = mix64(mc_seed ^ 0x4D435349434D4353).  *total (host) = the sum over
+ * the worlds of |reach_i(S)|; sigma_hat(S) = *total / nsims.  Needs a loaded
+ * graph (no sketches).  ESTATE without a graph, EINVAL for a seed >= n. */
+PACIM_API int pacim_simulate_ic(pacim_ctx *ctx, const uint32_t *seeds, uint32_t ns,
+                                uint32_t nsims, uint64_t mc_seed, uint64_t *total);
+
+/* NEXT f3, R20: the sampling rule of the sketches built after this call.
+ * rule 0 (default) = the paper's P:3-4, hash(r) xor hash(e) < p(u,v);
+ * rule 1 = decorrelated, hi32(mix64(hash(r) xor hash(e))) < T32(u,v)
+ * (independent sketches; no candidate-bucket pruning, every sketch is tested
+ * for every edge).  Drops built sketches (ESTATE for select until rebuilt);
+ * EINVAL for another rule. */
+PACIM_API int pacim_set_hash_rule(pacim_ctx *ctx, int rule);
+
 /* The Uniform model's parameter (R19): L = floor(lo 2^32), H = min(floor(hi
  * 2^32), 2^32 - 1) in IEEE double, returned packed as H << 32 | L (L <= H);
  * lo, hi are clamped to [0, 1] and swapped if lo > hi. */

@@ -22,6 +22,7 @@ EXPORTS = [
     "pacim_build_sketches", "pacim_select_seeds", "pacim_gain0_to_device",
     "pacim_select_reset", "pacim_cover_local", "pacim_cover_local_sparse",
     "pacim_apply_deltas", "pacim_apply_dense", "pacim_clear_deltas", "pacim_argmax_device",
+    "pacim_set_hash_rule", "pacim_simulate_ic",
     "pacim_get_gain0", "pacim_get_labels", "pacim_get_center_sketch",
     "pacim_get_stats",
 ]
@@ -89,6 +90,8 @@ def lib():
             "pacim_cover_local": (i32, [P, u32, P, P]),
             "pacim_cover_local_sparse": (i32, [P, u32, P, P, P, u64, P, P]),
             "pacim_apply_deltas": (i32, [P, P, P, P, u64, u32]),
+            "pacim_set_hash_rule": (i32, [P, i32]),
+            "pacim_simulate_ic": (i32, [P, P, u32, u32, u64, P]),
             "pacim_apply_dense": (i32, [P, P, P, u32, u32]),
             "pacim_clear_deltas": (i32, [P, P, P, u64]),
             "pacim_argmax_device": (i32, [P, P, u32, P, P]),
@@ -186,6 +189,18 @@ class Context:
         return off, nbr
 
     # ---------------------------------------------------------- sketches
+    def pacim_simulate_ic(self, seeds, nsims: int, mc_seed: int) -> int:
+        """Total vertices reached from `seeds` over nsims Monte-Carlo worlds (R21)."""
+        s = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint32))
+        t = C.c_uint64()
+        self._check(self._L.pacim_simulate_ic(self._h, _ptr(s), len(s), int(nsims), int(mc_seed),
+                                              C.byref(t)))
+        return t.value
+
+    def pacim_set_hash_rule(self, rule: int):
+        """0: the paper's rule; 1: decorrelated (R20)."""
+        self._check(self._L.pacim_set_hash_rule(self._h, int(rule)))
+
     def pacim_build_sketches(self, R: int, hash_seed: int, center_a32: int = 1 << 32,
                              shard_rank: int = 0, shard_world: int = 1):
         self._check(self._L.pacim_build_sketches(self._h, R, hash_seed, center_a32, shard_rank,

@@ -14,7 +14,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libpacim.so")
-SOURCES = ["api.cu", "graph.cu", "build.cu", "select.cu", "compressed.cu"]
+SOURCES = ["api.cu", "graph.cu", "build.cu", "select.cu", "compressed.cu", "mc.cu"]
 
 HEADERS = ["pacim_internal.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

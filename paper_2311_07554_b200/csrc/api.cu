@@ -79,7 +79,7 @@ static void free_all(pacim_ctx *ctx) {
 
                     &ctx->d_tab, &ctx->gain0,      &ctx->gain,     &ctx->center_of, &ctx->counters,
                     &ctx->scratch, &ctx->scratch2, &ctx->sel_seeds, &ctx->sel_gain,
-                    &ctx->sel_partial, &ctx->sel_list, &ctx->sel_flag, &ctx->argmax_part, &ctx->bfs, &ctx->tcsr, &ctx->hidx, &ctx->hla_off, &ctx->hla_row, &ctx->hla_raw, &ctx->d_smap, &ctx->pkeys, &ctx->cprobe, &ctx->cseed};
+                    &ctx->sel_partial, &ctx->sel_list, &ctx->sel_flag, &ctx->argmax_part, &ctx->bfs, &ctx->tcsr, &ctx->hidx, &ctx->hla_off, &ctx->hla_row, &ctx->hla_raw, &ctx->d_smap, &ctx->pkeys, &ctx->cprobe, &ctx->cseed, &ctx->d_hr64};
   for (DevBuf *b : bufs) pc_free(ctx, *b);
 }
 
@@ -353,6 +353,23 @@ int pacim_cover_local_sparse(pacim_ctx *ctx, uint32_t s, int64_t *d_delta, uint3
     PC_CUDA(cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, ctx->stream));
     PC_CUDA(cudaStreamSynchronize(ctx->stream));
     *count = h;
+  });
+}
+
+int pacim_simulate_ic(pacim_ctx *ctx, const uint32_t *seeds, uint32_t ns, uint32_t nsims,
+                      uint64_t mc_seed, uint64_t *total) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(ctx->has_graph, PACIM_ESTATE, "simulate before a graph is loaded");
+    PC_REQUIRE(total && (ns == 0 || seeds), PACIM_EINVAL, "bad argument");
+    pc_simulate_ic(ctx, seeds, ns, nsims, mc_seed, total);
+  });
+}
+
+int pacim_set_hash_rule(pacim_ctx *ctx, int rule) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(rule == 0 || rule == 1, PACIM_EINVAL, "hash rule must be 0 (P:3-4) or 1 (R20)");
+    if (rule != ctx->hash_rule) drop_sketches(ctx);
+    ctx->hash_rule = rule;
   });
 }
 

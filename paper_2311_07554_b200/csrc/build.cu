@@ -97,7 +97,7 @@ __device__ __forceinline__ void uf_unite(uint32_t *L, uint32_t B, uint32_t j, ui
 constexpr int EDGE_THREADS = 256;
 constexpr int EDGE_WARPS = EDGE_THREADS / 32;
 
-template <bool WIC, bool REC>
+template <bool WIC, bool REC, bool DECOR>
 __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__restrict__ keys,
                                                         const uint64_t *__restrict__ ckeys,
                                                         const uint32_t *__restrict__ tm1,
@@ -106,7 +106,8 @@ __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__res
                                                         const uint16_t *__restrict__ g_tab,
                                                         uint32_t B, uint32_t j0, uint32_t Bb,
                                                         uint32_t *L,
-                                                        unsigned long long *live_ctr, Hla hla) {
+                                                        unsigned long long *live_ctr, Hla hla,
+                                                        const uint64_t *__restrict__ hr64) {
   // slots [j0, j0 + Bb) of the B sorted slots go to L (row stride Bb)
   extern __shared__ uint32_t sm[];
   uint32_t *shr = sm;
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__res
   __shared__ uint32_t w_u[EDGE_WARPS][32], w_v[EDGE_WARPS][32], w_he[EDGE_WARPS][32];
   __shared__ uint32_t w_lo[EDGE_WARPS][32];
   __shared__ uint64_t w_T[EDGE_WARPS][32];
+  __shared__ uint64_t w_he64[DECOR ? EDGE_WARPS : 1][32];  // R20: the full hash(e)
   for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) shr[i] = g_shr[i];
   for (uint32_t i = threadIdx.x; i <= (1u << PACIM_TB); i += blockDim.x) tab[i] = g_tab[i];
   __syncthreads();
@@ -125,13 +127,17 @@ __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__res
     // ---- one edge per lane: hash and candidate slot range
     const size_t e = base + lane;
     uint32_t cnt = 0, eu = 0, ev = 0, ehe = 0, elo = 0;
-    uint64_t eT = 0;
+    uint64_t eT = 0, ehe64 = 0;
     if (e < m) {
       const uint64_t key = keys[e];
       const uint64_t T = WIC ? (uint64_t)tm1[e] + t32 : t32;  // per-edge: t32 = toff
-      const uint32_t he = (uint32_t)(pc_mix64(key ^ K) >> 32);
+      const uint64_t he64 = pc_mix64(key ^ K);
+      const uint32_t he = (uint32_t)(he64 >> 32);
       uint32_t lo = 0, hi = 0;
-      if (T != 0) {
+      if (DECOR) {  // R20: no leading-bit structure, every slot is a candidate
+        if (T != 0) hi = B;
+        ehe64 = he64;
+      } else if (T != 0) {
         const uint32_t w = __clz((uint32_t)(T - 1));
         if (w >= PACIM_TB) {
           uint32_t p = he >> (32 - PACIM_TB);
@@ -172,6 +178,7 @@ __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__res
       w_u[wid][k] = eu;
       w_v[wid][k] = ev;
       w_he[wid][k] = ehe;
+      if (DECOR) w_he64[DECOR ? wid : 0][k] = ehe64;
       if (WIC) w_T[wid][k] = eT;
       w_lo[wid][k] = elo - pre;  // slot of candidate position idx: w_lo + idx
     }
@@ -190,7 +197,11 @@ __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__res
         const uint32_t a = before + __popc(smask & (0xffffffffu >> (31 - lane))) - 1;
         j = w_lo[wid][a] + idx;
         const uint64_t T = WIC ? w_T[wid][a] : t32;
-        lv = (uint64_t)(shr[j] ^ w_he[wid][a]) < T;
+        if (DECOR)  // R20
+          lv = T >= (1ull << 32) ||
+               (pc_mix64(__ldg(hr64 + j) ^ w_he64[DECOR ? wid : 0][a]) >> 32) < T;
+        else
+          lv = (uint64_t)(shr[j] ^ w_he[wid][a]) < T;
         u = w_u[wid][a];
         v = w_v[wid][a];
         if (lv) {
@@ -594,16 +605,22 @@ void pc_slot_table(pacim_ctx *ctx) {
   const uint32_t B = ctx->R_local;
   ctx->slot_r.clear();
   ctx->r_slot.assign(ctx->R, -1);
-  std::vector<std::pair<uint32_t, uint32_t>> hs;
+  std::vector<std::pair<uint64_t, uint32_t>> hs;
   for (uint32_t r = ctx->rank; r < ctx->R; r += ctx->world) {
     uint64_t h = pc_mix64(((1ull << 63) | (uint64_t)r) ^ ctx->K);
-    hs.push_back({(uint32_t)(h >> 32), r});
+    hs.push_back({h, r});
   }
-  std::sort(hs.begin(), hs.end());
+  std::sort(hs.begin(), hs.end(),
+            [](const std::pair<uint64_t, uint32_t> &a, const std::pair<uint64_t, uint32_t> &b) {
+              return (a.first >> 32) != (b.first >> 32) ? (a.first >> 32) < (b.first >> 32)
+                                                        : a.second < b.second;
+            });
   ctx->shr.resize(B);
+  ctx->hr64.resize(B);
   ctx->slot_r.resize(B);
   for (uint32_t j = 0; j < B; j++) {
-    ctx->shr[j] = hs[j].first;
+    ctx->shr[j] = (uint32_t)(hs[j].first >> 32);
+    ctx->hr64[j] = hs[j].first;
     ctx->slot_r[j] = hs[j].second;
     ctx->r_slot[hs[j].second] = (int32_t)j;
   }
@@ -619,6 +636,9 @@ void pc_slot_table(pacim_ctx *ctx) {
   PC_CUDA(cudaMemcpyAsync(ctx->d_shr.p, ctx->shr.data(), B * 4, cudaMemcpyHostToDevice,
                           ctx->stream));
   PC_CUDA(cudaMemcpyAsync(ctx->d_tab.p, ctx->tab.data(), (NT + 1) * 2, cudaMemcpyHostToDevice,
+                          ctx->stream));
+  pc_ensure(ctx, ctx->d_hr64, B * sizeof(uint64_t));
+  PC_CUDA(cudaMemcpyAsync(ctx->d_hr64.p, ctx->hr64.data(), B * 8, cudaMemcpyHostToDevice,
                           ctx->stream));
 }
 
@@ -657,17 +677,21 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
     size_t smem = B * sizeof(uint32_t) + (NT + 1) * sizeof(uint16_t);
     unsigned g = pc_grid(ctx, (es.m + 31) / 32 * 32, EDGE_THREADS, 8);
     if (ctx->pmodel != PACIM_P_CONST) {  // per-edge thresholds (WIC, Uniform)
-      auto kern = hla.cnt ? k_edges<true, true> : k_edges<true, false>;
+      auto kern = ctx->hash_rule ? (hla.cnt ? k_edges<true, true, true> : k_edges<true, false, true>)
+                                 : (hla.cnt ? k_edges<true, true, false> : k_edges<true, false, false>);
       PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
           es.keys, es.ckeys, ctx->tm1.as<uint32_t>(), es.m,
-          ctx->K, ctx->toff(), ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla);
+          ctx->K, ctx->toff(), ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla,
+          ctx->d_hr64.as<uint64_t>());
     } else {
-      auto kern = hla.cnt ? k_edges<false, true> : k_edges<false, false>;
+      auto kern = ctx->hash_rule ? (hla.cnt ? k_edges<false, true, true> : k_edges<false, false, true>)
+                                 : (hla.cnt ? k_edges<false, true, false> : k_edges<false, false, false>);
       PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
           es.keys, es.ckeys, nullptr, es.m, ctx->K, ctx->t32,
-          ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla);
+          ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla,
+          ctx->d_hr64.as<uint64_t>());
     }
     PC_CHECK_LAUNCH();
   }
@@ -703,7 +727,8 @@ static uint32_t plan_windows(pacim_ctx *ctx) {
   // the single window [0, B)
   uint64_t budget = 0;
   if (const char *e = getenv("PACIM_L2_BUDGET")) budget = (uint64_t)atoll(e);
-  if (ctx->pmodel != PACIM_P_CONST || ctx->t32 < 2 || ctx->t32 >= (1ull << 32) || nr == 0 ||
+  if (ctx->pmodel != PACIM_P_CONST || ctx->hash_rule != 0 || ctx->t32 < 2 ||
+      ctx->t32 >= (1ull << 32) || nr == 0 ||
       budget == 0 || ctx->compressed)
     return 0;
   const uint32_t w = __builtin_clz((uint32_t)(ctx->t32 - 1));

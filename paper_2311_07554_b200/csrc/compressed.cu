@@ -137,6 +137,8 @@ struct ProbeParams {
   uint64_t K, t32;
   int wic;
   int unif;                 // R19: T32 from the edge key (t32 = H << 32 | L)
+  int decor;                // R20: live <=> hi32(mix64(hash(r) ^ hash(e))) < T32
+  const uint64_t *hr64;     // hash(r) per slot
   const uint32_t *shr;      // hi32(hash(r)) per slot
   uint32_t B;
   const uint32_t *center_of;
@@ -155,9 +157,10 @@ struct ProbeParams {
 };
 
 __device__ __forceinline__ bool live_edge(const ProbeParams &P, uint32_t x, uint32_t w,
-                                          uint32_t hr) {
+                                          uint32_t hr, uint64_t hrj) {
   const uint64_t a = x < w ? x : w, b = x < w ? w : x;
-  const uint32_t he = (uint32_t)(pc_mix64(((a << 32) | b) ^ P.K) >> 32);
+  const uint64_t he64 = pc_mix64(((a << 32) | b) ^ P.K);
+  const uint32_t he = (uint32_t)(he64 >> 32);
   uint64_t T = P.t32;
   if (P.wic) {  // R4
     const uint64_t s = (P.off[x + 1] - P.off[x]) + (P.off[w + 1] - P.off[w]);
@@ -166,6 +169,7 @@ __device__ __forceinline__ bool live_edge(const ProbeParams &P, uint32_t x, uint
   } else if (P.unif) {  // R19
     T = pc_t32_uniform(P.t32, (a << 32) | b);
   }
+  if (P.decor) return T >= (1ull << 32) || (pc_mix64(hrj ^ he64) >> 32) < T;  // R20
   return (uint64_t)(hr ^ he) < T;  // R3
 }
 
@@ -179,7 +183,8 @@ __global__ void k_seed_live(ProbeParams P, uint32_t s, uint32_t *slive, uint32_t
        e += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t w = P.nbr[e];
     const uint64_t a = s < w ? s : w, b = s < w ? w : s;
-    const uint32_t he = (uint32_t)(pc_mix64(((a << 32) | b) ^ P.K) >> 32);
+    const uint64_t he64 = pc_mix64(((a << 32) | b) ^ P.K);
+    const uint32_t he = (uint32_t)(he64 >> 32);
     uint64_t T = P.t32;
     if (P.wic) {
       const uint64_t sd = (e1 - e0) + (P.off[w + 1] - P.off[w]);
@@ -191,7 +196,10 @@ __global__ void k_seed_live(ProbeParams P, uint32_t s, uint32_t *slive, uint32_t
     if (T == 0) continue;
     const uint32_t wb = __clz((uint32_t)(T - 1));
     uint32_t lo, hi;
-    if (wb >= PACIM_TB) {
+    if (P.decor) {  // R20: every slot is a candidate
+      lo = 0;
+      hi = P.B;
+    } else if (wb >= PACIM_TB) {
       const uint32_t p = he >> (32 - PACIM_TB);
       lo = P.tab[p];
       hi = P.tab[p + 1];
@@ -204,7 +212,9 @@ __global__ void k_seed_live(ProbeParams P, uint32_t s, uint32_t *slive, uint32_t
       hi = P.tab[p + (1u << (PACIM_TB - wb))];
     }
     for (uint32_t j = lo; j < hi; j++) {
-      if ((uint64_t)(P.shr[j] ^ he) >= T) continue;
+      if (P.decor ? (T < (1ull << 32) && (pc_mix64(P.hr64[j] ^ he64) >> 32) >= T)
+                  : (uint64_t)(P.shr[j] ^ he) >= T)
+        continue;
       const uint32_t at = atomicAdd(scnt + j, 1u);
       if (at < QCAP - 1) slive[(size_t)j * QCAP + at] = w;
     }
@@ -220,6 +230,7 @@ __global__ void __launch_bounds__(PROBE_WARPS * 32) k_probe(ProbeParams P, uint3
   unsigned long long mysum = 0, nbig = 0, visits = 0, cvis = 0, nfound = 0;
   for (uint32_t j = blockIdx.x * PROBE_WARPS + w; j < P.B; j += gridDim.x * PROBE_WARPS) {
     const uint32_t hr = P.shr[j];
+    const uint64_t hrj = P.decor ? P.hr64[j] : 0;
     for (uint32_t i = lane; i < HCAP; i += 32) hs[w][i] = NONE;
     __syncwarp();
     if (lane == 0) {
@@ -280,7 +291,7 @@ __global__ void __launch_bounds__(PROBE_WARPS * 32) k_probe(ProbeParams P, uint3
         // inserting once the queue is full, so probing always terminates
         if (e < e1 && tail[w] < QCAP) {
           const uint32_t v = P.nbr[e];
-          if (live_edge(P, x, v, hr)) {
+          if (live_edge(P, x, v, hr, hrj)) {
             uint32_t h = (v * 2654435761u) & (HCAP - 1);
             for (;;) {
               const uint32_t old = atomicCAS(&hs[w][h], NONE, v);
@@ -584,6 +595,8 @@ void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *l
   P.t32 = ctx->t32;
   P.wic = ctx->pmodel == PACIM_P_WIC;
   P.unif = ctx->pmodel == PACIM_P_UNIFORM;
+  P.decor = ctx->hash_rule;
+  P.hr64 = ctx->d_hr64.as<uint64_t>();
   P.shr = ctx->d_shr.as<uint32_t>();
   P.B = B;
   P.center_of = ctx->center_of.as<uint32_t>();

@@ -156,7 +156,9 @@ struct pacim_ctx {
   std::vector<int32_t> r_slot;    // sketch id r -> slot j or -1
   std::vector<uint32_t> shr;      // hr32 of slot j (sorted ascending)
   std::vector<uint16_t> tab;      // bucket table, (1<<PACIM_TB)+1 entries
-  DevBuf d_shr, d_tab;
+  std::vector<uint64_t> hr64;     // full hash(r) of slot j (R20 decorrelated rule)
+  DevBuf d_shr, d_tab, d_hr64;
+  int hash_rule = 0;              // 0: P:3-4 literal, 1: decorrelated (R20)
   DevBuf d_hot;        // u32[2*B]: per slot the hub's root and its component id
   uint32_t hub = 0;    // a maximum-degree vertex (most likely in the giant CC)
 
@@ -300,6 +302,9 @@ void pc_cover_local(pacim_ctx *ctx, uint32_t s, int64_t *d_delta,
                     int64_t *local_gain);
 void pc_argmax(pacim_ctx *ctx, const int64_t *d_gain, uint32_t n, uint32_t *s,
                int64_t *g);
+// mc.cu (NEXT f3)
+void pc_simulate_ic(pacim_ctx *ctx, const uint32_t *seeds_host, uint32_t ns, uint32_t nsims,
+                    uint64_t mc_seed, uint64_t *total_out);
 void pc_apply_deltas(pacim_ctx *ctx, int64_t *d_gain, const uint32_t *v, const int64_t *d,
                      uint64_t count, uint32_t s);
 void pc_apply_dense(pacim_ctx *ctx, int64_t *d_gain, int64_t *d_delta, uint32_t n, uint32_t s);

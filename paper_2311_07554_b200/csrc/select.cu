@@ -149,6 +149,8 @@ struct Sel {
   int wic;                // per-edge thresholds (WIC or Uniform)
   uint32_t toff;
   const uint32_t *g_shr;   // hi32(hash(r)) of slot j (sorted)
+  const uint64_t *hr64;    // hash(r) of slot j (R20 decorrelated rule)
+  int decor;               // R20: live <=> hi32(mix64(hash(r) ^ hash(e))) < T32
   const uint16_t *g_tab;   // candidate bucket table of the sorted slots
   // store
   uint32_t *L;
@@ -312,6 +314,7 @@ __device__ bool warp_bfs(const Sel &S, uint32_t s, uint32_t j, uint32_t delta, u
                          uint32_t *hs, uint32_t *tail, const uint32_t *shr) {
   const int lane = threadIdx.x & 31;
   const uint32_t hr = shr[j];
+  const uint64_t hrj = S.decor ? __ldg(S.hr64 + j) : 0;
   for (uint32_t i = lane; i < HCAP; i += 32) hs[i] = NONE;
   __syncwarp();
   if (lane == 0) {
@@ -357,9 +360,14 @@ __device__ bool warp_bfs(const Sel &S, uint32_t s, uint32_t j, uint32_t delta, u
         const uint64_t e = ea + (t - pra);
         const uint32_t w = S.nbr[e];
         const uint64_t lo = xa < w ? xa : w, hi = xa < w ? w : xa;
-        const uint32_t he = (uint32_t)(pc_mix64(((lo << 32) | hi) ^ S.K) >> 32);
+        const uint64_t he64 = pc_mix64(((lo << 32) | hi) ^ S.K);
+        const uint32_t he = (uint32_t)(he64 >> 32);
         const uint64_t T = S.wic ? (uint64_t)S.tcsr[e] + S.toff : S.t32;  // R4 / R19
-        if ((uint64_t)(hr ^ he) >= T) continue;                        // R3
+        if (S.decor) {  // R20
+          if (T < (1ull << 32) && (pc_mix64(hrj ^ he64) >> 32) >= T) continue;
+        } else if ((uint64_t)(hr ^ he) >= T) {
+          continue;  // R3
+        }
         uint32_t h = (w * 2654435761u) & (HCAP - 1);
         for (;;) {
           const uint32_t old = atomicCAS(hs + h, NONE, w);
@@ -398,10 +406,14 @@ __device__ __forceinline__ void expand_edge(const Sel &S, uint32_t x, uint32_t w
                                             const LStack *ls) {
   const uint64_t a = x < w ? x : w, b = x < w ? w : x;
   if (T == 0) return;
-  const uint32_t he = (uint32_t)(pc_mix64(((a << 32) | b) ^ S.K) >> 32);
+  const uint64_t he64 = pc_mix64(((a << 32) | b) ^ S.K);
+  const uint32_t he = (uint32_t)(he64 >> 32);
   const uint32_t wb = __clz((uint32_t)(T - 1));
   uint32_t lo, hi;
-  if (wb >= PACIM_TB) {
+  if (S.decor) {  // R20: every slot is a candidate
+    lo = 0;
+    hi = S.B;
+  } else if (wb >= PACIM_TB) {
     const uint32_t p = he >> (32 - PACIM_TB);
     lo = tab[p];
     hi = tab[p + 1];
@@ -416,7 +428,7 @@ __device__ __forceinline__ void expand_edge(const Sel &S, uint32_t x, uint32_t w
   if (lo >= hi) return;
   // every candidate is live when T is the full bucket width 2^(32 - wb) and
   // the table resolves all wb bits
-  const bool all_live = wb <= PACIM_TB && T == (1ull << (32 - wb));
+  const bool all_live = S.decor ? T >= (1ull << 32) : (wb <= PACIM_TB && T == (1ull << (32 - wb)));
   uint32_t wr = NONE;
   const uint32_t w0 = lo >> 5, w1 = (hi - 1) >> 5;
   for (uint32_t wd = w0; wd <= w1; wd++) {
@@ -430,7 +442,10 @@ __device__ __forceinline__ void expand_edge(const Sel &S, uint32_t x, uint32_t w
       live = 0;
       for (uint32_t t = bits; t; t &= t - 1) {
         const uint32_t bit = __ffs(t) - 1;
-        if ((uint64_t)(shr[wd * 32 + bit] ^ he) < T) live |= 1u << bit;
+        const uint32_t j = wd * 32 + bit;
+        const bool lv = S.decor ? (pc_mix64(__ldg(S.hr64 + j) ^ he64) >> 32) < T
+                                : (uint64_t)(shr[j] ^ he) < T;
+        if (lv) live |= 1u << bit;
       }
       if (!live) continue;
     }
@@ -1067,6 +1082,8 @@ static Sel make_sel(pacim_ctx *ctx, long long *target) {
   S.wic = ctx->pmodel != PACIM_P_CONST;  // per-edge thresholds in tcsr
   S.toff = ctx->toff();
   S.g_shr = ctx->d_shr.as<uint32_t>();
+  S.hr64 = ctx->d_hr64.as<uint64_t>();
+  S.decor = ctx->hash_rule;
   S.g_tab = ctx->d_tab.as<uint16_t>();
   S.L = ctx->L.as<uint32_t>();
   S.smap = ctx->d_smap.as<uint32_t>();

@@ -132,3 +132,28 @@ def test_c5_shape_scale16(orc, ctx):
     model, t32 = orc.model_args(cfg)
     es, egn, esg, _ = orc.greedy(g, model, t32, cfg["R"], cfg["hash_seed"], cfg["k"])
     assert list(s) == list(es) and list(gn) == list(egn) and list(sg) == list(esg)
+
+
+@pytest.mark.parametrize("i", [1, 4, 10])
+def test_compressed_decorrelated_rule(orc, ctx, i):
+    """Compressed store + Get-center under the decorrelated rule (R20): the
+    greedy equals the oracle's memoised greedy with the same rule."""
+    from oracle.oracle import Graph
+    build_fn, p, R, k, a32 = CASES[i]
+    off, nbr = build_fn()
+    g = Graph(len(off) - 1, off, nbr)
+    if p == "wic":
+        model, t32 = 1, 0
+    elif isinstance(p, tuple):
+        model, t32 = 2, orc.uniform_param(p[1], p[2])
+    else:
+        model, t32 = 0, orc.t32_const(p)
+    ctx.pacim_set_hash_rule(1)
+    try:
+        ctx.pacim_load_graph(g.off, g.nbr, model, t32, 2)
+        ctx.pacim_build_sketches(R, 900 + i, a32)
+        s, gn, sg, _ = ctx.pacim_select_seeds(k)
+        es, egn, esg, _ = orc.greedy(g, model | orc.DECOR, t32, R, 900 + i, k)
+        assert list(s) == list(es) and list(gn) == list(egn) and list(sg) == list(esg)
+    finally:
+        ctx.pacim_set_hash_rule(0)

@@ -138,6 +138,32 @@ def test_window_layout(orc, ctx, i, budget, monkeypatch):
     test_tiny_corpus_parity(orc, ctx, i)
 
 
+@pytest.mark.parametrize("i", [0, 2, 3, 5, 7, 8, 10])
+def test_decorrelated_rule(orc, ctx, i):
+    """NEXT f3, R20: sketches sampled with live <=> hi32(mix64(hash(r) ^
+    hash(e))) < T32 (every sketch a candidate for every edge): labels, gain0
+    and the greedy equal the oracle's with the same rule."""
+    from oracle.oracle import Graph
+    build_fn, p, R, k = CASES[i]
+    off, nbr = build_fn()
+    g = Graph(len(off) - 1, off, nbr)
+    model, t32 = model_of(orc, p)
+    ctx.pacim_set_hash_rule(1)
+    try:
+        load_host(ctx, g, model, t32)
+        ctx.pacim_build_sketches(R, 2000 + i)
+        s, gn, sg, _ = ctx.pacim_select_seeds(min(k, g.n))
+        es, egn, esg, eg0 = orc.greedy(g, model | orc.DECOR, t32, R, 2000 + i, min(k, g.n),
+                                       want_gain0=True)
+        assert np.array_equal(ctx.pacim_get_gain0(), eg0)
+        for r in range(0, R, max(1, R // 8)):
+            lab, _ = orc.sketch_labels(g, model | orc.DECOR, t32, 2000 + i, r)
+            assert np.array_equal(ctx.pacim_get_labels(r), lab), r
+        assert list(s) == list(es) and list(gn) == list(egn) and list(sg) == list(esg)
+    finally:
+        ctx.pacim_set_hash_rule(0)
+
+
 def test_edge_cases(orc, ctx, pc):
     from oracle.oracle import Graph
     # single vertex, no edges, k = n = 1
@@ -311,3 +337,20 @@ def test_rank_emulation_matches_single(orc, pc, big_t, chunk, monkeypatch):
             assert list(sig) == list(esg)
         for c in ctxs:
             c.close()
+
+
+# ------------------------------------------------ Monte-Carlo sigma (f3)
+@pytest.mark.parametrize("i,nsims", [(0, 300), (3, 600), (8, 257), (10, 64), (11, 513), (6, 100)])
+def test_simulate_ic_equals_oracle(orc, ctx, i, nsims):
+    """R21: the GPU's multi-simulation BFS reaches exactly the oracle's total
+    over the same counter-based worlds (const, WIC and Uniform models; batch
+    tails of 1..31 simulations; repeated seed ids)."""
+    from oracle.oracle import Graph
+    build_fn, p, R, k = CASES[i]
+    off, nbr = build_fn()
+    g = Graph(len(off) - 1, off, nbr)
+    model, t32 = model_of(orc, p)
+    load_host(ctx, g, model, t32)
+    seeds = [0, min(5, g.n - 1), g.n // 2, 0]
+    got = ctx.pacim_simulate_ic(seeds, nsims, 31 + i)
+    assert got == orc.simulate_ic(g, model, t32, sorted(set(seeds)), nsims, 31 + i)
