@@ -94,6 +94,8 @@ typedef struct {
     uint64_t select_center_found;   /* compressed: probes that met a center */
     uint32_t batch_slots;           /* compressed: sketches per build batch (parent arrays
                                        rows x batch_slots u32 of scratch) */
+    uint64_t select_evaluations;    /* lazy selector: fresh marginal-gain evaluations */
+    uint64_t select_eval_rounds;    /* lazy selector: prefix-doubling batches */
 } pacim_stats;
 
 /* --------------------------------------------------------------- lifecycle */
@@ -128,6 +130,14 @@ PACIM_API uint64_t pacim_threshold_from_p(double p);
  * graph (no sketches).  ESTATE without a graph, EINVAL for a seed >= n. */
 PACIM_API int pacim_simulate_ic(pacim_ctx *ctx, const uint32_t *seeds, uint32_t ns,
                                 uint32_t nsims, uint64_t mc_seed, uint64_t *total);
+
+/* NEXT f2: the selector of pacim_select_seeds on an uncompressed store.
+ * 0 (default) = incremental (member gains updated when a CC is covered);
+ * 1 = lazy / CELF-style (stale upper bounds, fresh evaluations of prefixes of
+ * 1, 2, 4, ... candidates in (stale desc, id asc) order, P:536-578 and
+ * P:2381-2401), which counts evaluations (stats.select_evaluations).  Both
+ * return the same sequence (R17).  EINVAL for another value. */
+PACIM_API int pacim_set_selector(pacim_ctx *ctx, int selector);
 
 /* NEXT f3, R20: the sampling rule of the sketches built after this call.
  * rule 0 (default) = the paper's P:3-4, hash(r) xor hash(e) < p(u,v);

@@ -22,7 +22,7 @@ EXPORTS = [
     "pacim_build_sketches", "pacim_select_seeds", "pacim_gain0_to_device",
     "pacim_select_reset", "pacim_cover_local", "pacim_cover_local_sparse",
     "pacim_apply_deltas", "pacim_apply_dense", "pacim_clear_deltas", "pacim_argmax_device",
-    "pacim_set_hash_rule", "pacim_simulate_ic",
+    "pacim_set_hash_rule", "pacim_simulate_ic", "pacim_set_selector",
     "pacim_get_gain0", "pacim_get_labels", "pacim_get_center_sketch",
     "pacim_get_stats",
 ]
@@ -50,6 +50,7 @@ class Stats(C.Structure):
         ("select_chunk_items", C.c_uint64), ("select_inline_rows", C.c_uint64),
         ("select_edges", C.c_uint64), ("select_center_visits", C.c_uint64),
         ("select_center_found", C.c_uint64), ("batch_slots", C.c_uint32),
+        ("select_evaluations", C.c_uint64), ("select_eval_rounds", C.c_uint64),
     ]
 
     def asdict(self):
@@ -92,6 +93,7 @@ def lib():
             "pacim_apply_deltas": (i32, [P, P, P, P, u64, u32]),
             "pacim_set_hash_rule": (i32, [P, i32]),
             "pacim_simulate_ic": (i32, [P, P, u32, u32, u64, P]),
+            "pacim_set_selector": (i32, [P, i32]),
             "pacim_apply_dense": (i32, [P, P, P, u32, u32]),
             "pacim_clear_deltas": (i32, [P, P, P, u64]),
             "pacim_argmax_device": (i32, [P, P, u32, P, P]),
@@ -196,6 +198,10 @@ class Context:
         self._check(self._L.pacim_simulate_ic(self._h, _ptr(s), len(s), int(nsims), int(mc_seed),
                                               C.byref(t)))
         return t.value
+
+    def pacim_set_selector(self, selector: int):
+        """0: incremental (default); 1: lazy / CELF with evaluation counts (NEXT f2)."""
+        self._check(self._L.pacim_set_selector(self._h, int(selector)))
 
     def pacim_set_hash_rule(self, rule: int):
         """0: the paper's rule; 1: decorrelated (R20)."""

@@ -283,7 +283,10 @@ int pacim_select_seeds(pacim_ctx *ctx, uint32_t k, uint32_t *seeds_out, int64_t 
     if (ctx->compressed)
       pc_select_compressed(ctx, k, seeds_out, gain_num_out, sigma_num_out);
     else
-      pc_select(ctx, k, seeds_out, gain_num_out, sigma_num_out);
+      if (ctx->selector == 1)
+        pc_select_lazy(ctx, k, seeds_out, gain_num_out, sigma_num_out);
+      else
+        pc_select(ctx, k, seeds_out, gain_num_out, sigma_num_out);
     if (sigma_out)
       for (uint32_t i = 0; i < k; i++) sigma_out[i] = (double)sigma_num_out[i] / (double)ctx->R;
   });
@@ -362,6 +365,13 @@ int pacim_simulate_ic(pacim_ctx *ctx, const uint32_t *seeds, uint32_t ns, uint32
     PC_REQUIRE(ctx->has_graph, PACIM_ESTATE, "simulate before a graph is loaded");
     PC_REQUIRE(total && (ns == 0 || seeds), PACIM_EINVAL, "bad argument");
     pc_simulate_ic(ctx, seeds, ns, nsims, mc_seed, total);
+  });
+}
+
+int pacim_set_selector(pacim_ctx *ctx, int selector) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(selector == 0 || selector == 1, PACIM_EINVAL, "selector must be 0 or 1");
+    ctx->selector = selector;
   });
 }
 

@@ -159,6 +159,7 @@ struct pacim_ctx {
   std::vector<uint64_t> hr64;     // full hash(r) of slot j (R20 decorrelated rule)
   DevBuf d_shr, d_tab, d_hr64;
   int hash_rule = 0;              // 0: P:3-4 literal, 1: decorrelated (R20)
+  int selector = 0;               // 0: incremental, 1: lazy (NEXT f2)
   DevBuf d_hot;        // u32[2*B]: per slot the hub's root and its component id
   uint32_t hub = 0;    // a maximum-degree vertex (most likely in the giant CC)
 
@@ -298,6 +299,8 @@ void pc_get_center_sketch(pacim_ctx *ctx, uint32_t slot, uint32_t *label, uint32
 void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
                int64_t *sigma_num);
 void pc_select_reset(pacim_ctx *ctx);
+void pc_select_lazy(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
+                    int64_t *sigma_num);
 void pc_cover_local(pacim_ctx *ctx, uint32_t s, int64_t *d_delta,
                     int64_t *local_gain);
 void pc_argmax(pacim_ctx *ctx, const int64_t *d_gain, uint32_t n, uint32_t *s,

@@ -27,6 +27,7 @@
 // covered root slots is kept).  gain_num[i] = sum_j delta_j; the host checks
 // it against the argmax gain.
 #include <cooperative_groups.h>
+#include <cub/cub.cuh>
 
 #include <algorithm>
 #include <cstdio>
@@ -1053,6 +1054,86 @@ __global__ void k_clear_deltas(long long *delta, const uint32_t *v, unsigned lon
 }
 __global__ void k_set_gain(long long *gain, uint32_t s, long long x) { gain[s] = x; }
 
+// ---------------------------------------------------------- NEXT f2
+// Lazy (CELF-style) selection (prefix doubling P:2381-2401):
+// fresh marginal gain of candidate cand[t] at the current S, one warp per
+// candidate: sum over the slots of |C_j(v)| unless C_j(v) is covered (R17).
+__global__ void k_lazy_eval(Sel S, const uint32_t *cand, uint32_t b0, uint32_t b1,
+                            long long *delta) {
+  const int lane = threadIdx.x & 31;
+  const size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t t = b0 + warp; t < b1; t += nw) {
+    const uint32_t v = cand[t];
+    if (__ldcg(delta + v) < 0) continue;  // a seed (-1, R6): never a candidate again
+    const uint32_t row = S.cid[v];
+    long long g = 0;
+    if (row == NONE) {
+      g = S.B;  // isolated: a singleton in every sketch
+    } else {
+      for (uint32_t j = lane; j < S.B; j += 32) {
+        const uint32_t sv = __ldcg(S.L + pc_addr(S.smap, S.nr, row, j));
+        uint32_t rv;
+        if (sv == row) {
+          g += 1;  // {v}: never covered while v is not a seed
+          continue;
+        }
+        rv = (sv & PACIM_HIGH) ? sv : __ldcg(S.L + pc_addr(S.smap, S.nr, sv, j));
+        if (!(rv & COV)) g += rv & SIZE;
+      }
+      for (int d = 16; d; d >>= 1) g += __shfl_xor_sync(0xffffffffu, g, d);
+    }
+    if (lane == 0) delta[v] = g;
+  }
+}
+
+// MarkSeed(s) for every slot (no member updates in the lazy selector)
+__global__ void k_lazy_mark(Sel S, uint32_t s) {
+  const uint32_t srow = S.cid[s];
+  if (srow == NONE) return;
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < S.B; j += gridDim.x * blockDim.x) {
+    const uint32_t sl = S.L[pc_addr(S.smap, S.nr, srow, j)];
+    if (sl == srow) continue;
+    const uint32_t root = (sl & PACIM_HIGH) ? srow : sl;
+    const size_t ra = pc_addr(S.smap, S.nr, root, j);
+    const uint32_t x = atomicOr(S.L + ra, COV);
+    if (!(x & COV)) {
+      const unsigned long long at = atomicAdd(S.cov_cnt, 1ull);
+      if (at < S.cov_cap) S.cov_list[at] = ra;
+    }
+  }
+}
+
+// sort keys of the candidate order (stale gain desc, id asc via a stable
+// sort of ids in ascending order); seeds (gain -1) last
+__global__ void k_lazy_keys(const long long *delta, uint32_t n, uint64_t *key, uint32_t *id) {
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (size_t)gridDim.x * blockDim.x) {
+    const long long d = delta[v];
+    key[v] = d < 0 ? ~0ull : (~0ull >> 1) - (uint64_t)d;
+    id[v] = (uint32_t)v;
+  }
+}
+
+// best (fresh gain desc, id asc) of cand[0, b) -> out (block reduction + atomics-free
+// two-level: one block per 4096 candidates, then the host combines)
+__global__ void __launch_bounds__(SEL_THREADS) k_lazy_best(const long long *delta,
+                                                           const uint32_t *cand, uint32_t b,
+                                                           Best *part) {
+  __shared__ Best sh[33];
+  Best x{LLONG_MIN, 0xFFFFFFFFu};
+  for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < b; t += gridDim.x * blockDim.x) {
+    const uint32_t v = cand[t];
+    const long long g = delta[v];
+    if (better(g, v, x.g, x.v)) {
+      x.g = g;
+      x.v = v;
+    }
+  }
+  x = block_best(x, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = x;
+}
+
 // empty ring: slot i expects ticket i
 __global__ void k_ring_init(Item *ring, unsigned long long Q) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < Q;
@@ -1437,4 +1518,103 @@ void pc_traverse_slots(pacim_ctx *ctx, uint32_t s, int64_t *target, const uint32
   PC_CUDA(cudaMemcpyAsync(&abort_flag, S.diag + DG_ABORT, 8, cudaMemcpyDeviceToHost, ctx->stream));
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
   PC_REQUIRE(!abort_flag, PACIM_ECHECK, "compressed cover: traversal watchdog expired");
+}
+
+// NEXT f2: the lazy selector.  Per step: candidates ordered by (stale gain
+// desc, id asc); fresh gains evaluated for prefixes of 1, 2, 4, ... until the
+// best fresh (g*, v*) precedes the next unevaluated candidate in that order
+// (stale >= fresh by submodularity, so nothing unevaluated can beat it, ties
+// included) — the same sequence as GeneralGreedy (R17).  Evaluations are
+// counted (the paper's metric).
+void pc_select_lazy(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
+                    int64_t *sigma_num) {
+  const uint32_t n = ctx->n;
+  if (k > ctx->sel_k_cap) {
+    if (ctx->sel_list_valid) {
+      Sel old = make_sel(ctx, nullptr);
+      uncover(ctx, old);
+    }
+    ctx->sel_k_cap = k;
+    ctx->sel_list_valid = false;
+  }
+  pc_ensure(ctx, ctx->gain, (size_t)n * 8);
+  Sel S = make_sel(ctx, ctx->gain.as<long long>());
+  cudaEvent_t e0, e1;
+  PC_CUDA(cudaEventCreate(&e0));
+  PC_CUDA(cudaEventCreate(&e1));
+  PC_CUDA(cudaEventRecord(e0, ctx->stream));
+  uncover(ctx, S);
+  long long *delta = ctx->gain.as<long long>();
+  PC_CUDA(cudaMemcpyAsync(delta, ctx->gain0.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  // sort buffers: keys x2, ids x2, partial maxima
+  TmpBuf sb(ctx);
+  const unsigned pg = std::max<unsigned>(1, std::min<unsigned>((n + 4095) / 4096, 4096));
+  const size_t off_part = ((size_t)n * 24 + 15) & ~(size_t)15;  // 16-B aligned
+  pc_ensure(ctx, sb, off_part + (size_t)pg * sizeof(Best) + 64);
+  uint64_t *k0 = sb.as<uint64_t>(), *k1 = k0 + n;
+  uint32_t *i0 = reinterpret_cast<uint32_t *>(k1 + n), *i1 = i0 + n;
+  Best *part = reinterpret_cast<Best *>(sb.as<char>() + off_part);
+  size_t tmp = 0;
+  {
+    cub::DoubleBuffer<uint64_t> dk(k0, k1);
+    cub::DoubleBuffer<uint32_t> dv(i0, i1);
+    PC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, dk, dv, (int64_t)n, 0, 64, ctx->stream));
+  }
+  TmpBuf ct(ctx);
+  pc_ensure(ctx, ct, tmp + 16);
+  std::vector<Best> hp(pg);
+  unsigned long long evals = 0, rounds = 0;
+  long long run = 0;
+  for (uint32_t step = 0; step < k; step++) {
+    k_lazy_keys<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(delta, n, k0, i0);
+    PC_CHECK_LAUNCH();
+    cub::DoubleBuffer<uint64_t> dk(k0, k1);
+    cub::DoubleBuffer<uint32_t> dv(i0, i1);
+    PC_CUDA(cub::DeviceRadixSort::SortPairs(ct.p, tmp, dk, dv, (int64_t)n, 0, 64, ctx->stream));
+    const uint32_t *cand = dv.Current();
+    uint32_t done = 0, b = 1;
+    Best best{LLONG_MIN, NONE};
+    for (;;) {
+      k_lazy_eval<<<pc_grid(ctx, (size_t)(b - done) * 32, 256, 8), 256, 0, ctx->stream>>>(
+          S, cand, done, b, delta);
+      PC_CHECK_LAUNCH();
+      evals += b - done;
+      rounds++;
+      const unsigned g = std::min<unsigned>(pg, (b + SEL_THREADS - 1) / SEL_THREADS);
+      k_lazy_best<<<g, SEL_THREADS, 0, ctx->stream>>>(delta, cand, b, part);
+      PC_CHECK_LAUNCH();
+      uint32_t nxt = NONE;
+      long long nd = LLONG_MIN;
+      if (b < n) PC_CUDA(cudaMemcpyAsync(&nxt, cand + b, 4, cudaMemcpyDeviceToHost, ctx->stream));
+      PC_CUDA(cudaMemcpyAsync(hp.data(), part, g * sizeof(Best), cudaMemcpyDeviceToHost, ctx->stream));
+      PC_CUDA(cudaStreamSynchronize(ctx->stream));
+      best = Best{LLONG_MIN, NONE};
+      for (unsigned i = 0; i < g; i++)
+        if (hp[i].g > best.g || (hp[i].g == best.g && hp[i].v < best.v)) best = hp[i];
+      if (b >= n) break;
+      PC_CUDA(cudaMemcpyAsync(&nd, delta + nxt, 8, cudaMemcpyDeviceToHost, ctx->stream));
+      PC_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (best.g > nd || (best.g == nd && best.v < nxt)) break;  // nothing unevaluated can win
+      done = b;
+      b = (uint32_t)std::min<uint64_t>(2ull * b, n);
+    }
+    seeds[step] = best.v;
+    gain_num[step] = best.g;
+    run += best.g;
+    sigma_num[step] = run;
+    k_lazy_mark<<<(S.B + 255) / 256, 256, 0, ctx->stream>>>(S, best.v);
+    PC_CHECK_LAUNCH();
+    const long long m1 = -1;  // s leaves the candidate set (R6)
+    PC_CUDA(cudaMemcpyAsync(delta + best.v, &m1, 8, cudaMemcpyHostToDevice, ctx->stream));
+  }
+  PC_CUDA(cudaEventRecord(e1, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  ctx->stats.t_select_ms = ms;
+  ctx->stats.select_evaluations = evals;
+  ctx->stats.select_eval_rounds = rounds;
+  ctx->stats.kernel_launches_select = (uint32_t)(k * 3 + rounds * 2);
 }

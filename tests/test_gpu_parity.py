@@ -354,3 +354,32 @@ def test_simulate_ic_equals_oracle(orc, ctx, i, nsims):
     seeds = [0, min(5, g.n - 1), g.n // 2, 0]
     got = ctx.pacim_simulate_ic(seeds, nsims, 31 + i)
     assert got == orc.simulate_ic(g, model, t32, sorted(set(seeds)), nsims, 31 + i)
+
+
+# ------------------------------------------------------ lazy selector (f2)
+@pytest.mark.parametrize("i", [0, 2, 3, 5, 6, 7, 9, 10])
+def test_lazy_selector_equals_oracle(orc, ctx, i):
+    """NEXT f2: the lazy selector (stale bounds, prefix-doubling evaluations)
+    returns GeneralGreedy's sequence (R17), and never evaluates fewer than k
+    candidates nor more than k * n."""
+    from oracle.oracle import Graph
+    build_fn, p, R, k = CASES[i]
+    off, nbr = build_fn()
+    g = Graph(len(off) - 1, off, nbr)
+    model, t32 = model_of(orc, p)
+    k = min(k, g.n)
+    load_host(ctx, g, model, t32)
+    ctx.pacim_build_sketches(R, 3000 + i)
+    ctx.pacim_set_selector(1)
+    try:
+        s, gn, sg, _ = ctx.pacim_select_seeds(k)
+        st = ctx.pacim_get_stats()
+        s2, gn2, _, _ = ctx.pacim_select_seeds(k)  # repeated: restarts from S = empty
+    finally:
+        ctx.pacim_set_selector(0)
+    es, egn, esg, _ = orc.greedy(g, model, t32, R, 3000 + i, k)
+    assert list(s) == list(es) and list(gn) == list(egn) and list(sg) == list(esg)
+    assert list(s2) == list(es) and list(gn2) == list(egn)
+    assert k <= st["select_evaluations"] <= k * g.n
+    s3, gn3, _, _ = ctx.pacim_select_seeds(k)  # the incremental selector on the same store
+    assert list(s3) == list(es)
