@@ -97,7 +97,12 @@ __device__ __forceinline__ void uf_unite(uint32_t *L, uint32_t B, uint32_t j, ui
 constexpr int EDGE_THREADS = 256;
 constexpr int EDGE_WARPS = EDGE_THREADS / 32;
 
-template <bool WIC, bool REC, bool DECOR>
+// LEAN: no edge list — the warp reads 32 consecutive CSR entries (chunk c),
+// their rows from the chunk table (the row of the first entry, advanced while
+// an entry lies past the row's end), and keeps the upper ones (v > u); rows
+// are the vertex ids.  `keys` = CSR offsets, `ckeys` = neighbours (as u32),
+// `tm1` = chunk rows, m = CSR entries (2m).
+template <bool WIC, bool REC, bool DECOR, bool LEAN>
 __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__restrict__ keys,
                                                         const uint64_t *__restrict__ ckeys,
                                                         const uint32_t *__restrict__ tm1,
@@ -128,9 +133,18 @@ __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__res
     const size_t e = base + lane;
     uint32_t cnt = 0, eu = 0, ev = 0, ehe = 0, elo = 0;
     uint64_t eT = 0, ehe64 = 0;
-    if (e < m) {
-      const uint64_t key = keys[e];
-      const uint64_t T = WIC ? (uint64_t)tm1[e] + t32 : t32;  // per-edge: t32 = toff
+    uint64_t lkey = 0;
+    bool upper = e < m;
+    if (LEAN && upper) {
+      uint32_t u = tm1[base >> 5];
+      while (e >= keys[u + 1]) u++;
+      const uint32_t v = reinterpret_cast<const uint32_t *>(ckeys)[e];
+      upper = v > u;
+      lkey = ((uint64_t)u << 32) | v;
+    }
+    if (upper) {
+      const uint64_t key = LEAN ? lkey : keys[e];
+      const uint64_t T = (WIC && !LEAN) ? (uint64_t)tm1[e] + t32 : t32;  // per-edge: t32 = toff
       const uint64_t he64 = pc_mix64(key ^ K);
       const uint32_t he = (uint32_t)(he64 >> 32);
       uint32_t lo = 0, hi = 0;
@@ -156,7 +170,7 @@ __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__res
       hi = min(hi, j0 + Bb);
       if (hi < lo) hi = lo;
       cnt = hi - lo;
-      const uint64_t ck = ckeys[e];  // the endpoints' store rows (+ hub flags)
+      const uint64_t ck = LEAN ? lkey : ckeys[e];  // the endpoints' store rows (+ hub flags)
       eu = (uint32_t)(ck >> 32);
       ev = (uint32_t)ck;
       ehe = he;
@@ -676,17 +690,26 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
   {
     size_t smem = B * sizeof(uint32_t) + (NT + 1) * sizeof(uint16_t);
     unsigned g = pc_grid(ctx, (es.m + 31) / 32 * 32, EDGE_THREADS, 8);
-    if (ctx->pmodel != PACIM_P_CONST) {  // per-edge thresholds (WIC, Uniform)
-      auto kern = ctx->hash_rule ? (hla.cnt ? k_edges<true, true, true> : k_edges<true, false, true>)
-                                 : (hla.cnt ? k_edges<true, true, false> : k_edges<true, false, false>);
+    if (ctx->lean) {  // no edge list: the upper edges from the CSR (c5)
+      auto kern = ctx->hash_rule ? k_edges<false, false, true, true> : k_edges<false, false, false, true>;
+      PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const uint64_t nnz = 2 * ctx->m;
+      const unsigned gl = pc_grid(ctx, (nnz + 31) / 32 * 32, EDGE_THREADS, 8);
+      kern<<<gl, EDGE_THREADS, smem, ctx->stream>>>(
+          ctx->off.as<uint64_t>(), reinterpret_cast<const uint64_t *>(ctx->nbr.p),
+          ctx->crow.as<uint32_t>(), nnz, ctx->K, ctx->t32, ctx->d_shr.as<uint32_t>(),
+          ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>());
+    } else if (ctx->pmodel != PACIM_P_CONST) {  // per-edge thresholds (WIC, Uniform)
+      auto kern = ctx->hash_rule ? (hla.cnt ? k_edges<true, true, true, false> : k_edges<true, false, true, false>)
+                                 : (hla.cnt ? k_edges<true, true, false, false> : k_edges<true, false, false, false>);
       PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
           es.keys, es.ckeys, ctx->tm1.as<uint32_t>(), es.m,
           ctx->K, ctx->toff(), ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla,
           ctx->d_hr64.as<uint64_t>());
     } else {
-      auto kern = ctx->hash_rule ? (hla.cnt ? k_edges<false, true, true> : k_edges<false, false, true>)
-                                 : (hla.cnt ? k_edges<false, true, false> : k_edges<false, false, false>);
+      auto kern = ctx->hash_rule ? (hla.cnt ? k_edges<false, true, true, false> : k_edges<false, false, true, false>)
+                                 : (hla.cnt ? k_edges<false, true, false, false> : k_edges<false, false, false, false>);
       PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
           es.keys, es.ckeys, nullptr, es.m, ctx->K, ctx->t32,
@@ -727,7 +750,7 @@ static uint32_t plan_windows(pacim_ctx *ctx) {
   // the single window [0, B)
   uint64_t budget = 0;
   if (const char *e = getenv("PACIM_L2_BUDGET")) budget = (uint64_t)atoll(e);
-  if (ctx->pmodel != PACIM_P_CONST || ctx->hash_rule != 0 || ctx->t32 < 2 ||
+  if (ctx->pmodel != PACIM_P_CONST || ctx->hash_rule != 0 || ctx->lean || ctx->t32 < 2 ||
       ctx->t32 >= (1ull << 32) || nr == 0 ||
       budget == 0 || ctx->compressed)
     return 0;

@@ -309,10 +309,16 @@ __global__ void k_hub_index(const uint64_t *off, const uint32_t *rmap, uint32_t 
 // Everything derived from (off, nbr, keys): hub vertex, the store's row map
 // (isolated vertices are singletons in every sketch and get no row; rows keep
 // the vertex order, so min row = min id), compact edge endpoints, WIC T32.
+static void derive_lean(pacim_ctx *ctx);
+
 static void derive_common(pacim_ctx *ctx) {
   const uint32_t n = ctx->n;
   const uint64_t m = ctx->m;
   uint64_t *off = ctx->off.as<uint64_t>();
+  if (ctx->lean) {
+    derive_lean(ctx);
+    return;
+  }
   {
     pc_ensure(ctx, ctx->counters, 64 * 8);
     unsigned long long *t = ctx->counters.as<unsigned long long>();
@@ -395,6 +401,60 @@ static void derive_common(pacim_ctx *ctx) {
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+// Lean graphs (c5 at full scale): no upper edge list and no
+// row compaction — the store rows are the vertex ids (isolated vertices are
+// singleton rows), k_edges reads the upper edges straight from the CSR
+// through the chunk -> row table `crow`.  Constant probabilities only.
+namespace {
+__global__ void k_crow(const uint64_t *off, uint32_t n, uint32_t *crow);
+__global__ void k_iota_u32(uint32_t *a, uint32_t n);
+}  // namespace
+
+static void derive_lean(pacim_ctx *ctx) {
+  const uint32_t n = ctx->n;
+  uint64_t *off = ctx->off.as<uint64_t>();
+  PC_REQUIRE(ctx->pmodel == PACIM_P_CONST, PACIM_ENOTIMPL,
+             "lean graphs (no edge list) support the constant probability model only");
+  pc_ensure(ctx, ctx->counters, 64 * 8);
+  {  // hub: a maximum-degree vertex
+    unsigned long long *t = ctx->counters.as<unsigned long long>();
+    PC_CUDA(cudaMemsetAsync(t, 0, 8, ctx->stream));
+    k_max_deg<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(off, n, t);
+    PC_CHECK_LAUNCH();
+    unsigned long long h = 0;
+    PC_CUDA(cudaMemcpyAsync(&h, t, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->hub = (uint32_t)(0xFFFFFFFFull - (h & 0xFFFFFFFFull));
+    if (ctx->hub >= n) ctx->hub = 0;
+  }
+  ctx->nr = n;
+  ctx->hub_row = ctx->hub;
+  pc_ensure(ctx, ctx->cid, (size_t)n * 4);
+  pc_ensure(ctx, ctx->rmap, (size_t)n * 4);
+  k_iota_u32<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(ctx->cid.as<uint32_t>(), n);
+  k_iota_u32<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(ctx->rmap.as<uint32_t>(), n);
+  PC_CHECK_LAUNCH();
+  const uint64_t nch = (2 * ctx->m + 31) / 32;
+  pc_ensure(ctx, ctx->crow, (nch + 1) * 4);
+  k_crow<<<pc_grid(ctx, (size_t)n * 32, 256), 256, 0, ctx->stream>>>(off, n, ctx->crow.as<uint32_t>());
+  PC_CHECK_LAUNCH();
+  pc_free(ctx, ctx->keys);
+  pc_free(ctx, ctx->ckeys);
+  pc_free(ctx, ctx->hidx);
+  ctx->nhub = 0;
+  ctx->launches += 4;
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+// lean when asked (PACIM_LEAN=1) or when the edge lists (keys + ckeys, 16 B
+// per upper edge) would take more than a third of the device
+static bool want_lean(pacim_ctx *ctx) {
+  if (const char *e = getenv("PACIM_LEAN")) return atoi(e) != 0;
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  return ctx->pmodel == PACIM_P_CONST && 16 * ctx->m > tot / 3;
+}
+
 void pc_graph_finish_load(pacim_ctx *ctx, int validate) {
   const uint32_t n = ctx->n;
   uint64_t *off = ctx->off.as<uint64_t>();
@@ -418,6 +478,11 @@ void pc_graph_finish_load(pacim_ctx *ctx, int validate) {
                            (validate >= 2 ? " (range/order/loop/duplicate/asymmetry)"
                                           : " (range/order/loop/duplicate)")};
     }
+  }
+  ctx->lean = want_lean(ctx);
+  if (ctx->lean) {
+    derive_common(ctx);
+    return;
   }
   // upper edge list (sorted keys): counts -> scan -> fill
   pc_ensure(ctx, ctx->scratch, 2 * ((size_t)n + 1) * sizeof(uint64_t));
@@ -463,6 +528,93 @@ __device__ __forceinline__ uint64_t rmat_perm(uint64_t x, int s) {
 
 // R-MAT sample i: per level l, y = mix64(Kg ^ (i*64+l)) >> 11 picks the
 // quadrant against 53-bit thresholds; level l sets bit scale-1-l.
+// Bucketed R-MAT (the same samples as k_gen_rmat): the directed pairs
+// (src << 32 | dst) of every non-loop sample in both orientations whose
+// source lies in bucket b (top `bbits` of the scale-bit id), appended at a
+// warp-aggregated cursor (order irrelevant: the bucket is sorted next).
+// count_only: just count them.
+__global__ void k_gen_rmat_bucket(uint64_t Kg, int scale, uint64_t ns, uint64_t ta, uint64_t tab,
+                                  uint64_t tabc, int permute, int bbits, uint32_t b,
+                                  unsigned long long *cursor, uint64_t *out, int count_only) {
+  const int lane = threadIdx.x & 31;
+  for (size_t base = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(size_t)31; base < ns;
+       base += (size_t)gridDim.x * blockDim.x) {
+    const uint64_t i = base + lane;
+    uint64_t u = 0, v = 0;
+    bool ok = i < ns;
+    if (ok) {
+      for (int l = 0; l < scale; l++) {
+        uint64_t y = pc_mix64(Kg ^ (i * 64 + (uint64_t)l)) >> 11;
+        uint64_t bit = 1ull << (scale - 1 - l);
+        if (y < ta) {
+        } else if (y < tab) {
+          v |= bit;
+        } else if (y < tabc) {
+          u |= bit;
+        } else {
+          u |= bit;
+          v |= bit;
+        }
+      }
+      if (permute) {
+        u = rmat_perm(u, scale);
+        v = rmat_perm(v, scale);
+      }
+      ok = u != v;
+    }
+    const bool eu = ok && (uint32_t)(u >> (scale - bbits)) == b;
+    const bool ev = ok && (uint32_t)(v >> (scale - bbits)) == b;
+    const uint32_t mine = (eu ? 1u : 0u) + (ev ? 1u : 0u);
+    uint32_t pre = mine;
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, pre, d);
+      if (lane >= d) pre += y;
+    }
+    const uint32_t tot = __shfl_sync(0xffffffffu, pre, 31);
+    if (!tot) continue;
+    unsigned long long at = 0;
+    if (lane == 31) at = atomicAdd(cursor, (unsigned long long)tot);
+    at = __shfl_sync(0xffffffffu, at, 31) + (pre - mine);
+    if (!count_only) {
+      if (eu) out[at++] = (u << 32) | v;
+      if (ev) out[at] = (v << 32) | u;
+    }
+  }
+}
+
+// degrees of the bucket's sources from its sorted distinct pairs
+__global__ void k_bucket_deg(const uint64_t *p, uint64_t N, uint64_t lo, uint64_t *deg) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+       i += (size_t)gridDim.x * blockDim.x)
+    atomicAdd((unsigned long long *)(deg + ((p[i] >> 32) - lo)), 1ull);
+}
+__global__ void k_bucket_nbr(const uint64_t *p, uint64_t N, uint32_t *nbr) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+       i += (size_t)gridDim.x * blockDim.x)
+    nbr[i] = (uint32_t)p[i];
+}
+__global__ void k_add_u64(uint64_t *a, uint64_t N, uint64_t x) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+       i += (size_t)gridDim.x * blockDim.x)
+    a[i] += x;
+}
+
+// lean graphs: the row of the first CSR entry of every 32-entry chunk
+__global__ void k_crow(const uint64_t *off, uint32_t n, uint32_t *crow) {
+  const int lane = threadIdx.x & 31;
+  const size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t u = warp; u < n; u += nw) {
+    const uint64_t c0 = (off[u] + 31) / 32, c1 = (off[u + 1] + 31) / 32;
+    for (uint64_t c = c0 + lane; c < c1; c += 32) crow[c] = (uint32_t)u;
+  }
+}
+__global__ void k_iota_u32(uint32_t *a, uint32_t n) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    a[i] = (uint32_t)i;
+}
+
 __global__ void k_gen_rmat(uint64_t Kg, int scale, uint64_t i0, uint64_t cnt, uint64_t ta,
                            uint64_t tab, uint64_t tabc, int permute, uint64_t *key) {
   for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt;
@@ -671,6 +823,74 @@ static void csr_from_keys(pacim_ctx *ctx) {
   pc_free(ctx, d);
 }
 
+// R-MAT generated one source-id bucket at a time (sizes beyond one sort, c5):
+// per bucket every sample is drawn again, the pairs whose source is in the
+// bucket kept (both orientations: the symmetric CSR directly), sorted,
+// deduplicated and appended.  Same edge set as the all-at-once path.
+static void gen_rmat_bucketed(pacim_ctx *ctx, uint64_t Kg, int scale, uint64_t ns,
+                              const uint64_t *params, int bbits) {
+  const uint32_t n = ctx->n, NB = 1u << bbits;
+  const uint64_t per = (uint64_t)n / NB;  // sources per bucket
+  TmpBuf cur(ctx);
+  pc_ensure(ctx, cur, 64);
+  unsigned long long *cursor = cur.as<unsigned long long>();
+  const unsigned g = pc_grid(ctx, ns, 256, 16);
+  // pass 0: directed pairs per bucket (capacity of nbr and the bucket buffers)
+  std::vector<unsigned long long> cnt(NB);
+  for (uint32_t b = 0; b < NB; b++) {
+    PC_CUDA(cudaMemsetAsync(cursor, 0, 8, ctx->stream));
+    k_gen_rmat_bucket<<<g, 256, 0, ctx->stream>>>(Kg, scale, ns, params[2], params[3], params[4],
+                                                  (int)params[5], bbits, b, cursor, nullptr, 1);
+    PC_CHECK_LAUNCH();
+    PC_CUDA(cudaMemcpyAsync(&cnt[b], cursor, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
+  unsigned long long tot = 0, mx = 0;
+  for (auto c : cnt) {
+    tot += c;
+    mx = std::max(mx, c);
+  }
+  pc_free(ctx, ctx->keys);
+  pc_free(ctx, ctx->ckeys);
+  pc_ensure(ctx, ctx->off, ((size_t)n + 1) * 8);
+  pc_ensure(ctx, ctx->nbr, std::max<size_t>(tot, 1) * 4);
+  TmpBuf pa(ctx), pb(ctx), deg(ctx);
+  pc_ensure(ctx, pa, std::max<size_t>(mx, 1) * 8);
+  pc_ensure(ctx, pb, std::max<size_t>(mx, 1) * 8);
+  pc_ensure(ctx, deg, (per + 1) * 8);
+  uint64_t *off = ctx->off.as<uint64_t>();
+  uint64_t base = 0;
+  for (uint32_t b = 0; b < NB; b++) {
+    PC_CUDA(cudaMemsetAsync(cursor, 0, 8, ctx->stream));
+    k_gen_rmat_bucket<<<g, 256, 0, ctx->stream>>>(Kg, scale, ns, params[2], params[3], params[4],
+                                                  (int)params[5], bbits, b, cursor, pa.as<uint64_t>(),
+                                                  0);
+    PC_CHECK_LAUNCH();
+    uint64_t *sk = nullptr;
+    sort_keys(ctx, pa.as<uint64_t>(), pb.as<uint64_t>(), cnt[b], 64, &sk);
+    uint64_t *other = sk == pa.as<uint64_t>() ? pb.as<uint64_t>() : pa.as<uint64_t>();
+    const uint64_t u = cnt[b] ? unique_sorted(ctx, sk, nullptr, cnt[b], other, nullptr) : 0;
+    // rows [b * per, (b + 1) * per): degrees -> offsets (+ base), neighbours
+    PC_CUDA(cudaMemsetAsync(deg.p, 0, (per + 1) * 8, ctx->stream));
+    if (u) {
+      k_bucket_deg<<<pc_grid(ctx, u, 256), 256, 0, ctx->stream>>>(other, u, (uint64_t)b * per,
+                                                                  deg.as<uint64_t>());
+      PC_CHECK_LAUNCH();
+      k_bucket_nbr<<<pc_grid(ctx, u, 256), 256, 0, ctx->stream>>>(other, u,
+                                                                  ctx->nbr.as<uint32_t>() + base);
+      PC_CHECK_LAUNCH();
+    }
+    pc_exclusive_scan_u64(ctx, deg.as<uint64_t>(), off + (size_t)b * per, per);
+    k_add_u64<<<pc_grid(ctx, per, 256), 256, 0, ctx->stream>>>(off + (size_t)b * per, per, base);
+    PC_CHECK_LAUNCH();
+    base += u;
+  }
+  PC_CUDA(cudaMemcpyAsync(off + n, &base, 8, cudaMemcpyHostToDevice, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->m = base / 2;
+  ctx->launches += 5 * NB;
+}
+
 void pc_generate(pacim_ctx *ctx, int kind, const uint64_t *params, int nparams,
                  uint64_t gen_seed) {
   uint64_t Kg = pc_mix64(gen_seed ^ 0xD1B54A32D192ED03ull);
@@ -720,6 +940,26 @@ void pc_generate(pacim_ctx *ctx, int kind, const uint64_t *params, int nparams,
     PC_REQUIRE(ef >= 1 && ef <= 64, PACIM_EINVAL, "RMAT: ef must be in [1, 64]");
     ctx->n = 1u << scale;
     uint64_t ns = ef << scale;
+    // all samples sorted at once needs ~32 B per sample; else source buckets
+    int bbits = 0;
+    if (const char *e = getenv("PACIM_GEN_BUCKETS")) {
+      while ((1 << bbits) < atoi(e) && bbits < scale) bbits++;
+    } else {
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      if (32 * ns > fr / 3)  // a bucket holds ~2 ns / NB pairs at 32 B each in flight
+        while (bbits < scale && ((64 * ns) >> bbits) > fr / 3) bbits++;
+    }
+    if (bbits > 0) {
+      gen_rmat_bucketed(ctx, Kg, scale, ns, params, bbits);
+      ctx->lean = want_lean(ctx);
+      if (!ctx->lean) {  // the upper edge list from the CSR, as for a loaded graph
+        pc_graph_finish_load(ctx, 0);
+        return;
+      }
+      derive_common(ctx);
+      return;
+    }
     TmpBuf a(ctx), b(ctx);
     pc_ensure(ctx, a, ns * 8);
     pc_ensure(ctx, b, ns * 8);
@@ -766,5 +1006,7 @@ void pc_generate(pacim_ctx *ctx, int kind, const uint64_t *params, int nparams,
     throw PacimError{PACIM_EINVAL, "unknown generator kind"};
   }
   csr_from_keys(ctx);
+  ctx->lean = getenv("PACIM_LEAN") && atoi(getenv("PACIM_LEAN")) != 0 &&
+              ctx->pmodel == PACIM_P_CONST;  // tests force the lean path on small graphs
   derive_common(ctx);
 }

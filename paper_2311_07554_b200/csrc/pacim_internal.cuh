@@ -132,6 +132,8 @@ struct pacim_ctx {
   DevBuf cid;            // u32[n]   store row of v, or 0xFFFFFFFF for isolated v
   DevBuf rmap;           // u32[nr]  vertex id of store row c
   uint32_t nr = 0;       // store rows = non-isolated vertices (order kept)
+  bool lean = false;     // no keys / ckeys: rows = vertex ids, k_edges reads the CSR (c5)
+  DevBuf crow;           // lean: u32 row of the first CSR entry of each 32-entry chunk
   uint32_t hub_row = 0xFFFFFFFFu;  // store row of the hub vertex
 
   // hub rows (degree > hub_deg): index per row and the live hub adjacency of

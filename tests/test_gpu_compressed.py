@@ -157,3 +157,18 @@ def test_compressed_decorrelated_rule(orc, ctx, i):
         assert list(s) == list(es) and list(gn) == list(egn) and list(sg) == list(esg)
     finally:
         ctx.pacim_set_hash_rule(0)
+
+
+def test_c5_shape_scale16_lean_bucketed(orc, ctx, monkeypatch):
+    """The c5 path at full scale — bucketed generator, lean graph, compressed
+    store — at scale 16: the oracle's greedy."""
+    monkeypatch.setenv("PACIM_GEN_BUCKETS", "8")
+    monkeypatch.setenv("PACIM_LEAN", "1")
+    test_c5_shape_scale16(orc, ctx)
+    assert ctx.pacim_get_stats()["rows"] == 1 << 16
+
+
+@pytest.mark.parametrize("i", [0, 1, 3, 9])
+def test_compressed_lean(orc, ctx, i, monkeypatch):
+    monkeypatch.setenv("PACIM_LEAN", "1")
+    run_case(orc, ctx, i, check_sketches=True)

@@ -223,6 +223,29 @@ def test_generator_matches_oracle(orc, ctx, name, over):
     assert np.array_equal(nbr, g.nbr)
 
 
+@pytest.mark.parametrize("name,over,buckets", [
+    ("c2", {"scale": 14, "ef": 16}, "4"),
+    ("c4", {"scale": 13, "ef": 24}, "8"),
+    ("c5", {"scale": 13, "ef": 32}, "2"),
+    ("c5", {"scale": 15, "ef": 32}, "16"),
+])
+def test_bucketed_generator_matches_oracle(orc, ctx, name, over, buckets, monkeypatch):
+    """The source-bucketed R-MAT generator (the one that builds c5 at full
+    scale) gives the oracle's CSR bit for bit."""
+    monkeypatch.setenv("PACIM_GEN_BUCKETS", buckets)
+    test_generator_matches_oracle(orc, ctx, name, over)
+
+
+@pytest.mark.parametrize("i", [0, 1, 2, 5, 6, 7, 8, 9])
+def test_lean_graph(orc, ctx, i, monkeypatch):
+    """Lean graphs (no edge list, rows = vertex ids, k_edges over the CSR):
+    labels, gain0 and the greedy equal the oracle's (constant p)."""
+    monkeypatch.setenv("PACIM_LEAN", "1")
+    test_tiny_corpus_parity(orc, ctx, i)
+    st = ctx.pacim_get_stats()
+    assert st["rows"] == st["n"]
+
+
 def test_c1_full(orc, ctx):
     """BASELINE.json configs[0] end to end: generated on the GPU, all 64
     sketches' labels, gain0, seeds, gains, sigma vs the oracle."""
