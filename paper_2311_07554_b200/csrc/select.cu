@@ -1212,8 +1212,11 @@ static Sel make_sel(pacim_ctx *ctx, long long *target) {
   // items of 4 words).  Outstanding row items <= rows (one per row at a
   // time); chunk items are queued only while fewer than Q/2 items are
   // outstanding, so Q >= 2 (rows + 2^18) never blocks a producer for good.
+  // capped at 2^28 items (4 GB): outstanding rows are the rows reached but
+  // not yet expanded, far below `rows` in practice (c5: 268M rows); a full
+  // ring would stall producers until the watchdog reports it (ECHECK)
   uint64_t qcap = 1024;
-  while (qcap < 2ull * ((uint64_t)nr + (1ull << 18))) qcap <<= 1;
+  while (qcap < 2ull * ((uint64_t)nr + (1ull << 18)) && qcap < (1ull << 28)) qcap <<= 1;
   const size_t bw = (size_t)nr * S.BW;
   const size_t head = 2 * QC_WORDS + 2 * DG_WORDS + 4;
   const size_t words = head + 2 * bw + 4 * (size_t)nr + 4 * qcap + 4;
