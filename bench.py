@@ -155,7 +155,7 @@ def oracle_sample(cfg, seconds_target=15.0, max_sketches=None, g=None):
         O.sketch_labels(g, model, t32, cfg["hash_seed"], S)
         t += time.perf_counter() - t0
         S += 1
-    return S * g.m / t, S, t, g
+    return (S * g.m / t if t > 0 else 0.0), S, t, g
 
 
 def run_reference(args, cfg):
@@ -166,7 +166,7 @@ def run_reference(args, cfg):
     g = O.gen_config(cfg)
     per_step = max(1, args.ref_sketches)
     for _ in range(args.warmup):
-        oracle_sample(cfg, 0.0, per_step, g)
+        oracle_sample(cfg, 1e9, per_step, g)  # bounded by per_step sketches
     t = 0.0
     for _ in range(args.steps):
         _, S, dt, _ = oracle_sample(cfg, 1e9, per_step, g)
