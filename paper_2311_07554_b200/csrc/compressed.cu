@@ -644,7 +644,9 @@ void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *l
     std::vector<uint32_t> tdl(B, 0);
     // giant CCs stay with the batch rebuild + dense pass (a queue traversal of
     // a giant is slower)
-    const uint64_t big_t = std::max<uint64_t>(65536, nr / 8);
+    // measured: a queue traversal of c5's giant CCs took 3.4 s, the batch
+    // rebuild + dense pass a few hundred ms
+    const uint64_t big_t = 65536;
     for (uint32_t j = 0; j < B; j++) {
       if (hst[j] == ST_BIG_KNOWN && hdl[j] <= big_t) {
         tdl[j] = hdl[j];
