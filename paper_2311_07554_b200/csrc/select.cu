@@ -156,6 +156,7 @@ struct Sel {
   // store
   uint32_t *L;
   const uint32_t *smap;    // slot -> f << 16 | c of its store window (pc_addr)
+  int onew;                // one window [0, B): address row * B + j
   uint32_t nr, B, BW, nv;  // rows, slots, mask words per row, vertices
   const uint32_t *cid, *rmap;
   // per step
@@ -273,10 +274,10 @@ __device__ __forceinline__ uint32_t cover_slot(const Sel &S, uint32_t srow, uint
   S.dl[j] = 0;
   S.cov_root[j] = NONE;
   if (srow == NONE) return delta;  // isolated seed: singleton in every sketch
-  const uint32_t sl = S.L[pc_addr(S.smap, S.nr, srow, j)];
+  const uint32_t sl = S.L[S.onew ? (size_t)srow * S.B + j : pc_addr(S.smap, S.nr, srow, j)];
   if (sl == srow) return delta;    // singleton {s}
   const uint32_t root = (sl & PACIM_HIGH) ? srow : sl;
-  const size_t ra = pc_addr(S.smap, S.nr, root, j);
+  const size_t ra = S.onew ? (size_t)root * S.B + j : pc_addr(S.smap, S.nr, root, j);
   uint32_t *rs = S.L + ra;
   const uint32_t x = atomicOr(rs, COV);  // covered from now on
   if (x & COV) return 0;                 // covered by an earlier seed
@@ -773,13 +774,23 @@ __device__ void apply_dense(const Sel &S, uint32_t s, size_t warp0, size_t nwarp
     if (!__any_sync(0xffffffffu, any)) continue;
     for (size_t v0 = warp0 * DR; v0 < S.nr; v0 += nwarps * DR) {
       uint32_t x[DR][8];
+      if (S.onew) {  // one window (the default): the plain vertex-major address
 #pragma unroll
-      for (int r = 0; r < DR; r++)
+        for (int r = 0; r < DR; r++)
 #pragma unroll
-        for (int i = 0; i < 8; i++)
-          x[r][i] = (cr[i] != NONE && v0 + r < S.nr)
-                        ? __ldcs(S.L + pc_addr(S.smap, S.nr, (uint32_t)(v0 + r), j0 + lane + 32 * i))
-                        : NONE;
+          for (int i = 0; i < 8; i++)
+            x[r][i] = (cr[i] != NONE && v0 + r < S.nr)
+                          ? __ldcs(S.L + (v0 + r) * S.B + j0 + lane + 32 * i)
+                          : NONE;
+      } else {
+#pragma unroll
+        for (int r = 0; r < DR; r++)
+#pragma unroll
+          for (int i = 0; i < 8; i++)
+            x[r][i] = (cr[i] != NONE && v0 + r < S.nr)
+                          ? __ldcs(S.L + pc_addr(S.smap, S.nr, (uint32_t)(v0 + r), j0 + lane + 32 * i))
+                          : NONE;
+      }
 #pragma unroll
       for (int r = 0; r < DR; r++) {
         const uint32_t v = (uint32_t)(v0 + r);
@@ -1092,10 +1103,10 @@ __global__ void k_lazy_mark(Sel S, uint32_t s) {
   const uint32_t srow = S.cid[s];
   if (srow == NONE) return;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < S.B; j += gridDim.x * blockDim.x) {
-    const uint32_t sl = S.L[pc_addr(S.smap, S.nr, srow, j)];
+    const uint32_t sl = S.L[S.onew ? (size_t)srow * S.B + j : pc_addr(S.smap, S.nr, srow, j)];
     if (sl == srow) continue;
     const uint32_t root = (sl & PACIM_HIGH) ? srow : sl;
-    const size_t ra = pc_addr(S.smap, S.nr, root, j);
+    const size_t ra = S.onew ? (size_t)root * S.B + j : pc_addr(S.smap, S.nr, root, j);
     const uint32_t x = atomicOr(S.L + ra, COV);
     if (!(x & COV)) {
       const unsigned long long at = atomicAdd(S.cov_cnt, 1ull);
@@ -1168,6 +1179,7 @@ static Sel make_sel(pacim_ctx *ctx, long long *target) {
   S.g_tab = ctx->d_tab.as<uint16_t>();
   S.L = ctx->L.as<uint32_t>();
   S.smap = ctx->d_smap.as<uint32_t>();
+  S.onew = ctx->win_first.size() <= 2;
   S.nr = nr;
   S.B = B;
   S.BW = (B + 31) / 32;
