@@ -432,22 +432,39 @@ __global__ void k_big_apply(const uint32_t *Lb, uint32_t nr, uint32_t Bb, uint32
                             const uint32_t *st, const uint32_t *dl, const uint32_t *sroot,
                             const uint32_t *rmap, uint32_t s, long long *target,
                             DeltaList dlst) {
+  // one warp per 4 rows; lanes over the batch's slots, the slots' status,
+  // delta and root loaded once (Bb <= 32 per lane pass), rows in flight together
+  constexpr int AR = 4;
   const int lane = threadIdx.x & 31;
   size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
-  for (size_t v = warp; v < nr; v += nw) {
-    long long d = 0;
-    for (uint32_t jj = lane; jj < Bb; jj += 32) {
-      const uint32_t stt = st[j0 + jj];
-      if (stt == ST_DONE || dl[j0 + jj] == 0) continue;
-      if (root_of(Lb, Bb, (uint32_t)v, jj) == sroot[jj]) d += dl[j0 + jj];
-    }
-    for (int q = 16; q; q >>= 1) d += __shfl_xor_sync(0xffffffffu, d, q);
-    if (lane == 0 && d) {
-      const uint32_t vid = rmap[v];
-      if (vid != s) {
-        atomicAdd((unsigned long long *)&target[vid], (unsigned long long)(-d));
-        dlst.add(vid, -d);
+  for (uint32_t jb = 0; jb < Bb; jb += 32) {
+    const uint32_t jj = jb + lane;
+    const bool act = jj < Bb && st[j0 + jj] != ST_DONE && dl[j0 + jj] != 0;
+    if (!__any_sync(0xffffffffu, act)) continue;
+    const uint32_t d_j = act ? dl[j0 + jj] : 0, r_j = act ? sroot[jj] : NONE;
+    for (size_t v0 = warp * AR; v0 < nr; v0 += nw * AR) {
+      uint32_t sv[AR];
+#pragma unroll
+      for (int r = 0; r < AR; r++)
+        sv[r] = (act && v0 + r < nr) ? __ldcs(Lb + (v0 + r) * Bb + jj) : NONE;
+#pragma unroll
+      for (int r = 0; r < AR; r++) {
+        const uint32_t v = (uint32_t)(v0 + r);
+        long long d = 0;
+        if (sv[r] != NONE) {
+          const uint32_t root = (sv[r] == v || (sv[r] & PACIM_HIGH)) ? v : sv[r];
+          if (root == r_j) d = d_j;
+        }
+        if (!__any_sync(0xffffffffu, d != 0)) continue;
+        for (int q = 16; q; q >>= 1) d += __shfl_xor_sync(0xffffffffu, d, q);
+        if (lane == 0) {
+          const uint32_t vid = rmap[v];
+          if (vid != s) {
+            atomicAdd((unsigned long long *)&target[vid], (unsigned long long)(-d));
+            dlst.add(vid, -d);
+          }
+        }
       }
     }
   }

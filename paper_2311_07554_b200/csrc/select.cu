@@ -123,7 +123,7 @@ enum { QC_TAIL = 0, QC_HEAD = 16, QC_DONE = 32, QC_PROD = 48, QC_WORDS = 80 };
 // row items, chunk items, chunks expanded inline (queue guard)
 enum { DG_STEPS = 0, DG_DENSE, DG_WARP, DG_DEFER, DG_ROWS, DG_CHUNKS, DG_INLINE, DG_ABORT,
        DG_EDGES, DG_WORDS = 10 };
-constexpr unsigned long long WATCHDOG_NS = 4000000000ull;  // a wait this long is a bug: abort
+constexpr unsigned long long WATCHDOG_NS = 20000000000ull;  // a 20 s wait is a bug: abort
 
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
