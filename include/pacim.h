@@ -96,6 +96,9 @@ typedef struct {
                                        rows x batch_slots u32 of scratch) */
     uint64_t select_evaluations;    /* lazy selector: fresh marginal-gain evaluations */
     uint64_t select_eval_rounds;    /* lazy selector: prefix-doubling batches */
+    uint64_t hla_entries;           /* live hub adjacency of the last build: (hub, sketch,
+                                       neighbour) entries, 0 if not recorded */
+    uint32_t hubs;                  /* rows of degree > the hub degree (PACIM_HUB_DEG) */
 } pacim_stats;
 
 /* --------------------------------------------------------------- lifecycle */

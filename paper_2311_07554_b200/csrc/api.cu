@@ -79,7 +79,7 @@ static void free_all(pacim_ctx *ctx) {
 
                     &ctx->d_tab, &ctx->gain0,      &ctx->gain,     &ctx->center_of, &ctx->counters,
                     &ctx->scratch, &ctx->scratch2, &ctx->sel_seeds, &ctx->sel_gain,
-                    &ctx->sel_partial, &ctx->sel_list, &ctx->sel_flag, &ctx->argmax_part, &ctx->bfs, &ctx->tcsr, &ctx->hidx, &ctx->hla_off, &ctx->hla_row, &ctx->hla_raw, &ctx->d_smap, &ctx->pkeys, &ctx->cprobe, &ctx->cseed, &ctx->d_hr64, &ctx->crow};
+                    &ctx->sel_partial, &ctx->sel_list, &ctx->sel_flag, &ctx->argmax_part, &ctx->bfs, &ctx->tcsr, &ctx->hidx, &ctx->hub_tab, &ctx->hla_off, &ctx->hla_row, &ctx->hla_raw, &ctx->d_smap, &ctx->pkeys, &ctx->cprobe, &ctx->cseed, &ctx->d_hr64, &ctx->crow};
   for (DevBuf *b : bufs) pc_free(ctx, *b);
 }
 
@@ -460,6 +460,8 @@ int pacim_get_stats(pacim_ctx *ctx, pacim_stats *out) {
     s.nmember = ctx->nmember;
     s.rows = ctx->nr;
     s.batch_slots = ctx->compressed ? ctx->Bb : 0;
+    s.hla_entries = ctx->hla_ok ? ctx->hla_n : 0;
+    s.hubs = ctx->nhub;
     s.nnonsingle = ctx->nnonsingle;
     s.device_bytes = ctx->device_bytes;
     *out = s;

@@ -25,6 +25,8 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cub/cub.cuh>
+
 #include "pacim_internal.cuh"
 
 namespace {
@@ -121,6 +123,8 @@ __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__res
   __shared__ uint32_t w_lo[EDGE_WARPS][32];
   __shared__ uint64_t w_T[EDGE_WARPS][32];
   __shared__ uint64_t w_he64[DECOR ? EDGE_WARPS : 1][32];  // R20: the full hash(e)
+  __shared__ unsigned long long w_hla[REC ? EDGE_WARPS : 1][REC ? Hla::HLA_WBUF : 1];
+  uint32_t hla_n = 0;  // entries staged in w_hla[wid] (warp-uniform)
   for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) shr[i] = g_shr[i];
   for (uint32_t i = threadIdx.x; i <= (1u << PACIM_TB); i += blockDim.x) tab[i] = g_tab[i];
   __syncthreads();
@@ -218,17 +222,19 @@ __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__res
           lv = (uint64_t)(shr[j] ^ w_he[wid][a]) < T;
         u = w_u[wid][a];
         v = w_v[wid][a];
-        if (lv) {
-          uf_unite(L, Bb, j - j0, u & ~PACIM_HUBF, v & ~PACIM_HUBF);
-          live++;
-        }
       }
-      if (REC)  // live edges of hubs, appended with one counter update per warp
-        hla.add_warp(u & ~PACIM_HUBF, v & ~PACIM_HUBF, j, (lv && (u & PACIM_HUBF)) ? 1u : 0u,
-                     (lv && (v & PACIM_HUBF)) ? 1u : 0u);
+      if (REC)  // live edges of hubs, staged per warp (before the union: u, v, j
+                // need not survive it)
+        hla.stage(u & ~PACIM_HUBF, v & ~PACIM_HUBF, j, (lv && (u & PACIM_HUBF)) ? 1u : 0u,
+                  (lv && (v & PACIM_HUBF)) ? 1u : 0u, w_hla[REC ? wid : 0], hla_n);
+      if (lv) {
+        uf_unite(L, Bb, j - j0, u & ~PACIM_HUBF, v & ~PACIM_HUBF);
+        live++;
+      }
     }
     __syncwarp();
   }
+  if (REC) hla.flush(w_hla[REC ? wid : 0], hla_n);
   // block-aggregated counter
   for (int d = 16; d; d >>= 1) live += __shfl_xor_sync(0xffffffffu, live, d);
   __shared__ unsigned long long bsum;
@@ -391,13 +397,17 @@ __global__ void __launch_bounds__(256) k_gain0(const uint32_t *__restrict__ L, u
   }
 }
 
-// HLA: raw entries -> rows grouped by (hub, slot); cur = a copy of the offsets
-__global__ void k_hla_scatter(const unsigned long long *raw, unsigned long long n,
-                              unsigned long long *cur, uint32_t *rows) {
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+// HLA: entries sorted by key -> rows, and the segment offsets: off[q] = the
+// first entry of key >= q (off[nkeys] = n), each boundary filling the gap of
+// keys without entries
+__global__ void k_hla_offsets(const unsigned long long *sorted, unsigned long long n,
+                              unsigned long long nkeys, unsigned long long *off, uint32_t *rows) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n;
        i += (size_t)gridDim.x * blockDim.x) {
-    const unsigned long long r = raw[i];
-    rows[atomicAdd(cur + (r >> 32), 1ull)] = (uint32_t)r;
+    const unsigned long long kc = i < n ? sorted[i] >> 32 : nkeys;
+    const long long kp = i > 0 ? (long long)(sorted[i - 1] >> 32) : -1;
+    for (long long q = kp + 1; q <= (long long)kc; q++) off[q] = i;
+    if (i < n) rows[i] = (uint32_t)sorted[i];
   }
 }
 
@@ -657,6 +667,71 @@ void pc_slot_table(pacim_ctx *ctx) {
 }
 
 // One sketch pass over the edge list for slots [j0, j0+Bb): parent arrays in
+// ---------------------------------------------------------------- HLA
+bool pc_hla_begin(pacim_ctx *ctx, Hla *hla, double max_per_edge) {
+  ctx->hla_ok = false;
+  if (ctx->nhub == 0 || ctx->lean) return false;
+  const uint32_t B = ctx->R_local;
+  // expected live (hub, slot, neighbour) entries: every CSR entry of a hub is
+  // live in a slot with its edge probability — p (constant), the mean of
+  // U(lo, hi) (R19); WIC (R4): sum over a hub's entries of 2/(d_u + d_w) <= 2
+  double E;
+  if (ctx->pmodel == PACIM_P_WIC) {
+    E = 2.0 * ctx->nhub * B;
+  } else {
+    double p = (double)ctx->t32 / 4294967296.0;
+    if (ctx->pmodel == PACIM_P_UNIFORM)
+      p = 0.5 * ((double)(ctx->t32 >> 32) + (double)(ctx->t32 & 0xFFFFFFFFull)) / 4294967296.0;
+    E = std::min(p, 1.0) * (double)ctx->hub_entries * B;
+  }
+  if (E > max_per_edge * (double)ctx->m) return false;  // recording would cost more than it saves
+  const unsigned long long cap = (unsigned long long)(1.25 * E) + (1ull << 20);
+  const size_t keys = (size_t)ctx->nhub * B + 1;
+  if (keys >= (1ull << 32)) return false;  // key field of an entry is 32 bits
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  // raw + the sort's second buffer (8 B each), grouped rows (4 B), offsets
+  if ((cap + 1) * 20 + keys * 8 + (64ull << 20) > fr / 4) return false;
+  pc_ensure(ctx, ctx->hla_raw, (cap + 1) * 8);
+  PC_CUDA(cudaMemsetAsync(ctx->hla_raw.p, 0, 8, ctx->stream));
+  hla->tab = ctx->hub_tab.as<unsigned long long>();
+  hla->mask = ctx->hub_mask;
+  hla->n = ctx->hla_raw.as<unsigned long long>();
+  hla->raw = hla->n + 1;
+  hla->cap = cap;
+  hla->B = B;
+  return true;
+}
+
+void pc_hla_finish(pacim_ctx *ctx, Hla *hla) {
+  // sort the entries by key (the bits above the row), then rows + offsets
+  const unsigned long long nkeys = (unsigned long long)ctx->nhub * ctx->R_local;
+  unsigned long long nraw = 0;
+  PC_CUDA(cudaMemcpyAsync(&nraw, hla->n, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (nraw <= hla->cap) {
+    int kb = 1;
+    while (kb < 32 && (nkeys >> kb)) kb++;
+    TmpBuf alt(ctx), tmp(ctx);
+    pc_ensure(ctx, alt, std::max<size_t>(nraw, 1) * 8);
+    cub::DoubleBuffer<unsigned long long> db(hla->raw, alt.as<unsigned long long>());
+    size_t tb = 0;
+    PC_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tb, db, (int64_t)nraw, 32, 32 + kb, ctx->stream));
+    pc_ensure(ctx, tmp, std::max<size_t>(tb, 1));
+    PC_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tb, db, (int64_t)nraw, 32, 32 + kb, ctx->stream));
+    pc_ensure(ctx, ctx->hla_off, (nkeys + 1) * 8);
+    pc_ensure(ctx, ctx->hla_row, std::max<size_t>(nraw, 1) * 4);
+    k_hla_offsets<<<pc_grid(ctx, nraw + 1, 256), 256, 0, ctx->stream>>>(
+        db.Current(), nraw, nkeys, ctx->hla_off.as<unsigned long long>(), ctx->hla_row.as<uint32_t>());
+    PC_CHECK_LAUNCH();
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->hla_ok = true;
+    ctx->hla_n = nraw;
+    ctx->launches += 2;
+  }
+  pc_free(ctx, ctx->hla_raw);  // scratch
+}
+
 // Lb (rows x Bb), unions, full compression and CC sizes (root slot HIGH|size).
 // ctr[0] += non-singleton CCs, ctr[1] += non-roots, ctr[4] += live pairs.
 // ev (optional, 3 events) is recorded after init, edges and compress.
@@ -700,16 +775,16 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
           ctx->crow.as<uint32_t>(), nnz, ctx->K, ctx->t32, ctx->d_shr.as<uint32_t>(),
           ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>());
     } else if (ctx->pmodel != PACIM_P_CONST) {  // per-edge thresholds (WIC, Uniform)
-      auto kern = ctx->hash_rule ? (hla.cnt ? k_edges<true, true, true, false> : k_edges<true, false, true, false>)
-                                 : (hla.cnt ? k_edges<true, true, false, false> : k_edges<true, false, false, false>);
+      auto kern = ctx->hash_rule ? (hla.raw ? k_edges<true, true, true, false> : k_edges<true, false, true, false>)
+                                 : (hla.raw ? k_edges<true, true, false, false> : k_edges<true, false, false, false>);
       PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
           es.keys, es.ckeys, ctx->tm1.as<uint32_t>(), es.m,
           ctx->K, ctx->toff(), ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla,
           ctx->d_hr64.as<uint64_t>());
     } else {
-      auto kern = ctx->hash_rule ? (hla.cnt ? k_edges<false, true, true, false> : k_edges<false, false, true, false>)
-                                 : (hla.cnt ? k_edges<false, true, false, false> : k_edges<false, false, false, false>);
+      auto kern = ctx->hash_rule ? (hla.raw ? k_edges<false, true, true, false> : k_edges<false, false, true, false>)
+                                 : (hla.raw ? k_edges<false, true, false, false> : k_edges<false, false, false, false>);
       PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
           es.keys, es.ckeys, nullptr, es.m, ctx->K, ctx->t32,
@@ -787,8 +862,10 @@ void pc_build(pacim_ctx *ctx) {
   pc_slot_table(ctx);
   // a compressed store of an earlier build is released first (capacity for
   // this one: at c4 the two do not fit together)
-  for (DevBuf *d : {&ctx->clabel, &ctx->csz, &ctx->csz_work, &ctx->Ltmp, &ctx->cwork})
+  for (DevBuf *d : {&ctx->clabel, &ctx->csz, &ctx->csz_work, &ctx->Ltmp, &ctx->cwork,
+                    &ctx->hla_off, &ctx->hla_row, &ctx->hla_raw})
     pc_free(ctx, *d);
+  ctx->hla_ok = false;
   pc_ensure(ctx, ctx->L, (size_t)n * B * sizeof(uint32_t));
   pc_ensure(ctx, ctx->gain0, (size_t)ctx->n * sizeof(int64_t));
   pc_ensure(ctx, ctx->counters, 64 * sizeof(uint64_t));
@@ -800,24 +877,10 @@ void pc_build(pacim_ctx *ctx) {
   // live hub adjacency (HLA) of the hub rows: opt-in (PACIM_HLA=1): on c4
   // recording costs more build time than the selection saves (its traversal
   // is bound by hop latency, not edge work)
-  const bool want_hla = ctx->nhub > 0 && (getenv("PACIM_HLA") != nullptr ||
-                                          getenv("PACIM_FORCE_HLA") != nullptr);
+  const bool want_hla = (getenv("PACIM_HLA") != nullptr || getenv("PACIM_FORCE_HLA") != nullptr);
   ctx->hla_ok = false;
   Hla hla{};
-  if (want_hla) {
-    const size_t keys = (size_t)ctx->nhub * B + 1;
-    const unsigned long long cap = std::max<unsigned long long>(1ull << 20, (ctx->m / 16));
-    pc_ensure(ctx, ctx->hla_off, keys * 8);
-    pc_ensure(ctx, ctx->hla_raw, (cap + 1) * 8);
-    PC_CUDA(cudaMemsetAsync(ctx->hla_off.p, 0, keys * 8, ctx->stream));
-    PC_CUDA(cudaMemsetAsync(ctx->hla_raw.p, 0, 8, ctx->stream));
-    hla.hidx = ctx->hidx.as<uint32_t>();
-    hla.cnt = ctx->hla_off.as<unsigned long long>();
-    hla.n = ctx->hla_raw.as<unsigned long long>();
-    hla.raw = hla.n + 1;
-    hla.cap = cap;
-    hla.B = B;
-  }
+  const bool rec_hla = want_hla && pc_hla_begin(ctx, &hla, 1e30);
   const uint32_t W = plan_windows(ctx);
   const uint32_t nwin = (uint32_t)ctx->win_first.size() - 1;
   {  // per-slot window table (select / labels address the store through it)
@@ -875,7 +938,7 @@ void pc_build(pacim_ctx *ctx) {
       es.m = boff[b + 1] - boff[b];
     }
     PC_CUDA(cudaEventRecord(ev[1 + 4 * w], ctx->stream));
-    pc_sketch_pass(ctx, Lw, f, c, ctr, ev.data() + 2 + 4 * w, want_hla ? &hla : nullptr,
+    pc_sketch_pass(ctx, Lw, f, c, ctr, ev.data() + 2 + 4 * w, rec_hla ? &hla : nullptr,
                    W ? &es : nullptr);
     // CC sizes of the window into gain0 while it is still cached
     if (c < NARROW_W)
@@ -888,27 +951,7 @@ void pc_build(pacim_ctx *ctx) {
     ctx->launches++;
   }
   PC_CUDA(cudaEventRecord(ev.back(), ctx->stream));
-  if (want_hla) {
-    // counts -> offsets (in place via scratch), then rows grouped by key
-    const size_t keys = (size_t)ctx->nhub * B + 1;
-    unsigned long long nraw = 0;
-    PC_CUDA(cudaMemcpyAsync(&nraw, hla.n, 8, cudaMemcpyDeviceToHost, ctx->stream));
-    PC_CUDA(cudaStreamSynchronize(ctx->stream));
-    if (nraw <= hla.cap) {
-      TmpBuf cur(ctx);
-      pc_ensure(ctx, cur, keys * 8);
-      pc_exclusive_scan_u64(ctx, reinterpret_cast<const uint64_t *>(hla.cnt), cur.as<uint64_t>(), keys);
-      PC_CUDA(cudaMemcpyAsync(hla.cnt, cur.p, keys * 8, cudaMemcpyDeviceToDevice, ctx->stream));
-      pc_ensure(ctx, ctx->hla_row, std::max<size_t>(nraw, 1) * 4);
-      k_hla_scatter<<<pc_grid(ctx, nraw, 256), 256, 0, ctx->stream>>>(
-          hla.raw, nraw, cur.as<unsigned long long>(), ctx->hla_row.as<uint32_t>());
-      PC_CHECK_LAUNCH();
-      PC_CUDA(cudaStreamSynchronize(ctx->stream));
-      ctx->hla_ok = true;
-      ctx->hla_n = nraw;
-      ctx->launches += 2;
-    }
-  }
+  if (rec_hla) pc_hla_finish(ctx, &hla);
   ctx->launches += 1;  // fill
   unsigned long long h[6];
   PC_CUDA(cudaMemcpyAsync(h, ctr, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,

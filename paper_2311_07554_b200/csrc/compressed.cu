@@ -135,9 +135,15 @@ struct ProbeParams {
   const uint64_t *off;
   const uint32_t *nbr;
   uint64_t K, t32;
-  int wic;
-  int unif;                 // R19: T32 from the edge key (t32 = H << 32 | L)
+  const uint32_t *tcsr;     // per-edge models (WIC R4, Uniform R19): T32 - toff per CSR entry
+  uint32_t toff;
   int decor;                // R20: live <=> hi32(mix64(hash(r) ^ hash(e))) < T32
+  // live hub adjacency (hla_off != nullptr): a hub's live neighbours in slot j
+  // are the rows hla_row[hla_off[h * B + j] .. hla_off[h * B + j + 1])
+  const uint32_t *cid, *hidx, *rmap;
+  const unsigned long long *hla_off;
+  const uint32_t *hla_row;
+  uint64_t hub_deg;         // rows of degree > hub_deg are hubs
   const uint64_t *hr64;     // hash(r) per slot
   const uint32_t *shr;      // hi32(hash(r)) per slot
   uint32_t B;
@@ -156,19 +162,17 @@ struct ProbeParams {
   const uint32_t *scnt;     // [B] their number (> QCAP - 1: overflow, expand s in the probe)
 };
 
+__device__ __forceinline__ uint64_t thr_of(const ProbeParams &P, uint64_t e) {
+  return P.tcsr ? (uint64_t)P.tcsr[e] + P.toff : P.t32;
+}
+
+// edge (x, w) at CSR entry e live in the slot of hash hr (hrj: R20)
 __device__ __forceinline__ bool live_edge(const ProbeParams &P, uint32_t x, uint32_t w,
-                                          uint32_t hr, uint64_t hrj) {
+                                          uint64_t e, uint32_t hr, uint64_t hrj) {
   const uint64_t a = x < w ? x : w, b = x < w ? w : x;
   const uint64_t he64 = pc_mix64(((a << 32) | b) ^ P.K);
   const uint32_t he = (uint32_t)(he64 >> 32);
-  uint64_t T = P.t32;
-  if (P.wic) {  // R4
-    const uint64_t s = (P.off[x + 1] - P.off[x]) + (P.off[w + 1] - P.off[w]);
-    T = (1ull << 33) / s;
-    if (T > (1ull << 32)) T = 1ull << 32;
-  } else if (P.unif) {  // R19
-    T = pc_t32_uniform(P.t32, (a << 32) | b);
-  }
+  const uint64_t T = thr_of(P, e);
   if (P.decor) return T >= (1ull << 32) || (pc_mix64(hrj ^ he64) >> 32) < T;  // R20
   return (uint64_t)(hr ^ he) < T;  // R3
 }
@@ -185,14 +189,7 @@ __global__ void k_seed_live(ProbeParams P, uint32_t s, uint32_t *slive, uint32_t
     const uint64_t a = s < w ? s : w, b = s < w ? w : s;
     const uint64_t he64 = pc_mix64(((a << 32) | b) ^ P.K);
     const uint32_t he = (uint32_t)(he64 >> 32);
-    uint64_t T = P.t32;
-    if (P.wic) {
-      const uint64_t sd = (e1 - e0) + (P.off[w + 1] - P.off[w]);
-      T = (1ull << 33) / sd;
-      if (T > (1ull << 32)) T = 1ull << 32;
-    } else if (P.unif) {
-      T = pc_t32_uniform(P.t32, (a << 32) | b);
-    }
+    const uint64_t T = thr_of(P, e);
     if (T == 0) continue;
     const uint32_t wb = __clz((uint32_t)(T - 1));
     uint32_t lo, hi;
@@ -284,14 +281,26 @@ __global__ void __launch_bounds__(PROBE_WARPS * 32) k_probe(ProbeParams P, uint3
       }
       const uint32_t x = q[w][head++];
       if (!enumerate && P.is_seed[x]) seed_seen = true;
-      const uint64_t e1 = P.off[x + 1];
-      for (uint64_t e0 = P.off[x]; e0 < e1; e0 += 32) {
+      // a hub's live neighbours come from the HLA segment of (hub, j) instead
+      // of its whole adjacency (every entry live, no test)
+      uint64_t a0 = P.off[x], a1 = P.off[x + 1];
+      bool viah = false;
+      if (P.hla_off && a1 - a0 > P.hub_deg) {
+        const uint32_t h = P.hidx[P.cid[x]];
+        if (h != NONE) {
+          viah = true;
+          a0 = P.hla_off[(size_t)h * P.B + j];
+          a1 = P.hla_off[(size_t)h * P.B + j + 1];
+        }
+      }
+      const uint64_t e1 = a1;
+      for (uint64_t e0 = a0; e0 < e1; e0 += 32) {
         const uint64_t e = e0 + lane;
         // the set never holds more than QCAP + 31 < HCAP vertices: lanes stop
         // inserting once the queue is full, so probing always terminates
         if (e < e1 && tail[w] < QCAP) {
-          const uint32_t v = P.nbr[e];
-          if (live_edge(P, x, v, hr, hrj)) {
+          const uint32_t v = viah ? P.rmap[P.hla_row[e]] : P.nbr[e];
+          if (viah || live_edge(P, x, v, e, hr, hrj)) {
             uint32_t h = (v * 2654435761u) & (HCAP - 1);
             for (;;) {
               const uint32_t old = atomicCAS(&hs[w][h], NONE, v);
@@ -488,6 +497,7 @@ static uint32_t choose_batch(pacim_ctx *ctx) {
   if (const char *e = getenv("PACIM_BATCH")) return std::max<uint32_t>(1, std::min<uint32_t>(B, atoi(e)));
   size_t fr = 0, tot = 0;
   cudaMemGetInfo(&fr, &tot);
+  fr += ctx->Ltmp.bytes;  // an earlier batch buffer is reused (or freed before growing)
   size_t budget = std::min<size_t>(fr / 3, (size_t)24 << 30);
   size_t per = (size_t)std::max<uint32_t>(ctx->nr, 1) * 4;
   size_t bb = budget / per;
@@ -500,7 +510,11 @@ void pc_build_compressed(pacim_ctx *ctx) {
   pc_slot_table(ctx);
   // the uncompressed store and its selection state of an earlier build are
   // released first (the point of the compressed mode is not to hold them)
-  for (DevBuf *d : {&ctx->L, &ctx->bfs, &ctx->pkeys}) pc_free(ctx, *d);
+  // and so is the HLA of an earlier build; its batch parent arrays are kept
+  // for reuse (choose_batch counts them as free)
+  for (DevBuf *d : {&ctx->L, &ctx->bfs, &ctx->pkeys, &ctx->hla_off, &ctx->hla_row, &ctx->hla_raw})
+    pc_free(ctx, *d);
+  ctx->hla_ok = false;
   ctx->bfs_nr = 0;
   ctx->sel_list_valid = false;
   pc_ensure(ctx, ctx->counters, 64 * sizeof(uint64_t));
@@ -530,6 +544,8 @@ void pc_build_compressed(pacim_ctx *ctx) {
       flag, pos, n, ctx->center_of.as<uint32_t>(), ctx->centers.as<uint32_t>());
   PC_CHECK_LAUNCH();
   const size_t cs = std::max<size_t>((size_t)rho * B, 1) * 4;
+  for (DevBuf *d : {&ctx->clabel, &ctx->csz, &ctx->csz_work})
+    if (d->bytes > 2 * cs) pc_free(ctx, *d);  // an earlier, larger alpha's store
   pc_ensure(ctx, ctx->clabel, cs);
   pc_ensure(ctx, ctx->csz, cs);
   pc_ensure(ctx, ctx->csz_work, cs);
@@ -537,6 +553,15 @@ void pc_build_compressed(pacim_ctx *ctx) {
   k_fill_i64c<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(ctx->gain0.as<int64_t>(), n,
                                                             (int64_t)B);
   PC_CHECK_LAUNCH();
+  // live hub adjacency for the Get-center probes (a hub met by a probe is
+  // expanded from its live list, not its whole adjacency), recorded when its
+  // expected size is at most m / 4 entries (c4 WIC: 94M entries, the select
+  // 1.5 s -> 70 ms; c2 p = 0.01: 223M entries, +10 ms build for no select
+  // gain).  PACIM_HLA=1: always, PACIM_NO_HLA: never.
+  Hla hla{};
+  const double hla_lim = getenv("PACIM_HLA") || getenv("PACIM_FORCE_HLA") ? 1e30 : 0.25;
+  const bool rec_hla = getenv("PACIM_NO_HLA") == nullptr && pc_hla_begin(ctx, &hla, hla_lim);
+  if (!rec_hla) ctx->hla_ok = false;
   // ---- batches of Bb slots
   ctx->Bb = choose_batch(ctx);
   const uint32_t Bb = ctx->Bb;
@@ -547,7 +572,7 @@ void pc_build_compressed(pacim_ctx *ctx) {
   PC_CUDA(cudaEventRecord(e1, ctx->stream));
   for (uint32_t j0 = 0; j0 < B; j0 += Bb) {
     const uint32_t bb = std::min(Bb, B - j0);
-    pc_sketch_pass(ctx, Lb, j0, bb, ctr, nullptr);
+    pc_sketch_pass(ctx, Lb, j0, bb, ctr, nullptr, rec_hla ? &hla : nullptr);
     k_gain_sizes<<<pc_grid(ctx, (size_t)nr * 32, 256, 16), 256, 0, ctx->stream>>>(
         Lb, nr, bb, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>());
     PC_CHECK_LAUNCH();
@@ -567,6 +592,7 @@ void pc_build_compressed(pacim_ctx *ctx) {
     }
     ctx->launches += 1;
   }
+  if (rec_hla) pc_hla_finish(ctx, &hla);
   PC_CUDA(cudaMemcpyAsync(ctx->csz_work.p, ctx->csz.p, cs, cudaMemcpyDeviceToDevice, ctx->stream));
   PC_CUDA(cudaEventRecord(e2, ctx->stream));
   unsigned long long h[6];
@@ -610,9 +636,15 @@ void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *l
   P.nbr = ctx->nbr.as<uint32_t>();
   P.K = ctx->K;
   P.t32 = ctx->t32;
-  P.wic = ctx->pmodel == PACIM_P_WIC;
-  P.unif = ctx->pmodel == PACIM_P_UNIFORM;
+  P.tcsr = ctx->pmodel != PACIM_P_CONST ? ctx->tcsr.as<uint32_t>() : nullptr;
+  P.toff = ctx->toff();
   P.decor = ctx->hash_rule;
+  P.cid = ctx->cid.as<uint32_t>();
+  P.hidx = ctx->hidx.as<uint32_t>();
+  P.rmap = ctx->rmap.as<uint32_t>();
+  P.hla_off = ctx->hla_ok ? ctx->hla_off.as<unsigned long long>() : nullptr;
+  P.hla_row = ctx->hla_ok ? ctx->hla_row.as<uint32_t>() : nullptr;
+  P.hub_deg = ctx->hub_deg;
   P.hr64 = ctx->d_hr64.as<uint64_t>();
   P.shr = ctx->d_shr.as<uint32_t>();
   P.B = B;

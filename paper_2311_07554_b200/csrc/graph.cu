@@ -301,7 +301,22 @@ __global__ void k_hub_index(const uint64_t *off, const uint32_t *rmap, uint32_t 
   for (size_t u = (size_t)blockIdx.x * blockDim.x + threadIdx.x; u < nr;
        u += (size_t)gridDim.x * blockDim.x) {
     const uint32_t x = rmap[u];
-    hidx[u] = off[x + 1] - off[x] > hub_deg ? (uint32_t)atomicAdd(cnt, 1ull) : 0xFFFFFFFFu;
+    const uint64_t d = off[x + 1] - off[x];
+    hidx[u] = d > hub_deg ? (uint32_t)atomicAdd(cnt, 1ull) : 0xFFFFFFFFu;
+    if (d > hub_deg) atomicAdd(cnt + 1, (unsigned long long)d);  // hub CSR entries
+  }
+}
+
+// the hub rows into the hash table of Hla::hub_of (all slots start empty, ~0)
+__global__ void k_hub_table(const uint32_t *hidx, uint32_t nr, unsigned long long *tab,
+                            uint32_t mask) {
+  for (size_t u = (size_t)blockIdx.x * blockDim.x + threadIdx.x; u < nr;
+       u += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t hi = hidx[u];
+    if (hi == 0xFFFFFFFFu) continue;
+    const unsigned long long e = ((unsigned long long)u << 32) | hi;
+    for (uint32_t h = ((uint32_t)u * 2654435761u) & mask;; h = (h + 1) & mask)
+      if (atomicCAS(tab + h, ~0ull, e) == ~0ull) break;
   }
 }
 }  // namespace
@@ -361,14 +376,23 @@ static void derive_common(pacim_ctx *ctx) {
     if (const char *e = getenv("PACIM_HUB_DEG")) ctx->hub_deg = (uint64_t)std::max(1LL, atoll(e));
     pc_ensure(ctx, ctx->hidx, std::max<size_t>(ctx->nr, 1) * 4);
     unsigned long long *t = ctx->counters.as<unsigned long long>();
-    PC_CUDA(cudaMemsetAsync(t, 0, 8, ctx->stream));
+    PC_CUDA(cudaMemsetAsync(t, 0, 16, ctx->stream));
     k_hub_index<<<pc_grid(ctx, ctx->nr, 256), 256, 0, ctx->stream>>>(
         off, ctx->rmap.as<uint32_t>(), ctx->nr, ctx->hub_deg, ctx->hidx.as<uint32_t>(), t);
     PC_CHECK_LAUNCH();
-    unsigned long long h = 0;
-    PC_CUDA(cudaMemcpyAsync(&h, t, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    unsigned long long h[2] = {0, 0};
+    PC_CUDA(cudaMemcpyAsync(h, t, 16, cudaMemcpyDeviceToHost, ctx->stream));
     PC_CUDA(cudaStreamSynchronize(ctx->stream));
-    ctx->nhub = (uint32_t)h;
+    ctx->nhub = (uint32_t)h[0];
+    ctx->hub_entries = h[1];
+    uint32_t tsz = 1024;
+    while (tsz < 2ull * ctx->nhub) tsz *= 2;
+    ctx->hub_mask = tsz - 1;
+    pc_ensure(ctx, ctx->hub_tab, (size_t)tsz * 8);
+    PC_CUDA(cudaMemsetAsync(ctx->hub_tab.p, 0xFF, (size_t)tsz * 8, ctx->stream));
+    k_hub_table<<<pc_grid(ctx, ctx->nr, 256), 256, 0, ctx->stream>>>(
+        ctx->hidx.as<uint32_t>(), ctx->nr, ctx->hub_tab.as<unsigned long long>(), ctx->hub_mask);
+    PC_CHECK_LAUNCH();
   }
   pc_ensure(ctx, ctx->ckeys, std::max<size_t>(m, 1) * 8);
   k_ckeys<<<pc_grid(ctx, m, 256), 256, 0, ctx->stream>>>(ctx->keys.as<uint64_t>(), m,
@@ -441,7 +465,9 @@ static void derive_lean(pacim_ctx *ctx) {
   pc_free(ctx, ctx->keys);
   pc_free(ctx, ctx->ckeys);
   pc_free(ctx, ctx->hidx);
+  pc_free(ctx, ctx->hub_tab);
   ctx->nhub = 0;
+  ctx->hub_entries = 0;
   ctx->launches += 4;
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
 }

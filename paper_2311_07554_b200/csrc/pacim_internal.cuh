@@ -142,7 +142,10 @@ struct pacim_ctx {
   // hub's whole adjacency
   uint64_t hub_deg = 2048;
   uint32_t nhub = 0;
+  uint64_t hub_entries = 0;  // CSR entries of the hub rows
   DevBuf hidx;           // u32[nr] hub index of a row or 0xFFFFFFFF
+  DevBuf hub_tab;        // u64[hub_mask + 1] hash table (row << 32 | hub index), empty = ~0
+  uint32_t hub_mask = 0;
   bool hla_ok = false;   // HLA built for the current store
   uint64_t hla_n = 0;    // live (hub, slot, row) entries
   DevBuf hla_off;        // u64[nhub * B + 1] segment offsets by (hub, slot)
@@ -242,20 +245,34 @@ void pc_generate(pacim_ctx *ctx, int kind, const uint64_t *params, int nparams,
 void pc_build(pacim_ctx *ctx);
 void pc_slot_table(pacim_ctx *ctx);
 // Live hub adjacency (HLA) being recorded: raw (key << 32 | other row) with
-// key = hub index * B + slot, counted per key.  Entries past cap are dropped
-// (the build then flags the HLA invalid and the selection hashes hubs' edges).
+// key = hub index * B + slot, appended in any order (grouped by key after the
+// build: pc_hla_finish).  Entries past cap are dropped (the build then flags
+// the HLA invalid and the selection hashes hubs' edges).
 struct Hla {
-  const uint32_t *hidx;
-  unsigned long long *cnt;   // [nhub * B + 1]
+  // hub row -> hub index: open addressing over (row << 32 | index), a few MB
+  // and L2-resident (the per-row index hidx is not: one random DRAM read per entry)
+  const unsigned long long *tab;
+  uint32_t mask;
   unsigned long long *raw;   // [cap]
   unsigned long long *n;     // entries appended
   unsigned long long cap;
   uint32_t B;
-  // all 32 lanes call this together; lane i appends nu entries for hub row u
-  // and nv for hub row v (live edge (u, v) in slot j): one counter update per warp
-  __device__ __forceinline__ void add_warp(uint32_t u, uint32_t v, uint32_t j, uint32_t nu,
-                                           uint32_t nv) const {
+  __device__ __forceinline__ uint32_t hub_of(uint32_t row) const {
+    for (uint32_t h = (row * 2654435761u) & mask;; h = (h + 1) & mask) {
+      const unsigned long long e = __ldg(tab + h);
+      if ((uint32_t)(e >> 32) == row) return (uint32_t)e;
+    }
+  }
+  // all 32 lanes call this together; lane i stages nu entries for hub row u
+  // and nv for hub row v (live edge (u, v) in slot j) in the warp's shared
+  // buffer buf (HLA_WBUF entries, bn of them used); a nearly full buffer is
+  // flushed with one counter update (one global atomic per ~HLA_WBUF - 64
+  // entries instead of one per round: the counter is a single address)
+  static constexpr uint32_t HLA_WBUF = 128;
+  __device__ __forceinline__ void stage(uint32_t u, uint32_t v, uint32_t j, uint32_t nu,
+                                        uint32_t nv, unsigned long long *buf, uint32_t &bn) const {
     const uint32_t mine = nu + nv;
+    if (!__ballot_sync(0xffffffffu, mine)) return;
     const uint32_t lane = threadIdx.x & 31;
     uint32_t pre = mine;
     for (int d = 1; d < 32; d <<= 1) {
@@ -263,21 +280,23 @@ struct Hla {
       if (lane >= (uint32_t)d) pre += y;
     }
     const uint32_t tot = __shfl_sync(0xffffffffu, pre, 31);
-    if (!tot) return;
+    uint32_t pos = bn + pre - mine;
+    if (nu) buf[pos++] = ((unsigned long long)hub_of(u) * B + j) << 32 | v;
+    if (nv) buf[pos] = ((unsigned long long)hub_of(v) * B + j) << 32 | u;
+    bn += tot;
+    if (bn > HLA_WBUF - 64) flush(buf, bn);
+  }
+  __device__ __forceinline__ void flush(unsigned long long *buf, uint32_t &bn) const {
+    __syncwarp();
+    if (!bn) return;
+    const uint32_t lane = threadIdx.x & 31;
     unsigned long long base = 0;
-    if (lane == 31) base = atomicAdd(n, (unsigned long long)tot);
-    base = __shfl_sync(0xffffffffu, base, 31) + (pre - mine);
-    if (nu) {
-      const unsigned long long key = (unsigned long long)hidx[u] * B + j;
-      atomicAdd(cnt + key, 1ull);
-      if (base < cap) raw[base] = (key << 32) | v;
-      base++;
-    }
-    if (nv) {
-      const unsigned long long key = (unsigned long long)hidx[v] * B + j;
-      atomicAdd(cnt + key, 1ull);
-      if (base < cap) raw[base] = (key << 32) | u;
-    }
+    if (lane == 0) base = atomicAdd(n, (unsigned long long)bn);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (uint32_t i = lane; i < bn; i += 32)
+      if (base + i < cap) raw[base + i] = buf[i];
+    __syncwarp();
+    bn = 0;
   }
 };
 
@@ -287,6 +306,13 @@ struct EdgeSet {
   const uint64_t *keys = nullptr, *ckeys = nullptr;
   uint64_t m = 0;
 };
+// HLA recording around the sketch passes of a build: begin sizes the raw
+// buffer from the expected live hub entries E (false: not recorded — no hubs,
+// a lean graph, E > max_per_edge * m, or it does not fit in a slice of the
+// free memory); finish groups the entries by (hub, slot) and sets
+// ctx->hla_ok (false on overflow).
+bool pc_hla_begin(pacim_ctx *ctx, Hla *hla, double max_per_edge);
+void pc_hla_finish(pacim_ctx *ctx, Hla *hla);
 void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
                     unsigned long long *ctr, cudaEvent_t *ev, const Hla *hla = nullptr,
                     const EdgeSet *es = nullptr);

@@ -172,3 +172,34 @@ def test_c5_shape_scale16_lean_bucketed(orc, ctx, monkeypatch):
 def test_compressed_lean(orc, ctx, i, monkeypatch):
     monkeypatch.setenv("PACIM_LEAN", "1")
     run_case(orc, ctx, i, check_sketches=True)
+
+
+@pytest.mark.parametrize("i", [1, 4, 8, 9, 10])
+def test_compressed_hla(orc, ctx, i, monkeypatch):
+    """Get-center probes expand a hub from the live hub adjacency the build
+    recorded (forced; hub degree lowered to 4 so the small graphs have hubs): the
+    seeds, gains and gain0 equal the oracle's greedy."""
+    monkeypatch.setenv("PACIM_HUB_DEG", "4")
+    monkeypatch.setenv("PACIM_HLA", "1")
+    run_case(orc, ctx, i, check_sketches=False)
+    st = ctx.pacim_get_stats()
+    assert st["hubs"] > 0 and st["hla_entries"] > 0
+
+
+@pytest.mark.parametrize("i", [4, 10])
+def test_compressed_hla_multibatch(orc, ctx, i, monkeypatch):
+    """HLA recorded across several build batches (3 sketches per batch)."""
+    monkeypatch.setenv("PACIM_HUB_DEG", "4")
+    monkeypatch.setenv("PACIM_HLA", "1")
+    monkeypatch.setenv("PACIM_BATCH", "3")
+    run_case(orc, ctx, i, check_sketches=False)
+    assert ctx.pacim_get_stats()["hla_entries"] > 0
+
+
+def test_compressed_no_hla_star(orc, ctx, monkeypatch):
+    """PACIM_NO_HLA: hubs are scanned edge by edge (the star's hub has 4999
+    neighbours > the default hub degree)."""
+    monkeypatch.setenv("PACIM_NO_HLA", "1")
+    run_case(orc, ctx, 8)
+    st = ctx.pacim_get_stats()
+    assert st["hubs"] == 1 and st["hla_entries"] == 0
