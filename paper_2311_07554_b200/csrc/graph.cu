@@ -179,67 +179,59 @@ __global__ void k_upper_count(const uint64_t *off, const uint32_t *nbr, uint32_t
   }
 }
 
-// keys[ustart[v] + i] = v<<32 | w for the i-th neighbour w > v (warp per vertex).
-__global__ void k_upper_fill(const uint64_t *off, const uint32_t *nbr, uint32_t n,
-                             const uint64_t *ustart, const uint64_t *ucnt, uint64_t *keys) {
-  const int lane = threadIdx.x & 31;
-  size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  size_t nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
-  for (size_t v = warp; v < n; v += nwarps) {
-    uint64_t c = ucnt[v];
-    uint64_t first = off[v + 1] - c, dst = ustart[v];
-    for (uint64_t i = lane; i < c; i += 32)
-      keys[dst + i] = ((uint64_t)v << 32) | nbr[first + i];
+// row of CSR entry e: the chunk table gives the row of entry 32 * (e >> 5),
+// advanced past row ends (lane per entry: balanced whatever the degrees; a
+// warp per vertex left a hub's 10^6 entries to one warp: 87 ms at c4)
+__device__ __forceinline__ uint32_t entry_row(const uint64_t *off, const uint32_t *crow,
+                                              uint64_t e) {
+  uint32_t u = crow[e >> 5];
+  while (e >= off[u + 1]) u++;
+  return u;
+}
+
+// per vertex: degree << 32 | store row (+ hub flag) — the one gather per CSR
+// entry of k_edge_derive (separate cid / hidx / off gathers cost 5 random
+// reads per upper edge: 105 ms at c4)
+__global__ void k_vinfo(const uint64_t *off, const uint32_t *cid, const uint32_t *hidx,
+                        uint32_t n, uint64_t *vinfo) {
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (size_t)gridDim.x * blockDim.x) {
+    uint32_t c = cid[v];
+    if (c != 0xFFFFFFFFu && hidx[c] != 0xFFFFFFFFu) c |= PACIM_HUBF;
+    vinfo[v] = ((off[v + 1] - off[v]) << 32) | c;
   }
 }
 
-// R4: WIC threshold T32 = min(2^32, floor(2^33 / (d_u + d_v))), stored as T32-1.
-// R4 per CSR entry (warp per vertex): tcsr[e] = T32(x, nbr[e]) - 1
-__global__ void k_wic_csr(const uint64_t *off, const uint32_t *nbr, uint32_t n, uint32_t *tcsr) {
-  const int lane = threadIdx.x & 31;
-  size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
-  for (size_t x = warp; x < n; x += nw) {
-    const uint64_t a = off[x], b = off[x + 1];
-    for (uint64_t e = a + lane; e < b; e += 32) {
-      const uint32_t w = nbr[e];
-      const uint64_t s = (b - a) + (off[w + 1] - off[w]);
-      uint64_t t = (1ull << 33) / s;
-      if (t > (1ull << 32)) t = 1ull << 32;
-      tcsr[e] = (uint32_t)(t - 1);
-    }
-  }
-}
-
-// R19 Uniform thresholds per upper edge / per CSR entry (stored as T32, toff 0)
-__global__ void k_unif(const uint64_t *keys, uint64_t m, uint64_t packed, uint32_t *tm1) {
-  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
-       e += (size_t)gridDim.x * blockDim.x)
-    tm1[e] = (uint32_t)pc_t32_uniform(packed, keys[e]);
-}
-__global__ void k_unif_csr(const uint64_t *off, const uint32_t *nbr, uint32_t n, uint64_t packed,
-                           uint32_t *tcsr) {
-  const int lane = threadIdx.x & 31;
-  size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
-  for (size_t x = warp; x < n; x += nw) {
-    for (uint64_t e = off[x] + lane; e < off[x + 1]; e += 32) {
-      const uint64_t w = nbr[e];
-      const uint64_t key = x < w ? ((uint64_t)x << 32) | w : (w << 32) | x;
-      tcsr[e] = (uint32_t)pc_t32_uniform(packed, key);
-    }
-  }
-}
-
-__global__ void k_wic(const uint64_t *keys, uint64_t m, const uint64_t *off, uint32_t *tm1) {
-  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+// Lane per CSR entry e = (u, w): the upper edge list (keys[ustart[u] + i] =
+// u<<32 | w for the i-th neighbour w > u; lists are sorted, so keys are), the
+// same edge as store rows + hub flags (ckeys), and for the per-edge models the
+// threshold T32 - toff per upper edge (tm1) and per CSR entry (tcsr):
+// WIC R4 T32 = min(2^32, floor(2^33 / (d_u + d_w))), Uniform R19
+// pc_t32_uniform(packed, key).
+__global__ void k_edge_derive(const uint64_t *off, const uint32_t *nbr, const uint32_t *crow,
+                              uint64_t nnz, const uint64_t *ustart, const uint64_t *ucnt,
+                              const uint64_t *vinfo, int pmodel, uint64_t t32, uint32_t toff,
+                              uint64_t *keys, uint64_t *ckeys, uint32_t *tm1, uint32_t *tcsr) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
        e += (size_t)gridDim.x * blockDim.x) {
-    uint64_t k = keys[e];
-    uint32_t u = (uint32_t)(k >> 32), v = (uint32_t)k;
-    uint64_t s = (off[u + 1] - off[u]) + (off[v + 1] - off[v]);
-    uint64_t t = (1ull << 33) / s;
-    if (t > (1ull << 32)) t = 1ull << 32;
-    tm1[e] = (uint32_t)(t - 1);
+    const uint32_t u = entry_row(off, crow, e), w = nbr[e];
+    if (pmodel == PACIM_P_CONST && w < u) continue;  // lower entries: nothing to write
+    const uint64_t iu = vinfo[u], iw = vinfo[w];
+    uint64_t T = 0;
+    if (pmodel == PACIM_P_WIC) {
+      T = (1ull << 33) / ((iu >> 32) + (iw >> 32));
+      if (T > (1ull << 32)) T = 1ull << 32;
+    } else if (pmodel == PACIM_P_UNIFORM) {
+      const uint64_t a = u < w ? u : w, b = u < w ? w : u;
+      T = pc_t32_uniform(t32, (a << 32) | b);
+    }
+    if (pmodel != PACIM_P_CONST) tcsr[e] = (uint32_t)(T - toff);
+    if (w > u) {
+      const uint64_t pos = ustart[u] + (e - (off[u + 1] - ucnt[u]));
+      keys[pos] = ((uint64_t)u << 32) | w;
+      ckeys[pos] = ((iu & 0xFFFFFFFFull) << 32) | (iw & 0xFFFFFFFFull);
+      if (pmodel != PACIM_P_CONST) tm1[pos] = (uint32_t)(T - toff);
+    }
   }
 }
 }  // namespace
@@ -283,18 +275,6 @@ __global__ void k_rowmap(const uint64_t *flag, const uint64_t *pos, uint32_t n, 
   }
 }
 
-__global__ void k_ckeys(const uint64_t *keys, uint64_t m, const uint32_t *cid, const uint32_t *hidx,
-                        uint64_t *ckeys) {
-  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
-       e += (size_t)gridDim.x * blockDim.x) {
-    uint64_t k = keys[e];
-    uint32_t a = cid[k >> 32], b = cid[k & 0xFFFFFFFFull];
-    if (hidx[a] != 0xFFFFFFFFu) a |= PACIM_HUBF;
-    if (hidx[b] != 0xFFFFFFFFu) b |= PACIM_HUBF;
-    ckeys[e] = ((uint64_t)a << 32) | b;
-  }
-}
-
 // hub index of the store rows: degree > hub_deg
 __global__ void k_hub_index(const uint64_t *off, const uint32_t *rmap, uint32_t nr,
                             uint64_t hub_deg, uint32_t *hidx, unsigned long long *cnt) {
@@ -325,15 +305,25 @@ __global__ void k_hub_table(const uint32_t *hidx, uint32_t nr, unsigned long lon
 // (isolated vertices are singletons in every sketch and get no row; rows keep
 // the vertex order, so min row = min id), compact edge endpoints, WIC T32.
 static void derive_lean(pacim_ctx *ctx);
+namespace {
+__global__ void k_crow(const uint64_t *off, uint32_t n, uint32_t *crow);
+__global__ void k_iota_u32(uint32_t *a, uint32_t n);
+}  // namespace
 
-static void derive_common(pacim_ctx *ctx) {
+// crow[c] = row of CSR entry 32 c: the chunk table of the lane-per-entry kernels
+static void make_crow(pacim_ctx *ctx, DevBuf &crow) {
+  const uint64_t nch = (2 * ctx->m + 31) / 32;
+  pc_ensure(ctx, crow, (nch + 1) * 4);
+  k_crow<<<pc_grid(ctx, ctx->n, 256), 256, 0, ctx->stream>>>(ctx->off.as<uint64_t>(), ctx->n,
+                                                            crow.as<uint32_t>());
+  PC_CHECK_LAUNCH();
+  ctx->launches++;
+}
+
+// from the degrees alone: hub vertex, store rows (cid / rmap), hub rows
+static void derive_rows(pacim_ctx *ctx) {
   const uint32_t n = ctx->n;
-  const uint64_t m = ctx->m;
   uint64_t *off = ctx->off.as<uint64_t>();
-  if (ctx->lean) {
-    derive_lean(ctx);
-    return;
-  }
   {
     pc_ensure(ctx, ctx->counters, 64 * 8);
     unsigned long long *t = ctx->counters.as<unsigned long long>();
@@ -394,46 +384,58 @@ static void derive_common(pacim_ctx *ctx) {
         ctx->hidx.as<uint32_t>(), ctx->nr, ctx->hub_tab.as<unsigned long long>(), ctx->hub_mask);
     PC_CHECK_LAUNCH();
   }
-  pc_ensure(ctx, ctx->ckeys, std::max<size_t>(m, 1) * 8);
-  k_ckeys<<<pc_grid(ctx, m, 256), 256, 0, ctx->stream>>>(ctx->keys.as<uint64_t>(), m,
-                                                        ctx->cid.as<uint32_t>(),
-                                                        ctx->hidx.as<uint32_t>(),
-                                                        ctx->ckeys.as<uint64_t>());
+}
+
+// from the CSR: upper edge list, its store-row form, per-edge thresholds
+// (counts -> scan -> one lane-per-entry pass, k_edge_derive)
+static void derive_edges(pacim_ctx *ctx) {
+  const uint32_t n = ctx->n;
+  const uint64_t m = ctx->m, nnz = 2 * m;
+  uint64_t *off = ctx->off.as<uint64_t>();
+  const uint32_t *nbr = ctx->nbr.as<uint32_t>();
+  pc_ensure(ctx, ctx->scratch, 2 * ((size_t)n + 1) * sizeof(uint64_t));
+  uint64_t *ucnt = ctx->scratch.as<uint64_t>();
+  uint64_t *ustart = ucnt + n + 1;
+  k_upper_count<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(off, nbr, n, ucnt);
   PC_CHECK_LAUNCH();
-  if (ctx->pmodel == PACIM_P_UNIFORM) {
+  pc_exclusive_scan_u64(ctx, ucnt, ustart, n);
+  pc_ensure(ctx, ctx->keys, std::max<size_t>(m, 1) * 8);
+  pc_ensure(ctx, ctx->ckeys, std::max<size_t>(m, 1) * 8);
+  const bool per_edge = ctx->pmodel != PACIM_P_CONST;
+  if (per_edge) {
     pc_ensure(ctx, ctx->tm1, std::max<size_t>(m, 1) * sizeof(uint32_t));
-    k_unif<<<pc_grid(ctx, m, 256), 256, 0, ctx->stream>>>(ctx->keys.as<uint64_t>(), m, ctx->t32,
-                                                         ctx->tm1.as<uint32_t>());
+    pc_ensure(ctx, ctx->tcsr, std::max<size_t>(nnz, 1) * sizeof(uint32_t));
+  }
+  if (nnz) {
+    make_crow(ctx, ctx->crow);  // capacity kept across loads (no cudaMalloc per load)
+    pc_ensure(ctx, ctx->vinfo, (size_t)n * 8);
+    k_vinfo<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(off, ctx->cid.as<uint32_t>(),
+                                                          ctx->hidx.as<uint32_t>(), n,
+                                                          ctx->vinfo.as<uint64_t>());
     PC_CHECK_LAUNCH();
-    pc_ensure(ctx, ctx->tcsr, std::max<size_t>(2 * m, 1) * sizeof(uint32_t));
-    k_unif_csr<<<pc_grid(ctx, (size_t)n * 32, 256), 256, 0, ctx->stream>>>(
-        off, ctx->nbr.as<uint32_t>(), n, ctx->t32, ctx->tcsr.as<uint32_t>());
+    k_edge_derive<<<pc_grid(ctx, nnz, 256), 256, 0, ctx->stream>>>(
+        off, nbr, ctx->crow.as<uint32_t>(), nnz, ustart, ucnt, ctx->vinfo.as<uint64_t>(),
+        ctx->pmodel, ctx->t32, ctx->toff(), ctx->keys.as<uint64_t>(), ctx->ckeys.as<uint64_t>(),
+        per_edge ? ctx->tm1.as<uint32_t>() : nullptr, per_edge ? ctx->tcsr.as<uint32_t>() : nullptr);
     PC_CHECK_LAUNCH();
   }
-  if (ctx->pmodel == PACIM_P_WIC) {
-    pc_ensure(ctx, ctx->tm1, std::max<size_t>(m, 1) * sizeof(uint32_t));
-    k_wic<<<pc_grid(ctx, m, 256), 256, 0, ctx->stream>>>(ctx->keys.as<uint64_t>(), m, off,
-                                                        ctx->tm1.as<uint32_t>());
-    PC_CHECK_LAUNCH();
-    // the same thresholds in CSR order, for the traversals of the selection
-    pc_ensure(ctx, ctx->tcsr, std::max<size_t>(2 * m, 1) * sizeof(uint32_t));
-    k_wic_csr<<<pc_grid(ctx, (size_t)n * 32, 256), 256, 0, ctx->stream>>>(
-        off, ctx->nbr.as<uint32_t>(), n, ctx->tcsr.as<uint32_t>());
-    PC_CHECK_LAUNCH();
-  }
-  ctx->launches += 5;
+  ctx->launches += 4;
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+static void derive_common(pacim_ctx *ctx) {
+  if (ctx->lean) {
+    derive_lean(ctx);
+    return;
+  }
+  derive_rows(ctx);   // the store rows first: the edge pass writes edges as rows
+  derive_edges(ctx);
 }
 
 // Lean graphs (c5 at full scale): no upper edge list and no
 // row compaction — the store rows are the vertex ids (isolated vertices are
 // singleton rows), k_edges reads the upper edges straight from the CSR
 // through the chunk -> row table `crow`.  Constant probabilities only.
-namespace {
-__global__ void k_crow(const uint64_t *off, uint32_t n, uint32_t *crow);
-__global__ void k_iota_u32(uint32_t *a, uint32_t n);
-}  // namespace
-
 static void derive_lean(pacim_ctx *ctx) {
   const uint32_t n = ctx->n;
   uint64_t *off = ctx->off.as<uint64_t>();
@@ -458,10 +460,7 @@ static void derive_lean(pacim_ctx *ctx) {
   k_iota_u32<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(ctx->cid.as<uint32_t>(), n);
   k_iota_u32<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(ctx->rmap.as<uint32_t>(), n);
   PC_CHECK_LAUNCH();
-  const uint64_t nch = (2 * ctx->m + 31) / 32;
-  pc_ensure(ctx, ctx->crow, (nch + 1) * 4);
-  k_crow<<<pc_grid(ctx, (size_t)n * 32, 256), 256, 0, ctx->stream>>>(off, n, ctx->crow.as<uint32_t>());
-  PC_CHECK_LAUNCH();
+  make_crow(ctx, ctx->crow);
   pc_free(ctx, ctx->keys);
   pc_free(ctx, ctx->ckeys);
   pc_free(ctx, ctx->hidx);
@@ -506,22 +505,6 @@ void pc_graph_finish_load(pacim_ctx *ctx, int validate) {
     }
   }
   ctx->lean = want_lean(ctx);
-  if (ctx->lean) {
-    derive_common(ctx);
-    return;
-  }
-  // upper edge list (sorted keys): counts -> scan -> fill
-  pc_ensure(ctx, ctx->scratch, 2 * ((size_t)n + 1) * sizeof(uint64_t));
-  uint64_t *ucnt = ctx->scratch.as<uint64_t>();
-  uint64_t *ustart = ucnt + n + 1;
-  k_upper_count<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(off, nbr, n, ucnt);
-  PC_CHECK_LAUNCH();
-  pc_exclusive_scan_u64(ctx, ucnt, ustart, n);
-  pc_ensure(ctx, ctx->keys, std::max<size_t>(ctx->m, 1) * sizeof(uint64_t));
-  k_upper_fill<<<pc_grid(ctx, (size_t)n * 32, 256), 256, 0, ctx->stream>>>(
-      off, nbr, n, ustart, ucnt, ctx->keys.as<uint64_t>());
-  PC_CHECK_LAUNCH();
-  ctx->launches += 3;
   derive_common(ctx);
 }
 
@@ -626,13 +609,13 @@ __global__ void k_add_u64(uint64_t *a, uint64_t N, uint64_t x) {
 }
 
 // lean graphs: the row of the first CSR entry of every 32-entry chunk
+// thread per row: the chunks whose first entry lies in the row (stores only,
+// so a hub's many chunks do not stall its thread)
 __global__ void k_crow(const uint64_t *off, uint32_t n, uint32_t *crow) {
-  const int lane = threadIdx.x & 31;
-  const size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
-  for (size_t u = warp; u < n; u += nw) {
+  for (size_t u = (size_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+       u += (size_t)gridDim.x * blockDim.x) {
     const uint64_t c0 = (off[u] + 31) / 32, c1 = (off[u + 1] + 31) / 32;
-    for (uint64_t c = c0 + lane; c < c1; c += 32) crow[c] = (uint32_t)u;
+    for (uint64_t c = c0; c < c1; c++) crow[c] = (uint32_t)u;
   }
 }
 __global__ void k_iota_u32(uint32_t *a, uint32_t n) {

@@ -133,7 +133,9 @@ struct pacim_ctx {
   DevBuf rmap;           // u32[nr]  vertex id of store row c
   uint32_t nr = 0;       // store rows = non-isolated vertices (order kept)
   bool lean = false;     // no keys / ckeys: rows = vertex ids, k_edges reads the CSR (c5)
-  DevBuf crow;           // lean: u32 row of the first CSR entry of each 32-entry chunk
+  DevBuf vinfo;          // u64[n] degree << 32 | store row (+ hub flag), for the load's edge pass
+  DevBuf crow;           // u32 row of the first CSR entry of each 32-entry chunk (lane-per-entry
+                         // kernels; lean graphs: k_edges)
   uint32_t hub_row = 0xFFFFFFFFu;  // store row of the hub vertex
 
   // hub rows (degree > hub_deg): index per row and the live hub adjacency of
