@@ -188,6 +188,25 @@ def test_edge_cases(orc, ctx, pc):
         ctx.pacim_load_graph(np.array([0, 1, 1], np.uint64), np.array([1], np.uint32), 0, 1, 2)
 
 
+@pytest.mark.parametrize("p", [0.4, "wic", ("unif", 0.2, 0.6)])
+def test_load_derivation_shapes(orc, ctx, p):
+    """The load's edge pass (rows of CSR entries from the 32-entry chunk
+    table, one packed (degree, row + hub flag) gather per entry) on shapes
+    that stress it: isolated vertices between and after the edges, a hub whose
+    list spans several chunks next to degree-1 rows, a chunk starting inside a
+    row; and an edgeless graph.  Labels, gain0 and the greedy equal the
+    oracle's under the constant, WIC and Uniform models."""
+    from oracle.oracle import Graph
+    model, t32 = model_of(orc, p)
+    n = 300
+    edges = [(0, v) for v in range(5, 300, 2)] + [(7, 9), (11, 13), (250, 251), (3, 290)]
+    off, nbr = inputs.csr_from_edges(n, edges)
+    assert off[1] > 64 and (np.diff(off.astype(np.int64)) == 0).sum() > 100
+    full_parity(orc, ctx, Graph(n, off, nbr), model, t32, 16, 77, 6)
+    off, nbr = inputs.csr_from_edges(40, [])
+    full_parity(orc, ctx, Graph(40, off, nbr), model, t32, 5, 78, 4)
+
+
 def test_determinism(orc, ctx):
     from oracle.oracle import Graph
     off, nbr = inputs.random_powerlaw_graph(3000, 20000, 11)
