@@ -169,6 +169,7 @@ struct Sel {
   unsigned long long cov_cap;
   uint32_t big_t;
   int warp_ok;             // small CCs may use warp_bfs
+  uint32_t warp_max;       // ... up to this many vertices (<= QCAP)
   int trav_only;           // no store: dl[] preset per slot, only the member traversal
   // asynchronous traversal
   uint32_t *vis;           // rows x BW: slots in which the row was visited this step
@@ -347,39 +348,56 @@ __device__ bool warp_bfs(const Sel &S, uint32_t s, uint32_t j, uint32_t delta, u
       }
       const uint32_t total = __shfl_sync(FULL, pre, 31);
       pre -= (uint32_t)deg;  // exclusive
-      for (uint32_t c = 0; c < total; c += 32) {
-        const uint32_t t = c + lane;
-        uint32_t a = 0;  // the lane (vertex) owning pair t: largest a with pre[a] <= t
+      // WU rounds of 32 pairs at a time: their CSR (and threshold) loads are
+      // issued back to back, then the pairs are tested and inserted
+      constexpr int WU = 4;
+      for (uint32_t c = 0; c < total; c += 32 * WU) {
+        uint32_t wv[WU], xv[WU];
+        uint64_t tv[WU];
 #pragma unroll
-        for (int b = 16; b; b >>= 1) {
-          const uint32_t pa = __shfl_sync(FULL, pre, a + b);
-          if (pa <= t) a += b;
-        }
-        const uint32_t xa = __shfl_sync(FULL, x, a);
-        const uint64_t ea = __shfl_sync(FULL, e0, a);
-        const uint32_t pra = __shfl_sync(FULL, pre, a);
-        if (t >= total) continue;
-        const uint64_t e = ea + (t - pra);
-        const uint32_t w = S.nbr[e];
-        const uint64_t lo = xa < w ? xa : w, hi = xa < w ? w : xa;
-        const uint64_t he64 = pc_mix64(((lo << 32) | hi) ^ S.K);
-        const uint32_t he = (uint32_t)(he64 >> 32);
-        const uint64_t T = S.wic ? (uint64_t)S.tcsr[e] + S.toff : S.t32;  // R4 / R19
-        if (S.decor) {  // R20
-          if (T < (1ull << 32) && (pc_mix64(hrj ^ he64) >> 32) >= T) continue;
-        } else if ((uint64_t)(hr ^ he) >= T) {
-          continue;  // R3
-        }
-        uint32_t h = (w * 2654435761u) & (HCAP - 1);
-        for (;;) {
-          const uint32_t old = atomicCAS(hs + h, NONE, w);
-          if (old == NONE) {
-            const uint32_t pos = atomicAdd(tail, 1u);
-            if (pos < QCAP) q[pos] = w;
-            break;
+        for (int u = 0; u < WU; u++) {
+          const uint32_t t = c + 32 * u + lane;
+          uint32_t a = 0;  // the lane (vertex) owning pair t: largest a with pre[a] <= t
+#pragma unroll
+          for (int b = 16; b; b >>= 1) {
+            const uint32_t pa = __shfl_sync(FULL, pre, a + b);
+            if (pa <= t) a += b;
           }
-          if (old == w) break;
-          h = (h + 1) & (HCAP - 1);
+          xv[u] = __shfl_sync(FULL, x, a);
+          const uint64_t ea = __shfl_sync(FULL, e0, a);
+          const uint32_t pra = __shfl_sync(FULL, pre, a);
+          wv[u] = NONE;
+          tv[u] = S.t32;
+          if (t < total) {
+            const uint64_t e = ea + (t - pra);
+            wv[u] = S.nbr[e];
+            if (S.wic) tv[u] = (uint64_t)S.tcsr[e] + S.toff;  // R4 / R19
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < WU; u++) {
+          const uint32_t w = wv[u], xa = xv[u];
+          if (w == NONE) continue;
+          const uint64_t lo = xa < w ? xa : w, hi = xa < w ? w : xa;
+          const uint64_t he64 = pc_mix64(((lo << 32) | hi) ^ S.K);
+          const uint32_t he = (uint32_t)(he64 >> 32);
+          const uint64_t T = tv[u];
+          if (S.decor) {  // R20
+            if (T < (1ull << 32) && (pc_mix64(hrj ^ he64) >> 32) >= T) continue;
+          } else if ((uint64_t)(hr ^ he) >= T) {
+            continue;  // R3
+          }
+          uint32_t h = (w * 2654435761u) & (HCAP - 1);
+          for (;;) {
+            const uint32_t old = atomicCAS(hs + h, NONE, w);
+            if (old == NONE) {
+              const uint32_t pos = atomicAdd(tail, 1u);
+              if (pos < QCAP) q[pos] = w;
+              break;
+            }
+            if (old == w) break;
+            h = (h + 1) & (HCAP - 1);
+          }
         }
       }
       __syncwarp();
@@ -956,7 +974,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) k_select(Sel S0, SelOut O, uin
         const uint32_t small = __shfl_sync(0xffffffffu, lane == 0 ? __ldcg(S.dl + j) : 0u, 0);
         if (small) {
           bool done = false;
-          if (S.warp_ok && small <= QCAP)
+          if (S.warp_ok && small <= S.warp_max)
             done = warp_bfs(S, s, (uint32_t)j, small, wq, whs, wtail, shr);
           if (done) {
             nwarp++;
@@ -1191,6 +1209,8 @@ static Sel make_sel(pacim_ctx *ctx, long long *target) {
   // the store (tests force it down with PACIM_BIG_T)
   S.big_t = (uint32_t)env_u64("PACIM_BIG_T", std::max<uint64_t>(65536, nr / 8));
   S.warp_ok = getenv("PACIM_NO_WARP_BFS") == nullptr;
+  S.warp_max = (uint32_t)std::min<uint64_t>(
+      QCAP, getenv("PACIM_WARP_MAX") ? atoll(getenv("PACIM_WARP_MAX")) : QCAP);
   S.ch = (uint32_t)env_u64("PACIM_CHUNK", CH_DEFAULT);
   S.lkeep = (uint32_t)std::min<uint64_t>(16, getenv("PACIM_LKEEP") ? atoll(getenv("PACIM_LKEEP")) : 2);
   S.hidx = ctx->hidx.as<uint32_t>();
