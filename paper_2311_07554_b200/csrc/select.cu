@@ -792,6 +792,9 @@ __device__ void apply_dense(const Sel &S, uint32_t s, size_t warp0, size_t nwarp
     if (!__any_sync(0xffffffffu, any)) continue;
     for (size_t v0 = warp0 * DR; v0 < S.nr; v0 += nwarps * DR) {
       uint32_t x[DR][8];
+      // the rows' vertex ids, loaded with the slots (lane r: row v0 + r), so
+      // the per-row gain update does not wait on a dependent load
+      const uint32_t vids = (lane < DR && v0 + lane < S.nr) ? __ldg(S.rmap + v0 + lane) : NONE;
       if (S.onew) {  // one window (the default): the plain vertex-major address
 #pragma unroll
         for (int r = 0; r < DR; r++)
@@ -816,10 +819,10 @@ __device__ void apply_dense(const Sel &S, uint32_t s, size_t warp0, size_t nwarp
 #pragma unroll
         for (int i = 0; i < 8; i++)
           if (cr[i] != NONE && (x[r][i] == cr[i] || v == cr[i])) d += cd[i];
+        const uint32_t vid = __shfl_sync(0xffffffffu, vids, r);
         if (!__any_sync(0xffffffffu, d != 0)) continue;
         for (int q = 16; q; q >>= 1) d += __shfl_xor_sync(0xffffffffu, d, q);
         if (lane == 0 && d) {
-          const uint32_t vid = S.rmap[v];
           if (vid != s) {
             atomicAdd((unsigned long long *)&S.target[vid], (unsigned long long)(-d));
             S.dlst.add(vid, -d);
