@@ -40,20 +40,26 @@ constexpr uint32_t NONE = 0xFFFFFFFFu;
 __device__ __forceinline__ uint32_t ld_cg(const uint32_t *p) { return __ldcg(p); }
 
 // ---------------------------------------------------------------- k_init
+// A root slot holds HIGH | size (size 1 until k_compress_count counts the
+// members), a non-root slot its parent row: the union-find reads a HIGH value
+// as "parent = itself", and counting a member is a single atomicAdd.
+constexpr uint32_t ROOT1 = PACIM_HIGH | 1u;
+
 __global__ void k_init(uint32_t *L, uint32_t n, uint32_t B) {
   const int lane = threadIdx.x & 31;
   size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  // every slot starts as the root of a singleton: HIGH | 1 (R8 store form)
   if ((B & 3) == 0 && (reinterpret_cast<uintptr_t>(L) & 15) == 0) {
     const uint32_t B4 = B >> 2;
+    const uint4 x = make_uint4(ROOT1, ROOT1, ROOT1, ROOT1);
     for (size_t v = warp; v < n; v += nw) {
       uint4 *row = reinterpret_cast<uint4 *>(L + v * B);
-      uint4 x = make_uint4((uint32_t)v, (uint32_t)v, (uint32_t)v, (uint32_t)v);
       for (uint32_t j = lane; j < B4; j += 32) row[j] = x;
     }
   } else {
     for (size_t v = warp; v < n; v += nw)
-      for (uint32_t j = lane; j < B; j += 32) L[v * B + j] = (uint32_t)v;
+      for (uint32_t j = lane; j < B; j += 32) L[v * B + j] = ROOT1;
   }
 }
 
@@ -64,13 +70,15 @@ __global__ void k_init(uint32_t *L, uint32_t n, uint32_t B) {
 // splice the non-root's pointer over to the other side's (smaller) parent.
 // Parents stay strictly smaller than children, so the final root of every
 // CC is its minimum id (R8).  Two independent loads per step; the walk stops
-// as soon as the two paths meet.
+// as soon as the two paths meet.  A root slot holds ROOT1 (read as itself).
 __device__ __forceinline__ void uf_unite(uint32_t *L, uint32_t B, uint32_t j, uint32_t u,
                                          uint32_t v) {
   uint32_t *Lj = L + j;
   for (;;) {
     uint32_t pu = ld_cg(Lj + (size_t)u * B);
     uint32_t pv = ld_cg(Lj + (size_t)v * B);
+    if (pu & PACIM_HIGH) pu = u;
+    if (pv & PACIM_HIGH) pv = v;
     if (pu == pv) return;
     if (pu < pv) {
       uint32_t t = u;
@@ -82,7 +90,7 @@ __device__ __forceinline__ void uf_unite(uint32_t *L, uint32_t B, uint32_t j, ui
     }
     // now pu > pv
     if (u == pu) {
-      if (atomicCAS(Lj + (size_t)u * B, u, pv) == u) return;  // hook root u under pv
+      if (atomicCAS(Lj + (size_t)u * B, ROOT1, pv) == ROOT1) return;  // hook root u under pv
     } else {
       atomicCAS(Lj + (size_t)u * B, pu, pv);  // splice (may lose a race harmlessly)
       u = pu;
@@ -284,10 +292,8 @@ __global__ void k_hot_roots(const uint32_t *L, uint32_t nr, uint32_t B, uint32_t
 // and added once per block.  ctr[0] += CCs of size >= 2, ctr[1] += non-roots.
 __device__ __forceinline__ bool add_to_root(uint32_t *L, uint32_t B, uint32_t j, uint32_t root,
                                             uint32_t cnt) {
-  uint32_t *rs = L + (size_t)root * B + j;
-  if (!(ld_cg(rs) & PACIM_HIGH)) atomicCAS(rs, root, PACIM_HIGH | 1u);
-  uint32_t old = atomicAdd(rs, cnt);
-  return old == (PACIM_HIGH | 1u);  // the first add after conversion: a new CC
+  // the root slot is HIGH | size already (ROOT1 from k_init): one atomic
+  return atomicAdd(L + (size_t)root * B + j, cnt) == ROOT1;  // the first add: a new CC
 }
 
 __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n, uint32_t B,
@@ -311,13 +317,13 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
 #pragma unroll
       for (int i = 0; i < 8; i++) {
         uint32_t j = j0 + lane + 32 * i;
-        sv[i] = j < B ? ld_cg(L + v * B + j) : (uint32_t)v;
+        sv[i] = j < B ? ld_cg(L + v * B + j) : ROOT1;  // past B: skipped as a root
       }
 #pragma unroll
       for (int i = 0; i < 8; i++) {
         const uint32_t j = j0 + lane + 32 * i;
         const uint32_t s = sv[i];
-        if (s == (uint32_t)v || (s & PACIM_HIGH)) continue;  // root (or singleton)
+        if (s & PACIM_HIGH) continue;  // a root (of a singleton or not)
         // parent already the hot root: no walk (the common case for members
         // of the giant CC)
         uint32_t root = (j < H && s == hroot[j]) ? s : find_halve(L, B, j, s);
@@ -377,10 +383,8 @@ __global__ void __launch_bounds__(256) k_gain0(const uint32_t *__restrict__ L, u
         const uint32_t j = j0 + lane + 32 * i;
         const uint32_t s = sv[i];
         if (s == NONE) continue;
-        if (s == (uint32_t)v) {
-          g += 1;  // singleton CC
-        } else if (s & PACIM_HIGH) {
-          g += s & PACIM_LOW;
+        if (s & PACIM_HIGH) {
+          g += s & PACIM_LOW;  // a root (singleton: 1)
         } else {
           g += __ldg(L + (size_t)s * B + j) & PACIM_LOW;
         }
@@ -442,7 +446,7 @@ __global__ void __launch_bounds__(256) k_init_w(uint32_t *L, uint32_t nr, uint32
   for (size_t row0 = warp * wl.rpw; row0 < nr; row0 += nw * wl.rpw) {
     const size_t row = row0 + wl.r;
     if (!wl.act || row >= nr) continue;
-    for (uint32_t j = wl.jj; j < c; j += 32) L[row * c + j] = (uint32_t)row;
+    for (uint32_t j = wl.jj; j < c; j += 32) L[row * c + j] = ROOT1;
   }
 }
 
@@ -476,7 +480,7 @@ __global__ void __launch_bounds__(256) k_compress_w(uint32_t *L, uint32_t nr, ui
       for (int u = 0; u < WU; u++) {
         const size_t v = row0 + (size_t)u * wl.rpw + wl.r;
         const uint32_t s = sv[u];
-        if (s == NONE || s == (uint32_t)v || (s & PACIM_HIGH)) continue;  // root (or singleton)
+        if (s == NONE || (s & PACIM_HIGH)) continue;  // a root (of a singleton or not)
         const uint32_t root = (j < H && s == hroot[j]) ? s : find_halve(L, c, j, s);
         if (root != s) atomicMin(L + v * c + j, root);
         nnr++;
@@ -524,7 +528,7 @@ __global__ void __launch_bounds__(256) k_gain_w(const uint32_t *__restrict__ L, 
       for (int u = 0; u < WU; u++) {  // root sizes of the non-roots, in flight together
         const size_t v = row0 + (size_t)u * wl.rpw + wl.r;
         const uint32_t s = sv[u];
-        sz[u] = (s != NONE && s != (uint32_t)v && !(s & PACIM_HIGH))
+        sz[u] = (s != NONE && !(s & PACIM_HIGH))
                     ? (__ldg(L + (size_t)s * c + j) & PACIM_LOW) : 0u;
       }
 #pragma unroll
@@ -532,7 +536,7 @@ __global__ void __launch_bounds__(256) k_gain_w(const uint32_t *__restrict__ L, 
         const size_t v = row0 + (size_t)u * wl.rpw + wl.r;
         const uint32_t s = sv[u];
         if (s == NONE) continue;
-        const uint32_t size = s == (uint32_t)v ? 1u : (s & PACIM_HIGH) ? (s & PACIM_LOW) : sz[u];
+        const uint32_t size = (s & PACIM_HIGH) ? (s & PACIM_LOW) : sz[u];
         g[u] += acc ? (long long)size - 1 : (long long)size;
       }
     }

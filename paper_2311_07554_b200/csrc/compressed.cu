@@ -67,7 +67,7 @@ __global__ void k_gain_sizes(const uint32_t *Lb, uint32_t nr, uint32_t Bb, const
     long long g = 0;
     for (uint32_t j = lane; j < Bb; j += 32) {
       uint32_t s = Lb[v * Bb + j];
-      if (s == (uint32_t)v) continue;  // singleton: size 1, already counted
+      if (s == (PACIM_HIGH | 1u)) continue;  // singleton: size 1, already counted
       uint32_t sz = (s & PACIM_HIGH) ? (s & PACIM_LOW) : (Lb[(size_t)s * Bb + j] & PACIM_LOW);
       g += (long long)sz - 1;
     }
@@ -88,10 +88,12 @@ __global__ void k_center_a(const uint32_t *Lb, uint32_t Bb, uint32_t rho, const 
     uint32_t root = NONE, size = 1;
     if (r != NONE) {
       const uint32_t s = Lb[(size_t)r * Bb + jj];
-      if (s & PACIM_HIGH) {
+      if (s == (PACIM_HIGH | 1u)) {
+        // a singleton: no root (label = the center's own index)
+      } else if (s & PACIM_HIGH) {
         root = r;
         size = s & PACIM_LOW;
-      } else if (s != r) {
+      } else {
         root = s;
         size = Lb[(size_t)s * Bb + jj] & PACIM_LOW;
       }

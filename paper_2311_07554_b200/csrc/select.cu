@@ -276,7 +276,7 @@ __device__ __forceinline__ uint32_t cover_slot(const Sel &S, uint32_t srow, uint
   S.cov_root[j] = NONE;
   if (srow == NONE) return delta;  // isolated seed: singleton in every sketch
   const uint32_t sl = S.L[S.onew ? (size_t)srow * S.B + j : pc_addr(S.smap, S.nr, srow, j)];
-  if (sl == srow) return delta;    // singleton {s}
+  if (sl == (PACIM_HIGH | 1u)) return delta;  // singleton {s} (root of size 1)
   const uint32_t root = (sl & PACIM_HIGH) ? srow : sl;
   const size_t ra = S.onew ? (size_t)root * S.B + j : pc_addr(S.smap, S.nr, root, j);
   uint32_t *rs = S.L + ra;
@@ -1106,7 +1106,7 @@ __global__ void k_lazy_eval(Sel S, const uint32_t *cand, uint32_t b0, uint32_t b
       for (uint32_t j = lane; j < S.B; j += 32) {
         const uint32_t sv = __ldcg(S.L + pc_addr(S.smap, S.nr, row, j));
         uint32_t rv;
-        if (sv == row) {
+        if (sv == (PACIM_HIGH | 1u)) {
           g += 1;  // {v}: never covered while v is not a seed
           continue;
         }
@@ -1125,7 +1125,7 @@ __global__ void k_lazy_mark(Sel S, uint32_t s) {
   if (srow == NONE) return;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < S.B; j += gridDim.x * blockDim.x) {
     const uint32_t sl = S.L[S.onew ? (size_t)srow * S.B + j : pc_addr(S.smap, S.nr, srow, j)];
-    if (sl == srow) continue;
+    if (sl == (PACIM_HIGH | 1u)) continue;  // singleton
     const uint32_t root = (sl & PACIM_HIGH) ? srow : sl;
     const size_t ra = S.onew ? (size_t)root * S.B + j : pc_addr(S.smap, S.nr, root, j);
     const uint32_t x = atomicOr(S.L + ra, COV);
