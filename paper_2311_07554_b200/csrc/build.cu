@@ -289,11 +289,19 @@ __global__ void k_hot_roots(const uint32_t *L, uint32_t nr, uint32_t B, uint32_t
 // the owner's write are atomicMin, so the final slot is the root); the
 // root slot becomes HIGH | size by CAS(root -> HIGH|1) then atomicAdd per
 // member (H5).  Members of the slot's hot root are counted in shared memory
-// and added once per block.  ctr[0] += CCs of size >= 2, ctr[1] += non-roots.
-__device__ __forceinline__ bool add_to_root(uint32_t *L, uint32_t B, uint32_t j, uint32_t root,
+// and added once per block.  ctr[1] += non-roots (the CCs of size >= 2 are
+// counted into ctr[0] by the gain pass that reads every root slot anyway).
+__device__ __forceinline__ void add_to_root(uint32_t *L, uint32_t B, uint32_t j, uint32_t root,
                                             uint32_t cnt) {
-  // the root slot is HIGH | size already (ROOT1 from k_init): one atomic
-  return atomicAdd(L + (size_t)root * B + j, cnt) == ROOT1;  // the first add: a new CC
+  // the root slot is HIGH | size already (ROOT1 from k_init): one atomic whose
+  // result is not waited for (the CCs are counted by the gain pass)
+  atomicAdd(L + (size_t)root * B + j, cnt);
+}
+
+// warp-reduced counter update (lane 0 adds)
+__device__ __forceinline__ void add_count(unsigned long long *ctr, unsigned long long c) {
+  for (int d = 16; d; d >>= 1) c += __shfl_xor_sync(0xffffffffu, c, d);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(ctr, c);
 }
 
 __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n, uint32_t B,
@@ -310,7 +318,7 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
   const int lane = threadIdx.x & 31;
   size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long ncc = 0, nnr = 0;
+  unsigned long long nnr = 0;
   for (size_t v = warp; v < n; v += nw) {
     for (uint32_t j0 = 0; j0 < B; j0 += 256) {
       uint32_t sv[8];  // prefetch up to 8 slots per lane (independent loads)
@@ -329,33 +337,23 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
         uint32_t root = (j < H && s == hroot[j]) ? s : find_halve(L, B, j, s);
         if (root != s) atomicMin(L + v * B + j, root);
         nnr++;
-        if (j < H && root == hroot[j]) {
+        if (j < H && root == hroot[j])
           atomicAdd(hcnt + j, 1u);
-        } else if (add_to_root(L, B, j, root, 1u)) {
-          ncc++;
-        }
+        else
+          add_to_root(L, B, j, root, 1u);
       }
     }
   }
   __syncthreads();
   for (uint32_t j = threadIdx.x; j < H; j += blockDim.x)
-    if (hcnt[j] && add_to_root(L, B, j, hroot[j], hcnt[j])) ncc++;
-  for (int d = 16; d; d >>= 1) {
-    ncc += __shfl_xor_sync(0xffffffffu, ncc, d);
-    nnr += __shfl_xor_sync(0xffffffffu, nnr, d);
-  }
-  __shared__ unsigned long long s0, s1;
-  if (threadIdx.x == 0) s0 = s1 = 0;
+    if (hcnt[j]) add_to_root(L, B, j, hroot[j], hcnt[j]);
+  for (int d = 16; d; d >>= 1) nnr += __shfl_xor_sync(0xffffffffu, nnr, d);
+  __shared__ unsigned long long s1;
+  if (threadIdx.x == 0) s1 = 0;
   __syncthreads();
-  if (lane == 0) {
-    if (ncc) atomicAdd(&s0, ncc);
-    if (nnr) atomicAdd(&s1, nnr);
-  }
+  if (lane == 0 && nnr) atomicAdd(&s1, nnr);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    if (s0) atomicAdd(ctr + 0, s0);
-    if (s1) atomicAdd(ctr + 1, s1);
-  }
+  if (threadIdx.x == 0 && s1) atomicAdd(ctr + 1, s1);
 }
 
 // ---------------------------------------------------------------- k_gain0
@@ -365,7 +363,8 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
 // slots (gain0 starts at B); else gain0[v] = the sum over all B slots
 __global__ void __launch_bounds__(256) k_gain0(const uint32_t *__restrict__ L, uint32_t n,
                                                uint32_t B, const uint32_t *rmap, int64_t *gain0,
-                                               int acc) {
+                                               int acc, unsigned long long *ncc_ctr) {
+  unsigned long long ncc = 0;  // roots of size >= 2: the non-singleton CCs
   const int lane = threadIdx.x & 31;
   size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
@@ -385,6 +384,7 @@ __global__ void __launch_bounds__(256) k_gain0(const uint32_t *__restrict__ L, u
         if (s == NONE) continue;
         if (s & PACIM_HIGH) {
           g += s & PACIM_LOW;  // a root (singleton: 1)
+          ncc += (s & PACIM_LOW) >= 2;
         } else {
           g += __ldg(L + (size_t)s * B + j) & PACIM_LOW;
         }
@@ -399,6 +399,7 @@ __global__ void __launch_bounds__(256) k_gain0(const uint32_t *__restrict__ L, u
       }
     }
   }
+  add_count(ncc_ctr, ncc);
 }
 
 // HLA: entries sorted by key -> rows, and the segment offsets: off[q] = the
@@ -466,7 +467,7 @@ __global__ void __launch_bounds__(256) k_compress_w(uint32_t *L, uint32_t nr, ui
   const WLanes wl(c);
   const size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
-  unsigned long long ncc = 0, nnr = 0;
+  unsigned long long nnr = 0;
   const size_t step = (size_t)wl.rpw * WU;
   for (size_t row0 = warp * step; row0 < nr; row0 += nw * step) {
     for (uint32_t j = wl.jj; j < c; j += 32) {
@@ -485,21 +486,14 @@ __global__ void __launch_bounds__(256) k_compress_w(uint32_t *L, uint32_t nr, ui
         if (root != s) atomicMin(L + v * c + j, root);
         nnr++;
         if (j < H && root == hroot[j]) atomicAdd(hcnt + j, 1u);
-        else if (add_to_root(L, c, j, root, 1u)) ncc++;
+        else add_to_root(L, c, j, root, 1u);
       }
     }
   }
   __syncthreads();
   for (uint32_t j = threadIdx.x; j < H; j += blockDim.x)
-    if (hcnt[j] && add_to_root(L, c, j, hroot[j], hcnt[j])) ncc++;
-  for (int d = 16; d; d >>= 1) {
-    ncc += __shfl_xor_sync(0xffffffffu, ncc, d);
-    nnr += __shfl_xor_sync(0xffffffffu, nnr, d);
-  }
-  if ((threadIdx.x & 31) == 0) {
-    if (ncc) atomicAdd(ctr + 0, ncc);
-    if (nnr) atomicAdd(ctr + 1, nnr);
-  }
+    if (hcnt[j]) add_to_root(L, c, j, hroot[j], hcnt[j]);
+  add_count(ctr + 1, nnr);
 }
 
 // gain0 over a narrow window: acc ? gain0[v] += sum (|C| - 1) (gain0 starts
@@ -507,7 +501,8 @@ __global__ void __launch_bounds__(256) k_compress_w(uint32_t *L, uint32_t nr, ui
 // row are consecutive: segmented sum by shuffles; WU row groups in flight
 __global__ void __launch_bounds__(256) k_gain_w(const uint32_t *__restrict__ L, uint32_t nr,
                                                 uint32_t c, const uint32_t *rmap, int64_t *gain0,
-                                                int acc) {
+                                                int acc, unsigned long long *ncc_ctr) {
+  unsigned long long ncc = 0;  // roots of size >= 2: the non-singleton CCs
   const WLanes wl(c);
   const size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
@@ -537,6 +532,7 @@ __global__ void __launch_bounds__(256) k_gain_w(const uint32_t *__restrict__ L, 
         const uint32_t s = sv[u];
         if (s == NONE) continue;
         const uint32_t size = (s & PACIM_HIGH) ? (s & PACIM_LOW) : sz[u];
+        ncc += (s & PACIM_HIGH) && size >= 2;
         g[u] += acc ? (long long)size - 1 : (long long)size;
       }
     }
@@ -557,6 +553,7 @@ __global__ void __launch_bounds__(256) k_gain_w(const uint32_t *__restrict__ L, 
       }
     }
   }
+  add_count(ncc_ctr, ncc);
 }
 
 // ------------------------------------------------------ edge partition
@@ -737,7 +734,8 @@ void pc_hla_finish(pacim_ctx *ctx, Hla *hla) {
 }
 
 // Lb (rows x Bb), unions, full compression and CC sizes (root slot HIGH|size).
-// ctr[0] += non-singleton CCs, ctr[1] += non-roots, ctr[4] += live pairs.
+// ctr[1] += non-roots, ctr[4] += live pairs (ctr[0], the non-singleton CCs:
+// the gain pass that follows).
 // ev (optional, 3 events) is recorded after init, edges and compress.
 void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
                     unsigned long long *ctr, cudaEvent_t *ev, const Hla *hla_in,
@@ -947,10 +945,10 @@ void pc_build(pacim_ctx *ctx) {
     // CC sizes of the window into gain0 while it is still cached
     if (c < NARROW_W)
       k_gain_w<<<pc_grid(ctx, (size_t)n * c, 256, 16), 256, 0, ctx->stream>>>(
-          Lw, n, c, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>(), nwin > 1);
+          Lw, n, c, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>(), nwin > 1, ctr);
     else
       k_gain0<<<rows_grid, 256, 0, ctx->stream>>>(Lw, n, c, ctx->rmap.as<uint32_t>(),
-                                                 ctx->gain0.as<int64_t>(), nwin > 1);
+                                                 ctx->gain0.as<int64_t>(), nwin > 1, ctr);
     PC_CHECK_LAUNCH();
     ctx->launches++;
   }

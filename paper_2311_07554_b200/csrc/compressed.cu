@@ -59,7 +59,8 @@ __global__ void k_center_index(const uint64_t *flag, const uint64_t *pos, uint32
 // ------------------------------------------------------- batch outputs
 // gain0[v] += sum over the batch's slots of (|C_j(v)| - 1) (gain0 starts at B)
 __global__ void k_gain_sizes(const uint32_t *Lb, uint32_t nr, uint32_t Bb, const uint32_t *rmap,
-                             int64_t *gain0) {
+                             int64_t *gain0, unsigned long long *ncc_ctr) {
+  unsigned long long ncc = 0;  // roots of size >= 2: the non-singleton CCs
   const int lane = threadIdx.x & 31;
   size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
@@ -68,12 +69,15 @@ __global__ void k_gain_sizes(const uint32_t *Lb, uint32_t nr, uint32_t Bb, const
     for (uint32_t j = lane; j < Bb; j += 32) {
       uint32_t s = Lb[v * Bb + j];
       if (s == (PACIM_HIGH | 1u)) continue;  // singleton: size 1, already counted
+      ncc += (s & PACIM_HIGH) != 0;
       uint32_t sz = (s & PACIM_HIGH) ? (s & PACIM_LOW) : (Lb[(size_t)s * Bb + j] & PACIM_LOW);
       g += (long long)sz - 1;
     }
     for (int d = 16; d; d >>= 1) g += __shfl_xor_sync(0xffffffffu, g, d);
     if (lane == 0 && g) gain0[rmap[v]] += g;
   }
+  for (int d = 16; d; d >>= 1) ncc += __shfl_xor_sync(0xffffffffu, ncc, d);
+  if (lane == 0 && ncc) atomicAdd(ncc_ctr, ncc);
 }
 
 // center i, batch slot jj: its CC's root row (NONE: singleton) and CC size
@@ -576,7 +580,7 @@ void pc_build_compressed(pacim_ctx *ctx) {
     const uint32_t bb = std::min(Bb, B - j0);
     pc_sketch_pass(ctx, Lb, j0, bb, ctr, nullptr, rec_hla ? &hla : nullptr);
     k_gain_sizes<<<pc_grid(ctx, (size_t)nr * 32, 256, 16), 256, 0, ctx->stream>>>(
-        Lb, nr, bb, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>());
+        Lb, nr, bb, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>(), ctr);
     PC_CHECK_LAUNCH();
     const size_t tot = (size_t)rho * bb;
     if (tot) {
