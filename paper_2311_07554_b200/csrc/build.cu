@@ -361,6 +361,7 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
 // (H7), the CC size read from the root slot (HIGH | size).
 // acc: window of a multi-window store, gain0[v] += sum (|C| - 1) over its
 // slots (gain0 starts at B); else gain0[v] = the sum over all B slots
+constexpr int GR = 4;  // rows per warp iteration in k_gain0 (4 KB of slots in flight)
 __global__ void __launch_bounds__(256) k_gain0(const uint32_t *__restrict__ L, uint32_t n,
                                                uint32_t B, const uint32_t *rmap, int64_t *gain0,
                                                int acc, unsigned long long *ncc_ctr) {
@@ -368,34 +369,49 @@ __global__ void __launch_bounds__(256) k_gain0(const uint32_t *__restrict__ L, u
   const int lane = threadIdx.x & 31;
   size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
-  for (size_t v = warp; v < n; v += nw) {
-    long long g = 0;
+  for (size_t v0 = warp * GR; v0 < n; v0 += nw * GR) {
+    long long g[GR];
+#pragma unroll
+    for (int r = 0; r < GR; r++) g[r] = 0;
     for (uint32_t j0 = 0; j0 < B; j0 += 256) {
-      uint32_t sv[8];
+      uint32_t sv[GR][8];
 #pragma unroll
-      for (int i = 0; i < 8; i++) {
-        uint32_t j = j0 + lane + 32 * i;
-        sv[i] = j < B ? L[v * B + j] : NONE;
-      }
+      for (int r = 0; r < GR; r++)
 #pragma unroll
-      for (int i = 0; i < 8; i++) {
-        const uint32_t j = j0 + lane + 32 * i;
-        const uint32_t s = sv[i];
-        if (s == NONE) continue;
-        if (s & PACIM_HIGH) {
-          g += s & PACIM_LOW;  // a root (singleton: 1)
-          ncc += (s & PACIM_LOW) >= 2;
-        } else {
-          g += __ldg(L + (size_t)s * B + j) & PACIM_LOW;
+        for (int i = 0; i < 8; i++) {
+          const uint32_t j = j0 + lane + 32 * i;
+          sv[r][i] = (j < B && v0 + r < n) ? L[(v0 + r) * B + j] : NONE;
         }
-      }
+      // a non-root slot becomes its root's HIGH | size: the root loads of
+      // both rows in flight together
+#pragma unroll
+      for (int r = 0; r < GR; r++)
+#pragma unroll
+        for (int i = 0; i < 8; i++) {
+          const uint32_t j = j0 + lane + 32 * i;
+          const uint32_t s = sv[r][i];
+          if (s == NONE) continue;
+          if (s & PACIM_HIGH)
+            ncc += (s & PACIM_LOW) >= 2;
+          else
+            sv[r][i] = __ldg(L + (size_t)s * B + j);
+        }
+#pragma unroll
+      for (int r = 0; r < GR; r++)
+#pragma unroll
+        for (int i = 0; i < 8; i++)
+          if (sv[r][i] != NONE) g[r] += sv[r][i] & PACIM_LOW;
     }
-    for (int d = 16; d; d >>= 1) g += __shfl_xor_sync(0xffffffffu, g, d);
-    if (lane == 0) {
-      if (acc) {
-        if (g != (long long)B) gain0[rmap[v]] += g - (long long)B;
-      } else {
-        gain0[rmap[v]] = g;
+#pragma unroll
+    for (int r = 0; r < GR; r++) {
+      long long t = g[r];
+      for (int d = 16; d; d >>= 1) t += __shfl_xor_sync(0xffffffffu, t, d);
+      if (lane == 0 && v0 + r < n) {
+        if (acc) {
+          if (t != (long long)B) gain0[rmap[v0 + r]] += t - (long long)B;
+        } else {
+          gain0[rmap[v0 + r]] = t;
+        }
       }
     }
   }
