@@ -304,10 +304,14 @@ __device__ __forceinline__ void add_count(unsigned long long *ctr, unsigned long
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(ctr, c);
 }
 
+constexpr uint32_t CLCAP = 256 + 31;  // pending finds per warp: < 32 carried + one 256-slot block
+template <bool COMPACT>
 __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n, uint32_t B,
                                                         const uint32_t *hot,
                                                         unsigned long long *ctr) {
   extern __shared__ uint32_t hsm[];
+  __shared__ uint32_t cl_v[COMPACT ? 8 : 1][COMPACT ? CLCAP : 1],
+      cl_j[COMPACT ? 8 : 1][COMPACT ? CLCAP : 1], cl_s[COMPACT ? 8 : 1][COMPACT ? CLCAP : 1];
   const uint32_t H = min(B, HOT_MAX);
   uint32_t *hroot = hsm, *hcnt = hsm + H;
   for (uint32_t j = threadIdx.x; j < H; j += blockDim.x) {
@@ -319,6 +323,31 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
   size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long nnr = 0;
+  // the non-root slots that need a find, compacted per warp (over rows until
+  // >= 32 are pending) so that each lane walks one chain per round: a row's
+  // cost is its longest chain, not the sum over the 8 slots a lane holds
+  // (c2 compress 1.05 -> 0.79 ms, c4 21.6 -> 19.7 ms; dense stores keep the
+  // per-lane walk: on c3 compaction cost 18 -> 24 ms)
+  const int wib = COMPACT ? threadIdx.x >> 5 : 0;
+  uint32_t *cv = cl_v[wib], *cj = cl_j[wib], *cs = cl_s[wib];
+  uint32_t cnt = 0;  // warp-uniform
+  auto flush = [&]() {
+    __syncwarp();
+    for (uint32_t base = 0; base < cnt; base += 32) {
+      const uint32_t k = base + lane;
+      if (k < cnt) {
+        const uint32_t v = cv[k], j = cj[k], s = cs[k];
+        const uint32_t root = find_halve(L, B, j, s);
+        if (root != s) atomicMin(L + (size_t)v * B + j, root);
+        if (j < H && root == hroot[j])
+          atomicAdd(hcnt + j, 1u);
+        else
+          add_to_root(L, B, j, root, 1u);
+      }
+    }
+    __syncwarp();
+    cnt = 0;
+  };
   for (size_t v = warp; v < n; v += nw) {
     for (uint32_t j0 = 0; j0 < B; j0 += 256) {
       uint32_t sv[8];  // prefetch up to 8 slots per lane (independent loads)
@@ -331,19 +360,37 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
       for (int i = 0; i < 8; i++) {
         const uint32_t j = j0 + lane + 32 * i;
         const uint32_t s = sv[i];
-        if (s & PACIM_HIGH) continue;  // a root (of a singleton or not)
+        const bool nonroot = !(s & PACIM_HIGH);
         // parent already the hot root: no walk (the common case for members
         // of the giant CC)
-        uint32_t root = (j < H && s == hroot[j]) ? s : find_halve(L, B, j, s);
-        if (root != s) atomicMin(L + v * B + j, root);
-        nnr++;
-        if (j < H && root == hroot[j])
-          atomicAdd(hcnt + j, 1u);
-        else
-          add_to_root(L, B, j, root, 1u);
+        const bool hotp = nonroot && j < H && s == hroot[j];
+        if (hotp) atomicAdd(hcnt + j, 1u);
+        nnr += nonroot;
+        const bool need = nonroot && !hotp;
+        if (!COMPACT) {  // dense stores (c3): each lane walks its slots' chains in turn
+          if (need) {
+            const uint32_t root = find_halve(L, B, j, s);
+            if (root != s) atomicMin(L + v * B + j, root);
+            if (j < H && root == hroot[j])
+              atomicAdd(hcnt + j, 1u);
+            else
+              add_to_root(L, B, j, root, 1u);
+          }
+          continue;
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, need);
+        if (need) {
+          const uint32_t pos = cnt + __popc(m & ((1u << lane) - 1));
+          cv[pos] = (uint32_t)v;
+          cj[pos] = j;
+          cs[pos] = s;
+        }
+        cnt += __popc(m);
       }
+      if (COMPACT && cnt >= 32) flush();
     }
   }
+  if (COMPACT) flush();
   __syncthreads();
   for (uint32_t j = threadIdx.x; j < H; j += blockDim.x)
     if (hcnt[j]) add_to_root(L, B, j, hroot[j], hcnt[j]);
@@ -817,8 +864,21 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
   if (narrow)
     k_compress_w<<<wgrid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(Lb, n, Bb, hot_root, ctr);
   else
-    k_compress_count<<<rows_grid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(Lb, n, Bb,
-                                                                                hot_root, ctr);
+  {
+    // compacted finds unless the store is dense in non-roots: expected live
+    // (row, slot) pairs per row 2 m p / rows >= 1.5 (c3: 2.3; c2: 0.84; WIC:
+    // small p on most edges)
+    double p = (double)ctx->t32 / 4294967296.0;
+    if (ctx->pmodel == PACIM_P_UNIFORM)
+      p = 0.5 * ((double)(ctx->t32 >> 32) + (double)(ctx->t32 & 0xFFFFFFFFull)) / 4294967296.0;
+    const bool dense = ctx->pmodel != PACIM_P_WIC && 2.0 * ctx->m * p >= 1.5 * std::max(n, 1u);
+    if (dense)
+      k_compress_count<false><<<rows_grid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(
+          Lb, n, Bb, hot_root, ctr);
+    else
+      k_compress_count<true><<<rows_grid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(
+          Lb, n, Bb, hot_root, ctr);
+  }
   PC_CHECK_LAUNCH();
   if (ev) PC_CUDA(cudaEventRecord(ev[2], ctx->stream));
   ctx->launches += 4;
