@@ -51,7 +51,7 @@ def main(rep, out_md, cfg):
         f.write("\n".join(lines) + "\n")
     tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "traffic.json")
     allt = json.load(open(tp)) if os.path.exists(tp) else {}
-    allt[cfg] = traffic
+    allt.setdefault(cfg, {}).update(traffic)  # merge: a capture of some kernels keeps the others
     json.dump(allt, open(tp, "w"), indent=1)
     print("\n".join(lines))
 
