@@ -961,7 +961,9 @@ void pc_build(pacim_ctx *ctx) {
   const bool rec_hla = want_hla && pc_hla_begin(ctx, &hla, 1e30);
   const uint32_t W = plan_windows(ctx);
   const uint32_t nwin = (uint32_t)ctx->win_first.size() - 1;
-  {  // per-slot window table (select / labels address the store through it)
+  if (ctx->smap_of != ctx->win_first || ctx->d_smap.bytes < (size_t)B * 4) {
+    // per-slot window table (select / labels address the store through it);
+    // rebuilt only when the windows change (one window [0, B) by default)
     pc_ensure(ctx, ctx->d_smap, (size_t)B * 4);
     TmpBuf wf(ctx);
     pc_ensure(ctx, wf, ctx->win_first.size() * 4);
@@ -971,6 +973,7 @@ void pc_build(pacim_ctx *ctx) {
                                                                          ctx->d_smap.as<uint32_t>());
     PC_CHECK_LAUNCH();
     PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->smap_of = ctx->win_first;
   }
   // events: start, then per window init / edges / compress / gain done
   std::vector<cudaEvent_t> ev(2 + 4 * (size_t)nwin);

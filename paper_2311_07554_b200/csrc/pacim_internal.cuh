@@ -177,6 +177,7 @@ struct pacim_ctx {
   DevBuf L;
   std::vector<uint32_t> win_first;  // window starts, + B at the end
   DevBuf d_smap;
+  std::vector<uint32_t> smap_of;   // the windows d_smap was filled for
   DevBuf pkeys;          // per-build edge partition by bucket: keys, ckeys, counts
   uint64_t ncomp = 0, nmember = 0, nnonsingle = 0;
   uint32_t big_t = 0;
