@@ -257,10 +257,10 @@ def main():
     e0.record(stream)
     for _ in range(args.steps):
         out = step()
-        st = ctx.pacim_get_stats()
+        st = ctx.stats_raw()  # the struct's fields, no dict: little host time between steps
         for kk in keys:
-            acc[kk] += st[kk]
-        launches += st["kernel_launches_build"] + (st["kernel_launches_select"] if world == 1 else 0)
+            acc[kk] += getattr(st, kk)
+        launches += st.kernel_launches_build + (st.kernel_launches_select if world == 1 else 0)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     barrier()

@@ -277,6 +277,10 @@ class Context:
         return lab[:rho], sz[:rho]
 
     def pacim_get_stats(self) -> dict:
+        return self.stats_raw().asdict()
+
+    def stats_raw(self) -> "Stats":
+        """pacim_get_stats into the ctypes struct itself (no dict): for timed loops."""
         s = Stats()
         self._check(self._L.pacim_get_stats(self._h, C.byref(s)))
-        return s.asdict()
+        return s
