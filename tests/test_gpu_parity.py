@@ -207,6 +207,42 @@ def test_load_derivation_shapes(orc, ctx, p):
     full_parity(orc, ctx, Graph(40, off, nbr), model, t32, 5, 78, 4)
 
 
+@pytest.mark.parametrize("big_t", [None, "8"])
+@pytest.mark.parametrize("R,p", [(1000, 0.02), (1023, 0.1), (520, "wic")])
+def test_many_sketches(orc, ctx, R, p, big_t, monkeypatch):
+    """R above 256 on one GPU (several 256-slot blocks per store row, up to
+    1024 slots, odd counts): labels of sampled sketches, gain0 and the greedy
+    equal the oracle's, also with the dense pass forced."""
+    from oracle.oracle import Graph
+    if big_t:
+        monkeypatch.setenv("PACIM_BIG_T", big_t)
+    off, nbr = inputs.random_powerlaw_graph(600, 2400, 31)
+    g = Graph(600, off, nbr)
+    model, t32 = model_of(orc, p)
+    load_host(ctx, g, model, t32)
+    ctx.pacim_build_sketches(R, 41)
+    s, gn, sg, _ = ctx.pacim_select_seeds(12)
+    es, egn, esg, eg0 = orc.greedy(g, model, t32, R, 41, 12, want_gain0=True)
+    assert np.array_equal(ctx.pacim_get_gain0(), eg0)
+    for r in (0, R // 2, R - 1):
+        lab, _ = orc.sketch_labels(g, model, t32, 41, r)
+        assert np.array_equal(ctx.pacim_get_labels(r), lab), r
+    assert list(s) == list(es) and list(gn) == list(egn) and list(sg) == list(esg)
+
+
+def test_too_many_sketches_fail_cleanly(ctx, pc):
+    """More local sketches than the selection supports: an error, never a
+    wrong answer."""
+    off, nbr = inputs.random_graph(100, 300, 3)
+    ctx.pacim_load_graph(off, nbr, 0, 1 << 30, 1)
+    try:
+        ctx.pacim_build_sketches(2048, 1)
+        ctx.pacim_select_seeds(3)
+    except pc.PacimError:
+        return
+    raise AssertionError("R = 2048 on one GPU must be rejected")
+
+
 def test_determinism(orc, ctx):
     from oracle.oracle import Graph
     off, nbr = inputs.random_powerlaw_graph(3000, 20000, 11)
