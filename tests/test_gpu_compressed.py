@@ -203,3 +203,22 @@ def test_compressed_no_hla_star(orc, ctx, monkeypatch):
     run_case(orc, ctx, 8)
     st = ctx.pacim_get_stats()
     assert st["hubs"] == 1 and st["hla_entries"] == 0
+
+
+@pytest.mark.parametrize("batch", [None, "100"])
+def test_compressed_many_sketches(orc, ctx, batch, monkeypatch):
+    """Compressed store with R = 700 (probe warps over many slots, several
+    build batches when PACIM_BATCH = 100): the oracle's greedy and gain0."""
+    from oracle.oracle import Graph
+    if batch:
+        monkeypatch.setenv("PACIM_BATCH", batch)
+    off, nbr = inputs.random_powerlaw_graph(800, 3200, 61)
+    g = Graph(800, off, nbr)
+    t32 = orc.t32_const(0.08)
+    ctx.pacim_load_graph(g.off, g.nbr, 0, t32, 2)
+    ctx.pacim_build_sketches(700, 62, 1 << 29)
+    assert ctx.pacim_get_stats()["compressed"] == 1
+    s, gn, sg, _ = ctx.pacim_select_seeds(10)
+    es, egn, esg, eg0 = orc.greedy(g, 0, t32, 700, 62, 10, want_gain0=True)
+    assert np.array_equal(ctx.pacim_get_gain0(), eg0)
+    assert list(s) == list(es) and list(gn) == list(egn) and list(sg) == list(esg)
