@@ -204,6 +204,8 @@ def main():
     ap.add_argument("--ref-sketches", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--force-dist", action="store_true",
+                    help="testing: NCCL process group and the per-step collectives even at one rank")
     args = ap.parse_args()
     cfg = inputs.config(args.config, **({"scale": args.scale} if args.scale else {}))
     if args.alpha is not None:
@@ -218,7 +220,8 @@ def main():
     import torch
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    use_dist = world > 1 or args.force_dist
+    if use_dist:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     import paper_2311_07554_b200 as P
@@ -232,12 +235,12 @@ def main():
     R = cfg["R"]
 
     def barrier():
-        if world > 1:
+        if use_dist:
             torch.distributed.barrier()
 
     def step():
         ctx.pacim_build_sketches(R, cfg["hash_seed"], a32, rank, world)
-        if world == 1:
+        if not use_dist:
             return ctx.pacim_select_seeds(k)
         return pdist.distributed_select(ctx, n, k, dev)
 
@@ -360,7 +363,7 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()
-    if world > 1:
+    if use_dist:
         torch.distributed.destroy_process_group()
 
 
