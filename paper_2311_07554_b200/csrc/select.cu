@@ -1038,9 +1038,23 @@ __global__ void __launch_bounds__(SEL_THREADS) k_argmax_part(const long long *ga
                                                              Best *partial) {
   __shared__ Best sh[33];
   Best b{LLONG_MIN, 0xFFFFFFFFu};
-  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
-       v += (size_t)gridDim.x * blockDim.x) {
-    long long g = gain[v];
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // 8 independent streaming loads in flight per thread (one at a time left the
+  // scan at half of HBM bandwidth: 0.17 ms for c4's 67M gains)
+  for (; v + 7 * stride < n; v += 8 * stride) {
+    long long g[8];
+#pragma unroll
+    for (int u = 0; u < 8; u++) g[u] = __ldcs(gain + v + u * stride);
+#pragma unroll
+    for (int u = 0; u < 8; u++)
+      if (better(g[u], (uint32_t)(v + u * stride), b.g, b.v)) {
+        b.g = g[u];
+        b.v = (uint32_t)(v + u * stride);
+      }
+  }
+  for (; v < n; v += stride) {
+    const long long g = __ldcs(gain + v);
     if (better(g, (uint32_t)v, b.g, b.v)) {
       b.g = g;
       b.v = (uint32_t)v;
@@ -1480,7 +1494,7 @@ void pc_cover_local(pacim_ctx *ctx, uint32_t s, int64_t *d_delta, int64_t *local
 }
 
 void pc_argmax(pacim_ctx *ctx, const int64_t *d_gain, uint32_t n, uint32_t *s, int64_t *g) {
-  unsigned grid = pc_grid(ctx, n, SEL_THREADS, 2);
+  unsigned grid = pc_grid(ctx, n, SEL_THREADS, 4);
   DevBuf &part = ctx->argmax_part;  // persistent: no allocation per step
   pc_ensure(ctx, part, (size_t)(grid + 1) * sizeof(Best));
   k_argmax_part<<<grid, SEL_THREADS, 0, ctx->stream>>>(reinterpret_cast<const long long *>(d_gain),
