@@ -200,7 +200,7 @@ def main():
     ap.add_argument("--scale", type=int, default=None,
                     help="override the R-MAT scale (c5 at full scale needs 8 GPUs)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--ref-sketches", type=int, default=2)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -284,19 +284,46 @@ def main():
     h_nbr = torch.from_numpy(nbr).pin_memory()
     off_np, nbr_np = h_off.numpy(), h_nbr.numpy()
 
-    def e2e_step():
-        ctx.pacim_load_graph(off_np, nbr_np, pm, t32, 0)
-        return step()
-
-    e2e_step()
+    # Pipelined through the public API: step i+1's host CSR is enqueued
+    # (pacim_load_graph_async, pinned memory) before step i runs, so its H2D
+    # copy overlaps step i's build and selection; the build of step i+1 commits
+    # it (waits for the copy, derives the edge lists).  Every step's copy and
+    # its seeds/gains read-back stay inside the timed region.
+    # warm-up of the pipelined path: both staging slots allocated and used
+    ctx.pacim_load_graph_async(off_np, nbr_np, pm, t32)
+    ctx.pacim_load_graph_async(off_np, nbr_np, pm, t32)
+    step()
+    step()
     barrier()
     torch.cuda.synchronize(dev)
     f0 = torch.cuda.Event(enable_timing=True)
     f1 = torch.cuda.Event(enable_timing=True)
     f0.record(stream)
-    for _ in range(args.e2e_steps):
-        out = e2e_step()
+    # two loads in flight: steps 0 and 1 enqueued up front; the build of step
+    # i commits its graph (freeing that staging slot), then step i+2's load is
+    # enqueued before step i's selection, so the copy engine never waits on
+    # the host
+    ctx.pacim_load_graph_async(off_np, nbr_np, pm, t32)
+    if args.e2e_steps > 1:
+        ctx.pacim_load_graph_async(off_np, nbr_np, pm, t32)
+    _tw = [time.perf_counter()]
+    _sync = bool(os.environ.get("PACIM_E2E_SYNC"))  # debugging: the unpipelined loop
+    for i in range(args.e2e_steps):
+        if _sync:
+            ctx.pacim_load_graph(off_np, nbr_np, pm, t32, 0)
+        ctx.pacim_build_sketches(R, cfg["hash_seed"], a32, rank, world)  # commits step i's graph
+        if i + 2 < args.e2e_steps and not _sync:
+            ctx.pacim_load_graph_async(off_np, nbr_np, pm, t32)  # step i+2's input
+        out = ctx.pacim_select_seeds(k) if not use_dist else pdist.distributed_select(ctx, n, k, dev)
+        _tw.append(time.perf_counter())
+        if os.environ.get("PACIM_BENCH_DEBUG"):
+            _st = ctx.stats_raw()
+            print("  step", i, "build", round(_st.t_build_ms, 2), "select", round(_st.t_select_ms, 2),
+                  file=sys.stderr)
     f1.record(stream)
+    if os.environ.get("PACIM_BENCH_DEBUG"):
+        print("e2e wall ms per step:", [round(1e3 * (_tw[i + 1] - _tw[i]), 1) for i in range(len(_tw) - 1)],
+              file=sys.stderr)
     torch.cuda.synchronize(dev)
     barrier()
     ms_e2e = f0.elapsed_time(f1)
@@ -345,7 +372,9 @@ def main():
         "seconds_to_k_seeds": ms_step / 1000.0,
         "build_tests_per_s": R * m / (avg["t_build_ms"] / 1000.0),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e / args.e2e_steps},
+                "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e / args.e2e_steps,
+                "mode": "pacim_load_graph_async from pinned host CSR, two loads in flight: "
+                        "the next steps' H2D copies overlap this step's build and selection"},
         "gpu_launches": launches,
         "roofline": roofline,
         "clocks": clk,

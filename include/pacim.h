@@ -172,6 +172,21 @@ PACIM_API int pacim_load_graph(pacim_ctx *ctx, uint32_t n, uint64_t nnz,
                      const uint64_t *offsets, const uint32_t *neighbors,
                      int pmodel, uint64_t t32, int validate);
 
+/* H0, pipelined: the same load as pacim_load_graph (validate = 0), but the
+ * host -> device copies are only enqueued (on a copy stream of the ctx) and the
+ * call returns at once; the load is committed — copies awaited on the ctx
+ * stream, the CSR swapped in, the edge lists derived — by the next
+ * pacim_build_sketches (until then every other call sees the current graph),
+ * so the copy of the next graph overlaps the build and selection of the
+ * current one.  At most
+ * two loads may be pending (ESTATE beyond); they are committed in call order.
+ * The host arrays must stay valid and unmodified until the load is committed;
+ * they should be pinned (page-locked), else the copy does not overlap.  EINVAL
+ * as for pacim_load_graph (offsets[0], offsets[n], nnz, n, t32 checks). */
+PACIM_API int pacim_load_graph_async(pacim_ctx *ctx, uint32_t n, uint64_t nnz,
+                                     const uint64_t *offsets, const uint32_t *neighbors,
+                                     int pmodel, uint64_t t32);
+
 /* As pacim_load_graph but offsets/neighbors are DEVICE pointers on the ctx's
  * device (copied device-to-device; the caller keeps ownership). */
 PACIM_API int pacim_load_graph_device(pacim_ctx *ctx, uint32_t n, uint64_t nnz,

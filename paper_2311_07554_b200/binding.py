@@ -17,7 +17,8 @@ STATUS = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -5: "ESTATE",
 # Every function declared in include/pacim.h (tests check the .so exports them).
 EXPORTS = [
     "pacim_create", "pacim_destroy", "pacim_last_error", "pacim_version",
-    "pacim_threshold_from_p", "pacim_threshold_uniform", "pacim_load_graph", "pacim_load_graph_device",
+    "pacim_threshold_from_p", "pacim_threshold_uniform", "pacim_load_graph", "pacim_load_graph_async",
+    "pacim_load_graph_device",
     "pacim_generate_graph", "pacim_graph_info", "pacim_get_graph",
     "pacim_build_sketches", "pacim_select_seeds", "pacim_gain0_to_device",
     "pacim_select_reset", "pacim_cover_local", "pacim_cover_local_sparse",
@@ -81,6 +82,7 @@ def lib():
             "pacim_threshold_from_p": (u64, [C.c_double]),
             "pacim_threshold_uniform": (u64, [C.c_double, C.c_double]),
             "pacim_load_graph": (i32, [P, u32, u64, P, P, i32, u64, i32]),
+            "pacim_load_graph_async": (i32, [P, u32, u64, P, P, i32, u64]),
             "pacim_load_graph_device": (i32, [P, u32, u64, P, P, i32, u64, i32]),
             "pacim_generate_graph": (i32, [P, i32, P, i32, u64, i32, u64]),
             "pacim_graph_info": (i32, [P, P, P]),
@@ -168,6 +170,17 @@ class Context:
         nbr = np.ascontiguousarray(neighbors, dtype=np.uint32)
         self._check(self._L.pacim_load_graph(self._h, len(off) - 1, len(nbr), _ptr(off), _ptr(nbr),
                                              pmodel, t32, validate))
+
+    def pacim_load_graph_async(self, offsets: np.ndarray, neighbors: np.ndarray, pmodel: int,
+                               t32: int):
+        """Enqueue the copy of a host CSR (pinned arrays overlap with compute);
+        committed by the next pacim_build_sketches.  The arrays are
+        kept referenced here until then (at most two loads pending)."""
+        off = np.ascontiguousarray(offsets, dtype=np.uint64)
+        nbr = np.ascontiguousarray(neighbors, dtype=np.uint32)
+        self._check(self._L.pacim_load_graph_async(self._h, len(off) - 1, len(nbr), _ptr(off),
+                                                   _ptr(nbr), pmodel, t32))
+        self._staged = (getattr(self, "_staged", ()) + ((off, nbr),))[-3:]
 
     def pacim_load_graph_device(self, d_offsets, d_neighbors, n: int, nnz: int, pmodel: int,
                                 t32: int, validate: int = 0):

@@ -141,6 +141,16 @@ void pacim_destroy(pacim_ctx *ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  if (ctx->copy_stream) {
+    cudaStreamSynchronize(ctx->copy_stream);
+    cudaStreamDestroy(ctx->copy_stream);
+    cudaEventDestroy(ctx->released);
+    for (auto &g : ctx->stage) {
+      if (g.done) cudaEventDestroy(g.done);
+      pc_free(ctx, g.off);
+      pc_free(ctx, g.nbr);
+    }
+  }
   free_all(ctx);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
@@ -172,6 +182,32 @@ static void load_common(pacim_ctx *ctx, uint32_t n, uint64_t nnz, int pmodel, ui
   pc_ensure(ctx, ctx->nbr, std::max<uint64_t>(nnz, 1) * 4);
 }
 
+// commit the oldest pending asynchronous load (no-op without one)
+static void commit_staged(pacim_ctx *ctx) {
+  StagedGraph &st = ctx->stage[ctx->stage_commit];
+  if (!st.pending) return;
+  st.pending = false;
+  ctx->stage_commit ^= 1;
+  drop_graph(ctx);  // (the model was checked when the load was enqueued)
+  ctx->n = st.n;
+  ctx->m = st.nnz / 2;
+  ctx->pmodel = st.pmodel;
+  ctx->t32 = st.t32;
+  PC_CUDA(cudaStreamWaitEvent(ctx->stream, st.done, 0));
+  std::swap(ctx->off, st.off);  // the staged CSR becomes the graph; the old
+  std::swap(ctx->nbr, st.nbr);  // buffers are the slot's next staging area
+  pc_graph_finish_load(ctx, 0);
+  ctx->has_graph = true;
+  PC_CUDA(cudaEventRecord(ctx->released, ctx->stream));
+}
+
+// a synchronous load replaces anything still pending
+static void drop_staged(pacim_ctx *ctx) {
+  if (ctx->copy_stream) PC_CUDA(cudaStreamSynchronize(ctx->copy_stream));
+  ctx->stage[0].pending = ctx->stage[1].pending = false;
+  ctx->stage_fill = ctx->stage_commit = 0;
+}
+
 int pacim_load_graph(pacim_ctx *ctx, uint32_t n, uint64_t nnz, const uint64_t *offsets,
                      const uint32_t *neighbors, int pmodel, uint64_t t32, int validate) {
   return guarded(ctx, [&] {
@@ -179,6 +215,7 @@ int pacim_load_graph(pacim_ctx *ctx, uint32_t n, uint64_t nnz, const uint64_t *o
     PC_REQUIRE(n >= 1, PACIM_EINVAL, "n must be >= 1");
     PC_REQUIRE(offsets[0] == 0, PACIM_EINVAL, "offsets[0] != 0");
     PC_REQUIRE(offsets[n] == nnz, PACIM_EINVAL, "offsets[n] != nnz");
+    drop_staged(ctx);
     load_common(ctx, n, nnz, pmodel, t32);
     PC_CUDA(cudaMemcpyAsync(ctx->off.p, offsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice,
                             ctx->stream));
@@ -189,10 +226,48 @@ int pacim_load_graph(pacim_ctx *ctx, uint32_t n, uint64_t nnz, const uint64_t *o
   });
 }
 
+int pacim_load_graph_async(pacim_ctx *ctx, uint32_t n, uint64_t nnz, const uint64_t *offsets,
+                           const uint32_t *neighbors, int pmodel, uint64_t t32) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(offsets && (neighbors || nnz == 0), PACIM_EINVAL, "NULL CSR array");
+    PC_REQUIRE(n >= 1, PACIM_EINVAL, "n must be >= 1");
+    PC_REQUIRE(n < (1u << 31), PACIM_EINVAL, "n must be < 2^31 (R2 key packing)");
+    PC_REQUIRE((nnz & 1) == 0, PACIM_EINVAL, "nnz must be even (symmetric CSR)");
+    PC_REQUIRE(offsets[0] == 0, PACIM_EINVAL, "offsets[0] != 0");
+    PC_REQUIRE(offsets[n] == nnz, PACIM_EINVAL, "offsets[n] != nnz");
+    check_model(pmodel, t32);
+    StagedGraph &st = ctx->stage[ctx->stage_fill];
+    PC_REQUIRE(!st.pending, PACIM_ESTATE, "two graph loads are already pending");
+    if (!ctx->copy_stream) {
+      PC_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+      PC_CUDA(cudaEventCreateWithFlags(&ctx->released, cudaEventDisableTiming));
+      for (auto &g : ctx->stage) PC_CUDA(cudaEventCreateWithFlags(&g.done, cudaEventDisableTiming));
+      PC_CUDA(cudaEventRecord(ctx->released, ctx->stream));
+    }
+    pc_ensure(ctx, st.off, ((size_t)n + 1) * 8);
+    pc_ensure(ctx, st.nbr, std::max<uint64_t>(nnz, 1) * 4);
+    // the slot's buffers may have been the graph before the last commit
+    PC_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->released, 0));
+    PC_CUDA(cudaMemcpyAsync(st.off.p, offsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice,
+                            ctx->copy_stream));
+    if (nnz)
+      PC_CUDA(cudaMemcpyAsync(st.nbr.p, neighbors, nnz * 4, cudaMemcpyHostToDevice,
+                              ctx->copy_stream));
+    PC_CUDA(cudaEventRecord(st.done, ctx->copy_stream));
+    st.pending = true;
+    st.n = n;
+    st.nnz = nnz;
+    st.pmodel = pmodel;
+    st.t32 = t32;
+    ctx->stage_fill ^= 1;
+  });
+}
+
 int pacim_load_graph_device(pacim_ctx *ctx, uint32_t n, uint64_t nnz, const uint64_t *d_offsets,
                             const uint32_t *d_neighbors, int pmodel, uint64_t t32, int validate) {
   return guarded(ctx, [&] {
     PC_REQUIRE(d_offsets && (d_neighbors || nnz == 0), PACIM_EINVAL, "NULL CSR array");
+    drop_staged(ctx);
     load_common(ctx, n, nnz, pmodel, t32);
     PC_CUDA(cudaMemcpyAsync(ctx->off.p, d_offsets, ((size_t)n + 1) * 8, cudaMemcpyDeviceToDevice,
                             ctx->stream));
@@ -217,6 +292,7 @@ int pacim_generate_graph(pacim_ctx *ctx, int kind, const uint64_t *params, int n
   return guarded(ctx, [&] {
     PC_REQUIRE(params || nparams == 0, PACIM_EINVAL, "NULL params");
     check_model(pmodel, t32);
+    drop_staged(ctx);
     drop_graph(ctx);
     ctx->pmodel = pmodel;
     ctx->t32 = t32;
@@ -249,6 +325,7 @@ int pacim_get_graph(pacim_ctx *ctx, uint64_t *offsets_out, uint32_t *neighbors_o
 int pacim_build_sketches(pacim_ctx *ctx, uint32_t R, uint64_t hash_seed, uint64_t center_a32,
                          uint32_t shard_rank, uint32_t shard_world) {
   return guarded(ctx, [&] {
+    commit_staged(ctx);
     PC_REQUIRE(ctx->has_graph, PACIM_ESTATE, "build before load_graph");
     PC_REQUIRE(R >= 1, PACIM_EINVAL, "R must be >= 1");
     PC_REQUIRE(shard_world >= 1 && shard_rank < shard_world, PACIM_EINVAL,

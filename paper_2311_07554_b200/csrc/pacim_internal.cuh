@@ -105,6 +105,18 @@ struct DeltaList {
   }
 };
 
+// a graph load in flight (pacim_load_graph_async): the host CSR copied into
+// these buffers on the copy stream, committed by the next call needing the graph
+struct StagedGraph {
+  DevBuf off, nbr;
+  cudaEvent_t done = nullptr;  // recorded on the copy stream after the copies
+  bool pending = false;
+  uint32_t n = 0;
+  uint64_t nnz = 0;
+  int pmodel = 0;
+  uint64_t t32 = 0;
+};
+
 struct pacim_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -222,6 +234,12 @@ struct pacim_ctx {
 
   pacim_stats stats{};
   uint32_t launches = 0;
+
+  // asynchronous graph loads: two staging slots, filled in order on copy_stream
+  StagedGraph stage[2];
+  uint32_t stage_fill = 0, stage_commit = 0;  // next slot to fill / to commit
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t released = nullptr;  // main stream: the last commit's old buffers are free
 };
 
 // allocation with capacity reuse

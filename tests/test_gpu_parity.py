@@ -461,3 +461,37 @@ def test_lazy_selector_equals_oracle(orc, ctx, i):
     assert k <= st["select_evaluations"] <= k * g.n
     s3, gn3, _, _ = ctx.pacim_select_seeds(k)  # the incremental selector on the same store
     assert list(s3) == list(es)
+
+
+def test_load_graph_async(orc, ctx):
+    """Pipelined loads (pacim_load_graph_async): two graphs enqueued, each
+    committed by the build that follows; results equal the oracle's, and a
+    third pending load is rejected (ESTATE) while two are in flight."""
+    import torch
+    from oracle.oracle import Graph
+    from paper_2311_07554_b200 import PacimError
+    gs = [inputs.random_powerlaw_graph(900, 4000, 71), inputs.random_graph(700, 2500, 72)]
+    pinned = []
+    for off, nbr in gs:
+        po = torch.from_numpy(off.astype(np.uint64)).pin_memory().numpy()
+        pn = torch.from_numpy(nbr.astype(np.uint32)).pin_memory().numpy()
+        pinned.append((po, pn))
+    t32 = orc.t32_const(0.1)
+    ctx.pacim_load_graph_async(*pinned[0], 0, t32)
+    ctx.pacim_load_graph_async(*pinned[1], 0, t32)
+    with pytest.raises(PacimError):
+        ctx.pacim_load_graph_async(*pinned[0], 0, t32)
+    for i, (off, nbr) in enumerate(gs):
+        g = Graph(len(off) - 1, off, nbr)
+        ctx.pacim_build_sketches(24, 80 + i)  # commits graph i
+        assert ctx.pacim_graph_info() == (g.n, g.m)
+        s, gn, sg, _ = ctx.pacim_select_seeds(6)
+        es, egn, esg, eg0 = orc.greedy(g, 0, t32, 24, 80 + i, 6, want_gain0=True)
+        assert np.array_equal(ctx.pacim_get_gain0(), eg0)
+        assert list(s) == list(es) and list(gn) == list(egn) and list(sg) == list(esg)
+    # a synchronous load discards pending ones
+    ctx.pacim_load_graph_async(*pinned[0], 0, t32)
+    off, nbr = gs[1]
+    ctx.pacim_load_graph(off, nbr, 0, t32, 1)
+    ctx.pacim_build_sketches(24, 81)
+    assert ctx.pacim_graph_info() == (len(off) - 1, len(nbr) // 2)
