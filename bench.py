@@ -7,12 +7,17 @@ pacim_build_sketches (hash + live test, union-find, compression, CC sizes in
 the root slots, gain0) followed by pacim_select_seeds (k
 greedy steps, H8-H12).  value = R*m / t_step summed over the job (m =
 undirected edges; every logical (edge, sketch) test counted).  e2e repeats the
-step through pacim_load_graph from pinned HOST buffers (H2D inside the timed
+step through the public API from pinned HOST buffers: pacim_load_graph_async
+(two loads in flight, each committed by the next build, so a step's H2D copy
+overlaps the previous step's build and selection; every copy inside the timed
 region) with the seeds/gains read back to the host.
 
 N > 1 (torchrun): sketches are sharded r % N == rank over a replicated CSR,
-each greedy step all-reduces the gain deltas (NCCL); total work is fixed
-(strong scaling).  Timing: CUDA events on the library's stream (= torch's
+each greedy step exchanges sparse gain deltas (NCCL all-gathers; a dense
+all-reduce when a list overflows); total work is fixed (strong scaling).
+--force-dist runs that per-step exchange even at one rank (testing).
+Debugging: PACIM_BENCH_DEBUG=1 prints the e2e steps' wall times,
+PACIM_E2E_SYNC=1 uses the unpipelined pacim_load_graph in the e2e loop.  Timing: CUDA events on the library's stream (= torch's
 current stream), barrier + synchronize on both sides, max over ranks.
 
 --impl reference times the CPU oracle (oracle/, single-threaded C) on a
