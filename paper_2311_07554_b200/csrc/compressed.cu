@@ -503,9 +503,19 @@ static uint32_t choose_batch(pacim_ctx *ctx) {
   if (const char *e = getenv("PACIM_BATCH")) return std::max<uint32_t>(1, std::min<uint32_t>(B, atoi(e)));
   size_t fr = 0, tot = 0;
   cudaMemGetInfo(&fr, &tot);
-  fr += ctx->Ltmp.bytes;  // an earlier batch buffer is reused (or freed before growing)
-  size_t budget = std::min<size_t>(fr / 3, (size_t)24 << 30);
-  size_t per = (size_t)std::max<uint32_t>(ctx->nr, 1) * 4;
+  fr += ctx->Ltmp.bytes + ctx->cwork.bytes;  // earlier batch buffers: reused or freed before growing
+  // everything but what the selection will still allocate (its traversal
+  // state, for CCs too big for a probe) and 2 GB of headroom; at least a third
+  // (one batch of all 256 slots at c4 alpha = 1/8: build 132 -> 104 ms, one
+  // edge pass instead of two)
+  const size_t sel = ctx->bfs.bytes ? 0 : pc_select_state_bytes(ctx->nr, B);
+  const size_t keep = sel + ((size_t)2 << 30);
+  const size_t ample = fr > keep ? fr - keep : 0;
+  // tight memory (c4 alpha = 1/2: 103 GB store): the old third, capped at
+  // 24 GB — bigger batches there are re-allocated around the HLA every build
+  size_t budget = ample >= ((size_t)40 << 30) ? ample : std::min<size_t>(fr / 3, (size_t)24 << 30);
+  // per slot: a parent word per row (Ltmp) and a root word per center (cwork)
+  size_t per = ((size_t)std::max<uint32_t>(ctx->nr, 1) + ctx->rho) * 4;
   size_t bb = budget / per;
   return (uint32_t)std::max<size_t>(1, std::min<size_t>(B, bb));
 }

@@ -343,6 +343,8 @@ void pc_select_compressed(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *
                           int64_t *sigma_num);
 void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *local_gain);
 void pc_select_reset_compressed(pacim_ctx *ctx);
+// select.cu: device bytes of the selection's traversal state for nr rows, B slots
+size_t pc_select_state_bytes(uint32_t nr, uint32_t B);
 void pc_get_center_sketch(pacim_ctx *ctx, uint32_t slot, uint32_t *label, uint32_t *size);
 // select.cu
 void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,

@@ -1196,6 +1196,20 @@ static uint64_t env_u64(const char *name, uint64_t dflt) {
 }
 
 // Device state shared by the single-rank selection and the multi-rank steps.
+// work-queue ring items for rows: a power of two >= 2 (rows + 2^18), at most 2^28
+static uint64_t ring_items(uint32_t nr) {
+  uint64_t qcap = 1024;
+  while (qcap < 2ull * ((uint64_t)nr + (1ull << 18)) && qcap < (1ull << 28)) qcap <<= 1;
+  return qcap;
+}
+
+// device bytes of the selection's traversal state (make_sel's layout)
+size_t pc_select_state_bytes(uint32_t nr, uint32_t B) {
+  const size_t BW = (B + 31) / 32;
+  return 4 * (2 * (size_t)QC_WORDS + 2 * DG_WORDS + 4 + 2 * (size_t)nr * BW + 4 * (size_t)nr +
+              4 * ring_items(nr) + 4);
+}
+
 static Sel make_sel(pacim_ctx *ctx, long long *target) {
   const uint32_t B = ctx->R_local, n = ctx->n, nr = ctx->nr;
   PC_REQUIRE((B + 31) / 32 <= MAX_BW, PACIM_ENOTIMPL,
@@ -1264,8 +1278,7 @@ static Sel make_sel(pacim_ctx *ctx, long long *target) {
   // capped at 2^28 items (4 GB): outstanding rows are the rows reached but
   // not yet expanded, far below `rows` in practice (c5: 268M rows); a full
   // ring would stall producers until the watchdog reports it (ECHECK)
-  uint64_t qcap = 1024;
-  while (qcap < 2ull * ((uint64_t)nr + (1ull << 18)) && qcap < (1ull << 28)) qcap <<= 1;
+  const uint64_t qcap = ring_items(nr);
   const size_t bw = (size_t)nr * S.BW;
   const size_t head = 2 * QC_WORDS + 2 * DG_WORDS + 4;
   const size_t words = head + 2 * bw + 4 * (size_t)nr + 4 * qcap + 4;
