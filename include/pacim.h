@@ -99,6 +99,8 @@ typedef struct {
     uint64_t hla_entries;           /* live hub adjacency of the last build: (hub, sketch,
                                        neighbour) entries, 0 if not recorded */
     uint32_t hubs;                  /* rows of degree > the hub degree (PACIM_HUB_DEG) */
+    uint64_t select_hotsum_steps;   /* compressed: steps whose giant CCs were covered from the
+                                       build's hub sums (the hub chosen), without a rebuild */
 } pacim_stats;
 
 /* --------------------------------------------------------------- lifecycle */

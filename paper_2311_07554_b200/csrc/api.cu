@@ -79,7 +79,7 @@ static void free_all(pacim_ctx *ctx) {
 
                     &ctx->d_tab, &ctx->gain0,      &ctx->gain,     &ctx->center_of, &ctx->counters,
                     &ctx->scratch, &ctx->scratch2, &ctx->sel_seeds, &ctx->sel_gain,
-                    &ctx->sel_partial, &ctx->sel_list, &ctx->sel_flag, &ctx->argmax_part, &ctx->bfs, &ctx->tcsr, &ctx->hidx, &ctx->hub_tab, &ctx->hla_off, &ctx->hla_row, &ctx->hla_raw, &ctx->d_smap, &ctx->pkeys, &ctx->cprobe, &ctx->cseed, &ctx->d_hr64, &ctx->crow, &ctx->vinfo};
+                    &ctx->sel_partial, &ctx->sel_list, &ctx->sel_flag, &ctx->argmax_part, &ctx->bfs, &ctx->tcsr, &ctx->hidx, &ctx->hub_tab, &ctx->hla_off, &ctx->hla_row, &ctx->hla_raw, &ctx->d_smap, &ctx->pkeys, &ctx->cprobe, &ctx->cseed, &ctx->d_hr64, &ctx->crow, &ctx->vinfo, &ctx->hotsum, &ctx->d_hot_size};
   for (DevBuf *b : bufs) pc_free(ctx, *b);
 }
 

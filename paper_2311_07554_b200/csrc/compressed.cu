@@ -28,6 +28,7 @@ namespace {
 
 constexpr uint32_t NONE = 0xFFFFFFFFu;
 constexpr int PROBE_WARPS = 4;     // warps per block in k_probe
+constexpr uint32_t HOT_BIG_T = 65536;  // covered CCs above this go to the rebuild (or hotsum)
 constexpr uint32_t QCAP = 512;     // Get-center local queue capacity
 constexpr uint32_t HCAP = 1024;    // its visited hash set (power of two)
 
@@ -58,23 +59,37 @@ __global__ void k_center_index(const uint64_t *flag, const uint64_t *pos, uint32
 
 // ------------------------------------------------------- batch outputs
 // gain0[v] += sum over the batch's slots of (|C_j(v)| - 1) (gain0 starts at B)
+// ... and hotsum[v] += the sizes of the hub's CCs of more than big_t vertices
+// that contain v (hot[jj]: the hub's root row in batch slot jj; their sizes
+// to hot_size[j0 + jj]): the member update of the hub's giant CCs when the
+// hub itself is chosen, without a rebuild (pc_cover_compressed)
 __global__ void k_gain_sizes(const uint32_t *Lb, uint32_t nr, uint32_t Bb, const uint32_t *rmap,
-                             int64_t *gain0, unsigned long long *ncc_ctr) {
+                             int64_t *gain0, unsigned long long *ncc_ctr, const uint32_t *hot,
+                             uint32_t j0, uint32_t big_t, uint32_t *hot_size, int64_t *hotsum) {
   unsigned long long ncc = 0;  // roots of size >= 2: the non-singleton CCs
   const int lane = threadIdx.x & 31;
   size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  if (warp == 0)
+    for (uint32_t j = lane; j < Bb; j += 32)
+      hot_size[j0 + j] = hot[j] < nr ? (Lb[(size_t)hot[j] * Bb + j] & PACIM_LOW) : 0u;
   for (size_t v = warp; v < nr; v += nw) {
-    long long g = 0;
+    long long g = 0, hs = 0;
     for (uint32_t j = lane; j < Bb; j += 32) {
       uint32_t s = Lb[v * Bb + j];
       if (s == (PACIM_HIGH | 1u)) continue;  // singleton: size 1, already counted
       ncc += (s & PACIM_HIGH) != 0;
       uint32_t sz = (s & PACIM_HIGH) ? (s & PACIM_LOW) : (Lb[(size_t)s * Bb + j] & PACIM_LOW);
       g += (long long)sz - 1;
+      const uint32_t root = (s & PACIM_HIGH) ? (uint32_t)v : s;
+      if (root == hot[j] && sz > big_t) hs += sz;
     }
-    for (int d = 16; d; d >>= 1) g += __shfl_xor_sync(0xffffffffu, g, d);
+    for (int d = 16; d; d >>= 1) {
+      g += __shfl_xor_sync(0xffffffffu, g, d);
+      hs += __shfl_xor_sync(0xffffffffu, hs, d);
+    }
     if (lane == 0 && g) gain0[rmap[v]] += g;
+    if (lane == 0 && hs) hotsum[rmap[v]] += hs;
   }
   for (int d = 16; d; d >>= 1) ncc += __shfl_xor_sync(0xffffffffu, ncc, d);
   if (lane == 0 && ncc) atomicAdd(ncc_ctr, ncc);
@@ -490,6 +505,19 @@ __global__ void k_seed_roots(const uint32_t *Lb, uint32_t Bb, uint32_t srow, uin
     sroot[jj] = root_of(Lb, Bb, srow, jj);
 }
 
+// target[v] -= hotsum[v] for v != s (the hub's giant CCs covered at once)
+__global__ void k_apply_hotsum(long long *target, const int64_t *hotsum, uint32_t n, uint32_t s,
+                               DeltaList dlst) {
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (size_t)gridDim.x * blockDim.x) {
+    const long long h = hotsum[v];
+    if (h && v != s) {
+      atomicAdd((unsigned long long *)&target[v], (unsigned long long)(-h));
+      dlst.add((uint32_t)v, -h);
+    }
+  }
+}
+
 __global__ void k_set_seed(long long *gain, uint8_t *is_seed, uint32_t s, int set_gain) {
   if (set_gain) gain[s] = -1;
   is_seed[s] = 1;
@@ -569,6 +597,13 @@ void pc_build_compressed(pacim_ctx *ctx) {
   k_fill_i64c<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(ctx->gain0.as<int64_t>(), n,
                                                             (int64_t)B);
   PC_CHECK_LAUNCH();
+  // covered CCs above cbig_t go to the batch rebuild (or the hub's hotsum);
+  // PACIM_CBIG_T lowers it for tests (read once per build: select uses the same)
+  ctx->cbig_t = getenv("PACIM_CBIG_T") ? (uint32_t)std::max(1LL, atoll(getenv("PACIM_CBIG_T")))
+                                       : HOT_BIG_T;
+  pc_ensure(ctx, ctx->hotsum, (size_t)n * 8);
+  pc_ensure(ctx, ctx->d_hot_size, (size_t)B * 4);
+  PC_CUDA(cudaMemsetAsync(ctx->hotsum.p, 0, (size_t)n * 8, ctx->stream));
   // live hub adjacency for the Get-center probes (a hub met by a probe is
   // expanded from its live list, not its whole adjacency), recorded when its
   // expected size is at most m / 4 entries (c4 WIC: 94M entries, the select
@@ -590,7 +625,9 @@ void pc_build_compressed(pacim_ctx *ctx) {
     const uint32_t bb = std::min(Bb, B - j0);
     pc_sketch_pass(ctx, Lb, j0, bb, ctr, nullptr, rec_hla ? &hla : nullptr);
     k_gain_sizes<<<pc_grid(ctx, (size_t)nr * 32, 256, 16), 256, 0, ctx->stream>>>(
-        Lb, nr, bb, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>(), ctr);
+        Lb, nr, bb, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>(), ctr,
+        ctx->d_hot.as<uint32_t>(), j0, ctx->cbig_t, ctx->d_hot_size.as<uint32_t>(),
+        ctx->hotsum.as<int64_t>());
     PC_CHECK_LAUNCH();
     const size_t tot = (size_t)rho * bb;
     if (tot) {
@@ -609,6 +646,9 @@ void pc_build_compressed(pacim_ctx *ctx) {
     ctx->launches += 1;
   }
   if (rec_hla) pc_hla_finish(ctx, &hla);
+  ctx->hot_size.resize(B);
+  PC_CUDA(cudaMemcpyAsync(ctx->hot_size.data(), ctx->d_hot_size.p, (size_t)B * 4,
+                          cudaMemcpyDeviceToHost, ctx->stream));
   PC_CUDA(cudaMemcpyAsync(ctx->csz_work.p, ctx->csz.p, cs, cudaMemcpyDeviceToDevice, ctx->stream));
   PC_CUDA(cudaEventRecord(e2, ctx->stream));
   unsigned long long h[6];
@@ -711,19 +751,47 @@ void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *l
     // a giant is slower)
     // measured: a queue traversal of c5's giant CCs took 3.4 s, the batch
     // rebuild + dense pass a few hundred ms
-    const uint64_t big_t = 65536;
+    const uint64_t big_t = ctx->cbig_t;
+    bool changed = false;
+    if (s == ctx->hub && ctx->hot_size.size() == B) {
+      // the hub chosen while its giant CCs (> big_t) are all still uncovered:
+      // their member updates are the build's hotsum, no rebuild
+      bool ok = true, any = false;
+      for (uint32_t j = 0; j < B && ok; j++)
+        if (ctx->hot_size[j] > big_t) {
+          any = true;
+          ok = hst[j] == ST_BIG_KNOWN && hdl[j] == ctx->hot_size[j];
+        } else if (hst[j] == ST_BIG_KNOWN && hdl[j] > big_t) {
+          ok = false;  // (cannot happen: the hub's CC is the hot CC)
+        }
+      if (ok && any) {
+        k_apply_hotsum<<<pc_grid(ctx, ctx->n, 256), 256, 0, ctx->stream>>>(
+            reinterpret_cast<long long *>(target), ctx->hotsum.as<int64_t>(), ctx->n, s,
+            ctx->dlist);
+        PC_CHECK_LAUNCH();
+        ctx->launches++;
+        for (uint32_t j = 0; j < B; j++)
+          if (ctx->hot_size[j] > big_t) {
+            known += hdl[j];
+            hst[j] = ST_DONE;
+          }
+        changed = true;
+        ctx->stats.select_hotsum_steps++;
+      }
+    }
+    uint64_t tknown = 0;
     for (uint32_t j = 0; j < B; j++) {
       if (hst[j] == ST_BIG_KNOWN && hdl[j] <= big_t) {
         tdl[j] = hdl[j];
-        known += hdl[j];
+        tknown += hdl[j];
         hst[j] = ST_DONE;
       }
       unknown |= hst[j] == ST_BIG_UNKNOWN;
     }
-    if (known) {
-      pc_traverse_slots(ctx, s, target, tdl.data());
+    if (tknown) pc_traverse_slots(ctx, s, target, tdl.data());
+    known += tknown;
+    if (tknown || changed)
       PC_CUDA(cudaMemcpyAsync(st, hst.data(), (size_t)B * 4, cudaMemcpyHostToDevice, ctx->stream));
-    }
     total += known;
   }
   if (hs[1]) {
@@ -787,6 +855,7 @@ void pc_select_compressed(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *
   ctx->stats.select_bfs_visits = 0;
   ctx->stats.select_center_visits = 0;
   ctx->stats.select_center_found = 0;
+  ctx->stats.select_hotsum_steps = 0;
   ctx->launches = 0;
   long long run = 0;
   for (uint32_t i = 0; i < k; i++) {

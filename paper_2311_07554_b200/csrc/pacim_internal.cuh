@@ -214,6 +214,10 @@ struct pacim_ctx {
   DevBuf cwork;       // per-step compressed cover scratch
   DevBuf cprobe;      // compressed cover: per-slot status / label / delta + sums
   DevBuf cseed;       // compressed cover: the seed's live neighbours per slot
+  DevBuf hotsum;      // i64[n]: sizes of the hub's CCs of > 65536 vertices containing v
+  DevBuf d_hot_size;  // u32[B]: the hub's CC size per slot
+  std::vector<uint32_t> hot_size;
+  uint32_t cbig_t = 65536;  // compressed: covered CCs above it go to the rebuild / hotsum
 
   // scratch
   DevBuf counters;    // u64[64]

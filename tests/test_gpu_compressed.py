@@ -222,3 +222,16 @@ def test_compressed_many_sketches(orc, ctx, batch, monkeypatch):
     es, egn, esg, eg0 = orc.greedy(g, 0, t32, 700, 62, 10, want_gain0=True)
     assert np.array_equal(ctx.pacim_get_gain0(), eg0)
     assert list(s) == list(es) and list(gn) == list(egn) and list(sg) == list(esg)
+
+
+@pytest.mark.parametrize("big", ["8", "40"])
+@pytest.mark.parametrize("i", [1, 2, 4, 8, 9])
+def test_compressed_hub_hotsum(orc, ctx, i, big, monkeypatch):
+    """Covered CCs above a (lowered) size threshold: the batch rebuild + dense
+    pass, or — when the hub (maximum-degree vertex) is the seed while its big
+    CCs are all uncovered — the build's per-vertex hotsum; the greedy equals
+    the oracle's."""
+    monkeypatch.setenv("PACIM_CBIG_T", big)
+    run_case(orc, ctx, i, check_sketches=False)
+    if i == 8:  # the star's center is the hub and the first seed
+        assert ctx.pacim_get_stats()["select_hotsum_steps"] == 1
