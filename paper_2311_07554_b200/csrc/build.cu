@@ -408,18 +408,36 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
 // (H7), the CC size read from the root slot (HIGH | size).
 // acc: window of a multi-window store, gain0[v] += sum (|C| - 1) over its
 // slots (gain0 starts at B); else gain0[v] = the sum over all B slots
-constexpr int GR = 4;  // rows per warp iteration in k_gain0 (4 KB of slots in flight)
+constexpr int GR_PLAIN = 4;  // rows per warp iteration in k_gain0 (4 KB of slots in flight)
+// HOT: also hotsum[v] = the sizes of the hot (hub's) CCs above big_t that
+// contain v — the select covers them by one vector pass when they are
+// exactly the step's dense set (k_select phase D)
+template <bool HOT>
 __global__ void __launch_bounds__(256) k_gain0(const uint32_t *__restrict__ L, uint32_t n,
                                                uint32_t B, const uint32_t *rmap, int64_t *gain0,
-                                               int acc, unsigned long long *ncc_ctr) {
+                                               int acc, unsigned long long *ncc_ctr,
+                                               const uint32_t *hot, const uint32_t *hot_size,
+                                               uint32_t big_t, int64_t *hotsum) {
+  constexpr int GR = HOT ? 2 : GR_PLAIN;  // fewer rows in flight: the hot sums' registers
   unsigned long long ncc = 0;  // roots of size >= 2: the non-singleton CCs
+  extern __shared__ uint32_t hsm[];
+  const uint32_t H = HOT ? min(B, HOT_MAX) : 0;
+  uint32_t *hroot = hsm, *hsz = hsm + H;
+  if (HOT) {
+    for (uint32_t j = threadIdx.x; j < H; j += blockDim.x) {
+      hroot[j] = hot[j];
+      hsz[j] = hot_size[j] > big_t ? hot_size[j] : 0u;  // 0: not a giant
+    }
+    __syncthreads();
+  }
+
   const int lane = threadIdx.x & 31;
   size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
   for (size_t v0 = warp * GR; v0 < n; v0 += nw * GR) {
-    long long g[GR];
+    long long g[GR], hs[GR];
 #pragma unroll
-    for (int r = 0; r < GR; r++) g[r] = 0;
+    for (int r = 0; r < GR; r++) g[r] = hs[r] = 0;
     for (uint32_t j0 = 0; j0 < B; j0 += 256) {
       uint32_t sv[GR][8];
 #pragma unroll
@@ -438,6 +456,10 @@ __global__ void __launch_bounds__(256) k_gain0(const uint32_t *__restrict__ L, u
           const uint32_t j = j0 + lane + 32 * i;
           const uint32_t s = sv[r][i];
           if (s == NONE) continue;
+          if (HOT && j < H && hsz[j]) {  // a member of slot j's giant hot CC
+            const uint32_t root = (s & PACIM_HIGH) ? (uint32_t)(v0 + r) : s;
+            if (root == hroot[j]) hs[r] += hsz[j];
+          }
           if (s & PACIM_HIGH)
             ncc += (s & PACIM_LOW) >= 2;
           else
@@ -460,9 +482,21 @@ __global__ void __launch_bounds__(256) k_gain0(const uint32_t *__restrict__ L, u
           gain0[rmap[v0 + r]] = t;
         }
       }
+      if (HOT) {
+        long long h = hs[r];
+        for (int d = 16; d; d >>= 1) h += __shfl_xor_sync(0xffffffffu, h, d);
+        if (lane == 0 && v0 + r < n) hotsum[rmap[v0 + r]] = h;
+      }
     }
   }
   add_count(ncc_ctr, ncc);
+}
+
+// per slot the hot (hub's) CC size, read from its root slot after compression
+__global__ void k_hot_sizes(const uint32_t *L, uint32_t n, uint32_t B, const uint32_t *hot,
+                            uint32_t *hot_size) {
+  for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < B; j += gridDim.x * blockDim.x)
+    hot_size[j] = hot[j] < n ? (L[(size_t)hot[j] * B + j] & PACIM_LOW) : 0u;
 }
 
 // HLA: entries sorted by key -> rows, and the segment offsets: off[q] = the
@@ -968,6 +1002,7 @@ void pc_build(pacim_ctx *ctx) {
   ctx->hla_ok = false;
   Hla hla{};
   const bool rec_hla = want_hla && pc_hla_begin(ctx, &hla, 1e30);
+  ctx->hot_any = false;  // set by the single-window gain pass when hot sums are kept
   const uint32_t W = plan_windows(ctx);
   const uint32_t nwin = (uint32_t)ctx->win_first.size() - 1;
   if (ctx->smap_of != ctx->win_first || ctx->d_smap.bytes < (size_t)B * 4) {
@@ -1034,9 +1069,43 @@ void pc_build(pacim_ctx *ctx) {
     if (c < NARROW_W)
       k_gain_w<<<pc_grid(ctx, (size_t)n * c, 256, 16), 256, 0, ctx->stream>>>(
           Lw, n, c, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>(), nwin > 1, ctr);
-    else
-      k_gain0<<<rows_grid, 256, 0, ctx->stream>>>(Lw, n, c, ctx->rmap.as<uint32_t>(),
-                                                 ctx->gain0.as<int64_t>(), nwin > 1, ctr);
+    else if (nwin == 1) {
+      // one window: the hot CCs' sizes decide whether the per-vertex hot sums
+      // are worth accumulating (some slot's hot CC above the select's dense
+      // threshold — the same formula as make_sel)
+      const uint32_t big_t = (uint32_t)(getenv("PACIM_BIG_T")
+                                            ? std::max(1LL, atoll(getenv("PACIM_BIG_T")))
+                                            : std::max<uint64_t>(65536, n / 8));
+      pc_ensure(ctx, ctx->d_hot_size, (size_t)B * 4);
+      k_hot_sizes<<<(c + 255) / 256, 256, 0, ctx->stream>>>(Lw, n, c, ctx->d_hot.as<uint32_t>(),
+                                                            ctx->d_hot_size.as<uint32_t>());
+      PC_CHECK_LAUNCH();
+      ctx->hot_size.resize(B);
+      PC_CUDA(cudaMemcpyAsync(ctx->hot_size.data(), ctx->d_hot_size.p, (size_t)B * 4,
+                              cudaMemcpyDeviceToHost, ctx->stream));
+      PC_CUDA(cudaStreamSynchronize(ctx->stream));
+      bool any = false;
+      for (uint32_t j = 0; j < B; j++) any |= ctx->hot_size[j] > big_t;
+      ctx->hot_any = any;
+      ctx->hot_big_t = big_t;
+      if (any) {
+        pc_ensure(ctx, ctx->hotsum, (size_t)ctx->n * 8);
+        PC_CUDA(cudaMemsetAsync(ctx->hotsum.p, 0, (size_t)ctx->n * 8, ctx->stream));  // isolated: 0
+        k_gain0<true><<<rows_grid, 256, 2 * std::min<uint32_t>(c, HOT_MAX) * sizeof(uint32_t),
+                        ctx->stream>>>(Lw, n, c, ctx->rmap.as<uint32_t>(),
+                                       ctx->gain0.as<int64_t>(), 0, ctr, ctx->d_hot.as<uint32_t>(),
+                                       ctx->d_hot_size.as<uint32_t>(), big_t,
+                                       ctx->hotsum.as<int64_t>());
+      } else {
+        k_gain0<false><<<rows_grid, 256, 0, ctx->stream>>>(Lw, n, c, ctx->rmap.as<uint32_t>(),
+                                                          ctx->gain0.as<int64_t>(), 0, ctr,
+                                                          nullptr, nullptr, 0, nullptr);
+      }
+    } else {
+      k_gain0<false><<<rows_grid, 256, 0, ctx->stream>>>(Lw, n, c, ctx->rmap.as<uint32_t>(),
+                                                        ctx->gain0.as<int64_t>(), 1, ctr, nullptr,
+                                                        nullptr, 0, nullptr);
+    }
     PC_CHECK_LAUNCH();
     ctx->launches++;
   }

@@ -552,6 +552,7 @@ void pc_build_compressed(pacim_ctx *ctx) {
   const uint32_t n = ctx->n, nr = ctx->nr, B = ctx->R_local;
   PC_REQUIRE(B >= 1 && B <= 65535, PACIM_EINVAL, "local sketch count must be in [1, 65535]");
   pc_slot_table(ctx);
+  ctx->hot_any = false;
   // the uncompressed store and its selection state of an earlier build are
   // released first (the point of the compressed mode is not to hold them)
   // and so is the HLA of an earlier build; its batch parent arrays are kept

@@ -218,6 +218,8 @@ struct pacim_ctx {
   DevBuf d_hot_size;  // u32[B]: the hub's CC size per slot
   std::vector<uint32_t> hot_size;
   uint32_t cbig_t = 65536;  // compressed: covered CCs above it go to the rebuild / hotsum
+  bool hot_any = false;     // uncompressed: hotsum holds the giant hot CCs' sums (one window)
+  uint32_t hot_big_t = 0;   // ... for this select dense threshold
 
   // scratch
   DevBuf counters;    // u64[64]

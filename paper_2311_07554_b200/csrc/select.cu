@@ -170,6 +170,8 @@ struct Sel {
   uint32_t big_t;
   int warp_ok;             // small CCs may use warp_bfs
   uint32_t warp_max;       // ... up to this many vertices (<= QCAP)
+  const int64_t *hotsum;   // per vertex: sizes of the giant hot CCs containing it (or null)
+  const uint32_t *hot_root, *hot_size;  // per slot: the hub's root row and CC size
   int trav_only;           // no store: dl[] preset per slot, only the member traversal
   // asynchronous traversal
   uint32_t *vis;           // rows x BW: slots in which the row was visited this step
@@ -833,6 +835,31 @@ __device__ void apply_dense(const Sel &S, uint32_t s, size_t warp0, size_t nwarp
   }
 }
 
+// phase D shortcut: when the step's dense set is exactly the giant hot (hub's)
+// CCs, all covered now, the build's per-vertex hot sums are the member
+// updates — one vector pass instead of a pass over the store (c2's first
+// step).  Block-collective (uniform result); false: run the dense pass.
+__device__ __noinline__ bool dense_hot(const uint32_t *cov_root, const uint32_t *hot_size,
+                                       const uint32_t *hot_root, uint32_t big_t, uint32_t B,
+                                       const int64_t *hotsum, long long *target, uint32_t nv,
+                                       DeltaList dlst, uint32_t s, size_t tid, size_t nth) {
+  int ok = 1;
+  for (uint32_t j = threadIdx.x; j < B; j += blockDim.x) {
+    const uint32_t cr = __ldcg(cov_root + j);
+    const bool big = hot_size[j] > big_t;
+    if (big != (cr != NONE) || (big && cr != hot_root[j])) ok = 0;
+  }
+  if (!__syncthreads_and(ok)) return false;
+  for (size_t v = tid; v < nv; v += nth) {
+    const long long h = hotsum[v];
+    if (h && v != s) {
+      atomicAdd((unsigned long long *)&target[v], (unsigned long long)(-h));
+      dlst.add((uint32_t)v, -h);
+    }
+  }
+  return true;
+}
+
 __device__ void load_tables(const Sel &S, uint32_t *shr, uint16_t *tab) {
   for (uint32_t i = threadIdx.x; i < S.B; i += blockDim.x) shr[i] = S.g_shr[i];
   for (uint32_t i = threadIdx.x; i <= (1u << PACIM_TB); i += blockDim.x) tab[i] = S.g_tab[i];
@@ -1005,7 +1032,12 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) k_select(Sel S0, SelOut O, uin
     // ---- D: dense pass for big CCs (the flag is final: every B is done)
     const bool dense = __ldcg(S.dense + S.par) != 0;
     if (dense) {
-      apply_dense(S, s, gwarp, nwarps);
+      // the dense set exactly the giant hot (hub's) CCs, all covered now —
+      // the build's per-vertex hot sums are the member updates (one vector
+      // pass instead of a pass over the store; c2's first step)
+      if (!(S.hotsum && dense_hot(S.cov_root, S.hot_size, S.hot_root, S.big_t, S.B, S.hotsum,
+                                  S.target, S.nv, S.dlst, s, tid, nth)))
+        apply_dense(S, s, gwarp, nwarps);
       if (tid == 0 && S.diag) atomicAdd(S.diag + DG_DENSE, 1ull);
       grid.sync();
     }
@@ -1242,6 +1274,11 @@ static Sel make_sel(pacim_ctx *ctx, long long *target) {
   S.warp_ok = getenv("PACIM_NO_WARP_BFS") == nullptr;
   S.warp_max = (uint32_t)std::min<uint64_t>(
       QCAP, getenv("PACIM_WARP_MAX") ? atoll(getenv("PACIM_WARP_MAX")) : QCAP);
+  // the hot sums of this build, if kept for this dense threshold (one window)
+  S.hotsum = (ctx->hot_any && ctx->hot_big_t == S.big_t && S.onew) ? ctx->hotsum.as<int64_t>()
+                                                                   : nullptr;
+  S.hot_root = ctx->d_hot.as<uint32_t>();
+  S.hot_size = ctx->d_hot_size.as<uint32_t>();
   S.ch = (uint32_t)env_u64("PACIM_CHUNK", CH_DEFAULT);
   S.lkeep = (uint32_t)std::min<uint64_t>(16, getenv("PACIM_LKEEP") ? atoll(getenv("PACIM_LKEEP")) : 2);
   S.hidx = ctx->hidx.as<uint32_t>();
