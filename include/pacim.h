@@ -99,8 +99,9 @@ typedef struct {
     uint64_t hla_entries;           /* live hub adjacency of the last build: (hub, sketch,
                                        neighbour) entries, 0 if not recorded */
     uint32_t hubs;                  /* rows of degree > the hub degree (PACIM_HUB_DEG) */
-    uint64_t select_hotsum_steps;   /* compressed: steps whose giant CCs were covered from the
-                                       build's hub sums (the hub chosen), without a rebuild */
+    uint64_t select_hotsum_steps;   /* steps whose giant hot (hub's) CCs were covered from the
+                                       build's per-vertex hot sums (compressed: no batch
+                                       rebuild; uncompressed: no dense pass) */
 } pacim_stats;
 
 /* --------------------------------------------------------------- lifecycle */

@@ -122,7 +122,7 @@ enum { QC_TAIL = 0, QC_HEAD = 16, QC_DONE = 32, QC_PROD = 48, QC_WORDS = 80 };
 // diagnostics (u64): steps, dense steps, warp-BFS slots, deferred slots,
 // row items, chunk items, chunks expanded inline (queue guard)
 enum { DG_STEPS = 0, DG_DENSE, DG_WARP, DG_DEFER, DG_ROWS, DG_CHUNKS, DG_INLINE, DG_ABORT,
-       DG_EDGES, DG_WORDS = 10 };
+       DG_EDGES, DG_HOT, DG_WORDS = 10 };
 constexpr unsigned long long WATCHDOG_NS = 20000000000ull;  // a 20 s wait is a bug: abort
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -1035,9 +1035,12 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) k_select(Sel S0, SelOut O, uin
       // the dense set exactly the giant hot (hub's) CCs, all covered now —
       // the build's per-vertex hot sums are the member updates (one vector
       // pass instead of a pass over the store; c2's first step)
-      if (!(S.hotsum && dense_hot(S.cov_root, S.hot_size, S.hot_root, S.big_t, S.B, S.hotsum,
-                                  S.target, S.nv, S.dlst, s, tid, nth)))
+      if (S.hotsum && dense_hot(S.cov_root, S.hot_size, S.hot_root, S.big_t, S.B, S.hotsum,
+                                S.target, S.nv, S.dlst, s, tid, nth)) {
+        if (tid == 0 && S.diag) atomicAdd(S.diag + DG_HOT, 1ull);
+      } else {
         apply_dense(S, s, gwarp, nwarps);
+      }
       if (tid == 0 && S.diag) atomicAdd(S.diag + DG_DENSE, 1ull);
       grid.sync();
     }
@@ -1409,6 +1412,7 @@ static void read_diag(pacim_ctx *ctx, const Sel &S) {
   ctx->stats.select_chunk_items = d[DG_CHUNKS];
   ctx->stats.select_inline_rows = d[DG_INLINE];
   ctx->stats.select_edges = d[DG_EDGES];
+  ctx->stats.select_hotsum_steps = d[DG_HOT];
   PC_REQUIRE(!d[DG_ABORT], PACIM_ECHECK, "select: traversal watchdog expired (internal error)");
 }
 

@@ -243,6 +243,22 @@ def test_too_many_sketches_fail_cleanly(ctx, pc):
     raise AssertionError("R = 2048 on one GPU must be rejected")
 
 
+def test_hot_sums_dense_step(orc, ctx, monkeypatch):
+    """The hub (a star's center) chosen first with its CCs above the dense
+    threshold in every sketch: the select covers them from the build's
+    per-vertex hot sums (one vector pass, no dense pass over the store); the
+    greedy equals the oracle's, and a second selection repeats it."""
+    from oracle.oracle import Graph
+    monkeypatch.setenv("PACIM_BIG_T", "8")
+    off, nbr = inputs.star_graph(50)
+    g = Graph(len(off) - 1, off, nbr)
+    full_parity(orc, ctx, g, 0, orc.t32_const(0.3), 64, 1008, 4)
+    assert ctx.pacim_get_stats()["select_hotsum_steps"] == 1
+    s, gn, sg, _ = ctx.pacim_select_seeds(4)
+    es, egn, esg, _ = orc.greedy(g, 0, orc.t32_const(0.3), 64, 1008, 4)
+    assert list(s) == list(es) and list(gn) == list(egn)
+
+
 def test_determinism(orc, ctx):
     from oracle.oracle import Graph
     off, nbr = inputs.random_powerlaw_graph(3000, 20000, 11)
