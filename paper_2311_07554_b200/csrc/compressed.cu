@@ -536,8 +536,10 @@ static uint32_t choose_batch(pacim_ctx *ctx) {
   // state, for CCs too big for a probe) and 2 GB of headroom; at least a third
   // (one batch of all 256 slots at c4 alpha = 1/8: build 132 -> 104 ms, one
   // edge pass instead of two)
-  const size_t sel = ctx->bfs.bytes ? 0 : pc_select_state_bytes(ctx->nr, B);
-  const size_t keep = sel + ((size_t)2 << 30);
+  // the selection's traversal state is not reserved: if it is needed later,
+  // the batch buffer is released first and re-created smaller on demand
+  // (pc_release_batch / the rebuild in pc_cover_compressed)
+  const size_t keep = (size_t)2 << 30;
   const size_t ample = fr > keep ? fr - keep : 0;
   // tight memory (c4 alpha = 1/2: 103 GB store): the old third, capped at
   // 24 GB — bigger batches there are re-allocated around the HLA every build
@@ -789,7 +791,18 @@ void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *l
       }
       unknown |= hst[j] == ST_BIG_UNKNOWN;
     }
-    if (tknown) pc_traverse_slots(ctx, s, target, tdl.data());
+    if (tknown) {
+      if (!ctx->bfs.bytes) {  // the traversal state's first allocation: make room
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        if (fr < pc_select_state_bytes(ctx->nr, B) + ((size_t)1 << 30)) {
+          PC_CUDA(cudaStreamSynchronize(ctx->stream));
+          pc_free(ctx, ctx->Ltmp);
+          pc_free(ctx, ctx->cwork);
+        }
+      }
+      pc_traverse_slots(ctx, s, target, tdl.data());
+    }
     known += tknown;
     if (tknown || changed)
       PC_CUDA(cudaMemcpyAsync(st, hst.data(), (size_t)B * 4, cudaMemcpyHostToDevice, ctx->stream));
@@ -804,6 +817,11 @@ void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *l
     PC_CUDA(cudaMemcpyAsync(&srow, ctx->cid.as<uint32_t>() + s, 4, cudaMemcpyDeviceToHost,
                             ctx->stream));
     PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (ctx->Ltmp.bytes < (size_t)nr * ctx->Bb * 4) {  // released for the traversal state
+      pc_free(ctx, ctx->cwork);
+      ctx->Bb = choose_batch(ctx);
+      pc_ensure(ctx, ctx->Ltmp, std::max<size_t>((size_t)nr * ctx->Bb, 1) * 4);
+    }
     const uint32_t Bb = ctx->Bb;
     uint32_t *Lb = ctx->Ltmp.as<uint32_t>();
     pc_ensure(ctx, ctx->scratch2, (size_t)Bb * 24 + 64);
