@@ -201,10 +201,15 @@ static void commit_staged(pacim_ctx *ctx) {
   PC_CUDA(cudaEventRecord(ctx->released, ctx->stream));
 }
 
-// a synchronous load replaces anything still pending
+// a synchronous load replaces anything still pending (and releases the
+// staging buffers: a graph loaded synchronously may need all the memory)
 static void drop_staged(pacim_ctx *ctx) {
   if (ctx->copy_stream) PC_CUDA(cudaStreamSynchronize(ctx->copy_stream));
-  ctx->stage[0].pending = ctx->stage[1].pending = false;
+  for (auto &g : ctx->stage) {
+    g.pending = false;
+    pc_free(ctx, g.off);
+    pc_free(ctx, g.nbr);
+  }
   ctx->stage_fill = ctx->stage_commit = 0;
 }
 
