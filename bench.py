@@ -111,9 +111,14 @@ def kernel_bytes(st: dict, cfg: dict, k: int) -> dict:
     L = 4 * rows * B                      # the store: one u32 slot per (row, sketch)
     wic = 4 * m if cfg["pmodel"] != 0 else 0  # per-edge thresholds (WIC, Uniform)
     nonroot = st["nnonsingle"] - st["ncomp"]
+    # the edge source is read once per build batch (compressed mode); a lean
+    # graph's source is the CSR (u32 per entry, 2m entries), else the upper
+    # edge list (u64 key + u64 row pair, + T32)
+    nb = -(-B // st["batch_slots"]) if st.get("compressed") and st.get("batch_slots") else 1
+    edge_src = 8 * m if st.get("lean") else 16 * m + wic
     return {
         "k_init": L,                                        # write every slot
-        "k_edges": 16 * m + wic + 8 * st["live_pairs"],     # key + row pair (+T32), 2 slot reads per live pair
+        "k_edges": nb * edge_src + 8 * st["live_pairs"],    # edge source per pass, 2 slot reads per live pair
         "k_compress_count": L + 8 * nonroot,                # read slots; write root + count per non-root
         "k_gain0": L + 8 * n + 4 * nonroot,                 # slots, gain0, root-size reads
         # traversal reads (CSR entry + WIC threshold) + the dense passes over the
@@ -124,11 +129,17 @@ def kernel_bytes(st: dict, cfg: dict, k: int) -> dict:
 
 
 def build_bytes(st: dict, cfg: dict) -> int:
-    """CSR_upper * ceil(R_g/B) + 16 n R_g (one pass, B = R_g)."""
-    csr_upper = 16 * st["m"]  # u64 hash key + u64 row pair per upper edge read by k_edges
+    """CSR_upper * ceil(R_g/B) + 16 n R_g (B = sketches per pass:
+    R_g uncompressed, the batch in compressed mode)."""
+    if st.get("lean"):
+        csr_upper = 8 * st["m"]  # the CSR itself (u32 per entry, 2m entries)
+    else:
+        csr_upper = 16 * st["m"]  # u64 hash key + u64 row pair per upper edge read by k_edges
     if cfg["pmodel"] != 0:
         csr_upper += 4 * st["m"]
-    return csr_upper + 16 * st["rows"] * st["R_local"]
+    B = st["R_local"]
+    nb = -(-B // st["batch_slots"]) if st.get("compressed") and st.get("batch_slots") else 1
+    return csr_upper * nb + 16 * st["rows"] * B
 
 
 def load_peaks():
@@ -377,7 +388,7 @@ def main():
                 "kernel_ms": {kk: round(v, 4) for kk, v in dur.items()},
                 "build": {"bytes": bb, "ms": round(avg["t_build_ms"], 4),
                           "achieved": round(build_gbs, 1), "frac": round(build_gbs / hbm, 4),
-                          "model": "SURVEY 8(d): CSR_upper*ceil(R_g/B) + 16*rows*R_g, B=R_g (rows = non-isolated vertices)"}}
+                          "model": "SURVEY 8(d): CSR_upper*ceil(R_g/B) + 16*rows*R_g, B = sketches per pass (R_g; the batch in compressed mode), rows = store rows; CSR_upper = the edge source k_edges reads (edge list, or the CSR itself for lean graphs)"}}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,

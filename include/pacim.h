@@ -102,6 +102,7 @@ typedef struct {
     uint64_t select_hotsum_steps;   /* steps whose giant hot (hub's) CCs were covered from the
                                        build's per-vertex hot sums (compressed: no batch
                                        rebuild; uncompressed: no dense pass) */
+    uint32_t lean;                  /* 1: lean graph (no edge lists; k_edges reads the CSR) */
 } pacim_stats;
 
 /* --------------------------------------------------------------- lifecycle */

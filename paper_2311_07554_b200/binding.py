@@ -53,6 +53,7 @@ class Stats(C.Structure):
         ("select_center_found", C.c_uint64), ("batch_slots", C.c_uint32),
         ("select_evaluations", C.c_uint64), ("select_eval_rounds", C.c_uint64),
         ("hla_entries", C.c_uint64), ("hubs", C.c_uint32), ("select_hotsum_steps", C.c_uint64),
+        ("lean", C.c_uint32),
     ]
 
     def asdict(self):

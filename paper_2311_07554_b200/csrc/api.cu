@@ -544,6 +544,7 @@ int pacim_get_stats(pacim_ctx *ctx, pacim_stats *out) {
     s.batch_slots = ctx->compressed ? ctx->Bb : 0;
     s.hla_entries = ctx->hla_ok ? ctx->hla_n : 0;
     s.hubs = ctx->nhub;
+    s.lean = ctx->lean ? 1u : 0u;
     s.nnonsingle = ctx->nnonsingle;
     s.device_bytes = ctx->device_bytes;
     *out = s;

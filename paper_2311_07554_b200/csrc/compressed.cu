@@ -624,14 +624,21 @@ void pc_build_compressed(pacim_ctx *ctx) {
   uint32_t *Lb = ctx->Ltmp.as<uint32_t>();
   uint32_t *croot = ctx->cwork.as<uint32_t>();
   PC_CUDA(cudaEventRecord(e1, ctx->stream));
+  // per batch: start, after init / edges / compress, after the gain pass
+  const uint32_t nbat = (B + Bb - 1) / Bb;
+  std::vector<cudaEvent_t> bev(5 * (size_t)nbat);
+  for (auto &e : bev) PC_CUDA(cudaEventCreate(&e));
   for (uint32_t j0 = 0; j0 < B; j0 += Bb) {
     const uint32_t bb = std::min(Bb, B - j0);
-    pc_sketch_pass(ctx, Lb, j0, bb, ctr, nullptr, rec_hla ? &hla : nullptr);
+    cudaEvent_t *ev = bev.data() + 5 * (size_t)(j0 / Bb);
+    PC_CUDA(cudaEventRecord(ev[0], ctx->stream));
+    pc_sketch_pass(ctx, Lb, j0, bb, ctr, ev + 1, rec_hla ? &hla : nullptr);
     k_gain_sizes<<<pc_grid(ctx, (size_t)nr * 32, 256, 16), 256, 0, ctx->stream>>>(
         Lb, nr, bb, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>(), ctr,
         ctx->d_hot.as<uint32_t>(), j0, ctx->cbig_t, ctx->d_hot_size.as<uint32_t>(),
         ctx->hotsum.as<int64_t>());
     PC_CHECK_LAUNCH();
+    PC_CUDA(cudaEventRecord(ev[4], ctx->stream));
     const size_t tot = (size_t)rho * bb;
     if (tot) {
       k_center_a<<<pc_grid(ctx, tot, 256), 256, 0, ctx->stream>>>(
@@ -669,8 +676,26 @@ void pc_build_compressed(pacim_ctx *ctx) {
   ctx->stats.live_pairs = h[4];
   ctx->stats.t_build_ms = ms_all;
   ctx->stats.t_centers_ms = ms_pre;
-  ctx->stats.t_init_ms = ctx->stats.t_edges_ms = ctx->stats.t_compress_ms = 0;
-  ctx->stats.t_compact_ms = ctx->stats.t_gain_ms = 0;
+  // kernel times summed over the batches (bench: per-kernel roofline)
+  double ti = 0, te = 0, tc = 0, tg = 0;
+  for (uint32_t bi = 0; bi < nbat; bi++) {
+    cudaEvent_t *ev = bev.data() + 5 * (size_t)bi;
+    float a = 0, b2 = 0, c = 0, d = 0;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b2, ev[1], ev[2]);
+    cudaEventElapsedTime(&c, ev[2], ev[3]);
+    cudaEventElapsedTime(&d, ev[3], ev[4]);
+    ti += a;
+    te += b2;
+    tc += c;
+    tg += d;
+  }
+  for (auto &e : bev) cudaEventDestroy(e);
+  ctx->stats.t_init_ms = ti;
+  ctx->stats.t_edges_ms = te;
+  ctx->stats.t_compress_ms = tc;
+  ctx->stats.t_compact_ms = 0;
+  ctx->stats.t_gain_ms = tg;
   ctx->stats.kernel_launches_build = ctx->launches;
 }
 
