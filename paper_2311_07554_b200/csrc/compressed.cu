@@ -711,6 +711,11 @@ void pc_select_reset_compressed(pacim_ctx *ctx) {
 // decrease by delta_r.  Returns sum_r delta_r.  Marks s as a seed.
 void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *local_gain) {
   const uint32_t B = ctx->R_local, nr = ctx->nr;
+  if (getenv("PACIM_FORCE_RELEASE")) {  // tests: every rebuild re-creates the batch buffer
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    pc_free(ctx, ctx->Ltmp);
+    pc_free(ctx, ctx->cwork);
+  }
   pc_ensure(ctx, ctx->cprobe, (size_t)B * 16 + 64);
   uint32_t *st = ctx->cprobe.as<uint32_t>(), *lab = st + B, *dl = lab + B;
   unsigned long long *sum = reinterpret_cast<unsigned long long *>(dl + B + (B & 1));

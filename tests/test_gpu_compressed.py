@@ -235,3 +235,15 @@ def test_compressed_hub_hotsum(orc, ctx, i, big, monkeypatch):
     run_case(orc, ctx, i, check_sketches=False)
     if i == 8:  # the star's center is the hub and the first seed
         assert ctx.pacim_get_stats()["select_hotsum_steps"] == 1
+
+
+@pytest.mark.parametrize("i", [2, 3, 9])
+def test_compressed_batch_buffer_released(orc, ctx, i, monkeypatch):
+    """The batch buffer released (forced before every cover step, as when the
+    selection's traversal state needs the room) and re-created by the
+    rebuilds of big CCs (threshold lowered, 3 sketches per batch): the
+    oracle's greedy."""
+    monkeypatch.setenv("PACIM_FORCE_RELEASE", "1")
+    monkeypatch.setenv("PACIM_CBIG_T", "40")
+    monkeypatch.setenv("PACIM_BATCH", "3")
+    run_case(orc, ctx, i, check_sketches=False)
