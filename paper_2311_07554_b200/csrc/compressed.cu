@@ -202,7 +202,9 @@ __device__ __forceinline__ bool live_edge(const ProbeParams &P, uint32_t x, uint
 // edge hashed once by the whole grid (a hub seed would otherwise be scanned
 // by every slot's probe warp).  Candidate slots from the bucket table (R2),
 // live test R3 / R4.
-__global__ void k_seed_live(ProbeParams P, uint32_t s, uint32_t *slive, uint32_t *scnt) {
+__global__ void k_seed_live(ProbeParams P, uint32_t s, const uint32_t *s_dev, uint32_t *slive,
+                            uint32_t *scnt) {
+  if (s_dev) s = *s_dev;  // the argmax on the device
   const uint64_t e0 = P.off[s], e1 = P.off[s + 1];
   for (uint64_t e = e0 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < e1;
        e += (uint64_t)gridDim.x * blockDim.x) {
@@ -240,7 +242,9 @@ __global__ void k_seed_live(ProbeParams P, uint32_t s, uint32_t *slive, uint32_t
 }
 
 // one warp per slot: BFS from s with a shared-memory queue and visited set
-__global__ void __launch_bounds__(PROBE_WARPS * 32) k_probe(ProbeParams P, uint32_t s) {
+__global__ void __launch_bounds__(PROBE_WARPS * 32) k_probe(ProbeParams P, uint32_t s,
+                                                             const uint32_t *s_dev) {
+  if (s_dev) s = *s_dev;  // the argmax on the device
   __shared__ uint32_t q[PROBE_WARPS][QCAP];
   __shared__ uint32_t hs[PROBE_WARPS][HCAP];
   __shared__ uint32_t tail[PROBE_WARPS], ovf[PROBE_WARPS], found[PROBE_WARPS];
@@ -709,7 +713,10 @@ void pc_select_reset_compressed(pacim_ctx *ctx) {
 
 // MarkSeed(s) on this ctx's compressed sketches; member gains in target
 // decrease by delta_r.  Returns sum_r delta_r.  Marks s as a seed.
-void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *local_gain) {
+void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *local_gain,
+                         const void *dsel, uint32_t *s_out, int64_t *g_out) {
+  const uint32_t *s_dev =
+      dsel ? reinterpret_cast<const uint32_t *>(static_cast<const char *>(dsel) + 8) : nullptr;
   const uint32_t B = ctx->R_local, nr = ctx->nr;
   if (getenv("PACIM_FORCE_RELEASE")) {  // tests: every rebuild re-creates the batch buffer
     PC_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -750,7 +757,7 @@ void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *l
     PC_CUDA(cudaMemsetAsync(scnt, 0, (size_t)B * 4, ctx->stream));
     P.slive = nullptr;
     P.scnt = nullptr;
-    k_seed_live<<<ctx->sm_count * 4, 256, 0, ctx->stream>>>(P, s, slive, scnt);
+    k_seed_live<<<ctx->sm_count * 4, 256, 0, ctx->stream>>>(P, s, s_dev, slive, scnt);
     PC_CHECK_LAUNCH();
     P.slive = slive;
     P.scnt = scnt;
@@ -761,12 +768,22 @@ void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *l
   P.dl = dl;
   P.sum = sum;
   k_probe<<<std::min<unsigned>((B + PROBE_WARPS - 1) / PROBE_WARPS, ctx->sm_count * 8),
-            PROBE_WARPS * 32, 0, ctx->stream>>>(P, s);
+            PROBE_WARPS * 32, 0, ctx->stream>>>(P, s, s_dev);
   PC_CHECK_LAUNCH();
   ctx->launches++;
   unsigned long long hs[5];
   PC_CUDA(cudaMemcpyAsync(hs, sum, 40, cudaMemcpyDeviceToHost, ctx->stream));
+  struct {
+    long long g;
+    uint32_t v, pad;
+  } hb{0, 0, 0};
+  if (dsel) PC_CUDA(cudaMemcpyAsync(&hb, dsel, 16, cudaMemcpyDeviceToHost, ctx->stream));
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (dsel) {  // the seed and its gain, with the probe's sums in one read-back
+    s = hb.v;
+    if (s_out) *s_out = hb.v;
+    if (g_out) *g_out = hb.g;
+  }
   ctx->stats.select_bfs_visits += hs[2];
   ctx->stats.select_center_visits += hs[3];
   ctx->stats.select_center_found += hs[4];
@@ -908,11 +925,10 @@ void pc_select_compressed(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *
   ctx->launches = 0;
   long long run = 0;
   for (uint32_t i = 0; i < k; i++) {
-    uint32_t s;
-    int64_t g;
-    pc_argmax(ctx, ctx->gain.as<int64_t>(), n, &s, &g);
-    int64_t got = 0;
-    pc_cover_compressed(ctx, s, ctx->gain.as<int64_t>(), &got);
+    uint32_t s = 0;
+    int64_t g = 0, got = 0;
+    const void *dsel = pc_argmax_async(ctx, ctx->gain.as<int64_t>(), n);
+    pc_cover_compressed(ctx, 0, ctx->gain.as<int64_t>(), &got, dsel, &s, &g);
     k_set_seed<<<1, 1, 0, ctx->stream>>>(ctx->gain.as<long long>(), ctx->is_seed.as<uint8_t>(), s,
                                          1);
     PC_CHECK_LAUNCH();

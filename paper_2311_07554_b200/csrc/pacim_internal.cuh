@@ -347,7 +347,12 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
 void pc_build_compressed(pacim_ctx *ctx);
 void pc_select_compressed(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
                           int64_t *sigma_num);
-void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *local_gain);
+// dsel (optional): the argmax left on the device by pc_argmax_async — the seed
+// is read from it by the kernels and returned in *s_out / *g_out after the
+// step's one read-back (s is then ignored)
+void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *local_gain,
+                         const void *dsel = nullptr, uint32_t *s_out = nullptr,
+                         int64_t *g_out = nullptr);
 void pc_select_reset_compressed(pacim_ctx *ctx);
 // select.cu: device bytes of the selection's traversal state for nr rows, B slots
 size_t pc_select_state_bytes(uint32_t nr, uint32_t B);
@@ -360,6 +365,7 @@ void pc_select_lazy(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_n
                     int64_t *sigma_num);
 void pc_cover_local(pacim_ctx *ctx, uint32_t s, int64_t *d_delta,
                     int64_t *local_gain);
+const void *pc_argmax_async(pacim_ctx *ctx, const int64_t *d_gain, uint32_t n);
 void pc_argmax(pacim_ctx *ctx, const int64_t *d_gain, uint32_t n, uint32_t *s,
                int64_t *g);
 // mc.cu (NEXT f3)

@@ -27,6 +27,7 @@
 // covered root slots is kept).  gain_num[i] = sum_j delta_j; the host checks
 // it against the argmax gain.
 #include <cooperative_groups.h>
+#include <cstddef>
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -1547,7 +1548,8 @@ void pc_cover_local(pacim_ctx *ctx, uint32_t s, int64_t *d_delta, int64_t *local
   *local_gain = (int64_t)h;
 }
 
-void pc_argmax(pacim_ctx *ctx, const int64_t *d_gain, uint32_t n, uint32_t *s, int64_t *g) {
+// the argmax (gain desc, id asc) left on the device: {i64 gain at +0, u32 id at +8}
+const void *pc_argmax_async(pacim_ctx *ctx, const int64_t *d_gain, uint32_t n) {
   unsigned grid = pc_grid(ctx, n, SEL_THREADS, 4);
   DevBuf &part = ctx->argmax_part;  // persistent: no allocation per step
   pc_ensure(ctx, part, (size_t)(grid + 1) * sizeof(Best));
@@ -1557,9 +1559,14 @@ void pc_argmax(pacim_ctx *ctx, const int64_t *d_gain, uint32_t n, uint32_t *s, i
   k_argmax_final<<<1, SEL_THREADS, 0, ctx->stream>>>(part.as<Best>(), grid,
                                                      part.as<Best>() + grid);
   PC_CHECK_LAUNCH();
+  static_assert(sizeof(Best) == 16 && offsetof(Best, v) == 8, "Best layout");
+  return part.as<Best>() + grid;
+}
+
+void pc_argmax(pacim_ctx *ctx, const int64_t *d_gain, uint32_t n, uint32_t *s, int64_t *g) {
+  const Best *d = static_cast<const Best *>(pc_argmax_async(ctx, d_gain, n));
   Best h;
-  PC_CUDA(cudaMemcpyAsync(&h, part.as<Best>() + grid, sizeof(Best), cudaMemcpyDeviceToHost,
-                          ctx->stream));
+  PC_CUDA(cudaMemcpyAsync(&h, d, sizeof(Best), cudaMemcpyDeviceToHost, ctx->stream));
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
   *s = h.v;
   *g = h.g;
