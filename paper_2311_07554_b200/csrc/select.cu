@@ -248,8 +248,20 @@ __device__ __forceinline__ void q_write(Item *ring, unsigned long long mask, uns
 struct LStack {
   uint32_t *row, *x, *cnt;  // shared memory of the warp
   uint32_t keep;
+  uint32_t *trow, *tn;      // rows expanded, touched in batches of 32 (off the hop's path)
 };
 constexpr uint32_t LCAP = 16;
+
+// the warp's pending touches, one lane per row (before the item is done)
+__device__ __forceinline__ void flush_touches(const Sel &S, const LStack *ls) {
+  const int lane = threadIdx.x & 31;
+  __syncwarp();
+  const uint32_t n = *ls->tn;
+  if ((uint32_t)lane < n) touch(S, ls->trow[lane]);
+  __syncwarp();
+  if (lane == 0) *ls->tn = 0;
+  __syncwarp();
+}
 
 // (row wr of vertex w, mask word wd) newly reached in the slots nb: schedule
 // its expansion (one queue entry per row at a time; bits arriving meanwhile
@@ -309,7 +321,7 @@ constexpr uint32_t QCAP = 512;
 constexpr uint32_t HCAP = 1024;
 constexpr uint64_t WARP_DEG = 1024;
 // + mask, nonzero-word list (u8), local stack (rows, vertices, count)
-constexpr uint32_t WARP_WORDS = QCAP + HCAP + 1 + MAX_BW + MAX_BW / 4 + 2 * 16 + 1;
+constexpr uint32_t WARP_WORDS = QCAP + HCAP + 1 + MAX_BW + MAX_BW / 4 + 2 * 16 + 1 + 33;
 
 // shared-memory words of the slot tables (shr[B] + tab[2^TB + 1] u16), 16-B aligned
 __host__ __device__ __forceinline__ uint32_t table_words(uint32_t B) {
@@ -498,18 +510,33 @@ __device__ __forceinline__ void expand_edge(const Sel &S, uint32_t x, uint32_t w
 // threshold loads of EU entries per lane are issued before any of them is
 // tested, so a 256-entry chunk costs about one memory latency, not eight.
 constexpr int EU = 8;
+__device__ __forceinline__ void load_batch(const Sel &S, uint64_t base, uint64_t eb,
+                                           uint32_t (&w)[EU], uint32_t (&tm)[EU]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int u = 0; u < EU; u++) {
+    const uint64_t e = base + lane + 32 * u;
+    w[u] = e < eb ? __ldcs(S.nbr + e) : NONE;
+    tm[u] = (e < eb && S.wic) ? __ldcs(S.tcsr + e) : 0u;
+  }
+}
+// pre (optional): the batch at ea already loaded, bounded by pe >= eb
 __device__ __forceinline__ void expand_range(const Sel &S, uint32_t x, uint64_t ea, uint64_t eb,
                                              const uint32_t *M, uint32_t s, const uint32_t *shr,
                                              const uint16_t *tab, const uint32_t *sdl,
-                                             const LStack *ls) {
+                                             const LStack *ls, uint32_t (*pw)[EU] = nullptr,
+                                             uint32_t (*ptm)[EU] = nullptr) {
   const int lane = threadIdx.x & 31;
   for (uint64_t base = ea; base < eb; base += 32 * EU) {
     uint32_t w[EU], tm[EU];
+    if (pw && base == ea) {
 #pragma unroll
-    for (int u = 0; u < EU; u++) {
-      const uint64_t e = base + lane + 32 * u;
-      w[u] = e < eb ? __ldcs(S.nbr + e) : NONE;
-      tm[u] = (e < eb && S.wic) ? __ldcs(S.tcsr + e) : 0u;
+      for (int u = 0; u < EU; u++) {
+        w[u] = base + lane + 32 * u < eb ? (*pw)[u] : NONE;
+        tm[u] = (*ptm)[u];
+      }
+    } else {
+      load_batch(S, base, eb, w, tm);
     }
 #pragma unroll
     for (int u = 0; u < EU; u++) {
@@ -571,6 +598,8 @@ __device__ uint64_t process_item(const Sel &S, uint32_t s, uint32_t row, uint32_
   const int lane = threadIdx.x & 31;
   uint64_t c_lo, c_hi;  // chunks expanded by this warp
   uint64_t e0, e1, nch;
+  uint32_t pw[EU], ptm[EU];
+  bool pre = false;
   if (cw == CW_ROW) {
     nrow++;
     e0 = S.off[x];  // issued before the flag exchange (independent)
@@ -580,12 +609,19 @@ __device__ uint64_t process_item(const Sel &S, uint32_t s, uint32_t row, uint32_
     if (lane == 0) exch_acq_rel(S.inq + row, 0u);
     __syncwarp();
     const uint32_t m = lane < S.BW ? atomicExch(S.pend + (size_t)row * S.BW + lane, 0u) : 0u;
+    // the first adjacency batch in flight with the exchange (CSR: immutable)
+    load_batch(S, e0, min(e1, e0 + 32 * EU), pw, ptm);
     if (lane < S.BW) wm[lane] = m;
     const uint32_t nzb = __ballot_sync(FULL, m != 0);
     const uint32_t nnz = __popc(nzb);
     if (m) wl[__popc(nzb & ((1u << lane) - 1))] = lane;
-    if (lane == 0) touch(S, row);  // its visited bits are cleared before the next step
+    // its visited bits are cleared before the next step: touched in the
+    // warp's batch (flushed before the item is done)
     __syncwarp();
+    if (*ls->tn == 32) flush_touches(S, ls);  // warp-uniform
+    if (lane == 0) ls->trow[(*ls->tn)++] = row;
+    __syncwarp();
+    pre = true;
     nch = (e1 - e0 + S.ch - 1) / S.ch;
     c_lo = 0;
     c_hi = nnz ? nch : 0;
@@ -624,7 +660,8 @@ __device__ uint64_t process_item(const Sel &S, uint32_t s, uint32_t row, uint32_
       if (done_items < nitems) {
         ninl++;  // the queue is full: expand the rest here (with the full mask;
                  // repeated tests of already visited slots are no-ops)
-        expand_range(S, x, e0, min(e1, e0 + S.ch), wm, s, shr, tab, sdl, ls);
+        expand_range(S, x, e0, min(e1, e0 + S.ch), wm, s, shr, tab, sdl, ls, &pw, &ptm);
+        pre = false;
         c_lo = 1 + done_items / nnz;
         c_hi = nch;
       } else {
@@ -644,7 +681,10 @@ __device__ uint64_t process_item(const Sel &S, uint32_t s, uint32_t row, uint32_
     c_hi = c_lo + 1;
   }
   const uint64_t ea = min(e1, e0 + c_lo * S.ch), eb = min(e1, e0 + c_hi * S.ch);
-  expand_range(S, x, ea, eb, wm, s, shr, tab, sdl, ls);
+  if (pre && ea == e0)
+    expand_range(S, x, ea, eb, wm, s, shr, tab, sdl, ls, &pw, &ptm);
+  else
+    expand_range(S, x, ea, eb, wm, s, shr, tab, sdl, ls);
   return eb > ea ? eb - ea : 0;
 }
 
@@ -762,6 +802,7 @@ __device__ unsigned long long queue_phase(const Sel &S, uint32_t s, uint32_t *wm
       __syncwarp();
     }
     nedg += nedges;
+    flush_touches(S, ls);  // before QC_DONE: quiescence implies every touch
     if (lane == 0 && S.ilog) {
       const unsigned long long at = atomicAdd(S.ilog, 1ull);
       if (at < S.ilog_cap) {
@@ -931,6 +972,10 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) k_select(Sel S0, SelOut O, uin
   lst.x = lst.row + LCAP;
   lst.cnt = lst.x + LCAP;
   lst.keep = S.lkeep;
+  lst.trow = lst.cnt + 1;
+  lst.tn = lst.trow + 32;
+  if ((threadIdx.x & 31) == 0) *lst.tn = 0;
+  __syncwarp();
   uint32_t *sdl = dsm + table_words(S.B) + SEL_WARPS * WARP_WORDS;  // block's copy of dl[B]
   __shared__ Best sh[33];
   load_tables(S, shr, tab);
