@@ -223,6 +223,7 @@ def main():
     ap.add_argument("--force-dist", action="store_true",
                     help="testing: NCCL process group and the per-step collectives even at one rank")
     args = ap.parse_args()
+    args.e2e_steps = max(1, args.e2e_steps)  # the e2e number needs at least one step
     cfg = inputs.config(args.config, **({"scale": args.scale} if args.scale else {}))
     if args.alpha is not None:
         cfg["alpha"] = args.alpha

@@ -492,6 +492,79 @@ __global__ void __launch_bounds__(256) k_gain0(const uint32_t *__restrict__ L, u
   add_count(ncc_ctr, ncc);
 }
 
+// k_gain0 for B <= 256 (HOT: with the hot sums): a lane's slots (j = lane + 32 i) are the same
+// in every row, so the giant hot roots and sizes sit in registers; empty
+// entries (j >= B, rows past n) read as HIGH | 0 — a root of size 0, never a
+// stored value — so no entry needs a validity test (the HOT pass was issue
+// bound: 73 % SM throughput at c2 / c3 in ncu)
+template <int GR, bool HOT>
+__global__ void __launch_bounds__(256, GR == 2 ? 4 : 2) k_gain0_fast(const uint32_t *__restrict__ L, uint32_t n,
+                                                   uint32_t B, const uint32_t *rmap,
+                                                   int64_t *gain0, unsigned long long *ncc_ctr,
+                                                   const uint32_t *hot, const uint32_t *hot_size,
+                                                   uint32_t big_t, int64_t *hotsum) {
+  constexpr uint32_t VOID = PACIM_HIGH;  // HIGH | 0
+  const int lane = threadIdx.x & 31;
+  uint32_t hr[8], hz[8];
+#pragma unroll
+  for (int i = 0; i < 8; i++) {
+    const uint32_t j = lane + 32 * i;
+    const bool giant = HOT && j < B && hot_size[j] > big_t;
+    hr[i] = giant ? hot[j] : NONE;  // NONE: never a row
+    hz[i] = giant ? hot_size[j] : 0u;
+  }
+  uint32_t ncc = 0;  // roots of size >= 2
+  const size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  for (size_t v0 = warp * GR; v0 < n; v0 += nw * GR) {
+    uint32_t sv[GR][8];
+#pragma unroll
+    for (int r = 0; r < GR; r++) {
+      const uint32_t *Lr = L + (v0 + r) * B;
+      const bool rv = v0 + r < n;
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const uint32_t j = lane + 32 * i;
+        sv[r][i] = (rv && j < B) ? Lr[j] : VOID;
+      }
+    }
+    unsigned long long hs[GR];
+#pragma unroll
+    for (int r = 0; r < GR; r++) {
+      hs[r] = 0;
+#pragma unroll
+      for (int i = 0; i < 8; i++) {
+        const uint32_t s = sv[r][i];
+        const bool isroot = (s & PACIM_HIGH) != 0;
+        const uint32_t root = isroot ? (uint32_t)(v0 + r) : s;
+        if (HOT) hs[r] += root == hr[i] ? hz[i] : 0u;
+        if (isroot)
+          ncc += (s & PACIM_LOW) >= 2;
+        else
+          sv[r][i] = __ldg(L + (size_t)s * B + lane + 32 * i);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < GR; r++) {
+      // sizes < 2^31: a pair sums in 32 bits
+      unsigned long long t = 0;
+#pragma unroll
+      for (int i = 0; i < 8; i += 2) t += (sv[r][i] & PACIM_LOW) + (sv[r][i + 1] & PACIM_LOW);
+      unsigned long long h = hs[r];
+      for (int d = 16; d; d >>= 1) {
+        t += __shfl_xor_sync(0xffffffffu, t, d);
+        if (HOT) h += __shfl_xor_sync(0xffffffffu, h, d);
+      }
+      if (lane == 0 && v0 + r < n) {
+        const uint32_t v = rmap[v0 + r];
+        gain0[v] = (long long)t;
+        if (HOT) hotsum[v] = (long long)h;
+      }
+    }
+  }
+  add_count(ncc_ctr, ncc);
+}
+
 // per slot the hot (hub's) CC size, read from its root slot after compression
 __global__ void k_hot_sizes(const uint32_t *L, uint32_t n, uint32_t B, const uint32_t *hot,
                             uint32_t *hot_size) {
@@ -1091,11 +1164,25 @@ void pc_build(pacim_ctx *ctx) {
       if (any) {
         pc_ensure(ctx, ctx->hotsum, (size_t)ctx->n * 8);
         PC_CUDA(cudaMemsetAsync(ctx->hotsum.p, 0, (size_t)ctx->n * 8, ctx->stream));  // isolated: 0
-        k_gain0<true><<<rows_grid, 256, 2 * std::min<uint32_t>(c, HOT_MAX) * sizeof(uint32_t),
-                        ctx->stream>>>(Lw, n, c, ctx->rmap.as<uint32_t>(),
-                                       ctx->gain0.as<int64_t>(), 0, ctr, ctx->d_hot.as<uint32_t>(),
-                                       ctx->d_hot_size.as<uint32_t>(), big_t,
-                                       ctx->hotsum.as<int64_t>());
+        const char *gr = getenv("PACIM_GAIN_HOT");  // A/B: 0 = the generic kernel
+        const int ghot = c <= 256 ? (gr ? atoi(gr) : 2) : 0;
+        if (ghot == 4) {
+          k_gain0_fast<4, true><<<rows_grid, 256, 0, ctx->stream>>>(
+              Lw, n, c, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>(), ctr,
+              ctx->d_hot.as<uint32_t>(), ctx->d_hot_size.as<uint32_t>(), big_t,
+              ctx->hotsum.as<int64_t>());
+        } else if (ghot) {
+          k_gain0_fast<2, true><<<rows_grid, 256, 0, ctx->stream>>>(
+              Lw, n, c, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>(), ctr,
+              ctx->d_hot.as<uint32_t>(), ctx->d_hot_size.as<uint32_t>(), big_t,
+              ctx->hotsum.as<int64_t>());
+        } else {
+          k_gain0<true><<<rows_grid, 256, 2 * std::min<uint32_t>(c, HOT_MAX) * sizeof(uint32_t),
+                          ctx->stream>>>(Lw, n, c, ctx->rmap.as<uint32_t>(),
+                                         ctx->gain0.as<int64_t>(), 0, ctr,
+                                         ctx->d_hot.as<uint32_t>(), ctx->d_hot_size.as<uint32_t>(),
+                                         big_t, ctx->hotsum.as<int64_t>());
+        }
       } else {
         k_gain0<false><<<rows_grid, 256, 0, ctx->stream>>>(Lw, n, c, ctx->rmap.as<uint32_t>(),
                                                           ctx->gain0.as<int64_t>(), 0, ctr,
