@@ -259,6 +259,26 @@ def test_hot_sums_dense_step(orc, ctx, monkeypatch):
     assert list(s) == list(es) and list(gn) == list(egn)
 
 
+@pytest.mark.parametrize("R,gr", [(100, "2"), (37, "2"), (256, "4"), (100, "0")])
+def test_hot_gain_pass_ragged(orc, ctx, monkeypatch, R, gr):
+    """The gain pass with hot sums (register-cached hot roots, B <= 256) on
+    a ragged sketch count and an odd row count, giant hot CCs in some slots
+    only (PACIM_BIG_T = 765 between the slots' hub CC sizes): gain0, labels and the
+    greedy equal the oracle's for both row groupings and the generic kernel."""
+    from oracle.oracle import Graph
+    monkeypatch.setenv("PACIM_BIG_T", "765")
+    monkeypatch.setenv("PACIM_GAIN_HOT", gr)
+    off, nbr = inputs.random_powerlaw_graph(2001, 9000, 21)
+    g = Graph(2001, off, nbr)
+    hub = int(np.argmax(np.diff(off)))
+    sizes = []
+    for r in range(R):  # the hub's CC per sketch: giant in some slots only
+        lab, _ = orc.sketch_labels(g, 0, orc.t32_const(0.12), 77, r)
+        sizes.append(int(np.sum(lab == lab[hub])))
+    assert min(sizes) <= 765 < max(sizes), (min(sizes), max(sizes))
+    full_parity(orc, ctx, g, 0, orc.t32_const(0.12), R, 77, 12, check_labels=R <= 100)
+
+
 def test_determinism(orc, ctx):
     from oracle.oracle import Graph
     off, nbr = inputs.random_powerlaw_graph(3000, 20000, 11)
