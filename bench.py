@@ -1,6 +1,9 @@
 """bench.py — sampled edge-tests/s and seconds-to-k-seeds of the PaC-IM hot path.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+Default workload: c4 = BASELINE.json configs[3] (twitter-shaped R-MAT scale
+26, WIC, R = 256, k = 100), the largest configuration that fits one GPU.
 
 One step = one pass of the whole hot path over the resident synthetic graph:
 pacim_build_sketches (hash + live test, union-find, compression, CC sizes in
@@ -20,8 +23,11 @@ Debugging: PACIM_BENCH_DEBUG=1 prints the e2e steps' wall times,
 PACIM_E2E_SYNC=1 uses the unpipelined pacim_load_graph in the e2e loop.  Timing: CUDA events on the library's stream (= torch's
 current stream), barrier + synchronize on both sides, max over ranks.
 
---impl reference times the CPU oracle (oracle/, single-threaded C) on a
-bounded sample of the same workload (rank 0 only).
+--impl reference times the CPU oracle (oracle/, plain C) on a bounded sample
+of the same workload (rank 0 only): per step, the oracle's BFS labelling of
+one sketch per host core (verify mode's sketch-parallel loop), on the graph
+made by the oracle's own generator.  cpu_baseline (N = 1, rank 0) times the
+same on the CSR read back from the device.
 """
 from __future__ import annotations
 
@@ -105,41 +111,37 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------ roofline model
-def kernel_bytes(st: dict, cfg: dict, k: int) -> dict:
-    """Algorithmic bytes per launch of each kernel."""
+def build_terms(st: dict, cfg: dict) -> dict:
+    """SURVEY §8(d), literally: Bytes_build = ceil(R_g/B) * CSR_upper + 16 n R_g
+    [+ ceil(R_g/B) * 4m for per-edge WIC / Uniform thresholds], CSR_upper =
+    4m + 8(n+1).  The label term is counted per store row (the non-isolated
+    vertices the method labels; an isolated vertex is a singleton in every
+    sketch and has no row) and, beside it, per vertex as the formula is
+    written.  Random union traffic is NOT in the denominator (§8(d)); its
+    model (64 B per live pair, uncached) is reported separately."""
     n, m, B, rows = st["n"], st["m"], st["R_local"], st["rows"]
-    L = 4 * rows * B                      # the store: one u32 slot per (row, sketch)
-    wic = 4 * m if cfg["pmodel"] != 0 else 0  # per-edge thresholds (WIC, Uniform)
-    nonroot = st["nnonsingle"] - st["ncomp"]
-    # the edge source is read once per build batch (compressed mode); a lean
-    # graph's source is the CSR (u32 per entry, 2m entries), else the upper
-    # edge list (u64 key + u64 row pair, + T32)
     nb = -(-B // st["batch_slots"]) if st.get("compressed") and st.get("batch_slots") else 1
-    edge_src = 8 * m if st.get("lean") else 16 * m + wic
+    csr = nb * ((4 * m + 8 * (n + 1)) + (4 * m if cfg["pmodel"] != 0 else 0))
+    return {"csr": csr, "label_rows": 16 * rows * B, "label_n": 16 * n * B, "passes": nb,
+            "union_random_model": 64 * st["live_pairs"]}
+
+
+def kernel_bytes(st: dict, cfg: dict, k: int) -> dict:
+    """Algorithmic bytes per launch of each build kernel, the §8(d) terms
+    split over the kernels that move them (label term: 4 B init write, 8 B
+    finalize read + write, 4 B gain-pass read per (row, sketch)), and of the
+    selection (§8(d) "Selection": 12 B per member update + 4 B per (step,
+    sketch) lookup; the argmax's 8n B per step is NOT counted: the chunk-maxima
+    tournament does not read the whole gain vector per step)."""
+    t = build_terms(st, cfg)
+    L = 4 * st["rows"] * st["R_local"]
     return {
-        "k_init": L,                                        # write every slot
-        "k_edges": nb * edge_src + 8 * st["live_pairs"],    # edge source per pass, 2 slot reads per live pair
-        "k_compress_count": L + 8 * nonroot,                # read slots; write root + count per non-root
-        "k_gain0": L + 8 * n + 4 * nonroot,                 # slots, gain0, root-size reads
-        # traversal reads (CSR entry + WIC threshold) + the dense passes over the
-        # store + one read of the gains per step for the chunk maxima (upper bound)
-        "k_select": (4 + (4 if cfg["pmodel"] != 0 else 0)) * st["select_edges"]
-                    + L * st["select_dense_steps"] + k * 16 * 4096,
+        "k_init": L,
+        "k_edges": t["csr"],
+        "k_compress_count": 2 * L,
+        "k_gain0": L + 8 * st["n"],
+        "k_select": 12 * st["select_member_updates"] + 4 * k * st["R_local"],
     }
-
-
-def build_bytes(st: dict, cfg: dict) -> int:
-    """CSR_upper * ceil(R_g/B) + 16 n R_g (B = sketches per pass:
-    R_g uncompressed, the batch in compressed mode)."""
-    if st.get("lean"):
-        csr_upper = 8 * st["m"]  # the CSR itself (u32 per entry, 2m entries)
-    else:
-        csr_upper = 16 * st["m"]  # u64 hash key + u64 row pair per upper edge read by k_edges
-    if cfg["pmodel"] != 0:
-        csr_upper += 4 * st["m"]
-    B = st["R_local"]
-    nb = -(-B // st["batch_slots"]) if st.get("compressed") and st.get("batch_slots") else 1
-    return csr_upper * nb + 16 * st["rows"] * B
 
 
 def load_peaks():
@@ -158,20 +160,38 @@ def load_traffic():
 
 
 # ----------------------------------------------------------- CPU baseline
-def oracle_sample(cfg, seconds_target=15.0, max_sketches=None, g=None):
-    """Time the oracle's BFS sketch labelling (single thread) on sketches
-    0,1,2,... of the workload until ~seconds_target; returns (tests/s, S, t, g)."""
+def host_info() -> dict:
+    model = ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                model = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
+
+
+def oracle_label_sample(g, cfg, sketches: int, threads: int):
+    """Label sketches 0..sketches-1 of the workload with the oracle's BFS
+    labelling (orc_verify with k = 0: the verify mode's sketch loop, one
+    sketch per thread at a time); returns (seconds, tests/s)."""
     from oracle import oracle as O
-    if g is None:
-        g = O.gen_config(cfg)
     model, t32 = O.model_args(cfg)
-    S, t = 0, 0.0
-    while t < seconds_target and (max_sketches is None or S < max_sketches) and S < cfg["R"]:
-        t0 = time.perf_counter()
-        O.sketch_labels(g, model, t32, cfg["hash_seed"], S)
-        t += time.perf_counter() - t0
-        S += 1
-    return (S * g.m / t if t > 0 else 0.0), S, t, g
+    t0 = time.perf_counter()
+    rc, _ = O.verify(g, model, t32, sketches, cfg["hash_seed"], [], [], threads=threads)
+    dt = time.perf_counter() - t0
+    assert rc == 0
+    return dt, sketches * g.m / dt
+
+
+def oracle_golden_seconds(name: str):
+    """Measured single-thread derive-mode seconds to k seeds (golden files)."""
+    try:
+        gold = json.load(open(os.path.join(ROOT, "tests", "golden", f"{name}.json")))
+        return gold.get("oracle_seconds", {}).get("greedy")
+    except OSError:
+        return None
 
 
 def run_reference(args, cfg):
@@ -179,15 +199,21 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     from oracle import oracle as O
-    g = O.gen_config(cfg)
-    per_step = max(1, args.ref_sketches)
+    threads = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    g = O.gen_config(cfg, threads=threads)
+    t_gen = time.perf_counter() - t0
+    per_step = args.ref_sketches or threads
     for _ in range(args.warmup):
-        oracle_sample(cfg, 1e9, per_step, g)  # bounded by per_step sketches
+        oracle_label_sample(g, cfg, per_step, threads)
     t = 0.0
     for _ in range(args.steps):
-        _, S, dt, _ = oracle_sample(cfg, 1e9, per_step, g)
+        dt, _ = oracle_label_sample(g, cfg, per_step, threads)
         t += dt
     value = args.steps * per_step * g.m / t
+    sample = (f"oracle BFS labelling (orc_verify's sketch loop, k = 0) of sketches 0..{per_step - 1} "
+              f"of {cfg['R']} per step of {cfg['name']}, {threads} threads (one sketch per thread); "
+              f"graph from the oracle's own (threaded) generator in {t_gen:.0f} s, untimed")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
@@ -195,9 +221,8 @@ def run_reference(args, cfg):
         "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
         "config": {"workload": cfg["name"], "n": g.n, "m": g.m, "R": cfg["R"], "k": cfg["k"],
                    "sample": f"{per_step} sketch(es) per step"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"oracle BFS labelling (orc_sketch_labels) of {per_step} of "
-                                   f"{cfg['R']} sketches per step of {cfg['name']}, 1 thread"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                         "sample": sample, **host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -209,7 +234,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c4",
+                    help="BASELINE.json config (default c4 = configs[3], the largest single-GPU one)")
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--alpha", type=float, default=None,
                     help="override the config's alpha (< 1: compressed store)")
@@ -217,8 +243,8 @@ def main():
                     help="override the R-MAT scale (c5 at full scale needs 8 GPUs)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=20)
-    ap.add_argument("--ref-sketches", type=int, default=2)
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-sketches", type=int, default=0,
+                    help="sketches per reference step (default: one per host core)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-dist", action="store_true",
                     help="testing: NCCL process group and the per-step collectives even at one rank")
@@ -245,7 +271,7 @@ def main():
     from paper_2311_07554_b200 import dist as pdist
     from paper_2311_07554_b200 import pipeline
     stream = torch.cuda.current_stream(dev)
-    ctx = P.Context(local, stream.cuda_stream)
+    ctx = P.Context(local, stream)  # torch's current stream (legacy default: cudaStreamLegacy)
     n, m = pipeline.generate(ctx, cfg)
     pm, t32 = pipeline.model_of(cfg)
     a32 = pipeline.center_a32_of(cfg)
@@ -371,25 +397,45 @@ def main():
     # ---------------- roofline (dominant kernel, live CUDA-event durations)
     peaks = load_peaks()
     hbm = peaks.get("hbm_gbs")
-    peak_src = "measured" if hbm else "fallback"
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if hbm else "fallback (B200_PROFILING.md)"
     hbm = hbm or 6650.0
+    st["select_member_updates"] = int(out[2][-1]) if len(out[2]) else 0  # N(S_k): one update each
     kb = kernel_bytes(st, cfg, k)
     dur = {"k_init": avg["t_init_ms"], "k_edges": avg["t_edges_ms"],
            "k_compress_count": avg["t_compress_ms"], "k_gain0": avg["t_gain_ms"],
            "k_select": avg["t_select_ms"]}
     dom = max(dur, key=lambda x: dur[x])
     achieved = kb[dom] / (dur[dom] / 1000.0) / 1e9
-    traffic = load_traffic().get(args.config, {}).get(dom)
-    bb = build_bytes(st, cfg)
-    build_gbs = bb / (avg["t_build_ms"] / 1000.0) / 1e9
+    traffic_all = load_traffic().get(args.config, {})
+    bt = build_terms(st, cfg)
+    tb = avg["t_build_ms"] / 1000.0
+    b_rows = bt["csr"] + bt["label_rows"]
+    b_n = bt["csr"] + bt["label_n"]
+    te = dur["k_edges"] / 1000.0
     roofline = {"bound": "hbm", "kernel": dom, "achieved": round(achieved, 1),
                 "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                "traffic": traffic, "peak_source": peak_src,
+                "traffic": traffic_all.get(dom), "peak_source": peak_src,
                 "share_of_step": round(dur[dom] / ms_step, 3),
                 "kernel_ms": {kk: round(v, 4) for kk, v in dur.items()},
-                "build": {"bytes": bb, "ms": round(avg["t_build_ms"], 4),
-                          "achieved": round(build_gbs, 1), "frac": round(build_gbs / hbm, 4),
-                          "model": "SURVEY 8(d): CSR_upper*ceil(R_g/B) + 16*rows*R_g, B = sketches per pass (R_g; the batch in compressed mode), rows = store rows; CSR_upper = the edge source k_edges reads (edge list, or the CSR itself for lean graphs)"}}
+                "kernel_bytes": kb,
+                "build": {"model": "SURVEY 8(d): ceil(R_g/B)*(CSR_upper [+4m WIC/Uniform]) + 16*rows*R_g, "
+                                   "CSR_upper = 4m + 8(n+1); rows = store rows (non-isolated vertices); "
+                                   "'frac_n' counts 16*n*R_g as the formula is written",
+                          "csr_bytes": bt["csr"], "label_bytes_rows": bt["label_rows"],
+                          "label_bytes_n": bt["label_n"], "passes": bt["passes"],
+                          "bytes": b_rows, "ms": round(avg["t_build_ms"], 4),
+                          "achieved": round(b_rows / tb / 1e9, 1),
+                          "frac": round(b_rows / tb / 1e9 / hbm, 4),
+                          "frac_n": round(b_n / tb / 1e9 / hbm, 4),
+                          "frac_vs_8TBs": round(b_rows / tb / 8e12, 4)},
+                "k_edges": {"bytes": bt["csr"], "ms": round(dur["k_edges"], 4),
+                            "achieved": round(bt["csr"] / te / 1e9, 1),
+                            "frac": round(bt["csr"] / te / 1e9 / hbm, 4),
+                            "union_random_bytes_model": bt["union_random_model"],
+                            "traffic": traffic_all.get("k_edges"),
+                            "note": "algorithmic = the CSR term only (8(d)); random union traffic "
+                                    "(64 B per live pair uncached) reported beside it; traffic = "
+                                    "ncu dram__bytes_read+write per launch (profiles/traffic.json)"}}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -411,16 +457,31 @@ def main():
         "roofline": roofline,
         "clocks": clk,
         "stats": {kk: st[kk] for kk in ("rows", "ncomp", "nnonsingle", "live_pairs", "device_bytes",
+                                        "select_member_updates",
                                         "select_dense_steps", "select_warp_slots",
                                         "select_deferred_slots", "select_row_items",
                                         "select_chunk_items", "select_edges")},
         "seeds_head": [int(x) for x in out[0][:8]],
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, S, t, _ = oracle_sample(cfg, args.cpu_seconds)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                                "sample": f"oracle BFS labelling of sketches 0..{S - 1} of {R} "
-                                          f"({t:.1f} s, 1 thread) of {cfg['name']}"}
+        # the oracle labels the CSR read back from the device (its sha256 equals
+        # the oracle generator's golden digest: tests/test_gpu_parity.py)
+        from oracle.oracle import Graph
+        threads = os.cpu_count() or 1
+        dt, v = oracle_label_sample(Graph(n, off, nbr), cfg, threads, threads)
+        per_sketch_1t = dt  # one sketch per thread: ~ one sketch's single-thread time
+        line["cpu_baseline"] = {
+            "value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"oracle BFS labelling (orc_verify's sketch loop) of sketches 0..{threads - 1} "
+                      f"of {R} of {cfg['name']}, {threads} threads, one sketch each ({dt:.1f} s), on "
+                      f"the CSR read back from the device",
+            "oracle_seconds_to_k_seeds": {
+                "derive_1_thread_measured": oracle_golden_seconds(args.config),
+                "verify_est_all_threads": round(dt * R / threads, 1),
+                "derive_est_1_thread": round(per_sketch_1t * R, 1),
+                "note": "derive_1_thread_measured: tests/golden/<cfg>.json (c1-c3); est: R sketch "
+                        "labellings at the sampled rate (the selection of c4 adds seconds)"},
+            **host_info()}
     if rank == 0:
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -107,11 +107,20 @@ typedef struct {
 
 /* --------------------------------------------------------------- lifecycle */
 
-/* Create a context on CUDA device `device`.  `cuda_stream` is a cudaStream_t
- * (e.g. torch.cuda.current_stream().cuda_stream) or NULL for a private
- * non-blocking stream.  *out receives the ctx.  EINVAL if out is NULL or the
- * device does not exist; ECUDA on runtime failure. */
-PACIM_API int pacim_create(pacim_ctx **out, int device, void *cuda_stream);
+/* Create a context on CUDA device `device`.
+ * workspace, ws_bytes: a caller-owned DEVICE buffer (e.g. a torch uint8
+ *   tensor's data_ptr(), 256-byte aligned) from which the ctx carves every
+ *   device allocation (first fit; ENOMEM when no hole is large enough), or
+ *   NULL / 0 for cudaMalloc.  The caller keeps it alive until pacim_destroy.
+ * cuda_stream: a cudaStream_t all work is ordered on (e.g.
+ *   torch.cuda.current_stream().cuda_stream; pass cudaStreamLegacy = (void*)1
+ *   for the legacy default stream, whose handle is 0), or NULL for a private
+ *   non-blocking stream.
+ * *out receives the ctx.  EINVAL if out is NULL, the device does not exist,
+ * only one of workspace / ws_bytes is given or the workspace is misaligned;
+ * ECUDA on runtime failure. */
+PACIM_API int pacim_create(pacim_ctx **out, int device, void *workspace, size_t ws_bytes,
+                           void *cuda_stream);
 
 /* Free every device allocation of the ctx and the ctx itself.  NULL is a no-op. */
 PACIM_API void pacim_destroy(pacim_ctx *ctx);

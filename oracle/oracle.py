@@ -23,7 +23,7 @@ def build(force: bool = False) -> str:
     """Compile the oracle with plain gcc -O2 (single-threaded, no intrinsics)."""
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC",
-                               "-o", LIB, SRC, "-lm"])
+                               "-o", LIB, SRC, "-lm", "-pthread"])
     return LIB
 
 
@@ -50,6 +50,7 @@ def lib():
             "orc_live": (i32, [u64, u32, u32, u32, u64]),
             "orc_sketch_labels": (C.c_long, [u32, P, P, i32, u64, u64, u32, P, P]),
             "orc_greedy": (i32, [u32, P, P, i32, u64, u32, u64, u32, P, P, P, P]),
+            "orc_verify": (i32, [u32, P, P, i32, u64, u32, u64, u32, P, P, i32, P]),
             "orc_is_center": (i32, [u64, u32, u64]),
             "orc_centers": (u32, [u32, u64, u64, P, P]),
             "orc_compressed_sketch": (i32, [u32, P, P, i32, u64, u64, u32, u64, P, P]),
@@ -60,6 +61,7 @@ def lib():
             "orc_gen_rmat": (C.c_long, [i32, u32, u64, u64, u64, i32, u64, P]),
             "orc_gen_grid": (C.c_long, [u32, u32, u64, u64, P]),
             "orc_csr_from_keys": (None, [u32, u64, P, P, P]),
+            "orc_gen_rmat_csr_mt": (C.c_long, [i32, u32, u64, u64, u64, i32, u64, i32, P, P, P, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -149,6 +151,25 @@ def gen_rmat(scale: int, ef: int, thr, permute: int, gen_seed: int) -> Graph:
     return csr_from_keys(1 << scale, keys)
 
 
+def gen_rmat_mt(scale: int, ef: int, thr, permute: int, gen_seed: int,
+                threads: int | None = None) -> Graph:
+    """Threaded copy of gen_rmat (same CSR bit for bit; input side only)."""
+    threads = threads or os.cpu_count() or 1
+    cap = ef << scale
+    keys = np.empty(cap, np.uint64)
+    tmp = np.empty(cap, np.uint64)
+    n = 1 << scale
+    off = np.empty(n + 1, np.uint64)
+    # the CSR has 2m entries, m <= cap: sized after the call from off[n]
+    nbr = np.empty(2 * cap, np.uint32)
+    m = lib().orc_gen_rmat_csr_mt(scale, ef, thr[0], thr[1], thr[2], permute, gen_seed, threads,
+                                  _p(keys), _p(tmp), _p(off), _p(nbr))
+    if m < 0:
+        raise MemoryError("orc_gen_rmat_csr_mt")
+    del tmp
+    return Graph(n, off, nbr[:2 * m].copy(), keys[:m].copy())
+
+
 def gen_grid(W: int, H: int, d32: int, gen_seed: int) -> Graph:
     keys = np.zeros(3 * W * H, np.uint64)
     m = lib().orc_gen_grid(W, H, d32, gen_seed, _p(keys))
@@ -156,8 +177,12 @@ def gen_grid(W: int, H: int, d32: int, gen_seed: int) -> Graph:
     return csr_from_keys(W * H, keys)
 
 
-def gen_config(cfg: dict) -> Graph:
+def gen_config(cfg: dict, threads: int | None = None) -> Graph:
+    """threads > 1: the threaded R-MAT generator (identical output)."""
     from inputs import GEN_ER, GEN_RMAT, GEN_GRID
+    if cfg["gen"] == GEN_RMAT and threads and threads > 1:
+        return gen_rmat_mt(cfg["scale"], cfg["ef"], cfg["rmat_t"], cfg["permute"], cfg["gen_seed"],
+                           threads)
     if cfg["gen"] == GEN_ER:
         return gen_er(cfg["n"], cfg["m"], cfg["gen_seed"])
     if cfg["gen"] == GEN_RMAT:
@@ -198,6 +223,28 @@ def greedy(g: Graph, model: int, t32: int, R: int, seed: int, k: int, want_gain0
     if rc != 0:
         raise RuntimeError(f"orc_greedy rc={rc}")
     return seeds, gain, sigma, gain0
+
+
+VERIFY_RC = {0: "certified", 1: "claimed gain differs from the oracle's gain of the claimed seed",
+             2: "another vertex beats the claimed seed (gain desc, id asc)",
+             3: "claimed seed repeats or is out of range", -1: "out of memory"}
+
+
+def verify(g: Graph, model: int, t32: int, R: int, seed: int, seeds, gain_num,
+           threads: int | None = None):
+    """Verify mode: certify a claimed greedy sequence.  Returns
+    (rc, info): rc 0 = the sequence is exactly derive mode's; info = (step,
+    oracle argmax, its gain, claimed seed's true gain) at the first failure,
+    (k, 0, 0, covered entries) on success."""
+    s = np.ascontiguousarray(np.asarray(seeds, dtype=np.uint32))
+    gn = np.ascontiguousarray(np.asarray(gain_num, dtype=np.int64))
+    assert len(s) == len(gn)
+    info = np.zeros(4, np.int64)
+    if threads is None:
+        threads = os.cpu_count() or 1
+    rc = lib().orc_verify(g.n, _p(g.off), _p(g.nbr), model, t32, R, seed, len(s), _p(s), _p(gn),
+                          int(threads), _p(info))
+    return int(rc), tuple(int(x) for x in info)
 
 
 def centers(n: int, seed: int, a32: int):

@@ -11,6 +11,8 @@
  * it); DESIGN.md §"Readings" (R1..R12) lists every choice the paper leaves open.
  *
  * Everything is integer; results are defined exactly (no tolerance).
+ * Single-threaded except orc_verify, which may split its sketches over
+ * threads ("sketch-parallel threads allowed").
  *
  * Functions and what pins them (tests/test_oracle_*.py):
  *   orc_mix64 ............ published splitmix64 output vectors (pinned)
@@ -28,6 +30,10 @@
  *   orc_greedy ........... brute-force set-union greedy on tiny inputs, closed
  *                          forms (p=0, p=1, star, path), (1-1/e)*OPT, exact
  *                          sigma by 2^m world enumeration across hash seeds (pinned)
+ *   orc_verify ........... verify mode: certifies a claimed
+ *                          (seed, gain) sequence with O(n) memory per thread;
+ *                          pinned by verify(orc_greedy(x)) = accepted and by
+ *                          rejection of every one-seed swap / gain +-1
  *   orc_compressed_sketch / orc_get_center / orc_greedy_alg3 ....
  *                          Alg. 3 transcribed; pinned by SPEC-style trivia and
  *                          by equality with orc_greedy (compression transparency)
@@ -38,6 +44,7 @@
 #include <stdlib.h>
 #include <string.h>
 #include <math.h>
+#include <pthread.h>
 
 #define ORC_UNSET 0xFFFFFFFFu
 
@@ -157,18 +164,33 @@ static uint64_t edge_t32(int model, uint64_t t32, const uint64_t *off,
 /* Sketch(r): connected components of G'_r (Alg. 3)         */
 /* ------------------------------------------------------------------------ */
 
+/* The live test of P:3-4 (R3) / R20 on a precomputed h = hash_edge(u,v,r):
+ * the same rule as orc_live / orc_live_decor with the sketch's constants
+ * K = mix64(hash_seed) and hash(r) computed once per sketch. */
+static int live_h(int model, uint64_t h, uint64_t T)
+{
+    if (T >= (1ull << 32)) return 1;
+    if ((model >> 8) == 1) return (orc_mix64(h) >> 32) < T;
+    return h < (T << 32);
+}
+
 /*
  * label[v] = smallest vertex id in v's CC of G'_r (reading R8: canonical
  * label); if size_of_v != NULL, size_of_v[v] = |C_r(v)|.  Plain BFS from every
  * unlabelled vertex in ascending id order, testing liveness of each adjacency
  * entry with the hash rule.  Returns the number of CCs, or -1 on OOM.
+ * nbr_deg (optional, WIC only) = deg(nbr[e]) per adjacency entry, so the WIC
+ * threshold of an entry needs no random read of off[] (verify mode at c4).
  */
-long orc_sketch_labels(uint32_t n, const uint64_t *off, const uint32_t *nbr,
-                       int model, uint64_t t32, uint64_t hash_seed, uint32_t r,
-                       uint32_t *label, uint32_t *size_of_v)
+static long sketch_labels(uint32_t n, const uint64_t *off, const uint32_t *nbr,
+                          const uint32_t *nbr_deg, int model, uint64_t t32,
+                          uint64_t hash_seed, uint32_t r, uint32_t *label,
+                          uint32_t *size_of_v)
 {
     uint32_t *queue = (uint32_t *)malloc((size_t)(n ? n : 1) * sizeof(uint32_t));
     if (!queue) return -1;
+    const uint64_t K = orc_mix64(hash_seed);
+    const uint64_t hr = orc_mix64(((1ull << 63) | (uint64_t)r) ^ K);   /* R2 */
     for (uint32_t v = 0; v < n; v++) label[v] = ORC_UNSET;
     long ncc = 0;
     for (uint32_t v = 0; v < n; v++) {
@@ -180,11 +202,15 @@ long orc_sketch_labels(uint32_t n, const uint64_t *off, const uint32_t *nbr,
             uint32_t x = queue[head++];
             for (uint64_t e = off[x]; e < off[x + 1]; e++) {
                 uint32_t w = nbr[e];
+                uint64_t a = x < w ? x : w, b = x < w ? w : x;
+                uint64_t h = hr ^ orc_mix64(((a << 32) | b) ^ K);      /* P:3 */
+                uint64_t T = (nbr_deg && (model & 0xFF) == 1)
+                                 ? orc_t32_wic(off[x + 1] - off[x], nbr_deg[e])
+                                 : edge_t32(model, t32, off, x, w);
+                if (!live_h(model, h, T)) continue;                   /* P:4 */
                 if (label[w] != ORC_UNSET) continue;
-                if (live_m(model, hash_seed, x, w, r, edge_t32(model, t32, off, x, w))) {
-                    label[w] = v;
-                    queue[tail++] = w;
-                }
+                label[w] = v;
+                queue[tail++] = w;
             }
         }
         if (size_of_v)
@@ -193,6 +219,13 @@ long orc_sketch_labels(uint32_t n, const uint64_t *off, const uint32_t *nbr,
     }
     free(queue);
     return ncc;
+}
+
+long orc_sketch_labels(uint32_t n, const uint64_t *off, const uint32_t *nbr,
+                       int model, uint64_t t32, uint64_t hash_seed, uint32_t r,
+                       uint32_t *label, uint32_t *size_of_v)
+{
+    return sketch_labels(n, off, nbr, NULL, model, t32, hash_seed, r, label, size_of_v);
 }
 
 /* BFS of C_r(s) over live edges; writes members to out[], returns count.
@@ -296,6 +329,232 @@ int orc_greedy(uint32_t n, const uint64_t *off, const uint32_t *nbr, int model,
 done:
     free(labels); free(sizev); free(gain); free(is_seed); free(covered);
     free(stamp); free(members);
+    return rc;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Verify mode (SURVEY §8(c) "Verify mode"; GeneralGreedy P:396-401, Alg. 1's */
+/* NextSeed / MarkSeed loop P:524-530, tie by id P:2285-2286)                 */
+/* ------------------------------------------------------------------------ */
+/*
+ * Certifies a CLAIMED greedy sequence (s_1..s_k, g_1..g_k) — e.g. the GPU's —
+ * for configs whose derive mode is out of reach (c4, c5): O(n) memory per
+ * thread, one BFS labelling per sketch, sketches split over `nthreads`
+ * threads (sketch-parallel only; nothing else is parallel except the argmax
+ * scan of step 2, whose result is order independent).
+ *
+ * With S_{i-1} = {s_1..s_{i-1}} and first_r(c) = the first i with s_i in CC c
+ * of sketch r (none: infinity), the greedy's step-i gain of v is
+ *     gain_i(v) = sum_r [first_r(C_r(v)) >= i] |C_r(v)|
+ *               = gain0(v) - sum_{j<i} B_j(v),
+ *     B_j(v)    = sum_{r : first_r(C_r(v)) = j} |C_r(v)|.
+ * 1. For each sketch r: label it (sketch_labels, the derive mode's BFS),
+ *    find first_r of the claimed seeds' CCs, add |C_r(v)| to gain0(v) for
+ *    every v, and append (v, |C_r(v)|) to the list of step first_r(C_r(v))
+ *    when that is finite (the members of C_r(s_j) first covered at step j).
+ * 2. Sweep i = 1..k with acc = gain_i: check
+ *    (a) acc[s_i] = g_i, and
+ *    (b) s_i is the argmax of acc over v not in S_{i-1} under (gain desc,
+ *        id asc) — derive mode's NextSeed;
+ *    then subtract B_i.
+ * By induction on i a sequence that passes is exactly derive mode's output.
+ *
+ * Returns 0 = certified, 1 = (a) fails, 2 = (b) fails, 3 = a claimed seed
+ * repeats or is >= n, -1 = out of memory.  info[4] (may be NULL) receives
+ * {failing step (0-based), the oracle's argmax at that step, its gain, the
+ * claimed seed's true gain}; on success {k, 0, 0, sum of the B lists}.
+ */
+/* One step's list B_j of one thread: (v, |C_r(v)|) pairs, switched to a
+ * dense int64[n] accumulator once it holds n pairs (giant CCs, e.g. c3's first
+ * seed), so the memory stays below min(8 len, 8 n) bytes. */
+typedef struct { uint32_t v, size; } orc_vs;
+typedef struct { orc_vs *a; size_t len, cap; int64_t *dense; } orc_vs_list;
+
+typedef struct {
+    uint32_t n; const uint64_t *off; const uint32_t *nbr; const uint32_t *nbr_deg;
+    int model; uint64_t t32;
+    uint32_t R; uint64_t hash_seed; uint32_t k; const uint32_t *seeds;
+    int64_t *gain0;                 /* shared, updated atomically */
+    uint32_t next_r;                /* shared sketch counter */
+    int oom;
+} orc_vctx;
+
+typedef struct {
+    orc_vctx *c;
+    orc_vs_list *steps;             /* k lists owned by this thread */
+} orc_vthr;
+
+static int vs_push(orc_vs_list *l, uint32_t n, uint32_t v, uint32_t size)
+{
+    if (l->dense) {
+        l->dense[v] += size;
+        l->len++;
+        return 0;
+    }
+    if (l->len == n) {
+        l->dense = (int64_t *)calloc(n, sizeof(int64_t));
+        if (!l->dense) return -1;
+        for (size_t j = 0; j < l->len; j++) l->dense[l->a[j].v] += l->a[j].size;
+        free(l->a);
+        l->a = NULL;
+        l->cap = 0;
+        l->dense[v] += size;
+        l->len++;
+        return 0;
+    }
+    if (l->len == l->cap) {
+        size_t cap = l->cap ? 2 * l->cap : 64;
+        if (cap > n) cap = n;
+        orc_vs *a = (orc_vs *)realloc(l->a, cap * sizeof(orc_vs));
+        if (!a) return -1;
+        l->a = a;
+        l->cap = cap;
+    }
+    l->a[l->len].v = v;
+    l->a[l->len].size = size;
+    l->len++;
+    return 0;
+}
+
+static void *verify_worker(void *arg)
+{
+    orc_vthr *t = (orc_vthr *)arg;
+    orc_vctx *c = t->c;
+    uint32_t n = c->n;
+    uint32_t *label = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+    uint32_t *size = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+    uint32_t *first = (uint32_t *)malloc((size_t)n * sizeof(uint32_t));
+    if (!label || !size || !first) {
+        __atomic_store_n(&c->oom, 1, __ATOMIC_RELAXED);
+        goto out;
+    }
+    for (uint32_t v = 0; v < n; v++) first[v] = ORC_UNSET;
+    for (;;) {
+        uint32_t r = __atomic_fetch_add(&c->next_r, 1, __ATOMIC_RELAXED);
+        if (r >= c->R || __atomic_load_n(&c->oom, __ATOMIC_RELAXED)) break;
+        if (sketch_labels(n, c->off, c->nbr, c->nbr_deg, c->model, c->t32, c->hash_seed, r,
+                          label, size) < 0) {
+            __atomic_store_n(&c->oom, 1, __ATOMIC_RELAXED);
+            break;
+        }
+        /* first_r(c): the first step whose seed lies in CC c (labels are CC ids) */
+        for (uint32_t i = 0; i < c->k; i++) {
+            uint32_t cc = label[c->seeds[i]];
+            if (first[cc] == ORC_UNSET) first[cc] = i;
+        }
+        for (uint32_t v = 0; v < n; v++) {
+            __atomic_fetch_add(&c->gain0[v], (int64_t)size[v], __ATOMIC_RELAXED);
+            uint32_t j = first[label[v]];
+            if (j != ORC_UNSET && vs_push(&t->steps[j], n, v, size[v]) < 0) {
+                __atomic_store_n(&c->oom, 1, __ATOMIC_RELAXED);
+                break;
+            }
+        }
+        for (uint32_t i = 0; i < c->k; i++) first[label[c->seeds[i]]] = ORC_UNSET;
+    }
+out:
+    free(label); free(size); free(first);
+    return NULL;
+}
+
+typedef struct { const uint64_t *off; const uint32_t *nbr; uint32_t *out; uint64_t lo, hi; } orc_degslice;
+
+static void *degslice_worker(void *arg)
+{
+    orc_degslice *d = (orc_degslice *)arg;
+    for (uint64_t e = d->lo; e < d->hi; e++)
+        d->out[e] = (uint32_t)(d->off[d->nbr[e] + 1] - d->off[d->nbr[e]]);
+    return NULL;
+}
+
+int orc_verify(uint32_t n, const uint64_t *off, const uint32_t *nbr, int model,
+               uint64_t t32, uint32_t R, uint64_t hash_seed, uint32_t k,
+               const uint32_t *seeds, const int64_t *gain_num, int nthreads,
+               int64_t *info)
+{
+    int rc = 0;
+    if (nthreads < 1) nthreads = 1;
+    for (uint32_t i = 0; i < k; i++)
+        if (seeds[i] >= n) {
+            if (info) { info[0] = i; info[1] = info[2] = info[3] = -1; }
+            return 3;
+        }
+    orc_vctx c = {n, off, nbr, NULL, model, t32, R, hash_seed, k, seeds, NULL, 0, 0};
+    uint32_t *nbr_deg = NULL;
+    if ((model & 0xFF) == 1) {   /* WIC: deg(nbr[e]) per entry, one pass (threads: slices) */
+        nbr_deg = (uint32_t *)malloc((size_t)(off[n] ? off[n] : 1) * sizeof(uint32_t));
+        pthread_t *dt = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+        orc_degslice *ds = (orc_degslice *)calloc((size_t)nthreads, sizeof(orc_degslice));
+        if (!nbr_deg || !dt || !ds) { free(nbr_deg); free(dt); free(ds); return -1; }
+        for (int t = 0; t < nthreads; t++) {
+            ds[t].off = off; ds[t].nbr = nbr; ds[t].out = nbr_deg;
+            ds[t].lo = off[n] * (uint64_t)t / (uint64_t)nthreads;
+            ds[t].hi = off[n] * (uint64_t)(t + 1) / (uint64_t)nthreads;
+            if (t) pthread_create(&dt[t], NULL, degslice_worker, &ds[t]);
+        }
+        degslice_worker(&ds[0]);
+        for (int t = 1; t < nthreads; t++) pthread_join(dt[t], NULL);
+        free(dt); free(ds);
+        c.nbr_deg = nbr_deg;
+    }
+    c.gain0 = (int64_t *)calloc(n ? n : 1, sizeof(int64_t));
+    uint8_t *is_seed = (uint8_t *)calloc(n ? n : 1, 1);
+    orc_vthr *thr = (orc_vthr *)calloc((size_t)nthreads, sizeof(orc_vthr));
+    pthread_t *tid = (pthread_t *)calloc((size_t)nthreads, sizeof(pthread_t));
+    if (!c.gain0 || !is_seed || !thr || !tid) { rc = -1; goto done; }
+    for (int t = 0; t < nthreads; t++) {
+        thr[t].c = &c;
+        thr[t].steps = (orc_vs_list *)calloc(k ? k : 1, sizeof(orc_vs_list));
+        if (!thr[t].steps) { rc = -1; goto done; }
+    }
+    /* Step 1: sketches, one BFS labelling each, split over the threads. */
+    for (int t = 1; t < nthreads; t++) pthread_create(&tid[t], NULL, verify_worker, &thr[t]);
+    verify_worker(&thr[0]);
+    for (int t = 1; t < nthreads; t++) pthread_join(tid[t], NULL);
+    if (c.oom) { rc = -1; goto done; }
+    /* Step 2: acc = gain_i, i = 1..k (acc reuses gain0's storage). */
+    int64_t *acc = c.gain0;
+    int64_t total = 0;
+    for (uint32_t i = 0; i < k; i++) {
+        uint32_t s = seeds[i];
+        if (is_seed[s]) {
+            if (info) { info[0] = i; info[1] = s; info[2] = -1; info[3] = -1; }
+            rc = 3;
+            goto done;
+        }
+        /* NextSeed: max gain over v not in S_{i-1}, smallest id on ties */
+        int64_t best = -1;
+        uint32_t arg = 0;
+        for (uint32_t v = 0; v < n; v++)
+            if (!is_seed[v] && acc[v] > best) { best = acc[v]; arg = v; }
+        if (acc[s] != gain_num[i] || arg != s) {
+            if (info) { info[0] = i; info[1] = arg; info[2] = best; info[3] = acc[s]; }
+            rc = acc[s] != gain_num[i] ? 1 : 2;
+            goto done;
+        }
+        is_seed[s] = 1;
+        /* MarkSeed: the CCs first covered at step i leave every member's gain */
+        for (int t = 0; t < nthreads; t++) {
+            orc_vs_list *l = &thr[t].steps[i];
+            if (l->dense)
+                for (uint32_t v = 0; v < n; v++) acc[v] -= l->dense[v];
+            else
+                for (size_t j = 0; j < l->len; j++) acc[l->a[j].v] -= l->a[j].size;
+            total += (int64_t)l->len;
+        }
+    }
+    if (info) { info[0] = k; info[1] = 0; info[2] = 0; info[3] = total; }
+done:
+    if (thr)
+        for (int t = 0; t < nthreads; t++) {
+            if (!thr[t].steps) continue;
+            for (uint32_t i = 0; i < k; i++) {
+                free(thr[t].steps[i].a);
+                free(thr[t].steps[i].dense);
+            }
+            free(thr[t].steps);
+        }
+    free(thr); free(tid); free(c.gain0); free(is_seed); free(nbr_deg);
     return rc;
 }
 
@@ -611,6 +870,192 @@ void orc_csr_from_keys(uint32_t n, uint64_t m, const uint64_t *keys,
         nbr[fill[b]++] = a;
     }
     free(fill);
+}
+
+/* ------------------------------------------------------------------------ */
+/* Threaded copy of the R-MAT input generator (same recipe, same output as    */
+/* orc_gen_rmat + orc_csr_from_keys, checked bit for bit in the tests): the   */
+/* c4 graph (1.6e9 samples) takes ~18 min single-threaded, too long for the   */
+/* bench's reference arm.  Input generation only; no method arithmetic.       */
+/* ------------------------------------------------------------------------ */
+
+typedef struct {
+    int scale, permute; uint64_t ta, tab, tabc, Kg;
+    uint64_t lo, hi;              /* sample range */
+    uint64_t *out; uint64_t cnt;  /* loop-free keys written at out[lo..] */
+} orc_gen_slice;
+
+static void *gen_slice_worker(void *arg)
+{
+    orc_gen_slice *g = (orc_gen_slice *)arg;
+    uint64_t c = 0;
+    for (uint64_t i = g->lo; i < g->hi; i++) {
+        uint64_t u = 0, v = 0;
+        for (int l = 0; l < g->scale; l++) {
+            uint64_t y = orc_mix64(g->Kg ^ (i * 64 + (uint64_t)l)) >> 11;
+            uint64_t bit = 1ull << (g->scale - 1 - l);
+            if (y < g->ta) {
+            } else if (y < g->tab) {
+                v |= bit;
+            } else if (y < g->tabc) {
+                u |= bit;
+            } else {
+                u |= bit;
+                v |= bit;
+            }
+        }
+        if (g->permute) { u = rmat_perm(u, g->scale); v = rmat_perm(v, g->scale); }
+        if (u == v) continue;
+        uint64_t a = u < v ? u : v, b = u < v ? v : u;
+        g->out[g->lo + c++] = (a << 32) | b;
+    }
+    g->cnt = c;
+    return NULL;
+}
+
+/* LSD radix sort of u64 keys, 16-bit digits, T threads (per-thread digit
+ * histograms of contiguous slices, so the scatter is stable). */
+typedef struct {
+    const uint64_t *src; uint64_t *dst; uint64_t lo, hi; int shift;
+    uint64_t *hist;   /* 65536 counts, then the thread's write cursors */
+    int phase;
+} orc_rs_slice;
+
+static void *rs_worker(void *arg)
+{
+    orc_rs_slice *r = (orc_rs_slice *)arg;
+    if (r->phase == 0) {
+        memset(r->hist, 0, 65536 * sizeof(uint64_t));
+        for (uint64_t i = r->lo; i < r->hi; i++) r->hist[(r->src[i] >> r->shift) & 0xFFFF]++;
+    } else {
+        for (uint64_t i = r->lo; i < r->hi; i++) {
+            uint64_t d = (r->src[i] >> r->shift) & 0xFFFF;
+            r->dst[r->hist[d]++] = r->src[i];
+        }
+    }
+    return NULL;
+}
+
+static int radix_sort_mt(uint64_t *a, uint64_t *tmp, uint64_t N, int T)
+{
+    orc_rs_slice *sl = (orc_rs_slice *)calloc((size_t)T, sizeof(orc_rs_slice));
+    pthread_t *tid = (pthread_t *)calloc((size_t)T, sizeof(pthread_t));
+    uint64_t *hist = (uint64_t *)malloc((size_t)T * 65536 * sizeof(uint64_t));
+    if (!sl || !tid || !hist) { free(sl); free(tid); free(hist); return -1; }
+    uint64_t *src = a, *dst = tmp;
+    for (int shift = 0; shift < 64; shift += 16) {
+        for (int ph = 0; ph < 2; ph++) {
+            for (int t = 0; t < T; t++) {
+                sl[t].src = src; sl[t].dst = dst; sl[t].shift = shift; sl[t].phase = ph;
+                sl[t].lo = N * (uint64_t)t / (uint64_t)T;
+                sl[t].hi = N * (uint64_t)(t + 1) / (uint64_t)T;
+                sl[t].hist = hist + (size_t)t * 65536;
+                if (t) pthread_create(&tid[t], NULL, rs_worker, &sl[t]);
+            }
+            rs_worker(&sl[0]);
+            for (int t = 1; t < T; t++) pthread_join(tid[t], NULL);
+            if (ph == 0) {  /* exclusive prefix over (digit, thread) */
+                uint64_t run = 0;
+                for (uint64_t d = 0; d < 65536; d++)
+                    for (int t = 0; t < T; t++) {
+                        uint64_t c = hist[(size_t)t * 65536 + d];
+                        hist[(size_t)t * 65536 + d] = run;
+                        run += c;
+                    }
+            }
+        }
+        uint64_t *x = src; src = dst; dst = x;
+    }
+    /* 4 passes: the sorted keys are back in a */
+    free(sl); free(tid); free(hist);
+    return 0;
+}
+
+typedef struct {
+    const uint64_t *hi_keys, *lo_keys;  /* sorted by (min, max) and by (max, min) */
+    uint64_t m; const uint64_t *off; uint32_t *nbr;
+    uint32_t v0, v1; uint64_t ph, pl;   /* rows [v0, v1); key cursors at v0 */
+} orc_csr_slice;
+
+static void *csr_worker(void *arg)
+{
+    orc_csr_slice *c = (orc_csr_slice *)arg;
+    uint64_t ph = c->ph, pl = c->pl;
+    for (uint32_t x = c->v0; x < c->v1; x++) {
+        uint64_t w = c->off[x];
+        /* neighbours a < x: keys (a, x), listed by the (max, min) order */
+        while (pl < c->m && (c->lo_keys[pl] >> 32) == x) c->nbr[w++] = (uint32_t)c->lo_keys[pl++];
+        /* neighbours b > x: keys (x, b) */
+        while (ph < c->m && (c->hi_keys[ph] >> 32) == x) c->nbr[w++] = (uint32_t)c->hi_keys[ph++];
+    }
+    return NULL;
+}
+
+static uint64_t lower_bound_hi(const uint64_t *k, uint64_t m, uint64_t x)
+{
+    uint64_t lo = 0, hi = m;
+    while (lo < hi) {
+        uint64_t mid = lo + (hi - lo) / 2;
+        if ((k[mid] >> 32) < x) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+}
+
+/* R-MAT graph -> CSR (off n+1, nbr 2m), threaded; keys_out (capacity ef 2^s)
+ * receives the sorted distinct upper keys, tmp is scratch of the same size.
+ * Returns m, or -1 on OOM. */
+long orc_gen_rmat_csr_mt(int scale, uint32_t ef, uint64_t ta, uint64_t tab, uint64_t tabc,
+                         int permute, uint64_t gen_seed, int T, uint64_t *keys_out,
+                         uint64_t *tmp, uint64_t *off, uint32_t *nbr)
+{
+    if (T < 1) T = 1;
+    uint64_t ns = (uint64_t)ef << scale, n = 1ull << scale;
+    orc_gen_slice *gs = (orc_gen_slice *)calloc((size_t)T, sizeof(orc_gen_slice));
+    pthread_t *tid = (pthread_t *)calloc((size_t)T, sizeof(pthread_t));
+    if (!gs || !tid) { free(gs); free(tid); return -1; }
+    for (int t = 0; t < T; t++) {
+        gs[t] = (orc_gen_slice){scale, permute, ta, tab, tabc, gen_key(gen_seed),
+                                ns * (uint64_t)t / (uint64_t)T, ns * (uint64_t)(t + 1) / (uint64_t)T,
+                                keys_out, 0};
+        if (t) pthread_create(&tid[t], NULL, gen_slice_worker, &gs[t]);
+    }
+    gen_slice_worker(&gs[0]);
+    for (int t = 1; t < T; t++) pthread_join(tid[t], NULL);
+    uint64_t cnt = 0;
+    for (int t = 0; t < T; t++) {
+        memmove(keys_out + cnt, keys_out + gs[t].lo, gs[t].cnt * sizeof(uint64_t));
+        cnt += gs[t].cnt;
+    }
+    free(gs);
+    if (radix_sort_mt(keys_out, tmp, cnt, T) < 0) { free(tid); return -1; }
+    uint64_t m = 0;
+    for (uint64_t i = 0; i < cnt; i++)
+        if (m == 0 || keys_out[m - 1] != keys_out[i]) keys_out[m++] = keys_out[i];
+    /* degrees and offsets */
+    for (uint64_t v = 0; v <= n; v++) off[v] = 0;
+    for (uint64_t e = 0; e < m; e++) {
+        off[(keys_out[e] >> 32) + 1]++;
+        off[(keys_out[e] & 0xFFFFFFFFull) + 1]++;
+    }
+    for (uint64_t v = 0; v < n; v++) off[v + 1] += off[v];
+    /* the (max, min) order: swapped keys, sorted */
+    for (uint64_t e = 0; e < m; e++) tmp[e] = (keys_out[e] << 32) | (keys_out[e] >> 32);
+    uint64_t *tmp2 = (uint64_t *)malloc((size_t)(m ? m : 1) * sizeof(uint64_t));
+    if (!tmp2 || radix_sort_mt(tmp, tmp2, m, T) < 0) { free(tmp2); free(tid); return -1; }
+    free(tmp2);
+    orc_csr_slice *cs = (orc_csr_slice *)calloc((size_t)T, sizeof(orc_csr_slice));
+    if (!cs) { free(tid); return -1; }
+    for (int t = 0; t < T; t++) {
+        uint32_t v0 = (uint32_t)(n * (uint64_t)t / (uint64_t)T);
+        uint32_t v1 = (uint32_t)(n * (uint64_t)(t + 1) / (uint64_t)T);
+        cs[t] = (orc_csr_slice){keys_out, tmp, m, off, nbr, v0, v1,
+                                lower_bound_hi(keys_out, m, v0), lower_bound_hi(tmp, m, v0)};
+        if (t) pthread_create(&tid[t], NULL, csr_worker, &cs[t]);
+    }
+    csr_worker(&cs[0]);
+    for (int t = 1; t < T; t++) pthread_join(tid[t], NULL);
+    free(cs); free(tid);
+    return (long)m;
 }
 
 /* ------------------------------------------------------------------------ */

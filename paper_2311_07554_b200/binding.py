@@ -76,7 +76,7 @@ def lib():
         L = C.CDLL(_LIB_PATH)
         P, u32, u64, i32 = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int
         sig = {
-            "pacim_create": (i32, [C.POINTER(P), i32, P]),
+            "pacim_create": (i32, [C.POINTER(P), i32, P, C.c_size_t, P]),
             "pacim_destroy": (None, [P]),
             "pacim_last_error": (C.c_char_p, [P]),
             "pacim_version": (C.c_char_p, []),
@@ -138,12 +138,32 @@ def _dptr(t) -> C.c_void_p:
 class Context:
     """One pacim_ctx on one CUDA device (one per process/GPU)."""
 
-    def __init__(self, device: int = 0, stream=None):
+    def __init__(self, device: int = 0, stream=None, workspace=None):
+        """stream: a cudaStream_t (int) or a torch stream; default: torch's
+        current stream on `device` (the legacy default stream is passed as
+        cudaStreamLegacy), so library work is ordered with torch's work on the
+        tensors it reads or writes (pacim_gain0_to_device, apply_*, ...).
+        workspace: optional torch CUDA tensor (or (ptr, bytes)) the ctx
+        carves all its device memory from (pacim_create's workspace)."""
         self._L = lib()
         h = C.c_void_p()
+        if stream is None:
+            try:
+                import torch
+                if torch.cuda.is_available():
+                    stream = torch.cuda.current_stream(device).cuda_stream or 1  # 1: cudaStreamLegacy
+            except ImportError:
+                stream = None
         s = C.c_void_p(stream) if isinstance(stream, int) else (
-            C.c_void_p(stream.cuda_stream) if stream is not None else None)
-        rc = self._L.pacim_create(C.byref(h), int(device), s)
+            C.c_void_p(stream.cuda_stream or 1) if stream is not None else None)
+        if workspace is None:
+            wp, wb = None, 0
+        elif isinstance(workspace, tuple):
+            wp, wb = C.c_void_p(workspace[0]), int(workspace[1])
+        else:
+            wp, wb = C.c_void_p(workspace.data_ptr()), workspace.numel() * workspace.element_size()
+        self._ws = workspace  # kept alive as long as the ctx
+        rc = self._L.pacim_create(C.byref(h), int(device), wp, wb, s)
         if rc != 0:
             raise PacimError(rc, self._L.pacim_last_error(None).decode())
         self._h = h

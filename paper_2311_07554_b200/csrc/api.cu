@@ -3,26 +3,92 @@
 // capture; all compute is delegated to graph.cu / build.cu / select.cu.
 #include <cmath>
 #include <cstring>
+#include <iterator>
 
 #include "pacim_internal.cuh"
 
 static std::string g_create_err;
 
+// Device allocation: cudaMalloc, or first-fit sub-allocation from the
+// caller's workspace (pacim_create's torch-owned buffer, SURVEY 8(b)
+// ownership: "the ctx owns every device allocation, which it sub-allocates
+// from the torch workspace when one is given").  256-byte alignment.
+static void *ws_alloc(pacim_ctx *ctx, size_t bytes) {
+  bytes = (bytes + 255) & ~(size_t)255;
+  for (auto it = ctx->ws_free.begin(); it != ctx->ws_free.end(); ++it) {
+    if (it->second < bytes) continue;
+    const size_t off = it->first, len = it->second;
+    ctx->ws_free.erase(it);
+    if (len > bytes) ctx->ws_free[off + bytes] = len - bytes;
+    ctx->ws_used[off] = bytes;
+    return (char *)ctx->ws_base + off;
+  }
+  return nullptr;
+}
+
+static void ws_release(pacim_ctx *ctx, void *p) {
+  const size_t off = (size_t)((char *)p - (char *)ctx->ws_base);
+  auto u = ctx->ws_used.find(off);
+  if (u == ctx->ws_used.end()) return;
+  size_t start = off, len = u->second;
+  ctx->ws_used.erase(u);
+  auto nx = ctx->ws_free.lower_bound(start);
+  if (nx != ctx->ws_free.end() && nx->first == start + len) {  // merge with the next hole
+    len += nx->second;
+    nx = ctx->ws_free.erase(nx);
+  }
+  if (nx != ctx->ws_free.begin()) {  // and with the previous one
+    auto pv = std::prev(nx);
+    if (pv->first + pv->second == start) {
+      start = pv->first;
+      len += pv->second;
+      ctx->ws_free.erase(pv);
+    }
+  }
+  ctx->ws_free[start] = len;
+}
+
+void pc_mem_info(pacim_ctx *ctx, size_t *fr, size_t *tot) {
+  if (ctx->ws_base) {
+    *fr = pc_mem_free(ctx);
+    *tot = ctx->ws_bytes;
+  } else {
+    cudaMemGetInfo(fr, tot);
+  }
+}
+
+size_t pc_mem_free(pacim_ctx *ctx) {
+  if (ctx->ws_base) {
+    size_t best = 0;
+    for (auto &h : ctx->ws_free) best = std::max(best, h.second);
+    return best;
+  }
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  return fr;
+}
+
 void pc_ensure(pacim_ctx *ctx, DevBuf &b, size_t bytes) {
   if (bytes <= b.bytes && b.p) return;
-  if (b.p) {
-    cudaFree(b.p);
-    ctx->device_bytes -= b.bytes;
-    b.p = nullptr;
-    b.bytes = 0;
-  }
+  if (b.p) pc_free(ctx, b);
   if (bytes == 0) bytes = 16;
-  cudaError_t e = cudaMalloc(&b.p, bytes);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    b.p = nullptr;
-    throw PacimError{PACIM_ENOMEM, "cudaMalloc(" + std::to_string(bytes) +
-                                       " bytes) failed: " + cudaGetErrorString(e)};
+  if (ctx->ws_base) {
+    // stream-ordered reuse: work already queued may still read a block that
+    // was released, so a workspace allocation waits for the stream first
+    cudaStreamSynchronize(ctx->stream);
+    b.p = ws_alloc(ctx, bytes);
+    if (!b.p)
+      throw PacimError{PACIM_ENOMEM, "workspace: no free block of " + std::to_string(bytes) +
+                                         " bytes (largest " + std::to_string(pc_mem_free(ctx)) +
+                                         ")"};
+  } else {
+    cudaError_t e = cudaMalloc(&b.p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      b.p = nullptr;
+      throw PacimError{PACIM_ENOMEM, "cudaMalloc(" + std::to_string(bytes) +
+                                         " bytes) failed: " + cudaGetErrorString(e)};
+    }
   }
   b.bytes = bytes;
   ctx->device_bytes += bytes;
@@ -30,7 +96,12 @@ void pc_ensure(pacim_ctx *ctx, DevBuf &b, size_t bytes) {
 
 void pc_free(pacim_ctx *ctx, DevBuf &b) {
   if (b.p) {
-    cudaFree(b.p);
+    if (ctx->ws_base) {
+      cudaStreamSynchronize(ctx->stream);
+      ws_release(ctx, b.p);
+    } else {
+      cudaFree(b.p);
+    }
     ctx->device_bytes -= b.bytes;
   }
   b.p = nullptr;
@@ -102,7 +173,8 @@ uint64_t pacim_threshold_from_p(double p) {
   return (uint64_t)std::floor(p * 4294967296.0);
 }
 
-int pacim_create(pacim_ctx **out, int device, void *cuda_stream) {
+int pacim_create(pacim_ctx **out, int device, void *workspace, size_t ws_bytes,
+                 void *cuda_stream) {
   if (!out) return PACIM_EINVAL;
   *out = nullptr;
   int cnt = 0;
@@ -115,8 +187,21 @@ int pacim_create(pacim_ctx **out, int device, void *cuda_stream) {
     g_create_err = "no such CUDA device";
     return PACIM_EINVAL;
   }
+  if ((workspace == nullptr) != (ws_bytes == 0)) {
+    g_create_err = "workspace and ws_bytes must be given together";
+    return PACIM_EINVAL;
+  }
+  if (workspace && ((uintptr_t)workspace & 255)) {
+    g_create_err = "workspace must be 256-byte aligned";
+    return PACIM_EINVAL;
+  }
   pacim_ctx *ctx = new pacim_ctx();
   ctx->device = device;
+  if (workspace) {
+    ctx->ws_base = workspace;
+    ctx->ws_bytes = ws_bytes & ~(size_t)255;
+    ctx->ws_free[0] = ctx->ws_bytes;
+  }
   e = cudaSetDevice(device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount,
                                                    device);

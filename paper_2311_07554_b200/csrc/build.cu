@@ -862,14 +862,14 @@ bool pc_hla_begin(pacim_ctx *ctx, Hla *hla, double max_per_edge) {
   const size_t keys = (size_t)ctx->nhub * B + 1;
   if (keys >= (1ull << 32)) return false;  // key field of an entry is 32 bits
   size_t fr = 0, tot = 0;
-  cudaMemGetInfo(&fr, &tot);
+  pc_mem_info(ctx, &fr, &tot);
   // raw + the sort's second buffer (8 B each), grouped rows (4 B), offsets
   const size_t need = (cap + 1) * 20 + keys * 8 + (64ull << 20);
   if (need > fr / 4 && ctx->Ltmp.bytes) {
     // a compressed build's batch buffer kept from the previous build: release
     // it (the batch is sized after the HLA) rather than build without the HLA
     pc_free(ctx, ctx->Ltmp);
-    cudaMemGetInfo(&fr, &tot);
+    pc_mem_info(ctx, &fr, &tot);
   }
   if (need > fr / 4) return false;
   pc_ensure(ctx, ctx->hla_raw, (cap + 1) * 8);

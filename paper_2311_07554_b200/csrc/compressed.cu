@@ -534,7 +534,7 @@ static uint32_t choose_batch(pacim_ctx *ctx) {
   const uint32_t B = ctx->R_local;
   if (const char *e = getenv("PACIM_BATCH")) return std::max<uint32_t>(1, std::min<uint32_t>(B, atoi(e)));
   size_t fr = 0, tot = 0;
-  cudaMemGetInfo(&fr, &tot);
+  pc_mem_info(ctx, &fr, &tot);
   fr += ctx->Ltmp.bytes + ctx->cwork.bytes;  // earlier batch buffers: reused or freed before growing
   // everything but what the selection will still allocate (its traversal
   // state, for CCs too big for a probe) and 2 GB of headroom; at least a third
@@ -841,7 +841,7 @@ void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *l
     if (tknown) {
       if (!ctx->bfs.bytes) {  // the traversal state's first allocation: make room
         size_t fr = 0, tot = 0;
-        cudaMemGetInfo(&fr, &tot);
+        pc_mem_info(ctx, &fr, &tot);
         if (fr < pc_select_state_bytes(ctx->nr, B) + ((size_t)1 << 30)) {
           PC_CUDA(cudaStreamSynchronize(ctx->stream));
           pc_free(ctx, ctx->Ltmp);

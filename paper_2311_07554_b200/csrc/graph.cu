@@ -476,7 +476,7 @@ static void derive_lean(pacim_ctx *ctx) {
 static bool want_lean(pacim_ctx *ctx) {
   if (const char *e = getenv("PACIM_LEAN")) return atoi(e) != 0;
   size_t fr = 0, tot = 0;
-  cudaMemGetInfo(&fr, &tot);
+  pc_mem_info(ctx, &fr, &tot);
   return ctx->pmodel == PACIM_P_CONST && 16 * ctx->m > tot / 3;
 }
 
@@ -955,7 +955,7 @@ void pc_generate(pacim_ctx *ctx, int kind, const uint64_t *params, int nparams,
       while ((1 << bbits) < atoi(e) && bbits < scale) bbits++;
     } else {
       size_t fr = 0, tot = 0;
-      cudaMemGetInfo(&fr, &tot);
+      pc_mem_info(ctx, &fr, &tot);
       if (32 * ns > fr / 3)  // a bucket holds ~2 ns / NB pairs at 32 B each in flight
         while (bbits < scale && ((64 * ns) >> bbits) > fr / 3) bbits++;
     }

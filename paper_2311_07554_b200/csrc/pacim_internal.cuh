@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <map>
 #include <string>
 #include <vector>
 
@@ -121,6 +122,11 @@ struct pacim_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // caller-owned workspace (pacim_create): every device buffer is carved
+  // from it (first fit, 256-B aligned) instead of cudaMalloc
+  void *ws_base = nullptr;
+  size_t ws_bytes = 0;
+  std::map<size_t, size_t> ws_free, ws_used;  // offset -> length
   std::string err;
   int sm_count = 148;
   uint64_t device_bytes = 0;
@@ -248,9 +254,13 @@ struct pacim_ctx {
   cudaEvent_t released = nullptr;  // main stream: the last commit's old buffers are free
 };
 
-// allocation with capacity reuse
+// allocation with capacity reuse (cudaMalloc, or the caller's workspace)
 void pc_ensure(pacim_ctx *ctx, DevBuf &b, size_t bytes);
 void pc_free(pacim_ctx *ctx, DevBuf &b);
+// free device bytes for sizing decisions: cudaMemGetInfo's free memory, or
+// the largest hole of the workspace
+size_t pc_mem_free(pacim_ctx *ctx);
+void pc_mem_info(pacim_ctx *ctx, size_t *fr, size_t *tot);
 
 // temporary device buffer released at scope exit (also on exceptions)
 struct TmpBuf : DevBuf {

@@ -97,8 +97,29 @@ def make_partial(name: str, sketches):
     print(name, "partial done", out["oracle_seconds"], flush=True)
 
 
+def make_graph(name: str, scale: int):
+    """Graph-only golden of a config's generator at a reduced R-MAT scale
+    (c5 at scale 25: its full-size CSR does not fit this host): n, m and the
+    sha256 of the oracle's CSR.  The GPU test checks its own generator's CSR
+    against it and then certifies the GPU's seeds and gains in verify mode."""
+    cfg = inputs.config(name, scale=scale)
+    t0 = time.time()
+    g = O.gen_config(cfg)
+    t_gen = time.time() - t0
+    out = dict(config=name, scale=scale, graph_only=True,
+               source="oracle/pacim_oracle.c via tests/golden/make_golden.py --graph",
+               n=g.n, m=g.m, keys_sha256=sha(g.keys), off_sha256=sha(g.off),
+               nbr_sha256=sha(g.nbr), oracle_seconds=dict(generate=round(t_gen, 2)))
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), f"{name}_s{scale}_graph.json")
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1)
+    print(name, scale, "graph done", out["oracle_seconds"], flush=True)
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "--partial":
+    if sys.argv[1] == "--graph":
+        make_graph(sys.argv[2], int(sys.argv[3]))
+    elif sys.argv[1] == "--partial":
         make_partial(sys.argv[2], [int(x) for x in sys.argv[3].split(",")])
     else:
         for nm in sys.argv[1:]:

@@ -383,22 +383,22 @@ def test_config_golden(ctx, name):
     assert st["nmember"] + (n * cfg["R"] - st["nmember"]) == n * cfg["R"]
 
 
-def test_c4_full_scale_sampled(ctx):
+def test_c4_full_scale_certified(orc, ctx):
     """BASELINE.json configs[3] at full size (n = 2^26, m = 1.57e9, WIC, R =
-    256) in bench.py's launch configuration: the generated CSR and two
-    sketches' canonical labels against the oracle's golden digests; the
-    selection against properties that hold at any size."""
+    256, k = 100) in bench.py's launch configuration: the generated CSR and
+    two sketches' canonical labels against the oracle's golden digests, then
+    the GPU's whole greedy sequence (seeds AND per-step gains) CERTIFIED by
+    the oracle's verify mode (GeneralGreedy P:396-401, Alg. 1
+    P:524-530): a passing sequence is exactly derive mode's output."""
     path = os.path.join(GOLD, "c4.json")
-    if not os.path.exists(path):
-        pytest.skip("c4 golden not generated")
     gold = json.load(open(path))
+    from oracle.oracle import Graph
     from paper_2311_07554_b200 import pipeline
     cfg = inputs.config("c4")
     n, m = pipeline.generate(ctx, cfg)
     assert (n, m) == (gold["n"], gold["m"])
     off, nbr = ctx.pacim_get_graph()
     assert sha(off) == gold["off_sha256"] and sha(nbr) == gold["nbr_sha256"]
-    del nbr
     ctx.pacim_build_sketches(cfg["R"], cfg["hash_seed"])
     for r, h in gold["label_sha256"].items():
         lab = ctx.pacim_get_labels(int(r))
@@ -407,12 +407,47 @@ def test_c4_full_scale_sampled(ctx):
         sz = np.bincount(lab, minlength=n)[lab]
         st = gold["cc_stats"][r]
         assert int(roots.sum()) == st["ncc"] and int((sz > 1).sum()) == st["nonsingleton"]
-    g0 = ctx.pacim_get_gain0()
+        del lab, roots, sz
     s, gn, sg, _ = ctx.pacim_select_seeds(cfg["k"])
-    assert gn[0] == g0.max() and s[0] == int(np.argmax(g0))       # first NextSeed
-    assert all(a >= b for a, b in zip(gn, gn[1:]))                 # submodularity
-    assert len(set(int(x) for x in s)) == cfg["k"]                 # distinct seeds
     assert list(sg) == list(np.cumsum(gn))
+    g = Graph(n, off, nbr)
+    model, t32 = orc.model_args(cfg)
+    rc, info = orc.verify(g, model, t32, cfg["R"], cfg["hash_seed"], s, gn)
+    assert rc == 0, (orc.VERIFY_RC[rc], info)
+    assert info[3] == sg[-1]          # Σ_r |∪_i C_r(s_i)| = N(S_k)
+
+
+@pytest.mark.parametrize("lean", [False, True])
+def test_c5_shape_scale25_certified(orc, ctx, lean, monkeypatch):
+    """BASELINE.json configs[4]'s generator and method (web R-MAT .6/.15/.15/.1,
+    ef 32, p = 0.01, R = 256, compressed alpha = 1/16, k = 100) at scale 25
+    (n = 2^25): the full-size c5 CSR (58 GB) does not fit the oracle's host,
+    so SURVEY 8(c)'s fallback scale is used.  The GPU's CSR equals the
+    oracle generator's (golden digest, tests/golden/c5_s25_graph.json), and
+    the GPU's seeds and gains are certified by the oracle's verify mode.
+    lean: the path c5 takes at full scale (no edge lists, k_edges over the
+    CSR, source-bucketed generator)."""
+    path = os.path.join(GOLD, "c5_s25_graph.json")
+    gold = json.load(open(path))
+    if lean:
+        monkeypatch.setenv("PACIM_LEAN", "1")
+        monkeypatch.setenv("PACIM_GEN_BUCKETS", "8")
+    from oracle.oracle import Graph
+    from paper_2311_07554_b200 import pipeline
+    cfg = inputs.config("c5", scale=25)
+    n, m = pipeline.generate(ctx, cfg)
+    assert (n, m) == (gold["n"], gold["m"])
+    off, nbr = ctx.pacim_get_graph()
+    assert sha(off) == gold["off_sha256"] and sha(nbr) == gold["nbr_sha256"]
+    s, gn, sg, _ = pipeline.run(ctx, cfg)
+    st = ctx.pacim_get_stats()
+    assert st["compressed"] == 1 and st["rho"] < n // 8
+    assert bool(st["lean"]) == lean
+    g = Graph(n, off, nbr)
+    model, t32 = orc.model_args(cfg)
+    rc, info = orc.verify(g, model, t32, cfg["R"], cfg["hash_seed"], s, gn)
+    assert rc == 0, (orc.VERIFY_RC[rc], info)
+    assert info[3] == sg[-1]
 
 
 # ------------------------------------------------ multi-rank primitives
@@ -531,3 +566,33 @@ def test_load_graph_async(orc, ctx):
     ctx.pacim_load_graph(off, nbr, 0, t32, 1)
     ctx.pacim_build_sketches(24, 81)
     assert ctx.pacim_graph_info() == (len(off) - 1, len(nbr) // 2)
+
+
+def test_workspace_context(orc, pc):
+    """pacim_create with a caller-owned (torch) workspace: every device buffer
+    is carved from it; results equal the oracle's; a workspace too small for
+    the build fails with ENOMEM (no silent cudaMalloc)."""
+    import torch
+    from oracle.oracle import Graph
+    ws = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    c = pc.Context(0, workspace=ws)
+    try:
+        for i in (2, 3, 7):
+            build_fn, p, R, k = CASES[i]
+            off, nbr = build_fn()
+            g = Graph(len(off) - 1, off, nbr)
+            model, t32 = model_of(orc, p)
+            full_parity(orc, c, g, model, t32, R, 1000 + i, min(k, g.n), check_labels=False)
+            assert c.pacim_get_stats()["device_bytes"] <= ws.numel()
+    finally:
+        c.close()
+    small = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    c = pc.Context(0, workspace=small)
+    try:
+        off, nbr = inputs.random_powerlaw_graph(4000, 30000, 8)
+        with pytest.raises(pc.PacimError) as ei:
+            c.pacim_load_graph(off, nbr, 0, orc.t32_const(0.05), 1)
+            c.pacim_build_sketches(256, 1)
+        assert ei.value.code == -2
+    finally:
+        c.close()

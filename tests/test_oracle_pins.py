@@ -347,3 +347,17 @@ def test_sigma_hat_unbiased_across_hash_seeds(orc, case):
         assert abs(exact_sigma(n, edges, probs, [0]) - (1 + 5 * probs[0])) < 1e-12
     if case == "path":  # from an endpoint: sum_{i<L} p^i
         assert abs(exact_sigma(n, edges, probs, [0]) - sum(0.5**i for i in range(5))) < 1e-12
+
+
+# ------------------------------------------------------ threaded generator
+@pytest.mark.parametrize("scale,ef,abc,threads", [(9, 16, (0.57, 0.19, 0.19), 3),
+                                                  (13, 24, (0.57, 0.19, 0.19), 8),
+                                                  (14, 32, (0.6, 0.15, 0.15), 5)])
+def test_threaded_rmat_generator_equals_plain(orc, scale, ef, abc, threads):
+    """The threaded R-MAT input generator (bench reference arm, c4 at full
+    size) produces the plain generator's keys and CSR bit for bit."""
+    cfg = inputs.config("c2", scale=scale, ef=ef, abc=abc)
+    a = orc.gen_config(cfg)
+    b = orc.gen_config(cfg, threads=threads)
+    assert np.array_equal(a.keys, b.keys)
+    assert np.array_equal(a.off, b.off) and np.array_equal(a.nbr, b.nbr)
