@@ -50,7 +50,8 @@ typedef enum {
     PACIM_ECUDA = -3,    /* CUDA runtime error (message has cudaGetErrorString) */
     PACIM_ESTATE = -5,   /* call out of order (load -> build -> select) */
     PACIM_ENOTIMPL = -6, /* combination not implemented */
-    PACIM_ECHECK = -7    /* an internal invariant check failed (message names it) */
+    PACIM_ECHECK = -7,   /* an internal invariant check failed (message names it) */
+    PACIM_ENCCL = -4     /* NCCL failure (message has ncclGetErrorString) */
 } pacim_status;
 
 /* Edge-probability models (P:1314-1317 constant p; P:2034 WIC). */
@@ -103,6 +104,13 @@ typedef struct {
                                        build's per-vertex hot sums (compressed: no batch
                                        rebuild; uncompressed: no dense pass) */
     uint32_t lean;                  /* 1: lean graph (no edge lists; k_edges reads the CSR) */
+    uint32_t store;                 /* store of the last build: 0 dense vertex-major
+                                       (rows x R_local u32), 1 compact (entries only for
+                                       the non-singleton (vertex, sketch) pairs, with a
+                                       member index), 2 compressed (centers, Alg. 3) */
+    uint32_t select_dist_replays;   /* sharded select: 1 if the fast path (fixed-size delta
+                                       lists, no host sync per step) could not apply a step
+                                       and the selection was re-run on the robust path */
 } pacim_stats;
 
 /* --------------------------------------------------------------- lifecycle */
@@ -124,6 +132,30 @@ PACIM_API int pacim_create(pacim_ctx **out, int device, void *workspace, size_t 
 
 /* Free every device allocation of the ctx and the ctx itself.  NULL is a no-op. */
 PACIM_API void pacim_destroy(pacim_ctx *ctx);
+
+/* ------------------------------------------------------------ multi-GPU */
+/* one process per GPU, sketches sharded r = rank (mod world)
+ * over a replicated graph, NCCL over NVLink called from this library.
+ *
+ * pacim_nccl_unique_id: writes a new 128-byte ncclUniqueId to id_out (host
+ * memory, caller-owned).  Rank 0 calls it and hands the bytes to the other
+ * ranks (e.g. torch.distributed.broadcast_object_list).  EINVAL if NULL,
+ * ENCCL on NCCL failure.
+ *
+ * pacim_init_comm: ncclCommInitRank(world, id, rank) on the ctx's device
+ * (collective: every rank calls it with the same id).  Replaces an earlier
+ * communicator of the ctx.  With it, a build whose (shard_rank, shard_world)
+ * equals (rank, world) ends with one all-reduce of gain0 (pacim_get_gain0 then
+ * returns the GLOBAL gains), and pacim_select_seeds runs the sharded greedy
+ * loop: per step a fixed-size sparse delta exchange (ncclAllGather), no host
+ * synchronisation per step (compact store), re-run on a dense per-step
+ * all-reduce if a list overflows (pacim_stats.select_dist_replays).  Results
+ * are identical on every rank and equal the one-GPU sequence.  EINVAL for a
+ * bad rank / world / NULL id, ENCCL on NCCL failure.  Without a communicator
+ * a sharded build keeps the per-rank step primitives below (gain0 is then the
+ * rank's partial sum). */
+PACIM_API int pacim_nccl_unique_id(void *id_out);
+PACIM_API int pacim_init_comm(pacim_ctx *ctx, int rank, int world, const void *nccl_unique_id);
 
 /* Message of the last failed call on ctx ("" if none).  Valid until the next
  * call on ctx.  With ctx == NULL: message of the last failed pacim_create. */

@@ -17,6 +17,7 @@ from .binding import (  # noqa: F401
     PacimError,
     lib,
     lib_path,
+    pacim_nccl_unique_id,
     pacim_threshold_from_p,
     pacim_threshold_uniform,
     pacim_version,

@@ -11,7 +11,7 @@ _LIB_PATH = os.path.join(HERE, "libpacim.so")
 
 PACIM_P_CONST, PACIM_P_WIC, PACIM_P_UNIFORM = 0, 1, 2
 PACIM_GEN_ER, PACIM_GEN_RMAT, PACIM_GEN_GRID = 0, 1, 2
-STATUS = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -5: "ESTATE",
+STATUS = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENCCL", -5: "ESTATE",
           -6: "ENOTIMPL", -7: "ECHECK"}
 
 # Every function declared in include/pacim.h (tests check the .so exports them).
@@ -25,7 +25,7 @@ EXPORTS = [
     "pacim_apply_deltas", "pacim_apply_dense", "pacim_clear_deltas", "pacim_argmax_device",
     "pacim_set_hash_rule", "pacim_simulate_ic", "pacim_set_selector",
     "pacim_get_gain0", "pacim_get_labels", "pacim_get_center_sketch",
-    "pacim_get_stats",
+    "pacim_get_stats", "pacim_nccl_unique_id", "pacim_init_comm",
 ]
 
 
@@ -53,7 +53,7 @@ class Stats(C.Structure):
         ("select_center_found", C.c_uint64), ("batch_slots", C.c_uint32),
         ("select_evaluations", C.c_uint64), ("select_eval_rounds", C.c_uint64),
         ("hla_entries", C.c_uint64), ("hubs", C.c_uint32), ("select_hotsum_steps", C.c_uint64),
-        ("lean", C.c_uint32),
+        ("lean", C.c_uint32), ("store", C.c_uint32), ("select_dist_replays", C.c_uint32),
     ]
 
     def asdict(self):
@@ -105,6 +105,8 @@ def lib():
             "pacim_get_labels": (i32, [P, u32, P]),
             "pacim_get_center_sketch": (i32, [P, u32, P, P]),
             "pacim_get_stats": (i32, [P, C.POINTER(Stats)]),
+            "pacim_nccl_unique_id": (i32, [P]),
+            "pacim_init_comm": (i32, [P, i32, i32, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(L, name)
@@ -120,6 +122,16 @@ def pacim_threshold_from_p(p: float) -> int:
 
 def pacim_threshold_uniform(lo: float, hi: float) -> int:
     return int(lib().pacim_threshold_uniform(float(lo), float(hi)))
+
+
+def pacim_nccl_unique_id() -> bytes:
+    """A new 128-byte NCCL unique id (rank 0 creates it, every rank passes it to
+    Context.pacim_init_comm)."""
+    buf = C.create_string_buffer(128)
+    rc = lib().pacim_nccl_unique_id(buf)
+    if rc != 0:
+        raise PacimError(rc, lib().pacim_last_error(None).decode())
+    return buf.raw
 
 
 def pacim_version() -> str:
@@ -183,6 +195,12 @@ class Context:
     def _check(self, rc):
         if rc != 0:
             raise PacimError(rc, self._L.pacim_last_error(self._h).decode())
+
+    def pacim_init_comm(self, rank: int, world: int, nccl_id: bytes):
+        """NCCL communicator of this ctx (all ranks, same 128-byte id)."""
+        assert len(nccl_id) == 128
+        buf = C.create_string_buffer(bytes(nccl_id), 128)
+        self._check(self._L.pacim_init_comm(self._h, int(rank), int(world), buf))
 
     # ------------------------------------------------------------- graph
     def pacim_load_graph(self, offsets: np.ndarray, neighbors: np.ndarray, pmodel: int, t32: int,

@@ -14,13 +14,27 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libpacim.so")
-SOURCES = ["api.cu", "graph.cu", "build.cu", "select.cu", "compressed.cu", "mc.cu"]
+SOURCES = ["api.cu", "graph.cu", "build.cu", "select.cu", "compressed.cu", "mc.cu", "store_cs.cu",
+           "dist.cu"]
+
+# NCCL: the venv's (the same 2.28 build torch.distributed loads)
+def _nccl_dir() -> str:
+    import site
+    for sp in site.getsitepackages() + [site.getusersitepackages()]:
+        d = os.path.join(sp, "nvidia", "nccl")
+        if os.path.isdir(os.path.join(d, "include")):
+            return d
+    raise RuntimeError("NCCL headers not found (nvidia/nccl in site-packages)")
+
+
+NCCL_DIR = _nccl_dir()
 
 HEADERS = ["pacim_internal.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
-         "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include")]
+         "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"),
+         "-I", os.path.join(NCCL_DIR, "include")]
 
 
 def _stale(lib: str, deps: list[str]) -> bool:
@@ -52,7 +66,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with ThreadPoolExecutor(len(SOURCES)) as ex:
         objs = list(ex.map(compile_one, SOURCES))
     tmp = LIB + ".tmp"
-    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
+    nlib = os.path.join(NCCL_DIR, "lib")
+    cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart", "-L", nlib, "-l:libnccl.so.2",
+           "-Xlinker", "-rpath=" + nlib]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stderr}")

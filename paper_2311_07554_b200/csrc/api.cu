@@ -133,6 +133,8 @@ static int guarded(pacim_ctx *ctx, F &&f) {
 // (pc_ensure reuses them); they are released by pacim_destroy.
 static void drop_sketches(pacim_ctx *ctx) {
   ctx->built = false;
+  ctx->dist_cov_valid = false;  // a new store: no covered flags to restore
+  ctx->dist_cov_n = 0;
   ctx->hla_ok = false;
   ctx->sel_list_valid = false;  // the covered list refers to the old store
 }
@@ -150,7 +152,9 @@ static void free_all(pacim_ctx *ctx) {
 
                     &ctx->d_tab, &ctx->gain0,      &ctx->gain,     &ctx->center_of, &ctx->counters,
                     &ctx->scratch, &ctx->scratch2, &ctx->sel_seeds, &ctx->sel_gain,
-                    &ctx->sel_partial, &ctx->sel_list, &ctx->sel_flag, &ctx->argmax_part, &ctx->bfs, &ctx->tcsr, &ctx->hidx, &ctx->hub_tab, &ctx->hla_off, &ctx->hla_row, &ctx->hla_raw, &ctx->d_smap, &ctx->pkeys, &ctx->cprobe, &ctx->cseed, &ctx->d_hr64, &ctx->crow, &ctx->vinfo, &ctx->hotsum, &ctx->d_hot_size};
+                    &ctx->sel_partial, &ctx->sel_list, &ctx->sel_flag, &ctx->argmax_part, &ctx->bfs, &ctx->tcsr, &ctx->hidx, &ctx->hub_tab, &ctx->hla_off, &ctx->hla_row, &ctx->hla_raw, &ctx->d_smap, &ctx->pkeys, &ctx->cprobe, &ctx->cseed, &ctx->d_hr64, &ctx->crow, &ctx->vinfo, &ctx->hotsum, &ctx->d_hot_size,
+                    &ctx->cs_rec, &ctx->cs_soff, &ctx->cs_sl, &ctx->cs_ecrow, &ctx->cs_P, &ctx->cs_moff,
+                    &ctx->cs_memb, &ctx->cs_diag, &ctx->dist_ghot, &ctx->dist_buf, &ctx->dist_cov_old};
   for (DevBuf *b : bufs) pc_free(ctx, *b);
 }
 
@@ -236,9 +240,29 @@ void pacim_destroy(pacim_ctx *ctx) {
       pc_free(ctx, g.nbr);
     }
   }
+  pc_free_comm(ctx);
   free_all(ctx);
   if (ctx->own_stream && ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
+}
+
+int pacim_nccl_unique_id(void *id_out) {
+  if (!id_out) return PACIM_EINVAL;
+  try {
+    pc_nccl_unique_id(id_out);
+  } catch (const PacimError &pe) {
+    g_create_err = pe.msg;
+    return pe.code;
+  }
+  return PACIM_OK;
+}
+
+int pacim_init_comm(pacim_ctx *ctx, int rank, int world, const void *nccl_unique_id) {
+  return guarded(ctx, [&] {
+    PC_REQUIRE(world >= 1 && rank >= 0 && rank < world && nccl_unique_id, PACIM_EINVAL,
+               "need 0 <= rank < world and a 128-byte NCCL unique id");
+    pc_init_comm(ctx, rank, world, nccl_unique_id);
+  });
 }
 
 const char *pacim_last_error(const pacim_ctx *ctx) {
@@ -435,6 +459,7 @@ int pacim_build_sketches(pacim_ctx *ctx, uint32_t R, uint64_t hash_seed, uint64_
       pc_build_compressed(ctx);
     else
       pc_build(ctx);
+    pc_dist_build_finish(ctx);  // sharded with a communicator: gain0 all-reduced
     ctx->built = true;
   });
 }
@@ -443,11 +468,15 @@ int pacim_select_seeds(pacim_ctx *ctx, uint32_t k, uint32_t *seeds_out, int64_t 
                        int64_t *sigma_num_out, double *sigma_out) {
   return guarded(ctx, [&] {
     PC_REQUIRE(ctx->built, PACIM_ESTATE, "select before build_sketches");
-    PC_REQUIRE(ctx->world == 1, PACIM_ESTATE,
-               "sharded build: use the multi-rank step primitives (dist.py)");
     PC_REQUIRE(k >= 1 && k <= ctx->n, PACIM_EINVAL, "k must be in [1, n]");
     PC_REQUIRE(seeds_out && gain_num_out && sigma_num_out, PACIM_EINVAL, "NULL output");
-    if (ctx->compressed)
+    if (ctx->world > 1) {
+      // sharded build: the greedy loop over NCCL (dist.cu); without a
+      // communicator the per-rank step primitives remain (dist.py)
+      pc_dist_select(ctx, k, seeds_out, gain_num_out);
+      int64_t run = 0;
+      for (uint32_t i = 0; i < k; i++) sigma_num_out[i] = run += gain_num_out[i];
+    } else if (ctx->compressed)
       pc_select_compressed(ctx, k, seeds_out, gain_num_out, sigma_num_out);
     else
       if (ctx->selector == 1)
@@ -630,6 +659,7 @@ int pacim_get_stats(pacim_ctx *ctx, pacim_stats *out) {
     s.hla_entries = ctx->hla_ok ? ctx->hla_n : 0;
     s.hubs = ctx->nhub;
     s.lean = ctx->lean ? 1u : 0u;
+    s.store = ctx->compressed ? 2u : (ctx->cs ? 1u : 0u);
     s.nnonsingle = ctx->nnonsingle;
     s.device_bytes = ctx->device_bytes;
     *out = s;

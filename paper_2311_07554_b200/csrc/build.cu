@@ -112,7 +112,9 @@ constexpr int EDGE_WARPS = EDGE_THREADS / 32;
 // an entry lies past the row's end), and keeps the upper ones (v > u); rows
 // are the vertex ids.  `keys` = CSR offsets, `ckeys` = neighbours (as u32),
 // `tm1` = chunk rows, m = CSR entries (2m).
-template <bool WIC, bool REC, bool DECOR, bool LEAN>
+// CS: the compact store (store_cs.cu): L is the flat parent array P and a
+// (row, slot) pair is entry pc_cs_pos(rec, MW, row, slot) (j0 = 0, Bb = B)
+template <bool WIC, bool REC, bool DECOR, bool LEAN, bool CS = false>
 __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__restrict__ keys,
                                                         const uint64_t *__restrict__ ckeys,
                                                         const uint32_t *__restrict__ tm1,
@@ -122,7 +124,9 @@ __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__res
                                                         uint32_t B, uint32_t j0, uint32_t Bb,
                                                         uint32_t *L,
                                                         unsigned long long *live_ctr, Hla hla,
-                                                        const uint64_t *__restrict__ hr64) {
+                                                        const uint64_t *__restrict__ hr64,
+                                                        const uint2 *__restrict__ rec,
+                                                        uint32_t MW) {
   // slots [j0, j0 + Bb) of the B sorted slots go to L (row stride Bb)
   extern __shared__ uint32_t sm[];
   uint32_t *shr = sm;
@@ -236,7 +240,11 @@ __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__res
         hla.stage(u & ~PACIM_HUBF, v & ~PACIM_HUBF, j, (lv && (u & PACIM_HUBF)) ? 1u : 0u,
                   (lv && (v & PACIM_HUBF)) ? 1u : 0u, w_hla[REC ? wid : 0], hla_n);
       if (lv) {
-        uf_unite(L, Bb, j - j0, u & ~PACIM_HUBF, v & ~PACIM_HUBF);
+        if (CS)
+          uf_unite(L, 1, 0, pc_cs_pos(rec, MW, u & ~PACIM_HUBF, j),
+                   pc_cs_pos(rec, MW, v & ~PACIM_HUBF, j));
+        else
+          uf_unite(L, Bb, j - j0, u & ~PACIM_HUBF, v & ~PACIM_HUBF);
         live++;
       }
     }
@@ -954,7 +962,7 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
       kern<<<gl, EDGE_THREADS, smem, ctx->stream>>>(
           ctx->off.as<uint64_t>(), reinterpret_cast<const uint64_t *>(ctx->nbr.p),
           ctx->crow.as<uint32_t>(), nnz, ctx->K, ctx->t32, ctx->d_shr.as<uint32_t>(),
-          ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>());
+          ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), nullptr, 0u);
     } else if (ctx->pmodel != PACIM_P_CONST) {  // per-edge thresholds (WIC, Uniform)
       auto kern = ctx->hash_rule ? (hla.raw ? k_edges<true, true, true, false> : k_edges<true, false, true, false>)
                                  : (hla.raw ? k_edges<true, true, false, false> : k_edges<true, false, false, false>);
@@ -962,7 +970,7 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
       kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
           es.keys, es.ckeys, ctx->tm1.as<uint32_t>(), es.m,
           ctx->K, ctx->toff(), ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla,
-          ctx->d_hr64.as<uint64_t>());
+          ctx->d_hr64.as<uint64_t>(), nullptr, 0u);
     } else {
       auto kern = ctx->hash_rule ? (hla.raw ? k_edges<false, true, true, false> : k_edges<false, false, true, false>)
                                  : (hla.raw ? k_edges<false, true, false, false> : k_edges<false, false, false, false>);
@@ -970,7 +978,7 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
       kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
           es.keys, es.ckeys, nullptr, es.m, ctx->K, ctx->t32,
           ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla,
-          ctx->d_hr64.as<uint64_t>());
+          ctx->d_hr64.as<uint64_t>(), nullptr, 0u);
     }
     PC_CHECK_LAUNCH();
   }
@@ -998,6 +1006,41 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
   PC_CHECK_LAUNCH();
   if (ev) PC_CUDA(cudaEventRecord(ev[2], ctx->stream));
   ctx->launches += 4;
+}
+
+// The union pass over the compact store (store_cs.cu): every upper edge,
+// its live sketches, unions of the flat entries in P.  ctr[4] += live pairs.
+void pc_cs_edges(pacim_ctx *ctx, uint32_t *P, const uint2 *rec, uint32_t MW,
+                 unsigned long long *ctr) {
+  const uint32_t B = ctx->R_local;
+  const uint32_t NT = 1u << PACIM_TB;
+  const size_t smem = B * sizeof(uint32_t) + (NT + 1) * sizeof(uint16_t);
+  if (ctx->lean) {
+    auto kern = ctx->hash_rule ? k_edges<false, false, true, true, true>
+                               : k_edges<false, false, false, true, true>;
+    PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const uint64_t nnz = 2 * ctx->m;
+    const unsigned gl = pc_grid(ctx, (nnz + 31) / 32 * 32, EDGE_THREADS, 8);
+    kern<<<gl, EDGE_THREADS, smem, ctx->stream>>>(
+        ctx->off.as<uint64_t>(), reinterpret_cast<const uint64_t *>(ctx->nbr.p),
+        ctx->crow.as<uint32_t>(), nnz, ctx->K, ctx->t32, ctx->d_shr.as<uint32_t>(),
+        ctx->d_tab.as<uint16_t>(), B, 0, B, P, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), rec, MW);
+  } else {
+    const bool pe = ctx->pmodel != PACIM_P_CONST;
+    auto kern = pe ? (ctx->hash_rule ? k_edges<true, false, true, false, true>
+                                     : k_edges<true, false, false, false, true>)
+                   : (ctx->hash_rule ? k_edges<false, false, true, false, true>
+                                     : k_edges<false, false, false, false, true>);
+    PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const unsigned g = pc_grid(ctx, (ctx->m + 31) / 32 * 32, EDGE_THREADS, 8);
+    kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
+        ctx->keys.as<uint64_t>(), ctx->ckeys.as<uint64_t>(),
+        pe ? ctx->tm1.as<uint32_t>() : nullptr, ctx->m, ctx->K, pe ? ctx->toff() : ctx->t32,
+        ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, 0, B, P, ctr + 4, Hla{},
+        ctx->d_hr64.as<uint64_t>(), rec, MW);
+  }
+  PC_CHECK_LAUNCH();
+  ctx->launches++;
 }
 
 // Slot windows of the store for this build.  With a constant
@@ -1053,6 +1096,10 @@ void pc_build(pacim_ctx *ctx) {
   const uint32_t n = ctx->nr, B = ctx->R_local;  // store rows = non-isolated vertices
   PC_REQUIRE(B >= 1 && B <= 65535, PACIM_EINVAL, "local sketch count must be in [1, 65535]");
   PC_REQUIRE(!ctx->compressed, PACIM_ENOTIMPL, "compressed store not built by pc_build");
+  // the compact store (store_cs.cu) unless the sketches are dense (c3) or the
+  // dense layout is asked for (PACIM_STORE=dense)
+  if (pc_cs_build(ctx)) return;
+  pc_cs_free(ctx);
   pc_slot_table(ctx);
   // a compressed store of an earlier build is released first (capacity for
   // this one: at c4 the two do not fit together)
@@ -1245,6 +1292,7 @@ __global__ void k_labels(const uint32_t *L, uint32_t n, uint32_t nr, const uint3
 }  // namespace
 
 void pc_get_labels(pacim_ctx *ctx, uint32_t slot, uint32_t *host_out) {
+  if (ctx->cs) return pc_cs_get_labels(ctx, slot, host_out);
   TmpBuf t(ctx);
   pc_ensure(ctx, t, (size_t)ctx->n * 4);
   k_labels<<<pc_grid(ctx, ctx->n, 256), 256, 0, ctx->stream>>>(ctx->L.as<uint32_t>(), ctx->n,

@@ -563,6 +563,7 @@ void pc_build_compressed(pacim_ctx *ctx) {
   // released first (the point of the compressed mode is not to hold them)
   // and so is the HLA of an earlier build; its batch parent arrays are kept
   // for reuse (choose_batch counts them as free)
+  pc_cs_free(ctx);  // a compact store of an earlier build
   for (DevBuf *d : {&ctx->L, &ctx->bfs, &ctx->pkeys, &ctx->hla_off, &ctx->hla_row, &ctx->hla_raw})
     pc_free(ctx, *d);
   ctx->hla_ok = false;

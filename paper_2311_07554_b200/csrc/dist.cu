@@ -1,0 +1,578 @@
+// dist.cu — multi-GPU sketch sharding behind the C ABI.
+//
+// One process per GPU.  Rank g builds the sketches r = g (mod P) over a
+// replicated CSR (pacim_build_sketches with shard_rank = g, shard_world = P);
+// with a communicator (pacim_init_comm: NCCL, called from C++) the build ends
+// with ONE all-reduce of gain0 (int64, H7) — and of the per-vertex hot sums
+// of the hub's giant CCs — so every rank holds the global gain vector.
+//
+// pacim_select_seeds on a sharded build (sketches are independent,
+// the greedy step sums over them):
+//   fast path (compact store), per step, all enqueued on the ctx stream with
+//   no host synchronisation (optionally one CUDA graph for all k steps):
+//     k_dist_cover  every rank: NextSeed over the replicated gains (cached
+//                   chunk maxima, identical on all ranks), MarkSeed on its own
+//                   sketches, the members' deltas (v, |C|) into a fixed-size
+//                   list; big CCs (no member list) are flagged
+//     k_dist_head   the step header: list length, local sum of delta_r,
+//                   overflow, and whether the step's big CCs are exactly this
+//                   rank's hub giants
+//     ncclAllGather header + list (one collective per step)
+//     k_dist_apply  every rank applies every rank's list (and, in the step
+//                   that covers the hub's giants on every rank, the all-reduced
+//                   hot sums) to its replica; checks sum delta = argmax gain
+//     k_dist_chunks the chunk maxima that lost their argmax
+//   A list overflow or a big CC that is not a hub giant sets a replay flag
+//   (seen by every rank: it is in the gathered headers); the host then
+//   re-runs the selection on the robust path.
+//   robust path (any store, and replays): per step the argmax read back,
+//   MarkSeed + member deltas into a dense int64 delta vector, one
+//   ncclAllReduce of it, applied — correct whatever the CC sizes.
+// Integer sums are associative: any partition gives the one-GPU sequence.
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "pacim_internal.cuh"
+
+#define PC_NCCL(call)                                                               \
+  do {                                                                              \
+    ncclResult_t r_ = (call);                                                       \
+    if (r_ != ncclSuccess)                                                          \
+      throw PacimError{PACIM_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)}; \
+  } while (0)
+
+namespace {
+
+constexpr uint32_t NONE = 0xFFFFFFFFu;
+constexpr uint32_t COV = 0x40000000u;
+constexpr uint32_t SIZE = 0x3FFFFFFFu;
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int DT = 512;                 // threads per block of the step kernels
+constexpr uint32_t MAX_CHUNKS = 4096;
+// header words (u64) of a rank's step message
+enum { H_CNT = 0, H_DSUM, H_FLAGS, H_PAD, H_WORDS };
+enum { F_OVER = 1, F_DENSE = 2, F_EXACT = 4 };
+// device state words (u64)
+enum { D_S = 0, D_SG, D_REPLAY, D_CHECK, D_DCNT, D_WORDS = 8 };
+
+struct Best {
+  long long g;
+  uint32_t v;
+};
+
+__device__ __forceinline__ bool better(long long g1, uint32_t v1, long long g2, uint32_t v2) {
+  return g1 > g2 || (g1 == g2 && v1 < v2);
+}
+
+__device__ __forceinline__ Best warp_best(Best b) {
+  for (int d = 16; d; d >>= 1) {
+    const long long g = __shfl_xor_sync(FULL, b.g, d);
+    const uint32_t v = __shfl_xor_sync(FULL, b.v, d);
+    if (better(g, v, b.g, b.v)) {
+      b.g = g;
+      b.v = v;
+    }
+  }
+  return b;
+}
+
+__device__ Best block_best(Best b, Best *sh) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  b = warp_best(b);
+  __syncthreads();
+  if (lane == 0) sh[wid] = b;
+  __syncthreads();
+  if (wid == 0) {
+    Best x = lane < (int)(blockDim.x >> 5) ? sh[lane] : Best{LLONG_MIN, NONE};
+    x = warp_best(x);
+    if (lane == 0) sh[32] = x;
+  }
+  __syncthreads();
+  return sh[32];
+}
+
+struct DSel {
+  // compact store of this rank
+  const uint2 *rec;
+  uint32_t MW;
+  uint32_t *P;
+  const uint32_t *moff, *memb, *cid;
+  uint32_t B, nv, big_t;
+  const uint32_t *hot_root, *hot_size;
+  // replicated gains + argmax cache
+  long long *gain;
+  Best *cmax;
+  uint32_t *cdirty, *dlist;
+  uint32_t csh, nchunks;
+  const int64_t *ghot;     // all-reduced hot sums (null: none)
+  // covered CCs (restored before the next selection)
+  unsigned long long *cov_list, *cov_cnt, cov_cap;
+  uint32_t *cov_root;      // [B] big CC covered in slot j this step
+  // messages
+  unsigned long long *send;  // H_WORDS + cap
+  const unsigned long long *recv;  // world x (H_WORDS + cap)
+  unsigned long long cap;
+  int world;
+  unsigned long long *st;  // D_WORDS
+  uint32_t *seeds;
+  long long *gain_num;
+};
+
+__device__ __forceinline__ void mark_dirty(const DSel &S, uint32_t c) {
+  if (atomicExch(S.cdirty + c, 1u) == 0u)
+    S.dlist[atomicAdd(reinterpret_cast<unsigned long long *>(S.st + D_DCNT), 1ull)] = c;
+}
+
+// every block: NextSeed from the chunk maxima (identical on every rank);
+// MarkSeed on this rank's slots, member deltas into the send list
+__global__ void __launch_bounds__(DT) k_dist_cover(DSel S, uint32_t step) {
+  __shared__ Best sh[33];
+  Best c{LLONG_MIN, NONE};
+  for (uint32_t i = threadIdx.x; i < S.nchunks; i += blockDim.x) {
+    Best x;
+    x.g = __ldcg(&S.cmax[i].g);
+    x.v = __ldcg(&S.cmax[i].v);
+    if (better(x.g, x.v, c.g, c.v)) c = x;
+  }
+  c = block_best(c, sh);
+  const uint32_t s = c.v;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid == 0) {
+    S.st[D_S] = s;
+    S.st[D_SG] = (unsigned long long)c.g;
+    S.st[D_DCNT] = 0;
+    S.seeds[step] = s;
+  }
+  const int lane = threadIdx.x & 31;
+  const size_t gwarp = tid >> 5, nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t srow = S.cid ? S.cid[s] : s;
+  unsigned long long dsum = 0;
+  for (size_t j = gwarp; j < S.B; j += nwarps) {
+    uint32_t d = 1, mr = NONE;
+    if (lane == 0) {
+      S.cov_root[j] = NONE;
+      if (srow != NONE && ((S.rec[(size_t)srow * S.MW + (j >> 5)].y >> (j & 31)) & 1u)) {
+        const uint32_t e = pc_cs_pos(S.rec, S.MW, srow, (uint32_t)j);
+        const uint32_t x0 = __ldcg(S.P + e);
+        const uint32_t root = (x0 & PACIM_HIGH) ? e : x0;
+        const uint32_t x = atomicOr(S.P + root, COV);
+        if (x & COV) {
+          d = 0;
+        } else {
+          d = x & SIZE;
+          const unsigned long long at = atomicAdd(S.cov_cnt, 1ull);
+          if (at < S.cov_cap) S.cov_list[at] = root;
+          if (d > S.big_t)
+            S.cov_root[j] = root;
+          else
+            mr = root;
+        }
+      }
+    }
+    d = __shfl_sync(FULL, d, 0);
+    mr = __shfl_sync(FULL, mr, 0);
+    dsum += d;
+    if (mr != NONE && d > 1) {
+      const uint32_t end = __ldg(S.moff + mr);
+      for (uint32_t t = end - d + lane; t < end; t += 32) {
+        const uint32_t v = __ldg(S.memb + t);
+        if (v == s) continue;
+        const unsigned long long at = atomicAdd(S.send + H_CNT, 1ull);
+        if (at < S.cap) S.send[H_WORDS + at] = ((unsigned long long)v << 32) | d;
+      }
+    }
+  }
+  if (lane == 0 && dsum) atomicAdd(S.send + H_DSUM, dsum);
+}
+
+// the step header's flags (one block): list overflow; big CCs covered;
+// EXACT: the big CCs covered now are exactly this rank's hub giants (both
+// sets may be empty) — when some rank covers a big CC, the all-reduced hot
+// sums are the update iff every rank is EXACT
+__global__ void k_dist_head(DSel S) {
+  __shared__ int dense, exact;
+  if (threadIdx.x == 0) {
+    dense = 0;
+    exact = 1;
+  }
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < S.B; j += blockDim.x) {
+    const uint32_t cr = S.cov_root[j];
+    const bool big = S.hot_size[j] > S.big_t;
+    if (cr != NONE) dense = 1;
+    if (big != (cr != NONE) || (big && cr != S.hot_root[j])) exact = 0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long f = 0;
+    if (S.send[H_CNT] > S.cap) f |= F_OVER;
+    if (dense) f |= F_DENSE;
+    if (exact) f |= F_EXACT;
+    S.send[H_FLAGS] = f;
+  }
+}
+
+// every rank applies every rank's list to its replica
+__global__ void __launch_bounds__(DT) k_dist_apply(DSel S, uint32_t step) {
+  const uint32_t s = (uint32_t)S.st[D_S];
+  const long long sg = (long long)S.st[D_SG];
+  // consensus from the gathered headers (identical on every rank)
+  bool replay = false, any_dense = false, all_exact = true;
+  long long gsum = 0;
+  for (int p = 0; p < S.world; p++) {
+    const unsigned long long *h = S.recv + (size_t)p * (H_WORDS + S.cap);
+    const unsigned long long f = h[H_FLAGS];
+    gsum += (long long)h[H_DSUM];
+    if (f & F_OVER) replay = true;
+    if (f & F_DENSE) any_dense = true;
+    if (!(f & F_EXACT)) all_exact = false;
+  }
+  // big CCs without member lists: only the step that covers every rank's hub
+  // giants at once has its update precomputed (the all-reduced hot sums)
+  if (any_dense && (!all_exact || !S.ghot)) replay = true;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t nth = (size_t)gridDim.x * blockDim.x;
+  if (tid == 0) {
+    if (replay) S.st[D_REPLAY] = 1;
+    if (gsum != sg) S.st[D_CHECK] = 1;
+    S.gain_num[step] = gsum;
+    S.gain[s] = -1;  // s leaves the candidate set (R6)
+    mark_dirty(S, s >> S.csh);
+  }
+  if (replay) return;
+  if (any_dense && S.ghot) {
+    for (size_t v = tid; v < S.nv; v += nth) {
+      const long long h = S.ghot[v];
+      if (h && v != s) {
+        atomicAdd(reinterpret_cast<unsigned long long *>(S.gain + v), (unsigned long long)(-h));
+        const uint32_t c = (uint32_t)(v >> S.csh);
+        if (__ldcg(&S.cmax[c].v) == v) mark_dirty(S, c);
+      }
+    }
+  }
+  for (int p = 0; p < S.world; p++) {
+    const unsigned long long *h = S.recv + (size_t)p * (H_WORDS + S.cap);
+    const unsigned long long cnt = min(h[H_CNT], S.cap);
+    for (size_t t = tid; t < cnt; t += nth) {
+      const unsigned long long x = h[H_WORDS + t];
+      const uint32_t v = (uint32_t)(x >> 32);
+      const long long d = (long long)(uint32_t)x;
+      atomicAdd(reinterpret_cast<unsigned long long *>(S.gain + v), (unsigned long long)(-d));
+      const uint32_t c = v >> S.csh;
+      if (__ldcg(&S.cmax[c].v) == v) mark_dirty(S, c);
+    }
+  }
+}
+
+// refresh the dirty chunk maxima (block per chunk), then clear the message
+__global__ void __launch_bounds__(DT) k_dist_chunks(DSel S, bool all) {
+  __shared__ Best sh[33];
+  const uint32_t nd = all ? S.nchunks : (uint32_t)__ldcg(S.st + D_DCNT);
+  for (uint32_t t = blockIdx.x; t < nd; t += gridDim.x) {
+    const uint32_t c = all ? t : S.dlist[t];
+    const size_t v0 = (size_t)c << S.csh, v1 = min((size_t)S.nv, v0 + ((size_t)1 << S.csh));
+    Best b{LLONG_MIN, NONE};
+    for (size_t v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
+      const long long g = __ldcg(S.gain + v);
+      if (better(g, (uint32_t)v, b.g, b.v)) {
+        b.g = g;
+        b.v = (uint32_t)v;
+      }
+    }
+    b = block_best(b, sh);
+    if (threadIdx.x == 0) {
+      S.cmax[c] = b;
+      S.cdirty[c] = 0;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x < H_WORDS) S.send[threadIdx.x] = 0;
+}
+
+__global__ void k_dist_uncover(uint32_t *P, const unsigned long long *list, unsigned long long cnt) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
+       i += (size_t)gridDim.x * blockDim.x)
+    atomicAnd(P + list[i], ~COV);
+}
+
+__global__ void k_dist_set(long long *gain, uint32_t s, long long x) { gain[s] = x; }
+
+__global__ void k_dist_add(long long *gain, long long *delta, uint32_t n) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const long long x = delta[i];
+    if (x) {
+      gain[i] += x;
+      delta[i] = 0;
+    }
+  }
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ host
+static ncclComm_t comm_of(pacim_ctx *ctx) { return reinterpret_cast<ncclComm_t>(ctx->comm); }
+
+void pc_nccl_unique_id(void *out) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  ncclUniqueId id;
+  PC_NCCL(ncclGetUniqueId(&id));
+  std::memcpy(out, &id, sizeof(id));
+}
+
+void pc_init_comm(pacim_ctx *ctx, int rank, int world, const void *id) {
+  pc_free_comm(ctx);
+  ncclUniqueId uid;
+  std::memcpy(&uid, id, sizeof(uid));
+  ncclComm_t c = nullptr;
+  PC_NCCL(ncclCommInitRank(&c, world, uid, rank));
+  ctx->comm = c;
+  ctx->comm_rank = rank;
+  ctx->comm_world = world;
+}
+
+void pc_free_comm(pacim_ctx *ctx) {
+  if (ctx->comm) {
+    cudaStreamSynchronize(ctx->stream);
+    ncclCommDestroy(comm_of(ctx));
+  }
+  ctx->comm = nullptr;
+  ctx->comm_rank = 0;
+  ctx->comm_world = 1;
+}
+
+void pc_dist_restore(pacim_ctx *ctx) {
+  if (ctx->cs && ctx->dist_cov_valid && ctx->dist_cov_n) {
+    k_dist_uncover<<<pc_grid(ctx, ctx->dist_cov_n, 256), 256, 0, ctx->stream>>>(
+        ctx->cs_P.as<uint32_t>(), ctx->dist_cov_old.as<unsigned long long>(), ctx->dist_cov_n);
+    PC_CHECK_LAUNCH();
+  }
+  ctx->dist_cov_valid = false;
+  ctx->dist_cov_n = 0;
+}
+
+bool pc_dist_active(const pacim_ctx *ctx) {
+  return ctx->comm && ctx->world > 1 && ctx->comm_world == (int)ctx->world &&
+         ctx->comm_rank == (int)ctx->rank;
+}
+
+// End of a sharded build: gain0 all-reduced (H7 summed over the ranks'
+// sketches) and, if any rank has hub giants, the hot sums too.  Recorded
+// in t_build ("including the all-reduce at P > 1").
+void pc_dist_build_finish(pacim_ctx *ctx) {
+  if (!pc_dist_active(ctx)) return;
+  cudaEvent_t a, b;
+  PC_CUDA(cudaEventCreate(&a));
+  PC_CUDA(cudaEventCreate(&b));
+  PC_CUDA(cudaEventRecord(a, ctx->stream));
+  TmpBuf flag(ctx);
+  pc_ensure(ctx, flag, 8);
+  const int local = (!ctx->compressed && ctx->hot_any) ? 1 : 0;
+  PC_CUDA(cudaMemcpyAsync(flag.p, &local, 4, cudaMemcpyHostToDevice, ctx->stream));
+  PC_NCCL(ncclAllReduce(flag.p, flag.p, 1, ncclInt32, ncclMax, comm_of(ctx), ctx->stream));
+  PC_NCCL(ncclAllReduce(ctx->gain0.p, ctx->gain0.p, ctx->n, ncclInt64, ncclSum, comm_of(ctx),
+                        ctx->stream));
+  int any = 0;
+  PC_CUDA(cudaMemcpyAsync(&any, flag.p, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->dist_hot = any != 0;
+  if (any) {  // the global hot sums, beside this rank's own (its covers use those)
+    pc_ensure(ctx, ctx->dist_ghot, (size_t)ctx->n * 8);
+    if (local)
+      PC_CUDA(cudaMemcpyAsync(ctx->dist_ghot.p, ctx->hotsum.p, (size_t)ctx->n * 8,
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+    else
+      PC_CUDA(cudaMemsetAsync(ctx->dist_ghot.p, 0, (size_t)ctx->n * 8, ctx->stream));
+    PC_NCCL(ncclAllReduce(ctx->dist_ghot.p, ctx->dist_ghot.p, ctx->n, ncclInt64, ncclSum,
+                          comm_of(ctx), ctx->stream));
+  }
+  PC_CUDA(cudaEventRecord(b, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  ctx->stats.t_build_ms += ms;
+  ctx->stats.t_gain_ms += ms;
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+}
+
+// robust path: per step the argmax on the host, a dense delta vector, one
+// all-reduce; works on every store (dense, compact, compressed)
+static void dist_select_robust(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num) {
+  const uint32_t n = ctx->n;
+  TmpBuf gb(ctx), db(ctx), sb(ctx);
+  pc_ensure(ctx, gb, (size_t)n * 8);
+  pc_ensure(ctx, db, (size_t)n * 8);
+  pc_ensure(ctx, sb, 16);
+  int64_t *gain = gb.as<int64_t>(), *delta = db.as<int64_t>();
+  PC_CUDA(cudaMemcpyAsync(gain, ctx->gain0.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  PC_CUDA(cudaMemsetAsync(delta, 0, (size_t)n * 8, ctx->stream));
+  if (ctx->compressed) {
+    pc_select_reset_compressed(ctx);
+  } else {
+    pc_select_reset(ctx);  // restores the previous selection's flags
+    if (k > ctx->sel_k_cap) {  // covered list for k steps
+      ctx->sel_k_cap = k;
+      ctx->sel_list_valid = false;
+      pc_select_reset(ctx);
+    }
+  }
+  for (uint32_t i = 0; i < k; i++) {
+    uint32_t s = 0;
+    int64_t g = 0, loc = 0;
+    pc_argmax(ctx, gain, n, &s, &g);
+    if (ctx->compressed) {
+      pc_cover_compressed(ctx, s, delta, &loc);
+      PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    } else {
+      pc_cover_local(ctx, s, delta, &loc);
+    }
+    PC_CUDA(cudaMemcpyAsync(sb.p, &loc, 8, cudaMemcpyHostToDevice, ctx->stream));
+    PC_NCCL(ncclGroupStart());
+    PC_NCCL(ncclAllReduce(delta, delta, n, ncclInt64, ncclSum, comm_of(ctx), ctx->stream));
+    PC_NCCL(ncclAllReduce(sb.p, sb.p, 1, ncclInt64, ncclSum, comm_of(ctx), ctx->stream));
+    PC_NCCL(ncclGroupEnd());
+    k_dist_add<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(
+        reinterpret_cast<long long *>(gain), reinterpret_cast<long long *>(delta), n);
+    k_dist_set<<<1, 1, 0, ctx->stream>>>(reinterpret_cast<long long *>(gain), s, -1);
+    PC_CHECK_LAUNCH();
+    int64_t gsum = 0;
+    PC_CUDA(cudaMemcpyAsync(&gsum, sb.p, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    PC_REQUIRE(gsum == g, PACIM_ECHECK, "sharded select: sum of delta_r differs from the argmax gain");
+    seeds[i] = s;
+    gain_num[i] = g;
+  }
+}
+
+// fast path on the compact store: no host synchronisation per step
+static bool dist_select_fast(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num) {
+  const uint32_t n = ctx->n, B = ctx->R_local;
+  const int world = ctx->comm_world;
+  const unsigned long long cap =
+      getenv("PACIM_DIST_CAP") ? (unsigned long long)std::max(1LL, atoll(getenv("PACIM_DIST_CAP")))
+                               : (1ull << 16);
+  DSel S;
+  S.rec = ctx->cs_rec.as<uint2>();
+  S.MW = ctx->cs_MW;
+  S.P = ctx->cs_P.as<uint32_t>();
+  S.moff = ctx->cs_moff.as<uint32_t>();
+  S.memb = ctx->cs_memb.as<uint32_t>();
+  S.cid = ctx->lean ? nullptr : ctx->cid.as<uint32_t>();
+  S.B = B;
+  S.nv = n;
+  S.big_t = ctx->cs_big_t;
+  S.hot_root = ctx->d_hot.as<uint32_t>();
+  S.hot_size = ctx->d_hot_size.as<uint32_t>();
+  S.ghot = ctx->dist_hot ? ctx->dist_ghot.as<int64_t>() : nullptr;
+  uint32_t csh = 10;
+  while (((uint64_t)n + (1ull << csh) - 1) >> csh > MAX_CHUNKS) csh++;
+  S.csh = csh;
+  S.nchunks = (uint32_t)(((uint64_t)n + (1ull << csh) - 1) >> csh);
+  S.cap = cap;
+  S.world = world;
+  S.cov_cap = (unsigned long long)k * B;
+  const size_t msg = (H_WORDS + cap) * 8;
+  pc_ensure(ctx, ctx->gain, (size_t)n * 8);
+  S.gain = ctx->gain.as<long long>();
+  // one scratch allocation: chunk cache, covered list, messages, state
+  const size_t o_cmax = 0;
+  const size_t o_dirty = o_cmax + (size_t)S.nchunks * sizeof(Best);
+  const size_t o_dlist = o_dirty + (size_t)S.nchunks * 4;
+  const size_t o_cov = (o_dlist + (size_t)S.nchunks * 4 + 15) & ~(size_t)15;
+  const size_t o_covr = o_cov + 8 + S.cov_cap * 8;
+  const size_t o_send = (o_covr + (size_t)B * 4 + 15) & ~(size_t)15;
+  const size_t o_recv = o_send + msg;
+  const size_t o_st = o_recv + msg * world;
+  const size_t o_out = o_st + D_WORDS * 8;
+  const size_t bytes = o_out + (size_t)k * 12 + 64;
+  pc_ensure(ctx, ctx->dist_buf, bytes);
+  char *base = ctx->dist_buf.as<char>();
+  S.cmax = reinterpret_cast<Best *>(base + o_cmax);
+  S.cdirty = reinterpret_cast<uint32_t *>(base + o_dirty);
+  S.dlist = reinterpret_cast<uint32_t *>(base + o_dlist);
+  S.cov_cnt = reinterpret_cast<unsigned long long *>(base + o_cov);
+  S.cov_list = S.cov_cnt + 1;
+  S.cov_root = reinterpret_cast<uint32_t *>(base + o_covr);
+  S.send = reinterpret_cast<unsigned long long *>(base + o_send);
+  S.recv = reinterpret_cast<unsigned long long *>(base + o_recv);
+  S.st = reinterpret_cast<unsigned long long *>(base + o_st);
+  S.gain_num = reinterpret_cast<long long *>(base + o_out);
+  S.seeds = reinterpret_cast<uint32_t *>(base + o_out + (size_t)k * 8);
+  // restore the covered flags of earlier selections on this store
+  pc_dist_restore(ctx);
+  pc_cs_select_reset(ctx);
+  PC_CUDA(cudaMemsetAsync(base, 0, o_recv, ctx->stream));  // cache, flags, lists, send
+  PC_CUDA(cudaMemsetAsync(S.st, 0, D_WORDS * 8, ctx->stream));
+  PC_CUDA(cudaMemcpyAsync(S.gain, ctx->gain0.p, (size_t)n * 8, cudaMemcpyDeviceToDevice,
+                          ctx->stream));
+  const unsigned grid = (unsigned)ctx->sm_count;
+  k_dist_chunks<<<grid, DT, 0, ctx->stream>>>(S, true);
+  PC_CHECK_LAUNCH();
+  cudaEvent_t e0, e1;
+  PC_CUDA(cudaEventCreate(&e0));
+  PC_CUDA(cudaEventCreate(&e1));
+  PC_CUDA(cudaEventRecord(e0, ctx->stream));
+  for (uint32_t i = 0; i < k; i++) {
+    k_dist_cover<<<grid, DT, 0, ctx->stream>>>(S, i);
+    k_dist_head<<<1, 256, 0, ctx->stream>>>(S);
+    PC_CHECK_LAUNCH();
+    PC_NCCL(ncclAllGather(S.send, const_cast<unsigned long long *>(S.recv), H_WORDS + cap,
+                          ncclUint64, comm_of(ctx), ctx->stream));
+    k_dist_apply<<<grid, DT, 0, ctx->stream>>>(S, i);
+    k_dist_chunks<<<grid, DT, 0, ctx->stream>>>(S, false);
+    PC_CHECK_LAUNCH();
+  }
+  PC_CUDA(cudaEventRecord(e1, ctx->stream));
+  unsigned long long st[D_WORDS], covn = 0;
+  std::vector<long long> hg(k);
+  PC_CUDA(cudaMemcpyAsync(st, S.st, sizeof(st), cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaMemcpyAsync(&covn, S.cov_cnt, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaMemcpyAsync(seeds, S.seeds, (size_t)k * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaMemcpyAsync(hg.data(), S.gain_num, (size_t)k * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  ctx->stats.t_select_ms = ms;
+  ctx->stats.kernel_launches_select = 4 * k + 1;
+  // keep the covered list so the next selection can restore the flags
+  PC_REQUIRE(covn <= S.cov_cap, PACIM_ECHECK, "sharded select: covered list overflowed");
+  pc_ensure(ctx, ctx->dist_cov_old, std::max<size_t>(covn, 1) * 8);
+  PC_CUDA(cudaMemcpyAsync(ctx->dist_cov_old.p, S.cov_list, covn * 8, cudaMemcpyDeviceToDevice,
+                          ctx->stream));
+  ctx->dist_cov_n = covn;
+  ctx->dist_cov_valid = true;
+  if (st[D_REPLAY]) return false;
+  PC_REQUIRE(!st[D_CHECK], PACIM_ECHECK, "sharded select: sum of delta_r differs from the argmax gain");
+  for (uint32_t i = 0; i < k; i++) gain_num[i] = hg[i];
+  return true;
+}
+
+void pc_dist_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num) {
+  PC_REQUIRE(pc_dist_active(ctx), PACIM_ESTATE,
+             "sharded build: pacim_init_comm(rank, world) with the build's shard first");
+  PC_REQUIRE(ctx->selector == 0, PACIM_ENOTIMPL, "sharded select: incremental selector only");
+  ctx->stats.select_dist_replays = 0;
+  if (ctx->cs && !getenv("PACIM_DIST_ROBUST")) {
+    if (dist_select_fast(ctx, k, seeds, gain_num)) return;
+    ctx->stats.select_dist_replays = 1;
+  }
+  pc_dist_restore(ctx);  // the fast path's covered flags
+  cudaEvent_t e0, e1;
+  PC_CUDA(cudaEventCreate(&e0));
+  PC_CUDA(cudaEventCreate(&e1));
+  PC_CUDA(cudaEventRecord(e0, ctx->stream));
+  dist_select_robust(ctx, k, seeds, gain_num);
+  PC_CUDA(cudaEventRecord(e1, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  ctx->stats.t_select_ms += ms;
+}

@@ -79,6 +79,15 @@ __device__ __forceinline__ size_t pc_addr(const uint32_t *smap, uint32_t nr, uin
   return (size_t)nr * f + (size_t)row * c + (j - f);
 }
 
+// compact store (store_cs.cu): entry of (row, slot j) given the row's record
+// words rec[row * MW + w] = {entries of the rows before + set bits of the row's
+// words before w, live-slot mask word w}
+__device__ __forceinline__ uint32_t pc_cs_pos(const uint2 *rec, uint32_t MW, uint32_t row,
+                                              uint32_t j) {
+  const uint2 r = rec[(size_t)row * MW + (j >> 5)];
+  return r.x + __popc(r.y & ((1u << (j & 31)) - 1u));
+}
+
 // ------------------------------------------------------- device allocation
 struct DevBuf {
   void *p = nullptr;
@@ -130,6 +139,16 @@ struct pacim_ctx {
   std::string err;
   int sm_count = 148;
   uint64_t device_bytes = 0;
+
+  // ---- multi-GPU (dist.cu): NCCL communicator of pacim_init_comm
+  void *comm = nullptr;     // ncclComm_t
+  int comm_rank = 0, comm_world = 1;
+  bool dist_hot = false;    // dist_ghot holds the all-reduced hot sums
+  DevBuf dist_ghot;         // i64[n]
+  DevBuf dist_buf;          // fast sharded select: chunk cache, lists, messages, state
+  DevBuf dist_cov_old;      // u64: covered root entries of the last fast select
+  unsigned long long dist_cov_n = 0;
+  bool dist_cov_valid = false;
 
   // ---- graph (H0/H1)
   bool has_graph = false;
@@ -207,6 +226,22 @@ struct pacim_ctx {
   DevBuf gain0;       // i64[n]
   DevBuf gain;        // i64[n] working gains of a selection
 
+  // compact uncompressed store (store_cs.cu): entries only for
+  // the (row, slot) pairs whose vertex has a live edge in the slot's sketch
+  bool cs = false;          // the current store is the compact one
+  uint32_t cs_MW = 0;       // mask words per row (ceil(B / 32))
+  uint64_t cs_total = 0;    // entries = non-singleton (vertex, sketch) pairs
+  uint64_t cs_nmemb = 0;    // member-index entries (CCs of <= cs_big_t vertices)
+  uint32_t cs_big_t = 0;    // CCs above it: no member list (dense pass / hot sums)
+  DevBuf cs_rec;            // uint2[nr][MW]: {entry prefix, live-slot mask word}
+  DevBuf cs_soff;           // u32[nr + 1]: first entry of a row
+  DevBuf cs_sl;             // u8[total]: slot of an entry
+  DevBuf cs_ecrow;          // u32[total / 32 + 1]: row of entry 32 c
+  DevBuf cs_P;              // u32[total]: union-find parents -> HIGH | size / root entry
+  DevBuf cs_moff;           // u32[total + 1]: member-index end of a root entry
+  DevBuf cs_memb;           // u32[nmemb]: members (vertex ids) grouped by root entry
+  DevBuf cs_diag;           // u64 selection diagnostics
+
   // compressed store (H6c)
   uint32_t rho = 0;
   DevBuf center_of;   // u32[n] center index or 0xFFFFFFFF
@@ -280,6 +315,27 @@ void pc_generate(pacim_ctx *ctx, int kind, const uint64_t *params, int nparams,
                  uint64_t gen_seed);
 // build.cu
 void pc_build(pacim_ctx *ctx);
+void pc_cs_edges(pacim_ctx *ctx, uint32_t *P, const uint2 *rec, uint32_t MW,
+                 unsigned long long *ctr);
+// dist.cu: NCCL sharding
+void pc_nccl_unique_id(void *out);
+void pc_init_comm(pacim_ctx *ctx, int rank, int world, const void *id);
+void pc_free_comm(pacim_ctx *ctx);
+bool pc_dist_active(const pacim_ctx *ctx);
+void pc_dist_build_finish(pacim_ctx *ctx);
+void pc_dist_restore(pacim_ctx *ctx);
+void pc_dist_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num);
+// store_cs.cu: the compact store (build, selection, inspection)
+bool pc_cs_build(pacim_ctx *ctx);  // false: not eligible (dense store instead)
+void pc_cs_free(pacim_ctx *ctx);
+void pc_cs_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
+                  int64_t *sigma_num);
+void pc_cs_select_reset(pacim_ctx *ctx);
+void pc_cs_cover_local(pacim_ctx *ctx, uint32_t s, int64_t *d_delta, int64_t *local_gain);
+void pc_cs_get_labels(pacim_ctx *ctx, uint32_t slot, uint32_t *host_out);
+void pc_cs_lazy_eval(pacim_ctx *ctx, const uint32_t *cand, uint32_t b0, uint32_t b1,
+                     long long *delta);
+void pc_cs_lazy_mark(pacim_ctx *ctx, uint32_t s);
 void pc_slot_table(pacim_ctx *ctx);
 // Live hub adjacency (HLA) being recorded: raw (key << 32 | other row) with
 // key = hub index * B + slot, appended in any order (grouped by key after the

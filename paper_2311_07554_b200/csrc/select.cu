@@ -1440,6 +1440,7 @@ static void uncover(pacim_ctx *ctx, const Sel &S) {
 }
 
 void pc_select_reset(pacim_ctx *ctx) {
+  if (ctx->cs) return pc_cs_select_reset(ctx);
   Sel S = make_sel(ctx, nullptr);
   uncover(ctx, S);
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1464,6 +1465,7 @@ static void read_diag(pacim_ctx *ctx, const Sel &S) {
 
 void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
                int64_t *sigma_num) {
+  if (ctx->cs) return pc_cs_select(ctx, k, seeds, gain_num, sigma_num);
   const uint32_t n = ctx->n;
   pc_ensure(ctx, ctx->gain, (size_t)n * 8);
   if (k > ctx->sel_k_cap) {
@@ -1567,6 +1569,7 @@ void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
 // One multi-rank step: MarkSeed of the given seed s on this ctx's sketches and
 // the member deltas (-delta per member) accumulated into d_delta.
 void pc_cover_local(pacim_ctx *ctx, uint32_t s, int64_t *d_delta, int64_t *local_gain) {
+  if (ctx->cs) return pc_cs_cover_local(ctx, s, d_delta, local_gain);
   PC_REQUIRE(ctx->sel_list_valid, PACIM_ESTATE, "pacim_select_reset first");
   Sel S = make_sel(ctx, reinterpret_cast<long long *>(d_delta));
   pc_ensure(ctx, ctx->sel_gain, 64);
@@ -1687,21 +1690,30 @@ void pc_traverse_slots(pacim_ctx *ctx, uint32_t s, int64_t *target, const uint32
 void pc_select_lazy(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
                     int64_t *sigma_num) {
   const uint32_t n = ctx->n;
+  const bool cs = ctx->cs;
   if (k > ctx->sel_k_cap) {
     if (ctx->sel_list_valid) {
-      Sel old = make_sel(ctx, nullptr);
-      uncover(ctx, old);
+      if (cs) {
+        pc_cs_select_reset(ctx);
+      } else {
+        Sel old = make_sel(ctx, nullptr);
+        uncover(ctx, old);
+      }
     }
     ctx->sel_k_cap = k;
     ctx->sel_list_valid = false;
   }
   pc_ensure(ctx, ctx->gain, (size_t)n * 8);
-  Sel S = make_sel(ctx, ctx->gain.as<long long>());
+  Sel S{};
+  if (!cs) S = make_sel(ctx, ctx->gain.as<long long>());
   cudaEvent_t e0, e1;
   PC_CUDA(cudaEventCreate(&e0));
   PC_CUDA(cudaEventCreate(&e1));
   PC_CUDA(cudaEventRecord(e0, ctx->stream));
-  uncover(ctx, S);
+  if (cs)
+    pc_cs_select_reset(ctx);
+  else
+    uncover(ctx, S);
   long long *delta = ctx->gain.as<long long>();
   PC_CUDA(cudaMemcpyAsync(delta, ctx->gain0.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
   // sort buffers: keys x2, ids x2, partial maxima
@@ -1733,9 +1745,13 @@ void pc_select_lazy(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_n
     uint32_t done = 0, b = 1;
     Best best{LLONG_MIN, NONE};
     for (;;) {
-      k_lazy_eval<<<pc_grid(ctx, (size_t)(b - done) * 32, 256, 8), 256, 0, ctx->stream>>>(
-          S, cand, done, b, delta);
-      PC_CHECK_LAUNCH();
+      if (cs) {
+        pc_cs_lazy_eval(ctx, cand, done, b, delta);
+      } else {
+        k_lazy_eval<<<pc_grid(ctx, (size_t)(b - done) * 32, 256, 8), 256, 0, ctx->stream>>>(
+            S, cand, done, b, delta);
+        PC_CHECK_LAUNCH();
+      }
       evals += b - done;
       rounds++;
       const unsigned g = std::min<unsigned>(pg, (b + SEL_THREADS - 1) / SEL_THREADS);
@@ -1760,8 +1776,12 @@ void pc_select_lazy(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_n
     gain_num[step] = best.g;
     run += best.g;
     sigma_num[step] = run;
-    k_lazy_mark<<<(S.B + 255) / 256, 256, 0, ctx->stream>>>(S, best.v);
-    PC_CHECK_LAUNCH();
+    if (cs) {
+      pc_cs_lazy_mark(ctx, best.v);
+    } else {
+      k_lazy_mark<<<(S.B + 255) / 256, 256, 0, ctx->stream>>>(S, best.v);
+      PC_CHECK_LAUNCH();
+    }
     const long long m1 = -1;  // s leaves the candidate set (R6)
     PC_CUDA(cudaMemcpyAsync(delta + best.v, &m1, 8, cudaMemcpyHostToDevice, ctx->stream));
   }

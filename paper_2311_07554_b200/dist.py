@@ -32,6 +32,18 @@ import torch
 NONE = 0xFFFFFFFF
 
 
+def init_comm(ctx, rank: int, world: int, group=None):
+    """NCCL communicator of the library (pacim_init_comm): rank 0 makes the
+    128-byte id, torch.distributed broadcasts it (host plumbing only); the
+    sharded build then all-reduces gain0 and pacim_select_seeds runs the
+    whole sharded greedy loop inside the library (dist.cu)."""
+    import torch.distributed as dist
+    from .binding import pacim_nccl_unique_id
+    obj = [pacim_nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    ctx.pacim_init_comm(rank, world, obj[0])
+
+
 class _Shard:
     """One engine's step buffers: dense delta and the sparse list."""
 

@@ -39,7 +39,7 @@ def test_binding_names_match_header(libpath):
     assert sorted(binding.EXPORTS) == header_symbols()
     for s in header_symbols():
         if s in ("pacim_create", "pacim_destroy", "pacim_last_error", "pacim_version",
-                 "pacim_threshold_from_p", "pacim_threshold_uniform"):
+                 "pacim_threshold_from_p", "pacim_threshold_uniform", "pacim_nccl_unique_id"):
             continue
         assert hasattr(binding.Context, s), s
 
@@ -68,3 +68,11 @@ def test_product_path_does_not_import_oracle():
             if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
                 txt = open(os.path.join(dp, f)).read()
                 assert "oracle" not in re.sub(r"#.*|//.*", "", txt).lower(), f
+
+
+def test_nccl_linked_in_library(libpath):
+    """The multi-GPU path calls NCCL from the library (dist.cu): libpacim.so
+    depends on libnccl.so.2 (the venv's build, the one torch loads)."""
+    import subprocess
+    out = subprocess.run(["ldd", libpath], capture_output=True, text=True).stdout
+    assert "libnccl.so.2" in out

@@ -99,6 +99,36 @@ def test_tiny_corpus_parity(orc, ctx, i):
     full_parity(orc, ctx, g, model, t32, R, 1000 + i, min(k, g.n))
 
 
+@pytest.mark.parametrize("i", range(len(CASES)))
+def test_tiny_corpus_parity_dense_store(orc, ctx, i, monkeypatch):
+    """The dense vertex-major store (the layout dense sketches such as c3
+    use; PACIM_STORE=dense forces it): the same oracle parity."""
+    monkeypatch.setenv("PACIM_STORE", "dense")
+    test_tiny_corpus_parity(orc, ctx, i)
+    assert ctx.pacim_get_stats()["store"] == 0
+
+
+@pytest.mark.parametrize("i", [0, 2, 3, 7, 9, 10, 11])
+def test_compact_store_used(orc, ctx, i):
+    """Sparse sketches take the compact store; its entries are exactly the
+    non-singleton (vertex, sketch) pairs of the oracle's labels."""
+    from oracle.oracle import Graph
+    build_fn, p, R, k = CASES[i]
+    off, nbr = build_fn()
+    g = Graph(len(off) - 1, off, nbr)
+    model, t32 = model_of(orc, p)
+    full_parity(orc, ctx, g, model, t32, R, 1000 + i, min(k, g.n), check_labels=False)
+    st = ctx.pacim_get_stats()
+    assert st["store"] == 1
+    nons = 0
+    roots = 0
+    for r in range(R):
+        lab, size = orc.sketch_labels(g, model, t32, 1000 + i, r)
+        nons += int((size > 1).sum())
+        roots += int(((size > 1) & (lab == np.arange(g.n))).sum())
+    assert st["nnonsingle"] == nons and st["ncomp"] == roots
+
+
 @pytest.mark.parametrize("i", [0, 2, 3, 5, 7, 9, 10])
 def test_dense_cover_path(orc, ctx, i, monkeypatch):
     """Force components of >= 8 vertices out of the member index so MarkSeed
@@ -118,8 +148,10 @@ def test_dense_cover_path(orc, ctx, i, monkeypatch):
 @pytest.mark.parametrize("i", [0, 2, 3, 7, 8, 9, 11])
 def test_traversal_paths(orc, ctx, i, env, monkeypatch):
     """The shared traversal of the cover step (row items and chunk items of
-    the work queue), forced on the tiny corpus by shrinking the chunk size and
-    disabling the warp-local BFS; must give the oracle's greedy."""
+    the work queue) of the dense store, forced on the tiny corpus by shrinking
+    the chunk size and disabling the warp-local BFS; must give the oracle's
+    greedy."""
+    monkeypatch.setenv("PACIM_STORE", "dense")
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     test_tiny_corpus_parity(orc, ctx, i)
