@@ -248,6 +248,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-dist", action="store_true",
                     help="testing: NCCL process group and the per-step collectives even at one rank")
+    ap.add_argument("--py-dist", action="store_true",
+                    help="multi-rank select through dist.py's per-step primitives (torch.distributed) "
+                         "instead of the library's NCCL loop")
     args = ap.parse_args()
     args.e2e_steps = max(1, args.e2e_steps)  # the e2e number needs at least one step
     cfg = inputs.config(args.config, **({"scale": args.scale} if args.scale else {}))
@@ -267,11 +270,15 @@ def main():
     if use_dist:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
+        if world == 1:
+            os.environ["PACIM_FORCE_DIST"] = "1"  # the sharded code at one rank (testing)
     import paper_2311_07554_b200 as P
     from paper_2311_07554_b200 import dist as pdist
     from paper_2311_07554_b200 import pipeline
     stream = torch.cuda.current_stream(dev)
     ctx = P.Context(local, stream)  # torch's current stream (legacy default: cudaStreamLegacy)
+    if use_dist and not args.py_dist:
+        pdist.init_comm(ctx, rank, world)  # NCCL inside the library (pacim_init_comm)
     n, m = pipeline.generate(ctx, cfg)
     pm, t32 = pipeline.model_of(cfg)
     a32 = pipeline.center_a32_of(cfg)
@@ -283,9 +290,9 @@ def main():
 
     def step():
         ctx.pacim_build_sketches(R, cfg["hash_seed"], a32, rank, world)
-        if not use_dist:
-            return ctx.pacim_select_seeds(k)
-        return pdist.distributed_select(ctx, n, k, dev)
+        if use_dist and args.py_dist:
+            return pdist.distributed_select(ctx, n, k, dev)
+        return ctx.pacim_select_seeds(k)  # sharded: the whole greedy loop in the library
 
     for _ in range(max(3, args.warmup)):
         step()
@@ -306,7 +313,7 @@ def main():
         st = ctx.stats_raw()  # the struct's fields, no dict: little host time between steps
         for kk in keys:
             acc[kk] += getattr(st, kk)
-        launches += st.kernel_launches_build + (st.kernel_launches_select if world == 1 else 0)
+        launches += st.kernel_launches_build + (st.kernel_launches_select if not args.py_dist else 0)
     e1.record(stream)
     torch.cuda.synchronize(dev)
     barrier()
@@ -373,7 +380,8 @@ def main():
         ctx.pacim_build_sketches(R, cfg["hash_seed"], a32, rank, world)  # commits step i's graph
         if i + 2 < args.e2e_steps and not _sync:
             ctx.pacim_load_graph_async(off_np, nbr_np, pm, t32)  # step i+2's input
-        out = ctx.pacim_select_seeds(k) if not use_dist else pdist.distributed_select(ctx, n, k, dev)
+        out = (pdist.distributed_select(ctx, n, k, dev) if (use_dist and args.py_dist)
+               else ctx.pacim_select_seeds(k))
         _tw.append(time.perf_counter())
         if os.environ.get("PACIM_BENCH_DEBUG"):
             _st = ctx.stats_raw()
@@ -442,6 +450,8 @@ def main():
         "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (counter-based generator, DESIGN.md §Input recipe)",
+        "select_path": ("dist.py per-step primitives (torch.distributed)" if (use_dist and args.py_dist)
+                        else "library NCCL loop (pacim_init_comm)" if use_dist else "single GPU"),
         "config": {"workload": cfg["name"] + (f"-scale{args.scale}" if args.scale else ""),
                    "config": args.config, "n": n, "m": m, "R": R, "k": k,
                    "alpha": cfg.get("alpha"),

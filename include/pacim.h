@@ -111,6 +111,12 @@ typedef struct {
     uint32_t select_dist_replays;   /* sharded select: 1 if the fast path (fixed-size delta
                                        lists, no host sync per step) could not apply a step
                                        and the selection was re-run on the robust path */
+    uint64_t device_peak_bytes;     /* high-water mark of device_bytes since the last
+                                       pacim_build_sketches started (graph included) */
+    uint64_t select_celf_evaluations; /* incremental selector with PACIM_CELF_COUNT=1: the
+                                       re-evaluations CELF would make: at step
+                                       i >= 2, every non-seed whose stale score ranks at or
+                                       above the winner's fresh one (gain desc, id asc) */
 } pacim_stats;
 
 /* --------------------------------------------------------------- lifecycle */
@@ -181,10 +187,18 @@ PACIM_API int pacim_simulate_ic(pacim_ctx *ctx, const uint32_t *seeds, uint32_t 
 
 /* NEXT f2: the selector of pacim_select_seeds on an uncompressed store.
  * 0 (default) = incremental (member gains updated when a CC is covered);
- * 1 = lazy / CELF-style (stale upper bounds, fresh evaluations of prefixes of
- * 1, 2, 4, ... candidates in (stale desc, id asc) order, P:536-578 and
- * P:2381-2401), which counts evaluations (stats.select_evaluations).  Both
- * return the same sequence (R17).  EINVAL for another value. */
+ * 1 = lazy, prefix doubling (the P-tree scheme): stale upper
+ *     bounds, fresh evaluations of prefixes of 1, 2, 4, ... candidates in
+ *     (stale desc, id asc) order;
+ * 2 = lazy, Win-Tree: an implicit winning tree over the stale
+ *     bounds, FindMax pruning every subtree whose stale winner cannot beat the
+ *     best fresh score (compact store; the dense store falls back to 1).
+ * The lazy selectors count their re-evaluations (stats.select_evaluations;
+ * Win-Tree: stats.select_eval_rounds = tree nodes explored).  With the
+ * environment variable PACIM_CELF_COUNT=1 the incremental selector also counts
+ * the re-evaluations CELF would make on the same gains
+ * (stats.select_celf_evaluations).  All return the same sequence (R17).
+ * EINVAL for another value. */
 PACIM_API int pacim_set_selector(pacim_ctx *ctx, int selector);
 
 /* NEXT f3, R20: the sampling rule of the sketches built after this call.

@@ -54,6 +54,7 @@ class Stats(C.Structure):
         ("select_evaluations", C.c_uint64), ("select_eval_rounds", C.c_uint64),
         ("hla_entries", C.c_uint64), ("hubs", C.c_uint32), ("select_hotsum_steps", C.c_uint64),
         ("lean", C.c_uint32), ("store", C.c_uint32), ("select_dist_replays", C.c_uint32),
+        ("device_peak_bytes", C.c_uint64), ("select_celf_evaluations", C.c_uint64),
     ]
 
     def asdict(self):
@@ -253,7 +254,8 @@ class Context:
         return t.value
 
     def pacim_set_selector(self, selector: int):
-        """0: incremental (default); 1: lazy / CELF with evaluation counts (NEXT f2)."""
+        """0: incremental (default); 1: lazy, prefix doubling; 2: lazy, Win-Tree
+        (NEXT f2; both lazy selectors count their evaluations)."""
         self._check(self._L.pacim_set_selector(self._h, int(selector)))
 
     def pacim_set_hash_rule(self, rule: int):

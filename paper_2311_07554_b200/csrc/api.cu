@@ -92,6 +92,7 @@ void pc_ensure(pacim_ctx *ctx, DevBuf &b, size_t bytes) {
   }
   b.bytes = bytes;
   ctx->device_bytes += bytes;
+  ctx->device_peak = std::max(ctx->device_peak, ctx->device_bytes);
 }
 
 void pc_free(pacim_ctx *ctx, DevBuf &b) {
@@ -153,8 +154,8 @@ static void free_all(pacim_ctx *ctx) {
                     &ctx->d_tab, &ctx->gain0,      &ctx->gain,     &ctx->center_of, &ctx->counters,
                     &ctx->scratch, &ctx->scratch2, &ctx->sel_seeds, &ctx->sel_gain,
                     &ctx->sel_partial, &ctx->sel_list, &ctx->sel_flag, &ctx->argmax_part, &ctx->bfs, &ctx->tcsr, &ctx->hidx, &ctx->hub_tab, &ctx->hla_off, &ctx->hla_row, &ctx->hla_raw, &ctx->d_smap, &ctx->pkeys, &ctx->cprobe, &ctx->cseed, &ctx->d_hr64, &ctx->crow, &ctx->vinfo, &ctx->hotsum, &ctx->d_hot_size,
-                    &ctx->cs_rec, &ctx->cs_soff, &ctx->cs_sl, &ctx->cs_ecrow, &ctx->cs_P, &ctx->cs_moff,
-                    &ctx->cs_memb, &ctx->cs_diag, &ctx->dist_ghot, &ctx->dist_buf, &ctx->dist_cov_old};
+                    &ctx->cs_rec, &ctx->cs_soff, &ctx->cs_ecrow, &ctx->cs_E, &ctx->cs_vid,
+                    &ctx->cs_diag, &ctx->cs_cnt, &ctx->cs_roff, &ctx->cs_rcrow, &ctx->dist_ghot, &ctx->dist_buf, &ctx->dist_cov_old};
   for (DevBuf *b : bufs) pc_free(ctx, *b);
 }
 
@@ -307,6 +308,7 @@ static void commit_staged(pacim_ctx *ctx) {
   std::swap(ctx->nbr, st.nbr);  // buffers are the slot's next staging area
   pc_graph_finish_load(ctx, 0);
   ctx->has_graph = true;
+  ctx->graph_gen++;
   PC_CUDA(cudaEventRecord(ctx->released, ctx->stream));
 }
 
@@ -337,6 +339,7 @@ int pacim_load_graph(pacim_ctx *ctx, uint32_t n, uint64_t nnz, const uint64_t *o
       PC_CUDA(cudaMemcpyAsync(ctx->nbr.p, neighbors, nnz * 4, cudaMemcpyHostToDevice, ctx->stream));
     pc_graph_finish_load(ctx, validate);
     ctx->has_graph = true;
+  ctx->graph_gen++;
   });
 }
 
@@ -398,6 +401,7 @@ int pacim_load_graph_device(pacim_ctx *ctx, uint32_t n, uint64_t nnz, const uint
     PC_REQUIRE(ends[1] == nnz, PACIM_EINVAL, "offsets[n] != nnz");
     pc_graph_finish_load(ctx, validate);
     ctx->has_graph = true;
+  ctx->graph_gen++;
   });
 }
 
@@ -412,6 +416,7 @@ int pacim_generate_graph(pacim_ctx *ctx, int kind, const uint64_t *params, int n
     ctx->t32 = t32;
     pc_generate(ctx, kind, params, nparams, gen_seed);
     ctx->has_graph = true;
+  ctx->graph_gen++;
   });
 }
 
@@ -446,6 +451,7 @@ int pacim_build_sketches(pacim_ctx *ctx, uint32_t R, uint64_t hash_seed, uint64_
                "need 0 <= shard_rank < shard_world");
     PC_REQUIRE(shard_rank < R, PACIM_EINVAL, "shard holds no sketch (shard_rank >= R)");
     drop_sketches(ctx);
+    ctx->device_peak = ctx->device_bytes;  // high-water mark of this build + select
 
     ctx->R = R;
     ctx->rank = shard_rank;
@@ -470,7 +476,7 @@ int pacim_select_seeds(pacim_ctx *ctx, uint32_t k, uint32_t *seeds_out, int64_t 
     PC_REQUIRE(ctx->built, PACIM_ESTATE, "select before build_sketches");
     PC_REQUIRE(k >= 1 && k <= ctx->n, PACIM_EINVAL, "k must be in [1, n]");
     PC_REQUIRE(seeds_out && gain_num_out && sigma_num_out, PACIM_EINVAL, "NULL output");
-    if (ctx->world > 1) {
+    if (ctx->world > 1 || pc_dist_active(ctx)) {
       // sharded build: the greedy loop over NCCL (dist.cu); without a
       // communicator the per-rank step primitives remain (dist.py)
       pc_dist_select(ctx, k, seeds_out, gain_num_out);
@@ -479,7 +485,9 @@ int pacim_select_seeds(pacim_ctx *ctx, uint32_t k, uint32_t *seeds_out, int64_t 
     } else if (ctx->compressed)
       pc_select_compressed(ctx, k, seeds_out, gain_num_out, sigma_num_out);
     else
-      if (ctx->selector == 1)
+      if (ctx->selector == 2 && ctx->cs)
+        pc_cs_select_wintree(ctx, k, seeds_out, gain_num_out, sigma_num_out);
+      else if (ctx->selector >= 1)
         pc_select_lazy(ctx, k, seeds_out, gain_num_out, sigma_num_out);
       else
         pc_select(ctx, k, seeds_out, gain_num_out, sigma_num_out);
@@ -566,7 +574,8 @@ int pacim_simulate_ic(pacim_ctx *ctx, const uint32_t *seeds, uint32_t ns, uint32
 
 int pacim_set_selector(pacim_ctx *ctx, int selector) {
   return guarded(ctx, [&] {
-    PC_REQUIRE(selector == 0 || selector == 1, PACIM_EINVAL, "selector must be 0 or 1");
+    PC_REQUIRE(selector >= 0 && selector <= 2, PACIM_EINVAL,
+               "selector must be 0 (incremental), 1 (prefix doubling) or 2 (Win-Tree)");
     ctx->selector = selector;
   });
 }
@@ -662,6 +671,7 @@ int pacim_get_stats(pacim_ctx *ctx, pacim_stats *out) {
     s.store = ctx->compressed ? 2u : (ctx->cs ? 1u : 0u);
     s.nnonsingle = ctx->nnonsingle;
     s.device_bytes = ctx->device_bytes;
+    s.device_peak_bytes = ctx->device_peak;
     *out = s;
   });
 }

@@ -241,7 +241,7 @@ __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__res
                   (lv && (v & PACIM_HUBF)) ? 1u : 0u, w_hla[REC ? wid : 0], hla_n);
       if (lv) {
         if (CS)
-          uf_unite(L, 1, 0, pc_cs_pos(rec, MW, u & ~PACIM_HUBF, j),
+          uf_unite(L, 2, 0, pc_cs_pos(rec, MW, u & ~PACIM_HUBF, j),
                    pc_cs_pos(rec, MW, v & ~PACIM_HUBF, j));
         else
           uf_unite(L, Bb, j - j0, u & ~PACIM_HUBF, v & ~PACIM_HUBF);

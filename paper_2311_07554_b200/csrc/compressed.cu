@@ -26,6 +26,19 @@
 
 namespace {
 
+// A center's CC size in the store, with bit 31 set once MarkSeed covered the
+// CC in the current selection (one word per (center, slot): the paper's
+// label + size pair, no separate working copy); cleared by the select reset.
+constexpr uint32_t CSZ_COV = 0x80000000u;
+__device__ __forceinline__ uint32_t csz_live(uint32_t x) { return (x & CSZ_COV) ? 0u : x; }
+
+__global__ void k_csz_uncover(uint32_t *csz, size_t N) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+       i += (size_t)gridDim.x * blockDim.x)
+    if (csz[i] & CSZ_COV) csz[i] &= ~CSZ_COV;
+}
+
+
 constexpr uint32_t NONE = 0xFFFFFFFFu;
 constexpr int PROBE_WARPS = 4;     // warps per block in k_probe
 constexpr uint32_t HOT_BIG_T = 65536;  // covered CCs above this go to the rebuild (or hotsum)
@@ -170,7 +183,7 @@ struct ProbeParams {
   uint32_t B;
   const uint32_t *center_of;
   const uint32_t *clabel;   // [rho][B]
-  uint32_t *csw;            // [rho][B] working sizes
+  uint32_t *csw;            // [rho][B] sizes; bit 31 = covered in this selection
   const uint8_t *is_seed;
   long long *target;        // gain (or delta) vector, n entries
   DeltaList dlst;           // multi-rank sparse deltas (v == nullptr: off)
@@ -300,7 +313,7 @@ __global__ void __launch_bounds__(PROBE_WARPS * 32) k_probe(ProbeParams P, uint3
         label = found[w];
         cvis += head;  // Get-center visits until a center was met (Thm 3.1)
         nfound++;
-        delta = P.csw[(size_t)label * P.B + j];
+        delta = csz_live(P.csw[(size_t)label * P.B + j]);
         if (delta == 0 || delta > QCAP) break;  // covered, or too big to enumerate here
         enumerate = true;  // uncovered CC of delta <= QCAP vertices: list its members
       }
@@ -351,7 +364,7 @@ __global__ void __launch_bounds__(PROBE_WARPS * 32) k_probe(ProbeParams P, uint3
         label = found[w];
         cvis += head;
         nfound++;
-        delta = P.csw[(size_t)label * P.B + j];
+        delta = csz_live(P.csw[(size_t)label * P.B + j]);
         if (delta == 0 || delta > QCAP) break;
         // uncovered and small: restart the walk from the queue head to list
         // every member (the queue already holds the visited part of the CC;
@@ -378,7 +391,7 @@ __global__ void __launch_bounds__(PROBE_WARPS * 32) k_probe(ProbeParams P, uint3
           }
         }
       }
-      if (lane == 0 && delta > 0) P.csw[(size_t)label * P.B + j] = 0;  // MarkSeed
+      if (lane == 0 && delta > 0) P.csw[(size_t)label * P.B + j] |= CSZ_COV;  // MarkSeed
     } else if (ovf[w]) {
       status = ST_BIG_UNKNOWN;  // no center among the first QCAP vertices
     } else {
@@ -446,11 +459,11 @@ __global__ void k_big_decide(uint32_t Bb, uint32_t j0, uint32_t B, uint32_t *st,
     uint32_t d = 0;
     if (st[j] == ST_BIG_KNOWN) {
       d = dl[j];
-      csw[(size_t)lab[j] * B + j] = 0;
+      csw[(size_t)lab[j] * B + j] |= CSZ_COV;
     } else if (st[j] == ST_BIG_UNKNOWN) {
       if (clab[jj] != NONE) {
-        d = csw[(size_t)clab[jj] * B + j];
-        csw[(size_t)clab[jj] * B + j] = 0;
+        d = csz_live(csw[(size_t)clab[jj] * B + j]);
+        csw[(size_t)clab[jj] * B + j] |= CSZ_COV;
       } else {
         d = seedf[jj] ? 0 : (uint32_t)cnt[jj];
       }
@@ -543,11 +556,16 @@ static uint32_t choose_batch(pacim_ctx *ctx) {
   // the selection's traversal state is not reserved: if it is needed later,
   // the batch buffer is released first and re-created smaller on demand
   // (pc_release_batch / the rebuild in pc_cover_compressed)
+  // Thm 3.1: the store is O((1 + alpha R) n) words; the batch
+  // parent arrays are scratch on top of it, so their budget follows the store
+  // (twice its bytes, at least 4 GB) instead of taking the free memory —
+  // peak memory then tracks alpha.  PACIM_BATCH_MEM overrides (bytes).
   const size_t keep = (size_t)2 << 30;
-  const size_t ample = fr > keep ? fr - keep : 0;
-  // tight memory (c4 alpha = 1/2: 103 GB store): the old third, capped at
-  // 24 GB — bigger batches there are re-allocated around the HLA every build
-  size_t budget = ample >= ((size_t)40 << 30) ? ample : std::min<size_t>(fr / 3, (size_t)24 << 30);
+  const size_t avail = fr > keep ? fr - keep : fr / 2;
+  const size_t store = 2 * (size_t)ctx->rho * B * 4;  // label + size per (center, slot)
+  size_t budget = std::max<size_t>(2 * store, (size_t)4 << 30);
+  if (const char *e = getenv("PACIM_BATCH_MEM")) budget = (size_t)std::max(1LL, atoll(e));
+  budget = std::min(budget, avail);
   // per slot: a parent word per row (Ltmp) and a root word per center (cwork)
   size_t per = ((size_t)std::max<uint32_t>(ctx->nr, 1) + ctx->rho) * 4;
   size_t bb = budget / per;
@@ -596,11 +614,11 @@ void pc_build_compressed(pacim_ctx *ctx) {
       flag, pos, n, ctx->center_of.as<uint32_t>(), ctx->centers.as<uint32_t>());
   PC_CHECK_LAUNCH();
   const size_t cs = std::max<size_t>((size_t)rho * B, 1) * 4;
-  for (DevBuf *d : {&ctx->clabel, &ctx->csz, &ctx->csz_work})
+  pc_free(ctx, ctx->csz_work);  // no working copy (covered bit in csz)
+  for (DevBuf *d : {&ctx->clabel, &ctx->csz})
     if (d->bytes > 2 * cs) pc_free(ctx, *d);  // an earlier, larger alpha's store
   pc_ensure(ctx, ctx->clabel, cs);
   pc_ensure(ctx, ctx->csz, cs);
-  pc_ensure(ctx, ctx->csz_work, cs);
   pc_ensure(ctx, ctx->gain0, (size_t)n * 8);
   k_fill_i64c<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(ctx->gain0.as<int64_t>(), n,
                                                             (int64_t)B);
@@ -664,7 +682,6 @@ void pc_build_compressed(pacim_ctx *ctx) {
   ctx->hot_size.resize(B);
   PC_CUDA(cudaMemcpyAsync(ctx->hot_size.data(), ctx->d_hot_size.p, (size_t)B * 4,
                           cudaMemcpyDeviceToHost, ctx->stream));
-  PC_CUDA(cudaMemcpyAsync(ctx->csz_work.p, ctx->csz.p, cs, cudaMemcpyDeviceToDevice, ctx->stream));
   PC_CUDA(cudaEventRecord(e2, ctx->stream));
   unsigned long long h[6];
   PC_CUDA(cudaMemcpyAsync(h, ctr, 6 * 8, cudaMemcpyDeviceToHost, ctx->stream));
@@ -705,8 +722,10 @@ void pc_build_compressed(pacim_ctx *ctx) {
 }
 
 void pc_select_reset_compressed(pacim_ctx *ctx) {
-  const size_t cs = std::max<size_t>((size_t)ctx->rho * ctx->R_local, 1) * 4;
-  PC_CUDA(cudaMemcpyAsync(ctx->csz_work.p, ctx->csz.p, cs, cudaMemcpyDeviceToDevice, ctx->stream));
+  const size_t cw = (size_t)ctx->rho * ctx->R_local;
+  if (cw)
+    k_csz_uncover<<<pc_grid(ctx, cw, 256), 256, 0, ctx->stream>>>(ctx->csz.as<uint32_t>(), cw);
+  PC_CHECK_LAUNCH();
   pc_ensure(ctx, ctx->is_seed, ctx->n);
   PC_CUDA(cudaMemsetAsync(ctx->is_seed.p, 0, ctx->n, ctx->stream));
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -747,7 +766,7 @@ void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *l
   P.B = B;
   P.center_of = ctx->center_of.as<uint32_t>();
   P.clabel = ctx->clabel.as<uint32_t>();
-  P.csw = ctx->csz_work.as<uint32_t>();
+  P.csw = ctx->csz.as<uint32_t>();
   P.is_seed = ctx->is_seed.as<uint8_t>();
   P.target = reinterpret_cast<long long *>(target);
   P.dlst = ctx->dlist;
@@ -890,7 +909,7 @@ void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *l
           Lb, nr, bb, j0, B, st, sroot, ctx->rmap.as<uint32_t>(), ctx->center_of.as<uint32_t>(),
           ctx->clabel.as<uint32_t>(), ctx->is_seed.as<uint8_t>(), cnt, clab, seedf);
       k_big_decide<<<(bb + 255) / 256, 256, 0, ctx->stream>>>(bb, j0, B, st, dl, lab, cnt, clab,
-                                                             seedf, ctx->csz_work.as<uint32_t>(),
+                                                             seedf, ctx->csz.as<uint32_t>(),
                                                              sum);
       k_big_apply<<<pc_grid(ctx, (size_t)nr * 32, 256, 16), 256, 0, ctx->stream>>>(
           Lb, nr, bb, j0, st, dl, sroot, ctx->rmap.as<uint32_t>(), s,
@@ -958,11 +977,12 @@ void pc_get_center_sketch(pacim_ctx *ctx, uint32_t slot, uint32_t *label, uint32
   std::vector<uint32_t> a((size_t)rho * B), b((size_t)rho * B);
   PC_CUDA(cudaMemcpyAsync(a.data(), ctx->clabel.p, (size_t)rho * B * 4, cudaMemcpyDeviceToHost,
                           ctx->stream));
-  PC_CUDA(cudaMemcpyAsync(b.data(), ctx->csz_work.p, (size_t)rho * B * 4, cudaMemcpyDeviceToHost,
+  PC_CUDA(cudaMemcpyAsync(b.data(), ctx->csz.p, (size_t)rho * B * 4, cudaMemcpyDeviceToHost,
                           ctx->stream));
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
   for (uint32_t i = 0; i < rho; i++) {
     label[i] = a[(size_t)i * B + slot];
-    size[i] = b[(size_t)i * B + slot];
+    const uint32_t x = b[(size_t)i * B + slot];
+    size[i] = (x & 0x80000000u) ? 0u : x;  // covered in the last selection: 0
   }
 }

@@ -96,13 +96,13 @@ __device__ Best block_best(Best b, Best *sh) {
 }
 
 struct DSel {
-  // compact store of this rank
+  // compact store of this rank (store_cs.cu): E = {P, next} words, vid
   const uint2 *rec;
   uint32_t MW;
-  uint32_t *P;
-  const uint32_t *moff, *memb, *cid;
-  uint32_t B, nv, big_t;
-  const uint32_t *hot_root, *hot_size;
+  uint32_t *E;
+  const uint32_t *vid, *cid;
+  uint32_t B, nv, list_t;
+  const uint32_t *hot_root;
   // replicated gains + argmax cache
   long long *gain;
   Best *cmax;
@@ -148,44 +148,39 @@ __global__ void __launch_bounds__(DT) k_dist_cover(DSel S, uint32_t step) {
     S.seeds[step] = s;
   }
   const int lane = threadIdx.x & 31;
-  const size_t gwarp = tid >> 5, nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
   const uint32_t srow = S.cid ? S.cid[s] : s;
   unsigned long long dsum = 0;
-  for (size_t j = gwarp; j < S.B; j += nwarps) {
+  for (size_t j = tid; j < S.B; j += ((size_t)gridDim.x * blockDim.x)) {
     uint32_t d = 1, mr = NONE;
-    if (lane == 0) {
-      S.cov_root[j] = NONE;
-      if (srow != NONE && ((S.rec[(size_t)srow * S.MW + (j >> 5)].y >> (j & 31)) & 1u)) {
-        const uint32_t e = pc_cs_pos(S.rec, S.MW, srow, (uint32_t)j);
-        const uint32_t x0 = __ldcg(S.P + e);
-        const uint32_t root = (x0 & PACIM_HIGH) ? e : x0;
-        const uint32_t x = atomicOr(S.P + root, COV);
-        if (x & COV) {
-          d = 0;
-        } else {
-          d = x & SIZE;
-          const unsigned long long at = atomicAdd(S.cov_cnt, 1ull);
-          if (at < S.cov_cap) S.cov_list[at] = root;
-          if (d > S.big_t)
-            S.cov_root[j] = root;
-          else
-            mr = root;
-        }
+    S.cov_root[j] = NONE;
+    if (srow != NONE && ((S.rec[(size_t)srow * S.MW + (j >> 5)].y >> (j & 31)) & 1u)) {
+      const uint32_t e = pc_cs_pos(S.rec, S.MW, srow, (uint32_t)j);
+      const uint32_t x0 = __ldcg(S.E + 2 * (size_t)e);
+      const uint32_t root = (x0 & PACIM_HIGH) ? e : x0;
+      const uint32_t x = atomicOr(S.E + 2 * (size_t)root, COV);
+      if (x & COV) {
+        d = 0;
+      } else {
+        d = x & SIZE;
+        const unsigned long long at = atomicAdd(S.cov_cnt, 1ull);
+        if (at < S.cov_cap) S.cov_list[at] = root;
+        if (d > S.list_t || root == S.hot_root[j])
+          S.cov_root[j] = root;  // no member list
+        else
+          mr = root;
       }
     }
-    d = __shfl_sync(FULL, d, 0);
-    mr = __shfl_sync(FULL, mr, 0);
     dsum += d;
-    if (mr != NONE && d > 1) {
-      const uint32_t end = __ldg(S.moff + mr);
-      for (uint32_t t = end - d + lane; t < end; t += 32) {
-        const uint32_t v = __ldg(S.memb + t);
-        if (v == s) continue;
-        const unsigned long long at = atomicAdd(S.send + H_CNT, 1ull);
-        if (at < S.cap) S.send[H_WORDS + at] = ((unsigned long long)v << 32) | d;
-      }
+    uint32_t e = mr;
+    for (uint32_t t = 0; mr != NONE && t < d && e != NONE;
+         t++, e = __ldcg(S.E + 2 * (size_t)e + 1)) {  // the members
+      const uint32_t v = __ldg(S.vid + e);
+      if (v == s) continue;
+      const unsigned long long at = atomicAdd(S.send + H_CNT, 1ull);
+      if (at < S.cap) S.send[H_WORDS + at] = ((unsigned long long)v << 32) | d;
     }
   }
+  for (int q = 16; q; q >>= 1) dsum += __shfl_xor_sync(FULL, dsum, q);
   if (lane == 0 && dsum) atomicAdd(S.send + H_DSUM, dsum);
 }
 
@@ -202,9 +197,8 @@ __global__ void k_dist_head(DSel S) {
   __syncthreads();
   for (uint32_t j = threadIdx.x; j < S.B; j += blockDim.x) {
     const uint32_t cr = S.cov_root[j];
-    const bool big = S.hot_size[j] > S.big_t;
     if (cr != NONE) dense = 1;
-    if (big != (cr != NONE) || (big && cr != S.hot_root[j])) exact = 0;
+    if (cr != S.hot_root[j]) exact = 0;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -292,10 +286,10 @@ __global__ void __launch_bounds__(DT) k_dist_chunks(DSel S, bool all) {
   if (blockIdx.x == 0 && threadIdx.x < H_WORDS) S.send[threadIdx.x] = 0;
 }
 
-__global__ void k_dist_uncover(uint32_t *P, const unsigned long long *list, unsigned long long cnt) {
+__global__ void k_dist_uncover(uint32_t *E, const unsigned long long *list, unsigned long long cnt) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
        i += (size_t)gridDim.x * blockDim.x)
-    atomicAnd(P + list[i], ~COV);
+    atomicAnd(E + 2 * list[i], ~COV);
 }
 
 __global__ void k_dist_set(long long *gain, uint32_t s, long long x) { gain[s] = x; }
@@ -347,16 +341,18 @@ void pc_free_comm(pacim_ctx *ctx) {
 void pc_dist_restore(pacim_ctx *ctx) {
   if (ctx->cs && ctx->dist_cov_valid && ctx->dist_cov_n) {
     k_dist_uncover<<<pc_grid(ctx, ctx->dist_cov_n, 256), 256, 0, ctx->stream>>>(
-        ctx->cs_P.as<uint32_t>(), ctx->dist_cov_old.as<unsigned long long>(), ctx->dist_cov_n);
+        ctx->cs_E.as<uint32_t>(), ctx->dist_cov_old.as<unsigned long long>(), ctx->dist_cov_n);
     PC_CHECK_LAUNCH();
   }
   ctx->dist_cov_valid = false;
   ctx->dist_cov_n = 0;
 }
 
+// the sharded paths run when the build's shard matches the communicator; at
+// world 1 only on request (PACIM_FORCE_DIST=1: the one-GPU test of the same code)
 bool pc_dist_active(const pacim_ctx *ctx) {
-  return ctx->comm && ctx->world > 1 && ctx->comm_world == (int)ctx->world &&
-         ctx->comm_rank == (int)ctx->rank;
+  return ctx->comm && ctx->comm_world == (int)ctx->world && ctx->comm_rank == (int)ctx->rank &&
+         (ctx->world > 1 || getenv("PACIM_FORCE_DIST") != nullptr);
 }
 
 // End of a sharded build: gain0 all-reduced (H7 summed over the ranks'
@@ -458,15 +454,13 @@ static bool dist_select_fast(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_
   DSel S;
   S.rec = ctx->cs_rec.as<uint2>();
   S.MW = ctx->cs_MW;
-  S.P = ctx->cs_P.as<uint32_t>();
-  S.moff = ctx->cs_moff.as<uint32_t>();
-  S.memb = ctx->cs_memb.as<uint32_t>();
+  S.E = ctx->cs_E.as<uint32_t>();
+  S.vid = ctx->cs_vid.as<uint32_t>();
   S.cid = ctx->lean ? nullptr : ctx->cid.as<uint32_t>();
   S.B = B;
   S.nv = n;
-  S.big_t = ctx->cs_big_t;
+  S.list_t = ctx->cs_list_t;
   S.hot_root = ctx->d_hot.as<uint32_t>();
-  S.hot_size = ctx->d_hot_size.as<uint32_t>();
   S.ghot = ctx->dist_hot ? ctx->dist_ghot.as<int64_t>() : nullptr;
   uint32_t csh = 10;
   while (((uint64_t)n + (1ull << csh) - 1) >> csh > MAX_CHUNKS) csh++;

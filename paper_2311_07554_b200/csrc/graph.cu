@@ -334,6 +334,7 @@ static void derive_rows(pacim_ctx *ctx) {
     PC_CUDA(cudaMemcpyAsync(&h, t, 8, cudaMemcpyDeviceToHost, ctx->stream));
     PC_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx->hub = (uint32_t)(0xFFFFFFFFull - (h & 0xFFFFFFFFull));
+    ctx->hub_degree = h >> 32;
     if (ctx->hub >= n) ctx->hub = 0;
   }
   {
@@ -451,6 +452,7 @@ static void derive_lean(pacim_ctx *ctx) {
     PC_CUDA(cudaMemcpyAsync(&h, t, 8, cudaMemcpyDeviceToHost, ctx->stream));
     PC_CUDA(cudaStreamSynchronize(ctx->stream));
     ctx->hub = (uint32_t)(0xFFFFFFFFull - (h & 0xFFFFFFFFull));
+    ctx->hub_degree = h >> 32;
     if (ctx->hub >= n) ctx->hub = 0;
   }
   ctx->nr = n;

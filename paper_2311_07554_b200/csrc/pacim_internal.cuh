@@ -139,6 +139,7 @@ struct pacim_ctx {
   std::string err;
   int sm_count = 148;
   uint64_t device_bytes = 0;
+  uint64_t device_peak = 0;  // high-water mark since the last build started
 
   // ---- multi-GPU (dist.cu): NCCL communicator of pacim_init_comm
   void *comm = nullptr;     // ncclComm_t
@@ -152,6 +153,7 @@ struct pacim_ctx {
 
   // ---- graph (H0/H1)
   bool has_graph = false;
+  uint64_t graph_gen = 0;  // incremented by every graph load (derived-table caches)
   uint32_t n = 0;
   uint64_t m = 0;        // undirected edges
   int pmodel = 0;        // PACIM_P_CONST / PACIM_P_WIC / PACIM_P_UNIFORM
@@ -174,6 +176,7 @@ struct pacim_ctx {
   DevBuf crow;           // u32 row of the first CSR entry of each 32-entry chunk (lane-per-entry
                          // kernels; lean graphs: k_edges)
   uint32_t hub_row = 0xFFFFFFFFu;  // store row of the hub vertex
+  uint64_t hub_degree = 0;         // its degree
 
   // hub rows (degree > hub_deg): index per row and the live hub adjacency of
   // the last build (HLA: per (hub, slot) the rows joined to the hub by a live
@@ -231,16 +234,19 @@ struct pacim_ctx {
   bool cs = false;          // the current store is the compact one
   uint32_t cs_MW = 0;       // mask words per row (ceil(B / 32))
   uint64_t cs_total = 0;    // entries = non-singleton (vertex, sketch) pairs
-  uint64_t cs_nmemb = 0;    // member-index entries (CCs of <= cs_big_t vertices)
-  uint32_t cs_big_t = 0;    // CCs above it: no member list (dense pass / hot sums)
+  uint32_t cs_list_t = 0;   // CCs above it (or the hub's) are covered by the dense pass
   DevBuf cs_rec;            // uint2[nr][MW]: {entry prefix, live-slot mask word}
   DevBuf cs_soff;           // u32[nr + 1]: first entry of a row
-  DevBuf cs_sl;             // u8[total]: slot of an entry
   DevBuf cs_ecrow;          // u32[total / 32 + 1]: row of entry 32 c
-  DevBuf cs_P;              // u32[total]: union-find parents -> HIGH | size / root entry
-  DevBuf cs_moff;           // u32[total + 1]: member-index end of a root entry
-  DevBuf cs_memb;           // u32[nmemb]: members (vertex ids) grouped by root entry
+  DevBuf cs_E;              // uint2[total]: {parent -> HIGH | size / root entry, next member}
+  DevBuf cs_vid;            // u32[total]: vertex of an entry
   DevBuf cs_diag;           // u64 selection diagnostics
+  DevBuf cs_cnt;            // build scratch: row counts and their scan
+  DevBuf cs_roff, cs_rcrow; // store-row CSR offsets, row of CSR entry 32 c (mask pass)
+  uint64_t cs_rows_gen = ~0ull;  // graph_gen cs_roff / cs_rcrow were built for
+  uint64_t cs_pref_gen = ~0ull;  // store decision of the last build of graph_gen ...
+  uint32_t cs_pref_B = 0;        // ... with this many slots:
+  bool cs_pref_dense = false;    // too dense for the compact store
 
   // compressed store (H6c)
   uint32_t rho = 0;
@@ -336,6 +342,8 @@ void pc_cs_get_labels(pacim_ctx *ctx, uint32_t slot, uint32_t *host_out);
 void pc_cs_lazy_eval(pacim_ctx *ctx, const uint32_t *cand, uint32_t b0, uint32_t b1,
                      long long *delta);
 void pc_cs_lazy_mark(pacim_ctx *ctx, uint32_t s);
+void pc_cs_select_wintree(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
+                          int64_t *sigma_num);
 void pc_slot_table(pacim_ctx *ctx);
 // Live hub adjacency (HLA) being recorded: raw (key << 32 | other row) with
 // key = hub index * B + slot, appended in any order (grouped by key after the

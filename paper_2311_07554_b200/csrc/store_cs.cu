@@ -1,41 +1,44 @@
 // store_cs.cu — the COMPACT uncompressed store (H3-H7, H6u with its member
-// index) and the greedy loop over it (H8-H12).  DESIGN.md §5 / §6.
+// lists) and the greedy loop over it (H8-H12).  DESIGN.md §5 / §6.
 //
 // Why: in the paper's workloads a vertex is a singleton in most sketches (c4:
 // 9.8 % of the (row, sketch) pairs are in a CC of >= 2 vertices, c2: 23 %).
 // The dense vertex-major store (build.cu) writes, compresses and re-reads
 // every pair; the compact store keeps an entry only for the pairs (v, r) where
 // v has a live edge in sketch r (exactly the non-singleton pairs), laid out
-// row-major, so every streaming pass moves ~1/10 of the bytes at c4.
+// row-major, so every streaming pass moves ~1/10 of the bytes at c4, and the
+// members of every CC are linked so that covering a CC (MarkSeed + the
+// member updates) costs O(|C|) with no traversal of the sampled graph.
 //
 // Layout (per build, B local sketch slots <= 256, MW = ceil(B/32) words):
-//   rec[row][w]  = {first entry of the row + set bits of words < w, live-slot
-//                   mask word w}: entry of (row, j) = pc_cs_pos (one 8-B read)
-//   soff[row]    first entry of a row; sl[e] slot of entry e; ecrow[c] row of
-//                entry 32c (lane-per-entry kernels find their row from it)
-//   P[e]         union-find parent (an entry index: entries of one slot are in
-//                vertex order, so the minimum entry of a CC is its minimum
-//                vertex, R8), after compression: HIGH | |C| at the root entry,
+//   rec[row][w]  {first entry of the row + set bits of the row's words < w,
+//                 live-slot mask word w}: entry of (row, j) = pc_cs_pos (8 B)
+//   soff[row]    first entry of a row; ecrow[c] row of entry 32 c
+//   E[e] = {P, next}
+//     P          union-find parent (an entry index: the entries of one slot are
+//                in vertex order, so the minimum entry of a CC is its minimum
+//                vertex, R8); after compression HIGH | |C| at the root entry,
 //                the root entry elsewhere; bit 30 = covered during a selection
-//   moff, memb   member index: the vertices of every CC of <= big_t vertices,
-//                grouped by root entry (moff[root] = end of its group)
+//     next       the CC's member list: root -> ... -> NONE (members inserted
+//                right after the root by the compression pass)
+//   vid[e]       the entry's vertex
+// The hub's CCs (hot) and CCs above list_t have no list: covering them is one
+// vector pass over the build's per-vertex hot sums (when a step covers
+// exactly the hub's CCs) or one pass over the entries.
 //
-// Build: k_cs_mask (lane per CSR entry: live slots of the entry's edge, OR-ed
-// into the row's mask) -> counts, scan -> k_cs_rec (prefixes, slot ids, chunk
-// rows) -> P = HIGH|1 -> k_edges<CS> (build.cu: the unions, on entries) ->
-// k_cs_compress (full compression, CC sizes) -> member offsets (scan) ->
-// k_cs_gain (gain0 = sum_r |C_r(v)|, hot sums, member scatter).
-//
-// Selection (one persistent cooperative kernel, k steps): argmax over cached
-// chunk maxima (Win-Tree layout), MarkSeed per slot,
-// the members of each newly covered CC lose its size (from the member index,
-// O(members) per step); CCs above big_t by the build's hot sums or one pass
-// over the entries.
+// Build: k_cs_mask (lane per CSR entry: the live slots of its edge, OR-ed into
+// the row's mask) -> counts, scan -> k_cs_rec -> E = {HIGH|1, NONE} ->
+// k_edges<CS> (build.cu: the unions, on entries) -> k_cs_compress (full
+// compression, CC sizes, member lists) -> k_cs_gain (gain0 = sum_r |C_r(v)|,
+// hot sums, vid).
 #include <cooperative_groups.h>
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <cstring>
+#include <vector>
 
 #include "pacim_internal.cuh"
 
@@ -52,12 +55,29 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int CS_THREADS = 256;
 constexpr int SEL_THREADS = 512;
 constexpr uint32_t MAX_CHUNKS = 4096;
+constexpr uint32_t LIST_T = 4096;     // longest member list walked in a cover step
 
 // ---------------------------------------------------------------- helpers
-__device__ __forceinline__ uint32_t csr_row(const uint64_t *off, const uint32_t *crow, uint64_t e) {
-  uint32_t u = crow[e >> 5];
-  while (e >= off[u + 1]) u++;
-  return u;
+// Row of entry e (in [base, base + 32)) for a warp over 32 consecutive
+// entries of a CSR whose rows are given by offsets roff (u64) and the chunk
+// table crow (row of entry 32 c): lane L holds the end of row r0 + L, a
+// 5-step shuffle search finds each lane's row; rows beyond r0 + 31 (a run of
+// empty rows) by a scan.  All 32 lanes call it.
+__device__ __forceinline__ uint32_t warp_row(const uint64_t *roff, uint32_t nrows,
+                                             const uint32_t *crow, uint64_t base, uint64_t e) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t r0 = crow[base >> 5];
+  const uint64_t endL = (r0 + lane < nrows) ? roff[r0 + lane + 1] : ~0ull;
+  uint32_t cnt = 0;  // rows r0 + L with end <= e
+#pragma unroll
+  for (int st = 16; st; st >>= 1) {
+    const uint64_t o = __shfl_sync(FULL, endL, cnt + st - 1);
+    if (o <= e) cnt += st;
+  }
+  if (cnt == 31 && __shfl_sync(FULL, endL, 31) <= e) cnt = 32;
+  uint32_t r = r0 + cnt;
+  while (r < nrows && roff[r + 1] <= e) r++;  // more than 31 empty rows before e
+  return r;
 }
 
 __device__ __forceinline__ uint32_t entry_row(const uint32_t *soff, const uint32_t *ecrow,
@@ -92,20 +112,21 @@ __device__ __forceinline__ void cand_range(uint32_t he, uint64_t T, const uint16
   }
 }
 
-__device__ __forceinline__ uint32_t find_halve(uint32_t *P, uint32_t x) {
+// union-find on the P words of E (stride 2)
+__device__ __forceinline__ uint32_t find_halve(uint32_t *E, uint32_t x) {
   for (;;) {
-    const uint32_t p = __ldcg(P + x);
+    const uint32_t p = __ldcg(E + 2 * (size_t)x);
     if (p & PACIM_HIGH) return x;
-    const uint32_t gp = __ldcg(P + p);
+    const uint32_t gp = __ldcg(E + 2 * (size_t)p);
     if (gp & PACIM_HIGH) return p;
-    atomicMin(P + x, gp);
+    atomicMin(E + 2 * (size_t)x, gp);
     x = gp;
   }
 }
 
-__device__ __forceinline__ uint32_t find_ro(const uint32_t *P, uint32_t x) {
+__device__ __forceinline__ uint32_t find_ro(const uint32_t *E, uint32_t x) {
   for (;;) {
-    const uint32_t p = __ldcg(P + x);
+    const uint32_t p = __ldcg(E + 2 * (size_t)x);
     if (p & PACIM_HIGH) return x;
     x = p;
   }
@@ -123,62 +144,162 @@ __device__ __forceinline__ unsigned long long peer_sum(unsigned peers, uint32_t 
   return (unsigned long long)lo + ((unsigned long long)hi << 16);
 }
 
+// sorted copy of up to 256 root entries in shared memory (rank sort: each
+// thread counts the smaller keys); NONE entries sort last.  Returns the count.
+__device__ uint32_t load_sorted(const uint32_t *src, uint32_t B, uint32_t *dst) {
+  __shared__ uint32_t tmp[256];
+  __shared__ uint32_t nval;
+  if (threadIdx.x == 0) nval = 0;
+  for (uint32_t j = threadIdx.x; j < 256; j += blockDim.x) tmp[j] = j < B ? src[j] : NONE;
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < 256; j += blockDim.x) {
+    const uint32_t x = tmp[j];
+    uint32_t r = 0;
+    for (uint32_t i = 0; i < 256; i++) {
+      const uint32_t y = tmp[i];
+      r += (y < x) || (y == x && i < j);
+    }
+    dst[r] = x;
+    if (x != NONE) atomicAdd(&nval, 1u);
+  }
+  __syncthreads();
+  return nval;
+}
+
+// index of x in the sorted list (n entries), or -1
+__device__ __forceinline__ int find_sorted(const uint32_t *a, uint32_t n, uint32_t x) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo < n && a[lo] == x) ? (int)lo : -1;
+}
+
+// ------------------------------------------------------- row tables
+// store-row CSR offsets and the row of every 32nd CSR entry (mask pass)
+__global__ void k_cs_roff(const uint64_t *off, const uint32_t *rmap, uint32_t nr, uint64_t nnz,
+                          uint64_t *roff) {
+  for (size_t r = (size_t)blockIdx.x * blockDim.x + threadIdx.x; r <= nr;
+       r += (size_t)gridDim.x * blockDim.x)
+    roff[r] = r < nr ? off[rmap ? rmap[r] : r] : nnz;
+}
+
+__global__ void k_cs_rcrow(const uint64_t *roff, uint32_t nr, uint32_t *rcrow) {
+  for (size_t r = (size_t)blockIdx.x * blockDim.x + threadIdx.x; r < nr;
+       r += (size_t)gridDim.x * blockDim.x) {
+    const uint64_t a = roff[r], b = roff[r + 1];
+    for (uint64_t c = (a + 31) >> 5; (c << 5) < b; c++) rcrow[c] = (uint32_t)r;
+  }
+}
+
 // ------------------------------------------------------------ k_cs_mask
 // Lane per CSR entry (u, w) (balanced whatever the degrees): the live slots
 // of edge {u, w} (P:3-4 / R3; per-edge T32 for WIC / Uniform, R4 / R19; R20)
-// OR-ed into u's row mask.  Lanes of one row combine with one redux per word.
+// OR-ed into u's row mask.  As in k_edges, a warp flattens the candidate
+// (entry, slot) pairs of its 32 entries into rounds of 32 tests (no lane
+// waits on another's 256-slot range: WIC gives leaf-leaf edges T = 2^32);
+// a range whose candidates are all live (T = 2^32, or exactly the bucket
+// width) is set without tests.  Live bits gather in a per-warp shared
+// buffer, then the lanes of one row combine with one redux per word.
+constexpr int MASK_WARPS = CS_THREADS / 32;
 template <bool PERE, bool DECOR>
 __global__ void __launch_bounds__(CS_THREADS) k_cs_mask(
-    const uint64_t *__restrict__ off, const uint32_t *__restrict__ nbr,
-    const uint32_t *__restrict__ crow, uint64_t nnz, const uint32_t *__restrict__ cid,
+    const uint64_t *__restrict__ roff, const uint32_t *__restrict__ rcrow, uint32_t nr,
+    const uint32_t *__restrict__ rmap, const uint32_t *__restrict__ nbr, uint64_t nnz,
     const uint32_t *__restrict__ tcsr, uint32_t toff, uint64_t t32, uint64_t K,
     const uint32_t *__restrict__ g_shr, const uint16_t *__restrict__ g_tab,
     const uint64_t *__restrict__ hr64, uint32_t B, uint32_t MW, uint32_t *rec) {
   extern __shared__ uint32_t sm[];
   uint32_t *shr = sm;
   uint16_t *tab = reinterpret_cast<uint16_t *>(sm + B);
+  __shared__ uint32_t w_lo[MASK_WARPS][32], w_he[MASK_WARPS][32], w_own[MASK_WARPS][32];
+  __shared__ uint64_t w_T[PERE ? MASK_WARPS : 1][32], w_he64[DECOR ? MASK_WARPS : 1][32];
+  __shared__ uint32_t wb[MASK_WARPS][32][MAXW];  // live bits per entry of the warp
   for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) shr[i] = g_shr[i];
   for (uint32_t i = threadIdx.x; i <= (1u << PACIM_TB); i += blockDim.x) tab[i] = g_tab[i];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < (int)MAXW; q++) wb[wid][lane][q] = 0;
   __syncthreads();
-  const int lane = threadIdx.x & 31;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   for (size_t base = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(size_t)31; base < nnz;
        base += stride) {
     const uint64_t e = base + lane;
-    uint32_t row = NONE;
-    uint32_t bits[MAXW];
-#pragma unroll
-    for (int q = 0; q < (int)MAXW; q++) bits[q] = 0;
+    const uint32_t rw = warp_row(roff, nr, rcrow, base, e < nnz ? e : nnz - 1);
+    uint32_t row = NONE, cnt = 0, lo = 0, hi = 0, he = 0;
+    uint64_t T = t32, he64 = 0;
     if (e < nnz) {
-      const uint32_t u = csr_row(off, crow, e), w = nbr[e];
-      row = cid ? cid[u] : u;
-      const uint64_t T = PERE ? (uint64_t)tcsr[e] + toff : t32;
+      row = rw;
+      const uint32_t u = rmap ? rmap[row] : row, w = nbr[e];
+      if (PERE) T = (uint64_t)tcsr[e] + toff;
       const uint64_t a = u < w ? u : w, b = u < w ? w : u;
-      const uint64_t he64 = pc_mix64(((a << 32) | b) ^ K);
-      const uint32_t he = (uint32_t)(he64 >> 32);
-      uint32_t lo, hi;
+      he64 = pc_mix64(((a << 32) | b) ^ K);
+      he = (uint32_t)(he64 >> 32);
       cand_range(he, T, tab, B, DECOR, lo, hi);
-#pragma unroll
-      for (int q = 0; q < (int)MAXW; q++) {
-        const uint32_t j0 = max(lo, 32u * q), j1 = min(hi, 32u * q + 32);
-        uint32_t x = 0;
-        for (uint32_t j = j0; j < j1; j++) {
-          const bool lv = DECOR ? (T >= (1ull << 32) || (pc_mix64(__ldg(hr64 + j) ^ he64) >> 32) < T)
-                                : (uint64_t)(shr[j] ^ he) < T;
-          x |= (uint32_t)lv << (j & 31);
+      // every candidate live: T = 2^32, or T is exactly the bucket width and
+      // the table resolves all its bits
+      const uint32_t wb_ = T ? __clz((uint32_t)(T - 1)) : 0;
+      const bool all = T >= (1ull << 32) ||
+                       (!DECOR && wb_ >= 1 && wb_ <= PACIM_TB && T == (1ull << (32 - wb_)));
+      if (all) {
+        for (uint32_t q = lo >> 5; q < MW && 32 * q < hi; q++) {
+          uint32_t m = 0xFFFFFFFFu;
+          if (32 * q < lo) m &= 0xFFFFFFFFu << (lo & 31);
+          if (32 * q + 32 > hi) m &= 0xFFFFFFFFu >> (32 - (hi & 31));
+          wb[wid][lane][q] |= m;
         }
-        bits[q] = x;
+      } else {
+        cnt = hi - lo;
       }
     }
+    // flattened candidate tests (the k_edges scheme)
+    const uint32_t nz = __ballot_sync(FULL, cnt > 0);
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, inc, d);
+      if (lane >= d) inc += y;
+    }
+    const uint32_t pre = inc - cnt;
+    const uint32_t total = __shfl_sync(FULL, inc, 31);
+    if (cnt) {
+      const uint32_t k = __popc(nz & ((1u << lane) - 1));
+      w_lo[wid][k] = lo - pre;
+      w_he[wid][k] = he;
+      w_own[wid][k] = lane;
+      if (PERE) w_T[PERE ? wid : 0][k] = T;
+      if (DECOR) w_he64[DECOR ? wid : 0][k] = he64;
+    }
+    __syncwarp();
+    for (uint32_t c0 = 0; c0 < total; c0 += 32) {
+      const uint32_t idx = c0 + lane;
+      const uint32_t smask =
+          __reduce_or_sync(FULL, (cnt && pre >= c0 && pre < c0 + 32) ? 1u << (pre - c0) : 0u);
+      const uint32_t before = __popc(__ballot_sync(FULL, cnt && pre < c0));
+      if (idx < total) {
+        const uint32_t a = before + __popc(smask & (0xffffffffu >> (31 - lane))) - 1;
+        const uint32_t j = w_lo[wid][a] + idx;
+        const uint64_t Ta = PERE ? w_T[PERE ? wid : 0][a] : t32;
+        const bool lv = DECOR ? (pc_mix64(__ldg(hr64 + j) ^ w_he64[DECOR ? wid : 0][a]) >> 32) < Ta
+                              : (uint64_t)(shr[j] ^ w_he[wid][a]) < Ta;
+        if (lv) atomicOr(&wb[wid][w_own[wid][a]][j >> 5], 1u << (j & 31));
+      }
+    }
+    __syncwarp();
     const unsigned peers = __match_any_sync(FULL, row);
     const int leader = __ffs(peers) - 1;
 #pragma unroll
     for (int q = 0; q < (int)MAXW; q++) {
       if ((uint32_t)q >= MW) break;
-      if (!__any_sync(FULL, bits[q])) continue;
-      const uint32_t x = __reduce_or_sync(peers, bits[q]);
+      const uint32_t mine = wb[wid][lane][q];
+      wb[wid][lane][q] = 0;
+      if (!__any_sync(FULL, mine)) continue;
+      const uint32_t x = __reduce_or_sync(peers, mine);
       if (lane == leader && x && row != NONE) atomicOr(rec + ((size_t)row * MW + q) * 2 + 1, x);
     }
+    __syncwarp();
   }
 }
 
@@ -193,10 +314,10 @@ __global__ void k_cs_count(const uint2 *rec, uint32_t nr, uint32_t MW, uint64_t 
   }
 }
 
-// thread per row: word prefixes, soff, slot ids of the row's entries, and
-// the chunk table (row of entry 32 c for every chunk starting in the row)
+// thread per row: word prefixes (rec[.].x), soff, and the chunk table (row of
+// entry 32 c for every chunk starting in the row)
 __global__ void k_cs_rec(uint2 *rec, uint32_t nr, uint32_t MW, const uint64_t *pos,
-                         uint32_t *soff, uint8_t *sl, uint32_t *ecrow) {
+                         uint32_t *soff, uint32_t *ecrow) {
   for (size_t r = (size_t)blockIdx.x * blockDim.x + threadIdx.x; r < nr;
        r += (size_t)gridDim.x * blockDim.x) {
     const uint32_t base = (uint32_t)pos[r];
@@ -204,8 +325,8 @@ __global__ void k_cs_rec(uint2 *rec, uint32_t nr, uint32_t MW, const uint64_t *p
     for (uint32_t q = 0; q < MW; q++) {
       uint2 x = rec[r * MW + q];
       x.x = at;
+      at += __popc(x.y);
       rec[r * MW + q] = x;
-      for (uint32_t t = x.y; t; t &= t - 1) sl[at++] = (uint8_t)(q * 32 + __ffs(t) - 1);
     }
     soff[r] = base;
     if (r + 1 == nr) soff[nr] = at;
@@ -213,77 +334,69 @@ __global__ void k_cs_rec(uint2 *rec, uint32_t nr, uint32_t MW, const uint64_t *p
   }
 }
 
-__global__ void k_cs_fill(uint32_t *a, uint64_t N, uint32_t x) {
+__global__ void k_cs_fill(uint2 *E, uint64_t N) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
        i += (size_t)gridDim.x * blockDim.x)
-    a[i] = x;
+    E[i] = make_uint2(ROOT1, NONE);
 }
 
-// the hub row's root entry per slot (the hot, typically giant, CCs), NONE if
-// the hub is a singleton there
-__global__ void k_cs_hot(const uint2 *rec, uint32_t MW, const uint32_t *P, uint32_t hub_row,
+// the hub row's root entry per slot (the hot CCs), NONE if the hub is a
+// singleton there
+__global__ void k_cs_hot(const uint2 *rec, uint32_t MW, const uint32_t *E, uint32_t hub_row,
                          uint32_t nr, uint32_t B, uint32_t *hot) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < B; j += gridDim.x * blockDim.x) {
     uint32_t h = NONE;
     if (hub_row < nr && ((rec[(size_t)hub_row * MW + (j >> 5)].y >> (j & 31)) & 1u))
-      h = find_ro(P, pc_cs_pos(rec, MW, hub_row, j));
+      h = find_ro(E, pc_cs_pos(rec, MW, hub_row, j));
     hot[j] = h;
   }
 }
 
-// full compression (H4) and CC sizes into the root entries (H5): lane per
-// entry; members of a slot's hot CC counted per block in shared memory.
+// full compression (H4), CC sizes into the root entries (H5) and the member
+// lists (H6u): a non-root entry is linked in right after its root.  Members
+// of the hub's CCs (hot roots; c2: ~500K per sketch) get no list and count in
+// shared memory, one global increment per hot root per block at the end.
 // ctr[1] += non-root entries.
-__global__ void __launch_bounds__(CS_THREADS) k_cs_compress(uint32_t *P, uint64_t total,
-                                                            const uint8_t *sl, uint32_t B,
-                                                            const uint32_t *hot,
+__global__ void __launch_bounds__(CS_THREADS) k_cs_compress(uint32_t *E, uint64_t total,
+                                                            const uint32_t *hot, uint32_t B,
                                                             unsigned long long *ctr) {
-  __shared__ uint32_t hroot[256], hcnt[256];
-  for (uint32_t j = threadIdx.x; j < 256; j += blockDim.x) {
-    hroot[j] = j < B ? hot[j] : NONE;
-    hcnt[j] = 0;
-  }
+  __shared__ uint32_t hs[256], hcnt[256];
+  const uint32_t nh = load_sorted(hot, B, hs);
+  for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) hcnt[i] = 0;
   __syncthreads();
   unsigned long long nnr = 0;
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
        e += (size_t)gridDim.x * blockDim.x) {
-    const uint32_t s = __ldcg(P + e);
+    const uint32_t s = __ldcg(E + 2 * e);
     if (s & PACIM_HIGH) continue;
     nnr++;
-    const uint32_t j = sl[e];
+    int h = nh ? find_sorted(hs, nh, s) : -1;
     uint32_t root = s;
-    if (s != hroot[j]) {
-      root = find_halve(P, s);
-      if (root != s) atomicMin(P + e, root);
+    if (h < 0) {
+      root = find_halve(E, s);
+      if (root != s) {
+        atomicMin(E + 2 * e, root);
+        if (nh) h = find_sorted(hs, nh, root);
+      }
     }
-    if (root == hroot[j])
-      atomicAdd(hcnt + j, 1u);
-    else
-      atomicAdd(P + root, 1u);
+    if (h >= 0) {
+      atomicAdd(hcnt + h, 1u);
+    } else {
+      atomicAdd(E + 2 * (size_t)root, 1u);                               // |C|
+      E[2 * e + 1] = atomicExch(E + 2 * (size_t)root + 1, (uint32_t)e);  // link after the root
+    }
   }
   __syncthreads();
-  for (uint32_t j = threadIdx.x; j < B; j += blockDim.x)
-    if (hcnt[j]) atomicAdd(P + hroot[j], hcnt[j]);
+  for (uint32_t i = threadIdx.x; i < nh; i += blockDim.x)
+    if (hcnt[i]) atomicAdd(E + 2 * (size_t)hs[i], hcnt[i]);
   add_count(ctr + 1, nnr);
 }
 
-__global__ void k_cs_hot_sizes(const uint32_t *P, const uint32_t *hot, uint32_t B,
+__global__ void k_cs_hot_sizes(const uint32_t *E, const uint32_t *hot, uint32_t B,
                                uint32_t *hot_size) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < B; j += gridDim.x * blockDim.x)
-    hot_size[j] = hot[j] != NONE ? (P[hot[j]] & PACIM_LOW) : 0u;
+    hot_size[j] = hot[j] != NONE ? (E[2 * (size_t)hot[j]] & PACIM_LOW) : 0u;
 }
-
-// member-index sizes: |C| at a root entry of a CC of <= big_t vertices, else 0
-struct MembSize {
-  const uint32_t *P;
-  uint64_t total;
-  uint32_t big_t;
-  __host__ __device__ __forceinline__ uint32_t operator()(uint64_t e) const {
-    if (e >= total) return 0;
-    const uint32_t s = P[e];
-    return ((s & PACIM_HIGH) && (s & PACIM_LOW) <= big_t) ? (s & PACIM_LOW) : 0u;
-  }
-};
 
 // gain0 before the entries: B - (entries of the row) singletons (size 1 each);
 // isolated vertices B
@@ -297,48 +410,38 @@ __global__ void k_cs_gain_init(const uint32_t *cid, const uint32_t *soff, uint32
   }
 }
 
-// lane per entry: gain0[v] += |C_j(v)| (H7), hotsum[v] += |hot C_j| when v is
-// in slot j's giant hot CC, and the member scatter (H6u).  ctr[0] += roots.
+// lane per entry: gain0[v] += |C_j(v)| (H7), hotsum[v] += |C| when the
+// entry's CC is one of the hub's (HOT), vid[e] = v.  ctr[0] += roots.
 template <bool HOT>
 __global__ void __launch_bounds__(CS_THREADS) k_cs_gain(
-    const uint32_t *__restrict__ P, uint64_t total, const uint8_t *__restrict__ sl,
-    const uint32_t *__restrict__ soff, const uint32_t *__restrict__ ecrow,
-    const uint32_t *__restrict__ rmap, uint32_t B, const uint32_t *hot, const uint32_t *hot_size,
-    uint32_t big_t, uint32_t *moff, uint32_t *memb, int64_t *gain0, int64_t *hotsum,
+    const uint32_t *__restrict__ E, uint64_t total, const uint32_t *__restrict__ soff,
+    const uint32_t *__restrict__ ecrow, const uint32_t *__restrict__ rmap, uint32_t B,
+    const uint32_t *hot, uint32_t *vid, int64_t *gain0, int64_t *hotsum,
     unsigned long long *ctr) {
-  __shared__ uint32_t hroot[256], hsz[256];
-  if (HOT) {
-    for (uint32_t j = threadIdx.x; j < 256; j += blockDim.x) {
-      const bool giant = j < B && hot_size[j] > big_t;
-      hroot[j] = giant ? hot[j] : NONE;
-      hsz[j] = giant ? hot_size[j] : 0u;
-    }
-    __syncthreads();
-  }
+  __shared__ uint32_t hs[256];
+  uint32_t nh = 0;
+  if (HOT) nh = load_sorted(hot, B, hs);
   const int lane = threadIdx.x & 31;
   unsigned long long nroot = 0;
   const size_t stride = (size_t)gridDim.x * blockDim.x;
   for (size_t base = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(size_t)31; base < total;
        base += stride) {
     const size_t e = base + lane;
-    uint32_t row = NONE, size = 0, hs = 0, v = 0;
+    uint32_t row = NONE, size = 0, hsz = 0, v = 0;
     if (e < total) {
+      const uint32_t s = E[2 * e];
       row = entry_row(soff, ecrow, e);
-      v = rmap ? rmap[row] : row;
-      const uint32_t s = P[e];
       const uint32_t root = (s & PACIM_HIGH) ? (uint32_t)e : s;
-      const uint32_t rv = (s & PACIM_HIGH) ? s : __ldg(P + s);
+      const uint32_t rv = (s & PACIM_HIGH) ? s : __ldg(E + 2 * (size_t)s);
+      v = rmap ? rmap[row] : row;
+      vid[e] = v;
       size = rv & PACIM_LOW;
       nroot += (s & PACIM_HIGH) != 0;
-      if (HOT) {
-        const uint32_t j = sl[e];
-        if (root == hroot[j]) hs = hsz[j];
-      }
-      if (size <= big_t) memb[atomicAdd(moff + root, 1u)] = v;
+      if (HOT && find_sorted(hs, nh, root) >= 0) hsz = size;
     }
     const unsigned peers = __match_any_sync(FULL, row);
     const unsigned long long g = peer_sum(peers, size);
-    const unsigned long long h = HOT ? peer_sum(peers, hs) : 0ull;
+    const unsigned long long h = HOT ? peer_sum(peers, hsz) : 0ull;
     if (lane == __ffs(peers) - 1 && row != NONE) {
       atomicAdd(reinterpret_cast<unsigned long long *>(gain0 + v), g);
       if (HOT && h) atomicAdd(reinterpret_cast<unsigned long long *>(hotsum + v), h);
@@ -385,31 +488,30 @@ __device__ Best block_best(Best b, Best *sh) {
 }
 
 // diagnostics (u64): steps, dense steps, hot-sum steps, member updates
-enum { CD_STEPS = 0, CD_DENSE, CD_HOT, CD_UPD, CD_WORDS = 8 };
+enum { CD_STEPS = 0, CD_DENSE, CD_HOT, CD_UPD, CD_CELF, CD_WORDS = 8 };
 
 struct CSel {
   const uint2 *rec;
   uint32_t MW;
-  uint32_t *P;
-  const uint32_t *moff, *memb;
-  const uint8_t *sl;
-  const uint32_t *soff, *ecrow, *rmap, *cid;
+  uint32_t *E;             // {P, next} words
+  const uint32_t *vid, *soff, *rmap, *cid;
   uint32_t nr, B, nv;
   uint64_t total;
-  uint32_t big_t;
+  uint32_t list_t;
   long long *target;       // gains (single rank) or the delta vector (multi-rank)
-  uint32_t *cov_root, *cov_delta;  // [B] big CCs covered this step
+  uint32_t *cov_root, *cov_delta;  // [B] list-less CCs covered this step
   int *dense;              // [2] by step parity
   unsigned long long *cov_list, *cov_cnt;
   unsigned long long cov_cap;
   const int64_t *hotsum;
-  const uint32_t *hot_root, *hot_size;
+  const uint32_t *hot_root;  // [B] the hub's root entry per slot (NONE: singleton)
   Best *cmax;
   uint32_t *cdirty, *dlist, *dcnt;
   uint32_t csh, nchunks, par;
   int track;
   DeltaList dlst;
   unsigned long long *diag;
+  long long *celf;         // CELF's stale scores (PACIM_CELF_COUNT) or null
 };
 
 struct CSelOut {
@@ -434,8 +536,8 @@ __device__ __forceinline__ void sub_gain(const CSel &S, uint32_t u, long long d)
   }
 }
 
-// MarkSeed in slot j for the seed row srow (one thread):
-// returns delta_j; *mroot / *msize: a newly covered CC with a member list
+// MarkSeed in slot j for the seed row srow (one thread): returns
+// delta_j; *mroot: a newly covered CC whose member list is walked now
 __device__ __forceinline__ uint32_t cs_cover(const CSel &S, uint32_t srow, uint32_t j,
                                              uint32_t *mroot) {
   *mroot = NONE;
@@ -443,14 +545,14 @@ __device__ __forceinline__ uint32_t cs_cover(const CSel &S, uint32_t srow, uint3
   if (srow == NONE || !((S.rec[(size_t)srow * S.MW + (j >> 5)].y >> (j & 31)) & 1u))
     return 1;  // {s}: a singleton, uncovered while s is not a seed
   const uint32_t e = pc_cs_pos(S.rec, S.MW, srow, j);
-  const uint32_t x0 = __ldcg(S.P + e);
+  const uint32_t x0 = __ldcg(S.E + 2 * (size_t)e);
   const uint32_t root = (x0 & PACIM_HIGH) ? e : x0;
-  const uint32_t x = atomicOr(S.P + root, COV);
+  const uint32_t x = atomicOr(S.E + 2 * (size_t)root, COV);
   if (x & COV) return 0;  // covered by an earlier seed
   const uint32_t delta = x & SIZE;
   const unsigned long long at = atomicAdd(S.cov_cnt, 1ull);
   if (at < S.cov_cap) S.cov_list[at] = root;
-  if (delta > S.big_t) {
+  if (delta > S.list_t || root == S.hot_root[j]) {  // no member list: the dense pass
     S.cov_root[j] = root;
     S.cov_delta[j] = delta;
     S.dense[S.par] = 1;
@@ -481,15 +583,13 @@ __device__ void refresh_chunks(const CSel &S, uint32_t par, bool all, Best *sh) 
   }
 }
 
-// the covered big CCs of this step: exactly the hub's giant CCs -> hot sums
-// (one vector pass); block-collective, uniform result
+// the list-less CCs covered this step are exactly the hub's CCs (all of
+// them, now) -> the build's hot sums are the member updates (one vector
+// pass); block-collective, uniform result
 __device__ bool dense_hot(const CSel &S, uint32_t s, size_t tid, size_t nth) {
   int ok = S.hotsum != nullptr;
-  for (uint32_t j = threadIdx.x; j < S.B && ok; j += blockDim.x) {
-    const uint32_t cr = __ldcg(S.cov_root + j);
-    const bool big = S.hot_size[j] > S.big_t;
-    if (big != (cr != NONE) || (big && cr != S.hot_root[j])) ok = 0;
-  }
+  for (uint32_t j = threadIdx.x; j < S.B && ok; j += blockDim.x)
+    if (__ldcg(S.cov_root + j) != S.hot_root[j]) ok = 0;
   if (!__syncthreads_and(ok)) return false;
   for (size_t v = tid; v < S.nv; v += nth) {
     const long long h = S.hotsum[v];
@@ -498,30 +598,27 @@ __device__ bool dense_hot(const CSel &S, uint32_t s, size_t tid, size_t nth) {
   return true;
 }
 
-// dense pass: lane per entry; an entry of slot j whose root is slot j's
-// covered big CC loses cov_delta[j] at its vertex
+// dense pass: thread per entry; an entry whose root is one of this step's
+// covered list-less CCs (croot: sorted, nc of them, sizes in cdel) loses |C|
 __device__ void dense_pass(const CSel &S, uint32_t s, const uint32_t *croot, const uint32_t *cdel,
-                           size_t tid, size_t nth) {
+                           uint32_t nc, size_t tid, size_t nth) {
   for (size_t e = tid; e < S.total; e += nth) {
-    const uint32_t j = S.sl[e];
-    const uint32_t cr = croot[j];
-    if (cr == NONE) continue;
-    const uint32_t x = __ldcg(S.P + e);
+    const uint32_t x = __ldcg(S.E + 2 * e);
     const uint32_t root = (x & PACIM_HIGH) ? (uint32_t)e : x;
-    if (root != cr) continue;
-    const uint32_t row = entry_row(S.soff, S.ecrow, e);
-    const uint32_t v = S.rmap ? S.rmap[row] : row;
-    if (v != s) sub_gain(S, v, cdel[j]);
+    const int h = find_sorted(croot, nc, root);
+    if (h < 0) continue;
+    const uint32_t v = S.vid[e];
+    if (v != s) sub_gain(S, v, cdel[h]);
   }
 }
 
-// Step (parity par): A argmax -> B MarkSeed + member updates -> (dense) ->
+// Step (parity par): A argmax -> B MarkSeed + member-list walks -> (dense) ->
 // E refresh of the chunk maxima; grid barriers after B, the dense pass and E.
 __global__ void __launch_bounds__(SEL_THREADS, 1) k_cs_select(CSel S0, CSelOut O, uint32_t par0) {
   cg::grid_group grid = cg::this_grid();
   CSel S = S0;
   __shared__ Best sh[33];
-  __shared__ uint32_t croot[256], cdel[256];
+  __shared__ uint32_t croot[256], cdel[256], csort[256], dsort[256];
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t nth = (size_t)gridDim.x * blockDim.x;
   const size_t gwarp = tid >> 5, nwarps = nth >> 5;
@@ -553,6 +650,32 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) k_cs_select(CSel S0, CSelOut O
       s = O.given;
     }
     const uint32_t srow = S.cid ? S.cid[s] : s;
+    // ---- CELF's re-evaluations on the same gains (diagnostic):
+    //      from step 2 on, every non-seed whose stale score ranks at or above
+    //      the winner's fresh score (gain desc, id asc) is popped and
+    //      re-evaluated before the winner surfaces fresh
+    if (S.celf && O.given == NONE) {
+      if (step > 0) {
+        unsigned long long c = 0;
+        for (size_t v = tid; v < S.nv; v += nth) {
+          const long long kv = S.celf[v];
+          if (v == s) {
+            c++;
+            S.celf[v] = sg;
+            continue;
+          }
+          const long long gv = __ldcg(S.target + v);
+          if (gv < 0) continue;  // a seed
+          if (kv > sg || (kv == sg && v < s)) {
+            c++;
+            S.celf[v] = gv;
+          }
+        }
+        for (int q = 16; q; q >>= 1) c += __shfl_xor_sync(FULL, c, q);
+        if (lane == 0 && c) atomicAdd(S.diag + CD_CELF, c);
+      }
+      grid.sync();
+    }
     if (tid == 0) {
       O.seeds[step] = s;
       O.arg_gain[step] = sg;
@@ -561,41 +684,56 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) k_cs_select(CSel S0, CSelOut O
         mark_dirty(S, s >> S.csh);
       }
     }
-    // ---- B: MarkSeed per slot; members of the newly covered CCs lose |C|
+    // ---- B: MarkSeed per slot; the members of each newly covered CC lose |C|
+    //          (a lane per slot: the walks of a step's CCs run side by side)
     {
       unsigned long long dsum = 0, upd = 0;
-      for (size_t j = gwarp; j < S.B; j += nwarps) {
-        uint32_t d = 0, mr = NONE;
-        if (lane == 0) d = cs_cover(S, srow, (uint32_t)j, &mr);
-        d = __shfl_sync(FULL, d, 0);
-        mr = __shfl_sync(FULL, mr, 0);
+      for (size_t j = tid; j < S.B; j += nth) {
+        uint32_t mr = NONE;
+        const uint32_t d = cs_cover(S, srow, (uint32_t)j, &mr);
         dsum += d;
-        if (mr != NONE && d > 1) {
-          const uint32_t end = __ldg(S.moff + mr);
-          for (uint32_t t = end - d + lane; t < end; t += 32) {
-            const uint32_t v = __ldg(S.memb + t);
+        if (mr != NONE) {  // walk the list: the root, then its linked members
+          uint32_t e = mr;
+          for (uint32_t t = 0; t < d && e != NONE; t++, e = __ldcg(S.E + 2 * (size_t)e + 1)) {
+            const uint32_t v = __ldg(S.vid + e);
             if (v != s) sub_gain(S, v, d);
           }
           upd += d;
         }
+      }
+      for (int q = 16; q; q >>= 1) {
+        dsum += __shfl_xor_sync(FULL, dsum, q);
+        upd += __shfl_xor_sync(FULL, upd, q);
       }
       if (lane == 0) {
         if (dsum) atomicAdd(reinterpret_cast<unsigned long long *>(&O.gain_num[step]), dsum);
         if (upd) atomicAdd(S.diag + CD_UPD, upd);
       }
     }
+    (void)gwarp;
+    (void)nwarps;
     grid.sync();
-    // ---- dense: CCs above big_t covered this step
+    // ---- dense: list-less CCs covered this step
     if (__ldcg(S.dense + S.par)) {
       for (uint32_t j = threadIdx.x; j < 256; j += blockDim.x) {
         croot[j] = j < S.B ? __ldcg(S.cov_root + j) : NONE;
         cdel[j] = j < S.B ? __ldcg(S.cov_delta + j) : 0u;
       }
       __syncthreads();
+      uint32_t nc = 0;
+      for (uint32_t j = threadIdx.x; j < 256; j += blockDim.x) {
+        const uint32_t x = croot[j], d = cdel[j];
+        uint32_t r = 0;
+        for (uint32_t i = 0; i < 256; i++) r += (croot[i] < x) || (croot[i] == x && i < j);
+        csort[r] = x;
+        dsort[r] = d;
+      }
+      for (uint32_t j = 0; j < 256; j++) nc += croot[j] != NONE;  // uniform
+      __syncthreads();
       if (dense_hot(S, s, tid, nth)) {
         if (tid == 0) atomicAdd(S.diag + CD_HOT, 1ull);
       } else {
-        dense_pass(S, s, croot, cdel, tid, nth);
+        dense_pass(S, s, csort, dsort, nc, tid, nth);
       }
       if (tid == 0) atomicAdd(S.diag + CD_DENSE, 1ull);
       grid.sync();
@@ -611,10 +749,10 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) k_cs_select(CSel S0, CSelOut O
   }
 }
 
-__global__ void k_cs_uncover(uint32_t *P, const unsigned long long *list, unsigned long long cnt) {
+__global__ void k_cs_uncover(uint32_t *E, const unsigned long long *list, unsigned long long cnt) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
        i += (size_t)gridDim.x * blockDim.x)
-    atomicAnd(P + list[i], ~COV);
+    atomicAnd(E + 2 * list[i], ~COV);
 }
 
 // ---------------------------------------------------- lazy selector (f2)
@@ -639,8 +777,9 @@ __global__ void k_cs_lazy_eval(CSel S, const uint32_t *cand, uint32_t b0, uint32
           g += 1;
           continue;
         }
-        const uint32_t x = __ldcg(S.P + r.x + __popc(r.y & ((1u << (j & 31)) - 1u)));
-        const uint32_t rv = (x & PACIM_HIGH) ? x : __ldcg(S.P + x);
+        const uint32_t e = r.x + __popc(r.y & ((1u << (j & 31)) - 1u));
+        const uint32_t x = __ldcg(S.E + 2 * (size_t)e);
+        const uint32_t rv = (x & PACIM_HIGH) ? x : __ldcg(S.E + 2 * (size_t)x);
         if (!(rv & COV)) g += rv & SIZE;
       }
       for (int d = 16; d; d >>= 1) g += __shfl_xor_sync(FULL, g, d);
@@ -656,13 +795,177 @@ __global__ void k_cs_lazy_mark(CSel S, uint32_t s) {
     const uint2 r = S.rec[(size_t)srow * S.MW + (j >> 5)];
     if (!((r.y >> (j & 31)) & 1u)) continue;
     const uint32_t e = r.x + __popc(r.y & ((1u << (j & 31)) - 1u));
-    const uint32_t x = S.P[e];
+    const uint32_t x = S.E[2 * (size_t)e];
     const uint32_t root = (x & PACIM_HIGH) ? e : x;
-    if (!(atomicOr(S.P + root, COV) & COV)) {
+    if (!(atomicOr(S.E + 2 * (size_t)root, COV) & COV)) {
       const unsigned long long at = atomicAdd(S.cov_cnt, 1ull);
       if (at < S.cov_cap) S.cov_list[at] = root;
     }
   }
+}
+
+// ---------------------------------------------- Win-Tree selector (f2)
+// The paper's Win-Tree: an implicit winning tree T[1..2N-1]
+// over the stale scores key[v] (N = 2^ceil(log2 n) leaves, T[N + v] = v),
+// each internal node the id of its children's winner (key desc, id asc).
+// NextSeed = FindMax from the root with Delta* the best fresh score so far:
+// a node whose id is stale (not re-evaluated in this step) and cannot beat
+// Delta* prunes its whole subtree; a stale id that can is re-evaluated
+// (fresh marginal gain from the store, R17) and the search continues into
+// both children; a fresh id (re-evaluated at an ancestor) is passed through.
+// Level-synchronous in ONE block of 1024 threads (the frontier of the
+// paper's parallel recursion one level at a time); then MarkSeed and the
+// winners of the explored nodes recomputed bottom-up.  Evaluations counted.
+constexpr int WT_THREADS = 1024;
+
+__device__ __forceinline__ uint32_t wt_win(const long long *key, uint32_t a, uint32_t b) {
+  if (a == NONE) return b;
+  if (b == NONE) return a;
+  const long long ka = key[a], kb = key[b];
+  return (ka > kb || (ka == kb && a < b)) ? a : b;
+}
+
+// fresh marginal gain of v: sum over the slots of |C_j(v)| unless covered;
+// a singleton slot counts 1 (one warp)
+__device__ long long cs_eval(const CSel &S, uint32_t v) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t row = S.cid ? S.cid[v] : v;
+  long long g = 0;
+  if (row == NONE) return S.B;
+  for (uint32_t j = lane; j < S.B; j += 32) {
+    const uint2 r = S.rec[(size_t)row * S.MW + (j >> 5)];
+    if (!((r.y >> (j & 31)) & 1u)) {
+      g += 1;
+      continue;
+    }
+    const uint32_t e = r.x + __popc(r.y & ((1u << (j & 31)) - 1u));
+    const uint32_t x = __ldcg(S.E + 2 * (size_t)e);
+    const uint32_t rv = (x & PACIM_HIGH) ? x : __ldcg(S.E + 2 * (size_t)x);
+    if (!(rv & COV)) g += rv & SIZE;
+  }
+  for (int d = 16; d; d >>= 1) g += __shfl_xor_sync(FULL, g, d);
+  return g;
+}
+
+struct WT {
+  uint32_t *T;          // [2N]
+  uint32_t N, depth;    // leaves, levels below the root
+  long long *key;       // [n] stale scores (-1: a seed)
+  uint32_t *stamp;      // [n] step + 1 of the last re-evaluation
+  uint32_t *F;          // explored nodes, level after level (capacity 2N)
+  uint32_t *Ev;         // the level's re-evaluation list (capacity N)
+  uint32_t *seeds;
+  long long *gain_num;
+  unsigned long long *evals;  // [0] re-evaluations, [1] explored nodes
+};
+
+__global__ void __launch_bounds__(WT_THREADS, 1) k_cs_wintree(CSel S, WT W, uint32_t k) {
+  __shared__ uint32_t lvl_a[40], lvl_b[40];
+  __shared__ uint32_t nf, ne;
+  __shared__ Best sh[33];
+  __shared__ Best best;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long evals = 0, nodes = 0;
+  for (uint32_t step = 0; step < k; step++) {
+    if (threadIdx.x == 0) {
+      W.F[0] = 1;
+      lvl_a[0] = 0;
+      lvl_b[0] = 1;
+      nf = 1;
+      best = Best{LLONG_MIN, NONE};
+    }
+    __syncthreads();
+    // ---- FindMax, one tree level at a time
+    uint32_t L = 0;
+    for (;; L++) {
+      const uint32_t a = lvl_a[L], b = lvl_b[L];
+      if (a == b) break;
+      if (threadIdx.x == 0) ne = 0;
+      __syncthreads();
+      const Best cur = best;
+      for (uint32_t i = a + threadIdx.x; i < b; i += blockDim.x) {
+        const uint32_t t = W.F[i];
+        const uint32_t id = W.T[t];
+        if (id == NONE) continue;
+        if (W.stamp[id] != step + 1) {  // stale score
+          const long long kv = W.key[id];
+          if (!better(kv, id, cur.g, cur.v)) continue;  // the whole subtree is pruned
+          W.stamp[id] = step + 1;
+          W.Ev[atomicAdd(&ne, 1u)] = id;
+        }
+        if (t < W.N) {
+          const uint32_t at = atomicAdd(&nf, 2u);
+          W.F[at] = 2 * t;
+          W.F[at + 1] = 2 * t + 1;
+        }
+      }
+      __syncthreads();
+      // re-evaluate the level's list (a warp per vertex) and fold into Delta*
+      Best mine{LLONG_MIN, NONE};
+      for (uint32_t q = wid; q < ne; q += WT_THREADS / 32) {
+        const uint32_t v = W.Ev[q];
+        const long long g = cs_eval(S, v);
+        if (lane == 0) W.key[v] = g;
+        if (better(g, v, mine.g, mine.v)) mine = Best{g, v};
+      }
+      evals += ne;
+      nodes += b - a;
+      Best lb = block_best(mine, sh);
+      if (threadIdx.x == 0) {
+        if (better(lb.g, lb.v, best.g, best.v)) best = lb;
+        lvl_a[L + 1] = b;
+        lvl_b[L + 1] = nf;
+      }
+      __syncthreads();
+    }
+    const uint32_t s = best.v;
+    const long long g = best.g;
+    // ---- MarkSeed(s) (covered flags; the lazy selector updates no member)
+    const uint32_t srow = S.cid ? S.cid[s] : s;
+    if (srow != NONE)
+      for (uint32_t j = threadIdx.x; j < S.B; j += blockDim.x) {
+        const uint2 r = S.rec[(size_t)srow * S.MW + (j >> 5)];
+        if (!((r.y >> (j & 31)) & 1u)) continue;
+        const uint32_t e = r.x + __popc(r.y & ((1u << (j & 31)) - 1u));
+        const uint32_t x = S.E[2 * (size_t)e];
+        const uint32_t root = (x & PACIM_HIGH) ? e : x;
+        if (!(atomicOr(S.E + 2 * (size_t)root, COV) & COV)) {
+          const unsigned long long at = atomicAdd(S.cov_cnt, 1ull);
+          if (at < S.cov_cap) S.cov_list[at] = root;
+        }
+      }
+    if (threadIdx.x == 0) {
+      W.key[s] = -1;  // s leaves the candidate set (R6)
+      W.seeds[step] = s;
+      W.gain_num[step] = g;
+    }
+    __syncthreads();
+    // ---- the explored internal nodes' winners, bottom-up
+    for (int l = (int)L - 1; l >= 0; l--) {
+      for (uint32_t i = lvl_a[l] + threadIdx.x; i < lvl_b[l]; i += blockDim.x) {
+        const uint32_t t = W.F[i];
+        if (t < W.N) W.T[t] = wt_win(W.key, W.T[2 * t], W.T[2 * t + 1]);
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    W.evals[0] = evals;
+    W.evals[1] = nodes;
+  }
+}
+
+// leaves and one level of internal winners of the initial Win-Tree
+__global__ void k_wt_leaves(uint32_t *T, uint32_t N, uint32_t n) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+       i += (size_t)gridDim.x * blockDim.x)
+    T[N + i] = i < n ? (uint32_t)i : NONE;
+}
+
+__global__ void k_wt_level(uint32_t *T, const long long *key, uint32_t lo, uint32_t hi) {
+  for (size_t t = lo + (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < hi;
+       t += (size_t)gridDim.x * blockDim.x)
+    T[t] = wt_win(key, T[2 * t], T[2 * t + 1]);
 }
 
 // ------------------------------------------------------------- labels
@@ -675,16 +978,8 @@ __global__ void k_cs_labels(const CSel S, uint32_t j, uint32_t *out) {
       const uint2 r = S.rec[(size_t)row * S.MW + (j >> 5)];
       if ((r.y >> (j & 31)) & 1u) {
         const uint32_t e = r.x + __popc(r.y & ((1u << (j & 31)) - 1u));
-        const uint32_t x = S.P[e];
-        const uint32_t root = (x & PACIM_HIGH) ? e : x;
-        // row of the root entry: the last row whose first entry is <= root
-        uint32_t lo = 0, hi = S.nr;  // soff[lo] <= root < soff[hi]
-        while (hi - lo > 1) {
-          const uint32_t mid = lo + (hi - lo) / 2;
-          if (S.soff[mid] <= root) lo = mid;
-          else hi = mid;
-        }
-        lab = S.rmap ? S.rmap[lo] : lo;
+        const uint32_t x = S.E[2 * (size_t)e];
+        lab = S.vid[(x & PACIM_HIGH) ? e : x];  // the root entry's vertex (R8: min id)
       }
     }
     out[v] = lab;
@@ -700,14 +995,9 @@ static float ev_ms(cudaEvent_t a, cudaEvent_t b) {
   return ms;
 }
 
-static uint32_t cs_big_t(pacim_ctx *ctx) {
-  const char *e = getenv("PACIM_BIG_T");
-  return (uint32_t)(e ? std::max(1LL, atoll(e)) : std::max<uint64_t>(65536, ctx->nr / 8));
-}
-
 void pc_cs_free(pacim_ctx *ctx) {
-  for (DevBuf *d : {&ctx->cs_rec, &ctx->cs_soff, &ctx->cs_sl, &ctx->cs_ecrow, &ctx->cs_P,
-                    &ctx->cs_moff, &ctx->cs_memb, &ctx->cs_diag})
+  for (DevBuf *d : {&ctx->cs_rec, &ctx->cs_soff, &ctx->cs_ecrow, &ctx->cs_E, &ctx->cs_vid,
+                    &ctx->cs_diag, &ctx->cs_cnt})
     pc_free(ctx, *d);
   ctx->cs = false;
 }
@@ -717,25 +1007,55 @@ void pc_cs_free(pacim_ctx *ctx) {
 // non-singletons (c3: p = 1/2 on a grid), or 2^31 entries or more.
 bool pc_cs_build(pacim_ctx *ctx) {
   const uint32_t nr = ctx->nr, B = ctx->R_local, n = ctx->n;
+  bool force = false;
   if (const char *e = getenv("PACIM_STORE")) {
     if (std::string(e) == "dense") return false;
+    force = std::string(e) == "compact";
   } else if (getenv("PACIM_L2_BUDGET")) {
     return false;  // the slot-window layout is a dense-store experiment
   }
   if (B > 256 || nr == 0 || ctx->compressed) return false;
+  // an earlier build of this graph with these many slots found the sketches
+  // too dense for the compact store (the mask pass is not repeated)
+  if (!force && ctx->cs_pref_gen == ctx->graph_gen && ctx->cs_pref_B == B && ctx->cs_pref_dense)
+    return false;
   const uint32_t MW = (B + 31) / 32;
   pc_slot_table(ctx);
   pc_ensure(ctx, ctx->counters, 64 * sizeof(uint64_t));
   unsigned long long *ctr = ctx->counters.as<unsigned long long>();
   PC_CUDA(cudaMemsetAsync(ctr, 0, 64 * sizeof(uint64_t), ctx->stream));
   ctx->launches = 0;
-  cudaEvent_t ev[8];
-  for (auto &e : ev) PC_CUDA(cudaEventCreate(&e));
-  PC_CUDA(cudaEventRecord(ev[0], ctx->stream));
+  // phase events: named marks after each kernel (PACIM_BUILD_TIMES=1 prints them)
+  std::vector<std::pair<const char *, cudaEvent_t>> marks;
+  auto mark = [&](const char *name) {
+    cudaEvent_t e;
+    PC_CUDA(cudaEventCreate(&e));
+    PC_CUDA(cudaEventRecord(e, ctx->stream));
+    marks.push_back({name, e});
+  };
+  struct Cleanup {
+    std::vector<std::pair<const char *, cudaEvent_t>> &m;
+    ~Cleanup() {
+      for (auto &x : m) cudaEventDestroy(x.second);
+    }
+  } cleanup{marks};
+  const uint64_t nnz = 2 * ctx->m;
+  // store-row CSR tables of this graph (once per graph load)
+  if (ctx->cs_rows_gen != ctx->graph_gen) {
+    pc_ensure(ctx, ctx->cs_roff, ((size_t)nr + 1) * 8);
+    pc_ensure(ctx, ctx->cs_rcrow, (nnz / 32 + 2) * 4);
+    k_cs_roff<<<pc_grid(ctx, nr + 1, 256), 256, 0, ctx->stream>>>(
+        ctx->off.as<uint64_t>(), ctx->lean ? nullptr : ctx->rmap.as<uint32_t>(), nr, nnz,
+        ctx->cs_roff.as<uint64_t>());
+    k_cs_rcrow<<<pc_grid(ctx, nr, 256), 256, 0, ctx->stream>>>(ctx->cs_roff.as<uint64_t>(), nr,
+                                                               ctx->cs_rcrow.as<uint32_t>());
+    PC_CHECK_LAUNCH();
+    ctx->cs_rows_gen = ctx->graph_gen;
+  }
+  mark("start");
   // ---- masks (the rec array, .y words)
   pc_ensure(ctx, ctx->cs_rec, (size_t)nr * MW * 8);
   PC_CUDA(cudaMemsetAsync(ctx->cs_rec.p, 0, (size_t)nr * MW * 8, ctx->stream));
-  const uint64_t nnz = 2 * ctx->m;
   if (nnz) {
     const size_t smem = B * 4 + ((1u << PACIM_TB) + 1) * 2;
     const bool pe = ctx->pmodel != PACIM_P_CONST;
@@ -743,17 +1063,18 @@ bool pc_cs_build(pacim_ctx *ctx) {
                    : (ctx->hash_rule ? k_cs_mask<false, true> : k_cs_mask<false, false>);
     PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<pc_grid(ctx, (nnz + 31) / 32 * 32, CS_THREADS, 8), CS_THREADS, smem, ctx->stream>>>(
-        ctx->off.as<uint64_t>(), ctx->nbr.as<uint32_t>(), ctx->crow.as<uint32_t>(), nnz,
-        ctx->lean ? nullptr : ctx->cid.as<uint32_t>(), pe ? ctx->tcsr.as<uint32_t>() : nullptr,
-        ctx->toff(), ctx->t32, ctx->K, ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(),
-        ctx->d_hr64.as<uint64_t>(), B, MW, ctx->cs_rec.as<uint32_t>());
+        ctx->cs_roff.as<uint64_t>(), ctx->cs_rcrow.as<uint32_t>(), nr,
+        ctx->lean ? nullptr : ctx->rmap.as<uint32_t>(), ctx->nbr.as<uint32_t>(), nnz,
+        pe ? ctx->tcsr.as<uint32_t>() : nullptr, ctx->toff(), ctx->t32, ctx->K,
+        ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), ctx->d_hr64.as<uint64_t>(), B, MW,
+        ctx->cs_rec.as<uint32_t>());
     PC_CHECK_LAUNCH();
     ctx->launches++;
   }
-  // ---- counts -> entry offsets
-  TmpBuf cnt(ctx);
-  pc_ensure(ctx, cnt, 2 * ((size_t)nr + 1) * 8);
-  uint64_t *c64 = cnt.as<uint64_t>(), *pos = c64 + nr + 1;
+  mark("mask");
+  // ---- counts -> entry offsets (build scratch kept by the ctx)
+  pc_ensure(ctx, ctx->cs_cnt, 2 * ((size_t)nr + 1) * 8);
+  uint64_t *c64 = ctx->cs_cnt.as<uint64_t>(), *pos = c64 + nr + 1;
   k_cs_count<<<pc_grid(ctx, nr + 1, 256), 256, 0, ctx->stream>>>(ctx->cs_rec.as<uint2>(), nr, MW, c64);
   PC_CHECK_LAUNCH();
   pc_exclusive_scan_u64(ctx, c64, pos, (size_t)nr + 1);
@@ -761,8 +1082,18 @@ bool pc_cs_build(pacim_ctx *ctx) {
   PC_CUDA(cudaMemcpyAsync(&total, pos + nr, 8, cudaMemcpyDeviceToHost, ctx->stream));
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->launches += 2;
-  if (total >= (1ull << 31) || 2 * total > (uint64_t)nr * B) {
-    for (auto &e : ev) cudaEventDestroy(e);
+  mark("scan");
+  // the compact store pays when most (row, slot) pairs are singletons: its
+  // mask pass and per-entry indirection cost more than the dense passes save
+  // above ~15 % non-singleton pairs (measured: c4 9.8 % -> compact, c2 23 %
+  // -> dense); PACIM_CS_DENSITY overrides, PACIM_STORE=compact forces (up to 50 %)
+  const double dmax = force ? 0.5
+                            : (getenv("PACIM_CS_DENSITY") ? atof(getenv("PACIM_CS_DENSITY")) : 0.15);
+  const bool dense = total >= (1ull << 31) || (double)total > dmax * (double)nr * B;
+  ctx->cs_pref_gen = ctx->graph_gen;
+  ctx->cs_pref_B = B;
+  ctx->cs_pref_dense = dense;
+  if (dense) {
     pc_free(ctx, ctx->cs_rec);
     return false;  // dense: the vertex-major store is the better layout
   }
@@ -775,67 +1106,55 @@ bool pc_cs_build(pacim_ctx *ctx) {
   ctx->cs_total = total;
   const uint64_t T1 = std::max<uint64_t>(total, 1);
   pc_ensure(ctx, ctx->cs_soff, ((size_t)nr + 1) * 4);
-  pc_ensure(ctx, ctx->cs_sl, T1);
   pc_ensure(ctx, ctx->cs_ecrow, (T1 / 32 + 2) * 4);
-  pc_ensure(ctx, ctx->cs_P, T1 * 4);
-  pc_ensure(ctx, ctx->cs_moff, (T1 + 1) * 4);
+  pc_ensure(ctx, ctx->cs_E, T1 * 8);
+  pc_ensure(ctx, ctx->cs_vid, T1 * 4);
   k_cs_rec<<<pc_grid(ctx, nr, 256), 256, 0, ctx->stream>>>(
-      ctx->cs_rec.as<uint2>(), nr, MW, pos, ctx->cs_soff.as<uint32_t>(), ctx->cs_sl.as<uint8_t>(),
-      ctx->cs_ecrow.as<uint32_t>());
+      ctx->cs_rec.as<uint2>(), nr, MW, pos, ctx->cs_soff.as<uint32_t>(), ctx->cs_ecrow.as<uint32_t>());
   PC_CHECK_LAUNCH();
-  uint32_t *P = ctx->cs_P.as<uint32_t>();
-  k_cs_fill<<<pc_grid(ctx, total, 256), 256, 0, ctx->stream>>>(P, total, ROOT1);
+  mark("rec");
+  uint2 *E = ctx->cs_E.as<uint2>();
+  uint32_t *Ew = ctx->cs_E.as<uint32_t>();
+  k_cs_fill<<<pc_grid(ctx, total, 256), 256, 0, ctx->stream>>>(E, total);
   PC_CHECK_LAUNCH();
   ctx->launches += 2;
-  PC_CUDA(cudaEventRecord(ev[1], ctx->stream));
-  // ---- unions (H2, H3)
-  pc_cs_edges(ctx, P, ctx->cs_rec.as<uint2>(), MW, ctr);
-  PC_CUDA(cudaEventRecord(ev[2], ctx->stream));
-  // ---- compression + sizes (H4, H5)
+  mark("init");
+  // ---- unions (H2, H3) on the P words (stride 2)
+  pc_cs_edges(ctx, Ew, ctx->cs_rec.as<uint2>(), MW, ctr);
+  mark("edges");
+  // ---- compression, sizes, member lists (H4, H5, H6u)
   pc_ensure(ctx, ctx->d_hot, 2 * (size_t)B * 4);
   uint32_t *hot = ctx->d_hot.as<uint32_t>();
-  k_cs_hot<<<(B + 255) / 256, 256, 0, ctx->stream>>>(ctx->cs_rec.as<uint2>(), MW, P, ctx->hub_row,
-                                                     nr, B, hot);
+  // the hub's CCs are "hot" (counted in shared memory, covered by the hot sums)
+  // when they are expected to be giant: its expected live degree (deg * p)
+  // is large (c2: 163K * 0.02; never under WIC, whose hub edges have p ~ 1/deg)
+  double pm = (double)ctx->t32 / 4294967296.0;
+  if (ctx->pmodel == PACIM_P_UNIFORM)
+    pm = 0.5 * ((double)(ctx->t32 >> 32) + (double)(ctx->t32 & 0xFFFFFFFFull)) / 4294967296.0;
+  const bool hot_on = ctx->pmodel != PACIM_P_WIC && (double)ctx->hub_degree * pm >= 64.0 &&
+                      !getenv("PACIM_NO_HOT");
+  k_cs_hot<<<(B + 255) / 256, 256, 0, ctx->stream>>>(ctx->cs_rec.as<uint2>(), MW, Ew,
+                                                     hot_on ? ctx->hub_row : NONE, nr, B, hot);
   PC_CHECK_LAUNCH();
-  k_cs_compress<<<pc_grid(ctx, total, CS_THREADS, 8), CS_THREADS, 0, ctx->stream>>>(
-      P, total, ctx->cs_sl.as<uint8_t>(), B, hot, ctr);
+  k_cs_compress<<<pc_grid(ctx, total, CS_THREADS, 8), CS_THREADS, 0, ctx->stream>>>(Ew, total, hot,
+                                                                                   B, ctr);
   PC_CHECK_LAUNCH();
   pc_ensure(ctx, ctx->d_hot_size, (size_t)B * 4);
-  k_cs_hot_sizes<<<(B + 255) / 256, 256, 0, ctx->stream>>>(P, hot, B, ctx->d_hot_size.as<uint32_t>());
+  k_cs_hot_sizes<<<(B + 255) / 256, 256, 0, ctx->stream>>>(Ew, hot, B, ctx->d_hot_size.as<uint32_t>());
   PC_CHECK_LAUNCH();
   ctx->launches += 3;
-  PC_CUDA(cudaEventRecord(ev[3], ctx->stream));
-  // ---- member offsets: exclusive scan of the member-list sizes (H6u)
-  const uint32_t big_t = cs_big_t(ctx);
-  ctx->cs_big_t = big_t;
-  {
-    cub::CountingInputIterator<uint64_t> it(0);
-    cub::TransformInputIterator<uint32_t, MembSize, cub::CountingInputIterator<uint64_t>> in(
-        it, MembSize{P, total, big_t});
-    size_t tb = 0;
-    PC_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, in, ctx->cs_moff.as<uint32_t>(),
-                                          (int64_t)total + 1, ctx->stream));
-    TmpBuf tmp(ctx);
-    pc_ensure(ctx, tmp, std::max<size_t>(tb, 16));
-    PC_CUDA(cub::DeviceScan::ExclusiveSum(tmp.p, tb, in, ctx->cs_moff.as<uint32_t>(),
-                                          (int64_t)total + 1, ctx->stream));
-    uint32_t nm = 0;
-    PC_CUDA(cudaMemcpyAsync(&nm, ctx->cs_moff.as<uint32_t>() + total, 4, cudaMemcpyDeviceToHost,
-                            ctx->stream));
-    ctx->hot_size.resize(B);
-    PC_CUDA(cudaMemcpyAsync(ctx->hot_size.data(), ctx->d_hot_size.p, (size_t)B * 4,
-                            cudaMemcpyDeviceToHost, ctx->stream));
-    PC_CUDA(cudaStreamSynchronize(ctx->stream));
-    ctx->cs_nmemb = nm;
-    ctx->launches++;
-  }
-  pc_ensure(ctx, ctx->cs_memb, std::max<size_t>(ctx->cs_nmemb, 1) * 4);
-  PC_CUDA(cudaEventRecord(ev[4], ctx->stream));
-  // ---- gain0 (H7), hot sums, member scatter
+  mark("compress");
+  // ---- gain0 (H7), hot sums, vertex of each entry
+  ctx->cs_list_t = getenv("PACIM_BIG_T") ? (uint32_t)std::max(1LL, atoll(getenv("PACIM_BIG_T")))
+                                         : LIST_T;
+  ctx->hot_size.resize(B);
+  PC_CUDA(cudaMemcpyAsync(ctx->hot_size.data(), ctx->d_hot_size.p, (size_t)B * 4,
+                          cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
   bool any = false;
-  for (uint32_t j = 0; j < B; j++) any |= ctx->hot_size[j] > big_t;
+  for (uint32_t j = 0; j < B; j++) any |= ctx->hot_size[j] > 0;
   ctx->hot_any = any;
-  ctx->hot_big_t = big_t;
+  ctx->hot_big_t = 0;
   if (any) pc_ensure(ctx, ctx->hotsum, (size_t)n * 8);
   pc_ensure(ctx, ctx->gain0, (size_t)n * 8);
   k_cs_gain_init<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(
@@ -845,32 +1164,45 @@ bool pc_cs_build(pacim_ctx *ctx) {
   {
     auto kern = any ? k_cs_gain<true> : k_cs_gain<false>;
     kern<<<pc_grid(ctx, total, CS_THREADS, 8), CS_THREADS, 0, ctx->stream>>>(
-        P, total, ctx->cs_sl.as<uint8_t>(), ctx->cs_soff.as<uint32_t>(), ctx->cs_ecrow.as<uint32_t>(),
-        ctx->lean ? nullptr : ctx->rmap.as<uint32_t>(), B, hot, ctx->d_hot_size.as<uint32_t>(), big_t,
-        ctx->cs_moff.as<uint32_t>(), ctx->cs_memb.as<uint32_t>(), ctx->gain0.as<int64_t>(),
-        any ? ctx->hotsum.as<int64_t>() : nullptr, ctr);
+        Ew, total, ctx->cs_soff.as<uint32_t>(), ctx->cs_ecrow.as<uint32_t>(),
+        ctx->lean ? nullptr : ctx->rmap.as<uint32_t>(), B, hot, ctx->cs_vid.as<uint32_t>(),
+        ctx->gain0.as<int64_t>(), any ? ctx->hotsum.as<int64_t>() : nullptr, ctr);
     PC_CHECK_LAUNCH();
   }
   ctx->launches += 2;
-  PC_CUDA(cudaEventRecord(ev[5], ctx->stream));
+  mark("gain");
   unsigned long long h[6];
   PC_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream));
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->cs = true;
   ctx->ncomp = h[0];
   ctx->nnonsingle = total;
-  ctx->nmember = ctx->cs_nmemb;
+  ctx->nmember = total;
   ctx->stats.live_pairs = h[4];
   PC_REQUIRE(h[0] + h[1] == total, PACIM_ECHECK, "compact store: roots + non-roots != entries");
-  ctx->stats.t_init_ms = ev_ms(ev[0], ev[1]);      // masks, offsets, P = HIGH | 1
-  ctx->stats.t_edges_ms = ev_ms(ev[1], ev[2]);
-  ctx->stats.t_compress_ms = ev_ms(ev[2], ev[3]);
-  ctx->stats.t_compact_ms = ev_ms(ev[3], ev[4]);   // member offsets
-  ctx->stats.t_gain_ms = ev_ms(ev[4], ev[5]);
+  auto span = [&](const char *a, const char *b) {
+    cudaEvent_t ea = nullptr, eb = nullptr;
+    for (auto &x : marks) {
+      if (!strcmp(x.first, a)) ea = x.second;
+      if (!strcmp(x.first, b)) eb = x.second;
+    }
+    return ev_ms(ea, eb);
+  };
+  ctx->stats.t_init_ms = span("start", "init");      // masks, offsets, records, E
+  ctx->stats.t_edges_ms = span("init", "edges");
+  ctx->stats.t_compress_ms = span("edges", "compress");
+  ctx->stats.t_compact_ms = 0;
+  ctx->stats.t_gain_ms = span("compress", "gain");
   ctx->stats.t_centers_ms = 0;
-  ctx->stats.t_build_ms = ev_ms(ev[0], ev[5]);
+  ctx->stats.t_build_ms = span("start", "gain");
   ctx->stats.kernel_launches_build = ctx->launches;
-  for (auto &e : ev) cudaEventDestroy(e);
+  if (getenv("PACIM_BUILD_TIMES")) {
+    fprintf(stderr, "cs build ms:");
+    for (size_t i = 1; i < marks.size(); i++)
+      fprintf(stderr, " %s %.3f", marks[i].first, ev_ms(marks[i - 1].second, marks[i].second));
+    fprintf(stderr, " | total %.3f entries %llu\n", ctx->stats.t_build_ms,
+            (unsigned long long)total);
+  }
   ctx->sel_list_valid = false;
   return true;
 }
@@ -881,23 +1213,19 @@ static CSel make_csel(pacim_ctx *ctx, long long *target) {
   CSel S;
   S.rec = ctx->cs_rec.as<uint2>();
   S.MW = ctx->cs_MW;
-  S.P = ctx->cs_P.as<uint32_t>();
-  S.moff = ctx->cs_moff.as<uint32_t>();
-  S.memb = ctx->cs_memb.as<uint32_t>();
-  S.sl = ctx->cs_sl.as<uint8_t>();
+  S.E = ctx->cs_E.as<uint32_t>();
+  S.vid = ctx->cs_vid.as<uint32_t>();
   S.soff = ctx->cs_soff.as<uint32_t>();
-  S.ecrow = ctx->cs_ecrow.as<uint32_t>();
   S.rmap = ctx->lean ? nullptr : ctx->rmap.as<uint32_t>();
   S.cid = ctx->lean ? nullptr : ctx->cid.as<uint32_t>();
   S.nr = ctx->nr;
   S.B = B;
   S.nv = n;
   S.total = ctx->cs_total;
-  S.big_t = ctx->cs_big_t;
+  S.list_t = ctx->cs_list_t;
   S.target = target;
   S.hotsum = ctx->hot_any ? ctx->hotsum.as<int64_t>() : nullptr;
   S.hot_root = ctx->d_hot.as<uint32_t>();
-  S.hot_size = ctx->d_hot_size.as<uint32_t>();
   uint32_t csh = 10;
   while (((uint64_t)n + (1ull << csh) - 1) >> csh > MAX_CHUNKS) csh++;
   S.csh = csh;
@@ -922,6 +1250,7 @@ static CSel make_csel(pacim_ctx *ctx, long long *target) {
   S.par = 0;
   S.track = 0;
   S.dlst = ctx->dlist;
+  S.celf = nullptr;
   return S;
 }
 
@@ -932,7 +1261,7 @@ static void cs_uncover(pacim_ctx *ctx, const CSel &S) {
     PC_CUDA(cudaStreamSynchronize(ctx->stream));
   }
   PC_REQUIRE(cnt <= S.cov_cap, PACIM_ECHECK, "covered-CC list overflowed");
-  if (cnt) k_cs_uncover<<<pc_grid(ctx, cnt, 256), 256, 0, ctx->stream>>>(S.P, S.cov_list, cnt);
+  if (cnt) k_cs_uncover<<<pc_grid(ctx, cnt, 256), 256, 0, ctx->stream>>>(S.E, S.cov_list, cnt);
   PC_CUDA(cudaMemsetAsync(S.cov_cnt, 0, 8, ctx->stream));
   PC_CUDA(cudaMemsetAsync(S.dense, 0, 8, ctx->stream));
   PC_CUDA(cudaMemsetAsync(S.cov_root, 0xFF, (size_t)S.B * 4, ctx->stream));
@@ -992,6 +1321,13 @@ void pc_cs_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num
   PC_CUDA(cudaMemsetAsync(ctx->sel_gain.p, 0, (size_t)k * 16 + 64, ctx->stream));
   PC_CUDA(cudaMemsetAsync(S.cdirty, 0, (size_t)S.nchunks * 4, ctx->stream));
   PC_CUDA(cudaMemsetAsync(S.dcnt, 0, 8, ctx->stream));
+  TmpBuf celf(ctx);
+  if (getenv("PACIM_CELF_COUNT")) {  // CELF's evaluation count on the same gains (f2)
+    pc_ensure(ctx, celf, (size_t)n * 8);
+    PC_CUDA(cudaMemcpyAsync(celf.p, ctx->gain0.p, (size_t)n * 8, cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+    S.celf = celf.as<long long>();
+  }
   uint32_t par0 = ctx->sel_par;
   void *args[] = {&S, &O, &par0};
   PC_CUDA(cudaLaunchCooperativeKernel((void *)k_cs_select, grid, SEL_THREADS, args, 0, ctx->stream));
@@ -1012,6 +1348,7 @@ void pc_cs_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num
   ctx->stats.select_member_updates = d[CD_UPD];
   ctx->stats.select_dense_steps = d[CD_DENSE];
   ctx->stats.select_hotsum_steps = d[CD_HOT];
+  ctx->stats.select_celf_evaluations = d[CD_CELF];
   ctx->stats.select_bfs_visits = 0;
   ctx->stats.select_warp_slots = ctx->stats.select_deferred_slots = 0;
   ctx->stats.select_row_items = ctx->stats.select_chunk_items = 0;
@@ -1073,4 +1410,73 @@ void pc_cs_lazy_mark(pacim_ctx *ctx, uint32_t s) {
   CSel S = make_csel(ctx, nullptr);
   k_cs_lazy_mark<<<(S.B + 255) / 256, 256, 0, ctx->stream>>>(S, s);
   PC_CHECK_LAUNCH();
+}
+
+// NEXT f2: the Win-Tree selector (selector 2).  One single-block kernel runs
+// all k steps; the tree and the stale scores live in device memory.
+void pc_cs_select_wintree(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
+                          int64_t *sigma_num) {
+  const uint32_t n = ctx->n;
+  uint32_t N = 1, depth = 0;
+  while (N < n) {
+    N <<= 1;
+    depth++;
+  }
+  cs_grow_list(ctx, k);
+  pc_dist_restore(ctx);
+  pc_ensure(ctx, ctx->gain, (size_t)n * 8);
+  CSel S = make_csel(ctx, ctx->gain.as<long long>());
+  // scratch: T[2N], stamp[n], F[2N], Ev[N], seeds[k], gains[k], counters
+  TmpBuf wb(ctx);
+  const size_t bytes = (size_t)2 * N * 4 + (size_t)n * 4 + (size_t)2 * N * 4 + (size_t)N * 4 +
+                       (size_t)k * 12 + 64;
+  pc_ensure(ctx, wb, bytes);
+  WT W;
+  char *p = wb.as<char>();
+  W.T = reinterpret_cast<uint32_t *>(p);
+  W.stamp = W.T + 2 * (size_t)N;
+  W.F = W.stamp + n;
+  W.Ev = W.F + 2 * (size_t)N;
+  W.gain_num = reinterpret_cast<long long *>(
+      (reinterpret_cast<uintptr_t>(W.Ev + N) + 7) & ~(uintptr_t)7);
+  W.seeds = reinterpret_cast<uint32_t *>(W.gain_num + k);
+  W.evals = reinterpret_cast<unsigned long long *>(
+      (reinterpret_cast<uintptr_t>(W.seeds + k) + 7) & ~(uintptr_t)7);
+  W.N = N;
+  W.depth = depth;
+  W.key = ctx->gain.as<long long>();
+  cudaEvent_t e0, e1;
+  PC_CUDA(cudaEventCreate(&e0));
+  PC_CUDA(cudaEventCreate(&e1));
+  PC_CUDA(cudaEventRecord(e0, ctx->stream));
+  cs_uncover(ctx, S);
+  PC_CUDA(cudaMemcpyAsync(W.key, ctx->gain0.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  PC_CUDA(cudaMemsetAsync(W.stamp, 0, (size_t)n * 4, ctx->stream));
+  k_wt_leaves<<<pc_grid(ctx, N, 256), 256, 0, ctx->stream>>>(W.T, N, n);
+  for (uint32_t lo = N >> 1; lo >= 1; lo >>= 1)
+    k_wt_level<<<pc_grid(ctx, lo, 256), 256, 0, ctx->stream>>>(W.T, W.key, lo, 2 * lo);
+  PC_CHECK_LAUNCH();
+  k_cs_wintree<<<1, WT_THREADS, 0, ctx->stream>>>(S, W, k);
+  PC_CHECK_LAUNCH();
+  PC_CUDA(cudaEventRecord(e1, ctx->stream));
+  std::vector<long long> hg(k);
+  unsigned long long ev[2];
+  PC_CUDA(cudaMemcpyAsync(seeds, W.seeds, (size_t)k * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaMemcpyAsync(hg.data(), W.gain_num, (size_t)k * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaMemcpyAsync(ev, W.evals, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  ctx->stats.t_select_ms = ms;
+  ctx->stats.select_evaluations = ev[0];
+  ctx->stats.select_eval_rounds = ev[1];  // Win-Tree nodes explored
+  ctx->stats.kernel_launches_select = depth + 2;
+  long long run = 0;
+  for (uint32_t i = 0; i < k; i++) {
+    gain_num[i] = hg[i];
+    run += hg[i];
+    sigma_num[i] = run;
+  }
 }

@@ -36,9 +36,15 @@ def main():
           "recognised when discovered, so a center among the seed's live neighbours costs 0);\n"
           "Thm 3.1 bounds the expected visits by about 1/alpha.  Device total = every buffer\n"
           "the ctx holds (graph, store, selection state, scratch).\n")
+    print("Store: alpha < 1: label + size (one u32 each, the covered flag in the size word) per\n"
+          "(center, sketch); alpha = 1: the compact store (per non-singleton (vertex, sketch)\n"
+          "entry: parent/size, member offset, member id; per row the slot-mask records).\n"
+          "Peak = the high-water mark of the ctx's device bytes over build + select (graph\n"
+          "included; pacim_stats.device_peak_bytes).\n")
     print("| alpha | rho (centers) | sketch store (GB) | build scratch (GB) | device total (GB) "
-          "| build ms | select ms | Get-center visits / probe | 1/alpha | seeds = alpha 1 |")
-    print("|---|---|---|---|---|---|---|---|---|---|")
+          "| device peak (GB) | build ms | select ms | Get-center visits / probe | 1/alpha "
+          "| seeds = alpha 1 |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|")
     ref = None
     for al in [float(x) for x in a.alphas.split(",")]:
         a32 = 1 << 32 if al >= 1 else int(al * 4294967296.0)
@@ -51,9 +57,13 @@ def main():
             ts.append(st["t_select_ms"])
         B = st["R_local"]
         if st["compressed"]:
-            store = 3 * st["rho"] * B * 4  # label, pristine size, working size per (center, slot)
-            scratch = st["rows"] * st["batch_slots"] * 4  # parent arrays of one build batch
+            store = 2 * st["rho"] * B * 4  # label, size (+ covered bit) per (center, slot)
+            scratch = (st["rows"] + st["rho"]) * st["batch_slots"] * 4  # one build batch
             vis = st["select_center_visits"] / max(st["select_center_found"], 1)
+        elif st["store"] == 1:
+            store = 12 * st["nnonsingle"] + st["rows"] * ((B + 31) // 32) * 8
+            scratch = 4 * st["nnonsingle"]  # ranks in the CCs (member index build)
+            vis = float("nan")
         else:
             store = st["rows"] * B * 4
             scratch = 0
@@ -62,7 +72,7 @@ def main():
         if ref is None:
             ref = seeds
         print(f"| {al:g} | {st['rho']} | {store / 1e9:.3f} | {scratch / 1e9:.3f} "
-              f"| {st['device_bytes'] / 1e9:.2f} "
+              f"| {st['device_bytes'] / 1e9:.2f} | {st['device_peak_bytes'] / 1e9:.2f} "
               f"| {min(tb):.1f} | {min(ts):.1f} | {vis:.2f} | {1 / al:g} | {seeds == ref} |")
     ctx.close()
 

@@ -1,9 +1,16 @@
-"""the lazy (CELF-style) selector against the incremental
-one on the same store: evaluations (the paper's re-evaluation counts,
-P:1662-1693: social/web graphs need ~n evaluations over k = 100, road
-graphs ~140), prefix-doubling rounds, time, and identical seeds (R17).
+"""the lazy selectors against the incremental one on the
+same store, with CELF's evaluation count on the same gains:
 
-    python profiles/lazy_f2.py c2 c3 c4 > profiles/rNN_lazy.md
+* incremental (selector 0): member gains updated when a CC is covered; with
+  PACIM_CELF_COUNT=1 it also counts the re-evaluations CELF would make
+  (every non-seed whose stale score ranks at or above the step's winner);
+* prefix doubling (selector 1, the P-tree scheme);
+* Win-Tree (selector 2; compact store only).
+
+The paper reports P-tree / Win-Tree evaluations at 1.03x / 1.7x CELF's
+(P:1715-1720).  Re-evaluations exclude the initial n evaluations (gain0).
+
+    python profiles/lazy_f2.py c2 c4 > profiles/rNN_lazy.md
 """
 import os
 import sys
@@ -15,12 +22,13 @@ import inputs  # noqa: E402
 
 
 def main():
+    os.environ["PACIM_CELF_COUNT"] = "1"
     import paper_2311_07554_b200 as P
     from paper_2311_07554_b200 import pipeline
-    print("# f2 — lazy vs incremental selection, B200, 1 GPU, uncompressed store\n")
-    print("| config | n | k | incremental select ms | lazy select ms | evaluations "
-          "| evaluations / n | doubling rounds | same seeds |")
-    print("|---|---|---|---|---|---|---|---|---|")
+    print("# f2 — lazy selectors vs incremental, with CELF's count, B200, 1 GPU\n")
+    print("| config | store | n | k | incremental ms | CELF re-evals | prefix-doubling ms | "
+          "its re-evals | / CELF | Win-Tree ms | its re-evals | / CELF | tree nodes | same seeds |")
+    print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
     for name in sys.argv[1:] or ["c2"]:
         cfg = inputs.config(name)
         ctx = P.Context(0)
@@ -28,15 +36,21 @@ def main():
         ctx.pacim_build_sketches(cfg["R"], cfg["hash_seed"])
         k = cfg["k"]
         a = ctx.pacim_select_seeds(k)
-        ti = ctx.pacim_get_stats()["t_select_ms"]
-        ctx.pacim_set_selector(1)
-        b = ctx.pacim_select_seeds(k)
         st = ctx.pacim_get_stats()
+        ti, celf, store = st["t_select_ms"], st["select_celf_evaluations"], st["store"]
+        res = []
+        for sel in (1, 2):
+            ctx.pacim_set_selector(sel)
+            b = ctx.pacim_select_seeds(k)
+            s2 = ctx.pacim_get_stats()
+            same = list(a[0]) == list(b[0]) and list(a[1]) == list(b[1])
+            res.append((s2["t_select_ms"], s2["select_evaluations"], s2["select_eval_rounds"], same))
         ctx.pacim_set_selector(0)
-        same = list(a[0]) == list(b[0]) and list(a[1]) == list(b[1])
-        print(f"| {name} | {n} | {k} | {ti:.1f} | {st['t_select_ms']:.1f} | "
-              f"{st['select_evaluations']} | {st['select_evaluations'] / n:.3f} | "
-              f"{st['select_eval_rounds']} | {same} |")
+        (t1, e1, _, ok1), (t2, e2, nodes, ok2) = res
+        r1 = e1 / celf if celf else float("nan")
+        r2 = e2 / celf if celf else float("nan")
+        print(f"| {name} | {'compact' if store == 1 else 'dense'} | {n} | {k} | {ti:.1f} | {celf} | "
+              f"{t1:.1f} | {e1} | {r1:.2f} | {t2:.1f} | {e2} | {r2:.2f} | {nodes} | {ok1 and ok2} |")
         ctx.close()
 
 
