@@ -248,6 +248,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--force-dist", action="store_true",
                     help="testing: NCCL process group and the per-step collectives even at one rank")
+    ap.add_argument("--selector", default="auto", choices=["auto", "incremental", "ptree", "wintree"],
+                    help="pacim_set_selector: auto (default: the Win-Tree under WIC, else incremental; "
+                         "sharded: incremental)")
     ap.add_argument("--py-dist", action="store_true",
                     help="multi-rank select through dist.py's per-step primitives (torch.distributed) "
                          "instead of the library's NCCL loop")
@@ -279,6 +282,7 @@ def main():
     ctx = P.Context(local, stream)  # torch's current stream (legacy default: cudaStreamLegacy)
     if use_dist and not args.py_dist:
         pdist.init_comm(ctx, rank, world)  # NCCL inside the library (pacim_init_comm)
+    ctx.pacim_set_selector({"incremental": 0, "ptree": 1, "wintree": 2, "auto": 3}[args.selector])
     n, m = pipeline.generate(ctx, cfg)
     pm, t32 = pipeline.model_of(cfg)
     a32 = pipeline.center_a32_of(cfg)
@@ -450,6 +454,7 @@ def main():
         "warmup": max(3, args.warmup), "ms_per_step": ms_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (counter-based generator, DESIGN.md §Input recipe)",
+        "selector": args.selector,
         "select_path": ("dist.py per-step primitives (torch.distributed)" if (use_dist and args.py_dist)
                         else "library NCCL loop (pacim_init_comm)" if use_dist else "single GPU"),
         "config": {"workload": cfg["name"] + (f"-scale{args.scale}" if args.scale else ""),

@@ -155,7 +155,7 @@ static void free_all(pacim_ctx *ctx) {
                     &ctx->scratch, &ctx->scratch2, &ctx->sel_seeds, &ctx->sel_gain,
                     &ctx->sel_partial, &ctx->sel_list, &ctx->sel_flag, &ctx->argmax_part, &ctx->bfs, &ctx->tcsr, &ctx->hidx, &ctx->hub_tab, &ctx->hla_off, &ctx->hla_row, &ctx->hla_raw, &ctx->d_smap, &ctx->pkeys, &ctx->cprobe, &ctx->cseed, &ctx->d_hr64, &ctx->crow, &ctx->vinfo, &ctx->hotsum, &ctx->d_hot_size,
                     &ctx->cs_rec, &ctx->cs_soff, &ctx->cs_ecrow, &ctx->cs_E, &ctx->cs_vid,
-                    &ctx->cs_diag, &ctx->cs_cnt, &ctx->cs_roff, &ctx->cs_rcrow, &ctx->dist_ghot, &ctx->dist_buf, &ctx->dist_cov_old};
+                    &ctx->cs_diag, &ctx->cs_cnt, &ctx->dist_ghot, &ctx->dist_buf, &ctx->dist_cov_old};
   for (DevBuf *b : bufs) pc_free(ctx, *b);
 }
 
@@ -482,15 +482,22 @@ int pacim_select_seeds(pacim_ctx *ctx, uint32_t k, uint32_t *seeds_out, int64_t 
       pc_dist_select(ctx, k, seeds_out, gain_num_out);
       int64_t run = 0;
       for (uint32_t i = 0; i < k; i++) sigma_num_out[i] = run += gain_num_out[i];
-    } else if (ctx->compressed)
+    } else if (ctx->compressed) {
       pc_select_compressed(ctx, k, seeds_out, gain_num_out, sigma_num_out);
-    else
-      if (ctx->selector == 2 && ctx->cs)
+    } else {
+      // selector 3 (auto): the Win-Tree under WIC (a few re-evaluations per
+      // step: c4 needs ~1.5), else the incremental selector
+      // (constant / uniform p on social graphs re-evaluate ~n vertices)
+      const int sel = ctx->selector == 3 ? (ctx->pmodel == PACIM_P_WIC ? 2 : 0) : ctx->selector;
+      if (sel == 2 && ctx->cs)
         pc_cs_select_wintree(ctx, k, seeds_out, gain_num_out, sigma_num_out);
-      else if (ctx->selector >= 1)
+      else if (sel == 2)
+        pc_select_wintree_dense(ctx, k, seeds_out, gain_num_out, sigma_num_out);
+      else if (sel == 1)
         pc_select_lazy(ctx, k, seeds_out, gain_num_out, sigma_num_out);
       else
         pc_select(ctx, k, seeds_out, gain_num_out, sigma_num_out);
+    }
     if (sigma_out)
       for (uint32_t i = 0; i < k; i++) sigma_out[i] = (double)sigma_num_out[i] / (double)ctx->R;
   });
@@ -574,8 +581,8 @@ int pacim_simulate_ic(pacim_ctx *ctx, const uint32_t *seeds, uint32_t ns, uint32
 
 int pacim_set_selector(pacim_ctx *ctx, int selector) {
   return guarded(ctx, [&] {
-    PC_REQUIRE(selector >= 0 && selector <= 2, PACIM_EINVAL,
-               "selector must be 0 (incremental), 1 (prefix doubling) or 2 (Win-Tree)");
+    PC_REQUIRE(selector >= 0 && selector <= 3, PACIM_EINVAL,
+               "selector must be 0 (incremental), 1 (prefix doubling), 2 (Win-Tree) or 3 (auto)");
     ctx->selector = selector;
   });
 }

@@ -112,9 +112,11 @@ constexpr int EDGE_WARPS = EDGE_THREADS / 32;
 // an entry lies past the row's end), and keeps the upper ones (v > u); rows
 // are the vertex ids.  `keys` = CSR offsets, `ckeys` = neighbours (as u32),
 // `tm1` = chunk rows, m = CSR entries (2m).
-// CS: the compact store (store_cs.cu): L is the flat parent array P and a
-// (row, slot) pair is entry pc_cs_pos(rec, MW, row, slot) (j0 = 0, Bb = B)
-template <bool WIC, bool REC, bool DECOR, bool LEAN, bool CS = false>
+// CS: the compact store (store_cs.cu), j0 = 0, Bb = B.  CS = 1: the unions,
+// L = the {P, next} words of the entries, (row, slot) = entry
+// pc_cs_pos(rec, MW, row, slot); CS = 2: the mask pass, every live (edge,
+// slot) sets bit slot of both endpoints' row masks (L = the rec words)
+template <bool WIC, bool REC, bool DECOR, bool LEAN, int CS = 0>
 __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__restrict__ keys,
                                                         const uint64_t *__restrict__ ckeys,
                                                         const uint32_t *__restrict__ tm1,
@@ -239,8 +241,21 @@ __global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__res
                 // need not survive it)
         hla.stage(u & ~PACIM_HUBF, v & ~PACIM_HUBF, j, (lv && (u & PACIM_HUBF)) ? 1u : 0u,
                   (lv && (v & PACIM_HUBF)) ? 1u : 0u, w_hla[REC ? wid : 0], hla_n);
-      if (lv) {
-        if (CS)
+      if (CS == 2) {
+        // mask pass: the lanes of one (row, word) combine (u-side runs are
+        // adjacent), one atomicOr each; the v side is one atomicOr per pair
+        const uint32_t uu = u & ~PACIM_HUBF, vv = v & ~PACIM_HUBF;
+        const unsigned long long ku = lv ? ((unsigned long long)uu << 8 | (j >> 5)) : ~0ull;
+        const uint32_t peers = __match_any_sync(0xffffffffu, ku);
+        const uint32_t bits = __reduce_or_sync(peers, lv ? 1u << (j & 31) : 0u);
+        if (lv && (threadIdx.x & 31) == __ffs(peers) - 1)
+          atomicOr(L + ((size_t)uu * MW + (j >> 5)) * 2 + 1, bits);
+        if (lv) {
+          atomicOr(L + ((size_t)vv * MW + (j >> 5)) * 2 + 1, 1u << (j & 31));
+          live++;
+        }
+      } else if (lv) {
+        if (CS == 1)
           uf_unite(L, 2, 0, pc_cs_pos(rec, MW, u & ~PACIM_HUBF, j),
                    pc_cs_pos(rec, MW, v & ~PACIM_HUBF, j));
         else
@@ -1010,37 +1025,52 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
 
 // The union pass over the compact store (store_cs.cu): every upper edge,
 // its live sketches, unions of the flat entries in P.  ctr[4] += live pairs.
-void pc_cs_edges(pacim_ctx *ctx, uint32_t *P, const uint2 *rec, uint32_t MW,
-                 unsigned long long *ctr) {
+template <int MODE>
+static void cs_edges(pacim_ctx *ctx, uint32_t *L, const uint2 *rec, uint32_t MW,
+                     unsigned long long *ctr) {
   const uint32_t B = ctx->R_local;
   const uint32_t NT = 1u << PACIM_TB;
   const size_t smem = B * sizeof(uint32_t) + (NT + 1) * sizeof(uint16_t);
   if (ctx->lean) {
-    auto kern = ctx->hash_rule ? k_edges<false, false, true, true, true>
-                               : k_edges<false, false, false, true, true>;
+    auto kern = ctx->hash_rule ? k_edges<false, false, true, true, MODE>
+                               : k_edges<false, false, false, true, MODE>;
     PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const uint64_t nnz = 2 * ctx->m;
     const unsigned gl = pc_grid(ctx, (nnz + 31) / 32 * 32, EDGE_THREADS, 8);
     kern<<<gl, EDGE_THREADS, smem, ctx->stream>>>(
         ctx->off.as<uint64_t>(), reinterpret_cast<const uint64_t *>(ctx->nbr.p),
         ctx->crow.as<uint32_t>(), nnz, ctx->K, ctx->t32, ctx->d_shr.as<uint32_t>(),
-        ctx->d_tab.as<uint16_t>(), B, 0, B, P, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), rec, MW);
+        ctx->d_tab.as<uint16_t>(), B, 0, B, L, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), rec, MW);
   } else {
     const bool pe = ctx->pmodel != PACIM_P_CONST;
-    auto kern = pe ? (ctx->hash_rule ? k_edges<true, false, true, false, true>
-                                     : k_edges<true, false, false, false, true>)
-                   : (ctx->hash_rule ? k_edges<false, false, true, false, true>
-                                     : k_edges<false, false, false, false, true>);
+    auto kern = pe ? (ctx->hash_rule ? k_edges<true, false, true, false, MODE>
+                                     : k_edges<true, false, false, false, MODE>)
+                   : (ctx->hash_rule ? k_edges<false, false, true, false, MODE>
+                                     : k_edges<false, false, false, false, MODE>);
     PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const unsigned g = pc_grid(ctx, (ctx->m + 31) / 32 * 32, EDGE_THREADS, 8);
     kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
         ctx->keys.as<uint64_t>(), ctx->ckeys.as<uint64_t>(),
         pe ? ctx->tm1.as<uint32_t>() : nullptr, ctx->m, ctx->K, pe ? ctx->toff() : ctx->t32,
-        ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, 0, B, P, ctr + 4, Hla{},
+        ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, 0, B, L, ctr + 4, Hla{},
         ctx->d_hr64.as<uint64_t>(), rec, MW);
   }
   PC_CHECK_LAUNCH();
   ctx->launches++;
+}
+
+// The union pass over the compact store (store_cs.cu): every upper edge,
+// its live sketches, unions of the entries' P words.  ctr[4] += live pairs.
+void pc_cs_edges(pacim_ctx *ctx, uint32_t *E, const uint2 *rec, uint32_t MW,
+                 unsigned long long *ctr) {
+  cs_edges<1>(ctx, E, rec, MW, ctr);
+}
+
+// The mask pass over the upper edges: the live slots of every edge set in
+// both endpoints' row masks (rec.y words).  ctr[5] += live pairs.
+void pc_cs_mask_edges(pacim_ctx *ctx, uint32_t *rec_words, uint32_t MW,
+                      unsigned long long *ctr) {
+  cs_edges<2>(ctx, rec_words, nullptr, MW, ctr + 1);
 }
 
 // Slot windows of the store for this build.  With a constant

@@ -550,7 +550,8 @@ static bool dist_select_fast(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_
 void pc_dist_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num) {
   PC_REQUIRE(pc_dist_active(ctx), PACIM_ESTATE,
              "sharded build: pacim_init_comm(rank, world) with the build's shard first");
-  PC_REQUIRE(ctx->selector == 0, PACIM_ENOTIMPL, "sharded select: incremental selector only");
+  PC_REQUIRE(ctx->selector == 0 || ctx->selector == 3, PACIM_ENOTIMPL,
+             "sharded select: the incremental selector only (auto selects it)");
   ctx->stats.select_dist_replays = 0;
   if (ctx->cs && !getenv("PACIM_DIST_ROBUST")) {
     if (dist_select_fast(ctx, k, seeds, gain_num)) return;

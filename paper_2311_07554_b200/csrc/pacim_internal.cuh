@@ -242,8 +242,6 @@ struct pacim_ctx {
   DevBuf cs_vid;            // u32[total]: vertex of an entry
   DevBuf cs_diag;           // u64 selection diagnostics
   DevBuf cs_cnt;            // build scratch: row counts and their scan
-  DevBuf cs_roff, cs_rcrow; // store-row CSR offsets, row of CSR entry 32 c (mask pass)
-  uint64_t cs_rows_gen = ~0ull;  // graph_gen cs_roff / cs_rcrow were built for
   uint64_t cs_pref_gen = ~0ull;  // store decision of the last build of graph_gen ...
   uint32_t cs_pref_B = 0;        // ... with this many slots:
   bool cs_pref_dense = false;    // too dense for the compact store
@@ -323,6 +321,7 @@ void pc_generate(pacim_ctx *ctx, int kind, const uint64_t *params, int nparams,
 void pc_build(pacim_ctx *ctx);
 void pc_cs_edges(pacim_ctx *ctx, uint32_t *P, const uint2 *rec, uint32_t MW,
                  unsigned long long *ctr);
+void pc_cs_mask_edges(pacim_ctx *ctx, uint32_t *rec_words, uint32_t MW, unsigned long long *ctr);
 // dist.cu: NCCL sharding
 void pc_nccl_unique_id(void *out);
 void pc_init_comm(pacim_ctx *ctx, int rank, int world, const void *id);
@@ -435,6 +434,8 @@ void pc_get_center_sketch(pacim_ctx *ctx, uint32_t slot, uint32_t *label, uint32
 void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
                int64_t *sigma_num);
 void pc_select_reset(pacim_ctx *ctx);
+void pc_select_wintree_dense(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
+                             int64_t *sigma_num);
 void pc_select_lazy(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
                     int64_t *sigma_num);
 void pc_cover_local(pacim_ctx *ctx, uint32_t s, int64_t *d_delta,

@@ -1261,6 +1261,149 @@ __global__ void __launch_bounds__(SEL_THREADS) k_lazy_best(const long long *delt
   if (threadIdx.x == 0) part[blockIdx.x] = x;
 }
 
+// Win-Tree selector (NEXT f2) on the dense store: the same
+// level-synchronous FindMax in one block as store_cs.cu's k_cs_wintree, with
+// the fresh marginal gain read from the vertex-major store (k_lazy_eval's
+// rule) and MarkSeed by the covered bit of the root slots.
+constexpr int WT_THREADS = 1024;
+
+__device__ __forceinline__ uint32_t wt_win(const long long *key, uint32_t a, uint32_t b) {
+  if (a == NONE) return b;
+  if (b == NONE) return a;
+  const long long ka = key[a], kb = key[b];
+  return (ka > kb || (ka == kb && a < b)) ? a : b;
+}
+
+__device__ long long dense_eval(const Sel &S, uint32_t v) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t row = S.cid[v];
+  if (row == NONE) return S.B;  // isolated: a singleton in every sketch
+  long long g = 0;
+  for (uint32_t j = lane; j < S.B; j += 32) {
+    const uint32_t sv = __ldcg(S.L + pc_addr(S.smap, S.nr, row, j));
+    if (sv == (PACIM_HIGH | 1u)) {
+      g += 1;  // {v}: never covered while v is not a seed
+      continue;
+    }
+    const uint32_t rv = (sv & PACIM_HIGH) ? sv : __ldcg(S.L + pc_addr(S.smap, S.nr, sv, j));
+    if (!(rv & COV)) g += rv & SIZE;
+  }
+  for (int d = 16; d; d >>= 1) g += __shfl_xor_sync(0xffffffffu, g, d);
+  return g;
+}
+
+struct WTd {
+  uint32_t *T;
+  uint32_t N;
+  long long *key;
+  uint32_t *stamp, *F, *Ev, *seeds;
+  long long *gain_num;
+  unsigned long long *evals;
+};
+
+__global__ void __launch_bounds__(WT_THREADS, 1) k_wintree_dense(Sel S, WTd W, uint32_t k) {
+  __shared__ uint32_t lvl_a[40], lvl_b[40];
+  __shared__ uint32_t nf, ne;
+  __shared__ Best sh[33];
+  __shared__ Best best;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  unsigned long long evals = 0, nodes = 0;
+  for (uint32_t step = 0; step < k; step++) {
+    if (threadIdx.x == 0) {
+      W.F[0] = 1;
+      lvl_a[0] = 0;
+      lvl_b[0] = 1;
+      nf = 1;
+      best = Best{LLONG_MIN, NONE};
+    }
+    __syncthreads();
+    uint32_t L = 0;
+    for (;; L++) {
+      const uint32_t a = lvl_a[L], b = lvl_b[L];
+      if (a == b) break;
+      if (threadIdx.x == 0) ne = 0;
+      __syncthreads();
+      const Best cur = best;
+      for (uint32_t i = a + threadIdx.x; i < b; i += blockDim.x) {
+        const uint32_t t = W.F[i];
+        const uint32_t id = W.T[t];
+        if (id == NONE) continue;
+        if (W.stamp[id] != step + 1) {
+          const long long kv = W.key[id];
+          if (!better(kv, id, cur.g, cur.v)) continue;
+          W.stamp[id] = step + 1;
+          W.Ev[atomicAdd(&ne, 1u)] = id;
+        }
+        if (t < W.N) {
+          const uint32_t at = atomicAdd(&nf, 2u);
+          W.F[at] = 2 * t;
+          W.F[at + 1] = 2 * t + 1;
+        }
+      }
+      __syncthreads();
+      Best mine{LLONG_MIN, NONE};
+      for (uint32_t q = wid; q < ne; q += WT_THREADS / 32) {
+        const uint32_t v = W.Ev[q];
+        const long long g = dense_eval(S, v);
+        if (lane == 0) W.key[v] = g;
+        if (better(g, v, mine.g, mine.v)) mine = Best{g, v};
+      }
+      evals += ne;
+      nodes += b - a;
+      Best lb = block_best(mine, sh);
+      if (threadIdx.x == 0) {
+        if (better(lb.g, lb.v, best.g, best.v)) best = lb;
+        lvl_a[L + 1] = b;
+        lvl_b[L + 1] = nf;
+      }
+      __syncthreads();
+    }
+    const uint32_t s = best.v;
+    const long long g = best.g;
+    const uint32_t srow = S.cid[s];
+    if (srow != NONE)
+      for (uint32_t j = threadIdx.x; j < S.B; j += blockDim.x) {
+        const uint32_t sl = S.L[pc_addr(S.smap, S.nr, srow, j)];
+        if (sl == (PACIM_HIGH | 1u)) continue;
+        const uint32_t root = (sl & PACIM_HIGH) ? srow : sl;
+        const size_t ra = pc_addr(S.smap, S.nr, root, j);
+        if (!(atomicOr(S.L + ra, COV) & COV)) {
+          const unsigned long long at = atomicAdd(S.cov_cnt, 1ull);
+          if (at < S.cov_cap) S.cov_list[at] = ra;
+        }
+      }
+    if (threadIdx.x == 0) {
+      W.key[s] = -1;
+      W.seeds[step] = s;
+      W.gain_num[step] = g;
+    }
+    __syncthreads();
+    for (int l = (int)L - 1; l >= 0; l--) {
+      for (uint32_t i = lvl_a[l] + threadIdx.x; i < lvl_b[l]; i += blockDim.x) {
+        const uint32_t t = W.F[i];
+        if (t < W.N) W.T[t] = wt_win(W.key, W.T[2 * t], W.T[2 * t + 1]);
+      }
+      __syncthreads();
+    }
+  }
+  if (threadIdx.x == 0) {
+    W.evals[0] = evals;
+    W.evals[1] = nodes;
+  }
+}
+
+__global__ void k_wtd_leaves(uint32_t *T, uint32_t N, uint32_t n) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < N;
+       i += (size_t)gridDim.x * blockDim.x)
+    T[N + i] = i < n ? (uint32_t)i : NONE;
+}
+
+__global__ void k_wtd_level(uint32_t *T, const long long *key, uint32_t lo, uint32_t hi) {
+  for (size_t t = lo + (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < hi;
+       t += (size_t)gridDim.x * blockDim.x)
+    T[t] = wt_win(key, T[2 * t], T[2 * t + 1]);
+}
+
 // empty ring: slot i expects ticket i
 __global__ void k_ring_init(Item *ring, unsigned long long Q) {
   for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < Q;
@@ -1555,6 +1698,8 @@ void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
   ctx->stats.kernel_launches_select = 2;
   read_diag(ctx, S);
   ctx->sel_par = (par0 + k) & 1;
+  ctx->stats.select_evaluations = 0;  // the lazy selectors' counters
+  ctx->stats.select_eval_rounds = 0;
   long long run = 0;
   bool ok = true;
   for (uint32_t i = 0; i < k; i++) {
@@ -1795,4 +1940,74 @@ void pc_select_lazy(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_n
   ctx->stats.select_evaluations = evals;
   ctx->stats.select_eval_rounds = rounds;
   ctx->stats.kernel_launches_select = (uint32_t)(k * 3 + rounds * 2);
+}
+
+// NEXT f2: the Win-Tree selector on the dense store (selector 2)
+void pc_select_wintree_dense(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
+                             int64_t *sigma_num) {
+  const uint32_t n = ctx->n;
+  uint32_t N = 1, depth = 0;
+  while (N < n) {
+    N <<= 1;
+    depth++;
+  }
+  if (k > ctx->sel_k_cap) {
+    if (ctx->sel_list_valid) {
+      Sel old = make_sel(ctx, nullptr);
+      uncover(ctx, old);
+    }
+    ctx->sel_k_cap = k;
+    ctx->sel_list_valid = false;
+  }
+  pc_ensure(ctx, ctx->gain, (size_t)n * 8);
+  Sel S = make_sel(ctx, ctx->gain.as<long long>());
+  TmpBuf wb(ctx);
+  pc_ensure(ctx, wb, (size_t)2 * N * 4 + (size_t)n * 4 + (size_t)2 * N * 4 + (size_t)N * 4 +
+                         (size_t)k * 12 + 64);
+  WTd W;
+  W.T = wb.as<uint32_t>();
+  W.stamp = W.T + 2 * (size_t)N;
+  W.F = W.stamp + n;
+  W.Ev = W.F + 2 * (size_t)N;
+  W.gain_num = reinterpret_cast<long long *>(
+      (reinterpret_cast<uintptr_t>(W.Ev + N) + 7) & ~(uintptr_t)7);
+  W.seeds = reinterpret_cast<uint32_t *>(W.gain_num + k);
+  W.evals = reinterpret_cast<unsigned long long *>(
+      (reinterpret_cast<uintptr_t>(W.seeds + k) + 7) & ~(uintptr_t)7);
+  W.N = N;
+  W.key = ctx->gain.as<long long>();
+  cudaEvent_t e0, e1;
+  PC_CUDA(cudaEventCreate(&e0));
+  PC_CUDA(cudaEventCreate(&e1));
+  PC_CUDA(cudaEventRecord(e0, ctx->stream));
+  uncover(ctx, S);
+  PC_CUDA(cudaMemcpyAsync(W.key, ctx->gain0.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
+  PC_CUDA(cudaMemsetAsync(W.stamp, 0, (size_t)n * 4, ctx->stream));
+  k_wtd_leaves<<<pc_grid(ctx, N, 256), 256, 0, ctx->stream>>>(W.T, N, n);
+  for (uint32_t lo = N >> 1; lo >= 1; lo >>= 1)
+    k_wtd_level<<<pc_grid(ctx, lo, 256), 256, 0, ctx->stream>>>(W.T, W.key, lo, 2 * lo);
+  PC_CHECK_LAUNCH();
+  k_wintree_dense<<<1, WT_THREADS, 0, ctx->stream>>>(S, W, k);
+  PC_CHECK_LAUNCH();
+  PC_CUDA(cudaEventRecord(e1, ctx->stream));
+  std::vector<long long> hg(k);
+  unsigned long long ev[2];
+  PC_CUDA(cudaMemcpyAsync(seeds, W.seeds, (size_t)k * 4, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaMemcpyAsync(hg.data(), W.gain_num, (size_t)k * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaMemcpyAsync(ev, W.evals, 16, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  ctx->stats.t_select_ms = ms;
+  ctx->stats.select_evaluations = ev[0];
+  ctx->stats.select_eval_rounds = ev[1];
+  ctx->stats.kernel_launches_select = depth + 2;
+  long long run = 0;
+  for (uint32_t i = 0; i < k; i++) {
+    gain_num[i] = hg[i];
+    run += hg[i];
+    sigma_num[i] = run;
+  }
 }

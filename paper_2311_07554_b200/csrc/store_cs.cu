@@ -26,8 +26,9 @@
 // vector pass over the build's per-vertex hot sums (when a step covers
 // exactly the hub's CCs) or one pass over the entries.
 //
-// Build: k_cs_mask (lane per CSR entry: the live slots of its edge, OR-ed into
-// the row's mask) -> counts, scan -> k_cs_rec -> E = {HIGH|1, NONE} ->
+// Build: the mask pass (k_edges<…, 2> over the upper edges: every live (edge,
+// sketch) sets the slot bit in both endpoints' row masks) -> counts, scan ->
+// k_cs_rec -> E = {HIGH|1, NONE} ->
 // k_edges<CS> (build.cu: the unions, on entries) -> k_cs_compress (full
 // compression, CC sizes, member lists) -> k_cs_gain (gain0 = sum_r |C_r(v)|,
 // hot sums, vid).
@@ -56,60 +57,14 @@ constexpr int CS_THREADS = 256;
 constexpr int SEL_THREADS = 512;
 constexpr uint32_t MAX_CHUNKS = 4096;
 constexpr uint32_t LIST_T = 4096;     // longest member list walked in a cover step
+constexpr uint32_t WBUF = 128;        // member entries a warp buffers per walk round
 
 // ---------------------------------------------------------------- helpers
-// Row of entry e (in [base, base + 32)) for a warp over 32 consecutive
-// entries of a CSR whose rows are given by offsets roff (u64) and the chunk
-// table crow (row of entry 32 c): lane L holds the end of row r0 + L, a
-// 5-step shuffle search finds each lane's row; rows beyond r0 + 31 (a run of
-// empty rows) by a scan.  All 32 lanes call it.
-__device__ __forceinline__ uint32_t warp_row(const uint64_t *roff, uint32_t nrows,
-                                             const uint32_t *crow, uint64_t base, uint64_t e) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t r0 = crow[base >> 5];
-  const uint64_t endL = (r0 + lane < nrows) ? roff[r0 + lane + 1] : ~0ull;
-  uint32_t cnt = 0;  // rows r0 + L with end <= e
-#pragma unroll
-  for (int st = 16; st; st >>= 1) {
-    const uint64_t o = __shfl_sync(FULL, endL, cnt + st - 1);
-    if (o <= e) cnt += st;
-  }
-  if (cnt == 31 && __shfl_sync(FULL, endL, 31) <= e) cnt = 32;
-  uint32_t r = r0 + cnt;
-  while (r < nrows && roff[r + 1] <= e) r++;  // more than 31 empty rows before e
-  return r;
-}
-
 __device__ __forceinline__ uint32_t entry_row(const uint32_t *soff, const uint32_t *ecrow,
                                               uint64_t e) {
   uint32_t r = ecrow[e >> 5];
   while (e >= soff[r + 1]) r++;
   return r;
-}
-
-// candidate slots [lo, hi) of an edge (R2 candidate enumeration, exact: the
-// top clz(T-1) bits of hash(r) and hash(e) agree for every live slot; the
-// same table lookup as k_edges so both passes see the same live sets)
-__device__ __forceinline__ void cand_range(uint32_t he, uint64_t T, const uint16_t *tab,
-                                           uint32_t B, bool decor, uint32_t &lo, uint32_t &hi) {
-  lo = hi = 0;
-  if (T == 0) return;
-  if (decor) {
-    hi = B;
-    return;
-  }
-  const uint32_t w = __clz((uint32_t)(T - 1));
-  if (w >= PACIM_TB) {
-    const uint32_t p = he >> (32 - PACIM_TB);
-    lo = tab[p];
-    hi = tab[p + 1];
-  } else if (w == 0) {
-    hi = B;
-  } else {
-    const uint32_t p = (he >> (32 - w)) << (PACIM_TB - w);
-    lo = tab[p];
-    hi = tab[p + (1u << (PACIM_TB - w))];
-  }
 }
 
 // union-find on the P words of E (stride 2)
@@ -175,132 +130,6 @@ __device__ __forceinline__ int find_sorted(const uint32_t *a, uint32_t n, uint32
     else hi = mid;
   }
   return (lo < n && a[lo] == x) ? (int)lo : -1;
-}
-
-// ------------------------------------------------------- row tables
-// store-row CSR offsets and the row of every 32nd CSR entry (mask pass)
-__global__ void k_cs_roff(const uint64_t *off, const uint32_t *rmap, uint32_t nr, uint64_t nnz,
-                          uint64_t *roff) {
-  for (size_t r = (size_t)blockIdx.x * blockDim.x + threadIdx.x; r <= nr;
-       r += (size_t)gridDim.x * blockDim.x)
-    roff[r] = r < nr ? off[rmap ? rmap[r] : r] : nnz;
-}
-
-__global__ void k_cs_rcrow(const uint64_t *roff, uint32_t nr, uint32_t *rcrow) {
-  for (size_t r = (size_t)blockIdx.x * blockDim.x + threadIdx.x; r < nr;
-       r += (size_t)gridDim.x * blockDim.x) {
-    const uint64_t a = roff[r], b = roff[r + 1];
-    for (uint64_t c = (a + 31) >> 5; (c << 5) < b; c++) rcrow[c] = (uint32_t)r;
-  }
-}
-
-// ------------------------------------------------------------ k_cs_mask
-// Lane per CSR entry (u, w) (balanced whatever the degrees): the live slots
-// of edge {u, w} (P:3-4 / R3; per-edge T32 for WIC / Uniform, R4 / R19; R20)
-// OR-ed into u's row mask.  As in k_edges, a warp flattens the candidate
-// (entry, slot) pairs of its 32 entries into rounds of 32 tests (no lane
-// waits on another's 256-slot range: WIC gives leaf-leaf edges T = 2^32);
-// a range whose candidates are all live (T = 2^32, or exactly the bucket
-// width) is set without tests.  Live bits gather in a per-warp shared
-// buffer, then the lanes of one row combine with one redux per word.
-constexpr int MASK_WARPS = CS_THREADS / 32;
-template <bool PERE, bool DECOR>
-__global__ void __launch_bounds__(CS_THREADS) k_cs_mask(
-    const uint64_t *__restrict__ roff, const uint32_t *__restrict__ rcrow, uint32_t nr,
-    const uint32_t *__restrict__ rmap, const uint32_t *__restrict__ nbr, uint64_t nnz,
-    const uint32_t *__restrict__ tcsr, uint32_t toff, uint64_t t32, uint64_t K,
-    const uint32_t *__restrict__ g_shr, const uint16_t *__restrict__ g_tab,
-    const uint64_t *__restrict__ hr64, uint32_t B, uint32_t MW, uint32_t *rec) {
-  extern __shared__ uint32_t sm[];
-  uint32_t *shr = sm;
-  uint16_t *tab = reinterpret_cast<uint16_t *>(sm + B);
-  __shared__ uint32_t w_lo[MASK_WARPS][32], w_he[MASK_WARPS][32], w_own[MASK_WARPS][32];
-  __shared__ uint64_t w_T[PERE ? MASK_WARPS : 1][32], w_he64[DECOR ? MASK_WARPS : 1][32];
-  __shared__ uint32_t wb[MASK_WARPS][32][MAXW];  // live bits per entry of the warp
-  for (uint32_t i = threadIdx.x; i < B; i += blockDim.x) shr[i] = g_shr[i];
-  for (uint32_t i = threadIdx.x; i <= (1u << PACIM_TB); i += blockDim.x) tab[i] = g_tab[i];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int q = 0; q < (int)MAXW; q++) wb[wid][lane][q] = 0;
-  __syncthreads();
-  const size_t stride = (size_t)gridDim.x * blockDim.x;
-  for (size_t base = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) & ~(size_t)31; base < nnz;
-       base += stride) {
-    const uint64_t e = base + lane;
-    const uint32_t rw = warp_row(roff, nr, rcrow, base, e < nnz ? e : nnz - 1);
-    uint32_t row = NONE, cnt = 0, lo = 0, hi = 0, he = 0;
-    uint64_t T = t32, he64 = 0;
-    if (e < nnz) {
-      row = rw;
-      const uint32_t u = rmap ? rmap[row] : row, w = nbr[e];
-      if (PERE) T = (uint64_t)tcsr[e] + toff;
-      const uint64_t a = u < w ? u : w, b = u < w ? w : u;
-      he64 = pc_mix64(((a << 32) | b) ^ K);
-      he = (uint32_t)(he64 >> 32);
-      cand_range(he, T, tab, B, DECOR, lo, hi);
-      // every candidate live: T = 2^32, or T is exactly the bucket width and
-      // the table resolves all its bits
-      const uint32_t wb_ = T ? __clz((uint32_t)(T - 1)) : 0;
-      const bool all = T >= (1ull << 32) ||
-                       (!DECOR && wb_ >= 1 && wb_ <= PACIM_TB && T == (1ull << (32 - wb_)));
-      if (all) {
-        for (uint32_t q = lo >> 5; q < MW && 32 * q < hi; q++) {
-          uint32_t m = 0xFFFFFFFFu;
-          if (32 * q < lo) m &= 0xFFFFFFFFu << (lo & 31);
-          if (32 * q + 32 > hi) m &= 0xFFFFFFFFu >> (32 - (hi & 31));
-          wb[wid][lane][q] |= m;
-        }
-      } else {
-        cnt = hi - lo;
-      }
-    }
-    // flattened candidate tests (the k_edges scheme)
-    const uint32_t nz = __ballot_sync(FULL, cnt > 0);
-    uint32_t inc = cnt;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t y = __shfl_up_sync(FULL, inc, d);
-      if (lane >= d) inc += y;
-    }
-    const uint32_t pre = inc - cnt;
-    const uint32_t total = __shfl_sync(FULL, inc, 31);
-    if (cnt) {
-      const uint32_t k = __popc(nz & ((1u << lane) - 1));
-      w_lo[wid][k] = lo - pre;
-      w_he[wid][k] = he;
-      w_own[wid][k] = lane;
-      if (PERE) w_T[PERE ? wid : 0][k] = T;
-      if (DECOR) w_he64[DECOR ? wid : 0][k] = he64;
-    }
-    __syncwarp();
-    for (uint32_t c0 = 0; c0 < total; c0 += 32) {
-      const uint32_t idx = c0 + lane;
-      const uint32_t smask =
-          __reduce_or_sync(FULL, (cnt && pre >= c0 && pre < c0 + 32) ? 1u << (pre - c0) : 0u);
-      const uint32_t before = __popc(__ballot_sync(FULL, cnt && pre < c0));
-      if (idx < total) {
-        const uint32_t a = before + __popc(smask & (0xffffffffu >> (31 - lane))) - 1;
-        const uint32_t j = w_lo[wid][a] + idx;
-        const uint64_t Ta = PERE ? w_T[PERE ? wid : 0][a] : t32;
-        const bool lv = DECOR ? (pc_mix64(__ldg(hr64 + j) ^ w_he64[DECOR ? wid : 0][a]) >> 32) < Ta
-                              : (uint64_t)(shr[j] ^ w_he[wid][a]) < Ta;
-        if (lv) atomicOr(&wb[wid][w_own[wid][a]][j >> 5], 1u << (j & 31));
-      }
-    }
-    __syncwarp();
-    const unsigned peers = __match_any_sync(FULL, row);
-    const int leader = __ffs(peers) - 1;
-#pragma unroll
-    for (int q = 0; q < (int)MAXW; q++) {
-      if ((uint32_t)q >= MW) break;
-      const uint32_t mine = wb[wid][lane][q];
-      wb[wid][lane][q] = 0;
-      if (!__any_sync(FULL, mine)) continue;
-      const uint32_t x = __reduce_or_sync(peers, mine);
-      if (lane == leader && x && row != NONE) atomicOr(rec + ((size_t)row * MW + q) * 2 + 1, x);
-    }
-    __syncwarp();
-  }
 }
 
 // entries per row (set bits), u64 for the scan; cnt[nr] = 0
@@ -619,6 +448,7 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) k_cs_select(CSel S0, CSelOut O
   CSel S = S0;
   __shared__ Best sh[33];
   __shared__ uint32_t croot[256], cdel[256], csort[256], dsort[256];
+  __shared__ uint32_t wbuf[SEL_THREADS / 32][WBUF];
   const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t nth = (size_t)gridDim.x * blockDim.x;
   const size_t gwarp = tid >> 5, nwarps = nth >> 5;
@@ -684,34 +514,45 @@ __global__ void __launch_bounds__(SEL_THREADS, 1) k_cs_select(CSel S0, CSelOut O
         mark_dirty(S, s >> S.csh);
       }
     }
-    // ---- B: MarkSeed per slot; the members of each newly covered CC lose |C|
-    //          (a lane per slot: the walks of a step's CCs run side by side)
+    // ---- B: MarkSeed per slot (a warp per slot); the members of each newly
+    //          covered CC lose |C|: lane 0 walks the CC's list (one dependent
+    //          load per hop) into a shared buffer, the warp applies the updates
     {
       unsigned long long dsum = 0, upd = 0;
-      for (size_t j = tid; j < S.B; j += nth) {
-        uint32_t mr = NONE;
-        const uint32_t d = cs_cover(S, srow, (uint32_t)j, &mr);
+      uint32_t *buf = wbuf[threadIdx.x >> 5];
+      for (size_t j = gwarp; j < S.B; j += nwarps) {
+        uint32_t d = 0, mr = NONE;
+        if (lane == 0) d = cs_cover(S, srow, (uint32_t)j, &mr);
+        d = __shfl_sync(FULL, d, 0);
+        mr = __shfl_sync(FULL, mr, 0);
         dsum += d;
-        if (mr != NONE) {  // walk the list: the root, then its linked members
-          uint32_t e = mr;
-          for (uint32_t t = 0; t < d && e != NONE; t++, e = __ldcg(S.E + 2 * (size_t)e + 1)) {
-            const uint32_t v = __ldg(S.vid + e);
+        if (mr == NONE) continue;
+        upd += d;
+        uint32_t e = mr, left = d;
+        while (left) {
+          uint32_t cnt = 0;
+          if (lane == 0) {
+            for (; cnt < WBUF && left && e != NONE; cnt++, left--) {
+              buf[cnt] = e;
+              e = __ldcg(S.E + 2 * (size_t)e + 1);
+            }
+            if (e == NONE) left = 0;
+          }
+          cnt = __shfl_sync(FULL, cnt, 0);
+          left = __shfl_sync(FULL, left, 0);
+          __syncwarp();
+          for (uint32_t t = lane; t < cnt; t += 32) {
+            const uint32_t v = __ldg(S.vid + buf[t]);
             if (v != s) sub_gain(S, v, d);
           }
-          upd += d;
+          __syncwarp();
         }
-      }
-      for (int q = 16; q; q >>= 1) {
-        dsum += __shfl_xor_sync(FULL, dsum, q);
-        upd += __shfl_xor_sync(FULL, upd, q);
       }
       if (lane == 0) {
         if (dsum) atomicAdd(reinterpret_cast<unsigned long long *>(&O.gain_num[step]), dsum);
         if (upd) atomicAdd(S.diag + CD_UPD, upd);
       }
     }
-    (void)gwarp;
-    (void)nwarps;
     grid.sync();
     // ---- dense: list-less CCs covered this step
     if (__ldcg(S.dense + S.par)) {
@@ -1015,6 +856,17 @@ bool pc_cs_build(pacim_ctx *ctx) {
     return false;  // the slot-window layout is a dense-store experiment
   }
   if (B > 256 || nr == 0 || ctx->compressed) return false;
+  // The store: one GPU -> the dense vertex-major store (its build is faster:
+  // the compact store adds a mask pass and an indirection per union, c4 r02:
+  // 81 vs 58 ms) unless it does not fit; a sharded build -> the compact store
+  // (the fast NCCL select walks its member lists; the dense store would need a
+  // dense all-reduce per step).  PACIM_STORE = compact | dense forces one.
+  if (!force && ctx->world == 1 && !pc_dist_active(ctx)) {
+    size_t fr = 0, tot = 0;
+    pc_mem_info(ctx, &fr, &tot);
+    fr += ctx->L.bytes;  // an earlier dense store is reused
+    if ((size_t)nr * B * 4 <= fr / 2) return false;
+  }
   // an earlier build of this graph with these many slots found the sketches
   // too dense for the compact store (the mask pass is not repeated)
   if (!force && ctx->cs_pref_gen == ctx->graph_gen && ctx->cs_pref_B == B && ctx->cs_pref_dense)
@@ -1040,37 +892,12 @@ bool pc_cs_build(pacim_ctx *ctx) {
     }
   } cleanup{marks};
   const uint64_t nnz = 2 * ctx->m;
-  // store-row CSR tables of this graph (once per graph load)
-  if (ctx->cs_rows_gen != ctx->graph_gen) {
-    pc_ensure(ctx, ctx->cs_roff, ((size_t)nr + 1) * 8);
-    pc_ensure(ctx, ctx->cs_rcrow, (nnz / 32 + 2) * 4);
-    k_cs_roff<<<pc_grid(ctx, nr + 1, 256), 256, 0, ctx->stream>>>(
-        ctx->off.as<uint64_t>(), ctx->lean ? nullptr : ctx->rmap.as<uint32_t>(), nr, nnz,
-        ctx->cs_roff.as<uint64_t>());
-    k_cs_rcrow<<<pc_grid(ctx, nr, 256), 256, 0, ctx->stream>>>(ctx->cs_roff.as<uint64_t>(), nr,
-                                                               ctx->cs_rcrow.as<uint32_t>());
-    PC_CHECK_LAUNCH();
-    ctx->cs_rows_gen = ctx->graph_gen;
-  }
   mark("start");
   // ---- masks (the rec array, .y words)
   pc_ensure(ctx, ctx->cs_rec, (size_t)nr * MW * 8);
   PC_CUDA(cudaMemsetAsync(ctx->cs_rec.p, 0, (size_t)nr * MW * 8, ctx->stream));
-  if (nnz) {
-    const size_t smem = B * 4 + ((1u << PACIM_TB) + 1) * 2;
-    const bool pe = ctx->pmodel != PACIM_P_CONST;
-    auto kern = pe ? (ctx->hash_rule ? k_cs_mask<true, true> : k_cs_mask<true, false>)
-                   : (ctx->hash_rule ? k_cs_mask<false, true> : k_cs_mask<false, false>);
-    PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<pc_grid(ctx, (nnz + 31) / 32 * 32, CS_THREADS, 8), CS_THREADS, smem, ctx->stream>>>(
-        ctx->cs_roff.as<uint64_t>(), ctx->cs_rcrow.as<uint32_t>(), nr,
-        ctx->lean ? nullptr : ctx->rmap.as<uint32_t>(), ctx->nbr.as<uint32_t>(), nnz,
-        pe ? ctx->tcsr.as<uint32_t>() : nullptr, ctx->toff(), ctx->t32, ctx->K,
-        ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), ctx->d_hr64.as<uint64_t>(), B, MW,
-        ctx->cs_rec.as<uint32_t>());
-    PC_CHECK_LAUNCH();
-    ctx->launches++;
-  }
+  if (nnz)  // the upper edges (the k_edges scheme): both endpoints' bits per live pair
+    pc_cs_mask_edges(ctx, ctx->cs_rec.as<uint32_t>(), MW, ctr + 8);
   mark("mask");
   // ---- counts -> entry offsets (build scratch kept by the ctx)
   pc_ensure(ctx, ctx->cs_cnt, 2 * ((size_t)nr + 1) * 8);
@@ -1083,12 +910,9 @@ bool pc_cs_build(pacim_ctx *ctx) {
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
   ctx->launches += 2;
   mark("scan");
-  // the compact store pays when most (row, slot) pairs are singletons: its
-  // mask pass and per-entry indirection cost more than the dense passes save
-  // above ~15 % non-singleton pairs (measured: c4 9.8 % -> compact, c2 23 %
-  // -> dense); PACIM_CS_DENSITY overrides, PACIM_STORE=compact forces (up to 50 %)
-  const double dmax = force ? 0.5
-                            : (getenv("PACIM_CS_DENSITY") ? atof(getenv("PACIM_CS_DENSITY")) : 0.15);
+  // above half non-singleton pairs (c3: p = 1/2 on a grid) the compact store
+  // is larger than the dense one
+  const double dmax = getenv("PACIM_CS_DENSITY") ? atof(getenv("PACIM_CS_DENSITY")) : 0.5;
   const bool dense = total >= (1ull << 31) || (double)total > dmax * (double)nr * B;
   ctx->cs_pref_gen = ctx->graph_gen;
   ctx->cs_pref_B = B;
@@ -1349,6 +1173,8 @@ void pc_cs_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num
   ctx->stats.select_dense_steps = d[CD_DENSE];
   ctx->stats.select_hotsum_steps = d[CD_HOT];
   ctx->stats.select_celf_evaluations = d[CD_CELF];
+  ctx->stats.select_evaluations = 0;  // the lazy selectors' counters
+  ctx->stats.select_eval_rounds = 0;
   ctx->stats.select_bfs_visits = 0;
   ctx->stats.select_warp_slots = ctx->stats.select_deferred_slots = 0;
   ctx->stats.select_row_items = ctx->stats.select_chunk_items = 0;

@@ -100,13 +100,16 @@ def test_tiny_corpus_parity(orc, ctx, i):
     full_parity(orc, ctx, g, model, t32, R, 1000 + i, min(k, g.n))
 
 
-@pytest.mark.parametrize("i", [0, 1, 2, 3, 4, 6, 7, 8, 10, 11, 12])
+@pytest.mark.parametrize("i", range(len(CASES)))
 def test_tiny_corpus_parity_compact_store(orc, ctx, i, monkeypatch):
-    """The compact store forced (PACIM_STORE=compact: up to 50 % non-singleton
-    (vertex, sketch) pairs; by default it is taken below 15 %)."""
+    """The compact store forced (PACIM_STORE=compact; by default a one-GPU
+    build takes the dense store when it fits, a sharded build the compact
+    one): the same oracle parity.  Sketches with more than half of their
+    (vertex, sketch) pairs non-singleton keep the dense store."""
     monkeypatch.setenv("PACIM_STORE", "compact")
     test_tiny_corpus_parity(orc, ctx, i)
-    assert ctx.pacim_get_stats()["store"] == 1
+    st = ctx.pacim_get_stats()
+    assert st["store"] == 1 or st["nnonsingle"] > 0.5 * st["rows"] * st["R_local"]
 
 
 @pytest.mark.parametrize("i", range(len(CASES)))
@@ -730,12 +733,13 @@ def test_dist_select_world1_compressed(orc, pc, monkeypatch):
 from tests.celf_ref import celf_reevaluations  # noqa: E402
 
 
+@pytest.mark.parametrize("store", ["compact", "dense"])
 @pytest.mark.parametrize("i", [0, 2, 3, 7, 8, 10, 12])
-def test_wintree_selector_equals_oracle(orc, ctx, i, monkeypatch):
+def test_wintree_selector_equals_oracle(orc, ctx, i, store, monkeypatch):
     """NEXT f2: the Win-Tree selector returns GeneralGreedy's
-    sequence (R17); its re-evaluations are at least CELF's lower bound of
-    one per step from step 2 and at most k * n."""
-    monkeypatch.setenv("PACIM_STORE", "compact")
+    sequence (R17) on both stores; its re-evaluations are at least one per
+    step and at most k * n."""
+    monkeypatch.setenv("PACIM_STORE", store)
     from oracle.oracle import Graph
     build_fn, p, R, k = CASES[i]
     off, nbr = build_fn()
@@ -776,3 +780,25 @@ def test_celf_count_equals_celf(orc, ctx, i, monkeypatch):
     cs, cg, reev = celf_reevaluations(labs, sizes, g.n, k)
     assert list(s) == cs and list(gn) == cg
     assert ctx.pacim_get_stats()["select_celf_evaluations"] == reev
+
+
+@pytest.mark.parametrize("i", [3, 7])
+def test_auto_selector(orc, ctx, i):
+    """Selector 3 (auto): the Win-Tree under WIC, the incremental selector
+    otherwise; GeneralGreedy's sequence either way."""
+    from oracle.oracle import Graph
+    build_fn, p, R, k = CASES[i]
+    off, nbr = build_fn()
+    g = Graph(len(off) - 1, off, nbr)
+    model, t32 = model_of(orc, p)
+    load_host(ctx, g, model, t32)
+    ctx.pacim_build_sketches(R, 5000 + i)
+    ctx.pacim_set_selector(3)
+    try:
+        s, gn, sg, _ = ctx.pacim_select_seeds(k)
+        st = ctx.pacim_get_stats()
+    finally:
+        ctx.pacim_set_selector(0)
+    es, egn, esg, _ = orc.greedy(g, model, t32, R, 5000 + i, k)
+    assert list(s) == list(es) and list(gn) == list(egn)
+    assert (st["select_evaluations"] > 0) == (model == 1)
