@@ -36,7 +36,11 @@
 #include <cstring>
 #include <vector>
 
+#include <cooperative_groups.h>
+
 #include "pacim_internal.cuh"
+
+namespace cg = cooperative_groups;
 
 #define PC_NCCL(call)                                                               \
   do {                                                                              \
@@ -127,10 +131,20 @@ __device__ __forceinline__ void mark_dirty(const DSel &S, uint32_t c) {
     S.dlist[atomicAdd(reinterpret_cast<unsigned long long *>(S.st + D_DCNT), 1ull)] = c;
 }
 
-// every block: NextSeed from the chunk maxima (identical on every rank);
-// MarkSeed on this rank's slots, member deltas into the send list
-__global__ void __launch_bounds__(DT) k_dist_cover(DSel S, uint32_t step) {
+// Step part 1 (cooperative): every block takes NextSeed from the chunk
+// maxima (identical on every rank); MarkSeed on this rank's slots, a warp per
+// slot: lane 0 walks the newly covered CC's member list into a shared buffer,
+// the warp appends (v, |C|) to the send list; then, after a grid barrier,
+// block 0 writes the step header: list overflow; list-less CCs covered;
+// EXACT = those are exactly this rank's hub CCs (both sets may be empty) —
+// when some rank covers list-less CCs, the all-reduced hot sums are the
+// update iff every rank is EXACT.
+constexpr uint32_t WBUF = 128;
+__global__ void __launch_bounds__(DT, 1) k_dist_cover(DSel S, uint32_t step) {
+  cg::grid_group grid = cg::this_grid();
   __shared__ Best sh[33];
+  __shared__ uint32_t wbuf[DT / 32][WBUF];
+  __shared__ int dense, exact;
   Best c{LLONG_MIN, NONE};
   for (uint32_t i = threadIdx.x; i < S.nchunks; i += blockDim.x) {
     Best x;
@@ -148,126 +162,94 @@ __global__ void __launch_bounds__(DT) k_dist_cover(DSel S, uint32_t step) {
     S.seeds[step] = s;
   }
   const int lane = threadIdx.x & 31;
+  const size_t gwarp = tid >> 5, nwarps = ((size_t)gridDim.x * blockDim.x) >> 5;
+  uint32_t *buf = wbuf[threadIdx.x >> 5];
   const uint32_t srow = S.cid ? S.cid[s] : s;
   unsigned long long dsum = 0;
-  for (size_t j = tid; j < S.B; j += ((size_t)gridDim.x * blockDim.x)) {
+  for (size_t j = gwarp; j < S.B; j += nwarps) {
     uint32_t d = 1, mr = NONE;
-    S.cov_root[j] = NONE;
-    if (srow != NONE && ((S.rec[(size_t)srow * S.MW + (j >> 5)].y >> (j & 31)) & 1u)) {
-      const uint32_t e = pc_cs_pos(S.rec, S.MW, srow, (uint32_t)j);
-      const uint32_t x0 = __ldcg(S.E + 2 * (size_t)e);
-      const uint32_t root = (x0 & PACIM_HIGH) ? e : x0;
-      const uint32_t x = atomicOr(S.E + 2 * (size_t)root, COV);
-      if (x & COV) {
-        d = 0;
-      } else {
-        d = x & SIZE;
-        const unsigned long long at = atomicAdd(S.cov_cnt, 1ull);
-        if (at < S.cov_cap) S.cov_list[at] = root;
-        if (d > S.list_t || root == S.hot_root[j])
-          S.cov_root[j] = root;  // no member list
-        else
-          mr = root;
+    if (lane == 0) {
+      S.cov_root[j] = NONE;
+      if (srow != NONE && ((S.rec[(size_t)srow * S.MW + (j >> 5)].y >> (j & 31)) & 1u)) {
+        const uint32_t e = pc_cs_pos(S.rec, S.MW, srow, (uint32_t)j);
+        const uint32_t x0 = __ldcg(S.E + 2 * (size_t)e);
+        const uint32_t root = (x0 & PACIM_HIGH) ? e : x0;
+        const uint32_t x = atomicOr(S.E + 2 * (size_t)root, COV);
+        if (x & COV) {
+          d = 0;
+        } else {
+          d = x & SIZE;
+          const unsigned long long at = atomicAdd(S.cov_cnt, 1ull);
+          if (at < S.cov_cap) S.cov_list[at] = root;
+          if (d > S.list_t || root == S.hot_root[j])
+            S.cov_root[j] = root;  // no member list
+          else
+            mr = root;
+        }
       }
     }
+    d = __shfl_sync(FULL, d, 0);
+    mr = __shfl_sync(FULL, mr, 0);
     dsum += d;
-    uint32_t e = mr;
-    for (uint32_t t = 0; mr != NONE && t < d && e != NONE;
-         t++, e = __ldcg(S.E + 2 * (size_t)e + 1)) {  // the members
-      const uint32_t v = __ldg(S.vid + e);
-      if (v == s) continue;
-      const unsigned long long at = atomicAdd(S.send + H_CNT, 1ull);
-      if (at < S.cap) S.send[H_WORDS + at] = ((unsigned long long)v << 32) | d;
-    }
-  }
-  for (int q = 16; q; q >>= 1) dsum += __shfl_xor_sync(FULL, dsum, q);
-  if (lane == 0 && dsum) atomicAdd(S.send + H_DSUM, dsum);
-}
-
-// the step header's flags (one block): list overflow; big CCs covered;
-// EXACT: the big CCs covered now are exactly this rank's hub giants (both
-// sets may be empty) — when some rank covers a big CC, the all-reduced hot
-// sums are the update iff every rank is EXACT
-__global__ void k_dist_head(DSel S) {
-  __shared__ int dense, exact;
-  if (threadIdx.x == 0) {
-    dense = 0;
-    exact = 1;
-  }
-  __syncthreads();
-  for (uint32_t j = threadIdx.x; j < S.B; j += blockDim.x) {
-    const uint32_t cr = S.cov_root[j];
-    if (cr != NONE) dense = 1;
-    if (cr != S.hot_root[j]) exact = 0;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long f = 0;
-    if (S.send[H_CNT] > S.cap) f |= F_OVER;
-    if (dense) f |= F_DENSE;
-    if (exact) f |= F_EXACT;
-    S.send[H_FLAGS] = f;
-  }
-}
-
-// every rank applies every rank's list to its replica
-__global__ void __launch_bounds__(DT) k_dist_apply(DSel S, uint32_t step) {
-  const uint32_t s = (uint32_t)S.st[D_S];
-  const long long sg = (long long)S.st[D_SG];
-  // consensus from the gathered headers (identical on every rank)
-  bool replay = false, any_dense = false, all_exact = true;
-  long long gsum = 0;
-  for (int p = 0; p < S.world; p++) {
-    const unsigned long long *h = S.recv + (size_t)p * (H_WORDS + S.cap);
-    const unsigned long long f = h[H_FLAGS];
-    gsum += (long long)h[H_DSUM];
-    if (f & F_OVER) replay = true;
-    if (f & F_DENSE) any_dense = true;
-    if (!(f & F_EXACT)) all_exact = false;
-  }
-  // big CCs without member lists: only the step that covers every rank's hub
-  // giants at once has its update precomputed (the all-reduced hot sums)
-  if (any_dense && (!all_exact || !S.ghot)) replay = true;
-  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const size_t nth = (size_t)gridDim.x * blockDim.x;
-  if (tid == 0) {
-    if (replay) S.st[D_REPLAY] = 1;
-    if (gsum != sg) S.st[D_CHECK] = 1;
-    S.gain_num[step] = gsum;
-    S.gain[s] = -1;  // s leaves the candidate set (R6)
-    mark_dirty(S, s >> S.csh);
-  }
-  if (replay) return;
-  if (any_dense && S.ghot) {
-    for (size_t v = tid; v < S.nv; v += nth) {
-      const long long h = S.ghot[v];
-      if (h && v != s) {
-        atomicAdd(reinterpret_cast<unsigned long long *>(S.gain + v), (unsigned long long)(-h));
-        const uint32_t c = (uint32_t)(v >> S.csh);
-        if (__ldcg(&S.cmax[c].v) == v) mark_dirty(S, c);
+    if (mr == NONE) continue;
+    uint32_t e = mr, left = d;
+    while (left) {  // the members, a buffer of entries at a time
+      uint32_t cnt = 0;
+      if (lane == 0) {
+        for (; cnt < WBUF && left && e != NONE; cnt++, left--) {
+          buf[cnt] = e;
+          e = __ldcg(S.E + 2 * (size_t)e + 1);
+        }
+        if (e == NONE) left = 0;
       }
+      cnt = __shfl_sync(FULL, cnt, 0);
+      left = __shfl_sync(FULL, left, 0);
+      __syncwarp();
+      for (uint32_t t0 = 0; t0 < cnt; t0 += 32) {
+        const uint32_t t = t0 + lane;
+        uint32_t v = NONE;
+        if (t < cnt) v = __ldg(S.vid + buf[t]);
+        const bool put = t < cnt && v != s;
+        const uint32_t m = __ballot_sync(FULL, put);
+        unsigned long long at = 0;
+        if (lane == 0 && m) at = atomicAdd(S.send + H_CNT, (unsigned long long)__popc(m));
+        at = __shfl_sync(FULL, at, 0) + __popc(m & ((1u << lane) - 1));
+        if (put && at < S.cap) S.send[H_WORDS + at] = ((unsigned long long)v << 32) | d;
+      }
+      __syncwarp();
     }
   }
-  for (int p = 0; p < S.world; p++) {
-    const unsigned long long *h = S.recv + (size_t)p * (H_WORDS + S.cap);
-    const unsigned long long cnt = min(h[H_CNT], S.cap);
-    for (size_t t = tid; t < cnt; t += nth) {
-      const unsigned long long x = h[H_WORDS + t];
-      const uint32_t v = (uint32_t)(x >> 32);
-      const long long d = (long long)(uint32_t)x;
-      atomicAdd(reinterpret_cast<unsigned long long *>(S.gain + v), (unsigned long long)(-d));
-      const uint32_t c = v >> S.csh;
-      if (__ldcg(&S.cmax[c].v) == v) mark_dirty(S, c);
+  if (lane == 0 && dsum) atomicAdd(S.send + H_DSUM, dsum);
+  grid.sync();
+  if (blockIdx.x == 0) {
+    if (threadIdx.x == 0) {
+      dense = 0;
+      exact = 1;
+    }
+    __syncthreads();
+    for (uint32_t j = threadIdx.x; j < S.B; j += blockDim.x) {
+      const uint32_t cr = S.cov_root[j];
+      if (cr != NONE) dense = 1;
+      if (cr != S.hot_root[j]) exact = 0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long f = 0;
+      if (S.send[H_CNT] > S.cap) f |= F_OVER;
+      if (dense) f |= F_DENSE;
+      if (exact) f |= F_EXACT;
+      S.send[H_FLAGS] = f;
     }
   }
 }
 
-// refresh the dirty chunk maxima (block per chunk), then clear the message
-__global__ void __launch_bounds__(DT) k_dist_chunks(DSel S, bool all) {
-  __shared__ Best sh[33];
+// Step part 2 (cooperative): every rank applies every rank's list to its
+// replica; after a grid barrier the chunk maxima that lost their argmax are
+// rescanned (a block per chunk) and the send header cleared
+__device__ void refresh_dirty(const DSel &S, bool all, Best *sh) {
   const uint32_t nd = all ? S.nchunks : (uint32_t)__ldcg(S.st + D_DCNT);
   for (uint32_t t = blockIdx.x; t < nd; t += gridDim.x) {
-    const uint32_t c = all ? t : S.dlist[t];
+    const uint32_t c = all ? t : __ldcg(S.dlist + t);
     const size_t v0 = (size_t)c << S.csh, v1 = min((size_t)S.nv, v0 + ((size_t)1 << S.csh));
     Best b{LLONG_MIN, NONE};
     for (size_t v = v0 + threadIdx.x; v < v1; v += blockDim.x) {
@@ -283,6 +265,69 @@ __global__ void __launch_bounds__(DT) k_dist_chunks(DSel S, bool all) {
       S.cdirty[c] = 0;
     }
   }
+}
+
+__global__ void __launch_bounds__(DT, 1) k_dist_apply(DSel S, uint32_t step) {
+  cg::grid_group grid = cg::this_grid();
+  __shared__ Best sh[33];
+  const uint32_t s = (uint32_t)S.st[D_S];
+  const long long sg = (long long)S.st[D_SG];
+  // consensus from the gathered headers (identical on every rank)
+  bool replay = false, any_dense = false, all_exact = true;
+  long long gsum = 0;
+  for (int p = 0; p < S.world; p++) {
+    const unsigned long long *h = S.recv + (size_t)p * (H_WORDS + S.cap);
+    const unsigned long long f = h[H_FLAGS];
+    gsum += (long long)h[H_DSUM];
+    if (f & F_OVER) replay = true;
+    if (f & F_DENSE) any_dense = true;
+    if (!(f & F_EXACT)) all_exact = false;
+  }
+  // list-less CCs: only the step that covers every rank's hub CCs at once has
+  // its update precomputed (the all-reduced hot sums)
+  if (any_dense && (!all_exact || !S.ghot)) replay = true;
+  const size_t tid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t nth = (size_t)gridDim.x * blockDim.x;
+  if (tid == 0) {
+    if (replay) S.st[D_REPLAY] = 1;
+    if (gsum != sg) S.st[D_CHECK] = 1;
+    S.gain_num[step] = gsum;
+    S.gain[s] = -1;  // s leaves the candidate set (R6)
+    mark_dirty(S, s >> S.csh);
+  }
+  if (!replay) {
+    if (any_dense && S.ghot) {
+      for (size_t v = tid; v < S.nv; v += nth) {
+        const long long h = S.ghot[v];
+        if (h && v != s) {
+          atomicAdd(reinterpret_cast<unsigned long long *>(S.gain + v), (unsigned long long)(-h));
+          const uint32_t c = (uint32_t)(v >> S.csh);
+          if (__ldcg(&S.cmax[c].v) == v) mark_dirty(S, c);
+        }
+      }
+    }
+    for (int p = 0; p < S.world; p++) {
+      const unsigned long long *h = S.recv + (size_t)p * (H_WORDS + S.cap);
+      const unsigned long long cnt = min(h[H_CNT], S.cap);
+      for (size_t t = tid; t < cnt; t += nth) {
+        const unsigned long long x = h[H_WORDS + t];
+        const uint32_t v = (uint32_t)(x >> 32);
+        const long long d = (long long)(uint32_t)x;
+        atomicAdd(reinterpret_cast<unsigned long long *>(S.gain + v), (unsigned long long)(-d));
+        const uint32_t c = v >> S.csh;
+        if (__ldcg(&S.cmax[c].v) == v) mark_dirty(S, c);
+      }
+    }
+  }
+  grid.sync();
+  refresh_dirty(S, false, sh);
+  if (blockIdx.x == 0 && threadIdx.x < H_WORDS) S.send[threadIdx.x] = 0;
+}
+
+// the initial chunk maxima (all chunks) and a cleared send header
+__global__ void __launch_bounds__(DT) k_dist_chunks(DSel S) {
+  __shared__ Best sh[33];
+  refresh_dirty(S, true, sh);
   if (blockIdx.x == 0 && threadIdx.x < H_WORDS) S.send[threadIdx.x] = 0;
 }
 
@@ -450,7 +495,7 @@ static bool dist_select_fast(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_
   const int world = ctx->comm_world;
   const unsigned long long cap =
       getenv("PACIM_DIST_CAP") ? (unsigned long long)std::max(1LL, atoll(getenv("PACIM_DIST_CAP")))
-                               : (1ull << 16);
+                               : (1ull << 14);
   DSel S;
   S.rec = ctx->cs_rec.as<uint2>();
   S.MW = ctx->cs_MW;
@@ -504,21 +549,19 @@ static bool dist_select_fast(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_
   PC_CUDA(cudaMemcpyAsync(S.gain, ctx->gain0.p, (size_t)n * 8, cudaMemcpyDeviceToDevice,
                           ctx->stream));
   const unsigned grid = (unsigned)ctx->sm_count;
-  k_dist_chunks<<<grid, DT, 0, ctx->stream>>>(S, true);
+  k_dist_chunks<<<grid, DT, 0, ctx->stream>>>(S);
   PC_CHECK_LAUNCH();
   cudaEvent_t e0, e1;
   PC_CUDA(cudaEventCreate(&e0));
   PC_CUDA(cudaEventCreate(&e1));
   PC_CUDA(cudaEventRecord(e0, ctx->stream));
   for (uint32_t i = 0; i < k; i++) {
-    k_dist_cover<<<grid, DT, 0, ctx->stream>>>(S, i);
-    k_dist_head<<<1, 256, 0, ctx->stream>>>(S);
-    PC_CHECK_LAUNCH();
+    uint32_t step = i;
+    void *args[] = {&S, &step};
+    PC_CUDA(cudaLaunchCooperativeKernel((void *)k_dist_cover, grid, DT, args, 0, ctx->stream));
     PC_NCCL(ncclAllGather(S.send, const_cast<unsigned long long *>(S.recv), H_WORDS + cap,
                           ncclUint64, comm_of(ctx), ctx->stream));
-    k_dist_apply<<<grid, DT, 0, ctx->stream>>>(S, i);
-    k_dist_chunks<<<grid, DT, 0, ctx->stream>>>(S, false);
-    PC_CHECK_LAUNCH();
+    PC_CUDA(cudaLaunchCooperativeKernel((void *)k_dist_apply, grid, DT, args, 0, ctx->stream));
   }
   PC_CUDA(cudaEventRecord(e1, ctx->stream));
   unsigned long long st[D_WORDS], covn = 0;
@@ -533,7 +576,7 @@ static bool dist_select_fast(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   ctx->stats.t_select_ms = ms;
-  ctx->stats.kernel_launches_select = 4 * k + 1;
+  ctx->stats.kernel_launches_select = 2 * k + 1;
   // keep the covered list so the next selection can restore the flags
   PC_REQUIRE(covn <= S.cov_cap, PACIM_ECHECK, "sharded select: covered list overflowed");
   pc_ensure(ctx, ctx->dist_cov_old, std::max<size_t>(covn, 1) * 8);

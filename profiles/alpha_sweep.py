@@ -30,6 +30,7 @@ def main():
     k = a.k or cfg["k"]
     ctx = P.Context(0)
     n, m = pipeline.generate(ctx, cfg)
+    ctx.close()
     print(f"# alpha sweep — {cfg['name']}" + (f" scale {a.scale}" if a.scale else "")
           + f" (n = {n}, m = {m}, R = {cfg['R']}, k = {k}), B200, 1 GPU\n")
     print("Get-center visits / probe: vertices dequeued before a center is met (centers are\n"
@@ -37,8 +38,8 @@ def main():
           "Thm 3.1 bounds the expected visits by about 1/alpha.  Device total = every buffer\n"
           "the ctx holds (graph, store, selection state, scratch).\n")
     print("Store: alpha < 1: label + size (one u32 each, the covered flag in the size word) per\n"
-          "(center, sketch); alpha = 1: the compact store (per non-singleton (vertex, sketch)\n"
-          "entry: parent/size, member offset, member id; per row the slot-mask records).\n"
+          "(center, sketch); alpha = 1: the uncompressed store of a one-GPU build (dense\n"
+          "vertex-major: one u32 per (non-isolated vertex, sketch)).\n"
           "Peak = the high-water mark of the ctx's device bytes over build + select (graph\n"
           "included; pacim_stats.device_peak_bytes).\n")
     print("| alpha | rho (centers) | sketch store (GB) | build scratch (GB) | device total (GB) "
@@ -47,6 +48,10 @@ def main():
     print("|---|---|---|---|---|---|---|---|---|---|---|")
     ref = None
     for al in [float(x) for x in a.alphas.split(",")]:
+        # a fresh context per alpha: the peak is this alpha's alone (a ctx keeps
+        # buffer capacity across builds)
+        ctx = P.Context(0)
+        pipeline.generate(ctx, cfg)
         a32 = 1 << 32 if al >= 1 else int(al * 4294967296.0)
         tb, ts = [], []
         for _ in range(a.reps):
@@ -74,7 +79,7 @@ def main():
         print(f"| {al:g} | {st['rho']} | {store / 1e9:.3f} | {scratch / 1e9:.3f} "
               f"| {st['device_bytes'] / 1e9:.2f} | {st['device_peak_bytes'] / 1e9:.2f} "
               f"| {min(tb):.1f} | {min(ts):.1f} | {vis:.2f} | {1 / al:g} | {seeds == ref} |")
-    ctx.close()
+        ctx.close()
 
 
 if __name__ == "__main__":
