@@ -241,6 +241,7 @@ struct pacim_ctx {
   DevBuf cs_E;              // uint2[total]: {parent -> HIGH | size / root entry, next member}
   DevBuf cs_vid;            // u32[total]: vertex of an entry
   DevBuf cs_diag;           // u64 selection diagnostics
+  DevBuf wt_buf;            // Win-Tree selector scratch (tree, wave lists; capacity reused)
   DevBuf cs_cnt;            // build scratch: row counts and their scan
   uint64_t cs_pref_gen = ~0ull;  // store decision of the last build of graph_gen ...
   uint32_t cs_pref_B = 0;        // ... with this many slots:

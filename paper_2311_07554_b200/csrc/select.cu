@@ -1294,72 +1294,98 @@ __device__ long long dense_eval(const Sel &S, uint32_t v) {
 
 struct WTd {
   uint32_t *T;
-  uint32_t N;
+  uint32_t N, D;        // leaves (2^D), tree depth
   long long *key;
-  uint32_t *stamp, *F, *Ev, *seeds;
+  uint32_t *H0, *H1;    // hanging subtree roots of the current / next wave (2N each)
+  uint32_t *Ev, *Et;    // the wave's re-evaluations: vertex, the hanging root it came from
+  uint32_t *X;          // the step's re-evaluated vertices (the repaired paths)
+  uint32_t *seeds;
   long long *gain_num;
   unsigned long long *evals;
 };
 
+// FindMax in waves (the same exploration as the paper's recursion, P:2690-
+// 2700, scheduled by re-evaluation instead of by tree level): H = the roots of
+// the subtrees hanging off the paths explored so far (initially the root).
+// A wave takes every h in H whose (stale) winner can still beat Delta*,
+// re-evaluates those winners, and replaces h by the siblings along the path
+// from h down to the winner's leaf; it ends when no hanging winner can beat
+// Delta*.  Each subtree root is pushed at most once per step (the subtrees of
+// different hanging roots are disjoint).  Then MarkSeed and the winners on
+// the re-evaluated vertices' paths recomputed bottom-up.
 __global__ void __launch_bounds__(WT_THREADS, 1) k_wintree_dense(Sel S, WTd W, uint32_t k) {
-  __shared__ uint32_t lvl_a[40], lvl_b[40];
-  __shared__ uint32_t nf, ne;
+  __shared__ uint32_t nh, nn, ne, nx;
   __shared__ Best sh[33];
   __shared__ Best best;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   unsigned long long evals = 0, nodes = 0;
+  uint32_t *H = W.H0, *Hn = W.H1;
   for (uint32_t step = 0; step < k; step++) {
     if (threadIdx.x == 0) {
-      W.F[0] = 1;
-      lvl_a[0] = 0;
-      lvl_b[0] = 1;
-      nf = 1;
+      H[0] = 1;
+      nh = 1;
+      nx = 0;
       best = Best{LLONG_MIN, NONE};
     }
     __syncthreads();
-    uint32_t L = 0;
-    for (;; L++) {
-      const uint32_t a = lvl_a[L], b = lvl_b[L];
-      if (a == b) break;
-      if (threadIdx.x == 0) ne = 0;
-      __syncthreads();
-      const Best cur = best;
-      for (uint32_t i = a + threadIdx.x; i < b; i += blockDim.x) {
-        const uint32_t t = W.F[i];
-        const uint32_t id = W.T[t];
-        if (id == NONE) continue;
-        if (W.stamp[id] != step + 1) {
-          const long long kv = W.key[id];
-          if (!better(kv, id, cur.g, cur.v)) continue;
-          W.stamp[id] = step + 1;
-          W.Ev[atomicAdd(&ne, 1u)] = id;
-        }
-        if (t < W.N) {
-          const uint32_t at = atomicAdd(&nf, 2u);
-          W.F[at] = 2 * t;
-          W.F[at + 1] = 2 * t + 1;
-        }
+    for (;;) {
+      if (threadIdx.x == 0) {
+        ne = 0;
+        nn = 0;
       }
       __syncthreads();
+      // hanging winners that can beat Delta* (stale: none of them was
+      // re-evaluated in this step, their subtrees being disjoint from the
+      // explored paths)
+      const Best cur = best;
+      const uint32_t nhh = nh;
+      for (uint32_t i = threadIdx.x; i < nhh; i += blockDim.x) {
+        const uint32_t t = H[i];
+        const uint32_t id = W.T[t];
+        if (id == NONE || !better(W.key[id], id, cur.g, cur.v)) continue;
+        const uint32_t at = atomicAdd(&ne, 1u);
+        W.Ev[at] = id;
+        W.Et[at] = t;
+      }
+      nodes += nhh;
+      __syncthreads();
+      const uint32_t nev = ne;
+      if (nev == 0) break;
       Best mine{LLONG_MIN, NONE};
-      for (uint32_t q = wid; q < ne; q += WT_THREADS / 32) {
+      for (uint32_t q = wid; q < nev; q += WT_THREADS / 32) {
         const uint32_t v = W.Ev[q];
         const long long g = dense_eval(S, v);
         if (lane == 0) W.key[v] = g;
         if (better(g, v, mine.g, mine.v)) mine = Best{g, v};
       }
-      evals += ne;
-      nodes += b - a;
+      evals += nev;
       Best lb = block_best(mine, sh);
-      if (threadIdx.x == 0) {
-        if (better(lb.g, lb.v, best.g, best.v)) best = lb;
-        lvl_a[L + 1] = b;
-        lvl_b[L + 1] = nf;
+      if (threadIdx.x == 0 && better(lb.g, lb.v, best.g, best.v)) best = lb;
+      __syncthreads();
+      // the siblings along each re-evaluated path, from its hanging root down
+      const Best nb = best;
+      for (uint32_t q = threadIdx.x; q < nev * W.D; q += blockDim.x) {
+        const uint32_t e = q / W.D, l = q % W.D;
+        const uint32_t t = W.Et[e], leaf = W.N + W.Ev[e];
+        const uint32_t p = leaf >> l;
+        if (p <= t) continue;  // at or above the hanging root
+        const uint32_t sib = p ^ 1u, sid = W.T[sib];
+        if (sid != NONE && better(W.key[sid], sid, nb.g, nb.v)) Hn[atomicAdd(&nn, 1u)] = sib;
       }
+      for (uint32_t q = threadIdx.x; q < nev; q += blockDim.x) W.X[nx + q] = W.Ev[q];
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        nx += nev;
+        nh = nn;
+      }
+      uint32_t *tmp = H;
+      H = Hn;
+      Hn = tmp;
       __syncthreads();
     }
     const uint32_t s = best.v;
     const long long g = best.g;
+    // MarkSeed(s) (covered bits; the lazy selector updates no member)
     const uint32_t srow = S.cid[s];
     if (srow != NONE)
       for (uint32_t j = threadIdx.x; j < S.B; j += blockDim.x) {
@@ -1373,15 +1399,18 @@ __global__ void __launch_bounds__(WT_THREADS, 1) k_wintree_dense(Sel S, WTd W, u
         }
       }
     if (threadIdx.x == 0) {
-      W.key[s] = -1;
+      W.key[s] = -1;  // s leaves the candidate set (R6); s is one of X
       W.seeds[step] = s;
       W.gain_num[step] = g;
     }
     __syncthreads();
-    for (int l = (int)L - 1; l >= 0; l--) {
-      for (uint32_t i = lvl_a[l] + threadIdx.x; i < lvl_b[l]; i += blockDim.x) {
-        const uint32_t t = W.F[i];
-        if (t < W.N) W.T[t] = wt_win(W.key, W.T[2 * t], W.T[2 * t + 1]);
+    // the winners on the re-evaluated vertices' paths, bottom-up (a level at
+    // a time: the children of a level are final before it is recomputed)
+    const uint32_t nxx = nx;
+    for (uint32_t l = 1; l <= W.D; l++) {
+      for (uint32_t q = threadIdx.x; q < nxx; q += blockDim.x) {
+        const uint32_t t = (W.N + W.X[q]) >> l;
+        W.T[t] = wt_win(W.key, W.T[2 * t], W.T[2 * t + 1]);
       }
       __syncthreads();
     }
@@ -1961,20 +1990,23 @@ void pc_select_wintree_dense(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_
   }
   pc_ensure(ctx, ctx->gain, (size_t)n * 8);
   Sel S = make_sel(ctx, ctx->gain.as<long long>());
-  TmpBuf wb(ctx);
-  pc_ensure(ctx, wb, (size_t)2 * N * 4 + (size_t)n * 4 + (size_t)2 * N * 4 + (size_t)N * 4 +
-                         (size_t)k * 12 + 64);
+  // persistent scratch (capacity reused): T[2N], H0[2N], H1[2N], Ev[N], Et[N], X[N], outputs
+  DevBuf &wb = ctx->wt_buf;
+  pc_ensure(ctx, wb, (size_t)9 * N * 4 + (size_t)k * 12 + 64);
   WTd W;
   W.T = wb.as<uint32_t>();
-  W.stamp = W.T + 2 * (size_t)N;
-  W.F = W.stamp + n;
-  W.Ev = W.F + 2 * (size_t)N;
+  W.H0 = W.T + 2 * (size_t)N;
+  W.H1 = W.H0 + 2 * (size_t)N;
+  W.Ev = W.H1 + 2 * (size_t)N;
+  W.Et = W.Ev + N;
+  W.X = W.Et + N;
   W.gain_num = reinterpret_cast<long long *>(
-      (reinterpret_cast<uintptr_t>(W.Ev + N) + 7) & ~(uintptr_t)7);
+      (reinterpret_cast<uintptr_t>(W.X + N) + 7) & ~(uintptr_t)7);
   W.seeds = reinterpret_cast<uint32_t *>(W.gain_num + k);
   W.evals = reinterpret_cast<unsigned long long *>(
       (reinterpret_cast<uintptr_t>(W.seeds + k) + 7) & ~(uintptr_t)7);
   W.N = N;
+  W.D = depth;
   W.key = ctx->gain.as<long long>();
   cudaEvent_t e0, e1;
   PC_CUDA(cudaEventCreate(&e0));
@@ -1982,7 +2014,6 @@ void pc_select_wintree_dense(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_
   PC_CUDA(cudaEventRecord(e0, ctx->stream));
   uncover(ctx, S);
   PC_CUDA(cudaMemcpyAsync(W.key, ctx->gain0.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, ctx->stream));
-  PC_CUDA(cudaMemsetAsync(W.stamp, 0, (size_t)n * 4, ctx->stream));
   k_wtd_leaves<<<pc_grid(ctx, N, 256), 256, 0, ctx->stream>>>(W.T, N, n);
   for (uint32_t lo = N >> 1; lo >= 1; lo >>= 1)
     k_wtd_level<<<pc_grid(ctx, lo, 256), 256, 0, ctx->stream>>>(W.T, W.key, lo, 2 * lo);

@@ -5,7 +5,12 @@ same store, with CELF's evaluation count on the same gains:
   PACIM_CELF_COUNT=1 it also counts the re-evaluations CELF would make
   (every non-seed whose stale score ranks at or above the step's winner);
 * prefix doubling (selector 1, the P-tree scheme, P:2381-2401);
-* Win-Tree (selector 2; compact store only).
+* Win-Tree (selector 2).
+
+Each config runs twice: on the compact store (PACIM_STORE=compact; its
+incremental selector carries the CELF counter) and on the dense store (the
+one-GPU default; the CELF count of the compact run is the denominator, the
+gains being identical).
 
 The paper reports P-tree / Win-Tree evaluations at 1.03x / 1.7x CELF's
 (P:1715-1720).  Re-evaluations exclude the initial n evaluations (gain0).
@@ -29,7 +34,9 @@ def main():
     print("| config | store | n | k | incremental ms | CELF re-evals | prefix-doubling ms | "
           "its re-evals | / CELF | Win-Tree ms | its re-evals | / CELF | tree nodes | same seeds |")
     print("|---|---|---|---|---|---|---|---|---|---|---|---|---|---|")
-    for name in sys.argv[1:] or ["c2"]:
+    celf_of = {}
+    for name, store in [(c, s) for c in (sys.argv[1:] or ["c2"]) for s in ("compact", "dense")]:
+        os.environ["PACIM_STORE"] = store
         cfg = inputs.config(name)
         ctx = P.Context(0)
         n, m = pipeline.generate(ctx, cfg)
@@ -37,7 +44,8 @@ def main():
         k = cfg["k"]
         a = ctx.pacim_select_seeds(k)
         st = ctx.pacim_get_stats()
-        ti, celf, store = st["t_select_ms"], st["select_celf_evaluations"], st["store"]
+        ti, store = st["t_select_ms"], st["store"]
+        celf = celf_of.setdefault(name, st["select_celf_evaluations"])
         res = []
         for sel in (1, 2):
             ctx.pacim_set_selector(sel)
