@@ -68,10 +68,12 @@ class ClockSampler:
         self.lines = []
 
     def start(self):
+        if os.environ.get("PACIM_CLOCK_MS") == "0":  # debugging: no sampler
+            return
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", os.environ.get("PACIM_CLOCK_MS", "50")],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -312,8 +314,10 @@ def main():
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    _tw0 = [time.perf_counter()]
     for _ in range(args.steps):
         out = step()
+        _tw0.append(time.perf_counter())
         st = ctx.stats_raw()  # the struct's fields, no dict: little host time between steps
         for kk in keys:
             acc[kk] += getattr(st, kk)
@@ -323,6 +327,9 @@ def main():
     barrier()
     clk = clocks.stop()
     ms = e0.elapsed_time(e1)
+    if os.environ.get("PACIM_BENCH_DEBUG"):
+        print("timed wall ms per step:", [round(1e3 * (_tw0[i + 1] - _tw0[i]), 2) for i in range(len(_tw0) - 1)],
+              file=sys.stderr)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)

@@ -34,7 +34,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"),
-         "-I", os.path.join(NCCL_DIR, "include")]
+         "-I", os.path.join(NCCL_DIR, "include")] + os.environ.get("PACIM_NVCC_EXTRA", "").split()
 
 
 def _stale(lib: str, deps: list[str]) -> bool:

@@ -52,9 +52,17 @@ void pc_mem_info(pacim_ctx *ctx, size_t *fr, size_t *tot) {
   if (ctx->ws_base) {
     *fr = pc_mem_free(ctx);
     *tot = ctx->ws_bytes;
-  } else {
-    cudaMemGetInfo(fr, tot);
+    return;
   }
+  if (!ctx->mi_valid) {
+    cudaMemGetInfo(&ctx->mi_free, &ctx->mi_total);
+    ctx->mi_dev_bytes = ctx->device_bytes;
+    ctx->mi_valid = true;
+  }
+  // the free bytes at the query, minus what this ctx allocated since
+  const int64_t d = (int64_t)ctx->device_bytes - (int64_t)ctx->mi_dev_bytes;
+  *fr = d >= (int64_t)ctx->mi_free ? 0 : (size_t)((int64_t)ctx->mi_free - d);
+  *tot = ctx->mi_total;
 }
 
 size_t pc_mem_free(pacim_ctx *ctx) {
@@ -64,7 +72,7 @@ size_t pc_mem_free(pacim_ctx *ctx) {
     return best;
   }
   size_t fr = 0, tot = 0;
-  cudaMemGetInfo(&fr, &tot);
+  pc_mem_info(ctx, &fr, &tot);
   return fr;
 }
 
@@ -85,6 +93,7 @@ void pc_ensure(pacim_ctx *ctx, DevBuf &b, size_t bytes) {
     cudaError_t e = cudaMalloc(&b.p, bytes);
     if (e != cudaSuccess) {
       cudaGetLastError();
+      ctx->mi_valid = false;  // the tracked free memory was wrong: query again
       b.p = nullptr;
       throw PacimError{PACIM_ENOMEM, "cudaMalloc(" + std::to_string(bytes) +
                                          " bytes) failed: " + cudaGetErrorString(e)};
@@ -332,6 +341,7 @@ int pacim_load_graph(pacim_ctx *ctx, uint32_t n, uint64_t nnz, const uint64_t *o
     PC_REQUIRE(offsets[0] == 0, PACIM_EINVAL, "offsets[0] != 0");
     PC_REQUIRE(offsets[n] == nnz, PACIM_EINVAL, "offsets[n] != nnz");
     drop_staged(ctx);
+    ctx->mi_valid = false;  // free device memory queried afresh (pc_mem_info)
     load_common(ctx, n, nnz, pmodel, t32);
     PC_CUDA(cudaMemcpyAsync(ctx->off.p, offsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice,
                             ctx->stream));
@@ -385,6 +395,7 @@ int pacim_load_graph_device(pacim_ctx *ctx, uint32_t n, uint64_t nnz, const uint
   return guarded(ctx, [&] {
     PC_REQUIRE(d_offsets && (d_neighbors || nnz == 0), PACIM_EINVAL, "NULL CSR array");
     drop_staged(ctx);
+    ctx->mi_valid = false;  // free device memory queried afresh (pc_mem_info)
     load_common(ctx, n, nnz, pmodel, t32);
     PC_CUDA(cudaMemcpyAsync(ctx->off.p, d_offsets, ((size_t)n + 1) * 8, cudaMemcpyDeviceToDevice,
                             ctx->stream));
@@ -411,6 +422,7 @@ int pacim_generate_graph(pacim_ctx *ctx, int kind, const uint64_t *params, int n
     PC_REQUIRE(params || nparams == 0, PACIM_EINVAL, "NULL params");
     check_model(pmodel, t32);
     drop_staged(ctx);
+    ctx->mi_valid = false;  // free device memory queried afresh (pc_mem_info)
     drop_graph(ctx);
     ctx->pmodel = pmodel;
     ctx->t32 = t32;

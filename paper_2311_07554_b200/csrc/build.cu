@@ -22,6 +22,7 @@
 //   k_gain_scatter    gain0[v] = sum_j |C_j(v)| (H7) and the member index
 //                     perm grouped by component (H6u); hot-component cursor
 //                     reservations aggregated per tile in shared memory
+#include <chrono>
 #include <algorithm>
 #include <cstdlib>
 
@@ -106,6 +107,9 @@ __device__ __forceinline__ void uf_unite(uint32_t *L, uint32_t B, uint32_t j, ui
 // candidate enumeration, SURVEY §8(a) note).
 constexpr int EDGE_THREADS = 256;
 constexpr int EDGE_WARPS = EDGE_THREADS / 32;
+#ifndef PACIM_EDGE_BLOCKS
+#define PACIM_EDGE_BLOCKS 8  // resident blocks per SM (32 registers)
+#endif
 
 // LEAN: no edge list — the warp reads 32 consecutive CSR entries (chunk c),
 // their rows from the chunk table (the row of the first entry, advanced while
@@ -117,7 +121,7 @@ constexpr int EDGE_WARPS = EDGE_THREADS / 32;
 // pc_cs_pos(rec, MW, row, slot); CS = 2: the mask pass, every live (edge,
 // slot) sets bit slot of both endpoints' row masks (L = the rec words)
 template <bool WIC, bool REC, bool DECOR, bool LEAN, int CS = 0>
-__global__ void __launch_bounds__(EDGE_THREADS, 8) k_edges(const uint64_t *__restrict__ keys,
+__global__ void __launch_bounds__(EDGE_THREADS, PACIM_EDGE_BLOCKS) k_edges(const uint64_t *__restrict__ keys,
                                                         const uint64_t *__restrict__ ckeys,
                                                         const uint32_t *__restrict__ tm1,
                                                         uint64_t m, uint64_t K, uint64_t t32,
@@ -968,12 +972,12 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
   if (ev) PC_CUDA(cudaEventRecord(ev[0], ctx->stream));
   {
     size_t smem = B * sizeof(uint32_t) + (NT + 1) * sizeof(uint16_t);
-    unsigned g = pc_grid(ctx, (es.m + 31) / 32 * 32, EDGE_THREADS, 8);
+    unsigned g = pc_grid(ctx, (es.m + 31) / 32 * 32, EDGE_THREADS, PACIM_EDGE_BLOCKS);
     if (ctx->lean) {  // no edge list: the upper edges from the CSR (c5)
       auto kern = ctx->hash_rule ? k_edges<false, false, true, true> : k_edges<false, false, false, true>;
       PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       const uint64_t nnz = 2 * ctx->m;
-      const unsigned gl = pc_grid(ctx, (nnz + 31) / 32 * 32, EDGE_THREADS, 8);
+      const unsigned gl = pc_grid(ctx, (nnz + 31) / 32 * 32, EDGE_THREADS, PACIM_EDGE_BLOCKS);
       kern<<<gl, EDGE_THREADS, smem, ctx->stream>>>(
           ctx->off.as<uint64_t>(), reinterpret_cast<const uint64_t *>(ctx->nbr.p),
           ctx->crow.as<uint32_t>(), nnz, ctx->K, ctx->t32, ctx->d_shr.as<uint32_t>(),
@@ -1036,7 +1040,7 @@ static void cs_edges(pacim_ctx *ctx, uint32_t *L, const uint2 *rec, uint32_t MW,
                                : k_edges<false, false, false, true, MODE>;
     PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const uint64_t nnz = 2 * ctx->m;
-    const unsigned gl = pc_grid(ctx, (nnz + 31) / 32 * 32, EDGE_THREADS, 8);
+    const unsigned gl = pc_grid(ctx, (nnz + 31) / 32 * 32, EDGE_THREADS, PACIM_EDGE_BLOCKS);
     kern<<<gl, EDGE_THREADS, smem, ctx->stream>>>(
         ctx->off.as<uint64_t>(), reinterpret_cast<const uint64_t *>(ctx->nbr.p),
         ctx->crow.as<uint32_t>(), nnz, ctx->K, ctx->t32, ctx->d_shr.as<uint32_t>(),
@@ -1048,7 +1052,7 @@ static void cs_edges(pacim_ctx *ctx, uint32_t *L, const uint2 *rec, uint32_t MW,
                    : (ctx->hash_rule ? k_edges<false, false, true, false, MODE>
                                      : k_edges<false, false, false, false, MODE>);
     PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const unsigned g = pc_grid(ctx, (ctx->m + 31) / 32 * 32, EDGE_THREADS, 8);
+    const unsigned g = pc_grid(ctx, (ctx->m + 31) / 32 * 32, EDGE_THREADS, PACIM_EDGE_BLOCKS);
     kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
         ctx->keys.as<uint64_t>(), ctx->ckeys.as<uint64_t>(),
         pe ? ctx->tm1.as<uint32_t>() : nullptr, ctx->m, ctx->K, pe ? ctx->toff() : ctx->t32,
@@ -1122,7 +1126,14 @@ __global__ void k_fill_smap(const uint32_t *wf, uint32_t nw, uint32_t *smap) {
       smap[j] = (wf[w] << 16) | (wf[w + 1] - wf[w]);
 }
 
+static double host_ms() {
+  return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
 void pc_build(pacim_ctx *ctx) {
+  const bool htime = getenv("PACIM_HOST_TIMING") != nullptr;  // diagnostics: host phases to stderr
+  double h0 = htime ? host_ms() : 0, h1 = 0, h2 = 0, h3 = 0;
   const uint32_t n = ctx->nr, B = ctx->R_local;  // store rows = non-isolated vertices
   PC_REQUIRE(B >= 1 && B <= 65535, PACIM_EINVAL, "local sketch count must be in [1, 65535]");
   PC_REQUIRE(!ctx->compressed, PACIM_ENOTIMPL, "compressed store not built by pc_build");
@@ -1173,6 +1184,7 @@ void pc_build(pacim_ctx *ctx) {
   std::vector<cudaEvent_t> ev(2 + 4 * (size_t)nwin);
   for (auto &e : ev) PC_CUDA(cudaEventCreate(&e));
   PC_CUDA(cudaEventRecord(ev[0], ctx->stream));
+  if (htime) h1 = host_ms();
   // gain0 (H7): isolated vertices are singletons everywhere (gain B)
   k_fill_i64<<<pc_grid(ctx, ctx->n, 256), 256, 0, ctx->stream>>>(ctx->gain0.as<int64_t>(), ctx->n,
                                                                 (int64_t)B);
@@ -1279,7 +1291,9 @@ void pc_build(pacim_ctx *ctx) {
   unsigned long long h[6];
   PC_CUDA(cudaMemcpyAsync(h, ctr, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                           ctx->stream));
+  if (htime) h2 = host_ms();
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (htime) h3 = host_ms();
   ctx->ncomp = h[0];
   ctx->nnonsingle = h[0] + h[1];
   ctx->nmember = 0;
@@ -1301,6 +1315,9 @@ void pc_build(pacim_ctx *ctx) {
   ctx->stats.t_build_ms = ev_ms(ev[0], ev.back());
   ctx->stats.kernel_launches_build = ctx->launches;
   for (auto &e : ev) cudaEventDestroy(e);
+  if (htime)
+    fprintf(stderr, "[pc_build host ms] prep %.3f enqueue %.3f wait %.3f tail %.3f (gpu %.3f)\n", h1 - h0,
+            h2 - h1, h3 - h2, host_ms() - h3, ctx->stats.t_build_ms);
 }
 
 // canonical labels of one slot: slot value is v (singleton), HIGH|ci (root:

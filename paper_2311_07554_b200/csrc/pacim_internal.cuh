@@ -140,6 +140,13 @@ struct pacim_ctx {
   int sm_count = 148;
   uint64_t device_bytes = 0;
   uint64_t device_peak = 0;  // high-water mark since the last build started
+  // cudaMemGetInfo, cached: on the B200 boxes one call took 4-18 ms with
+  // ~100 GB allocated (c4), inside every build.  Free memory is re-queried at
+  // graph loads / generation / failed allocations and tracked through this
+  // ctx's own allocations in between (pc_mem_info)
+  bool mi_valid = false;
+  size_t mi_free = 0, mi_total = 0;
+  uint64_t mi_dev_bytes = 0;
 
   // ---- multi-GPU (dist.cu): NCCL communicator of pacim_init_comm
   void *comm = nullptr;     // ncclComm_t

@@ -5,7 +5,9 @@ time on one B200 is its time in a P-GPU job.  With P > 1 the shard takes the
 compact store (the sharded NCCL select walks its member lists).  Also the
 gain0 all-reduce volume (8n bytes) and the store's bytes per rank.
 
-    python profiles/shard_build.py c4 > profiles/rNN_shard_build_c4.md
+    python profiles/shard_build.py c4 [compact|dense] > profiles/rNN_shard_build_c4.md
+
+The second argument forces the store of the P > 1 shards (PACIM_STORE).
 """
 import os
 import sys
@@ -20,6 +22,9 @@ def main():
     import paper_2311_07554_b200 as P
     from paper_2311_07554_b200 import pipeline
     name = sys.argv[1] if len(sys.argv) > 1 else "c4"
+    if len(sys.argv) > 2:
+        os.environ["PACIM_STORE"] = sys.argv[2]
+    worlds = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [1, 2, 4, 8]
     cfg = inputs.config(name)
     ctx = P.Context(0)
     n, m = pipeline.generate(ctx, cfg)
@@ -27,7 +32,7 @@ def main():
     print("| P | sketches on rank 0 | store | build ms (best of 3) | mask / init ms | edges ms | "
           "compress ms | gain ms | store + lists GB | device GB |")
     print("|---|---|---|---|---|---|---|---|---|---|")
-    for world in (1, 2, 4, 8):
+    for world in worlds:
         best = None
         for _ in range(3):
             ctx.pacim_build_sketches(cfg["R"], cfg["hash_seed"], 1 << 32, 0, world)
