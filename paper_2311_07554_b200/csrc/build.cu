@@ -111,6 +111,18 @@ constexpr int EDGE_WARPS = EDGE_THREADS / 32;
 #define PACIM_EDGE_BLOCKS 8  // resident blocks per SM (32 registers)
 #endif
 
+// The live (edge, slot) pairs of the compact store's mask pass (CS = 2), for
+// its union pass to read instead of hashing every edge again: entry =
+// u_row << 36 | v_row << 8 | slot (rows < 2^28, slots < 256).  Each warp
+// reserves PL_CHUNK entries at a time (*cnt += PL_CHUNK; unused ones = ~0);
+// entries at or past cap are dropped (*cnt > cap: the host runs the full pass)
+constexpr uint32_t PL_CHUNK = 512;  // list entries reserved per warp at a time
+struct PairList {
+  unsigned long long *p = nullptr;
+  unsigned long long *cnt = nullptr;
+  unsigned long long cap = 0;
+};
+
 // LEAN: no edge list — the warp reads 32 consecutive CSR entries (chunk c),
 // their rows from the chunk table (the row of the first entry, advanced while
 // an entry lies past the row's end), and keeps the upper ones (v > u); rows
@@ -132,7 +144,7 @@ __global__ void __launch_bounds__(EDGE_THREADS, PACIM_EDGE_BLOCKS) k_edges(const
                                                         unsigned long long *live_ctr, Hla hla,
                                                         const uint64_t *__restrict__ hr64,
                                                         const uint2 *__restrict__ rec,
-                                                        uint32_t MW) {
+                                                        uint32_t MW, PairList pl) {
   // slots [j0, j0 + Bb) of the B sorted slots go to L (row stride Bb)
   extern __shared__ uint32_t sm[];
   uint32_t *shr = sm;
@@ -150,6 +162,10 @@ __global__ void __launch_bounds__(EDGE_THREADS, PACIM_EDGE_BLOCKS) k_edges(const
   const size_t gw = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long live = 0;
+  // pair list (CS = 2): the warp's current chunk [pl_base, pl_base + PL_CHUNK)
+  // of the list, pl_used of it filled (warp-uniform; one counter add per chunk)
+  unsigned long long pl_base = 0;
+  uint32_t pl_used = PL_CHUNK;
   for (size_t base = gw * 32; base < m; base += nw * 32) {
     // ---- one edge per lane: hash and candidate slot range
     const size_t e = base + lane;
@@ -258,6 +274,24 @@ __global__ void __launch_bounds__(EDGE_THREADS, PACIM_EDGE_BLOCKS) k_edges(const
           atomicOr(L + ((size_t)vv * MW + (j >> 5)) * 2 + 1, 1u << (j & 31));
           live++;
         }
+        if (pl.p) {  // the pair for the union pass, into the warp's reserved chunk
+          const uint32_t lm = __ballot_sync(0xffffffffu, lv);
+          const uint32_t nl = __popc(lm);
+          if (nl) {
+            if (pl_used + nl > PL_CHUNK) {  // close the chunk (holes: ~0) and take the next
+              for (uint32_t q = pl_used + lane; q < PL_CHUNK; q += 32)
+                if (pl_base + q < pl.cap) pl.p[pl_base + q] = ~0ull;
+              unsigned long long b0 = 0;
+              if (lane == 0) b0 = atomicAdd(pl.cnt, (unsigned long long)PL_CHUNK);
+              pl_base = __shfl_sync(0xffffffffu, b0, 0);
+              pl_used = 0;
+            }
+            const unsigned long long at = pl_base + pl_used + __popc(lm & ((1u << lane) - 1));
+            if (lv && at < pl.cap)
+              pl.p[at] = (unsigned long long)uu << 36 | (unsigned long long)vv << 8 | j;
+            pl_used += nl;
+          }
+        }
       } else if (lv) {
         if (CS == 1)
           uf_unite(L, 2, 0, pc_cs_pos(rec, MW, u & ~PACIM_HUBF, j),
@@ -270,6 +304,9 @@ __global__ void __launch_bounds__(EDGE_THREADS, PACIM_EDGE_BLOCKS) k_edges(const
     __syncwarp();
   }
   if (REC) hla.flush(w_hla[REC ? wid : 0], hla_n);
+  if (CS == 2 && pl.p)  // the last chunk's holes
+    for (uint32_t q = pl_used + lane; q < PL_CHUNK; q += 32)
+      if (pl_base + q < pl.cap) pl.p[pl_base + q] = ~0ull;
   // block-aggregated counter
   for (int d = 16; d; d >>= 1) live += __shfl_xor_sync(0xffffffffu, live, d);
   __shared__ unsigned long long bsum;
@@ -981,7 +1018,7 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
       kern<<<gl, EDGE_THREADS, smem, ctx->stream>>>(
           ctx->off.as<uint64_t>(), reinterpret_cast<const uint64_t *>(ctx->nbr.p),
           ctx->crow.as<uint32_t>(), nnz, ctx->K, ctx->t32, ctx->d_shr.as<uint32_t>(),
-          ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), nullptr, 0u);
+          ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), nullptr, 0u, PairList{});
     } else if (ctx->pmodel != PACIM_P_CONST) {  // per-edge thresholds (WIC, Uniform)
       auto kern = ctx->hash_rule ? (hla.raw ? k_edges<true, true, true, false> : k_edges<true, false, true, false>)
                                  : (hla.raw ? k_edges<true, true, false, false> : k_edges<true, false, false, false>);
@@ -989,7 +1026,7 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
       kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
           es.keys, es.ckeys, ctx->tm1.as<uint32_t>(), es.m,
           ctx->K, ctx->toff(), ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla,
-          ctx->d_hr64.as<uint64_t>(), nullptr, 0u);
+          ctx->d_hr64.as<uint64_t>(), nullptr, 0u, PairList{});
     } else {
       auto kern = ctx->hash_rule ? (hla.raw ? k_edges<false, true, true, false> : k_edges<false, false, true, false>)
                                  : (hla.raw ? k_edges<false, true, false, false> : k_edges<false, false, false, false>);
@@ -997,7 +1034,7 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
       kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
           es.keys, es.ckeys, nullptr, es.m, ctx->K, ctx->t32,
           ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla,
-          ctx->d_hr64.as<uint64_t>(), nullptr, 0u);
+          ctx->d_hr64.as<uint64_t>(), nullptr, 0u, PairList{});
     }
     PC_CHECK_LAUNCH();
   }
@@ -1031,7 +1068,7 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
 // its live sketches, unions of the flat entries in P.  ctr[4] += live pairs.
 template <int MODE>
 static void cs_edges(pacim_ctx *ctx, uint32_t *L, const uint2 *rec, uint32_t MW,
-                     unsigned long long *ctr) {
+                     unsigned long long *ctr, PairList pl = PairList{}) {
   const uint32_t B = ctx->R_local;
   const uint32_t NT = 1u << PACIM_TB;
   const size_t smem = B * sizeof(uint32_t) + (NT + 1) * sizeof(uint16_t);
@@ -1044,7 +1081,7 @@ static void cs_edges(pacim_ctx *ctx, uint32_t *L, const uint2 *rec, uint32_t MW,
     kern<<<gl, EDGE_THREADS, smem, ctx->stream>>>(
         ctx->off.as<uint64_t>(), reinterpret_cast<const uint64_t *>(ctx->nbr.p),
         ctx->crow.as<uint32_t>(), nnz, ctx->K, ctx->t32, ctx->d_shr.as<uint32_t>(),
-        ctx->d_tab.as<uint16_t>(), B, 0, B, L, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), rec, MW);
+        ctx->d_tab.as<uint16_t>(), B, 0, B, L, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), rec, MW, pl);
   } else {
     const bool pe = ctx->pmodel != PACIM_P_CONST;
     auto kern = pe ? (ctx->hash_rule ? k_edges<true, false, true, false, MODE>
@@ -1057,7 +1094,7 @@ static void cs_edges(pacim_ctx *ctx, uint32_t *L, const uint2 *rec, uint32_t MW,
         ctx->keys.as<uint64_t>(), ctx->ckeys.as<uint64_t>(),
         pe ? ctx->tm1.as<uint32_t>() : nullptr, ctx->m, ctx->K, pe ? ctx->toff() : ctx->t32,
         ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, 0, B, L, ctr + 4, Hla{},
-        ctx->d_hr64.as<uint64_t>(), rec, MW);
+        ctx->d_hr64.as<uint64_t>(), rec, MW, pl);
   }
   PC_CHECK_LAUNCH();
   ctx->launches++;
@@ -1071,10 +1108,46 @@ void pc_cs_edges(pacim_ctx *ctx, uint32_t *E, const uint2 *rec, uint32_t MW,
 }
 
 // The mask pass over the upper edges: the live slots of every edge set in
-// both endpoints' row masks (rec.y words).  ctr[5] += live pairs.
-void pc_cs_mask_edges(pacim_ctx *ctx, uint32_t *rec_words, uint32_t MW,
-                      unsigned long long *ctr) {
-  cs_edges<2>(ctx, rec_words, nullptr, MW, ctr + 1);
+// both endpoints' row masks (rec.y words).  ctr[5] += live pairs.  With a
+// pair list (plist != null) the live pairs are also written there, in chunks
+// of PL_CHUNK entries reserved per warp (*pcnt = the slots reserved, holes
+// ~0; entries at or past cap are dropped: *pcnt > cap means overflow).
+void pc_cs_mask_edges(pacim_ctx *ctx, uint32_t *rec_words, uint32_t MW, unsigned long long *ctr,
+                      unsigned long long *plist, unsigned long long *pcnt, unsigned long long cap) {
+  PairList pl;
+  pl.p = plist;
+  pl.cnt = pcnt;
+  pl.cap = cap;
+  cs_edges<2>(ctx, rec_words, nullptr, MW, ctr + 1, pl);
+}
+
+namespace {
+// the union pass from the mask pass's pair list: no edge is read or hashed
+// again (H2, H3 on the recorded live pairs)
+__global__ void __launch_bounds__(256) k_cs_list_unite(uint32_t *E, const uint2 *__restrict__ rec,
+                                                       uint32_t MW,
+                                                       const unsigned long long *__restrict__ pl,
+                                                       unsigned long long cnt,
+                                                       unsigned long long *live_ctr,
+                                                       const unsigned long long *mask_live) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(live_ctr, *mask_live);
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const unsigned long long x = pl[i];
+    if (x == ~0ull) continue;  // a hole of a warp's chunk
+    const uint32_t u = (uint32_t)(x >> 36), v = (uint32_t)(x >> 8) & 0x0FFFFFFFu, j = (uint32_t)x & 255u;
+    uf_unite(E, 2, 0, pc_cs_pos(rec, MW, u, j), pc_cs_pos(rec, MW, v, j));
+  }
+}
+}  // namespace
+
+void pc_cs_list_unite(pacim_ctx *ctx, uint32_t *E, const uint2 *rec, uint32_t MW,
+                      const unsigned long long *plist, unsigned long long cnt,
+                      unsigned long long *ctr, const unsigned long long *mask_live) {
+  k_cs_list_unite<<<pc_grid(ctx, cnt, 256, 8), 256, 0, ctx->stream>>>(E, rec, MW, plist, cnt, ctr + 4,
+                                                                     mask_live);
+  PC_CHECK_LAUNCH();
+  ctx->launches++;
 }
 
 // Slot windows of the store for this build.  With a constant
@@ -1148,6 +1221,9 @@ void pc_build(pacim_ctx *ctx) {
                     &ctx->hla_off, &ctx->hla_row, &ctx->hla_raw})
     pc_free(ctx, *d);
   ctx->hla_ok = false;
+  const bool want_hla = (getenv("PACIM_HLA") != nullptr || getenv("PACIM_FORCE_HLA") != nullptr);
+  const uint32_t W = plan_windows(ctx);
+  const uint32_t nwin = (uint32_t)ctx->win_first.size() - 1;
   pc_ensure(ctx, ctx->L, (size_t)n * B * sizeof(uint32_t));
   pc_ensure(ctx, ctx->gain0, (size_t)ctx->n * sizeof(int64_t));
   pc_ensure(ctx, ctx->counters, 64 * sizeof(uint64_t));
@@ -1159,13 +1235,10 @@ void pc_build(pacim_ctx *ctx) {
   // live hub adjacency (HLA) of the hub rows: opt-in (PACIM_HLA=1): on c4
   // recording costs more build time than the selection saves (its traversal
   // is bound by hop latency, not edge work)
-  const bool want_hla = (getenv("PACIM_HLA") != nullptr || getenv("PACIM_FORCE_HLA") != nullptr);
   ctx->hla_ok = false;
   Hla hla{};
   const bool rec_hla = want_hla && pc_hla_begin(ctx, &hla, 1e30);
   ctx->hot_any = false;  // set by the single-window gain pass when hot sums are kept
-  const uint32_t W = plan_windows(ctx);
-  const uint32_t nwin = (uint32_t)ctx->win_first.size() - 1;
   if (ctx->smap_of != ctx->win_first || ctx->d_smap.bytes < (size_t)B * 4) {
     // per-slot window table (select / labels address the store through it);
     // rebuilt only when the windows change (one window [0, B) by default)

@@ -250,6 +250,12 @@ struct pacim_ctx {
   DevBuf cs_diag;           // u64 selection diagnostics
   DevBuf wt_buf;            // Win-Tree selector scratch (tree, wave lists; capacity reused)
   DevBuf cs_cnt;            // build scratch: row counts and their scan
+  DevBuf cs_plist;          // build scratch: the mask pass's live (edge, slot) pairs
+  double cs_live_rate = -1;      // its live pairs per (edge, slot)
+  uint64_t cs_live_hint = 0;     // list slots of the last compact build of ...
+  uint64_t cs_live_gen = ~0ull;  // ... graph_gen, with cs_live_B slots and key cs_live_K
+  uint32_t cs_live_B = 0;
+  uint64_t cs_live_K = 0;
   uint64_t cs_pref_gen = ~0ull;  // store decision of the last build of graph_gen ...
   uint32_t cs_pref_B = 0;        // ... with this many slots:
   bool cs_pref_dense = false;    // too dense for the compact store
@@ -329,7 +335,11 @@ void pc_generate(pacim_ctx *ctx, int kind, const uint64_t *params, int nparams,
 void pc_build(pacim_ctx *ctx);
 void pc_cs_edges(pacim_ctx *ctx, uint32_t *P, const uint2 *rec, uint32_t MW,
                  unsigned long long *ctr);
-void pc_cs_mask_edges(pacim_ctx *ctx, uint32_t *rec_words, uint32_t MW, unsigned long long *ctr);
+void pc_cs_mask_edges(pacim_ctx *ctx, uint32_t *rec_words, uint32_t MW, unsigned long long *ctr,
+                      unsigned long long *plist, unsigned long long *pcnt, unsigned long long cap);
+void pc_cs_list_unite(pacim_ctx *ctx, uint32_t *E, const uint2 *rec, uint32_t MW,
+                      const unsigned long long *plist, unsigned long long cnt,
+                      unsigned long long *ctr, const unsigned long long *mask_live);
 // dist.cu: NCCL sharding
 void pc_nccl_unique_id(void *out);
 void pc_init_comm(pacim_ctx *ctx, int rank, int world, const void *id);
@@ -459,6 +469,8 @@ void pc_apply_deltas(pacim_ctx *ctx, int64_t *d_gain, const uint32_t *v, const i
 void pc_apply_dense(pacim_ctx *ctx, int64_t *d_gain, int64_t *d_delta, uint32_t n, uint32_t s);
 void pc_clear_deltas(pacim_ctx *ctx, int64_t *d_delta, const uint32_t *v, uint64_t count);
 void pc_get_labels(pacim_ctx *ctx, uint32_t slot, uint32_t *host_out);
+void pc_free_lalt(pacim_ctx *ctx);
+void pc_reset_next(pacim_ctx *ctx);  // enqueue the due reset of the second store  // waits for a pending reset, frees the second store
 // the cover traversal alone (no store): for every slot j with delta[j] > 0
 // (HOST array of R_local), the members of C_j(s) lose delta[j] in target
 void pc_traverse_slots(pacim_ctx *ctx, uint32_t s, int64_t *target, const uint32_t *delta);

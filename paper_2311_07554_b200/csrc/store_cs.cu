@@ -860,7 +860,7 @@ static float ev_ms(cudaEvent_t a, cudaEvent_t b) {
 
 void pc_cs_free(pacim_ctx *ctx) {
   for (DevBuf *d : {&ctx->cs_rec, &ctx->cs_soff, &ctx->cs_ecrow, &ctx->cs_E, &ctx->cs_vid,
-                    &ctx->cs_diag, &ctx->cs_cnt})
+                    &ctx->cs_diag, &ctx->cs_cnt, &ctx->cs_plist})
     pc_free(ctx, *d);
   ctx->cs = false;
 }
@@ -918,8 +918,40 @@ bool pc_cs_build(pacim_ctx *ctx) {
   // ---- masks (the rec array, .y words)
   pc_ensure(ctx, ctx->cs_rec, (size_t)nr * MW * 8);
   PC_CUDA(cudaMemsetAsync(ctx->cs_rec.p, 0, (size_t)nr * MW * 8, ctx->stream));
+  // the pair list: the union pass reads the mask pass's live pairs instead of
+  // hashing every edge again (c4 shard of 32 sketches: 14 ms per edge pass);
+  // sized by the last build of this graph / slot count / key, else a quarter
+  // of the free memory; an overflow falls back to the full union pass
+  // (PACIM_CS_PAIRLIST = 0: no list; > 1: that capacity, for tests)
+  unsigned long long pcap = 0;
+  const long long pl_env = getenv("PACIM_CS_PAIRLIST") ? atoll(getenv("PACIM_CS_PAIRLIST")) : 1;
+  // the list pays when live pairs are rare per edge: its union pass costs
+  // ~60 ps per pair, the full pass ~9 ps per edge plus the unions (c4 builds
+  // of one rank's shard: 256 slots, 0.34 pairs per edge: 90 vs 83 ms; 128
+  // slots: 58 vs 56; 64: 38 vs 42; 32: 25.5 vs 33.6); the rate of the last
+  // build of this graph and key decides, else the slot count
+  const bool same = ctx->cs_live_gen == ctx->graph_gen && ctx->cs_live_K == ctx->K &&
+                    ctx->cs_live_rate >= 0;
+  const bool want_list = pl_env > 1 || (same ? ctx->cs_live_rate * B < 0.12 : B <= 64);
+  if (nr < (1u << 28) && B <= 256 && pl_env != 0 && want_list) {
+    if (pl_env > 1) {
+      pcap = (unsigned long long)pl_env;
+    } else if (same && ctx->cs_live_B == B) {
+      pcap = ctx->cs_live_hint + ctx->cs_live_hint / 16 + (1ull << 22);  // + chunk holes
+    } else {
+      size_t fr = 0, tot = 0;
+      pc_mem_info(ctx, &fr, &tot);
+      fr += ctx->cs_plist.bytes;
+      pcap = std::min<unsigned long long>(fr / 4 / 8, 1ull << 33);
+    }
+    if (ctx->cs_plist.bytes < pcap * 8 || ctx->cs_plist.bytes > 2 * pcap * 8 + (64ull << 20)) {
+      pc_free(ctx, ctx->cs_plist);
+      pc_ensure(ctx, ctx->cs_plist, pcap * 8);
+    }
+  }
   if (nnz)  // the upper edges (the k_edges scheme): both endpoints' bits per live pair
-    pc_cs_mask_edges(ctx, ctx->cs_rec.as<uint32_t>(), MW, ctr + 8);
+    pc_cs_mask_edges(ctx, ctx->cs_rec.as<uint32_t>(), MW, ctr + 8,
+                     pcap ? ctx->cs_plist.as<unsigned long long>() : nullptr, ctr + 16, pcap);
   mark("mask");
   // ---- counts -> entry offsets (build scratch kept by the ctx)
   pc_ensure(ctx, ctx->cs_cnt, 2 * ((size_t)nr + 1) * 8);
@@ -928,8 +960,16 @@ bool pc_cs_build(pacim_ctx *ctx) {
   PC_CHECK_LAUNCH();
   pc_exclusive_scan_u64(ctx, c64, pos, (size_t)nr + 1);
   uint64_t total = 0;
+  unsigned long long npairs = 0, nlive = 0;
   PC_CUDA(cudaMemcpyAsync(&total, pos + nr, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaMemcpyAsync(&npairs, ctr + 16, 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaMemcpyAsync(&nlive, ctr + 13, 8, cudaMemcpyDeviceToHost, ctx->stream));
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  ctx->cs_live_gen = ctx->graph_gen;
+  ctx->cs_live_K = ctx->K;
+  ctx->cs_live_rate = ctx->m ? (double)nlive / ((double)ctx->m * B) : 0.0;
+  ctx->cs_live_B = pcap ? B : 0;
+  ctx->cs_live_hint = npairs;
   ctx->launches += 2;
   mark("scan");
   // above half non-singleton pairs (c3: p = 1/2 on a grid) the compact store
@@ -965,8 +1005,15 @@ bool pc_cs_build(pacim_ctx *ctx) {
   PC_CHECK_LAUNCH();
   ctx->launches += 2;
   mark("init");
-  // ---- unions (H2, H3) on the P words (stride 2)
-  pc_cs_edges(ctx, Ew, ctx->cs_rec.as<uint2>(), MW, ctr);
+  // ---- unions (H2, H3) on the P words (stride 2): from the pair list, or
+  // (none, or it overflowed) over every edge again
+  if (pcap && npairs <= pcap) {
+    if (npairs)
+      pc_cs_list_unite(ctx, Ew, ctx->cs_rec.as<uint2>(), MW, ctx->cs_plist.as<unsigned long long>(),
+                       npairs, ctr, ctr + 13);  // the mask pass's live count (ctr + 8 + 1 + 4)
+  } else {
+    pc_cs_edges(ctx, Ew, ctx->cs_rec.as<uint2>(), MW, ctr);
+  }
   mark("edges");
   // ---- compression, sizes, member lists (H4, H5, H6u)
   pc_ensure(ctx, ctx->d_hot, 2 * (size_t)B * 4);

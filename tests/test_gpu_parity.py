@@ -138,6 +138,23 @@ def test_compact_store_hot_and_dense_cover(orc, ctx, env, monkeypatch):
         assert st["select_dense_steps"] >= 1
 
 
+@pytest.mark.parametrize("pl", ["0", "64"])
+@pytest.mark.parametrize("i", [0, 2, 3, 7, 10, 12])
+def test_compact_store_pair_list_modes(orc, ctx, i, pl, monkeypatch):
+    """The compact store's union pass without the mask pass's pair list
+    (PACIM_CS_PAIRLIST=0: every edge hashed again) and with a list too small
+    for the live pairs (64: overflow, the full pass runs instead): the same
+    oracle parity and the same live-pair count as the default list."""
+    monkeypatch.setenv("PACIM_STORE", "compact")
+    test_tiny_corpus_parity(orc, ctx, i)
+    live = ctx.pacim_get_stats()["live_pairs"]
+    monkeypatch.setenv("PACIM_CS_PAIRLIST", pl)
+    test_tiny_corpus_parity(orc, ctx, i)
+    st = ctx.pacim_get_stats()
+    assert st["live_pairs"] == live
+    assert st["store"] == 1 or st["nnonsingle"] > 0.5 * st["rows"] * st["R_local"]
+
+
 @pytest.mark.parametrize("i", [0, 2, 3, 7, 10, 12])
 def test_compact_store_used(orc, ctx, i, monkeypatch):
     """The compact store's entries are exactly the non-singleton (vertex,
