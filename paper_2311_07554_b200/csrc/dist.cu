@@ -374,6 +374,15 @@ void pc_init_comm(pacim_ctx *ctx, int rank, int world, const void *id) {
 }
 
 void pc_free_comm(pacim_ctx *ctx) {
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);  // a launched select graph
+  if (ctx->dist_graph) {
+    cudaGraphExecDestroy(reinterpret_cast<cudaGraphExec_t>(ctx->dist_graph));
+    ctx->dist_graph = nullptr;
+  }
+  if (ctx->dist_cap_stream) {
+    cudaStreamDestroy(ctx->dist_cap_stream);
+    ctx->dist_cap_stream = nullptr;
+  }
   if (ctx->comm) {
     cudaStreamSynchronize(ctx->stream);
     ncclCommDestroy(comm_of(ctx));
@@ -496,7 +505,7 @@ static bool dist_select_fast(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_
   const unsigned long long cap =
       getenv("PACIM_DIST_CAP") ? (unsigned long long)std::max(1LL, atoll(getenv("PACIM_DIST_CAP")))
                                : (1ull << 14);
-  DSel S;
+  DSel S{};  // zeroed, padding included: its bytes are the graph's cache key
   S.rec = ctx->cs_rec.as<uint2>();
   S.MW = ctx->cs_MW;
   S.E = ctx->cs_E.as<uint32_t>();
@@ -555,13 +564,50 @@ static bool dist_select_fast(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_
   PC_CUDA(cudaEventCreate(&e0));
   PC_CUDA(cudaEventCreate(&e1));
   PC_CUDA(cudaEventRecord(e0, ctx->stream));
-  for (uint32_t i = 0; i < k; i++) {
-    uint32_t step = i;
-    void *args[] = {&S, &step};
-    PC_CUDA(cudaLaunchCooperativeKernel((void *)k_dist_cover, grid, DT, args, 0, ctx->stream));
-    PC_NCCL(ncclAllGather(S.send, const_cast<unsigned long long *>(S.recv), H_WORDS + cap,
-                          ncclUint64, comm_of(ctx), ctx->stream));
-    PC_CUDA(cudaLaunchCooperativeKernel((void *)k_dist_apply, grid, DT, args, 0, ctx->stream));
+  auto enqueue_loop = [&](cudaStream_t st) {
+    for (uint32_t i = 0; i < k; i++) {
+      uint32_t step = i;
+      void *args[] = {&S, &step};
+      PC_CUDA(cudaLaunchCooperativeKernel((void *)k_dist_cover, grid, DT, args, 0, st));
+      PC_NCCL(ncclAllGather(S.send, const_cast<unsigned long long *>(S.recv), H_WORDS + cap,
+                            ncclUint64, comm_of(ctx), st));
+      PC_CUDA(cudaLaunchCooperativeKernel((void *)k_dist_apply, grid, DT, args, 0, st));
+    }
+  };
+  if (getenv("PACIM_DIST_NOGRAPH")) {
+    enqueue_loop(ctx->stream);
+  } else {
+    // the loop as one CUDA graph (2k cooperative kernels + k all-gathers:
+    // ~70 us of launches per step otherwise), captured on a side stream and
+    // launched on the ctx stream; re-captured when its arguments change
+    std::vector<unsigned char> key(sizeof(S) + 16);
+    memcpy(key.data(), &S, sizeof(S));
+    const uint64_t kw[2] = {(uint64_t)k, (uint64_t)(uintptr_t)ctx->comm};
+    memcpy(key.data() + sizeof(S), kw, 16);
+    if (!ctx->dist_graph || key != ctx->dist_graph_key) {
+      if (ctx->dist_graph) {
+        cudaGraphExecDestroy(reinterpret_cast<cudaGraphExec_t>(ctx->dist_graph));
+        ctx->dist_graph = nullptr;
+      }
+      if (!ctx->dist_cap_stream)
+        PC_CUDA(cudaStreamCreateWithFlags(&ctx->dist_cap_stream, cudaStreamNonBlocking));
+      cudaGraph_t g = nullptr;
+      PC_CUDA(cudaStreamBeginCapture(ctx->dist_cap_stream, cudaStreamCaptureModeRelaxed));
+      try {
+        enqueue_loop(ctx->dist_cap_stream);
+      } catch (...) {
+        cudaStreamEndCapture(ctx->dist_cap_stream, &g);  // leave capture mode
+        if (g) cudaGraphDestroy(g);
+        throw;
+      }
+      PC_CUDA(cudaStreamEndCapture(ctx->dist_cap_stream, &g));
+      cudaGraphExec_t ge = nullptr;
+      PC_CUDA(cudaGraphInstantiate(&ge, g, 0));
+      cudaGraphDestroy(g);
+      ctx->dist_graph = ge;
+      ctx->dist_graph_key = key;
+    }
+    PC_CUDA(cudaGraphLaunch(reinterpret_cast<cudaGraphExec_t>(ctx->dist_graph), ctx->stream));
   }
   PC_CUDA(cudaEventRecord(e1, ctx->stream));
   unsigned long long st[D_WORDS], covn = 0;

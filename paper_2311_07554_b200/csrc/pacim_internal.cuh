@@ -157,6 +157,11 @@ struct pacim_ctx {
   DevBuf dist_cov_old;      // u64: covered root entries of the last fast select
   unsigned long long dist_cov_n = 0;
   bool dist_cov_valid = false;
+  // the fast select's k-step loop captured once as a CUDA graph (per-step
+  // launch overhead), replayed while its arguments are unchanged
+  cudaStream_t dist_cap_stream = nullptr;
+  void *dist_graph = nullptr;              // cudaGraphExec_t
+  std::vector<unsigned char> dist_graph_key;
 
   // ---- graph (H0/H1)
   bool has_graph = false;
