@@ -261,19 +261,21 @@ __global__ void __launch_bounds__(EDGE_THREADS, PACIM_EDGE_BLOCKS) k_edges(const
                 // need not survive it)
         hla.stage(u & ~PACIM_HUBF, v & ~PACIM_HUBF, j, (lv && (u & PACIM_HUBF)) ? 1u : 0u,
                   (lv && (v & PACIM_HUBF)) ? 1u : 0u, w_hla[REC ? wid : 0], hla_n);
-      if (CS == 2) {
-        // mask pass: the lanes of one (row, word) combine (u-side runs are
-        // adjacent), one atomicOr each; the v side is one atomicOr per pair
+      if (CS >= 2) {
         const uint32_t uu = u & ~PACIM_HUBF, vv = v & ~PACIM_HUBF;
-        const unsigned long long ku = lv ? ((unsigned long long)uu << 8 | (j >> 5)) : ~0ull;
-        const uint32_t peers = __match_any_sync(0xffffffffu, ku);
-        const uint32_t bits = __reduce_or_sync(peers, lv ? 1u << (j & 31) : 0u);
-        if (lv && (threadIdx.x & 31) == __ffs(peers) - 1)
-          atomicOr(L + ((size_t)uu * MW + (j >> 5)) * 2 + 1, bits);
-        if (lv) {
-          atomicOr(L + ((size_t)vv * MW + (j >> 5)) * 2 + 1, 1u << (j & 31));
-          live++;
+        if (CS == 2) {
+          // mask pass: the lanes of one (row, word) combine (u-side runs are
+          // adjacent), one atomicOr each; the v side is one atomicOr per pair
+          const unsigned long long ku = lv ? ((unsigned long long)uu << 8 | (j >> 5)) : ~0ull;
+          const uint32_t peers = __match_any_sync(0xffffffffu, ku);
+          const uint32_t bits = __reduce_or_sync(peers, lv ? 1u << (j & 31) : 0u);
+          if (lv && (threadIdx.x & 31) == __ffs(peers) - 1)
+            atomicOr(L + ((size_t)uu * MW + (j >> 5)) * 2 + 1, bits);
+          if (lv) atomicOr(L + ((size_t)vv * MW + (j >> 5)) * 2 + 1, 1u << (j & 31));
         }
+        live += lv;
+        // CS = 3 (edge-partitioned sharded build): the pair list only, slot =
+        // the global sorted slot of the sketch (its owner rank routes it)
         if (pl.p) {  // the pair for the union pass, into the warp's reserved chunk
           const uint32_t lm = __ballot_sync(0xffffffffu, lv);
           const uint32_t nl = __popc(lm);
@@ -304,7 +306,7 @@ __global__ void __launch_bounds__(EDGE_THREADS, PACIM_EDGE_BLOCKS) k_edges(const
     __syncwarp();
   }
   if (REC) hla.flush(w_hla[REC ? wid : 0], hla_n);
-  if (CS == 2 && pl.p)  // the last chunk's holes
+  if (CS >= 2 && pl.p)  // the last chunk's holes
     for (uint32_t q = pl_used + lane; q < PL_CHUNK; q += 32)
       if (pl_base + q < pl.cap) pl.p[pl_base + q] = ~0ull;
   // block-aggregated counter
@@ -1119,6 +1121,35 @@ void pc_cs_mask_edges(pacim_ctx *ctx, uint32_t *rec_words, uint32_t MW, unsigned
   pl.cnt = pcnt;
   pl.cap = cap;
   cs_edges<2>(ctx, rec_words, nullptr, MW, ctr + 1, pl);
+}
+
+// The edge-partitioned pass of a sharded compact build (dist.cu): the upper
+// edges [e0, e1) against all R sketches (the global sorted slot table
+// d_shr_all / d_tab_all), every live (edge, global slot) into the pair list
+// (PL_CHUNK chunks per warp; *pcnt = slots reserved).  ctr[4] += live pairs.
+void pc_ep_edges(pacim_ctx *ctx, uint64_t e0, uint64_t e1, const uint32_t *d_shr_all,
+                 const uint16_t *d_tab_all, uint32_t R, unsigned long long *plist,
+                 unsigned long long *pcnt, unsigned long long cap, unsigned long long *ctr) {
+  PC_REQUIRE(!ctx->lean && !ctx->hash_rule && R <= 256, PACIM_ENOTIMPL,
+             "edge-partitioned build: edge lists, rule R2, R <= 256");
+  if (e1 <= e0) return;
+  PairList pl;
+  pl.p = plist;
+  pl.cnt = pcnt;
+  pl.cap = cap;
+  const uint32_t NT = 1u << PACIM_TB;
+  const size_t smem = R * sizeof(uint32_t) + (NT + 1) * sizeof(uint16_t);
+  const bool pe = ctx->pmodel != PACIM_P_CONST;
+  auto kern = pe ? k_edges<true, false, false, false, 3> : k_edges<false, false, false, false, 3>;
+  PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const uint64_t m = e1 - e0;
+  const unsigned g = pc_grid(ctx, (m + 31) / 32 * 32, EDGE_THREADS, PACIM_EDGE_BLOCKS);
+  kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
+      ctx->keys.as<uint64_t>() + e0, ctx->ckeys.as<uint64_t>() + e0,
+      pe ? ctx->tm1.as<uint32_t>() + e0 : nullptr, m, ctx->K, pe ? ctx->toff() : ctx->t32, d_shr_all,
+      d_tab_all, R, 0, R, nullptr, ctr + 4, Hla{}, nullptr, nullptr, 0u, pl);
+  PC_CHECK_LAUNCH();
+  ctx->launches++;
 }
 
 namespace {

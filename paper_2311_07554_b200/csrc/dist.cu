@@ -32,6 +32,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -354,6 +355,232 @@ __global__ void k_dist_add(long long *gain, long long *delta, uint32_t n) {
 
 // ------------------------------------------------------------------ host
 static ncclComm_t comm_of(pacim_ctx *ctx) { return reinterpret_cast<ncclComm_t>(ctx->comm); }
+
+// ------------------------------------------------ edge-partitioned build
+// Every rank hashing every edge for its own sketches costs each rank the
+// whole edge stream (c4, 32 sketches per rank: a 16 ms mask pass of a 25 ms
+// build).  Instead rank g tests its 1/P of the upper edges against all R
+// sketches (pc_ep_edges), groups the live (edge, sketch) pairs by the
+// sketch's owner (r mod P, the sharding of everything downstream), and the
+// ranks exchange them (ncclSend / ncclRecv; the rank's own part by a device
+// copy).  What each rank receives is exactly the live pairs of its sketches;
+// their bits go into the compact store's masks and the union pass reads
+// them (pc_cs_list_unite).  The exchange is the only collective; every
+// pair moves once.
+namespace {
+constexpr uint32_t EP_TILE = 4096;  // pairs per block of the owner histogram / scatter
+
+// per-owner counts of the pair list (holes ~0 skipped); map[g] = owner << 8 | local slot
+__global__ void __launch_bounds__(256) k_ep_count(const unsigned long long *__restrict__ pl,
+                                                  unsigned long long cnt,
+                                                  const uint32_t *__restrict__ map, uint32_t P,
+                                                  unsigned long long *hist) {
+  __shared__ uint32_t h[256];
+  for (uint32_t o = threadIdx.x; o < P; o += blockDim.x) h[o] = 0;
+  __syncthreads();
+  for (unsigned long long t0 = (unsigned long long)blockIdx.x * EP_TILE; t0 < cnt;
+       t0 += (unsigned long long)gridDim.x * EP_TILE) {
+    const unsigned long long t1 = min(cnt, t0 + EP_TILE);
+    for (unsigned long long i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
+      const unsigned long long x = pl[i];
+      if (x != ~0ull) atomicAdd(&h[map[x & 255u] >> 8], 1u);
+    }
+  }
+  __syncthreads();
+  for (uint32_t o = threadIdx.x; o < P; o += blockDim.x)
+    if (h[o]) atomicAdd(hist + o, (unsigned long long)h[o]);
+}
+
+// the pairs into their owner's segment (cursor[o] starts at its offset),
+// slot field = the owner's local slot; one global add per (tile, owner)
+__global__ void __launch_bounds__(256) k_ep_scatter(const unsigned long long *__restrict__ pl,
+                                                    unsigned long long cnt,
+                                                    const uint32_t *__restrict__ map, uint32_t P,
+                                                    unsigned long long *cursor,
+                                                    unsigned long long *out) {
+  __shared__ uint32_t h[256];
+  __shared__ unsigned long long base[256];
+  for (unsigned long long t0 = (unsigned long long)blockIdx.x * EP_TILE; t0 < cnt;
+       t0 += (unsigned long long)gridDim.x * EP_TILE) {
+    const unsigned long long t1 = min(cnt, t0 + EP_TILE);
+    for (uint32_t o = threadIdx.x; o < P; o += blockDim.x) h[o] = 0;
+    __syncthreads();
+    for (unsigned long long i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
+      const unsigned long long x = pl[i];
+      if (x != ~0ull) atomicAdd(&h[map[x & 255u] >> 8], 1u);
+    }
+    __syncthreads();
+    for (uint32_t o = threadIdx.x; o < P; o += blockDim.x) {
+      base[o] = h[o] ? atomicAdd(cursor + o, (unsigned long long)h[o]) : 0ull;
+      h[o] = 0;
+    }
+    __syncthreads();
+    for (unsigned long long i = t0 + threadIdx.x; i < t1; i += blockDim.x) {
+      const unsigned long long x = pl[i];
+      if (x == ~0ull) continue;
+      const uint32_t mo = map[x & 255u], o = mo >> 8;
+      out[base[o] + atomicAdd(&h[o], 1u)] = (x & ~255ull) | (mo & 255u);
+    }
+    __syncthreads();
+  }
+}
+
+// the received pairs' bits in both endpoints' row masks (rec .y words)
+__global__ void k_ep_mask(const unsigned long long *__restrict__ pl, unsigned long long cnt,
+                          uint32_t *rec_words, uint32_t MW) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const unsigned long long x = pl[i];
+    const uint32_t u = (uint32_t)(x >> 36), v = (uint32_t)(x >> 8) & 0x0FFFFFFFu, j = (uint32_t)x & 255u;
+    atomicOr(rec_words + ((size_t)u * MW + (j >> 5)) * 2 + 1, 1u << (j & 31));
+    atomicOr(rec_words + ((size_t)v * MW + (j >> 5)) * 2 + 1, 1u << (j & 31));
+  }
+}
+}  // namespace
+
+unsigned long long pc_cs_ep_pairs(pacim_ctx *ctx, uint32_t MW, unsigned long long *ctr) {
+  const uint32_t R = ctx->R, P = ctx->world, rank = ctx->rank;
+  if (!pc_dist_active(ctx) || ctx->lean || ctx->hash_rule || R > 256 || ctx->nr >= (1u << 28) ||
+      (getenv("PACIM_EP") && !atoi(getenv("PACIM_EP"))) || (P == 1 && !getenv("PACIM_EP")))
+    return ~0ull;  // (at one rank only on request: the plain list build is the same work)
+  // global slot table (all R sketches, sorted by hi32(hash(r)), then r) and
+  // for each global slot its owner and the owner's local slot (its rank
+  // among the owner's sketches in the same order: pc_slot_table's)
+  std::vector<std::pair<uint64_t, uint32_t>> hs(R);
+  for (uint32_t r = 0; r < R; r++) hs[r] = {pc_mix64(((1ull << 63) | (uint64_t)r) ^ ctx->K), r};
+  std::sort(hs.begin(), hs.end(), [](const std::pair<uint64_t, uint32_t> &a,
+                                     const std::pair<uint64_t, uint32_t> &b) {
+    return (a.first >> 32) != (b.first >> 32) ? (a.first >> 32) < (b.first >> 32) : a.second < b.second;
+  });
+  const uint32_t NT = 1u << PACIM_TB;
+  std::vector<uint32_t> tab32((size_t)2 * R + (NT + 2) / 2, 0);
+  uint32_t *shr = tab32.data();
+  uint16_t *tab = reinterpret_cast<uint16_t *>(shr + R);
+  uint32_t *map = shr + R + (NT + 2) / 2;
+  std::vector<uint32_t> seen(P, 0);
+  for (uint32_t g = 0; g < R; g++) {
+    shr[g] = (uint32_t)(hs[g].first >> 32);
+    const uint32_t o = hs[g].second % P;
+    map[g] = o << 8 | seen[o]++;
+  }
+  for (uint32_t p = 0, g = 0; p <= NT; p++) {
+    while (g < R && (shr[g] >> (32 - PACIM_TB)) < p) g++;
+    tab[p] = (uint16_t)g;
+  }
+  PC_REQUIRE(seen[rank] == ctx->R_local, PACIM_ECHECK, "edge-partitioned build: owner map");
+  pc_ensure(ctx, ctx->ep_tab, tab32.size() * 4);
+  PC_CUDA(cudaMemcpyAsync(ctx->ep_tab.p, tab32.data(), tab32.size() * 4, cudaMemcpyHostToDevice,
+                          ctx->stream));
+  const uint32_t *d_shr = ctx->ep_tab.as<uint32_t>();
+  const uint16_t *d_tab = reinterpret_cast<const uint16_t *>(d_shr + R);
+  const uint32_t *d_map = d_shr + R + (NT + 2) / 2;
+  // counters: [0] list slots reserved, [1, 1+P) per-owner counts, then
+  // cursors (P), then all ranks' counts (P x P)
+  pc_ensure(ctx, ctx->ep_cnt, (1 + 2 * (size_t)P + (size_t)P * P) * 8);
+  unsigned long long *c = ctx->ep_cnt.as<unsigned long long>();
+  unsigned long long *cown = c + 1, *cur = cown + P, *call = cur + P;
+  // this rank's 1/P of the upper edges, all sketches, into the pair list
+  const uint64_t m = ctx->m, e0 = m * rank / P, e1 = m * (rank + 1) / P;
+  const bool same = ctx->ep_gen == ctx->graph_gen && ctx->ep_K == ctx->K;
+  unsigned long long cap = same ? ctx->ep_hint + ctx->ep_hint / 16 + (1ull << 22) : 0;
+  if (const char *e = getenv("PACIM_EP_CAP")) cap = std::max(1LL, atoll(e));  // tests: overflow
+  if (!cap) {
+    size_t fr = 0, tot = 0;
+    pc_mem_info(ctx, &fr, &tot);
+    fr += ctx->cs_plist.bytes;
+    cap = std::min<unsigned long long>(fr / 6 / 8, 1ull << 33);
+  }
+  // phase marks (PACIM_BUILD_TIMES=1: printed to stderr)
+  const bool times = getenv("PACIM_BUILD_TIMES") != nullptr;
+  cudaEvent_t ev[5] = {};
+  if (times)
+    for (auto &e : ev) PC_CUDA(cudaEventCreate(&e));
+  if (times) PC_CUDA(cudaEventRecord(ev[0], ctx->stream));
+  unsigned long long reserved = 0;
+  for (int attempt = 0; attempt < 2; attempt++) {
+    if (ctx->cs_plist.bytes < cap * 8) {
+      pc_free(ctx, ctx->cs_plist);
+      pc_ensure(ctx, ctx->cs_plist, cap * 8);
+    }
+    PC_CUDA(cudaMemsetAsync(c, 0, (1 + 2 * (size_t)P) * 8, ctx->stream));
+    // (its live count, pairs of every rank's sketches, goes to a scratch
+    // counter: the rank's own live pairs are what it receives)
+    pc_ep_edges(ctx, e0, e1, d_shr, d_tab, R, ctx->cs_plist.as<unsigned long long>(), c, cap,
+                ctr + 20);
+    PC_CUDA(cudaMemcpyAsync(&reserved, c, 8, cudaMemcpyDeviceToHost, ctx->stream));
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (reserved <= cap) break;
+    PC_REQUIRE(attempt == 0, PACIM_ECHECK, "edge-partitioned build: pair list overflow twice");
+    cap = reserved;  // exact: every warp reserved its chunks (the pass is repeated)
+  }
+  ctx->ep_hint = reserved;
+  ctx->ep_gen = ctx->graph_gen;
+  ctx->ep_K = ctx->K;
+  if (times) PC_CUDA(cudaEventRecord(ev[1], ctx->stream));
+  // group by owner
+  const unsigned long long *pl = ctx->cs_plist.as<unsigned long long>();
+  const unsigned tg = pc_grid(ctx, (reserved + EP_TILE - 1) / EP_TILE * 256, 256, 4);
+  k_ep_count<<<tg, 256, 0, ctx->stream>>>(pl, reserved, d_map, P, cown);
+  PC_CHECK_LAUNCH();
+  std::vector<unsigned long long> sc(P), so(P + 1, 0);
+  PC_CUDA(cudaMemcpyAsync(sc.data(), cown, (size_t)P * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  for (uint32_t o = 0; o < P; o++) so[o + 1] = so[o] + sc[o];
+  pc_ensure(ctx, ctx->ep_send, std::max<unsigned long long>(so[P], 1) * 8);
+  unsigned long long *send = ctx->ep_send.as<unsigned long long>();
+  PC_CUDA(cudaMemcpyAsync(cur, so.data(), (size_t)P * 8, cudaMemcpyHostToDevice, ctx->stream));
+  k_ep_scatter<<<tg, 256, 0, ctx->stream>>>(pl, reserved, d_map, P, cur, send);
+  PC_CHECK_LAUNCH();
+  if (times) PC_CUDA(cudaEventRecord(ev[2], ctx->stream));
+  // every rank's per-owner counts -> what this rank receives from each
+  std::vector<unsigned long long> all((size_t)P * P);
+  PC_NCCL(ncclAllGather(cown, call, P, ncclUint64, comm_of(ctx), ctx->stream));
+  PC_CUDA(cudaMemcpyAsync(all.data(), call, (size_t)P * P * 8, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::vector<unsigned long long> ro(P + 1, 0);
+  for (uint32_t q = 0; q < P; q++) ro[q + 1] = ro[q] + all[(size_t)q * P + rank];
+  const unsigned long long total = ro[P];
+  PC_REQUIRE(all[(size_t)rank * P + rank] == sc[rank], PACIM_ECHECK, "edge-partitioned build: counts");
+  // the receive buffer is the pair list (its pairs were scattered to send)
+  if (ctx->cs_plist.bytes < std::max<unsigned long long>(total, 1) * 8) {
+    pc_free(ctx, ctx->cs_plist);
+    pc_ensure(ctx, ctx->cs_plist, std::max<unsigned long long>(total, 1) * 8);
+  }
+  unsigned long long *recv = ctx->cs_plist.as<unsigned long long>();
+  if (sc[rank])
+    PC_CUDA(cudaMemcpyAsync(recv + ro[rank], send + so[rank], sc[rank] * 8, cudaMemcpyDeviceToDevice,
+                            ctx->stream));
+  if (P > 1) {
+    PC_NCCL(ncclGroupStart());
+    for (uint32_t q = 0; q < P; q++) {
+      if (q == rank) continue;
+      if (sc[q]) PC_NCCL(ncclSend(send + so[q], sc[q], ncclUint64, (int)q, comm_of(ctx), ctx->stream));
+      const unsigned long long rq = ro[q + 1] - ro[q];
+      if (rq) PC_NCCL(ncclRecv(recv + ro[q], rq, ncclUint64, (int)q, comm_of(ctx), ctx->stream));
+    }
+    PC_NCCL(ncclGroupEnd());
+  }
+  if (times) PC_CUDA(cudaEventRecord(ev[3], ctx->stream));
+  // the pairs' bits in the row masks (the compact store's entries)
+  if (total)
+    k_ep_mask<<<pc_grid(ctx, total, 256, 8), 256, 0, ctx->stream>>>(recv, total,
+                                                                  ctx->cs_rec.as<uint32_t>(), MW);
+  PC_CHECK_LAUNCH();
+  ctx->launches += 3;
+  if (times) {
+    PC_CUDA(cudaEventRecord(ev[4], ctx->stream));
+    PC_CUDA(cudaEventSynchronize(ev[4]));
+    float t[4];
+    for (int i = 0; i < 4; i++) cudaEventElapsedTime(&t[i], ev[i], ev[i + 1]);
+    fprintf(stderr,
+            "ep pairs ms: pass %.3f (edges %llu of %llu, list %llu) group %.3f (%llu pairs) exchange "
+            "%.3f (recv %llu) masks %.3f\n",
+            t[0], (unsigned long long)(e1 - e0), (unsigned long long)m, reserved, t[1], so[P], t[2],
+            total, t[3]);
+    for (auto &e : ev) cudaEventDestroy(e);
+  }
+  return total;
+}
 
 void pc_nccl_unique_id(void *out) {
   static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");

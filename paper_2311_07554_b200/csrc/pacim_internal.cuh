@@ -159,6 +159,11 @@ struct pacim_ctx {
   bool dist_cov_valid = false;
   // the fast select's k-step loop captured once as a CUDA graph (per-step
   // launch overhead), replayed while its arguments are unchanged
+  DevBuf ep_tab;            // edge-partitioned build: global slot table, owner map
+  DevBuf ep_send;           // ... the pairs grouped by owner rank
+  DevBuf ep_cnt;            // ... per-owner counts / cursors, all ranks' counts
+  unsigned long long ep_hint = 0;  // list slots the last EP pass reserved (same graph, key)
+  uint64_t ep_gen = ~0ull, ep_K = 0;
   cudaStream_t dist_cap_stream = nullptr;
   void *dist_graph = nullptr;              // cudaGraphExec_t
   std::vector<unsigned char> dist_graph_key;
@@ -342,6 +347,15 @@ void pc_cs_edges(pacim_ctx *ctx, uint32_t *P, const uint2 *rec, uint32_t MW,
                  unsigned long long *ctr);
 void pc_cs_mask_edges(pacim_ctx *ctx, uint32_t *rec_words, uint32_t MW, unsigned long long *ctr,
                       unsigned long long *plist, unsigned long long *pcnt, unsigned long long cap);
+void pc_ep_edges(pacim_ctx *ctx, uint64_t e0, uint64_t e1, const uint32_t *d_shr_all,
+                 const uint16_t *d_tab_all, uint32_t R, unsigned long long *plist,
+                 unsigned long long *pcnt, unsigned long long cap, unsigned long long *ctr);
+// dist.cu: the edge-partitioned live pairs of a sharded compact build —
+// this rank's edge range tested against all R sketches, routed to the
+// sketches' owners (NCCL send/recv); the rank's pairs (local slots) land in
+// ctx->cs_plist and their bits in the rec masks.  Returns their count, or
+// ~0 if the build cannot take this path.
+unsigned long long pc_cs_ep_pairs(pacim_ctx *ctx, uint32_t MW, unsigned long long *ctr);
 void pc_cs_list_unite(pacim_ctx *ctx, uint32_t *E, const uint2 *rec, uint32_t MW,
                       const unsigned long long *plist, unsigned long long cnt,
                       unsigned long long *ctr, const unsigned long long *mask_live);

@@ -949,9 +949,19 @@ bool pc_cs_build(pacim_ctx *ctx) {
       pc_ensure(ctx, ctx->cs_plist, pcap * 8);
     }
   }
-  if (nnz)  // the upper edges (the k_edges scheme): both endpoints' bits per live pair
+  // a sharded build with a communicator: the edge-partitioned pairs (each
+  // rank tests 1/P of the edges against all sketches, NCCL routes the pairs
+  // to the sketches' owners; dist.cu) instead of every rank's full mask pass
+  const unsigned long long ep = nnz ? pc_cs_ep_pairs(ctx, MW, ctr) : ~0ull;
+  if (ep != ~0ull) {
+    pcap = std::max<unsigned long long>(ep, 1);  // the union pass reads the received pairs
+    const unsigned long long two[1] = {ep};
+    PC_CUDA(cudaMemcpyAsync(ctr + 13, two, 8, cudaMemcpyHostToDevice, ctx->stream));  // live
+    PC_CUDA(cudaMemcpyAsync(ctr + 16, two, 8, cudaMemcpyHostToDevice, ctx->stream));  // list
+  } else if (nnz) {  // the upper edges (the k_edges scheme): both endpoints' bits per live pair
     pc_cs_mask_edges(ctx, ctx->cs_rec.as<uint32_t>(), MW, ctr + 8,
                      pcap ? ctx->cs_plist.as<unsigned long long>() : nullptr, ctr + 16, pcap);
+  }
   mark("mask");
   // ---- counts -> entry offsets (build scratch kept by the ctx)
   pc_ensure(ctx, ctx->cs_cnt, 2 * ((size_t)nr + 1) * 8);

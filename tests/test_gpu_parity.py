@@ -728,6 +728,48 @@ def test_dist_select_world1(orc, pc, i, env, monkeypatch):
         c.close()
 
 
+@pytest.mark.parametrize("i,env", [
+    (0, {}), (2, {}), (3, {}), (7, {}), (9, {}), (10, {}), (12, {}),
+    (7, {"PACIM_EP_CAP": "100"}),                  # pair list overflow: the pass repeated
+    (12, {"PACIM_NO_HOT": "1", "PACIM_BIG_T": "50"}),
+])
+def test_dist_edge_partitioned_world1(orc, pc, i, env, monkeypatch):
+    """The edge-partitioned sharded build (dist.cu pc_cs_ep_pairs: the rank's
+    edge range against all sketches, pairs routed to the sketches' owners,
+    the compact store built from the received pairs) at world 1 (PACIM_EP=1):
+    labels of every sketch, gain0, the live-pair count of the mask-pass build,
+    and the oracle's greedy through the NCCL select."""
+    monkeypatch.setenv("PACIM_FORCE_DIST", "1")
+    monkeypatch.setenv("PACIM_STORE", "compact")
+    for k_, v_ in env.items():
+        monkeypatch.setenv(k_, v_)
+    from oracle.oracle import Graph
+    build_fn, p, R, k = CASES[i]
+    off, nbr = build_fn()
+    g = Graph(len(off) - 1, off, nbr)
+    model, t32 = model_of(orc, p)
+    k = min(k, g.n)
+    c = _dist_ctx(pc)
+    try:
+        c.pacim_load_graph(g.off, g.nbr, model, t32, 1)
+        c.pacim_build_sketches(R, 1000 + i, 1 << 32, 0, 1)
+        live = c.pacim_get_stats()["live_pairs"]
+        monkeypatch.setenv("PACIM_EP", "1")
+        c.pacim_build_sketches(R, 1000 + i, 1 << 32, 0, 1)
+        st = c.pacim_get_stats()
+        assert st["live_pairs"] == live
+        if st["store"] == 1:
+            for r in range(R):
+                lab, _ = orc.sketch_labels(g, model, t32, 1000 + i, r)
+                assert np.array_equal(c.pacim_get_labels(r), lab), r
+        es, egn, esg, eg0 = orc.greedy(g, model, t32, R, 1000 + i, k, want_gain0=True)
+        assert np.array_equal(c.pacim_get_gain0(), eg0)
+        s, gn, sg, _ = c.pacim_select_seeds(k)
+        assert list(s) == list(es) and list(gn) == list(egn) and list(sg) == list(esg)
+    finally:
+        c.close()
+
+
 def test_dist_select_world1_compressed(orc, pc, monkeypatch):
     """Compressed store (Alg. 3) under the sharded select: robust path."""
     monkeypatch.setenv("PACIM_FORCE_DIST", "1")
