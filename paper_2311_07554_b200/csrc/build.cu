@@ -73,14 +73,17 @@ __global__ void k_init(uint32_t *L, uint32_t n, uint32_t B) {
 // CC is its minimum id (R8).  Two independent loads per step; the walk stops
 // as soon as the two paths meet.  A root slot holds ROOT1 (read as itself).
 __device__ __forceinline__ void uf_unite(uint32_t *L, uint32_t B, uint32_t j, uint32_t u,
-                                         uint32_t v) {
+                                         uint32_t v, Ep ep = Ep{}) {
+  // ep: slot epochs (a stale slot is a root; every write carries ep.tag and
+  // every CAS expects the raw word it read)
   uint32_t *Lj = L + j;
   for (;;) {
-    uint32_t pu = ld_cg(Lj + (size_t)u * B);
-    uint32_t pv = ld_cg(Lj + (size_t)v * B);
+    const uint32_t ru = ld_cg(Lj + (size_t)u * B), rv = ld_cg(Lj + (size_t)v * B);
+    uint32_t pu = ep_rd(ru, ep), pv = ep_rd(rv, ep);
     if (pu & PACIM_HIGH) pu = u;
     if (pv & PACIM_HIGH) pv = v;
     if (pu == pv) return;
+    uint32_t raw = ru;  // the word of the side that moves (u after the swap)
     if (pu < pv) {
       uint32_t t = u;
       u = v;
@@ -88,12 +91,13 @@ __device__ __forceinline__ void uf_unite(uint32_t *L, uint32_t B, uint32_t j, ui
       t = pu;
       pu = pv;
       pv = t;
+      raw = rv;
     }
     // now pu > pv
     if (u == pu) {
-      if (atomicCAS(Lj + (size_t)u * B, ROOT1, pv) == ROOT1) return;  // hook root u under pv
+      if (atomicCAS(Lj + (size_t)u * B, raw, pv | ep.tag) == raw) return;  // hook root u under pv
     } else {
-      atomicCAS(Lj + (size_t)u * B, pu, pv);  // splice (may lose a race harmlessly)
+      atomicCAS(Lj + (size_t)u * B, raw, pv | ep.tag);  // splice (may lose a race harmlessly)
       u = pu;
     }
   }
@@ -132,7 +136,7 @@ struct PairList {
 // L = the {P, next} words of the entries, (row, slot) = entry
 // pc_cs_pos(rec, MW, row, slot); CS = 2: the mask pass, every live (edge,
 // slot) sets bit slot of both endpoints' row masks (L = the rec words)
-template <bool WIC, bool REC, bool DECOR, bool LEAN, int CS = 0>
+template <bool WIC, bool REC, bool DECOR, bool LEAN, int CS = 0, bool EP = false>
 __global__ void __launch_bounds__(EDGE_THREADS, PACIM_EDGE_BLOCKS) k_edges(const uint64_t *__restrict__ keys,
                                                         const uint64_t *__restrict__ ckeys,
                                                         const uint32_t *__restrict__ tm1,
@@ -144,7 +148,7 @@ __global__ void __launch_bounds__(EDGE_THREADS, PACIM_EDGE_BLOCKS) k_edges(const
                                                         unsigned long long *live_ctr, Hla hla,
                                                         const uint64_t *__restrict__ hr64,
                                                         const uint2 *__restrict__ rec,
-                                                        uint32_t MW, PairList pl) {
+                                                        uint32_t MW, PairList pl, Ep ep) {
   // slots [j0, j0 + Bb) of the B sorted slots go to L (row stride Bb)
   extern __shared__ uint32_t sm[];
   uint32_t *shr = sm;
@@ -299,7 +303,7 @@ __global__ void __launch_bounds__(EDGE_THREADS, PACIM_EDGE_BLOCKS) k_edges(const
           uf_unite(L, 2, 0, pc_cs_pos(rec, MW, u & ~PACIM_HUBF, j),
                    pc_cs_pos(rec, MW, v & ~PACIM_HUBF, j));
         else
-          uf_unite(L, Bb, j - j0, u & ~PACIM_HUBF, v & ~PACIM_HUBF);
+          uf_unite(L, Bb, j - j0, u & ~PACIM_HUBF, v & ~PACIM_HUBF, EP ? ep : Ep{});
         live++;
       }
     }
@@ -322,9 +326,9 @@ __global__ void __launch_bounds__(EDGE_THREADS, PACIM_EDGE_BLOCKS) k_edges(const
 // ---------------------------------------------------------- hot roots
 // read-only find that also stops at a converted root slot (HIGH set)
 __device__ __forceinline__ uint32_t find_ro(const uint32_t *L, uint32_t B, uint32_t j,
-                                            uint32_t x) {
+                                            uint32_t x, Ep ep = Ep{}) {
   for (;;) {
-    uint32_t p = ld_cg(L + (size_t)x * B + j);
+    const uint32_t p = ep_rd(ld_cg(L + (size_t)x * B + j), ep);
     if (p == x || (p & PACIM_HIGH)) return x;
     x = p;
   }
@@ -333,21 +337,30 @@ __device__ __forceinline__ uint32_t find_ro(const uint32_t *L, uint32_t B, uint3
 // find with path halving for compress_count: every write is an atomicMin, so
 // a slot only ever moves towards its root (ids decrease along parent
 // pointers) and racing halvings can never undo an owner's full compression.
-__device__ __forceinline__ uint32_t find_halve(uint32_t *L, uint32_t B, uint32_t j, uint32_t x) {
+// ep: slot epochs; *root_raw = the root slot's word as read (stale: the root
+// was never written in this build — add_to_root makes it current first)
+__device__ __forceinline__ uint32_t find_halve(uint32_t *L, uint32_t B, uint32_t j, uint32_t x,
+                                               Ep ep = Ep{}, uint32_t *root_raw = nullptr) {
   for (;;) {
-    uint32_t p = ld_cg(L + (size_t)x * B + j);
-    if (p == x || (p & PACIM_HIGH)) return x;
-    uint32_t gp = ld_cg(L + (size_t)p * B + j);
-    if (gp == p || (gp & PACIM_HIGH)) return p;
-    atomicMin(L + (size_t)x * B + j, gp);
+    const uint32_t rp = ld_cg(L + (size_t)x * B + j), p = ep_rd(rp, ep);
+    if (p == x || (p & PACIM_HIGH)) {
+      if (root_raw) *root_raw = rp;
+      return x;
+    }
+    const uint32_t rg = ld_cg(L + (size_t)p * B + j), gp = ep_rd(rg, ep);
+    if (gp == p || (gp & PACIM_HIGH)) {
+      if (root_raw) *root_raw = rg;
+      return p;
+    }
+    atomicMin(L + (size_t)x * B + j, gp | ep.tag);  // same epoch bits: the min of the ids
     x = gp;
   }
 }
 
 __global__ void k_hot_roots(const uint32_t *L, uint32_t nr, uint32_t B, uint32_t hub,
-                            uint32_t *hot) {
+                            uint32_t *hot, Ep ep) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < B; j += gridDim.x * blockDim.x)
-    hot[j] = hub < nr ? find_ro(L, B, j, hub) : NONE;
+    hot[j] = hub < nr ? find_ro(L, B, j, hub, ep) : NONE;
 }
 
 // ------------------------------------------------------ k_compress_count
@@ -358,10 +371,22 @@ __global__ void k_hot_roots(const uint32_t *L, uint32_t nr, uint32_t B, uint32_t
 // and added once per block.  ctr[1] += non-roots (the CCs of size >= 2 are
 // counted into ctr[0] by the gain pass that reads every root slot anyway).
 __device__ __forceinline__ void add_to_root(uint32_t *L, uint32_t B, uint32_t j, uint32_t root,
-                                            uint32_t cnt) {
-  // the root slot is HIGH | size already (ROOT1 from k_init): one atomic whose
-  // result is not waited for (the CCs are counted by the gain pass)
-  atomicAdd(L + (size_t)root * B + j, cnt);
+                                            uint32_t cnt, Ep ep = Ep{}, uint32_t root_raw = 0) {
+  uint32_t *a = L + (size_t)root * B + j;
+  if ((root_raw & ep.mask) != ep.tag) {
+    // a stale root slot (a singleton until this build): HIGH | 1 of this
+    // epoch first (racing members: the first CAS wins, the others see a
+    // current word)
+    uint32_t x = root_raw;
+    for (;;) {
+      const uint32_t y = atomicCAS(a, x, (PACIM_HIGH | 1u) | ep.tag);
+      if (y == x || (y & ep.mask) == ep.tag) break;
+      x = y;
+    }
+  }
+  // the root slot is HIGH | size (ROOT1 from k_init or the line above): one
+  // atomic whose result is not waited for (the CCs are counted by the gain pass)
+  atomicAdd(a, cnt);
 }
 
 // warp-reduced counter update (lane 0 adds)
@@ -371,10 +396,11 @@ __device__ __forceinline__ void add_count(unsigned long long *ctr, unsigned long
 }
 
 constexpr uint32_t CLCAP = 256 + 31;  // pending finds per warp: < 32 carried + one 256-slot block
-template <bool COMPACT>
+template <bool COMPACT, bool EP>
 __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n, uint32_t B,
                                                         const uint32_t *hot,
-                                                        unsigned long long *ctr) {
+                                                        unsigned long long *ctr, Ep ep_in) {
+  const Ep ep = EP ? ep_in : Ep{};  // without epochs every epoch operation folds away
   extern __shared__ uint32_t hsm[];
   __shared__ uint32_t cl_v[COMPACT ? 8 : 1][COMPACT ? CLCAP : 1],
       cl_j[COMPACT ? 8 : 1][COMPACT ? CLCAP : 1], cl_s[COMPACT ? 8 : 1][COMPACT ? CLCAP : 1];
@@ -403,12 +429,13 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
       const uint32_t k = base + lane;
       if (k < cnt) {
         const uint32_t v = cv[k], j = cj[k], s = cs[k];
-        const uint32_t root = find_halve(L, B, j, s);
-        if (root != s) atomicMin(L + (size_t)v * B + j, root);
+        uint32_t rr = 0;
+        const uint32_t root = find_halve(L, B, j, s, ep, &rr);
+        if (root != s) atomicMin(L + (size_t)v * B + j, root | ep.tag);
         if (j < H && root == hroot[j])
           atomicAdd(hcnt + j, 1u);
         else
-          add_to_root(L, B, j, root, 1u);
+          add_to_root(L, B, j, root, 1u, ep, rr);
       }
     }
     __syncwarp();
@@ -420,13 +447,14 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
 #pragma unroll
       for (int i = 0; i < 8; i++) {
         uint32_t j = j0 + lane + 32 * i;
-        sv[i] = j < B ? ld_cg(L + v * B + j) : ROOT1;  // past B: skipped as a root
+        sv[i] = j < B ? ld_cg(L + v * B + j) : PACIM_HIGH;  // past B: skipped as a root
       }
 #pragma unroll
       for (int i = 0; i < 8; i++) {
         const uint32_t j = j0 + lane + 32 * i;
-        const uint32_t s = sv[i];
-        const bool nonroot = !(s & PACIM_HIGH);
+        // a member of this epoch (stale slots and roots need nothing)
+        const bool nonroot = (sv[i] & (PACIM_HIGH | ep.mask)) == ep.tag;
+        const uint32_t s = sv[i] & ~ep.mask;
         // parent already the hot root: no walk (the common case for members
         // of the giant CC)
         const bool hotp = nonroot && j < H && s == hroot[j];
@@ -435,12 +463,13 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
         const bool need = nonroot && !hotp;
         if (!COMPACT) {  // dense stores (c3): each lane walks its slots' chains in turn
           if (need) {
-            const uint32_t root = find_halve(L, B, j, s);
-            if (root != s) atomicMin(L + v * B + j, root);
+            uint32_t rr = 0;
+            const uint32_t root = find_halve(L, B, j, s, ep, &rr);
+            if (root != s) atomicMin(L + v * B + j, root | ep.tag);
             if (j < H && root == hroot[j])
               atomicAdd(hcnt + j, 1u);
             else
-              add_to_root(L, B, j, root, 1u);
+              add_to_root(L, B, j, root, 1u, ep, rr);
           }
           continue;
         }
@@ -459,7 +488,8 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
   if (COMPACT) flush();
   __syncthreads();
   for (uint32_t j = threadIdx.x; j < H; j += blockDim.x)
-    if (hcnt[j]) add_to_root(L, B, j, hroot[j], hcnt[j]);
+    if (hcnt[j])
+      add_to_root(L, B, j, hroot[j], hcnt[j], ep, ld_cg(L + (size_t)hroot[j] * B + j));
   for (int d = 16; d; d >>= 1) nnr += __shfl_xor_sync(0xffffffffu, nnr, d);
   __shared__ unsigned long long s1;
   if (threadIdx.x == 0) s1 = 0;
@@ -478,12 +508,13 @@ constexpr int GR_PLAIN = 4;  // rows per warp iteration in k_gain0 (4 KB of slot
 // HOT: also hotsum[v] = the sizes of the hot (hub's) CCs above big_t that
 // contain v — the select covers them by one vector pass when they are
 // exactly the step's dense set (k_select phase D)
-template <bool HOT>
+template <bool HOT, bool EP>
 __global__ void __launch_bounds__(256) k_gain0(const uint32_t *__restrict__ L, uint32_t n,
                                                uint32_t B, const uint32_t *rmap, int64_t *gain0,
                                                int acc, unsigned long long *ncc_ctr,
                                                const uint32_t *hot, const uint32_t *hot_size,
-                                               uint32_t big_t, int64_t *hotsum) {
+                                               uint32_t big_t, int64_t *hotsum, Ep ep_in) {
+  const Ep ep = EP ? ep_in : Ep{};
   constexpr int GR = HOT ? 2 : GR_PLAIN;  // fewer rows in flight: the hot sums' registers
   unsigned long long ncc = 0;  // roots of size >= 2: the non-singleton CCs
   extern __shared__ uint32_t hsm[];
@@ -514,28 +545,35 @@ __global__ void __launch_bounds__(256) k_gain0(const uint32_t *__restrict__ L, u
           sv[r][i] = (j < B && v0 + r < n) ? L[(v0 + r) * B + j] : NONE;
         }
       // a non-root slot becomes its root's HIGH | size: the root loads of
-      // both rows in flight together
+      // both rows in flight together (raw words: the epoch bits are masked
+      // off in the sum, a stale slot becomes HIGH | 1 of this epoch)
 #pragma unroll
       for (int r = 0; r < GR; r++)
 #pragma unroll
         for (int i = 0; i < 8; i++) {
           const uint32_t j = j0 + lane + 32 * i;
-          const uint32_t s = sv[r][i];
-          if (s == NONE) continue;
+          const uint32_t raw = sv[r][i];
+          if (raw == NONE) continue;
+          const bool cur = (raw & ep.mask) == ep.tag;
+          const bool nonroot = cur && !(raw & PACIM_HIGH);
+          const uint32_t s = raw & ~ep.mask;
           if (HOT && j < H && hsz[j]) {  // a member of slot j's giant hot CC
-            const uint32_t root = (s & PACIM_HIGH) ? (uint32_t)(v0 + r) : s;
+            const uint32_t root = nonroot ? s : (uint32_t)(v0 + r);
             if (root == hroot[j]) hs[r] += hsz[j];
           }
-          if (s & PACIM_HIGH)
-            ncc += (s & PACIM_LOW) >= 2;
-          else
-            sv[r][i] = __ldg(L + (size_t)s * B + j);
+          if (!nonroot) {
+            ncc += cur && (s & PACIM_LOW) >= 2;
+            if (!cur) sv[r][i] = (PACIM_HIGH | 1u) | ep.tag;
+          } else {
+            sv[r][i] = __ldg(L + (size_t)s * B + j);  // the root's word (of this epoch)
+          }
         }
+      const uint32_t szm = PACIM_LOW & ~ep.mask;
 #pragma unroll
       for (int r = 0; r < GR; r++)
 #pragma unroll
         for (int i = 0; i < 8; i++)
-          if (sv[r][i] != NONE) g[r] += sv[r][i] & PACIM_LOW;
+          if (sv[r][i] != NONE) g[r] += sv[r][i] & szm;
     }
 #pragma unroll
     for (int r = 0; r < GR; r++) {
@@ -563,13 +601,14 @@ __global__ void __launch_bounds__(256) k_gain0(const uint32_t *__restrict__ L, u
 // entries (j >= B, rows past n) read as HIGH | 0 — a root of size 0, never a
 // stored value — so no entry needs a validity test (the HOT pass was issue
 // bound: 73 % SM throughput at c2 / c3 in ncu)
-template <int GR, bool HOT>
-__global__ void __launch_bounds__(256, GR == 2 ? 4 : 2) k_gain0_fast(const uint32_t *__restrict__ L, uint32_t n,
+template <int GR, bool HOT, bool EP>
+__global__ void __launch_bounds__(256, GR == 2 ? (EP ? 3 : 4) : 2) k_gain0_fast(const uint32_t *__restrict__ L, uint32_t n,
                                                    uint32_t B, const uint32_t *rmap,
                                                    int64_t *gain0, unsigned long long *ncc_ctr,
                                                    const uint32_t *hot, const uint32_t *hot_size,
-                                                   uint32_t big_t, int64_t *hotsum) {
-  constexpr uint32_t VOID = PACIM_HIGH;  // HIGH | 0
+                                                   uint32_t big_t, int64_t *hotsum, Ep ep_in) {
+  const Ep ep = EP ? ep_in : Ep{};
+  const uint32_t VOID = PACIM_HIGH | ep.tag;  // HIGH | 0 of this epoch
   const int lane = threadIdx.x & 31;
   uint32_t hr[8], hz[8];
 #pragma unroll
@@ -600,14 +639,18 @@ __global__ void __launch_bounds__(256, GR == 2 ? 4 : 2) k_gain0_fast(const uint3
       hs[r] = 0;
 #pragma unroll
       for (int i = 0; i < 8; i++) {
-        const uint32_t s = sv[r][i];
-        const bool isroot = (s & PACIM_HIGH) != 0;
+        const uint32_t raw = sv[r][i];
+        const bool cur = (raw & ep.mask) == ep.tag;
+        const uint32_t s = raw & ~ep.mask;
+        const bool isroot = !cur || (raw & PACIM_HIGH) != 0;  // stale: a singleton root
         const uint32_t root = isroot ? (uint32_t)(v0 + r) : s;
         if (HOT) hs[r] += root == hr[i] ? hz[i] : 0u;
-        if (isroot)
-          ncc += (s & PACIM_LOW) >= 2;
-        else
-          sv[r][i] = __ldg(L + (size_t)s * B + lane + 32 * i);
+        if (isroot) {
+          ncc += cur && (s & PACIM_LOW) >= 2;
+          if (!cur) sv[r][i] = (PACIM_HIGH | 1u) | ep.tag;
+        } else {
+          sv[r][i] = __ldg(L + (size_t)s * B + lane + 32 * i);  // the root's word (this epoch)
+        }
       }
     }
 #pragma unroll
@@ -615,7 +658,9 @@ __global__ void __launch_bounds__(256, GR == 2 ? 4 : 2) k_gain0_fast(const uint3
       // sizes < 2^31: a pair sums in 32 bits
       unsigned long long t = 0;
 #pragma unroll
-      for (int i = 0; i < 8; i += 2) t += (sv[r][i] & PACIM_LOW) + (sv[r][i + 1] & PACIM_LOW);
+      const uint32_t szm = PACIM_LOW & ~ep.mask;
+#pragma unroll
+      for (int i = 0; i < 8; i += 2) t += (sv[r][i] & szm) + (sv[r][i + 1] & szm);
       unsigned long long h = hs[r];
       for (int d = 16; d; d >>= 1) {
         t += __shfl_xor_sync(0xffffffffu, t, d);
@@ -633,9 +678,9 @@ __global__ void __launch_bounds__(256, GR == 2 ? 4 : 2) k_gain0_fast(const uint3
 
 // per slot the hot (hub's) CC size, read from its root slot after compression
 __global__ void k_hot_sizes(const uint32_t *L, uint32_t n, uint32_t B, const uint32_t *hot,
-                            uint32_t *hot_size) {
+                            uint32_t *hot_size, Ep ep) {
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < B; j += gridDim.x * blockDim.x)
-    hot_size[j] = hot[j] < n ? (L[(size_t)hot[j] * B + j] & PACIM_LOW) : 0u;
+    hot_size[j] = hot[j] < n ? (ep_rd(L[(size_t)hot[j] * B + j], ep) & PACIM_LOW) : 0u;
 }
 
 // HLA: entries sorted by key -> rows, and the segment offsets: off[q] = the
@@ -996,6 +1041,7 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
     es.m = ctx->m;
   }
   const uint32_t n = ctx->nr, B = ctx->R_local;
+  const bool ep_on = ctx->ep.mask != 0;  // slot epochs (pc_build)
   const uint32_t NT = 1u << PACIM_TB;
   pc_ensure(ctx, ctx->d_hot, 2 * (size_t)B * sizeof(uint32_t));
   uint32_t *hot_root = ctx->d_hot.as<uint32_t>();
@@ -1003,45 +1049,48 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
   const unsigned rows_grid = pc_grid(ctx, (size_t)n * 32, 256, 16);
   const bool narrow = Bb < NARROW_W;  // lanes over (row, slot) pairs
   const unsigned wgrid = pc_grid(ctx, (size_t)n * Bb, 256, 16);
-  if (narrow)
+  if (ctx->skip_init) {
+    // slot epochs (pc_build): the stale slots of earlier builds read as roots
+  } else if (narrow) {
     k_init_w<<<wgrid, 256, 0, ctx->stream>>>(Lb, n, Bb);
-  else
+  } else {
     k_init<<<rows_grid, 256, 0, ctx->stream>>>(Lb, n, Bb);
+  }
   PC_CHECK_LAUNCH();
   if (ev) PC_CUDA(cudaEventRecord(ev[0], ctx->stream));
   {
     size_t smem = B * sizeof(uint32_t) + (NT + 1) * sizeof(uint16_t);
     unsigned g = pc_grid(ctx, (es.m + 31) / 32 * 32, EDGE_THREADS, PACIM_EDGE_BLOCKS);
     if (ctx->lean) {  // no edge list: the upper edges from the CSR (c5)
-      auto kern = ctx->hash_rule ? k_edges<false, false, true, true> : k_edges<false, false, false, true>;
+      auto kern = ctx->hash_rule ? (ep_on ? k_edges<false, false, true, true, 0, true> : k_edges<false, false, true, true>) : (ep_on ? k_edges<false, false, false, true, 0, true> : k_edges<false, false, false, true>);
       PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       const uint64_t nnz = 2 * ctx->m;
       const unsigned gl = pc_grid(ctx, (nnz + 31) / 32 * 32, EDGE_THREADS, PACIM_EDGE_BLOCKS);
       kern<<<gl, EDGE_THREADS, smem, ctx->stream>>>(
           ctx->off.as<uint64_t>(), reinterpret_cast<const uint64_t *>(ctx->nbr.p),
           ctx->crow.as<uint32_t>(), nnz, ctx->K, ctx->t32, ctx->d_shr.as<uint32_t>(),
-          ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), nullptr, 0u, PairList{});
+          ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), nullptr, 0u, PairList{}, ctx->ep);
     } else if (ctx->pmodel != PACIM_P_CONST) {  // per-edge thresholds (WIC, Uniform)
-      auto kern = ctx->hash_rule ? (hla.raw ? k_edges<true, true, true, false> : k_edges<true, false, true, false>)
-                                 : (hla.raw ? k_edges<true, true, false, false> : k_edges<true, false, false, false>);
+      auto kern = ctx->hash_rule ? (hla.raw ? (ep_on ? k_edges<true, true, true, false, 0, true> : k_edges<true, true, true, false>) : (ep_on ? k_edges<true, false, true, false, 0, true> : k_edges<true, false, true, false>))
+                                 : (hla.raw ? (ep_on ? k_edges<true, true, false, false, 0, true> : k_edges<true, true, false, false>) : (ep_on ? k_edges<true, false, false, false, 0, true> : k_edges<true, false, false, false>));
       PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
           es.keys, es.ckeys, ctx->tm1.as<uint32_t>(), es.m,
           ctx->K, ctx->toff(), ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla,
-          ctx->d_hr64.as<uint64_t>(), nullptr, 0u, PairList{});
+          ctx->d_hr64.as<uint64_t>(), nullptr, 0u, PairList{}, ctx->ep);
     } else {
-      auto kern = ctx->hash_rule ? (hla.raw ? k_edges<false, true, true, false> : k_edges<false, false, true, false>)
-                                 : (hla.raw ? k_edges<false, true, false, false> : k_edges<false, false, false, false>);
+      auto kern = ctx->hash_rule ? (hla.raw ? (ep_on ? k_edges<false, true, true, false, 0, true> : k_edges<false, true, true, false>) : (ep_on ? k_edges<false, false, true, false, 0, true> : k_edges<false, false, true, false>))
+                                 : (hla.raw ? (ep_on ? k_edges<false, true, false, false, 0, true> : k_edges<false, true, false, false>) : (ep_on ? k_edges<false, false, false, false, 0, true> : k_edges<false, false, false, false>));
       PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
           es.keys, es.ckeys, nullptr, es.m, ctx->K, ctx->t32,
           ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla,
-          ctx->d_hr64.as<uint64_t>(), nullptr, 0u, PairList{});
+          ctx->d_hr64.as<uint64_t>(), nullptr, 0u, PairList{}, ctx->ep);
     }
     PC_CHECK_LAUNCH();
   }
   if (ev) PC_CUDA(cudaEventRecord(ev[1], ctx->stream));
-  k_hot_roots<<<(Bb + 255) / 256, 256, 0, ctx->stream>>>(Lb, n, Bb, ctx->hub_row, hot_root);
+  k_hot_roots<<<(Bb + 255) / 256, 256, 0, ctx->stream>>>(Lb, n, Bb, ctx->hub_row, hot_root, ctx->ep);
   PC_CHECK_LAUNCH();
   if (narrow)
     k_compress_w<<<wgrid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(Lb, n, Bb, hot_root, ctr);
@@ -1055,11 +1104,13 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
       p = 0.5 * ((double)(ctx->t32 >> 32) + (double)(ctx->t32 & 0xFFFFFFFFull)) / 4294967296.0;
     const bool dense = ctx->pmodel != PACIM_P_WIC && 2.0 * ctx->m * p >= 1.5 * std::max(n, 1u);
     if (dense)
-      k_compress_count<false><<<rows_grid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(
-          Lb, n, Bb, hot_root, ctr);
+      (ctx->ep.mask ? k_compress_count<false, true> : k_compress_count<false, false>)
+          <<<rows_grid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(Lb, n, Bb, hot_root, ctr,
+                                                                     ctx->ep);
     else
-      k_compress_count<true><<<rows_grid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(
-          Lb, n, Bb, hot_root, ctr);
+      (ctx->ep.mask ? k_compress_count<true, true> : k_compress_count<true, false>)
+          <<<rows_grid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(Lb, n, Bb, hot_root, ctr,
+                                                                     ctx->ep);
   }
   PC_CHECK_LAUNCH();
   if (ev) PC_CUDA(cudaEventRecord(ev[2], ctx->stream));
@@ -1083,7 +1134,7 @@ static void cs_edges(pacim_ctx *ctx, uint32_t *L, const uint2 *rec, uint32_t MW,
     kern<<<gl, EDGE_THREADS, smem, ctx->stream>>>(
         ctx->off.as<uint64_t>(), reinterpret_cast<const uint64_t *>(ctx->nbr.p),
         ctx->crow.as<uint32_t>(), nnz, ctx->K, ctx->t32, ctx->d_shr.as<uint32_t>(),
-        ctx->d_tab.as<uint16_t>(), B, 0, B, L, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), rec, MW, pl);
+        ctx->d_tab.as<uint16_t>(), B, 0, B, L, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), rec, MW, pl, Ep{});
   } else {
     const bool pe = ctx->pmodel != PACIM_P_CONST;
     auto kern = pe ? (ctx->hash_rule ? k_edges<true, false, true, false, MODE>
@@ -1096,7 +1147,7 @@ static void cs_edges(pacim_ctx *ctx, uint32_t *L, const uint2 *rec, uint32_t MW,
         ctx->keys.as<uint64_t>(), ctx->ckeys.as<uint64_t>(),
         pe ? ctx->tm1.as<uint32_t>() : nullptr, ctx->m, ctx->K, pe ? ctx->toff() : ctx->t32,
         ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, 0, B, L, ctr + 4, Hla{},
-        ctx->d_hr64.as<uint64_t>(), rec, MW, pl);
+        ctx->d_hr64.as<uint64_t>(), rec, MW, pl, Ep{});
   }
   PC_CHECK_LAUNCH();
   ctx->launches++;
@@ -1147,7 +1198,7 @@ void pc_ep_edges(pacim_ctx *ctx, uint64_t e0, uint64_t e1, const uint32_t *d_shr
   kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
       ctx->keys.as<uint64_t>() + e0, ctx->ckeys.as<uint64_t>() + e0,
       pe ? ctx->tm1.as<uint32_t>() + e0 : nullptr, m, ctx->K, pe ? ctx->toff() : ctx->t32, d_shr_all,
-      d_tab_all, R, 0, R, nullptr, ctr + 4, Hla{}, nullptr, nullptr, 0u, pl);
+      d_tab_all, R, 0, R, nullptr, ctr + 4, Hla{}, nullptr, nullptr, 0u, pl, Ep{});
   PC_CHECK_LAUNCH();
   ctx->launches++;
 }
@@ -1255,7 +1306,49 @@ void pc_build(pacim_ctx *ctx) {
   const bool want_hla = (getenv("PACIM_HLA") != nullptr || getenv("PACIM_FORCE_HLA") != nullptr);
   const uint32_t W = plan_windows(ctx);
   const uint32_t nwin = (uint32_t)ctx->win_first.size() - 1;
+  const bool fresh = !ctx->L.p || ctx->L.bytes < (size_t)n * B * sizeof(uint32_t);
   pc_ensure(ctx, ctx->L, (size_t)n * B * sizeof(uint32_t));
+  // slot epochs (Ep, pacim_internal.cuh): no reset pass over the store in
+  // this build unless the epoch count wraps (every 2^bits builds), the store
+  // is new, or an earlier build reset it without epochs (slot windows,
+  // narrow slot counts, HLA recording: their kernels read slots as stored).
+  // The epoch field takes the bits between the largest id / size (<= rows)
+  // and COV (bit 30), at most 6 (PACIM_EPOCH_BITS caps it; 0: off)
+  {
+    const int idbits = 32 - __builtin_clz(std::max(n, 1u));
+    int eb = std::min(6, 30 - idbits);
+    const char *eb_env = getenv("PACIM_EPOCH_BITS");
+    if (eb_env) eb = std::min(eb, atoi(eb_env));
+    // worth it when the reset is large against the unions: the epoch tests
+    // cost ~4 ps per live pair in the union, compression and gain passes,
+    // the reset ~0.6 ps per slot (c4: 9.3 G slots, 0.54 G pairs: -5.3 ms
+    // reset, +2.1 ms; c2: 0.6 G slots, 0.33 G pairs and c3: 4.3 G slots,
+    // 4.9 G pairs lose); judged on the last dense build of this graph
+    const bool worth = eb_env ? true
+                              : ctx->ep_live_gen == ctx->graph_gen &&
+                                    (double)n * B > 7.0 * ctx->ep_live_per_slot * B;
+    const bool on = eb >= 1 && nwin == 1 && B >= NARROW_W && !want_hla && worth;
+    if (!on) {
+      ctx->ep = Ep{};
+      ctx->ep_clean = false;
+      ctx->skip_init = false;
+    } else {
+      const bool cont = !fresh && ctx->ep_clean && ctx->ep_bits == (uint32_t)eb &&
+                        ctx->ep_store == ctx->L.p && ctx->ep_nr == n && ctx->ep_B == B &&
+                        ctx->ep_cur + 1 < (1u << eb);
+      ctx->ep_cur = cont ? ctx->ep_cur + 1 : 0;  // 0: a full reset writes HIGH | 1 (epoch 0)
+      ctx->skip_init = cont;
+      ctx->ep_bits = (uint32_t)eb;
+      ctx->ep_clean = true;
+      ctx->ep_store = ctx->L.p;
+      ctx->ep_nr = n;
+      ctx->ep_B = B;
+      const uint32_t sh = 30 - (uint32_t)eb;
+      ctx->ep.tag = ctx->ep_cur << sh;
+      ctx->ep.mask = ((1u << eb) - 1) << sh;
+    }
+  }
+  const bool ep_on = ctx->ep.mask != 0;
   pc_ensure(ctx, ctx->gain0, (size_t)ctx->n * sizeof(int64_t));
   pc_ensure(ctx, ctx->counters, 64 * sizeof(uint64_t));
   unsigned long long *ctr = ctx->counters.as<unsigned long long>();
@@ -1344,7 +1437,7 @@ void pc_build(pacim_ctx *ctx) {
                                             : std::max<uint64_t>(65536, n / 8));
       pc_ensure(ctx, ctx->d_hot_size, (size_t)B * 4);
       k_hot_sizes<<<(c + 255) / 256, 256, 0, ctx->stream>>>(Lw, n, c, ctx->d_hot.as<uint32_t>(),
-                                                            ctx->d_hot_size.as<uint32_t>());
+                                                            ctx->d_hot_size.as<uint32_t>(), ctx->ep);
       PC_CHECK_LAUNCH();
       ctx->hot_size.resize(B);
       PC_CUDA(cudaMemcpyAsync(ctx->hot_size.data(), ctx->d_hot_size.p, (size_t)B * 4,
@@ -1360,36 +1453,37 @@ void pc_build(pacim_ctx *ctx) {
         const char *gr = getenv("PACIM_GAIN_HOT");  // A/B: 0 = the generic kernel
         const int ghot = c <= 256 ? (gr ? atoi(gr) : 2) : 0;
         if (ghot == 4) {
-          k_gain0_fast<4, true><<<rows_grid, 256, 0, ctx->stream>>>(
+          (ep_on ? k_gain0_fast<4, true, true> : k_gain0_fast<4, true, false>)<<<rows_grid, 256, 0, ctx->stream>>>(
               Lw, n, c, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>(), ctr,
               ctx->d_hot.as<uint32_t>(), ctx->d_hot_size.as<uint32_t>(), big_t,
-              ctx->hotsum.as<int64_t>());
+              ctx->hotsum.as<int64_t>(), ctx->ep);
         } else if (ghot) {
-          k_gain0_fast<2, true><<<rows_grid, 256, 0, ctx->stream>>>(
+          (ep_on ? k_gain0_fast<2, true, true> : k_gain0_fast<2, true, false>)<<<rows_grid, 256, 0, ctx->stream>>>(
               Lw, n, c, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>(), ctr,
               ctx->d_hot.as<uint32_t>(), ctx->d_hot_size.as<uint32_t>(), big_t,
-              ctx->hotsum.as<int64_t>());
+              ctx->hotsum.as<int64_t>(), ctx->ep);
         } else {
-          k_gain0<true><<<rows_grid, 256, 2 * std::min<uint32_t>(c, HOT_MAX) * sizeof(uint32_t),
+          (ep_on ? k_gain0<true, true> : k_gain0<true, false>)<<<rows_grid, 256, 2 * std::min<uint32_t>(c, HOT_MAX) * sizeof(uint32_t),
                           ctx->stream>>>(Lw, n, c, ctx->rmap.as<uint32_t>(),
                                          ctx->gain0.as<int64_t>(), 0, ctr,
                                          ctx->d_hot.as<uint32_t>(), ctx->d_hot_size.as<uint32_t>(),
-                                         big_t, ctx->hotsum.as<int64_t>());
+                                         big_t, ctx->hotsum.as<int64_t>(), ctx->ep);
         }
       } else {
-        k_gain0<false><<<rows_grid, 256, 0, ctx->stream>>>(Lw, n, c, ctx->rmap.as<uint32_t>(),
+        (ep_on ? k_gain0<false, true> : k_gain0<false, false>)<<<rows_grid, 256, 0, ctx->stream>>>(Lw, n, c, ctx->rmap.as<uint32_t>(),
                                                           ctx->gain0.as<int64_t>(), 0, ctr,
-                                                          nullptr, nullptr, 0, nullptr);
+                                                          nullptr, nullptr, 0, nullptr, ctx->ep);
       }
     } else {
-      k_gain0<false><<<rows_grid, 256, 0, ctx->stream>>>(Lw, n, c, ctx->rmap.as<uint32_t>(),
+      k_gain0<false, false><<<rows_grid, 256, 0, ctx->stream>>>(Lw, n, c, ctx->rmap.as<uint32_t>(),
                                                         ctx->gain0.as<int64_t>(), 1, ctr, nullptr,
-                                                        nullptr, 0, nullptr);
+                                                        nullptr, 0, nullptr, ctx->ep);
     }
     PC_CHECK_LAUNCH();
     ctx->launches++;
   }
   PC_CUDA(cudaEventRecord(ev.back(), ctx->stream));
+  ctx->skip_init = false;  // other callers of pc_sketch_pass reset their stores
   if (rec_hla) pc_hla_finish(ctx, &hla);
   ctx->launches += 1;  // fill
   unsigned long long h[6];
@@ -1402,6 +1496,8 @@ void pc_build(pacim_ctx *ctx) {
   ctx->nnonsingle = h[0] + h[1];
   ctx->nmember = 0;
   ctx->stats.live_pairs = h[4];
+  ctx->ep_live_gen = ctx->graph_gen;  // the slot-epoch decision of the next build
+  ctx->ep_live_per_slot = (double)h[4] / std::max(B, 1u);
   double ti = 0, te = 0, tc = 0, tg = 0;
   for (uint32_t w = 0; w < nwin; w++) {
     cudaEvent_t *e = ev.data() + 1 + 4 * w;  // window start, init, edges, compress
@@ -1428,7 +1524,7 @@ void pc_build(pacim_ctx *ctx) {
 // label v) or the root id (R8: min id of the CC)
 namespace {
 __global__ void k_labels(const uint32_t *L, uint32_t n, uint32_t nr, const uint32_t *smap, uint32_t j,
-                         const uint32_t *cid, const uint32_t *rmap, uint32_t *out) {
+                         const uint32_t *cid, const uint32_t *rmap, uint32_t *out, Ep ep) {
   for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
        v += (size_t)gridDim.x * blockDim.x) {
     const uint32_t c = cid[v];
@@ -1436,7 +1532,7 @@ __global__ void k_labels(const uint32_t *L, uint32_t n, uint32_t nr, const uint3
       out[v] = (uint32_t)v;
       continue;
     }
-    uint32_t s = L[pc_addr(smap, nr, c, j)];
+    const uint32_t s = ep_rd(L[pc_addr(smap, nr, c, j)], ep);
     out[v] = (s == c || (s & PACIM_HIGH)) ? (uint32_t)v : rmap[s];
   }
 }
@@ -1450,7 +1546,7 @@ void pc_get_labels(pacim_ctx *ctx, uint32_t slot, uint32_t *host_out) {
                                                               ctx->nr, ctx->d_smap.as<uint32_t>(), slot,
                                                               ctx->cid.as<uint32_t>(),
                                                               ctx->rmap.as<uint32_t>(),
-                                                              t.as<uint32_t>());
+                                                              t.as<uint32_t>(), ctx->ep);
   PC_CHECK_LAUNCH();
   PC_CUDA(cudaMemcpyAsync(host_out, t.p, (size_t)ctx->n * 4, cudaMemcpyDeviceToHost, ctx->stream));
   PC_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -582,6 +582,8 @@ void pc_build_compressed(pacim_ctx *ctx) {
   // and so is the HLA of an earlier build; its batch parent arrays are kept
   // for reuse (choose_batch counts them as free)
   pc_cs_free(ctx);  // a compact store of an earlier build
+  ctx->ep = Ep{};   // batch stores are reset in line (no slot epochs)
+  ctx->skip_init = false;
   for (DevBuf *d : {&ctx->L, &ctx->bfs, &ctx->pkeys, &ctx->hla_off, &ctx->hla_row, &ctx->hla_raw})
     pc_free(ctx, *d);
   ctx->hla_ok = false;

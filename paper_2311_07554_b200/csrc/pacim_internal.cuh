@@ -23,6 +23,19 @@
 //   otherwise                  slot(v, j) = root id of v's CC (< v)
 #define PACIM_HIGH 0x80000000u
 #define PACIM_LOW 0x7FFFFFFFu
+
+// Slot epochs of the dense store (build.cu pc_build): the
+// `mask` bits just below bit 30 (COV) of every slot hold the epoch of the
+// build that last wrote it; a slot whose epoch differs from the current
+// build's (`tag`) reads as a singleton root (HIGH | 1), so a build needs no
+// pass that resets the store — one full reset per 2^bits builds.  Ep{}
+// (mask 0) reads every slot as stored (stores reset in line).
+struct Ep {
+  uint32_t tag = 0, mask = 0;
+};
+__host__ __device__ __forceinline__ uint32_t ep_rd(uint32_t raw, Ep e) {
+  return (raw & e.mask) == e.tag ? (raw & ~e.mask) : (PACIM_HIGH | 1u);
+}
 #define PACIM_TB 12  // bits of the sketch bucket table (R2 candidate enumeration)
 #define PACIM_HUBF 0x80000000u  // hub flag of a row in ckeys
 // Components of at least max(PACIM_BIG_MIN, n / PACIM_BIG_DIV) vertices are
@@ -232,6 +245,16 @@ struct pacim_ctx {
   // (row, j) lives at nr * f + row * c + (j - f).  One window [0, B) is the
   // plain vertex-major layout.  d_smap[j] = f << 16 | c of j's window.
   DevBuf L;
+  // slot epochs of L (Ep above): the current build's, the epoch count and
+  // bits, and the store they are valid for (a full reset otherwise)
+  Ep ep;
+  uint32_t ep_bits = 0, ep_cur = 0;
+  bool ep_clean = false;
+  const void *ep_store = nullptr;
+  uint32_t ep_nr = 0, ep_B = 0;
+  bool skip_init = false;  // pc_sketch_pass: the store needs no reset this build
+  uint64_t ep_live_gen = ~0ull;  // live pairs per slot of the last dense build of graph_gen
+  double ep_live_per_slot = 0;
   std::vector<uint32_t> win_first;  // window starts, + B at the end
   DevBuf d_smap;
   std::vector<uint32_t> smap_of;   // the windows d_smap was filled for

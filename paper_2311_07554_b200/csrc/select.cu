@@ -143,6 +143,7 @@ struct Item {
 constexpr uint32_t CW_ROW = 0xFFFFFFFFu;
 
 struct Sel {
+  Ep ep;  // slot epochs of the store (build.cu): every slot read through ep_rd
   // graph (traversals over live edges)
   const uint64_t *off;
   const uint32_t *nbr;
@@ -290,13 +291,15 @@ __device__ __forceinline__ uint32_t cover_slot(const Sel &S, uint32_t srow, uint
   S.dl[j] = 0;
   S.cov_root[j] = NONE;
   if (srow == NONE) return delta;  // isolated seed: singleton in every sketch
-  const uint32_t sl = S.L[S.onew ? (size_t)srow * S.B + j : pc_addr(S.smap, S.nr, srow, j)];
+  const uint32_t sl =
+      ep_rd(S.L[S.onew ? (size_t)srow * S.B + j : pc_addr(S.smap, S.nr, srow, j)], S.ep);
   if (sl == (PACIM_HIGH | 1u)) return delta;  // singleton {s} (root of size 1)
   const uint32_t root = (sl & PACIM_HIGH) ? srow : sl;
   const size_t ra = S.onew ? (size_t)root * S.B + j : pc_addr(S.smap, S.nr, root, j);
   uint32_t *rs = S.L + ra;
-  const uint32_t x = atomicOr(rs, COV);  // covered from now on
-  if (x & COV) return 0;                 // covered by an earlier seed
+  // (a root of >= 2 members: its slot is of this build's epoch)
+  const uint32_t x = ep_rd(atomicOr(rs, COV), S.ep);  // covered from now on
+  if (x & COV) return 0;                              // covered by an earlier seed
   delta = x & SIZE;
   const unsigned long long at = atomicAdd(S.cov_cnt, 1ull);
   if (at < S.cov_cap) S.cov_list[at] = ra;
@@ -845,7 +848,7 @@ __device__ void apply_dense(const Sel &S, uint32_t s, size_t warp0, size_t nwarp
 #pragma unroll
           for (int i = 0; i < 8; i++)
             x[r][i] = (cr[i] != NONE && v0 + r < S.nr)
-                          ? __ldcs(S.L + (v0 + r) * S.B + j0 + lane + 32 * i)
+                          ? ep_rd(__ldcs(S.L + (v0 + r) * S.B + j0 + lane + 32 * i), S.ep)
                           : NONE;
       } else {
 #pragma unroll
@@ -853,7 +856,7 @@ __device__ void apply_dense(const Sel &S, uint32_t s, size_t warp0, size_t nwarp
 #pragma unroll
           for (int i = 0; i < 8; i++)
             x[r][i] = (cr[i] != NONE && v0 + r < S.nr)
-                          ? __ldcs(S.L + pc_addr(S.smap, S.nr, (uint32_t)(v0 + r), j0 + lane + 32 * i))
+                          ? ep_rd(__ldcs(S.L + pc_addr(S.smap, S.nr, (uint32_t)(v0 + r), j0 + lane + 32 * i)), S.ep)
                           : NONE;
       }
 #pragma unroll
@@ -1199,13 +1202,13 @@ __global__ void k_lazy_eval(Sel S, const uint32_t *cand, uint32_t b0, uint32_t b
       g = S.B;  // isolated: a singleton in every sketch
     } else {
       for (uint32_t j = lane; j < S.B; j += 32) {
-        const uint32_t sv = __ldcg(S.L + pc_addr(S.smap, S.nr, row, j));
+        const uint32_t sv = ep_rd(__ldcg(S.L + pc_addr(S.smap, S.nr, row, j)), S.ep);
         uint32_t rv;
         if (sv == (PACIM_HIGH | 1u)) {
           g += 1;  // {v}: never covered while v is not a seed
           continue;
         }
-        rv = (sv & PACIM_HIGH) ? sv : __ldcg(S.L + pc_addr(S.smap, S.nr, sv, j));
+        rv = (sv & PACIM_HIGH) ? sv : ep_rd(__ldcg(S.L + pc_addr(S.smap, S.nr, sv, j)), S.ep);
         if (!(rv & COV)) g += rv & SIZE;
       }
       for (int d = 16; d; d >>= 1) g += __shfl_xor_sync(0xffffffffu, g, d);
@@ -1219,7 +1222,8 @@ __global__ void k_lazy_mark(Sel S, uint32_t s) {
   const uint32_t srow = S.cid[s];
   if (srow == NONE) return;
   for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < S.B; j += gridDim.x * blockDim.x) {
-    const uint32_t sl = S.L[S.onew ? (size_t)srow * S.B + j : pc_addr(S.smap, S.nr, srow, j)];
+    const uint32_t sl =
+        ep_rd(S.L[S.onew ? (size_t)srow * S.B + j : pc_addr(S.smap, S.nr, srow, j)], S.ep);
     if (sl == (PACIM_HIGH | 1u)) continue;  // singleton
     const uint32_t root = (sl & PACIM_HIGH) ? srow : sl;
     const size_t ra = S.onew ? (size_t)root * S.B + j : pc_addr(S.smap, S.nr, root, j);
@@ -1280,12 +1284,13 @@ __device__ long long dense_eval(const Sel &S, uint32_t v) {
   if (row == NONE) return S.B;  // isolated: a singleton in every sketch
   long long g = 0;
   for (uint32_t j = lane; j < S.B; j += 32) {
-    const uint32_t sv = __ldcg(S.L + pc_addr(S.smap, S.nr, row, j));
+    const uint32_t sv = ep_rd(__ldcg(S.L + pc_addr(S.smap, S.nr, row, j)), S.ep);
     if (sv == (PACIM_HIGH | 1u)) {
       g += 1;  // {v}: never covered while v is not a seed
       continue;
     }
-    const uint32_t rv = (sv & PACIM_HIGH) ? sv : __ldcg(S.L + pc_addr(S.smap, S.nr, sv, j));
+    const uint32_t rv =
+        (sv & PACIM_HIGH) ? sv : ep_rd(__ldcg(S.L + pc_addr(S.smap, S.nr, sv, j)), S.ep);
     if (!(rv & COV)) g += rv & SIZE;
   }
   for (int d = 16; d; d >>= 1) g += __shfl_xor_sync(0xffffffffu, g, d);
@@ -1389,7 +1394,7 @@ __global__ void __launch_bounds__(WT_THREADS, 1) k_wintree_dense(Sel S, WTd W, u
     const uint32_t srow = S.cid[s];
     if (srow != NONE)
       for (uint32_t j = threadIdx.x; j < S.B; j += blockDim.x) {
-        const uint32_t sl = S.L[pc_addr(S.smap, S.nr, srow, j)];
+        const uint32_t sl = ep_rd(S.L[pc_addr(S.smap, S.nr, srow, j)], S.ep);
         if (sl == (PACIM_HIGH | 1u)) continue;
         const uint32_t root = (sl & PACIM_HIGH) ? srow : sl;
         const size_t ra = pc_addr(S.smap, S.nr, root, j);
@@ -1480,6 +1485,7 @@ static Sel make_sel(pacim_ctx *ctx, long long *target) {
   S.decor = ctx->hash_rule;
   S.g_tab = ctx->d_tab.as<uint16_t>();
   S.L = ctx->L.as<uint32_t>();
+  S.ep = ctx->ep;
   S.smap = ctx->d_smap.as<uint32_t>();
   S.onew = ctx->win_first.size() <= 2;
   S.nr = nr;

@@ -121,6 +121,36 @@ def test_tiny_corpus_parity_dense_store(orc, ctx, i, monkeypatch):
     assert ctx.pacim_get_stats()["store"] == 0
 
 
+@pytest.mark.parametrize("bits", ["1", "2", "6"])
+@pytest.mark.parametrize("i", [0, 3, 7, 9, 10, 12])
+def test_dense_store_slot_epochs(orc, ctx, i, bits, monkeypatch):
+    """Slot epochs of the dense store (no reset pass between builds; a full
+    reset every 2^bits builds): a run of builds with changing hash seeds —
+    through the epoch wrap — each equal to the oracle (labels of every
+    sketch, gain0, seeds and gains), and a repeated selection on the last."""
+    monkeypatch.setenv("PACIM_STORE", "dense")
+    monkeypatch.setenv("PACIM_EPOCH_BITS", bits)
+    from oracle.oracle import Graph
+    build_fn, p, R, k = CASES[i]
+    off, nbr = build_fn()
+    g = Graph(len(off) - 1, off, nbr)
+    model, t32 = model_of(orc, p)
+    k = min(k, g.n)
+    load_host(ctx, g, model, t32)
+    for t in range(5):
+        seed = 4000 + 7 * i + t
+        ctx.pacim_build_sketches(R, seed)
+        assert ctx.pacim_get_stats()["store"] == 0
+        for r in range(R):
+            lab, _ = orc.sketch_labels(g, model, t32, seed, r)
+            assert np.array_equal(ctx.pacim_get_labels(r), lab), (t, r)
+        es, egn, esg, eg0 = orc.greedy(g, model, t32, R, seed, k, want_gain0=True)
+        assert np.array_equal(ctx.pacim_get_gain0(), eg0), t
+        for rep in range(2 if t == 4 else 1):
+            s, gn, sg, _ = ctx.pacim_select_seeds(k)
+            assert list(s) == list(es) and list(gn) == list(egn), (t, rep)
+
+
 @pytest.mark.parametrize("env", [{}, {"PACIM_NO_HOT": "1"}, {"PACIM_NO_HOT": "1", "PACIM_BIG_T": "30"}])
 def test_compact_store_hot_and_dense_cover(orc, ctx, env, monkeypatch):
     """The hub's CCs (hot: no member lists, covered by the build's hot sums),
