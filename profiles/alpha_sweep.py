@@ -51,6 +51,7 @@ def main():
         # a fresh context per alpha: the peak is this alpha's alone (a ctx keeps
         # buffer capacity across builds)
         ctx = P.Context(0)
+        ctx.pacim_set_selector(3)  # auto, as bench.py (alpha = 1 under WIC: the Win-Tree)
         pipeline.generate(ctx, cfg)
         a32 = 1 << 32 if al >= 1 else int(al * 4294967296.0)
         tb, ts = [], []
