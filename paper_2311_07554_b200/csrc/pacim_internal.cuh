@@ -245,6 +245,7 @@ struct pacim_ctx {
   // (row, j) lives at nr * f + row * c + (j - f).  One window [0, B) is the
   // plain vertex-major layout.  d_smap[j] = f << 16 | c of j's window.
   DevBuf L;
+  DevBuf edge_work;  // k_edges' chunk counter (dynamic work distribution)
   // slot epochs of L (Ep above): the current build's, the epoch count and
   // bits, and the store they are valid for (a full reset otherwise)
   Ep ep;
