@@ -117,6 +117,9 @@ typedef struct {
                                        re-evaluations CELF would make: at step
                                        i >= 2, every non-seed whose stale score ranks at or
                                        above the winner's fresh one (gain desc, id asc) */
+    uint32_t build_hook_list;       /* dense store with slot epochs: 1 if the last build's
+                                       compression read k_edges' hook list (the non-root
+                                       slots) instead of streaming the store */
 } pacim_stats;
 
 /* --------------------------------------------------------------- lifecycle */

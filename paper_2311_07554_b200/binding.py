@@ -55,6 +55,7 @@ class Stats(C.Structure):
         ("hla_entries", C.c_uint64), ("hubs", C.c_uint32), ("select_hotsum_steps", C.c_uint64),
         ("lean", C.c_uint32), ("store", C.c_uint32), ("select_dist_replays", C.c_uint32),
         ("device_peak_bytes", C.c_uint64), ("select_celf_evaluations", C.c_uint64),
+        ("build_hook_list", C.c_uint32),
     ]
 
     def asdict(self):

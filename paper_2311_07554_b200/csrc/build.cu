@@ -72,8 +72,12 @@ __global__ void k_init(uint32_t *L, uint32_t n, uint32_t B) {
 // Parents stay strictly smaller than children, so the final root of every
 // CC is its minimum id (R8).  Two independent loads per step; the walk stops
 // as soon as the two paths meet.  A root slot holds ROOT1 (read as itself).
+// *hu / *hp (optional): the row hooked and the parent it was hooked under —
+// every non-root slot of a build is hooked exactly once (a CAS from its root
+// state; splices only move non-roots), so these pairs are the hook list
 __device__ __forceinline__ void uf_unite(uint32_t *L, uint32_t B, uint32_t j, uint32_t u,
-                                         uint32_t v, Ep ep = Ep{}) {
+                                         uint32_t v, Ep ep = Ep{}, uint32_t *hu = nullptr,
+                                         uint32_t *hp = nullptr) {
   // ep: slot epochs (a stale slot is a root; every write carries ep.tag and
   // every CAS expects the raw word it read)
   uint32_t *Lj = L + j;
@@ -95,7 +99,13 @@ __device__ __forceinline__ void uf_unite(uint32_t *L, uint32_t B, uint32_t j, ui
     }
     // now pu > pv
     if (u == pu) {
-      if (atomicCAS(Lj + (size_t)u * B, raw, pv | ep.tag) == raw) return;  // hook root u under pv
+      if (atomicCAS(Lj + (size_t)u * B, raw, pv | ep.tag) == raw) {  // hook root u under pv
+        if (hu) {
+          *hu = u;
+          *hp = pv;
+        }
+        return;
+      }
     } else {
       atomicCAS(Lj + (size_t)u * B, raw, pv | ep.tag);  // splice (may lose a race harmlessly)
       u = pu;
@@ -135,6 +145,28 @@ struct PairList {
   unsigned long long *cnt = nullptr;
   unsigned long long cap = 0;
 };
+// warp-wide (every lane calls it): the lanes with `has` append `val` to the
+// warp's reserved chunk [base, base + PL_CHUNK) of `pl`, `used` of it filled
+// (warp-uniform); a chunk that cannot take them is closed (holes: ~0) and
+// the next one reserved with one counter add
+__device__ __forceinline__ void pl_append(const PairList &pl, unsigned long long &base,
+                                          uint32_t &used, bool has, unsigned long long val,
+                                          int lane) {
+  const uint32_t lm = __ballot_sync(0xffffffffu, has);
+  const uint32_t nl = __popc(lm);
+  if (!nl) return;
+  if (used + nl > PL_CHUNK) {
+    for (uint32_t q = used + lane; q < PL_CHUNK; q += 32)
+      if (base + q < pl.cap) pl.p[base + q] = ~0ull;
+    unsigned long long b0 = 0;
+    if (lane == 0) b0 = atomicAdd(pl.cnt, (unsigned long long)PL_CHUNK);
+    base = __shfl_sync(0xffffffffu, b0, 0);
+    used = 0;
+  }
+  const unsigned long long at = base + used + __popc(lm & ((1u << lane) - 1));
+  if (has && at < pl.cap) pl.p[at] = val;
+  used += nl;
+}
 
 // LEAN: no edge list — the warp reads 32 consecutive CSR entries (chunk c),
 // their rows from the chunk table (the row of the first entry, advanced while
@@ -298,37 +330,33 @@ __global__ void __launch_bounds__(EDGE_THREADS, PACIM_EDGE_BLOCKS) k_edges(const
         live += lv;
         // CS = 3 (edge-partitioned sharded build): the pair list only, slot =
         // the global sorted slot of the sketch (its owner rank routes it)
-        if (pl.p) {  // the pair for the union pass, into the warp's reserved chunk
-          const uint32_t lm = __ballot_sync(0xffffffffu, lv);
-          const uint32_t nl = __popc(lm);
-          if (nl) {
-            if (pl_used + nl > PL_CHUNK) {  // close the chunk (holes: ~0) and take the next
-              for (uint32_t q = pl_used + lane; q < PL_CHUNK; q += 32)
-                if (pl_base + q < pl.cap) pl.p[pl_base + q] = ~0ull;
-              unsigned long long b0 = 0;
-              if (lane == 0) b0 = atomicAdd(pl.cnt, (unsigned long long)PL_CHUNK);
-              pl_base = __shfl_sync(0xffffffffu, b0, 0);
-              pl_used = 0;
-            }
-            const unsigned long long at = pl_base + pl_used + __popc(lm & ((1u << lane) - 1));
-            if (lv && at < pl.cap)
-              pl.p[at] = (unsigned long long)uu << 36 | (unsigned long long)vv << 8 | j;
-            pl_used += nl;
-          }
+        if (pl.p)  // the pair for the union pass, into the warp's reserved chunk
+          pl_append(pl, pl_base, pl_used, lv,
+                    (unsigned long long)uu << 36 | (unsigned long long)vv << 8 | j, lane);
+      } else {
+        // the hook list of an epoch build (CS = 0, EP, pl.p): {parent << 36 |
+        // row << 8 | slot} of every successful hook — exactly the build's
+        // non-root slots, so the compression pass reads them instead of
+        // streaming the store (k_compress_count<…, LIST>)
+        uint32_t hu = NONE, hp = 0;
+        if (lv) {
+          if (CS == 1)
+            uf_unite(L, 2, 0, pc_cs_pos(rec, MW, u & ~PACIM_HUBF, j),
+                     pc_cs_pos(rec, MW, v & ~PACIM_HUBF, j));
+          else
+            uf_unite(L, Bb, j - j0, u & ~PACIM_HUBF, v & ~PACIM_HUBF, EP ? ep : Ep{},
+                     (CS == 0 && EP) ? &hu : nullptr, (CS == 0 && EP) ? &hp : nullptr);
+          live++;
         }
-      } else if (lv) {
-        if (CS == 1)
-          uf_unite(L, 2, 0, pc_cs_pos(rec, MW, u & ~PACIM_HUBF, j),
-                   pc_cs_pos(rec, MW, v & ~PACIM_HUBF, j));
-        else
-          uf_unite(L, Bb, j - j0, u & ~PACIM_HUBF, v & ~PACIM_HUBF, EP ? ep : Ep{});
-        live++;
+        if (CS == 0 && EP && pl.p)
+          pl_append(pl, pl_base, pl_used, hu != NONE,
+                    (unsigned long long)hp << 36 | (unsigned long long)hu << 8 | (j - j0), lane);
       }
     }
     __syncwarp();
   }
   if (REC) hla.flush(w_hla[REC ? wid : 0], hla_n);
-  if (CS >= 2 && pl.p)  // the last chunk's holes
+  if ((CS >= 2 || (CS == 0 && EP)) && pl.p)  // the last chunk's holes
     for (uint32_t q = pl_used + lane; q < PL_CHUNK; q += 32)
       if (pl_base + q < pl.cap) pl.p[pl_base + q] = ~0ull;
   // block-aggregated counter
@@ -414,10 +442,19 @@ __device__ __forceinline__ void add_count(unsigned long long *ctr, unsigned long
 }
 
 constexpr uint32_t CLCAP = 256 + 31;  // pending finds per warp: < 32 carried + one 256-slot block
-template <bool COMPACT, bool EP>
+// LIST (epoch builds): when the hook list of k_edges is complete (*hl_cnt <=
+// hl_cap) the non-root slots are read from it — lane per entry, the find
+// starting at the parent recorded at the hook (an ancestor: later splices
+// only moved the slot closer to the root) — instead of streaming all
+// rows x B slots of the store (c4: 37 GB for 0.54 G non-roots); an
+// overflowed list falls back to the row stream on the device
+template <bool COMPACT, bool EP, bool LIST = false>
 __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n, uint32_t B,
                                                         const uint32_t *hot,
-                                                        unsigned long long *ctr, Ep ep_in) {
+                                                        unsigned long long *ctr, Ep ep_in,
+                                                        const unsigned long long *hl = nullptr,
+                                                        const unsigned long long *hl_cnt = nullptr,
+                                                        unsigned long long hl_cap = 0) {
   const Ep ep = EP ? ep_in : Ep{};  // without epochs every epoch operation folds away
   extern __shared__ uint32_t hsm[];
   __shared__ uint32_t cl_v[COMPACT ? 8 : 1][COMPACT ? CLCAP : 1],
@@ -459,6 +496,28 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
     __syncwarp();
     cnt = 0;
   };
+  const unsigned long long hl_n = LIST ? *hl_cnt : 0;
+  if (LIST && hl_n <= hl_cap) {
+    const size_t nt = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < hl_n; i += nt) {
+      const unsigned long long e = hl[i];
+      if (e == ~0ull) continue;  // a chunk's hole
+      const uint32_t j = (uint32_t)e & 255u, v = (uint32_t)(e >> 8) & 0x0FFFFFFFu,
+                     s = (uint32_t)(e >> 36);
+      nnr++;
+      if (j < H && s == hroot[j]) {  // hooked under the hot root itself
+        atomicAdd(hcnt + j, 1u);
+        continue;
+      }
+      uint32_t rr = 0;
+      const uint32_t root = find_halve(L, B, j, s, ep, &rr);
+      if (root != s) atomicMin(L + (size_t)v * B + j, root | ep.tag);
+      if (j < H && root == hroot[j])
+        atomicAdd(hcnt + j, 1u);
+      else
+        add_to_root(L, B, j, root, 1u, ep, rr);
+    }
+  } else
   for (size_t v = warp; v < n; v += nw) {
     for (uint32_t j0 = 0; j0 < B; j0 += 256) {
       uint32_t sv[8];  // prefetch up to 8 slots per lane (independent loads)
@@ -1089,6 +1148,38 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
   }
   PC_CHECK_LAUNCH();
   if (ev) PC_CUDA(cudaEventRecord(ev[0], ctx->stream));
+  // the hook list of an epoch build (k_edges records every successful hook,
+  // k_compress_count<…, LIST> reads it): capacity from the non-root count of
+  // the last dense build of this graph (+ chunk holes); an overflow makes the
+  // compression stream the store (decided on the device).  PACIM_HOOKLIST =
+  // 0: off; > 1: that capacity (tests)
+  // compacted finds unless the store is dense in non-roots: expected live
+  // (row, slot) pairs per row 2 m p / rows >= 1.5 (c3: 2.3; c2: 0.84; WIC:
+  // small p on most edges)
+  double p = (double)ctx->t32 / 4294967296.0;
+  if (ctx->pmodel == PACIM_P_UNIFORM)
+    p = 0.5 * ((double)(ctx->t32 >> 32) + (double)(ctx->t32 & 0xFFFFFFFFull)) / 4294967296.0;
+  const bool dense = ctx->pmodel != PACIM_P_WIC && 2.0 * ctx->m * p >= 1.5 * std::max(n, 1u);
+  PairList hk{};
+  ctx->hk_cap = 0;
+  {
+    const long long env = getenv("PACIM_HOOKLIST") ? atoll(getenv("PACIM_HOOKLIST")) : 1;
+    const bool known = ctx->hk_gen == ctx->graph_gen && ctx->hk_B == Bb;
+    if (ep_on && !dense && !narrow && env != 0 && Bb <= 256 && j0 == 0 && n < (1u << 28) && (known || env > 1)) {
+      unsigned long long cap = env > 1 ? (unsigned long long)env
+                                       : ctx->hk_hint + ctx->hk_hint / 8 + (1ull << 24);
+      if (ctx->hk_list.bytes < cap * 8 || ctx->hk_list.bytes > 2 * cap * 8 + (64ull << 20)) {
+        pc_free(ctx, ctx->hk_list);
+        if (pc_mem_free(ctx) > cap * 8 + (2ull << 30)) pc_ensure(ctx, ctx->hk_list, cap * 8);
+      }
+      if (ctx->hk_list.bytes >= cap * 8) {
+        hk.p = ctx->hk_list.as<unsigned long long>();
+        hk.cnt = ctr + 20;
+        hk.cap = cap;
+        ctx->hk_cap = cap;
+      }
+    }
+  }
   {
     size_t smem = B * sizeof(uint32_t) + (NT + 1) * sizeof(uint16_t);
     unsigned g = pc_grid(ctx, (es.m + 31) / 32 * 32, EDGE_THREADS, PACIM_EDGE_BLOCKS);
@@ -1100,7 +1191,7 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
       kern<<<gl, EDGE_THREADS, smem, ctx->stream>>>(
           ctx->off.as<uint64_t>(), reinterpret_cast<const uint64_t *>(ctx->nbr.p),
           ctx->crow.as<uint32_t>(), nnz, ctx->K, ctx->t32, ctx->d_shr.as<uint32_t>(),
-          ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), nullptr, 0u, PairList{}, ctx->ep,
+          ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), nullptr, 0u, hk, ctx->ep,
           edge_work(ctx, nnz, gl));
     } else if (ctx->pmodel != PACIM_P_CONST) {  // per-edge thresholds (WIC, Uniform)
       auto kern = ctx->hash_rule ? (hla.raw ? (ep_on ? k_edges<true, true, true, false, 0, true> : k_edges<true, true, true, false>) : (ep_on ? k_edges<true, false, true, false, 0, true> : k_edges<true, false, true, false>))
@@ -1109,7 +1200,7 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
       kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
           es.keys, es.ckeys, ctx->tm1.as<uint32_t>(), es.m,
           ctx->K, ctx->toff(), ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla,
-          ctx->d_hr64.as<uint64_t>(), nullptr, 0u, PairList{}, ctx->ep, edge_work(ctx, es.m, g));
+          ctx->d_hr64.as<uint64_t>(), nullptr, 0u, hk, ctx->ep, edge_work(ctx, es.m, g));
     } else {
       auto kern = ctx->hash_rule ? (hla.raw ? (ep_on ? k_edges<false, true, true, false, 0, true> : k_edges<false, true, true, false>) : (ep_on ? k_edges<false, false, true, false, 0, true> : k_edges<false, false, true, false>))
                                  : (hla.raw ? (ep_on ? k_edges<false, true, false, false, 0, true> : k_edges<false, true, false, false>) : (ep_on ? k_edges<false, false, false, false, 0, true> : k_edges<false, false, false, false>));
@@ -1117,7 +1208,7 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
       kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
           es.keys, es.ckeys, nullptr, es.m, ctx->K, ctx->t32,
           ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla,
-          ctx->d_hr64.as<uint64_t>(), nullptr, 0u, PairList{}, ctx->ep, edge_work(ctx, es.m, g));
+          ctx->d_hr64.as<uint64_t>(), nullptr, 0u, hk, ctx->ep, edge_work(ctx, es.m, g));
     }
     PC_CHECK_LAUNCH();
   }
@@ -1128,21 +1219,18 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
     k_compress_w<<<wgrid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(Lb, n, Bb, hot_root, ctr);
   else
   {
-    // compacted finds unless the store is dense in non-roots: expected live
-    // (row, slot) pairs per row 2 m p / rows >= 1.5 (c3: 2.3; c2: 0.84; WIC:
-    // small p on most edges)
-    double p = (double)ctx->t32 / 4294967296.0;
-    if (ctx->pmodel == PACIM_P_UNIFORM)
-      p = 0.5 * ((double)(ctx->t32 >> 32) + (double)(ctx->t32 & 0xFFFFFFFFull)) / 4294967296.0;
-    const bool dense = ctx->pmodel != PACIM_P_WIC && 2.0 * ctx->m * p >= 1.5 * std::max(n, 1u);
     if (dense)
       (ctx->ep.mask ? k_compress_count<false, true> : k_compress_count<false, false>)
           <<<rows_grid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(Lb, n, Bb, hot_root, ctr,
-                                                                     ctx->ep);
+                                                                     ctx->ep, nullptr, nullptr, 0);
+    else if (hk.p)
+      k_compress_count<true, true, true><<<pc_grid(ctx, (size_t)n * 32, 256, 8), 256,
+                                           2 * H * sizeof(uint32_t), ctx->stream>>>(
+          Lb, n, Bb, hot_root, ctr, ctx->ep, hk.p, hk.cnt, hk.cap);
     else
       (ctx->ep.mask ? k_compress_count<true, true> : k_compress_count<true, false>)
           <<<rows_grid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(Lb, n, Bb, hot_root, ctr,
-                                                                     ctx->ep);
+                                                                     ctx->ep, nullptr, nullptr, 0);
   }
   PC_CHECK_LAUNCH();
   if (ev) PC_CUDA(cudaEventRecord(ev[2], ctx->stream));
@@ -1327,6 +1415,8 @@ void pc_build(pacim_ctx *ctx) {
   PC_REQUIRE(!ctx->compressed, PACIM_ENOTIMPL, "compressed store not built by pc_build");
   // the compact store (store_cs.cu) unless the sketches are dense (c3) or the
   // dense layout is asked for (PACIM_STORE=dense)
+  ctx->stats.build_hook_list = 0;
+  ctx->hk_cap = 0;
   if (pc_cs_build(ctx)) return;
   pc_cs_free(ctx);
   pc_slot_table(ctx);
@@ -1519,8 +1609,8 @@ void pc_build(pacim_ctx *ctx) {
   ctx->skip_init = false;  // other callers of pc_sketch_pass reset their stores
   if (rec_hla) pc_hla_finish(ctx, &hla);
   ctx->launches += 1;  // fill
-  unsigned long long h[6];
-  PC_CUDA(cudaMemcpyAsync(h, ctr, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+  unsigned long long h[21];
+  PC_CUDA(cudaMemcpyAsync(h, ctr, 21 * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
                           ctx->stream));
   if (htime) h2 = host_ms();
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
@@ -1529,6 +1619,10 @@ void pc_build(pacim_ctx *ctx) {
   ctx->nnonsingle = h[0] + h[1];
   ctx->nmember = 0;
   ctx->stats.live_pairs = h[4];
+  ctx->hk_gen = ctx->graph_gen;  // the hook list's capacity in the next build
+  ctx->hk_B = B;
+  ctx->hk_hint = h[1];
+  ctx->stats.build_hook_list = ctx->hk_cap && h[20] <= ctx->hk_cap ? 1 : 0;
   ctx->ep_live_gen = ctx->graph_gen;  // the slot-epoch decision of the next build
   ctx->ep_live_per_slot = (double)h[4] / std::max(B, 1u);
   double ti = 0, te = 0, tc = 0, tg = 0;

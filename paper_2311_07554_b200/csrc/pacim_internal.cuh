@@ -256,6 +256,11 @@ struct pacim_ctx {
   bool skip_init = false;  // pc_sketch_pass: the store needs no reset this build
   uint64_t ep_live_gen = ~0ull;  // live pairs per slot of the last dense build of graph_gen
   double ep_live_per_slot = 0;
+  // hook list of epoch builds (k_edges -> k_compress_count<…, LIST>): capacity
+  // from the non-root count of the last dense build of graph_gen (hk_gen)
+  DevBuf hk_list;
+  uint64_t hk_hint = 0, hk_gen = ~0ull, hk_cap = 0;
+  uint32_t hk_B = 0;
   std::vector<uint32_t> win_first;  // window starts, + B at the end
   DevBuf d_smap;
   std::vector<uint32_t> smap_of;   // the windows d_smap was filled for

@@ -121,15 +121,21 @@ def test_tiny_corpus_parity_dense_store(orc, ctx, i, monkeypatch):
     assert ctx.pacim_get_stats()["store"] == 0
 
 
+@pytest.mark.parametrize("hl", ["1", "0", "40"])
 @pytest.mark.parametrize("bits", ["1", "2", "6"])
 @pytest.mark.parametrize("i", [0, 3, 7, 9, 10, 12])
-def test_dense_store_slot_epochs(orc, ctx, i, bits, monkeypatch):
+def test_dense_store_slot_epochs(orc, ctx, i, bits, hl, monkeypatch):
     """Slot epochs of the dense store (no reset pass between builds; a full
     reset every 2^bits builds): a run of builds with changing hash seeds —
     through the epoch wrap — each equal to the oracle (labels of every
-    sketch, gain0, seeds and gains), and a repeated selection on the last."""
+    sketch, gain0, seeds and gains), and a repeated selection on the last.
+    hl: the compression reads k_edges' hook list (the non-root slots) from
+    the second build on (1, the default; not case 9, whose sketches are
+    dense in non-roots), never (0), or the list overflows its capacity (40:
+    the compression streams the store instead, decided on the device)."""
     monkeypatch.setenv("PACIM_STORE", "dense")
     monkeypatch.setenv("PACIM_EPOCH_BITS", bits)
+    monkeypatch.setenv("PACIM_HOOKLIST", hl)
     from oracle.oracle import Graph
     build_fn, p, R, k = CASES[i]
     off, nbr = build_fn()
@@ -140,7 +146,10 @@ def test_dense_store_slot_epochs(orc, ctx, i, bits, monkeypatch):
     for t in range(5):
         seed = 4000 + 7 * i + t
         ctx.pacim_build_sketches(R, seed)
-        assert ctx.pacim_get_stats()["store"] == 0
+        st = ctx.pacim_get_stats()
+        assert st["store"] == 0
+        want = hl == "1" and t >= 1 and i != 9 and R >= 16
+        assert st["build_hook_list"] == int(want), (t, st["build_hook_list"])
         for r in range(R):
             lab, _ = orc.sketch_labels(g, model, t32, seed, r)
             assert np.array_equal(ctx.pacim_get_labels(r), lab), (t, r)
