@@ -442,12 +442,6 @@ __device__ __forceinline__ void add_count(unsigned long long *ctr, unsigned long
 }
 
 constexpr uint32_t CLCAP = 256 + 31;  // pending finds per warp: < 32 carried + one 256-slot block
-// LIST (epoch builds): when the hook list of k_edges is complete (*hl_cnt <=
-// hl_cap) the non-root slots are read from it — lane per entry, the find
-// starting at the parent recorded at the hook (an ancestor: later splices
-// only moved the slot closer to the root) — instead of streaming all
-// rows x B slots of the store (c4: 37 GB for 0.54 G non-roots); an
-// overflowed list falls back to the row stream on the device
 template <bool COMPACT, bool EP, bool LIST = false>
 __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n, uint32_t B,
                                                         const uint32_t *hot,
@@ -496,28 +490,9 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
     __syncwarp();
     cnt = 0;
   };
-  const unsigned long long hl_n = LIST ? *hl_cnt : 0;
-  if (LIST && hl_n <= hl_cap) {
-    const size_t nt = (size_t)gridDim.x * blockDim.x;
-    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < hl_n; i += nt) {
-      const unsigned long long e = hl[i];
-      if (e == ~0ull) continue;  // a chunk's hole
-      const uint32_t j = (uint32_t)e & 255u, v = (uint32_t)(e >> 8) & 0x0FFFFFFFu,
-                     s = (uint32_t)(e >> 36);
-      nnr++;
-      if (j < H && s == hroot[j]) {  // hooked under the hot root itself
-        atomicAdd(hcnt + j, 1u);
-        continue;
-      }
-      uint32_t rr = 0;
-      const uint32_t root = find_halve(L, B, j, s, ep, &rr);
-      if (root != s) atomicMin(L + (size_t)v * B + j, root | ep.tag);
-      if (j < H && root == hroot[j])
-        atomicAdd(hcnt + j, 1u);
-      else
-        add_to_root(L, B, j, root, 1u, ep, rr);
-    }
-  } else
+  // LIST: the fallback of k_compress_list — the row stream only when the hook
+  // list overflowed its capacity
+  if (LIST && *hl_cnt <= hl_cap) return;
   for (size_t v = warp; v < n; v += nw) {
     for (uint32_t j0 = 0; j0 < B; j0 += 256) {
       uint32_t sv[8];  // prefetch up to 8 slots per lane (independent loads)
@@ -574,6 +549,73 @@ __global__ void __launch_bounds__(256) k_compress_count(uint32_t *L, uint32_t n,
   if (lane == 0 && nnr) atomicAdd(&s1, nnr);
   __syncthreads();
   if (threadIdx.x == 0 && s1) atomicAdd(ctr + 1, s1);
+}
+
+// k_compress_count from the hook list (epoch builds): when k_edges' list is
+// complete (*hl_cnt <= hl_cap) the non-root slots are read from it — lane per
+// entry, the find starting at the parent recorded at the hook (an ancestor:
+// later splices only moved the slot closer to the root) — instead of
+// streaming all rows x B slots of the store (c4: 37 GB for 0.54 G
+// non-roots).  An overflowed list: nothing here, k_compress_count<…, LIST>
+// streams the rows instead (both launched, each decides on the device)
+template <bool EP>
+__global__ void __launch_bounds__(256, 8) k_compress_list(uint32_t *L, uint32_t B,
+                                                          const uint32_t *hot,
+                                                          unsigned long long *ctr, Ep ep_in,
+                                                          const unsigned long long *__restrict__ hl,
+                                                          const unsigned long long *hl_cnt,
+                                                          unsigned long long hl_cap,
+                                                          unsigned long long *work) {
+  const Ep ep = EP ? ep_in : Ep{};
+  const unsigned long long hl_n = *hl_cnt;
+  if (hl_n > hl_cap) return;
+  extern __shared__ uint32_t hsm[];
+  const uint32_t H = min(B, HOT_MAX);
+  uint32_t *hroot = hsm, *hcnt = hsm + H;
+  for (uint32_t j = threadIdx.x; j < H; j += blockDim.x) {
+    hroot[j] = hot[j];
+    hcnt[j] = 0;
+  }
+  __syncthreads();
+  unsigned long long nnr = 0;
+  // dynamic work distribution: a warp takes LCH entries at a time from
+  // *work (zeroed before the launch) — chains and root contention differ
+  // between entries, so a static split leaves SMs idle at the end
+  constexpr uint32_t LCH = 2048;
+  const int lane = threadIdx.x & 31;
+  unsigned long long b = 0, b_end = 0;  // warp-uniform
+  for (;;) {
+    if (b >= b_end) {
+      unsigned long long c0 = 0;
+      if (lane == 0) c0 = atomicAdd(work, (unsigned long long)LCH);
+      c0 = __shfl_sync(0xffffffffu, c0, 0);
+      if (c0 >= hl_n) break;
+      b = c0;
+      b_end = min(c0 + LCH, hl_n);
+    }
+    const unsigned long long i = b + lane;
+    b += 32;
+    const unsigned long long e = i < b_end ? hl[i] : ~0ull;
+    if (e == ~0ull) continue;  // a chunk's hole (or past the end)
+    const uint32_t j = (uint32_t)e & 255u, v = (uint32_t)(e >> 8) & 0x0FFFFFFFu,
+                   s = (uint32_t)(e >> 36);
+    nnr++;
+    if (j < H && s == hroot[j]) {  // hooked under the hot root itself
+      atomicAdd(hcnt + j, 1u);
+      continue;
+    }
+    uint32_t rr = 0;
+    const uint32_t root = find_halve(L, B, j, s, ep, &rr);
+    if (root != s) atomicMin(L + (size_t)v * B + j, root | ep.tag);
+    if (j < H && root == hroot[j])
+      atomicAdd(hcnt + j, 1u);
+    else
+      add_to_root(L, B, j, root, 1u, ep, rr);
+  }
+  __syncthreads();
+  for (uint32_t j = threadIdx.x; j < H; j += blockDim.x)
+    if (hcnt[j]) add_to_root(L, B, j, hroot[j], hcnt[j], ep, ld_cg(L + (size_t)hroot[j] * B + j));
+  add_count(ctr + 1, nnr);
 }
 
 // ---------------------------------------------------------------- k_gain0
@@ -1219,18 +1261,25 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
     k_compress_w<<<wgrid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(Lb, n, Bb, hot_root, ctr);
   else
   {
-    if (dense)
-      (ctx->ep.mask ? k_compress_count<false, true> : k_compress_count<false, false>)
-          <<<rows_grid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(Lb, n, Bb, hot_root, ctr,
-                                                                     ctx->ep, nullptr, nullptr, 0);
-    else if (hk.p)
-      k_compress_count<true, true, true><<<pc_grid(ctx, (size_t)n * 32, 256, 8), 256,
-                                           2 * H * sizeof(uint32_t), ctx->stream>>>(
+    // grid-stride kernels: one full wave of resident blocks (pc_grid_occ)
+    const size_t csm = 2 * H * sizeof(uint32_t);
+    if (dense) {
+      auto kc = ctx->ep.mask ? k_compress_count<false, true> : k_compress_count<false, false>;
+      kc<<<pc_grid_occ(ctx, kc, (size_t)n * 32, 256, csm), 256, csm, ctx->stream>>>(
+          Lb, n, Bb, hot_root, ctr, ctx->ep, nullptr, nullptr, 0);
+    } else if (hk.p) {
+      auto kl = k_compress_list<true>;
+      PC_CUDA(cudaMemsetAsync(ctr + 21, 0, 8, ctx->stream));
+      kl<<<pc_grid_occ(ctx, kl, (size_t)n * 32, 256, csm), 256, csm, ctx->stream>>>(
+          Lb, Bb, hot_root, ctr, ctx->ep, hk.p, hk.cnt, hk.cap, ctr + 21);
+      auto kc = k_compress_count<true, true, true>;  // only if the list overflowed
+      kc<<<pc_grid_occ(ctx, kc, (size_t)n * 32, 256, csm), 256, csm, ctx->stream>>>(
           Lb, n, Bb, hot_root, ctr, ctx->ep, hk.p, hk.cnt, hk.cap);
-    else
-      (ctx->ep.mask ? k_compress_count<true, true> : k_compress_count<true, false>)
-          <<<rows_grid, 256, 2 * H * sizeof(uint32_t), ctx->stream>>>(Lb, n, Bb, hot_root, ctr,
-                                                                     ctx->ep, nullptr, nullptr, 0);
+    } else {
+      auto kc = ctx->ep.mask ? k_compress_count<true, true> : k_compress_count<true, false>;
+      kc<<<pc_grid_occ(ctx, kc, (size_t)n * 32, 256, csm), 256, csm, ctx->stream>>>(
+          Lb, n, Bb, hot_root, ctr, ctx->ep, nullptr, nullptr, 0);
+    }
   }
   PC_CHECK_LAUNCH();
   if (ev) PC_CUDA(cudaEventRecord(ev[2], ctx->stream));
@@ -1576,24 +1625,29 @@ void pc_build(pacim_ctx *ctx) {
         const char *gr = getenv("PACIM_GAIN_HOT");  // A/B: 0 = the generic kernel
         const int ghot = c <= 256 ? (gr ? atoi(gr) : 2) : 0;
         if (ghot == 4) {
-          (ep_on ? k_gain0_fast<4, true, true> : k_gain0_fast<4, true, false>)<<<rows_grid, 256, 0, ctx->stream>>>(
+          auto kg = ep_on ? k_gain0_fast<4, true, true> : k_gain0_fast<4, true, false>;
+          kg<<<rows_grid, 256, 0, ctx->stream>>>(
               Lw, n, c, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>(), ctr,
               ctx->d_hot.as<uint32_t>(), ctx->d_hot_size.as<uint32_t>(), big_t,
               ctx->hotsum.as<int64_t>(), ctx->ep);
         } else if (ghot) {
-          (ep_on ? k_gain0_fast<2, true, true> : k_gain0_fast<2, true, false>)<<<rows_grid, 256, 0, ctx->stream>>>(
+          auto kg = ep_on ? k_gain0_fast<2, true, true> : k_gain0_fast<2, true, false>;
+          kg<<<rows_grid, 256, 0, ctx->stream>>>(
               Lw, n, c, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>(), ctr,
               ctx->d_hot.as<uint32_t>(), ctx->d_hot_size.as<uint32_t>(), big_t,
               ctx->hotsum.as<int64_t>(), ctx->ep);
         } else {
-          (ep_on ? k_gain0<true, true> : k_gain0<true, false>)<<<rows_grid, 256, 2 * std::min<uint32_t>(c, HOT_MAX) * sizeof(uint32_t),
+          auto kg = ep_on ? k_gain0<true, true> : k_gain0<true, false>;
+          const size_t gsm = 2 * std::min<uint32_t>(c, HOT_MAX) * sizeof(uint32_t);
+          kg<<<rows_grid, 256, gsm,
                           ctx->stream>>>(Lw, n, c, ctx->rmap.as<uint32_t>(),
                                          ctx->gain0.as<int64_t>(), 0, ctr,
                                          ctx->d_hot.as<uint32_t>(), ctx->d_hot_size.as<uint32_t>(),
                                          big_t, ctx->hotsum.as<int64_t>(), ctx->ep);
         }
       } else {
-        (ep_on ? k_gain0<false, true> : k_gain0<false, false>)<<<rows_grid, 256, 0, ctx->stream>>>(Lw, n, c, ctx->rmap.as<uint32_t>(),
+        auto kg = ep_on ? k_gain0<false, true> : k_gain0<false, false>;
+        kg<<<rows_grid, 256, 0, ctx->stream>>>(Lw, n, c, ctx->rmap.as<uint32_t>(),
                                                           ctx->gain0.as<int64_t>(), 0, ctr,
                                                           nullptr, nullptr, 0, nullptr, ctx->ep);
       }

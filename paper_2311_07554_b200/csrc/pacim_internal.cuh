@@ -531,3 +531,17 @@ inline unsigned pc_grid(const pacim_ctx *ctx, size_t work, unsigned block,
   if (need < 1) need = 1;
   return (unsigned)(need < cap ? need : cap);
 }
+// Grid of a grid-stride kernel: at most one full wave of resident blocks
+// (the occupancy the kernel's registers and shared memory allow), so no block
+// starts after the first ones finish — a partial second wave runs its share
+// of the loop at a fraction of the occupancy (ncu: k_compress_count at 1.33
+// waves spent up to half its time in the tail)
+template <typename K>
+inline unsigned pc_grid_occ(const pacim_ctx *ctx, K kern, size_t work, unsigned block,
+                            size_t smem = 0) {
+  int nb = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, (int)block, smem) != cudaSuccess ||
+      nb < 1)
+    nb = 1;
+  return pc_grid(ctx, work, block, (unsigned)nb);
+}
