@@ -40,6 +40,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -231,6 +233,32 @@ def run_reference(args, cfg):
 
 
 # ------------------------------------------------------------------- ours
+def upper_csr(off, nbr, chunk=1 << 28):
+    """The upper CSR of a symmetric CSR (row u keeps its neighbours > u; the
+    rows stay sorted), built on the host in chunks of rows."""
+    n = len(off) - 1
+    off = off.astype(np.int64)
+    deg = np.diff(off)
+    keep_cnt = np.zeros(n, dtype=np.uint64)
+    parts = []
+    a = 0
+    while a < n:
+        b = int(np.searchsorted(off, off[a] + chunk, side="right"))
+        b = min(max(b - 1, a + 1), n)
+        rows = np.repeat(np.arange(a, b, dtype=np.uint32), deg[a:b])
+        seg = nbr[off[a]:off[b]]
+        keep = seg > rows
+        parts.append(seg[keep])
+        cs = np.zeros(len(seg) + 1, dtype=np.uint64)
+        np.cumsum(keep, out=cs[1:])
+        rel = (off[a:b + 1] - off[a]).astype(np.int64)
+        keep_cnt[a:b] = cs[rel[1:]] - cs[rel[:-1]]
+        a = b
+    uoff = np.zeros(n + 1, dtype=np.uint64)
+    np.cumsum(keep_cnt, out=uoff[1:])
+    return uoff, (np.concatenate(parts) if parts else np.zeros(0, np.uint32)).astype(np.uint32)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -340,10 +368,24 @@ def main():
     st = ctx.pacim_get_stats()
 
     # ---------------- end to end through the public API (host CSR, pinned)
+    # The input crosses PCIe as the upper CSR (each undirected edge once:
+    # pacim_load_graph_upper_async; the device builds the symmetric CSR), half
+    # the bytes of the symmetric CSR; PACIM_E2E_FULL=1 sends the symmetric CSR
+    # (pacim_load_graph_async) instead
     off, nbr = ctx.pacim_get_graph()
+    _full = bool(os.environ.get("PACIM_E2E_FULL"))
+    if not _full:
+        off, nbr = upper_csr(off, nbr)
     h_off = torch.from_numpy(off).pin_memory()
     h_nbr = torch.from_numpy(nbr).pin_memory()
     off_np, nbr_np = h_off.numpy(), h_nbr.numpy()
+    load_async = ctx.pacim_load_graph_async if _full else ctx.pacim_load_graph_upper_async
+
+    def load_sync():
+        if _full:
+            ctx.pacim_load_graph(off_np, nbr_np, pm, t32, 0)
+        else:
+            ctx.pacim_load_graph_upper(off_np, nbr_np, pm, t32, 0)
 
     # Pipelined through the public API: step i+1's host CSR is enqueued
     # (pacim_load_graph_async, pinned memory) before step i runs, so its H2D
@@ -354,22 +396,23 @@ def main():
     # (graphs whose two staged copies do not fit beside the resident one — c5
     # — take the unpipelined loop)
     _sync = bool(os.environ.get("PACIM_E2E_SYNC"))  # debugging: the unpipelined loop
-    e2e_mode = ("pacim_load_graph_async from pinned host CSR, two loads in flight: "
+    src = "symmetric CSR" if _full else "upper CSR (symmetrized on the device)"
+    e2e_mode = (f"{load_async.__name__} from the pinned host {src}, two loads in flight: "
                 "the next steps' H2D copies overlap this step's build and selection")
     if not _sync:
         try:
-            ctx.pacim_load_graph_async(off_np, nbr_np, pm, t32)
-            ctx.pacim_load_graph_async(off_np, nbr_np, pm, t32)
+            load_async(off_np, nbr_np, pm, t32)
+            load_async(off_np, nbr_np, pm, t32)
             step()
             step()
         except P.PacimError as e:
             if "ENOMEM" not in str(e):
                 raise
             _sync = True
-            ctx.pacim_load_graph(off_np, nbr_np, pm, t32, 0)  # drops the pending loads
+            load_sync()  # drops the pending loads
     if _sync:
-        e2e_mode = "pacim_load_graph from pinned host CSR (two staged copies do not fit)"
-        ctx.pacim_load_graph(off_np, nbr_np, pm, t32, 0)
+        e2e_mode = f"synchronous load from the pinned host {src} (two staged copies do not fit)"
+        load_sync()
         step()
     barrier()
     torch.cuda.synchronize(dev)
@@ -381,16 +424,16 @@ def main():
     # enqueued before step i's selection, so the copy engine never waits on
     # the host
     if not _sync:
-        ctx.pacim_load_graph_async(off_np, nbr_np, pm, t32)
+        load_async(off_np, nbr_np, pm, t32)
         if args.e2e_steps > 1:
-            ctx.pacim_load_graph_async(off_np, nbr_np, pm, t32)
+            load_async(off_np, nbr_np, pm, t32)
     _tw = [time.perf_counter()]
     for i in range(args.e2e_steps):
         if _sync:
-            ctx.pacim_load_graph(off_np, nbr_np, pm, t32, 0)
+            load_sync()
         ctx.pacim_build_sketches(R, cfg["hash_seed"], a32, rank, world)  # commits step i's graph
         if i + 2 < args.e2e_steps and not _sync:
-            ctx.pacim_load_graph_async(off_np, nbr_np, pm, t32)  # step i+2's input
+            load_async(off_np, nbr_np, pm, t32)  # step i+2's input
         out = (pdist.distributed_select(ctx, n, k, dev) if (use_dist and args.py_dist)
                else ctx.pacim_select_seeds(k))
         _tw.append(time.perf_counter())

@@ -249,6 +249,33 @@ PACIM_API int pacim_load_graph_async(pacim_ctx *ctx, uint32_t n, uint64_t nnz,
                                      const uint64_t *offsets, const uint32_t *neighbors,
                                      int pmodel, uint64_t t32);
 
+/* H0 from the UPPER CSR: each undirected edge {u, v} given once, in row
+ * min(u, v) — uoffsets[n+1] (host, uoffsets[0] = 0, uoffsets[n] = m), and
+ * uneighbors[m] (host): row u lists its neighbours v > u in increasing order.
+ * Half the bytes of the symmetric CSR cross PCIe; the device builds the
+ * symmetric CSR (lower lists by a transpose: target histogram, scan, atomic
+ * cursors, per-vertex segmented sort; rows = sorted lower ++ upper), so the
+ * graph is exactly the one pacim_load_graph would load from the symmetric
+ * CSR of the same edge set ("symmetrize", R14).  validate: 0 = trust
+ * the caller; != 0 = check offsets, 0 <= u < v < n and strictly increasing
+ * rows on the device (EINVAL naming the first bad vertex).  Other EINVAL and
+ * the model as for pacim_load_graph; m = 0 is allowed (n isolated vertices).
+ * The caller keeps ownership of the host arrays. */
+PACIM_API int pacim_load_graph_upper(pacim_ctx *ctx, uint32_t n, uint64_t m,
+                                     const uint64_t *uoffsets, const uint32_t *uneighbors,
+                                     int pmodel, uint64_t t32, int validate);
+
+/* Pipelined pacim_load_graph_upper (validate = 0): the copies of the upper
+ * CSR are enqueued on the copy stream like pacim_load_graph_async, and the
+ * symmetrization runs on the ctx stream when the next pacim_build_sketches
+ * commits the load.  Same rules as pacim_load_graph_async (at most two
+ * pending loads, host arrays valid and unmodified until committed, pinned
+ * for overlap). */
+PACIM_API int pacim_load_graph_upper_async(pacim_ctx *ctx, uint32_t n, uint64_t m,
+                                           const uint64_t *uoffsets,
+                                           const uint32_t *uneighbors, int pmodel,
+                                           uint64_t t32);
+
 /* As pacim_load_graph but offsets/neighbors are DEVICE pointers on the ctx's
  * device (copied device-to-device; the caller keeps ownership). */
 PACIM_API int pacim_load_graph_device(pacim_ctx *ctx, uint32_t n, uint64_t nnz,

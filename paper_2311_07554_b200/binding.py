@@ -18,7 +18,7 @@ STATUS = {0: "OK", -1: "EINVAL", -2: "ENOMEM", -3: "ECUDA", -4: "ENCCL", -5: "ES
 EXPORTS = [
     "pacim_create", "pacim_destroy", "pacim_last_error", "pacim_version",
     "pacim_threshold_from_p", "pacim_threshold_uniform", "pacim_load_graph", "pacim_load_graph_async",
-    "pacim_load_graph_device",
+    "pacim_load_graph_upper", "pacim_load_graph_upper_async", "pacim_load_graph_device",
     "pacim_generate_graph", "pacim_graph_info", "pacim_get_graph",
     "pacim_build_sketches", "pacim_select_seeds", "pacim_gain0_to_device",
     "pacim_select_reset", "pacim_cover_local", "pacim_cover_local_sparse",
@@ -86,6 +86,8 @@ def lib():
             "pacim_threshold_uniform": (u64, [C.c_double, C.c_double]),
             "pacim_load_graph": (i32, [P, u32, u64, P, P, i32, u64, i32]),
             "pacim_load_graph_async": (i32, [P, u32, u64, P, P, i32, u64]),
+            "pacim_load_graph_upper": (i32, [P, u32, u64, P, P, i32, u64, i32]),
+            "pacim_load_graph_upper_async": (i32, [P, u32, u64, P, P, i32, u64]),
             "pacim_load_graph_device": (i32, [P, u32, u64, P, P, i32, u64, i32]),
             "pacim_generate_graph": (i32, [P, i32, P, i32, u64, i32, u64]),
             "pacim_graph_info": (i32, [P, P, P]),
@@ -221,6 +223,25 @@ class Context:
         nbr = np.ascontiguousarray(neighbors, dtype=np.uint32)
         self._check(self._L.pacim_load_graph_async(self._h, len(off) - 1, len(nbr), _ptr(off),
                                                    _ptr(nbr), pmodel, t32))
+        self._staged = (getattr(self, "_staged", ()) + ((off, nbr),))[-3:]
+
+    def pacim_load_graph_upper(self, uoffsets: np.ndarray, uneighbors: np.ndarray, pmodel: int,
+                               t32: int, validate: int = 1):
+        """Load from the upper CSR (each edge once, row u lists v > u sorted);
+        the device builds the symmetric CSR."""
+        off = np.ascontiguousarray(uoffsets, dtype=np.uint64)
+        nbr = np.ascontiguousarray(uneighbors, dtype=np.uint32)
+        self._check(self._L.pacim_load_graph_upper(self._h, len(off) - 1, len(nbr), _ptr(off),
+                                                   _ptr(nbr), pmodel, t32, validate))
+
+    def pacim_load_graph_upper_async(self, uoffsets: np.ndarray, uneighbors: np.ndarray,
+                                     pmodel: int, t32: int):
+        """Enqueue the copy of a host upper CSR (committed, and symmetrized on
+        the device, by the next pacim_build_sketches); arrays kept referenced."""
+        off = np.ascontiguousarray(uoffsets, dtype=np.uint64)
+        nbr = np.ascontiguousarray(uneighbors, dtype=np.uint32)
+        self._check(self._L.pacim_load_graph_upper_async(self._h, len(off) - 1, len(nbr),
+                                                         _ptr(off), _ptr(nbr), pmodel, t32))
         self._staged = (getattr(self, "_staged", ()) + ((off, nbr),))[-3:]
 
     def pacim_load_graph_device(self, d_offsets, d_neighbors, n: int, nnz: int, pmodel: int,

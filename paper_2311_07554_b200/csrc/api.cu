@@ -149,6 +149,15 @@ static void drop_sketches(pacim_ctx *ctx) {
   ctx->sel_list_valid = false;  // the covered list refers to the old store
 }
 
+void pc_graph_loaded(pacim_ctx *ctx) {
+  ctx->graph_gen++;
+  uint64_t sig = pc_mix64(ctx->n);
+  for (uint64_t x : {ctx->m, (uint64_t)ctx->nr, (uint64_t)ctx->pmodel, ctx->t32, (uint64_t)ctx->lean})
+    sig = pc_mix64(sig ^ x);
+  if (sig != ctx->graph_sig || ctx->hint_gen == 0) ctx->hint_gen++;
+  ctx->graph_sig = sig;
+}
+
 static void drop_graph(pacim_ctx *ctx) {
   drop_sketches(ctx);
   ctx->has_graph = false;
@@ -166,6 +175,7 @@ static void free_all(pacim_ctx *ctx) {
                     &ctx->cs_rec, &ctx->cs_soff, &ctx->cs_ecrow, &ctx->cs_E, &ctx->cs_vid,
                     &ctx->cs_diag, &ctx->cs_cnt, &ctx->cs_plist, &ctx->edge_work, &ctx->wt_buf, &ctx->dist_ghot, &ctx->dist_buf, &ctx->dist_cov_old, &ctx->ep_tab, &ctx->ep_send, &ctx->ep_cnt, &ctx->hk_list};
   for (DevBuf *b : bufs) pc_free(ctx, *b);
+  pc_sym_free(ctx);
 }
 
 extern "C" {
@@ -313,11 +323,15 @@ static void commit_staged(pacim_ctx *ctx) {
   ctx->pmodel = st.pmodel;
   ctx->t32 = st.t32;
   PC_CUDA(cudaStreamWaitEvent(ctx->stream, st.done, 0));
-  std::swap(ctx->off, st.off);  // the staged CSR becomes the graph; the old
-  std::swap(ctx->nbr, st.nbr);  // buffers are the slot's next staging area
+  if (st.upper) {  // the symmetric CSR built on the device from the upper one
+    pc_symmetrize_upper(ctx, st.off.as<uint64_t>(), st.nbr.as<uint32_t>(), st.n, st.nnz / 2);
+  } else {
+    std::swap(ctx->off, st.off);  // the staged CSR becomes the graph; the old
+    std::swap(ctx->nbr, st.nbr);  // buffers are the slot's next staging area
+  }
   pc_graph_finish_load(ctx, 0);
   ctx->has_graph = true;
-  ctx->graph_gen++;
+  pc_graph_loaded(ctx);
   PC_CUDA(cudaEventRecord(ctx->released, ctx->stream));
 }
 
@@ -341,6 +355,7 @@ int pacim_load_graph(pacim_ctx *ctx, uint32_t n, uint64_t nnz, const uint64_t *o
     PC_REQUIRE(offsets[0] == 0, PACIM_EINVAL, "offsets[0] != 0");
     PC_REQUIRE(offsets[n] == nnz, PACIM_EINVAL, "offsets[n] != nnz");
     drop_staged(ctx);
+    pc_sym_free(ctx);  // the upper loads' scratch
     ctx->mi_valid = false;  // free device memory queried afresh (pc_mem_info)
     load_common(ctx, n, nnz, pmodel, t32);
     PC_CUDA(cudaMemcpyAsync(ctx->off.p, offsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice,
@@ -349,44 +364,83 @@ int pacim_load_graph(pacim_ctx *ctx, uint32_t n, uint64_t nnz, const uint64_t *o
       PC_CUDA(cudaMemcpyAsync(ctx->nbr.p, neighbors, nnz * 4, cudaMemcpyHostToDevice, ctx->stream));
     pc_graph_finish_load(ctx, validate);
     ctx->has_graph = true;
-  ctx->graph_gen++;
+  pc_graph_loaded(ctx);
   });
+}
+
+// enqueue the host -> device copies of a graph on the copy stream (committed
+// by the next build): the symmetric CSR (nnz = 2m entries) or, upper, the
+// upper CSR (nnz = m entries, symmetrized on the device at commit)
+static void load_async(pacim_ctx *ctx, uint32_t n, uint64_t nnz, const uint64_t *offsets,
+                       const uint32_t *neighbors, int pmodel, uint64_t t32, bool upper) {
+  PC_REQUIRE(offsets && (neighbors || nnz == 0), PACIM_EINVAL, "NULL CSR array");
+  PC_REQUIRE(n >= 1, PACIM_EINVAL, "n must be >= 1");
+  PC_REQUIRE(n < (1u << 31), PACIM_EINVAL, "n must be < 2^31 (R2 key packing)");
+  PC_REQUIRE(upper || (nnz & 1) == 0, PACIM_EINVAL, "nnz must be even (symmetric CSR)");
+  PC_REQUIRE(offsets[0] == 0, PACIM_EINVAL, "offsets[0] != 0");
+  PC_REQUIRE(offsets[n] == nnz, PACIM_EINVAL, upper ? "offsets[n] != m" : "offsets[n] != nnz");
+  check_model(pmodel, t32);
+  StagedGraph &st = ctx->stage[ctx->stage_fill];
+  PC_REQUIRE(!st.pending, PACIM_ESTATE, "two graph loads are already pending");
+  if (!ctx->copy_stream) {
+    PC_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    PC_CUDA(cudaEventCreateWithFlags(&ctx->released, cudaEventDisableTiming));
+    for (auto &g : ctx->stage) PC_CUDA(cudaEventCreateWithFlags(&g.done, cudaEventDisableTiming));
+    PC_CUDA(cudaEventRecord(ctx->released, ctx->stream));
+  }
+  pc_ensure(ctx, st.off, ((size_t)n + 1) * 8);
+  pc_ensure(ctx, st.nbr, std::max<uint64_t>(nnz, 1) * 4);
+  // the slot's buffers may have been the graph before the last commit (or
+  // the source of its symmetrization)
+  PC_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->released, 0));
+  PC_CUDA(cudaMemcpyAsync(st.off.p, offsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice,
+                          ctx->copy_stream));
+  if (nnz)
+    PC_CUDA(cudaMemcpyAsync(st.nbr.p, neighbors, nnz * 4, cudaMemcpyHostToDevice,
+                            ctx->copy_stream));
+  PC_CUDA(cudaEventRecord(st.done, ctx->copy_stream));
+  st.pending = true;
+  st.upper = upper;
+  st.n = n;
+  st.nnz = upper ? 2 * nnz : nnz;
+  st.pmodel = pmodel;
+  st.t32 = t32;
+  ctx->stage_fill ^= 1;
 }
 
 int pacim_load_graph_async(pacim_ctx *ctx, uint32_t n, uint64_t nnz, const uint64_t *offsets,
                            const uint32_t *neighbors, int pmodel, uint64_t t32) {
+  return guarded(ctx, [&] { load_async(ctx, n, nnz, offsets, neighbors, pmodel, t32, false); });
+}
+
+int pacim_load_graph_upper_async(pacim_ctx *ctx, uint32_t n, uint64_t m, const uint64_t *uoffsets,
+                                 const uint32_t *uneighbors, int pmodel, uint64_t t32) {
+  return guarded(ctx, [&] { load_async(ctx, n, m, uoffsets, uneighbors, pmodel, t32, true); });
+}
+
+int pacim_load_graph_upper(pacim_ctx *ctx, uint32_t n, uint64_t m, const uint64_t *uoffsets,
+                           const uint32_t *uneighbors, int pmodel, uint64_t t32, int validate) {
   return guarded(ctx, [&] {
-    PC_REQUIRE(offsets && (neighbors || nnz == 0), PACIM_EINVAL, "NULL CSR array");
+    PC_REQUIRE(uoffsets && (uneighbors || m == 0), PACIM_EINVAL, "NULL CSR array");
     PC_REQUIRE(n >= 1, PACIM_EINVAL, "n must be >= 1");
-    PC_REQUIRE(n < (1u << 31), PACIM_EINVAL, "n must be < 2^31 (R2 key packing)");
-    PC_REQUIRE((nnz & 1) == 0, PACIM_EINVAL, "nnz must be even (symmetric CSR)");
-    PC_REQUIRE(offsets[0] == 0, PACIM_EINVAL, "offsets[0] != 0");
-    PC_REQUIRE(offsets[n] == nnz, PACIM_EINVAL, "offsets[n] != nnz");
-    check_model(pmodel, t32);
-    StagedGraph &st = ctx->stage[ctx->stage_fill];
-    PC_REQUIRE(!st.pending, PACIM_ESTATE, "two graph loads are already pending");
-    if (!ctx->copy_stream) {
-      PC_CUDA(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
-      PC_CUDA(cudaEventCreateWithFlags(&ctx->released, cudaEventDisableTiming));
-      for (auto &g : ctx->stage) PC_CUDA(cudaEventCreateWithFlags(&g.done, cudaEventDisableTiming));
-      PC_CUDA(cudaEventRecord(ctx->released, ctx->stream));
-    }
-    pc_ensure(ctx, st.off, ((size_t)n + 1) * 8);
-    pc_ensure(ctx, st.nbr, std::max<uint64_t>(nnz, 1) * 4);
-    // the slot's buffers may have been the graph before the last commit
-    PC_CUDA(cudaStreamWaitEvent(ctx->copy_stream, ctx->released, 0));
-    PC_CUDA(cudaMemcpyAsync(st.off.p, offsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice,
-                            ctx->copy_stream));
-    if (nnz)
-      PC_CUDA(cudaMemcpyAsync(st.nbr.p, neighbors, nnz * 4, cudaMemcpyHostToDevice,
-                              ctx->copy_stream));
-    PC_CUDA(cudaEventRecord(st.done, ctx->copy_stream));
-    st.pending = true;
-    st.n = n;
-    st.nnz = nnz;
-    st.pmodel = pmodel;
-    st.t32 = t32;
-    ctx->stage_fill ^= 1;
+    PC_REQUIRE(uoffsets[0] == 0, PACIM_EINVAL, "offsets[0] != 0");
+    PC_REQUIRE(uoffsets[n] == m, PACIM_EINVAL, "offsets[n] != m");
+    drop_staged(ctx);
+    ctx->mi_valid = false;  // free device memory queried afresh (pc_mem_info)
+    load_common(ctx, n, 2 * m, pmodel, t32);
+    TmpBuf uo(ctx), un(ctx);
+    pc_ensure(ctx, uo, ((size_t)n + 1) * 8);
+    pc_ensure(ctx, un, std::max<uint64_t>(m, 1) * 4);
+    PC_CUDA(cudaMemcpyAsync(uo.p, uoffsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice,
+                            ctx->stream));
+    if (m)
+      PC_CUDA(cudaMemcpyAsync(un.p, uneighbors, m * 4, cudaMemcpyHostToDevice, ctx->stream));
+    if (validate) pc_validate_upper(ctx, uo.as<uint64_t>(), un.as<uint32_t>(), n);
+    pc_symmetrize_upper(ctx, uo.as<uint64_t>(), un.as<uint32_t>(), n, m);
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));  // the temporaries are released next
+    pc_graph_finish_load(ctx, 0);
+    ctx->has_graph = true;
+    pc_graph_loaded(ctx);
   });
 }
 
@@ -412,7 +466,7 @@ int pacim_load_graph_device(pacim_ctx *ctx, uint32_t n, uint64_t nnz, const uint
     PC_REQUIRE(ends[1] == nnz, PACIM_EINVAL, "offsets[n] != nnz");
     pc_graph_finish_load(ctx, validate);
     ctx->has_graph = true;
-  ctx->graph_gen++;
+  pc_graph_loaded(ctx);
   });
 }
 
@@ -428,7 +482,7 @@ int pacim_generate_graph(pacim_ctx *ctx, int kind, const uint64_t *params, int n
     ctx->t32 = t32;
     pc_generate(ctx, kind, params, nparams, gen_seed);
     ctx->has_graph = true;
-  ctx->graph_gen++;
+  pc_graph_loaded(ctx);
   });
 }
 

@@ -1206,7 +1206,7 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
   ctx->hk_cap = 0;
   {
     const long long env = getenv("PACIM_HOOKLIST") ? atoll(getenv("PACIM_HOOKLIST")) : 1;
-    const bool known = ctx->hk_gen == ctx->graph_gen && ctx->hk_B == Bb;
+    const bool known = ctx->hk_gen == ctx->hint_gen && ctx->hk_B == Bb;
     if (ep_on && !dense && !narrow && env != 0 && Bb <= 256 && j0 == 0 && n < (1u << 28) && (known || env > 1)) {
       unsigned long long cap = env > 1 ? (unsigned long long)env
                                        : ctx->hk_hint + ctx->hk_hint / 8 + (1ull << 24);
@@ -1497,7 +1497,7 @@ void pc_build(pacim_ctx *ctx) {
     // reset, +2.1 ms; c2: 0.6 G slots, 0.33 G pairs and c3: 4.3 G slots,
     // 4.9 G pairs lose); judged on the last dense build of this graph
     const bool worth = eb_env ? true
-                              : ctx->ep_live_gen == ctx->graph_gen &&
+                              : ctx->ep_live_gen == ctx->hint_gen &&
                                     (double)n * B > 7.0 * ctx->ep_live_per_slot * B;
     const bool on = eb >= 1 && nwin == 1 && B >= NARROW_W && !want_hla && worth;
     if (!on) {
@@ -1673,11 +1673,11 @@ void pc_build(pacim_ctx *ctx) {
   ctx->nnonsingle = h[0] + h[1];
   ctx->nmember = 0;
   ctx->stats.live_pairs = h[4];
-  ctx->hk_gen = ctx->graph_gen;  // the hook list's capacity in the next build
+  ctx->hk_gen = ctx->hint_gen;  // the hook list's capacity in the next build
   ctx->hk_B = B;
   ctx->hk_hint = h[1];
   ctx->stats.build_hook_list = ctx->hk_cap && h[20] <= ctx->hk_cap ? 1 : 0;
-  ctx->ep_live_gen = ctx->graph_gen;  // the slot-epoch decision of the next build
+  ctx->ep_live_gen = ctx->hint_gen;  // the slot-epoch decision of the next build
   ctx->ep_live_per_slot = (double)h[4] / std::max(B, 1u);
   double ti = 0, te = 0, tc = 0, tg = 0;
   for (uint32_t w = 0; w < nwin; w++) {

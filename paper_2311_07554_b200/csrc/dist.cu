@@ -481,7 +481,7 @@ unsigned long long pc_cs_ep_pairs(pacim_ctx *ctx, uint32_t MW, unsigned long lon
   unsigned long long *cown = c + 1, *cur = cown + P, *call = cur + P;
   // this rank's 1/P of the upper edges, all sketches, into the pair list
   const uint64_t m = ctx->m, e0 = m * rank / P, e1 = m * (rank + 1) / P;
-  const bool same = ctx->ep_gen == ctx->graph_gen && ctx->ep_K == ctx->K;
+  const bool same = ctx->ep_gen == ctx->hint_gen && ctx->ep_K == ctx->K;
   unsigned long long cap = same ? ctx->ep_hint + ctx->ep_hint / 16 + (1ull << 22) : 0;
   if (const char *e = getenv("PACIM_EP_CAP")) cap = std::max(1LL, atoll(e));  // tests: overflow
   if (!cap) {
@@ -514,7 +514,7 @@ unsigned long long pc_cs_ep_pairs(pacim_ctx *ctx, uint32_t MW, unsigned long lon
     cap = reserved;  // exact: every warp reserved its chunks (the pass is repeated)
   }
   ctx->ep_hint = reserved;
-  ctx->ep_gen = ctx->graph_gen;
+  ctx->ep_gen = ctx->hint_gen;
   ctx->ep_K = ctx->K;
   if (times) PC_CUDA(cudaEventRecord(ev[1], ctx->stream));
   // group by owner

@@ -6,6 +6,7 @@
 #include <cub/cub.cuh>
 
 #include <cstdlib>
+#include <vector>
 
 #include "pacim_internal.cuh"
 
@@ -508,6 +509,191 @@ void pc_graph_finish_load(pacim_ctx *ctx, int validate) {
   }
   ctx->lean = want_lean(ctx);
   derive_common(ctx);
+}
+
+// --------------------------------------------------- upper CSR -> full CSR
+// pacim_load_graph_upper (H0): the caller sends each undirected edge once, as
+// the upper CSR (row u lists its neighbours v > u, sorted) — half the bytes of
+// the symmetric CSR over PCIe — and the device builds the symmetric CSR.  The
+// lower lists are the transpose: the upper entries (u, v) are in u order, so
+// a STABLE radix sort of the pairs by v (CUB, LSD: ceil(log2 n) key bits)
+// leaves every v's sources sorted; run boundaries of the sorted targets give
+// the lower degrees; one lane-per-entry pass writes every row as [lower ++
+// upper].  (Atomic cursors + a per-vertex segmented sort cost 255 ms at c4
+// against the sort's tens of ms.)
+namespace {
+// validate = 1 for upper CSRs: offsets non-decreasing, rows strictly
+// increasing, every neighbour in (u, n); *bad = the smallest bad vertex
+__global__ void k_validate_upper(const uint64_t *uoff, const uint32_t *unbr, uint32_t n,
+                                 uint32_t *bad) {
+  for (size_t u = (size_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+       u += (size_t)gridDim.x * blockDim.x) {
+    const uint64_t a = uoff[u], b = uoff[u + 1];
+    bool ok = a <= b;
+    for (uint64_t e = a; ok && e < b; e++) {
+      const uint32_t v = unbr[e];
+      ok = v > u && v < n && (e == a || v > unbr[e - 1]);
+    }
+    if (!ok) atomicMin(bad, (uint32_t)u);
+  }
+}
+
+// the sort's input: keys = targets v (a copy: unbr is read again for the
+// upper halves), values = sources u (row of entry e from the chunk table)
+__global__ void k_upper_pairs(const uint64_t *uoff, const uint32_t *ucrow, const uint32_t *unbr,
+                              uint64_t m, uint32_t *key, uint32_t *val) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (size_t)gridDim.x * blockDim.x) {
+    uint32_t u = ucrow[e >> 5];
+    while (e >= uoff[u + 1]) u++;
+    key[e] = unbr[e];
+    val[e] = u;
+  }
+}
+
+// run boundaries of the sorted targets: lo[v] = first index, hi[v] = one
+// past the last (both 0 for a vertex without lower neighbours)
+__global__ void k_target_runs(const uint32_t *skey, uint64_t m, uint64_t *lo, uint64_t *hi) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t k = skey[i];
+    if (i == 0 || skey[i - 1] != k) lo[k] = i;
+    if (i + 1 == m || skey[i + 1] != k) hi[k] = i + 1;
+  }
+}
+
+// deg[v] = upper + lower degree, lc[v] = lower degree (deg[n] = lc[n] = 0,
+// for the exclusive scans)
+__global__ void k_full_deg(const uint64_t *uoff, const uint64_t *lo, const uint64_t *hi,
+                           uint32_t n, uint64_t *deg, uint64_t *lc) {
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v <= n;
+       v += (size_t)gridDim.x * blockDim.x) {
+    const uint64_t l = v < n ? hi[v] - lo[v] : 0;
+    deg[v] = v < n ? uoff[v + 1] - uoff[v] + l : 0;
+    lc[v] = l;
+  }
+}
+
+// row v of the symmetric CSR = its sorted lower list ++ its upper list
+__global__ void k_full_rows(const uint64_t *off, const uint32_t *crow, uint64_t nnz,
+                            const uint64_t *loff, const uint32_t *lsorted, const uint64_t *uoff,
+                            const uint32_t *unbr, uint32_t *nbr) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
+       e += (size_t)gridDim.x * blockDim.x) {
+    uint32_t v = crow[e >> 5];
+    while (e >= off[v + 1]) v++;
+    const uint64_t i = e - off[v], nl = loff[v + 1] - loff[v];
+    nbr[e] = i < nl ? lsorted[loff[v] + i] : unbr[uoff[v] + (i - nl)];
+  }
+}
+
+// crow-style chunk table over any offsets array: row of entry 32 c
+__global__ void k_crow_of(const uint64_t *off, uint32_t n, uint32_t *crow) {
+  for (size_t u = (size_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+       u += (size_t)gridDim.x * blockDim.x) {
+    const uint64_t c0 = (off[u] + 31) / 32, c1 = (off[u + 1] + 31) / 32;
+    for (uint64_t c = c0; c < c1; c++) crow[c] = (uint32_t)u;
+  }
+}
+}  // namespace
+
+void pc_validate_upper(pacim_ctx *ctx, const uint64_t *d_uoff, const uint32_t *d_unbr, uint32_t n) {
+  pc_ensure(ctx, ctx->counters, 64 * sizeof(uint64_t));
+  uint32_t *bad = ctx->counters.as<uint32_t>();
+  PC_CUDA(cudaMemsetAsync(bad, 0xFF, 4, ctx->stream));
+  k_validate_upper<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(d_uoff, d_unbr, n, bad);
+  PC_CHECK_LAUNCH();
+  uint32_t h = 0;
+  PC_CUDA(cudaMemcpyAsync(&h, bad, 4, cudaMemcpyDeviceToHost, ctx->stream));
+  PC_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (h != 0xFFFFFFFFu)
+    throw PacimError{PACIM_EINVAL, "upper CSR invalid at vertex " + std::to_string(h) +
+                                       " (offsets/order/range: neighbours must be > u, < n, sorted)"};
+}
+
+void pc_sym_free(pacim_ctx *ctx) {
+  for (DevBuf &d : ctx->sym) pc_free(ctx, d);
+}
+
+// d_uoff[n+1], d_unbr[m] (device, the upper CSR) -> ctx->off, ctx->nbr (the
+// symmetric CSR, 2m entries), on the ctx stream; ctx->m = m already
+void pc_symmetrize_upper(pacim_ctx *ctx, const uint64_t *d_uoff, const uint32_t *d_unbr,
+                         uint32_t n, uint64_t m) {
+  const uint64_t nnz = 2 * m;
+  // PACIM_SYM_TIMES=1: phase times on stderr (diagnostics)
+  const bool tm = getenv("PACIM_SYM_TIMES") != nullptr;
+  std::vector<cudaEvent_t> evs;
+  auto mark = [&]() {
+    if (!tm) return;
+    cudaEvent_t e;
+    PC_CUDA(cudaEventCreate(&e));
+    PC_CUDA(cudaEventRecord(e, ctx->stream));
+    evs.push_back(e);
+  };
+  mark();
+  pc_ensure(ctx, ctx->off, ((size_t)n + 1) * 8);
+  pc_ensure(ctx, ctx->nbr, std::max<uint64_t>(nnz, 1) * 4);
+  // scratch kept by the ctx (capacity reused by the next upper load: a
+  // cudaMalloc / cudaFree of ~25 GB per load at c4 would cost more than the
+  // sort); released by a load of the symmetric CSR
+  DevBuf *sb = ctx->sym;
+  DevBuf &lo = sb[0], &hi = sb[1], &deg = sb[2], &lc = sb[3], &loff = sb[4], &k0 = sb[5],
+         &k1 = sb[6], &v0 = sb[7], &v1 = sb[8], &ucrow = sb[9], &stmp = sb[10];
+  for (DevBuf *d : {&lo, &hi, &deg, &lc, &loff}) pc_ensure(ctx, *d, ((size_t)n + 1) * 8);
+  PC_CUDA(cudaMemsetAsync(lo.p, 0, ((size_t)n + 1) * 8, ctx->stream));
+  PC_CUDA(cudaMemsetAsync(hi.p, 0, ((size_t)n + 1) * 8, ctx->stream));
+  uint64_t *off = ctx->off.as<uint64_t>();
+  const uint32_t *lsorted = nullptr;
+  if (m) {
+    for (DevBuf *d : {&k0, &k1, &v0, &v1}) pc_ensure(ctx, *d, m * 4);
+    pc_ensure(ctx, ucrow, ((m + 31) / 32 + 1) * 4);
+    k_crow_of<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(d_uoff, n, ucrow.as<uint32_t>());
+    PC_CHECK_LAUNCH();
+    k_upper_pairs<<<pc_grid(ctx, m, 256, 16), 256, 0, ctx->stream>>>(
+        d_uoff, ucrow.as<uint32_t>(), d_unbr, m, k0.as<uint32_t>(), v0.as<uint32_t>());
+    PC_CHECK_LAUNCH();
+    mark();
+    const int bits = std::max(1, 32 - __builtin_clz(std::max(n - 1, 1u)));
+    cub::DoubleBuffer<uint32_t> dk(k0.as<uint32_t>(), k1.as<uint32_t>()),
+        dv(v0.as<uint32_t>(), v1.as<uint32_t>());
+    size_t tb = 0;
+    PC_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tb, dk, dv, (int64_t)m, 0, bits, ctx->stream));
+    pc_ensure(ctx, stmp, tb + 16);
+    PC_CUDA(cub::DeviceRadixSort::SortPairs(stmp.p, tb, dk, dv, (int64_t)m, 0, bits, ctx->stream));
+    mark();
+    k_target_runs<<<pc_grid(ctx, m, 256, 16), 256, 0, ctx->stream>>>(
+        dk.Current(), m, lo.as<uint64_t>(), hi.as<uint64_t>());
+    PC_CHECK_LAUNCH();
+    lsorted = dv.Current();
+    ctx->launches += 4;
+  }
+  k_full_deg<<<pc_grid(ctx, (size_t)n + 1, 256), 256, 0, ctx->stream>>>(
+      d_uoff, lo.as<uint64_t>(), hi.as<uint64_t>(), n, deg.as<uint64_t>(), lc.as<uint64_t>());
+  PC_CHECK_LAUNCH();
+  pc_exclusive_scan_u64(ctx, deg.as<uint64_t>(), off, (size_t)n + 1);
+  pc_exclusive_scan_u64(ctx, lc.as<uint64_t>(), loff.as<uint64_t>(), (size_t)n + 1);
+  ctx->launches += 3;
+  mark();
+  if (m) {
+    make_crow(ctx, ctx->crow);
+    k_full_rows<<<pc_grid(ctx, nnz, 256, 16), 256, 0, ctx->stream>>>(
+        off, ctx->crow.as<uint32_t>(), nnz, loff.as<uint64_t>(), lsorted, d_uoff, d_unbr,
+        ctx->nbr.as<uint32_t>());
+    PC_CHECK_LAUNCH();
+    ctx->launches += 1;
+  }
+  mark();
+  if (tm) {
+    PC_CUDA(cudaStreamSynchronize(ctx->stream));
+    fprintf(stderr, "[symmetrize ms]");
+    for (size_t i = 1; i < evs.size(); i++) {
+      float x = 0;
+      cudaEventElapsedTime(&x, evs[i - 1], evs[i]);
+      fprintf(stderr, " %.3f", x);
+    }
+    fprintf(stderr, "  (pairs, sort, runs+degrees+scans, rows)\n");
+    for (auto e : evs) cudaEventDestroy(e);
+  }
 }
 
 // ------------------------------------------------------------- generators

@@ -131,7 +131,8 @@ struct DeltaList {
 // a graph load in flight (pacim_load_graph_async): the host CSR copied into
 // these buffers on the copy stream, committed by the next call needing the graph
 struct StagedGraph {
-  DevBuf off, nbr;
+  DevBuf off, nbr;  // the CSR as sent (upper: the upper CSR, symmetrized at commit)
+  bool upper = false;
   cudaEvent_t done = nullptr;  // recorded on the copy stream after the copies
   bool pending = false;
   uint32_t n = 0;
@@ -184,6 +185,12 @@ struct pacim_ctx {
   // ---- graph (H0/H1)
   bool has_graph = false;
   uint64_t graph_gen = 0;  // incremented by every graph load (derived-table caches)
+  // strategy hints of the builds (store choice, slot epochs, list capacities)
+  // are remembered per hint_gen: it changes only when a load brings a graph of
+  // another shape (n, m, rows, edge model) — the same graph loaded again (the
+  // e2e loop) keeps the measured choices
+  uint64_t hint_gen = 0;
+  uint64_t graph_sig = 0;
   uint32_t n = 0;
   uint64_t m = 0;        // undirected edges
   int pmodel = 0;        // PACIM_P_CONST / PACIM_P_WIC / PACIM_P_UNIFORM
@@ -258,6 +265,7 @@ struct pacim_ctx {
   double ep_live_per_slot = 0;
   // hook list of epoch builds (k_edges -> k_compress_count<…, LIST>): capacity
   // from the non-root count of the last dense build of graph_gen (hk_gen)
+  DevBuf sym[11];       // scratch of the upper-CSR symmetrization (graph.cu), kept across loads
   DevBuf hk_list;
   uint64_t hk_hint = 0, hk_gen = ~0ull, hk_cap = 0;
   uint32_t hk_B = 0;
@@ -368,6 +376,14 @@ struct TmpBuf : DevBuf {
 void pc_exclusive_scan_u64(pacim_ctx *ctx, const uint64_t *in, uint64_t *out,
                            size_t N);
 void pc_graph_finish_load(pacim_ctx *ctx, int validate);
+// upper CSR (each undirected edge once, neighbours > u, sorted; device arrays)
+// -> the symmetric CSR in ctx->off / ctx->nbr (graph.cu)
+void pc_validate_upper(pacim_ctx *ctx, const uint64_t *d_uoff, const uint32_t *d_unbr, uint32_t n);
+void pc_symmetrize_upper(pacim_ctx *ctx, const uint64_t *d_uoff, const uint32_t *d_unbr,
+                         uint32_t n, uint64_t m);
+void pc_sym_free(pacim_ctx *ctx);
+// after every graph load: graph_gen++, hint_gen++ if the shape changed (api.cu)
+void pc_graph_loaded(pacim_ctx *ctx);
 void pc_generate(pacim_ctx *ctx, int kind, const uint64_t *params, int nparams,
                  uint64_t gen_seed);
 // build.cu

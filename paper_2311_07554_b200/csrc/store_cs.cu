@@ -891,7 +891,7 @@ bool pc_cs_build(pacim_ctx *ctx) {
   }
   // an earlier build of this graph with these many slots found the sketches
   // too dense for the compact store (the mask pass is not repeated)
-  if (!force && ctx->cs_pref_gen == ctx->graph_gen && ctx->cs_pref_B == B && ctx->cs_pref_dense)
+  if (!force && ctx->cs_pref_gen == ctx->hint_gen && ctx->cs_pref_B == B && ctx->cs_pref_dense)
     return false;
   const uint32_t MW = (B + 31) / 32;
   pc_slot_table(ctx);
@@ -930,7 +930,7 @@ bool pc_cs_build(pacim_ctx *ctx) {
   // of one rank's shard: 256 slots, 0.34 pairs per edge: 90 vs 83 ms; 128
   // slots: 58 vs 56; 64: 38 vs 42; 32: 25.5 vs 33.6); the rate of the last
   // build of this graph and key decides, else the slot count
-  const bool same = ctx->cs_live_gen == ctx->graph_gen && ctx->cs_live_K == ctx->K &&
+  const bool same = ctx->cs_live_gen == ctx->hint_gen && ctx->cs_live_K == ctx->K &&
                     ctx->cs_live_rate >= 0;
   const bool want_list = pl_env > 1 || (same ? ctx->cs_live_rate * B < 0.12 : B <= 64);
   if (nr < (1u << 28) && B <= 256 && pl_env != 0 && want_list) {
@@ -975,7 +975,7 @@ bool pc_cs_build(pacim_ctx *ctx) {
   PC_CUDA(cudaMemcpyAsync(&npairs, ctr + 16, 8, cudaMemcpyDeviceToHost, ctx->stream));
   PC_CUDA(cudaMemcpyAsync(&nlive, ctr + 13, 8, cudaMemcpyDeviceToHost, ctx->stream));
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
-  ctx->cs_live_gen = ctx->graph_gen;
+  ctx->cs_live_gen = ctx->hint_gen;
   ctx->cs_live_K = ctx->K;
   ctx->cs_live_rate = ctx->m ? (double)nlive / ((double)ctx->m * B) : 0.0;
   ctx->cs_live_B = pcap ? B : 0;
@@ -986,7 +986,7 @@ bool pc_cs_build(pacim_ctx *ctx) {
   // is larger than the dense one
   const double dmax = getenv("PACIM_CS_DENSITY") ? atof(getenv("PACIM_CS_DENSITY")) : 0.5;
   const bool dense = total >= (1ull << 31) || (double)total > dmax * (double)nr * B;
-  ctx->cs_pref_gen = ctx->graph_gen;
+  ctx->cs_pref_gen = ctx->hint_gen;
   ctx->cs_pref_B = B;
   ctx->cs_pref_dense = dense;
   if (dense) {

@@ -148,8 +148,11 @@ def test_dense_store_slot_epochs(orc, ctx, i, bits, hl, monkeypatch):
         ctx.pacim_build_sketches(R, seed)
         st = ctx.pacim_get_stats()
         assert st["store"] == 0
-        want = hl == "1" and t >= 1 and i != 9 and R >= 16
-        assert st["build_hook_list"] == int(want), (t, st["build_hook_list"])
+        # (the first build of a load may already use the list when the last
+        # graph loaded had the same shape: the hints survive such reloads)
+        want = hl == "1" and i != 9 and R >= 16
+        if t >= 1 or not want:
+            assert st["build_hook_list"] == int(want), (t, st["build_hook_list"])
         for r in range(R):
             lab, _ = orc.sketch_labels(g, model, t32, seed, r)
             assert np.array_equal(ctx.pacim_get_labels(r), lab), (t, r)
@@ -305,6 +308,92 @@ def test_edge_cases(orc, ctx, pc):
         ctx.pacim_build_sketches(4, 1)  # graph dropped by the failed load -> ESTATE
     with pytest.raises(pc.PacimError):  # asymmetric CSR
         ctx.pacim_load_graph(np.array([0, 1, 1], np.uint64), np.array([1], np.uint32), 0, 1, 2)
+
+
+def upper_of(off, nbr):
+    """The upper CSR (row u keeps its neighbours > u) of a symmetric CSR."""
+    off = np.asarray(off, np.int64)
+    nbr = np.asarray(nbr, np.uint32)
+    n = len(off) - 1
+    rows = np.repeat(np.arange(n, dtype=np.int64), np.diff(off))
+    keep = nbr.astype(np.int64) > rows
+    uoff = np.zeros(n + 1, np.uint64)
+    np.cumsum(np.bincount(rows[keep], minlength=n), out=uoff[1:])
+    return uoff, nbr[keep]
+
+
+@pytest.mark.parametrize("mode", ["sync", "async"])
+@pytest.mark.parametrize("i", range(len(CASES)))
+def test_upper_csr_load(orc, ctx, i, mode):
+    """H0 from the upper CSR (pacim_load_graph_upper[_async]: each edge once,
+    the device builds the symmetric CSR — the transpose by a target
+    histogram, atomic cursors and a segmented sort): exactly the symmetric CSR
+    (pacim_get_graph), then the oracle's greedy on it."""
+    from oracle.oracle import Graph
+    build_fn, p, R, k = CASES[i]
+    off, nbr = build_fn()
+    g = Graph(len(off) - 1, off, nbr)
+    model, t32 = model_of(orc, p)
+    uo, un = upper_of(off, nbr)
+    if mode == "sync":
+        ctx.pacim_load_graph_upper(uo, un, model, t32, 1)
+    else:
+        ctx.pacim_load_graph_upper_async(uo, un, model, t32)
+    seed = 1500 + i
+    ctx.pacim_build_sketches(R, seed)  # commits an asynchronous load
+    o2, n2 = ctx.pacim_get_graph()
+    assert np.array_equal(o2, np.asarray(off, np.uint64)) and np.array_equal(n2, np.asarray(nbr, np.uint32))
+    s, gn, sg, _ = ctx.pacim_select_seeds(min(k, g.n))
+    es, egn, esg, eg0 = orc.greedy(g, model, t32, R, seed, min(k, g.n), want_gain0=True)
+    assert list(s) == list(es) and list(gn) == list(egn) and list(sg) == list(esg)
+    assert np.array_equal(ctx.pacim_get_gain0(), eg0)
+
+
+def test_upper_csr_load_edge_cases(orc, ctx, pc):
+    """Upper loads: no edges, isolated vertices between and after the edges,
+    a hub whose lower list spans many chunks, and invalid upper CSRs (an entry
+    v <= u, unsorted rows, v >= n, offsets[n] != m) raise."""
+    from oracle.oracle import Graph
+    ctx.pacim_load_graph_upper(np.zeros(9, np.uint64), np.zeros(0, np.uint32), 0, 1 << 31, 1)
+    o2, n2 = ctx.pacim_get_graph()
+    assert list(o2) == [0] * 9 and len(n2) == 0
+    # vertex 3000 adjacent to every even vertex below it (its lower list: 1500
+    # entries), isolated odd vertices, a tail of isolated vertices
+    edges = [(v, 3000) for v in range(0, 3000, 2)] + [(v, v + 2) for v in range(0, 2990, 6)]
+    off, nbr = inputs.csr_from_edges(3100, edges)
+    uo, un = upper_of(off, nbr)
+    ctx.pacim_load_graph_upper(uo, un, 0, orc.t32_const(0.3), 1)
+    o2, n2 = ctx.pacim_get_graph()
+    assert np.array_equal(o2, np.asarray(off, np.uint64)) and np.array_equal(n2, np.asarray(nbr, np.uint32))
+    ctx.pacim_build_sketches(16, 5)
+    s, gn, _, _ = ctx.pacim_select_seeds(5)
+    es, egn, _, _ = orc.greedy(Graph(3100, off, nbr), 0, orc.t32_const(0.3), 16, 5, 5)
+    assert list(s) == list(es) and list(gn) == list(egn)
+    for bad_off, bad_nbr in [([0, 1, 1], [0]),          # v == u
+                             ([0, 2, 2, 2], [2, 1]),    # unsorted row
+                             ([0, 1, 1], [5]),          # v >= n
+                             ([0, 1, 2], [1, 2])]:      # row 1: 2 >= n
+        with pytest.raises(pc.PacimError):
+            ctx.pacim_load_graph_upper(np.array(bad_off, np.uint64), np.array(bad_nbr, np.uint32),
+                                       0, 1 << 31, 1)
+    with pytest.raises(pc.PacimError):  # offsets[n] != m
+        ctx.pacim_load_graph_upper(np.array([0, 2, 2], np.uint64), np.array([1], np.uint32),
+                                   0, 1 << 31, 1)
+
+
+def test_upper_csr_load_c2(ctx):
+    """The full c2 graph through the upper load: the device-built symmetric
+    CSR equals the generated one (sha256 of both arrays)."""
+    from paper_2311_07554_b200 import pipeline
+    cfg = inputs.config("c2")
+    pipeline.generate(ctx, cfg)
+    off, nbr = ctx.pacim_get_graph()
+    h = (sha(off), sha(nbr))
+    uo, un = upper_of(off, nbr)
+    assert len(un) * 2 == len(nbr)
+    ctx.pacim_load_graph_upper(uo, un, *pipeline.model_of(cfg), 1)
+    o2, n2 = ctx.pacim_get_graph()
+    assert (sha(o2), sha(n2)) == h
 
 
 @pytest.mark.parametrize("p", [0.4, "wic", ("unif", 0.2, 0.6)])
