@@ -754,6 +754,7 @@ void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *l
   P.nbr = ctx->nbr.as<uint32_t>();
   P.K = ctx->K;
   P.t32 = ctx->t32;
+  pc_ensure_tcsr(ctx);
   P.tcsr = ctx->pmodel != PACIM_P_CONST ? ctx->tcsr.as<uint32_t>() : nullptr;
   P.toff = ctx->toff();
   P.decor = ctx->hash_rule;

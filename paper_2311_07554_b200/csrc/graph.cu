@@ -216,7 +216,7 @@ __global__ void k_edge_derive(const uint64_t *off, const uint32_t *nbr, const ui
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
        e += (size_t)gridDim.x * blockDim.x) {
     const uint32_t u = entry_row(off, crow, e), w = nbr[e];
-    if (pmodel == PACIM_P_CONST && w < u) continue;  // lower entries: nothing to write
+    if (!tcsr && w < u) continue;  // lower entries: nothing to write
     const uint64_t iu = vinfo[u], iw = vinfo[w];
     uint64_t T = 0;
     if (pmodel == PACIM_P_WIC) {
@@ -226,7 +226,7 @@ __global__ void k_edge_derive(const uint64_t *off, const uint32_t *nbr, const ui
       const uint64_t a = u < w ? u : w, b = u < w ? w : u;
       T = pc_t32_uniform(t32, (a << 32) | b);
     }
-    if (pmodel != PACIM_P_CONST) tcsr[e] = (uint32_t)(T - toff);
+    if (tcsr) tcsr[e] = (uint32_t)(T - toff);
     if (w > u) {
       const uint64_t pos = ustart[u] + (e - (off[u + 1] - ucnt[u]));
       keys[pos] = ((uint64_t)u << 32) | w;
@@ -404,10 +404,11 @@ static void derive_edges(pacim_ctx *ctx) {
   pc_ensure(ctx, ctx->keys, std::max<size_t>(m, 1) * 8);
   pc_ensure(ctx, ctx->ckeys, std::max<size_t>(m, 1) * 8);
   const bool per_edge = ctx->pmodel != PACIM_P_CONST;
-  if (per_edge) {
-    pc_ensure(ctx, ctx->tm1, std::max<size_t>(m, 1) * sizeof(uint32_t));
-    pc_ensure(ctx, ctx->tcsr, std::max<size_t>(nnz, 1) * sizeof(uint32_t));
-  }
+  if (per_edge) pc_ensure(ctx, ctx->tm1, std::max<size_t>(m, 1) * sizeof(uint32_t));
+  // the per-CSR-entry thresholds (tcsr) are derived on first use
+  // (pc_ensure_tcsr: traversal selections, compressed probes, Monte Carlo):
+  // the build reads the per-edge tm1 only
+  ctx->tcsr_ok = false;
   if (nnz) {
     make_crow(ctx, ctx->crow);  // capacity kept across loads (no cudaMalloc per load)
     pc_ensure(ctx, ctx->vinfo, (size_t)n * 8);
@@ -418,11 +419,45 @@ static void derive_edges(pacim_ctx *ctx) {
     k_edge_derive<<<pc_grid(ctx, nnz, 256), 256, 0, ctx->stream>>>(
         off, nbr, ctx->crow.as<uint32_t>(), nnz, ustart, ucnt, ctx->vinfo.as<uint64_t>(),
         ctx->pmodel, ctx->t32, ctx->toff(), ctx->keys.as<uint64_t>(), ctx->ckeys.as<uint64_t>(),
-        per_edge ? ctx->tm1.as<uint32_t>() : nullptr, per_edge ? ctx->tcsr.as<uint32_t>() : nullptr);
+        per_edge ? ctx->tm1.as<uint32_t>() : nullptr, nullptr);
     PC_CHECK_LAUNCH();
   }
   ctx->launches += 4;
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+namespace {
+// tcsr[e] = T32 - toff of CSR entry e = (u, w): WIC R4 from the two degrees
+// (vinfo), Uniform R19 from the edge key
+__global__ void k_tcsr(const uint64_t *off, const uint32_t *nbr, const uint32_t *crow, uint64_t nnz,
+                       const uint64_t *vinfo, int pmodel, uint64_t t32, uint32_t toff,
+                       uint32_t *tcsr) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
+       e += (size_t)gridDim.x * blockDim.x) {
+    const uint32_t u = entry_row(off, crow, e), w = nbr[e];
+    uint64_t T;
+    if (pmodel == PACIM_P_WIC) {
+      T = (1ull << 33) / ((vinfo[u] >> 32) + (vinfo[w] >> 32));
+      if (T > (1ull << 32)) T = 1ull << 32;
+    } else {
+      const uint64_t a = u < w ? u : w, b = u < w ? w : u;
+      T = pc_t32_uniform(t32, (a << 32) | b);
+    }
+    tcsr[e] = (uint32_t)(T - toff);
+  }
+}
+}  // namespace
+
+void pc_ensure_tcsr(pacim_ctx *ctx) {
+  if (ctx->pmodel == PACIM_P_CONST || ctx->tcsr_ok) return;
+  const uint64_t nnz = 2 * ctx->m;
+  pc_ensure(ctx, ctx->tcsr, std::max<size_t>(nnz, 1) * sizeof(uint32_t));
+  if (nnz)
+    k_tcsr<<<pc_grid(ctx, nnz, 256), 256, 0, ctx->stream>>>(
+        ctx->off.as<uint64_t>(), ctx->nbr.as<uint32_t>(), ctx->crow.as<uint32_t>(), nnz,
+        ctx->vinfo.as<uint64_t>(), ctx->pmodel, ctx->t32, ctx->toff(), ctx->tcsr.as<uint32_t>());
+  PC_CHECK_LAUNCH();
+  ctx->tcsr_ok = true;
 }
 
 static void derive_common(pacim_ctx *ctx) {

@@ -136,6 +136,7 @@ void pc_simulate_ic(pacim_ctx *ctx, const uint32_t *seeds_host, uint32_t ns, uin
   M.off = ctx->off.as<uint64_t>();
   M.nbr = ctx->nbr.as<uint32_t>();
   M.per_edge = ctx->pmodel != PACIM_P_CONST;
+  pc_ensure_tcsr(ctx);
   M.tcsr = ctx->tcsr.as<uint32_t>();
   M.toff = ctx->toff();
   M.t32 = ctx->t32;

@@ -266,6 +266,7 @@ struct pacim_ctx {
   // hook list of epoch builds (k_edges -> k_compress_count<…, LIST>): capacity
   // from the non-root count of the last dense build of graph_gen (hk_gen)
   DevBuf sym[11];       // scratch of the upper-CSR symmetrization (graph.cu), kept across loads
+  bool tcsr_ok = false;  // tcsr derived for the current graph (pc_ensure_tcsr)
   DevBuf hk_list;
   uint64_t hk_hint = 0, hk_gen = ~0ull, hk_cap = 0;
   uint32_t hk_B = 0;
@@ -382,6 +383,8 @@ void pc_validate_upper(pacim_ctx *ctx, const uint64_t *d_uoff, const uint32_t *d
 void pc_symmetrize_upper(pacim_ctx *ctx, const uint64_t *d_uoff, const uint32_t *d_unbr,
                          uint32_t n, uint64_t m);
 void pc_sym_free(pacim_ctx *ctx);
+// the per-CSR-entry thresholds of per-edge models, derived on first use (graph.cu)
+void pc_ensure_tcsr(pacim_ctx *ctx);
 // after every graph load: graph_gen++, hint_gen++ if the shape changed (api.cu)
 void pc_graph_loaded(pacim_ctx *ctx);
 void pc_generate(pacim_ctx *ctx, int kind, const uint64_t *params, int nparams,

@@ -1477,7 +1477,7 @@ static Sel make_sel(pacim_ctx *ctx, long long *target) {
   S.nbr = ctx->nbr.as<uint32_t>();
   S.K = ctx->K;
   S.t32 = ctx->t32;
-  S.tcsr = ctx->tcsr.as<uint32_t>();
+  S.tcsr = ctx->tcsr.as<uint32_t>();  // valid after pc_ensure_tcsr (the traversals' callers)
   S.wic = ctx->pmodel != PACIM_P_CONST;  // per-edge thresholds in tcsr
   S.toff = ctx->toff();
   S.g_shr = ctx->d_shr.as<uint32_t>();
@@ -1644,6 +1644,7 @@ static void read_diag(pacim_ctx *ctx, const Sel &S) {
 void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
                int64_t *sigma_num) {
   if (ctx->cs) return pc_cs_select(ctx, k, seeds, gain_num, sigma_num);
+  pc_ensure_tcsr(ctx);  // the cover traversal reads per-entry thresholds
   const uint32_t n = ctx->n;
   pc_ensure(ctx, ctx->gain, (size_t)n * 8);
   if (k > ctx->sel_k_cap) {
@@ -1749,6 +1750,7 @@ void pc_select(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_num,
 // One multi-rank step: MarkSeed of the given seed s on this ctx's sketches and
 // the member deltas (-delta per member) accumulated into d_delta.
 void pc_cover_local(pacim_ctx *ctx, uint32_t s, int64_t *d_delta, int64_t *local_gain) {
+  pc_ensure_tcsr(ctx);  // the cover traversal reads per-entry thresholds
   if (ctx->cs) return pc_cs_cover_local(ctx, s, d_delta, local_gain);
   PC_REQUIRE(ctx->sel_list_valid, PACIM_ESTATE, "pacim_select_reset first");
   Sel S = make_sel(ctx, reinterpret_cast<long long *>(d_delta));
@@ -1837,6 +1839,7 @@ void pc_clear_deltas(pacim_ctx *ctx, int64_t *d_delta, const uint32_t *v, uint64
 // Store-less member traversal for the compressed store's big CCs (H10 with
 // H6c): slot j's members of C_j(s) lose delta[j] (HOST, R_local entries).
 void pc_traverse_slots(pacim_ctx *ctx, uint32_t s, int64_t *target, const uint32_t *delta) {
+  pc_ensure_tcsr(ctx);  // the cover traversal reads per-entry thresholds
   Sel S = make_sel(ctx, reinterpret_cast<long long *>(target));
   S.trav_only = 1;
   S.warp_ok = 0;  // these CCs are larger than the probe's queue
