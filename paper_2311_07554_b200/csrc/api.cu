@@ -173,7 +173,7 @@ static void free_all(pacim_ctx *ctx) {
                     &ctx->scratch, &ctx->scratch2, &ctx->sel_seeds, &ctx->sel_gain,
                     &ctx->sel_partial, &ctx->sel_list, &ctx->sel_flag, &ctx->argmax_part, &ctx->bfs, &ctx->tcsr, &ctx->hidx, &ctx->hub_tab, &ctx->hla_off, &ctx->hla_row, &ctx->hla_raw, &ctx->d_smap, &ctx->pkeys, &ctx->cprobe, &ctx->cseed, &ctx->d_hr64, &ctx->crow, &ctx->vinfo, &ctx->hotsum, &ctx->d_hot_size,
                     &ctx->cs_rec, &ctx->cs_soff, &ctx->cs_ecrow, &ctx->cs_E, &ctx->cs_vid,
-                    &ctx->cs_diag, &ctx->cs_cnt, &ctx->cs_plist, &ctx->edge_work, &ctx->wt_buf, &ctx->dist_ghot, &ctx->dist_buf, &ctx->dist_cov_old, &ctx->ep_tab, &ctx->ep_send, &ctx->ep_cnt, &ctx->hk_list};
+                    &ctx->cs_diag, &ctx->cs_cnt, &ctx->cs_plist, &ctx->edge_work, &ctx->wt_buf, &ctx->dist_ghot, &ctx->dist_buf, &ctx->dist_cov_old, &ctx->ep_tab, &ctx->ep_send, &ctx->ep_cnt, &ctx->hk_list, &ctx->uoff, &ctx->ucrow, &ctx->rk, &ctx->unbr, &ctx->ud16, &ctx->uvrow, &ctx->ucrowr};
   for (DevBuf *b : bufs) pc_free(ctx, *b);
   pc_sym_free(ctx);
 }

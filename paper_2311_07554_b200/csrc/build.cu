@@ -177,7 +177,11 @@ __device__ __forceinline__ void pl_append(const PairList &pl, unsigned long long
 // L = the {P, next} words of the entries, (row, slot) = entry
 // pc_cs_pos(rec, MW, row, slot); CS = 2: the mask pass, every live (edge,
 // slot) sets bit slot of both endpoints' row masks (L = the rec words)
-template <bool WIC, bool REC, bool DECOR, bool LEAN, int CS = 0, bool EP = false>
+// LEAN = 2 (UpperCsr, the dense store, no HLA): upper edge e from the
+// symmetric CSR (row by the chunk table ucrow, neighbour nbr[off[u+1] -
+// (uoff[u+1] - e)]), the threshold tm1[e] (per-edge models), the store rows
+// from the rank map — 8 B streamed per edge instead of keys + ckeys + tm1's 20
+template <bool WIC, bool REC, bool DECOR, int LEAN, int CS = 0, bool EP = false>
 __global__ void __launch_bounds__(EDGE_THREADS, PACIM_EDGE_BLOCKS) k_edges(const uint64_t *__restrict__ keys,
                                                         const uint64_t *__restrict__ ckeys,
                                                         const uint32_t *__restrict__ tm1,
@@ -190,7 +194,7 @@ __global__ void __launch_bounds__(EDGE_THREADS, PACIM_EDGE_BLOCKS) k_edges(const
                                                         const uint64_t *__restrict__ hr64,
                                                         const uint2 *__restrict__ rec,
                                                         uint32_t MW, PairList pl, Ep ep,
-                                                        EdgeWork ew) {
+                                                        EdgeWork ew, UpperCsr uc = UpperCsr{}) {
   // slots [j0, j0 + Bb) of the B sorted slots go to L (row stride Bb)
   extern __shared__ uint32_t sm[];
   uint32_t *shr = sm;
@@ -225,18 +229,38 @@ __global__ void __launch_bounds__(EDGE_THREADS, PACIM_EDGE_BLOCKS) k_edges(const
     const size_t e = base + lane;
     uint32_t cnt = 0, eu = 0, ev = 0, ehe = 0, elo = 0;
     uint64_t eT = 0, ehe64 = 0;
-    uint64_t lkey = 0;
+    uint64_t lkey = 0, lrow = 0;
     bool upper = e < m;
-    if (LEAN && upper) {
-      uint32_t u = tm1[base >> 5];
-      while (e >= keys[u + 1]) u++;
+    if (LEAN == 2 && upper) {
+      const uint32_t v = uc.unbr[e], d = uc.ud16[e];
+      uint32_t u = uc.ucrow[base >> 5], ru = uc.ucrowr[base >> 5] + (d >> 8);
+      if ((d & 255u) != 255u)
+        u += d & 255u;
+      else  // the offsets search from the chunk's first row to the next chunk's
+        u = pc_row_of(uc.uoff, u, (base >> 5) + 1 < niter ? uc.ucrow[(base >> 5) + 1] : uc.nv - 1, e);
+      if ((d >> 8) == 255u) {
+        const uint2 a = uc.rk[u >> 5];
+        ru = a.x + __popc(a.y & ((1u << (u & 31)) - 1));
+      }
+      lkey = ((uint64_t)u << 32) | v;
+      uint32_t rv;
+      if (uc.uvrow) {
+        rv = uc.uvrow[e];
+      } else {
+        const uint2 b = uc.rk[v >> 5];
+        rv = b.x + __popc(b.y & ((1u << (v & 31)) - 1));
+      }
+      lrow = ((uint64_t)ru << 32) | rv;
+    } else if (LEAN && upper) {
+      const uint32_t u = pc_row_of(keys, tm1[base >> 5],
+                                   (base >> 5) + 1 < niter ? tm1[(base >> 5) + 1] : uc.nv - 1, e);
       const uint32_t v = reinterpret_cast<const uint32_t *>(ckeys)[e];
       upper = v > u;
       lkey = ((uint64_t)u << 32) | v;
     }
     if (upper) {
       const uint64_t key = LEAN ? lkey : keys[e];
-      const uint64_t T = (WIC && !LEAN) ? (uint64_t)tm1[e] + t32 : t32;  // per-edge: t32 = toff
+      const uint64_t T = (WIC && LEAN != 1) ? (uint64_t)tm1[e] + t32 : t32;  // per-edge: t32 = toff
       const uint64_t he64 = pc_mix64(key ^ K);
       const uint32_t he = (uint32_t)(he64 >> 32);
       uint32_t lo = 0, hi = 0;
@@ -262,7 +286,7 @@ __global__ void __launch_bounds__(EDGE_THREADS, PACIM_EDGE_BLOCKS) k_edges(const
       hi = min(hi, j0 + Bb);
       if (hi < lo) hi = lo;
       cnt = hi - lo;
-      const uint64_t ck = LEAN ? lkey : ckeys[e];  // the endpoints' store rows (+ hub flags)
+      const uint64_t ck = LEAN == 2 ? lrow : LEAN ? lkey : ckeys[e];  // the endpoints' store rows (+ hub flags)
       eu = (uint32_t)(ck >> 32);
       ev = (uint32_t)ck;
       ehe = he;
@@ -1168,9 +1192,7 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
   if (es_in) {
     es = *es_in;
   } else {
-    es.keys = ctx->keys.as<uint64_t>();
-    es.ckeys = ctx->ckeys.as<uint64_t>();
-    es.m = ctx->m;
+    es.m = ctx->m;  // the edge lists, if used, below
   }
   const uint32_t n = ctx->nr, B = ctx->R_local;
   const bool ep_on = ctx->ep.mask != 0;  // slot epochs (pc_build)
@@ -1225,7 +1247,41 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
   {
     size_t smem = B * sizeof(uint32_t) + (NT + 1) * sizeof(uint16_t);
     unsigned g = pc_grid(ctx, (es.m + 31) / 32 * 32, EDGE_THREADS, PACIM_EDGE_BLOCKS);
-    if (ctx->lean) {  // no edge list: the upper edges from the CSR (c5)
+    // graphs loaded with the upper-edge stream (derive_edges): the dense
+    // store's one-window builds without HLA recording read it
+    const bool ucsr = ctx->ucsr && !ctx->lean && !es_in && !hla.raw;
+    if (!ctx->lean && !ucsr) {
+      pc_ensure_edge_lists(ctx);
+      if (!es_in) {
+        es.keys = ctx->keys.as<uint64_t>();
+        es.ckeys = ctx->ckeys.as<uint64_t>();
+      }
+    }
+    UpperCsr uc;
+    if (ucsr) {
+      uc.nv = ctx->n;
+      uc.uoff = ctx->uoff.as<uint64_t>();
+      uc.unbr = ctx->unbr.as<uint32_t>();
+      uc.ud16 = ctx->ud16.as<uint16_t>();
+      uc.ucrowr = ctx->ucrowr.as<uint32_t>();
+      uc.uvrow = ctx->uvrow.p ? ctx->uvrow.as<uint32_t>() : nullptr;
+      uc.ucrow = ctx->ucrow.as<uint32_t>();
+      uc.rk = ctx->rk.as<uint2>();
+    }
+    if (ucsr) {
+      const bool pe = ctx->pmodel != PACIM_P_CONST;
+      auto kern = ctx->hash_rule
+                      ? (pe ? (ep_on ? k_edges<true, false, true, 2, 0, true> : k_edges<true, false, true, 2>)
+                            : (ep_on ? k_edges<false, false, true, 2, 0, true> : k_edges<false, false, true, 2>))
+                      : (pe ? (ep_on ? k_edges<true, false, false, 2, 0, true> : k_edges<true, false, false, 2>)
+                            : (ep_on ? k_edges<false, false, false, 2, 0, true> : k_edges<false, false, false, 2>));
+      PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
+          nullptr, nullptr, pe ? ctx->tm1.as<uint32_t>() : nullptr, ctx->m, ctx->K,
+          pe ? ctx->toff() : ctx->t32, ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb,
+          ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), nullptr, 0u, hk, ctx->ep,
+          edge_work(ctx, ctx->m, g), uc);
+    } else if (ctx->lean) {  // no edge list: the upper edges from the CSR (c5)
       auto kern = ctx->hash_rule ? (ep_on ? k_edges<false, false, true, true, 0, true> : k_edges<false, false, true, true>) : (ep_on ? k_edges<false, false, false, true, 0, true> : k_edges<false, false, false, true>);
       PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       const uint64_t nnz = 2 * ctx->m;
@@ -1234,7 +1290,7 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
           ctx->off.as<uint64_t>(), reinterpret_cast<const uint64_t *>(ctx->nbr.p),
           ctx->crow.as<uint32_t>(), nnz, ctx->K, ctx->t32, ctx->d_shr.as<uint32_t>(),
           ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), nullptr, 0u, hk, ctx->ep,
-          edge_work(ctx, nnz, gl));
+          edge_work(ctx, nnz, gl), UpperCsr{ctx->n});
     } else if (ctx->pmodel != PACIM_P_CONST) {  // per-edge thresholds (WIC, Uniform)
       auto kern = ctx->hash_rule ? (hla.raw ? (ep_on ? k_edges<true, true, true, false, 0, true> : k_edges<true, true, true, false>) : (ep_on ? k_edges<true, false, true, false, 0, true> : k_edges<true, false, true, false>))
                                  : (hla.raw ? (ep_on ? k_edges<true, true, false, false, 0, true> : k_edges<true, true, false, false>) : (ep_on ? k_edges<true, false, false, false, 0, true> : k_edges<true, false, false, false>));
@@ -1242,7 +1298,7 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
       kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
           es.keys, es.ckeys, ctx->tm1.as<uint32_t>(), es.m,
           ctx->K, ctx->toff(), ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla,
-          ctx->d_hr64.as<uint64_t>(), nullptr, 0u, hk, ctx->ep, edge_work(ctx, es.m, g));
+          ctx->d_hr64.as<uint64_t>(), nullptr, 0u, hk, ctx->ep, edge_work(ctx, es.m, g), UpperCsr{});
     } else {
       auto kern = ctx->hash_rule ? (hla.raw ? (ep_on ? k_edges<false, true, true, false, 0, true> : k_edges<false, true, true, false>) : (ep_on ? k_edges<false, false, true, false, 0, true> : k_edges<false, false, true, false>))
                                  : (hla.raw ? (ep_on ? k_edges<false, true, false, false, 0, true> : k_edges<false, true, false, false>) : (ep_on ? k_edges<false, false, false, false, 0, true> : k_edges<false, false, false, false>));
@@ -1250,7 +1306,7 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
       kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
           es.keys, es.ckeys, nullptr, es.m, ctx->K, ctx->t32,
           ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, hla,
-          ctx->d_hr64.as<uint64_t>(), nullptr, 0u, hk, ctx->ep, edge_work(ctx, es.m, g));
+          ctx->d_hr64.as<uint64_t>(), nullptr, 0u, hk, ctx->ep, edge_work(ctx, es.m, g), UpperCsr{});
     }
     PC_CHECK_LAUNCH();
   }
@@ -1304,8 +1360,9 @@ static void cs_edges(pacim_ctx *ctx, uint32_t *L, const uint2 *rec, uint32_t MW,
         ctx->off.as<uint64_t>(), reinterpret_cast<const uint64_t *>(ctx->nbr.p),
         ctx->crow.as<uint32_t>(), nnz, ctx->K, ctx->t32, ctx->d_shr.as<uint32_t>(),
         ctx->d_tab.as<uint16_t>(), B, 0, B, L, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), rec, MW, pl, Ep{},
-        edge_work(ctx, nnz, gl));
+        edge_work(ctx, nnz, gl), UpperCsr{ctx->n});
   } else {
+    pc_ensure_edge_lists(ctx);
     const bool pe = ctx->pmodel != PACIM_P_CONST;
     auto kern = pe ? (ctx->hash_rule ? k_edges<true, false, true, false, MODE>
                                      : k_edges<true, false, false, false, MODE>)
@@ -1317,7 +1374,7 @@ static void cs_edges(pacim_ctx *ctx, uint32_t *L, const uint2 *rec, uint32_t MW,
         ctx->keys.as<uint64_t>(), ctx->ckeys.as<uint64_t>(),
         pe ? ctx->tm1.as<uint32_t>() : nullptr, ctx->m, ctx->K, pe ? ctx->toff() : ctx->t32,
         ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, 0, B, L, ctr + 4, Hla{},
-        ctx->d_hr64.as<uint64_t>(), rec, MW, pl, Ep{}, edge_work(ctx, ctx->m, g));
+        ctx->d_hr64.as<uint64_t>(), rec, MW, pl, Ep{}, edge_work(ctx, ctx->m, g), UpperCsr{});
   }
   PC_CHECK_LAUNCH();
   ctx->launches++;
@@ -1354,6 +1411,7 @@ void pc_ep_edges(pacim_ctx *ctx, uint64_t e0, uint64_t e1, const uint32_t *d_shr
   PC_REQUIRE(!ctx->lean && !ctx->hash_rule && R <= 256, PACIM_ENOTIMPL,
              "edge-partitioned build: edge lists, rule R2, R <= 256");
   if (e1 <= e0) return;
+  pc_ensure_edge_lists(ctx);
   PairList pl;
   pl.p = plist;
   pl.cnt = pcnt;
@@ -1368,7 +1426,7 @@ void pc_ep_edges(pacim_ctx *ctx, uint64_t e0, uint64_t e1, const uint32_t *d_shr
   kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
       ctx->keys.as<uint64_t>() + e0, ctx->ckeys.as<uint64_t>() + e0,
       pe ? ctx->tm1.as<uint32_t>() + e0 : nullptr, m, ctx->K, pe ? ctx->toff() : ctx->t32, d_shr_all,
-      d_tab_all, R, 0, R, nullptr, ctr + 4, Hla{}, nullptr, nullptr, 0u, pl, Ep{}, edge_work(ctx, m, g));
+      d_tab_all, R, 0, R, nullptr, ctr + 4, Hla{}, nullptr, nullptr, 0u, pl, Ep{}, edge_work(ctx, m, g), UpperCsr{});
   PC_CHECK_LAUNCH();
   ctx->launches++;
 }
@@ -1563,6 +1621,7 @@ void pc_build(pacim_ctx *ctx) {
   if (W) {
     const uint32_t NB = 1u << W;
     const uint64_t m = ctx->m;
+    pc_ensure_edge_lists(ctx);
     pc_ensure(ctx, ctx->pkeys, std::max<uint64_t>(m, 1) * 16 + (NB + 1) * 16);
     uint64_t *pk = ctx->pkeys.as<uint64_t>(), *pck = pk + m;
     unsigned long long *cnt = reinterpret_cast<unsigned long long *>(pck + m);

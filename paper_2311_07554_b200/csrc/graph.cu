@@ -209,17 +209,33 @@ __global__ void k_vinfo(const uint64_t *off, const uint32_t *cid, const uint32_t
 // threshold T32 - toff per upper edge (tm1) and per CSR entry (tcsr):
 // WIC R4 T32 = min(2^32, floor(2^33 / (d_u + d_w))), Uniform R19
 // pc_t32_uniform(packed, key).
+// keys / ckeys null: the thresholds only (the per-build stream reads the CSR,
+// UpperCsr); tm1 null: the edge lists only (pc_ensure_edge_lists).
+// unbr / ud8 (UpperCsr): the upper neighbours and row deltas (ucrow given).
 __global__ void k_edge_derive(const uint64_t *off, const uint32_t *nbr, const uint32_t *crow,
-                              uint64_t nnz, const uint64_t *ustart, const uint64_t *ucnt,
+                              uint64_t nnz, const uint64_t *uoff,
                               const uint64_t *vinfo, int pmodel, uint64_t t32, uint32_t toff,
-                              uint64_t *keys, uint64_t *ckeys, uint32_t *tm1, uint32_t *tcsr) {
+                              uint64_t *keys, uint64_t *ckeys, uint32_t *tm1, uint32_t *tcsr,
+                              uint32_t *unbr = nullptr, uint16_t *ud16 = nullptr,
+                              const uint32_t *ucrow = nullptr, uint32_t *uvrow = nullptr,
+                              const uint32_t *ucrowr = nullptr, bool cap_all = false) {
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < nnz;
        e += (size_t)gridDim.x * blockDim.x) {
     const uint32_t u = entry_row(off, crow, e), w = nbr[e];
     if (!tcsr && w < u) continue;  // lower entries: nothing to write
+    if (unbr) {
+      const uint64_t pos = uoff[u + 1] - (off[u + 1] - e);
+      unbr[pos] = w;
+      const uint32_t du = min(255u, u - ucrow[pos >> 5]),
+                     dr = min(255u, ((uint32_t)vinfo[u] & ~PACIM_HUBF) - ucrowr[pos >> 5]);
+      ud16[pos] = cap_all ? (uint16_t)0xFFFF : (uint16_t)(du | dr << 8);
+      if (uvrow) uvrow[pos] = (uint32_t)vinfo[w] & ~PACIM_HUBF;
+    }
+    if (!tcsr && !tm1 && !keys) continue;
     const uint64_t iu = vinfo[u], iw = vinfo[w];
     uint64_t T = 0;
-    if (pmodel == PACIM_P_WIC) {
+    if (!tm1 && !tcsr) {
+    } else if (pmodel == PACIM_P_WIC) {
       T = (1ull << 33) / ((iu >> 32) + (iw >> 32));
       if (T > (1ull << 32)) T = 1ull << 32;
     } else if (pmodel == PACIM_P_UNIFORM) {
@@ -228,11 +244,36 @@ __global__ void k_edge_derive(const uint64_t *off, const uint32_t *nbr, const ui
     }
     if (tcsr) tcsr[e] = (uint32_t)(T - toff);
     if (w > u) {
-      const uint64_t pos = ustart[u] + (e - (off[u + 1] - ucnt[u]));
-      keys[pos] = ((uint64_t)u << 32) | w;
-      ckeys[pos] = ((iu & 0xFFFFFFFFull) << 32) | (iw & 0xFFFFFFFFull);
-      if (pmodel != PACIM_P_CONST) tm1[pos] = (uint32_t)(T - toff);
+      const uint64_t pos = uoff[u + 1] - (off[u + 1] - e);  // upper edge index
+      if (keys) {
+        keys[pos] = ((uint64_t)u << 32) | w;
+        ckeys[pos] = ((iu & 0xFFFFFFFFull) << 32) | (iw & 0xFFFFFFFFull);
+      }
+      if (tm1 && pmodel != PACIM_P_CONST) tm1[pos] = (uint32_t)(T - toff);
     }
+  }
+}
+
+// store row of every chunk's first upper-edge vertex (UpperCsr)
+__global__ void k_chunk_rows(const uint32_t *ucrow, const uint32_t *cid, uint64_t nch,
+                             uint32_t *ucrowr) {
+  for (size_t c = (size_t)blockIdx.x * blockDim.x + threadIdx.x; c < nch;
+       c += (size_t)gridDim.x * blockDim.x)
+    ucrowr[c] = cid[ucrow[c]];
+}
+
+// rank map of the store rows (UpperCsr): warp per 32 vertices, rk[w] = {row
+// of the word's first non-isolated vertex (cid), bitmap of its non-isolated
+// vertices}; rows keep the vertex order, so row(v) = rk.x + popc(below v)
+__global__ void k_rank_map(const uint64_t *off, const uint32_t *cid, uint32_t n, uint2 *rk) {
+  const uint32_t lane = threadIdx.x & 31;
+  const size_t nw = ((size_t)n + 31) / 32;
+  for (size_t w = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nw;
+       w += ((size_t)gridDim.x * blockDim.x) >> 5) {
+    const size_t v = w * 32 + lane;
+    const bool ni = v < n && off[v + 1] > off[v];
+    const uint32_t bm = __ballot_sync(0xffffffffu, ni);
+    if (lane == 0) rk[w] = make_uint2(bm ? cid[w * 32 + __ffs(bm) - 1] : 0u, bm);
   }
 }
 }  // namespace
@@ -308,6 +349,7 @@ __global__ void k_hub_table(const uint32_t *hidx, uint32_t nr, unsigned long lon
 static void derive_lean(pacim_ctx *ctx);
 namespace {
 __global__ void k_crow(const uint64_t *off, uint32_t n, uint32_t *crow);
+__global__ void k_crow_of(const uint64_t *off, uint32_t n, uint32_t *crow);
 __global__ void k_iota_u32(uint32_t *a, uint32_t n);
 }  // namespace
 
@@ -395,20 +437,55 @@ static void derive_edges(pacim_ctx *ctx) {
   const uint64_t m = ctx->m, nnz = 2 * m;
   uint64_t *off = ctx->off.as<uint64_t>();
   const uint32_t *nbr = ctx->nbr.as<uint32_t>();
-  pc_ensure(ctx, ctx->scratch, 2 * ((size_t)n + 1) * sizeof(uint64_t));
+  pc_ensure(ctx, ctx->scratch, ((size_t)n + 1) * sizeof(uint64_t));
   uint64_t *ucnt = ctx->scratch.as<uint64_t>();
-  uint64_t *ustart = ucnt + n + 1;
+  pc_ensure(ctx, ctx->uoff, ((size_t)n + 1) * sizeof(uint64_t));
+  uint64_t *uoff = ctx->uoff.as<uint64_t>();
   k_upper_count<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(off, nbr, n, ucnt);
   PC_CHECK_LAUNCH();
-  pc_exclusive_scan_u64(ctx, ucnt, ustart, n);
-  pc_ensure(ctx, ctx->keys, std::max<size_t>(m, 1) * 8);
-  pc_ensure(ctx, ctx->ckeys, std::max<size_t>(m, 1) * 8);
+  PC_CUDA(cudaMemsetAsync(ucnt + n, 0, 8, ctx->stream));
+  pc_exclusive_scan_u64(ctx, ucnt, uoff, (size_t)n + 1);
+  // Two forms of the upper edges for the build's edge pass (k_edges):
+  // * the edge lists keys / ckeys (16 B per upper edge, 25 GB at c4; + tm1):
+  //   fastest (k_edges is issue bound: the stream's decode adds ~11 % warp
+  //   instructions, c4 22.8 -> 24.3 ms), the default when they take at most a
+  //   fifth of the device;
+  // * the stream UpperCsr (unbr, ud16, uvrow: 10 B per edge + tm1) otherwise
+  //   (or PACIM_UCSR=1/2/3; 0: the lists): the edge lists are then derived
+  //   only on first use (pc_ensure_edge_lists: compact store, edge-
+  //   partitioned and bucketed builds, HLA recording).
+  // On first use either way: the per-CSR-entry thresholds (pc_ensure_tcsr:
+  // traversal selections, compressed probes, Monte Carlo)
+  const char *ue = getenv("PACIM_UCSR");
+  const int ucsr = ue ? atoi(ue) : -1;
+  {
+    size_t fr = 0, tot = 0;
+    pc_mem_info(ctx, &fr, &tot);
+    ctx->ucsr = ucsr > 0 || (ucsr < 0 && 16 * m > tot / 5);
+  }
   const bool per_edge = ctx->pmodel != PACIM_P_CONST;
   if (per_edge) pc_ensure(ctx, ctx->tm1, std::max<size_t>(m, 1) * sizeof(uint32_t));
-  // the per-CSR-entry thresholds (tcsr) are derived on first use
-  // (pc_ensure_tcsr: traversal selections, compressed probes, Monte Carlo):
-  // the build reads the per-edge tm1 only
   ctx->tcsr_ok = false;
+  ctx->elist_ok = false;
+  if (ctx->ucsr) {
+    pc_free(ctx, ctx->keys);
+    pc_free(ctx, ctx->ckeys);
+    pc_ensure(ctx, ctx->rk, ((size_t)n / 32 + 1) * sizeof(uint2));
+    k_rank_map<<<pc_grid(ctx, (size_t)n + 31, 256), 256, 0, ctx->stream>>>(
+        off, ctx->cid.as<uint32_t>(), n, ctx->rk.as<uint2>());
+    PC_CHECK_LAUNCH();
+    pc_ensure(ctx, ctx->ucrow, ((m + 31) / 32 + 1) * 4);
+    if (m) {
+      k_crow_of<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(uoff, n, ctx->ucrow.as<uint32_t>());
+      PC_CHECK_LAUNCH();
+    }
+    ctx->launches += 2;
+  } else {
+    for (DevBuf *d : {&ctx->rk, &ctx->ucrow, &ctx->unbr, &ctx->ud16, &ctx->uvrow, &ctx->ucrowr})
+      pc_free(ctx, *d);
+    pc_ensure(ctx, ctx->keys, std::max<size_t>(m, 1) * 8);
+    pc_ensure(ctx, ctx->ckeys, std::max<size_t>(m, 1) * 8);
+  }
   if (nnz) {
     make_crow(ctx, ctx->crow);  // capacity kept across loads (no cudaMalloc per load)
     pc_ensure(ctx, ctx->vinfo, (size_t)n * 8);
@@ -416,14 +493,55 @@ static void derive_edges(pacim_ctx *ctx) {
                                                           ctx->hidx.as<uint32_t>(), n,
                                                           ctx->vinfo.as<uint64_t>());
     PC_CHECK_LAUNCH();
-    k_edge_derive<<<pc_grid(ctx, nnz, 256), 256, 0, ctx->stream>>>(
-        off, nbr, ctx->crow.as<uint32_t>(), nnz, ustart, ucnt, ctx->vinfo.as<uint64_t>(),
-        ctx->pmodel, ctx->t32, ctx->toff(), ctx->keys.as<uint64_t>(), ctx->ckeys.as<uint64_t>(),
-        per_edge ? ctx->tm1.as<uint32_t>() : nullptr, nullptr);
+    if (ctx->ucsr) {
+      pc_ensure(ctx, ctx->unbr, m * 4);
+      pc_ensure(ctx, ctx->ud16, m * 2);
+      pc_ensure(ctx, ctx->ucrowr, ((m + 31) / 32 + 1) * 4);
+      k_chunk_rows<<<pc_grid(ctx, (m + 31) / 32, 256), 256, 0, ctx->stream>>>(
+          ctx->ucrow.as<uint32_t>(), ctx->cid.as<uint32_t>(), (m + 31) / 32,
+          ctx->ucrowr.as<uint32_t>());
+      PC_CHECK_LAUNCH();
+      // the neighbours' store rows as a stream (a rank-map lookup per edge is
+      // a dependent L2 gather in k_edges' front end; PACIM_UCSR=2: the rank
+      // map; 3, tests: every delta capped — the offsets search and the rank
+      // map for every edge)
+      const bool vrow = ucsr != 2 && ucsr != 3;
+      if (vrow) pc_ensure(ctx, ctx->uvrow, m * 4);
+      else pc_free(ctx, ctx->uvrow);
+      k_edge_derive<<<pc_grid(ctx, nnz, 256), 256, 0, ctx->stream>>>(
+          off, nbr, ctx->crow.as<uint32_t>(), nnz, uoff, ctx->vinfo.as<uint64_t>(), ctx->pmodel,
+          ctx->t32, ctx->toff(), nullptr, nullptr, per_edge ? ctx->tm1.as<uint32_t>() : nullptr,
+          nullptr, ctx->unbr.as<uint32_t>(), ctx->ud16.as<uint16_t>(), ctx->ucrow.as<uint32_t>(),
+          vrow ? ctx->uvrow.as<uint32_t>() : nullptr, ctx->ucrowr.as<uint32_t>(), ucsr == 3);
+    } else {
+      k_edge_derive<<<pc_grid(ctx, nnz, 256), 256, 0, ctx->stream>>>(
+          off, nbr, ctx->crow.as<uint32_t>(), nnz, uoff, ctx->vinfo.as<uint64_t>(), ctx->pmodel,
+          ctx->t32, ctx->toff(), ctx->keys.as<uint64_t>(), ctx->ckeys.as<uint64_t>(),
+          per_edge ? ctx->tm1.as<uint32_t>() : nullptr, nullptr);
+      ctx->elist_ok = true;
+    }
     PC_CHECK_LAUNCH();
+  } else {
+    ctx->elist_ok = !ctx->ucsr;
   }
-  ctx->launches += 4;
+  ctx->launches += 6;
   PC_CUDA(cudaStreamSynchronize(ctx->stream));
+}
+
+void pc_ensure_edge_lists(pacim_ctx *ctx) {
+  if (ctx->lean || ctx->elist_ok) return;
+  const uint64_t m = ctx->m, nnz = 2 * m;
+  pc_ensure(ctx, ctx->keys, std::max<size_t>(m, 1) * 8);
+  pc_ensure(ctx, ctx->ckeys, std::max<size_t>(m, 1) * 8);
+  if (nnz) {
+    k_edge_derive<<<pc_grid(ctx, nnz, 256), 256, 0, ctx->stream>>>(
+        ctx->off.as<uint64_t>(), ctx->nbr.as<uint32_t>(), ctx->crow.as<uint32_t>(), nnz,
+        ctx->uoff.as<uint64_t>(), ctx->vinfo.as<uint64_t>(), ctx->pmodel, ctx->t32, ctx->toff(),
+        ctx->keys.as<uint64_t>(), ctx->ckeys.as<uint64_t>(), nullptr, nullptr);
+    PC_CHECK_LAUNCH();
+    ctx->launches++;
+  }
+  ctx->elist_ok = true;
 }
 
 namespace {
@@ -492,6 +610,7 @@ static void derive_lean(pacim_ctx *ctx) {
     if (ctx->hub >= n) ctx->hub = 0;
   }
   ctx->nr = n;
+  ctx->ucsr = false;
   ctx->hub_row = ctx->hub;
   pc_ensure(ctx, ctx->cid, (size_t)n * 4);
   pc_ensure(ctx, ctx->rmap, (size_t)n * 4);

@@ -205,6 +205,13 @@ struct pacim_ctx {
   DevBuf tcsr;           // u32[2m]  per-edge models: T32 - toff() per CSR entry (traversals)
   DevBuf ckeys;          // u64[m]   the same edges as store rows: row(min)<<32|row(max);
                          //          bit 31 of a half flags a hub row (PACIM_HUBF)
+  DevBuf uoff;           // u64[n+1] exclusive prefix of the upper degrees (UpperCsr)
+  DevBuf ucrow;          // u32      row of every 32nd upper edge (UpperCsr)
+  DevBuf rk;             // uint2[n/32+1] rank map vertex -> store row (UpperCsr)
+  DevBuf unbr;           // u32[m]   upper neighbours in upper-edge order (UpperCsr)
+  DevBuf ud16;           // u16[m]   vertex / row deltas of upper edge e from chunk e >> 5
+  DevBuf ucrowr;         // u32      store row of ucrow[c]
+  DevBuf uvrow;          // u32[m]   store row of unbr[e] (PACIM_UCSR=2: from the rank map)
   DevBuf cid;            // u32[n]   store row of v, or 0xFFFFFFFF for isolated v
   DevBuf rmap;           // u32[nr]  vertex id of store row c
   uint32_t nr = 0;       // store rows = non-isolated vertices (order kept)
@@ -266,7 +273,9 @@ struct pacim_ctx {
   // hook list of epoch builds (k_edges -> k_compress_count<…, LIST>): capacity
   // from the non-root count of the last dense build of graph_gen (hk_gen)
   DevBuf sym[11];       // scratch of the upper-CSR symmetrization (graph.cu), kept across loads
-  bool tcsr_ok = false;  // tcsr derived for the current graph (pc_ensure_tcsr)
+  bool tcsr_ok = false;
+  bool elist_ok = false;
+  bool ucsr = false;      // the build streams the upper edges (UpperCsr), derive_edges  // keys / ckeys derived for the current graph (pc_ensure_edge_lists)  // tcsr derived for the current graph (pc_ensure_tcsr)
   DevBuf hk_list;
   uint64_t hk_hint = 0, hk_gen = ~0ull, hk_cap = 0;
   uint32_t hk_B = 0;
@@ -491,6 +500,47 @@ struct EdgeSet {
   const uint64_t *keys = nullptr, *ckeys = nullptr;
   uint64_t m = 0;
 };
+// The upper edges as a compact stream (k_edges LEAN = 2, the dense store's
+// one-window builds): upper edge e = (u, unbr[e]) with u = ucrow[c] + (ud16[e]
+// & 255) and row(u) = ucrowr[c] + (ud16[e] >> 8), c = e >> 5 (ucrow[c] = the
+// vertex of upper edge 32 c, ucrowr[c] its store row; a byte of 255: that
+// far or more, the vertex then by the offsets walk from ucrow[c], the row by
+// the rank map
+// rk[u >> 5] = {row of the word's first non-isolated vertex, bitmap of its
+// non-isolated vertices}: rk.x + popc(rk.y & below(u))); the neighbour's
+// store row uvrow[e] (or, PACIM_UCSR=2, the rank map).  10 B per edge (+ 4 B
+// tm1) instead of keys + ckeys' 16, and no load depends on another: a
+// dependent rank-map gather in k_edges' front end cost 22.8 -> 31.5 ms at c4.
+struct UpperCsr {
+  uint32_t nv = 0;  // vertices
+  const uint64_t *uoff = nullptr;
+  const uint32_t *unbr = nullptr, *ucrow = nullptr, *uvrow = nullptr, *ucrowr = nullptr;
+  const uint16_t *ud16 = nullptr;
+  const uint2 *rk = nullptr;
+};
+// The row u in [lo, hi] of entry e of a CSR-like offsets array: off[lo] <=
+// e, hi >= the row.  A few linear steps, then a binary search for the
+// largest u with off[u] <= e (a linear walk over a run of empty rows — the
+// top of an R-MAT id range has thousands of vertices without upper edges —
+// kept one SM busy 24M cycles after the rest finished: c4 k_edges 22.8 ->
+// 36 ms)
+__device__ __forceinline__ uint32_t pc_row_of(const uint64_t *off, uint32_t lo, uint32_t hi,
+                                              uint64_t e) {
+#pragma unroll 1
+  for (int i = 0; i < 4; i++) {
+    if (e < off[lo + 1]) return lo;
+    lo++;
+  }
+  while (lo < hi) {
+    const uint32_t mid = lo + ((hi - lo + 1) >> 1);
+    if (off[mid] <= e) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+// keys / ckeys of the current graph (derived on first use: the compact
+// store, the edge-partitioned and bucketed builds, HLA recording)
+void pc_ensure_edge_lists(pacim_ctx *ctx);
 // HLA recording around the sketch passes of a build: begin sizes the raw
 // buffer from the expected live hub entries E (false: not recorded — no hubs,
 // a lean graph, E > max_per_edge * m, or it does not fit in a slice of the

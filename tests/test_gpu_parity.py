@@ -121,6 +121,39 @@ def test_tiny_corpus_parity_dense_store(orc, ctx, i, monkeypatch):
     assert ctx.pacim_get_stats()["store"] == 0
 
 
+def gapped_graph(nv, m, gap, seed):
+    """random_graph's edges on the ids v * gap + v % 5 of a graph with
+    nv * gap vertices: runs of isolated vertices longer than 255, so the
+    edge stream's vertex and row deltas overflow their bytes."""
+    off, nbr = inputs.random_graph(nv, m, seed)
+    e = [(u * gap + u % 5, int(v) * gap + int(v) % 5)
+         for u in range(nv) for v in nbr[int(off[u]):int(off[u + 1])] if v > u]
+    return inputs.csr_from_edges(nv * gap, e)
+
+
+@pytest.mark.parametrize("ucsr", ["1", "0", "2", "3"])
+@pytest.mark.parametrize("i", [0, 2, 3, 7, 10, 12, -1])
+def test_dense_store_edge_streams(orc, ctx, i, ucsr, monkeypatch):
+    """The dense store's upper-edge stream (UpperCsr: neighbours, row deltas
+    and the neighbours' rows per edge; 1, the default when the edge lists
+    would take more than a fifth of the device), the edge lists
+    keys / ckeys (0), the neighbours' rows from the rank map (2), every delta
+    capped so the offsets walk and the rank map serve every edge (3): the
+    same oracle parity (labels, gain0, seeds, gains).  i = -1: a graph whose
+    runs of isolated vertices exceed a byte (deltas overflow naturally)."""
+    monkeypatch.setenv("PACIM_STORE", "dense")
+    monkeypatch.setenv("PACIM_UCSR", ucsr)
+    if i < 0:
+        from oracle.oracle import Graph
+        off, nbr = gapped_graph(300, 2400, 301, 17)
+        g = Graph(len(off) - 1, off, nbr)
+        model, t32 = model_of(orc, 0.2)
+        full_parity(orc, ctx, g, model, t32, 48, 777, 10)
+    else:
+        test_tiny_corpus_parity(orc, ctx, i)
+    assert ctx.pacim_get_stats()["store"] == 0
+
+
 @pytest.mark.parametrize("hl", ["1", "0", "40"])
 @pytest.mark.parametrize("bits", ["1", "2", "6"])
 @pytest.mark.parametrize("i", [0, 3, 7, 9, 10, 12])
