@@ -396,7 +396,9 @@ def main():
     # (graphs whose two staged copies do not fit beside the resident one — c5
     # — take the unpipelined loop)
     _sync = bool(os.environ.get("PACIM_E2E_SYNC"))  # debugging: the unpipelined loop
-    src = "symmetric CSR" if _full else "upper CSR (symmetrized on the device)"
+    src = ("symmetric CSR" if _full else
+           "upper CSR (symmetric offsets from the degrees; the symmetric lists are built "
+           "on the device only when read, never on this path)")
     e2e_mode = (f"{load_async.__name__} from the pinned host {src}, two loads in flight: "
                 "the next steps' H2D copies overlap this step's build and selection")
     if not _sync:

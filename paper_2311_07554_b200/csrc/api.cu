@@ -161,6 +161,8 @@ void pc_graph_loaded(pacim_ctx *ctx) {
 static void drop_graph(pacim_ctx *ctx) {
   drop_sketches(ctx);
   ctx->has_graph = false;
+  ctx->upper_src = false;  // (an upper load sets both again)
+  ctx->sym_pending = false;
 }
 
 static void free_all(pacim_ctx *ctx) {
@@ -323,8 +325,13 @@ static void commit_staged(pacim_ctx *ctx) {
   ctx->pmodel = st.pmodel;
   ctx->t32 = st.t32;
   PC_CUDA(cudaStreamWaitEvent(ctx->stream, st.done, 0));
-  if (st.upper) {  // the symmetric CSR built on the device from the upper one
-    pc_symmetrize_upper(ctx, st.off.as<uint64_t>(), st.nbr.as<uint32_t>(), st.n, st.nnz / 2);
+  if (st.upper) {
+    // the upper CSR becomes the graph's (the old uoff / unbr buffers are the
+    // slot's next staging area); the symmetric offsets from the degrees, the
+    // symmetric lists only when something reads them (pc_ensure_sym)
+    std::swap(ctx->uoff, st.off);
+    std::swap(ctx->unbr, st.nbr);
+    pc_upper_degrees(ctx);
   } else {
     std::swap(ctx->off, st.off);  // the staged CSR becomes the graph; the old
     std::swap(ctx->nbr, st.nbr);  // buffers are the slot's next staging area
@@ -428,16 +435,15 @@ int pacim_load_graph_upper(pacim_ctx *ctx, uint32_t n, uint64_t m, const uint64_
     drop_staged(ctx);
     ctx->mi_valid = false;  // free device memory queried afresh (pc_mem_info)
     load_common(ctx, n, 2 * m, pmodel, t32);
-    TmpBuf uo(ctx), un(ctx);
-    pc_ensure(ctx, uo, ((size_t)n + 1) * 8);
-    pc_ensure(ctx, un, std::max<uint64_t>(m, 1) * 4);
-    PC_CUDA(cudaMemcpyAsync(uo.p, uoffsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice,
+    pc_free(ctx, ctx->nbr);  // built on first use (pc_ensure_sym)
+    pc_ensure(ctx, ctx->uoff, ((size_t)n + 1) * 8);
+    pc_ensure(ctx, ctx->unbr, std::max<uint64_t>(m, 1) * 4);
+    PC_CUDA(cudaMemcpyAsync(ctx->uoff.p, uoffsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice,
                             ctx->stream));
     if (m)
-      PC_CUDA(cudaMemcpyAsync(un.p, uneighbors, m * 4, cudaMemcpyHostToDevice, ctx->stream));
-    if (validate) pc_validate_upper(ctx, uo.as<uint64_t>(), un.as<uint32_t>(), n);
-    pc_symmetrize_upper(ctx, uo.as<uint64_t>(), un.as<uint32_t>(), n, m);
-    PC_CUDA(cudaStreamSynchronize(ctx->stream));  // the temporaries are released next
+      PC_CUDA(cudaMemcpyAsync(ctx->unbr.p, uneighbors, m * 4, cudaMemcpyHostToDevice, ctx->stream));
+    if (validate) pc_validate_upper(ctx, ctx->uoff.as<uint64_t>(), ctx->unbr.as<uint32_t>(), n);
+    pc_upper_degrees(ctx);
     pc_graph_finish_load(ctx, 0);
     ctx->has_graph = true;
     pc_graph_loaded(ctx);
@@ -497,6 +503,7 @@ int pacim_graph_info(pacim_ctx *ctx, uint32_t *n, uint64_t *m) {
 int pacim_get_graph(pacim_ctx *ctx, uint64_t *offsets_out, uint32_t *neighbors_out) {
   return guarded(ctx, [&] {
     PC_REQUIRE(ctx->has_graph, PACIM_ESTATE, "no graph loaded");
+    if (neighbors_out) pc_ensure_sym(ctx);
     if (offsets_out)
       PC_CUDA(cudaMemcpyAsync(offsets_out, ctx->off.p, ((size_t)ctx->n + 1) * 8,
                               cudaMemcpyDeviceToHost, ctx->stream));

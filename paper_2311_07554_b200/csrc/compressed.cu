@@ -750,6 +750,7 @@ void pc_cover_compressed(pacim_ctx *ctx, uint32_t s, int64_t *target, int64_t *l
   unsigned long long *sum = reinterpret_cast<unsigned long long *>(dl + B + (B & 1));
   PC_CUDA(cudaMemsetAsync(sum, 0, 5 * 8, ctx->stream));
   ProbeParams P;
+  pc_ensure_tcsr(ctx);  // (and the symmetric lists of an upper-loaded graph)
   P.off = ctx->off.as<uint64_t>();
   P.nbr = ctx->nbr.as<uint32_t>();
   P.K = ctx->K;

@@ -254,6 +254,59 @@ __global__ void k_edge_derive(const uint64_t *off, const uint32_t *nbr, const ui
   }
 }
 
+// k_edge_derive for a graph held as an upper CSR (uoff, unbr; lane per upper
+// edge e, its row by the chunk table ucrow and pc_row_of): the edge lists
+// (keys, ckeys) or the stream's deltas and neighbour rows (ud16, uvrow), and
+// tm1 for the per-edge models
+__global__ void k_edge_derive_up(const uint64_t *uoff, const uint32_t *unbr, const uint32_t *ucrow,
+                                 uint64_t m, uint32_t n, const uint64_t *vinfo, int pmodel,
+                                 uint64_t t32, uint32_t toff, uint64_t *keys, uint64_t *ckeys,
+                                 uint32_t *tm1, uint16_t *ud16, uint32_t *uvrow,
+                                 const uint32_t *ucrowr, bool cap_all) {
+  const uint64_t nch = (m + 31) / 32;
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (size_t)gridDim.x * blockDim.x) {
+    const uint64_t c = e >> 5;
+    const uint32_t u0 = ucrow[c];
+    const uint32_t u = pc_row_of(uoff, u0, c + 1 < nch ? ucrow[c + 1] : n - 1, e);
+    const uint32_t w = unbr[e];
+    const uint64_t iu = vinfo[u], iw = vinfo[w];
+    if (keys) {
+      keys[e] = ((uint64_t)u << 32) | w;
+      ckeys[e] = ((iu & 0xFFFFFFFFull) << 32) | (iw & 0xFFFFFFFFull);
+    }
+    if (ud16) {
+      const uint32_t du = min(255u, u - u0),
+                     dr = min(255u, ((uint32_t)iu & ~PACIM_HUBF) - ucrowr[c]);
+      ud16[e] = cap_all ? (uint16_t)0xFFFF : (uint16_t)(du | dr << 8);
+      if (uvrow) uvrow[e] = (uint32_t)iw & ~PACIM_HUBF;
+    }
+    if (tm1 && pmodel != PACIM_P_CONST) {
+      uint64_t T;
+      if (pmodel == PACIM_P_WIC) {
+        T = (1ull << 33) / ((iu >> 32) + (iw >> 32));
+        if (T > (1ull << 32)) T = 1ull << 32;
+      } else {
+        T = pc_t32_uniform(t32, ((uint64_t)u << 32) | w);
+      }
+      tm1[e] = (uint32_t)(T - toff);
+    }
+  }
+}
+
+// lower degrees of an upper CSR: lcnt[v] = #{upper edges (u, v)}
+__global__ void k_lower_hist(const uint32_t *unbr, uint64_t m, uint32_t *lcnt) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < m;
+       e += (size_t)gridDim.x * blockDim.x)
+    atomicAdd(lcnt + unbr[e], 1u);
+}
+// deg[v] = upper + lower degree (deg[n] = 0, for the exclusive scan)
+__global__ void k_up_deg(const uint64_t *uoff, const uint32_t *lcnt, uint32_t n, uint64_t *deg) {
+  for (size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x; v <= n;
+       v += (size_t)gridDim.x * blockDim.x)
+    deg[v] = v < n ? uoff[v + 1] - uoff[v] + lcnt[v] : 0;
+}
+
 // store row of every chunk's first upper-edge vertex (UpperCsr)
 __global__ void k_chunk_rows(const uint32_t *ucrow, const uint32_t *cid, uint64_t nch,
                              uint32_t *ucrowr) {
@@ -437,14 +490,17 @@ static void derive_edges(pacim_ctx *ctx) {
   const uint64_t m = ctx->m, nnz = 2 * m;
   uint64_t *off = ctx->off.as<uint64_t>();
   const uint32_t *nbr = ctx->nbr.as<uint32_t>();
-  pc_ensure(ctx, ctx->scratch, ((size_t)n + 1) * sizeof(uint64_t));
-  uint64_t *ucnt = ctx->scratch.as<uint64_t>();
-  pc_ensure(ctx, ctx->uoff, ((size_t)n + 1) * sizeof(uint64_t));
+  const bool up = ctx->upper_src;  // uoff / unbr / ucrow hold the upper CSR
+  if (!up) {
+    pc_ensure(ctx, ctx->scratch, ((size_t)n + 1) * sizeof(uint64_t));
+    uint64_t *ucnt = ctx->scratch.as<uint64_t>();
+    pc_ensure(ctx, ctx->uoff, ((size_t)n + 1) * sizeof(uint64_t));
+    k_upper_count<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(off, nbr, n, ucnt);
+    PC_CHECK_LAUNCH();
+    PC_CUDA(cudaMemsetAsync(ucnt + n, 0, 8, ctx->stream));
+    pc_exclusive_scan_u64(ctx, ucnt, ctx->uoff.as<uint64_t>(), (size_t)n + 1);
+  }
   uint64_t *uoff = ctx->uoff.as<uint64_t>();
-  k_upper_count<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(off, nbr, n, ucnt);
-  PC_CHECK_LAUNCH();
-  PC_CUDA(cudaMemsetAsync(ucnt + n, 0, 8, ctx->stream));
-  pc_exclusive_scan_u64(ctx, ucnt, uoff, (size_t)n + 1);
   // Two forms of the upper edges for the build's edge pass (k_edges):
   // * the edge lists keys / ckeys (16 B per upper edge, 25 GB at c4; + tm1):
   //   fastest (k_edges is issue bound: the stream's decode adds ~11 % warp
@@ -474,15 +530,18 @@ static void derive_edges(pacim_ctx *ctx) {
     k_rank_map<<<pc_grid(ctx, (size_t)n + 31, 256), 256, 0, ctx->stream>>>(
         off, ctx->cid.as<uint32_t>(), n, ctx->rk.as<uint2>());
     PC_CHECK_LAUNCH();
-    pc_ensure(ctx, ctx->ucrow, ((m + 31) / 32 + 1) * 4);
-    if (m) {
-      k_crow_of<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(uoff, n, ctx->ucrow.as<uint32_t>());
-      PC_CHECK_LAUNCH();
+    if (!up) {
+      pc_ensure(ctx, ctx->ucrow, ((m + 31) / 32 + 1) * 4);
+      if (m) {
+        k_crow_of<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(uoff, n, ctx->ucrow.as<uint32_t>());
+        PC_CHECK_LAUNCH();
+      }
     }
     ctx->launches += 2;
   } else {
-    for (DevBuf *d : {&ctx->rk, &ctx->ucrow, &ctx->unbr, &ctx->ud16, &ctx->uvrow, &ctx->ucrowr})
-      pc_free(ctx, *d);
+    for (DevBuf *d : {&ctx->rk, &ctx->ud16, &ctx->uvrow, &ctx->ucrowr}) pc_free(ctx, *d);
+    if (!up)
+      for (DevBuf *d : {&ctx->ucrow, &ctx->unbr}) pc_free(ctx, *d);
     pc_ensure(ctx, ctx->keys, std::max<size_t>(m, 1) * 8);
     pc_ensure(ctx, ctx->ckeys, std::max<size_t>(m, 1) * 8);
   }
@@ -493,7 +552,27 @@ static void derive_edges(pacim_ctx *ctx) {
                                                           ctx->hidx.as<uint32_t>(), n,
                                                           ctx->vinfo.as<uint64_t>());
     PC_CHECK_LAUNCH();
-    if (ctx->ucsr) {
+    if (up) {  // lane per upper edge of the upper CSR
+      const bool vrow = ucsr != 2 && ucsr != 3;
+      if (ctx->ucsr) {
+        pc_ensure(ctx, ctx->ud16, m * 2);
+        pc_ensure(ctx, ctx->ucrowr, ((m + 31) / 32 + 1) * 4);
+        k_chunk_rows<<<pc_grid(ctx, (m + 31) / 32, 256), 256, 0, ctx->stream>>>(
+            ctx->ucrow.as<uint32_t>(), ctx->cid.as<uint32_t>(), (m + 31) / 32,
+            ctx->ucrowr.as<uint32_t>());
+        PC_CHECK_LAUNCH();
+        if (vrow) pc_ensure(ctx, ctx->uvrow, m * 4);
+        else pc_free(ctx, ctx->uvrow);
+      }
+      k_edge_derive_up<<<pc_grid(ctx, m, 256, 16), 256, 0, ctx->stream>>>(
+          uoff, ctx->unbr.as<uint32_t>(), ctx->ucrow.as<uint32_t>(), m, n, ctx->vinfo.as<uint64_t>(),
+          ctx->pmodel, ctx->t32, ctx->toff(), ctx->ucsr ? nullptr : ctx->keys.as<uint64_t>(),
+          ctx->ucsr ? nullptr : ctx->ckeys.as<uint64_t>(), per_edge ? ctx->tm1.as<uint32_t>() : nullptr,
+          ctx->ucsr ? ctx->ud16.as<uint16_t>() : nullptr,
+          (ctx->ucsr && vrow) ? ctx->uvrow.as<uint32_t>() : nullptr, ctx->ucrowr.as<uint32_t>(),
+          ucsr == 3);
+      ctx->elist_ok = !ctx->ucsr;
+    } else if (ctx->ucsr) {
       pc_ensure(ctx, ctx->unbr, m * 4);
       pc_ensure(ctx, ctx->ud16, m * 2);
       pc_ensure(ctx, ctx->ucrowr, ((m + 31) / 32 + 1) * 4);
@@ -533,7 +612,14 @@ void pc_ensure_edge_lists(pacim_ctx *ctx) {
   const uint64_t m = ctx->m, nnz = 2 * m;
   pc_ensure(ctx, ctx->keys, std::max<size_t>(m, 1) * 8);
   pc_ensure(ctx, ctx->ckeys, std::max<size_t>(m, 1) * 8);
-  if (nnz) {
+  if (ctx->upper_src && m) {
+    k_edge_derive_up<<<pc_grid(ctx, m, 256, 16), 256, 0, ctx->stream>>>(
+        ctx->uoff.as<uint64_t>(), ctx->unbr.as<uint32_t>(), ctx->ucrow.as<uint32_t>(), m, ctx->n,
+        ctx->vinfo.as<uint64_t>(), ctx->pmodel, ctx->t32, ctx->toff(), ctx->keys.as<uint64_t>(),
+        ctx->ckeys.as<uint64_t>(), nullptr, nullptr, nullptr, nullptr, false);
+    PC_CHECK_LAUNCH();
+    ctx->launches++;
+  } else if (nnz) {
     k_edge_derive<<<pc_grid(ctx, nnz, 256), 256, 0, ctx->stream>>>(
         ctx->off.as<uint64_t>(), ctx->nbr.as<uint32_t>(), ctx->crow.as<uint32_t>(), nnz,
         ctx->uoff.as<uint64_t>(), ctx->vinfo.as<uint64_t>(), ctx->pmodel, ctx->t32, ctx->toff(),
@@ -567,6 +653,7 @@ __global__ void k_tcsr(const uint64_t *off, const uint32_t *nbr, const uint32_t 
 }  // namespace
 
 void pc_ensure_tcsr(pacim_ctx *ctx) {
+  pc_ensure_sym(ctx);  // every reader of tcsr reads the neighbour lists too
   if (ctx->pmodel == PACIM_P_CONST || ctx->tcsr_ok) return;
   const uint64_t nnz = 2 * ctx->m;
   pc_ensure(ctx, ctx->tcsr, std::max<size_t>(nnz, 1) * sizeof(uint32_t));
@@ -592,6 +679,7 @@ static void derive_common(pacim_ctx *ctx) {
 // singleton rows), k_edges reads the upper edges straight from the CSR
 // through the chunk -> row table `crow`.  Constant probabilities only.
 static void derive_lean(pacim_ctx *ctx) {
+  pc_ensure_sym(ctx);  // k_edges reads the symmetric CSR
   const uint32_t n = ctx->n;
   uint64_t *off = ctx->off.as<uint64_t>();
   PC_REQUIRE(ctx->pmodel == PACIM_P_CONST, PACIM_ENOTIMPL,
@@ -848,6 +936,39 @@ void pc_symmetrize_upper(pacim_ctx *ctx, const uint64_t *d_uoff, const uint32_t 
     fprintf(stderr, "  (pairs, sort, runs+degrees+scans, rows)\n");
     for (auto e : evs) cudaEventDestroy(e);
   }
+}
+
+void pc_upper_degrees(pacim_ctx *ctx) {
+  const uint32_t n = ctx->n;
+  const uint64_t m = ctx->m;
+  DevBuf *sb = ctx->sym;  // the symmetrization's scratch (kept across upper loads)
+  DevBuf &deg = sb[2], &lcnt = sb[3];
+  pc_ensure(ctx, deg, ((size_t)n + 1) * 8);
+  pc_ensure(ctx, lcnt, ((size_t)n + 1) * 8);
+  pc_ensure(ctx, ctx->off, ((size_t)n + 1) * 8);
+  PC_CUDA(cudaMemsetAsync(lcnt.p, 0, (size_t)n * 4, ctx->stream));
+  pc_ensure(ctx, ctx->ucrow, ((m + 31) / 32 + 1) * 4);
+  if (m) {
+    k_crow_of<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(ctx->uoff.as<uint64_t>(), n,
+                                                            ctx->ucrow.as<uint32_t>());
+    PC_CHECK_LAUNCH();
+    k_lower_hist<<<pc_grid(ctx, m, 256, 16), 256, 0, ctx->stream>>>(ctx->unbr.as<uint32_t>(), m,
+                                                                   lcnt.as<uint32_t>());
+    PC_CHECK_LAUNCH();
+  }
+  k_up_deg<<<pc_grid(ctx, (size_t)n + 1, 256), 256, 0, ctx->stream>>>(
+      ctx->uoff.as<uint64_t>(), lcnt.as<uint32_t>(), n, deg.as<uint64_t>());
+  PC_CHECK_LAUNCH();
+  pc_exclusive_scan_u64(ctx, deg.as<uint64_t>(), ctx->off.as<uint64_t>(), (size_t)n + 1);
+  ctx->launches += 4;
+  ctx->upper_src = true;
+  ctx->sym_pending = true;
+}
+
+void pc_ensure_sym(pacim_ctx *ctx) {
+  if (!ctx->sym_pending) return;
+  pc_symmetrize_upper(ctx, ctx->uoff.as<uint64_t>(), ctx->unbr.as<uint32_t>(), ctx->n, ctx->m);
+  ctx->sym_pending = false;
 }
 
 // ------------------------------------------------------------- generators

@@ -133,6 +133,7 @@ void pc_simulate_ic(pacim_ctx *ctx, const uint32_t *seeds_host, uint32_t ns, uin
   pc_ensure(ctx, buf, words * 4);
   uint32_t *base = buf.as<uint32_t>();
   Mc M;
+  pc_ensure_tcsr(ctx);  // (and the symmetric lists of an upper-loaded graph)
   M.off = ctx->off.as<uint64_t>();
   M.nbr = ctx->nbr.as<uint32_t>();
   M.per_edge = ctx->pmodel != PACIM_P_CONST;

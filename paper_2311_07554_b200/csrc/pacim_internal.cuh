@@ -275,7 +275,15 @@ struct pacim_ctx {
   DevBuf sym[11];       // scratch of the upper-CSR symmetrization (graph.cu), kept across loads
   bool tcsr_ok = false;
   bool elist_ok = false;
-  bool ucsr = false;      // the build streams the upper edges (UpperCsr), derive_edges  // keys / ckeys derived for the current graph (pc_ensure_edge_lists)  // tcsr derived for the current graph (pc_ensure_tcsr)
+  bool ucsr = false;      // the build streams the upper edges (UpperCsr), derive_edges
+  // graphs loaded as an upper CSR (pacim_load_graph_upper[_async]): the upper
+  // CSR stays in uoff / unbr, off holds the symmetric offsets (from the
+  // degrees), and the symmetric neighbour lists nbr are built only when
+  // something reads them (pc_ensure_sym: traversal selections, compressed
+  // probes, Monte Carlo, lean builds, pacim_get_graph) — the dense store's
+  // build and its Win-Tree selection read the upper edges only
+  bool upper_src = false;
+  bool sym_pending = false;  // keys / ckeys derived for the current graph (pc_ensure_edge_lists)  // tcsr derived for the current graph (pc_ensure_tcsr)
   DevBuf hk_list;
   uint64_t hk_hint = 0, hk_gen = ~0ull, hk_cap = 0;
   uint32_t hk_B = 0;
@@ -538,6 +546,11 @@ __device__ __forceinline__ uint32_t pc_row_of(const uint64_t *off, uint32_t lo, 
   }
   return lo;
 }
+// the symmetric neighbour lists of an upper-loaded graph (no-op otherwise)
+void pc_ensure_sym(pacim_ctx *ctx);
+// an upper CSR in uoff / unbr (n, m set): the symmetric offsets off from the
+// degrees (lower degrees by a histogram of the targets), ucrow; nbr pending
+void pc_upper_degrees(pacim_ctx *ctx);
 // keys / ckeys of the current graph (derived on first use: the compact
 // store, the edge-partitioned and bucketed builds, HLA recording)
 void pc_ensure_edge_lists(pacim_ctx *ctx);

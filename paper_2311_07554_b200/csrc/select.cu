@@ -1888,6 +1888,7 @@ void pc_select_lazy(pacim_ctx *ctx, uint32_t k, uint32_t *seeds, int64_t *gain_n
   }
   pc_ensure(ctx, ctx->gain, (size_t)n * 8);
   Sel S{};
+  if (!cs) pc_ensure_tcsr(ctx);  // the cover traversal reads the lists and thresholds
   if (!cs) S = make_sel(ctx, ctx->gain.as<long long>());
   cudaEvent_t e0, e1;
   PC_CUDA(cudaEventCreate(&e0));

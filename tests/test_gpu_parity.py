@@ -382,6 +382,50 @@ def test_upper_csr_load(orc, ctx, i, mode):
     assert np.array_equal(ctx.pacim_get_gain0(), eg0)
 
 
+@pytest.mark.parametrize("ucsr", ["0", "1"])
+@pytest.mark.parametrize("sel", [0, 1, 2])
+@pytest.mark.parametrize("i", [0, 3, 7, 10, 12])
+def test_upper_load_deferred_sym(orc, ctx, i, sel, ucsr, monkeypatch):
+    """An upper-loaded graph keeps the upper CSR and the symmetric offsets;
+    its symmetric neighbour lists are built only when something reads them
+    (pc_ensure_sym).  Without pacim_get_graph first: the build (edge lists or
+    the upper-edge stream) and every selector — incremental (cover
+    traversal: builds the lists), prefix doubling, Win-Tree — equal the
+    oracle; then a compressed build (probes: lists), Monte Carlo, and the
+    symmetric CSR read back."""
+    from oracle.oracle import Graph
+    monkeypatch.setenv("PACIM_STORE", "dense")
+    monkeypatch.setenv("PACIM_UCSR", ucsr)
+    build_fn, p, R, k = CASES[i]
+    off, nbr = build_fn()
+    g = Graph(len(off) - 1, off, nbr)
+    model, t32 = model_of(orc, p)
+    uo, un = upper_of(off, nbr)
+    if i % 2:
+        ctx.pacim_load_graph_upper(uo, un, model, t32, 1)
+    else:
+        ctx.pacim_load_graph_upper_async(uo, un, model, t32)
+    k = min(k, g.n)
+    seed = 2500 + i
+    ctx.pacim_set_selector(sel)
+    try:
+        ctx.pacim_build_sketches(R, seed)
+        s, gn, sg, _ = ctx.pacim_select_seeds(k)
+    finally:
+        ctx.pacim_set_selector(0)
+    es, egn, esg, eg0 = orc.greedy(g, model, t32, R, seed, k, want_gain0=True)
+    assert list(s) == list(es) and list(gn) == list(egn) and list(sg) == list(esg)
+    assert np.array_equal(ctx.pacim_get_gain0(), eg0)
+    if sel == 0:
+        ctx.pacim_build_sketches(R, seed, 1 << 30)  # alpha = 1/4: Get-center probes
+        s2, gn2, _, _ = ctx.pacim_select_seeds(k)
+        assert list(s2) == list(es) and list(gn2) == list(egn)
+        seeds = [0, g.n // 2]
+        assert ctx.pacim_simulate_ic(seeds, 5, 9) == orc.simulate_ic(g, model, t32, seeds, 5, 9)
+    o2, n2 = ctx.pacim_get_graph()
+    assert np.array_equal(o2, np.asarray(off, np.uint64)) and np.array_equal(n2, np.asarray(nbr, np.uint32))
+
+
 def test_upper_csr_load_edge_cases(orc, ctx, pc):
     """Upper loads: no edges, isolated vertices between and after the edges,
     a hub whose lower list spans many chunks, and invalid upper CSRs (an entry
