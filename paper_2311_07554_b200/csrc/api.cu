@@ -299,7 +299,8 @@ static void check_model(int pmodel, uint64_t t32) {
              "uniform model: L > H in t32 = H << 32 | L");
 }
 
-static void load_common(pacim_ctx *ctx, uint32_t n, uint64_t nnz, int pmodel, uint64_t t32) {
+static void load_common(pacim_ctx *ctx, uint32_t n, uint64_t nnz, int pmodel, uint64_t t32,
+                        bool want_nbr = true) {
   PC_REQUIRE(n >= 1, PACIM_EINVAL, "n must be >= 1");
   PC_REQUIRE(n < (1u << 31), PACIM_EINVAL, "n must be < 2^31 (R2 key packing)");
   PC_REQUIRE((nnz & 1) == 0, PACIM_EINVAL, "nnz must be even (symmetric CSR)");
@@ -310,7 +311,8 @@ static void load_common(pacim_ctx *ctx, uint32_t n, uint64_t nnz, int pmodel, ui
   ctx->pmodel = pmodel;
   ctx->t32 = t32;
   pc_ensure(ctx, ctx->off, ((size_t)n + 1) * 8);
-  pc_ensure(ctx, ctx->nbr, std::max<uint64_t>(nnz, 1) * 4);
+  if (want_nbr) pc_ensure(ctx, ctx->nbr, std::max<uint64_t>(nnz, 1) * 4);
+  else pc_free(ctx, ctx->nbr);  // an upper load: built on first use (pc_ensure_sym)
 }
 
 // commit the oldest pending asynchronous load (no-op without one)
@@ -331,6 +333,7 @@ static void commit_staged(pacim_ctx *ctx) {
     // symmetric lists only when something reads them (pc_ensure_sym)
     std::swap(ctx->uoff, st.off);
     std::swap(ctx->unbr, st.nbr);
+    pc_free(ctx, ctx->nbr);  // an earlier graph's lists
     pc_upper_degrees(ctx);
   } else {
     std::swap(ctx->off, st.off);  // the staged CSR becomes the graph; the old
@@ -434,8 +437,7 @@ int pacim_load_graph_upper(pacim_ctx *ctx, uint32_t n, uint64_t m, const uint64_
     PC_REQUIRE(uoffsets[n] == m, PACIM_EINVAL, "offsets[n] != m");
     drop_staged(ctx);
     ctx->mi_valid = false;  // free device memory queried afresh (pc_mem_info)
-    load_common(ctx, n, 2 * m, pmodel, t32);
-    pc_free(ctx, ctx->nbr);  // built on first use (pc_ensure_sym)
+    load_common(ctx, n, 2 * m, pmodel, t32, false);
     pc_ensure(ctx, ctx->uoff, ((size_t)n + 1) * 8);
     pc_ensure(ctx, ctx->unbr, std::max<uint64_t>(m, 1) * 4);
     PC_CUDA(cudaMemcpyAsync(ctx->uoff.p, uoffsets, ((size_t)n + 1) * 8, cudaMemcpyHostToDevice,
