@@ -251,6 +251,14 @@ __global__ void __launch_bounds__(EDGE_THREADS, PACIM_EDGE_BLOCKS) k_edges(const
         rv = b.x + __popc(b.y & ((1u << (v & 31)) - 1));
       }
       lrow = ((uint64_t)ru << 32) | rv;
+    } else if (LEAN == 3 && upper) {
+      // lean graphs, upper entries only: e = upper edge index, the row by
+      // the upper chunk table (tm1) and the upper offsets, the neighbour at
+      // the row's upper part of the symmetric CSR (rows are [lower ++ upper])
+      const uint64_t c = base >> 5;
+      const uint32_t u = pc_row_of(uc.uoff, tm1[c], c + 1 < niter ? tm1[c + 1] : uc.nv - 1, e);
+      const uint32_t v = reinterpret_cast<const uint32_t *>(ckeys)[keys[u + 1] - (uc.uoff[u + 1] - e)];
+      lkey = ((uint64_t)u << 32) | v;
     } else if (LEAN && upper) {
       const uint32_t u = pc_row_of(keys, tm1[base >> 5],
                                    (base >> 5) + 1 < niter ? tm1[(base >> 5) + 1] : uc.nv - 1, e);
@@ -1281,6 +1289,20 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
           pe ? ctx->toff() : ctx->t32, ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb,
           ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), nullptr, 0u, hk, ctx->ep,
           edge_work(ctx, ctx->m, g), uc);
+    } else if (ctx->lean && ctx->uoff.p && (!getenv("PACIM_LEAN_UPPER") || atoi(getenv("PACIM_LEAN_UPPER")) != 0)) {
+      // no edge list (c5): the upper entries of the CSR by the upper offsets
+      // (half the lanes of the full-CSR pass below, which drops the lower ones)
+      auto kern = ctx->hash_rule ? (ep_on ? k_edges<false, false, true, 3, 0, true> : k_edges<false, false, true, 3>) : (ep_on ? k_edges<false, false, false, 3, 0, true> : k_edges<false, false, false, 3>);
+      PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      UpperCsr ul;
+      ul.nv = ctx->n;
+      ul.uoff = ctx->uoff.as<uint64_t>();
+      const unsigned gl = pc_grid(ctx, (ctx->m + 31) / 32 * 32, EDGE_THREADS, PACIM_EDGE_BLOCKS);
+      kern<<<gl, EDGE_THREADS, smem, ctx->stream>>>(
+          ctx->off.as<uint64_t>(), reinterpret_cast<const uint64_t *>(ctx->nbr.p),
+          ctx->ucrow.as<uint32_t>(), ctx->m, ctx->K, ctx->t32, ctx->d_shr.as<uint32_t>(),
+          ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), nullptr, 0u, hk, ctx->ep,
+          edge_work(ctx, ctx->m, gl), ul);
     } else if (ctx->lean) {  // no edge list: the upper edges from the CSR (c5)
       auto kern = ctx->hash_rule ? (ep_on ? k_edges<false, false, true, true, 0, true> : k_edges<false, false, true, true>) : (ep_on ? k_edges<false, false, false, true, 0, true> : k_edges<false, false, false, true>);
       PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -560,7 +560,10 @@ static uint32_t choose_batch(pacim_ctx *ctx) {
   // parent arrays are scratch on top of it, so their budget follows the store
   // (twice its bytes, at least 4 GB) instead of taking the free memory —
   // peak memory then tracks alpha.  PACIM_BATCH_MEM overrides (bytes).
-  const size_t keep = (size_t)2 << 30;
+  // headroom: 2 GB + the selection's per-vertex arrays (gain i64[n], is_seed
+  // u8[n]) allocated after the build (c5 ran out by 268 MB once the lean
+  // graph's upper offsets took 3 GB more)
+  const size_t keep = ((size_t)2 << 30) + 9 * (size_t)ctx->n;
   const size_t avail = fr > keep ? fr - keep : fr / 2;
   const size_t store = 2 * (size_t)ctx->rho * B * 4;  // label + size per (center, slot)
   size_t budget = std::max<size_t>(2 * store, (size_t)4 << 30);

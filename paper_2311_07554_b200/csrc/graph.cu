@@ -706,6 +706,24 @@ static void derive_lean(pacim_ctx *ctx) {
   k_iota_u32<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(ctx->rmap.as<uint32_t>(), n);
   PC_CHECK_LAUNCH();
   make_crow(ctx, ctx->crow);
+  {
+    // the upper offsets and their chunk table: k_edges<…, 3> visits only the
+    // upper entries (half the lanes of a pass over the full CSR)
+    pc_ensure(ctx, ctx->scratch, ((size_t)n + 1) * 8);
+    uint64_t *ucnt = ctx->scratch.as<uint64_t>();
+    pc_ensure(ctx, ctx->uoff, ((size_t)n + 1) * 8);
+    k_upper_count<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(off, ctx->nbr.as<uint32_t>(), n,
+                                                               ucnt);
+    PC_CHECK_LAUNCH();
+    PC_CUDA(cudaMemsetAsync(ucnt + n, 0, 8, ctx->stream));
+    pc_exclusive_scan_u64(ctx, ucnt, ctx->uoff.as<uint64_t>(), (size_t)n + 1);
+    pc_ensure(ctx, ctx->ucrow, ((ctx->m + 31) / 32 + 1) * 4);
+    if (ctx->m) {
+      k_crow_of<<<pc_grid(ctx, n, 256), 256, 0, ctx->stream>>>(ctx->uoff.as<uint64_t>(), n,
+                                                              ctx->ucrow.as<uint32_t>());
+      PC_CHECK_LAUNCH();
+    }
+  }
   pc_free(ctx, ctx->keys);
   pc_free(ctx, ctx->ckeys);
   pc_free(ctx, ctx->hidx);

@@ -168,9 +168,11 @@ def test_c5_shape_scale16_lean_bucketed(orc, ctx, monkeypatch):
     assert ctx.pacim_get_stats()["rows"] == 1 << 16
 
 
+@pytest.mark.parametrize("upper", ["1", "0"])
 @pytest.mark.parametrize("i", [0, 1, 3, 9])
-def test_compressed_lean(orc, ctx, i, monkeypatch):
+def test_compressed_lean(orc, ctx, i, upper, monkeypatch):
     monkeypatch.setenv("PACIM_LEAN", "1")
+    monkeypatch.setenv("PACIM_LEAN_UPPER", upper)
     run_case(orc, ctx, i, check_sketches=True)
 
 

@@ -612,12 +612,24 @@ def test_bucketed_generator_matches_oracle(orc, ctx, name, over, buckets, monkey
     test_generator_matches_oracle(orc, ctx, name, over)
 
 
-@pytest.mark.parametrize("i", [0, 1, 2, 5, 6, 7, 8, 9])
-def test_lean_graph(orc, ctx, i, monkeypatch):
+@pytest.mark.parametrize("upper", ["1", "0"])
+@pytest.mark.parametrize("i", [0, 1, 2, 5, 6, 7, 8, 9, -1])
+def test_lean_graph(orc, ctx, i, upper, monkeypatch):
     """Lean graphs (no edge list, rows = vertex ids, k_edges over the CSR):
-    labels, gain0 and the greedy equal the oracle's (constant p)."""
+    labels, gain0 and the greedy equal the oracle's (constant p).  upper:
+    the pass visits the upper entries only (by the upper offsets, the
+    default) or every CSR entry, dropping the lower ones (0).  i = -1: runs
+    of isolated vertices longer than the row search's linear steps."""
     monkeypatch.setenv("PACIM_LEAN", "1")
-    test_tiny_corpus_parity(orc, ctx, i)
+    monkeypatch.setenv("PACIM_LEAN_UPPER", upper)
+    if i < 0:
+        from oracle.oracle import Graph
+        off, nbr = gapped_graph(300, 2400, 301, 18)
+        g = Graph(len(off) - 1, off, nbr)
+        model, t32 = model_of(orc, 0.2)
+        full_parity(orc, ctx, g, model, t32, 48, 778, 10)
+    else:
+        test_tiny_corpus_parity(orc, ctx, i)
     st = ctx.pacim_get_stats()
     assert st["rows"] == st["n"]
 
