@@ -372,11 +372,12 @@ def main():
     # pacim_load_graph_upper_async; the device builds the symmetric CSR), half
     # the bytes of the symmetric CSR; PACIM_E2E_FULL=1 sends the symmetric CSR
     # (pacim_load_graph_async) instead
-    # Lean graphs (c5: constant p, edge lists too large) send the symmetric
-    # CSR: their build and Get-center probes read it, and the device-side
-    # transpose of an upper CSR needs 16 B of scratch per edge (133 GB at c5)
+    # Lean graphs and compressed builds (c5) send the symmetric CSR: their
+    # build or Get-center probes read it, and the device-side transpose of an
+    # upper CSR needs 16 B of scratch per edge (133 GB at c5)
     off, nbr = ctx.pacim_get_graph()
-    _full = bool(os.environ.get("PACIM_E2E_FULL")) or bool(st.get("lean"))
+    _full = (bool(os.environ.get("PACIM_E2E_FULL")) or bool(st.get("lean"))
+             or a32 < (1 << 32))
     if not _full:
         off, nbr = upper_csr(off, nbr)
     h_off = torch.from_numpy(off).pin_memory()

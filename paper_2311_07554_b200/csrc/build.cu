@@ -251,6 +251,14 @@ __global__ void __launch_bounds__(EDGE_THREADS, PACIM_EDGE_BLOCKS) k_edges(const
         rv = b.x + __popc(b.y & ((1u << (v & 31)) - 1));
       }
       lrow = ((uint64_t)ru << 32) | rv;
+    } else if (LEAN == 4 && upper) {
+      const uint64_t c = base >> 5;
+      const uint32_t u = pc_row_of(uc.uoff, uc.ucrow[c], c + 1 < niter ? uc.ucrow[c + 1] : uc.nv - 1, e);
+      const uint32_t v = uc.nbr ? uc.nbr[uc.off[u + 1] - (uc.uoff[u + 1] - e)] : uc.unbr[e];
+      lkey = ((uint64_t)u << 32) | v;
+      const uint2 a = uc.rk[u >> 5], b = uc.rk[v >> 5];
+      lrow = ((uint64_t)(a.x + __popc(a.y & ((1u << (u & 31)) - 1))) << 32) |
+             (b.x + __popc(b.y & ((1u << (v & 31)) - 1)));
     } else if (LEAN == 3 && upper) {
       // lean graphs, upper entries only: e = upper edge index, the row by
       // the upper chunk table (tm1) and the upper offsets, the neighbour at
@@ -294,7 +302,7 @@ __global__ void __launch_bounds__(EDGE_THREADS, PACIM_EDGE_BLOCKS) k_edges(const
       hi = min(hi, j0 + Bb);
       if (hi < lo) hi = lo;
       cnt = hi - lo;
-      const uint64_t ck = LEAN == 2 ? lrow : LEAN ? lkey : ckeys[e];  // the endpoints' store rows (+ hub flags)
+      const uint64_t ck = (LEAN == 2 || LEAN == 4) ? lrow : LEAN ? lkey : ckeys[e];  // the endpoints' store rows (+ hub flags)
       eu = (uint32_t)(ck >> 32);
       ev = (uint32_t)ck;
       ehe = he;
@@ -1103,7 +1111,9 @@ void pc_slot_table(pacim_ctx *ctx) {
 // ---------------------------------------------------------------- HLA
 bool pc_hla_begin(pacim_ctx *ctx, Hla *hla, double max_per_edge) {
   ctx->hla_ok = false;
-  if (ctx->nhub == 0 || ctx->lean) return false;
+  // (HLA recording reads the edge lists' hub flags: not when the build
+  // streams the upper edges and the lists were not derived — c5)
+  if (ctx->nhub == 0 || ctx->lean || (ctx->ucsr && !ctx->elist_ok)) return false;
   const uint32_t B = ctx->R_local;
   // expected live (hub, slot, neighbour) entries: every CSR entry of a hub is
   // live in a slot with its edge probability — p (constant), the mean of
@@ -1266,7 +1276,15 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
       }
     }
     UpperCsr uc;
-    if (ucsr) {
+    if (ucsr && ctx->ucsr_direct) {
+      uc.nv = ctx->n;
+      uc.off = ctx->off.as<uint64_t>();
+      uc.nbr = ctx->upper_src ? nullptr : ctx->nbr.as<uint32_t>();
+      uc.unbr = ctx->upper_src ? ctx->unbr.as<uint32_t>() : nullptr;
+      uc.uoff = ctx->uoff.as<uint64_t>();
+      uc.ucrow = ctx->ucrow.as<uint32_t>();
+      uc.rk = ctx->rk.as<uint2>();
+    } else if (ucsr) {
       uc.nv = ctx->n;
       uc.uoff = ctx->uoff.as<uint64_t>();
       uc.unbr = ctx->unbr.as<uint32_t>();
@@ -1276,7 +1294,20 @@ void pc_sketch_pass(pacim_ctx *ctx, uint32_t *Lb, uint32_t j0, uint32_t Bb,
       uc.ucrow = ctx->ucrow.as<uint32_t>();
       uc.rk = ctx->rk.as<uint2>();
     }
-    if (ucsr) {
+    if (ucsr && ctx->ucsr_direct) {
+      const bool pe = ctx->pmodel != PACIM_P_CONST;
+      auto kern = ctx->hash_rule
+                      ? (pe ? (ep_on ? k_edges<true, false, true, 4, 0, true> : k_edges<true, false, true, 4>)
+                            : (ep_on ? k_edges<false, false, true, 4, 0, true> : k_edges<false, false, true, 4>))
+                      : (pe ? (ep_on ? k_edges<true, false, false, 4, 0, true> : k_edges<true, false, false, 4>)
+                            : (ep_on ? k_edges<false, false, false, 4, 0, true> : k_edges<false, false, false, 4>));
+      PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
+          nullptr, nullptr, pe ? ctx->tm1.as<uint32_t>() : nullptr, ctx->m, ctx->K,
+          pe ? ctx->toff() : ctx->t32, ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, j0, Bb, Lb,
+          ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), nullptr, 0u, hk, ctx->ep,
+          edge_work(ctx, ctx->m, g), uc);
+    } else if (ucsr) {
       const bool pe = ctx->pmodel != PACIM_P_CONST;
       auto kern = ctx->hash_rule
                       ? (pe ? (ep_on ? k_edges<true, false, true, 2, 0, true> : k_edges<true, false, true, 2>)
@@ -1383,6 +1414,28 @@ static void cs_edges(pacim_ctx *ctx, uint32_t *L, const uint2 *rec, uint32_t MW,
         ctx->crow.as<uint32_t>(), nnz, ctx->K, ctx->t32, ctx->d_shr.as<uint32_t>(),
         ctx->d_tab.as<uint16_t>(), B, 0, B, L, ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), rec, MW, pl, Ep{},
         edge_work(ctx, nnz, gl), UpperCsr{ctx->n});
+  } else if (ctx->ucsr && !ctx->elist_ok) {
+    // the upper-edge stream's CSR-direct form (no edge lists derived)
+    const bool pe = ctx->pmodel != PACIM_P_CONST;
+    auto kern = pe ? (ctx->hash_rule ? k_edges<true, false, true, 4, MODE>
+                                     : k_edges<true, false, false, 4, MODE>)
+                   : (ctx->hash_rule ? k_edges<false, false, true, 4, MODE>
+                                     : k_edges<false, false, false, 4, MODE>);
+    PC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    PC_REQUIRE(ctx->rk.p && ctx->ucrow.p, PACIM_ESTATE, "upper-edge stream tables missing");
+    UpperCsr uc;
+    uc.nv = ctx->n;
+    uc.off = ctx->off.as<uint64_t>();
+    uc.nbr = ctx->upper_src ? nullptr : ctx->nbr.as<uint32_t>();
+    uc.unbr = ctx->upper_src ? ctx->unbr.as<uint32_t>() : nullptr;
+    uc.uoff = ctx->uoff.as<uint64_t>();
+    uc.ucrow = ctx->ucrow.as<uint32_t>();
+    uc.rk = ctx->rk.as<uint2>();
+    const unsigned g = pc_grid(ctx, (ctx->m + 31) / 32 * 32, EDGE_THREADS, PACIM_EDGE_BLOCKS);
+    kern<<<g, EDGE_THREADS, smem, ctx->stream>>>(
+        nullptr, nullptr, pe ? ctx->tm1.as<uint32_t>() : nullptr, ctx->m, ctx->K,
+        pe ? ctx->toff() : ctx->t32, ctx->d_shr.as<uint32_t>(), ctx->d_tab.as<uint16_t>(), B, 0, B, L,
+        ctr + 4, Hla{}, ctx->d_hr64.as<uint64_t>(), rec, MW, pl, Ep{}, edge_work(ctx, ctx->m, g), uc);
   } else {
     pc_ensure_edge_lists(ctx);
     const bool pe = ctx->pmodel != PACIM_P_CONST;

@@ -440,7 +440,7 @@ __global__ void k_ep_mask(const unsigned long long *__restrict__ pl, unsigned lo
 
 unsigned long long pc_cs_ep_pairs(pacim_ctx *ctx, uint32_t MW, unsigned long long *ctr) {
   const uint32_t R = ctx->R, P = ctx->world, rank = ctx->rank;
-  if (!pc_dist_active(ctx) || ctx->lean || ctx->hash_rule || R > 256 || ctx->nr >= (1u << 28) ||
+  if (!pc_dist_active(ctx) || ctx->lean || (ctx->ucsr && !ctx->elist_ok) || ctx->hash_rule || R > 256 || ctx->nr >= (1u << 28) ||
       (getenv("PACIM_EP") && !atoi(getenv("PACIM_EP"))) || (P == 1 && !getenv("PACIM_EP")))
     return ~0ull;  // (at one rank only on request: the plain list build is the same work)
   // global slot table (all R sketches, sorted by hi32(hash(r)), then r) and

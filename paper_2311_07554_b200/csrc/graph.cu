@@ -512,12 +512,16 @@ static void derive_edges(pacim_ctx *ctx) {
   //   partitioned and bucketed builds, HLA recording).
   // On first use either way: the per-CSR-entry thresholds (pc_ensure_tcsr:
   // traversal selections, compressed probes, Monte Carlo)
+  // * the CSR-direct form (no per-edge array: rows by the rank map, the
+  //   neighbour from the CSR) when not even the stream fits in a fifth (c5),
+  //   or PACIM_UCSR=4.
   const char *ue = getenv("PACIM_UCSR");
   const int ucsr = ue ? atoi(ue) : -1;
   {
     size_t fr = 0, tot = 0;
     pc_mem_info(ctx, &fr, &tot);
     ctx->ucsr = ucsr > 0 || (ucsr < 0 && 16 * m > tot / 5);
+    ctx->ucsr_direct = ucsr == 4 || (ucsr < 0 && 10 * m > tot / 5);
   }
   const bool per_edge = ctx->pmodel != PACIM_P_CONST;
   if (per_edge) pc_ensure(ctx, ctx->tm1, std::max<size_t>(m, 1) * sizeof(uint32_t));
@@ -552,7 +556,20 @@ static void derive_edges(pacim_ctx *ctx) {
                                                           ctx->hidx.as<uint32_t>(), n,
                                                           ctx->vinfo.as<uint64_t>());
     PC_CHECK_LAUNCH();
-    if (up) {  // lane per upper edge of the upper CSR
+    if (ctx->ucsr && ctx->ucsr_direct) {  // per-edge arrays: tm1 only
+      for (DevBuf *d : {&ctx->ud16, &ctx->uvrow, &ctx->ucrowr}) pc_free(ctx, *d);
+      if (!up) pc_free(ctx, ctx->unbr);
+      if (per_edge && up) {
+        k_edge_derive_up<<<pc_grid(ctx, m, 256, 16), 256, 0, ctx->stream>>>(
+            uoff, ctx->unbr.as<uint32_t>(), ctx->ucrow.as<uint32_t>(), m, n, ctx->vinfo.as<uint64_t>(),
+            ctx->pmodel, ctx->t32, ctx->toff(), nullptr, nullptr, ctx->tm1.as<uint32_t>(), nullptr,
+            nullptr, nullptr, false);
+      } else if (per_edge) {
+        k_edge_derive<<<pc_grid(ctx, nnz, 256), 256, 0, ctx->stream>>>(
+            off, nbr, ctx->crow.as<uint32_t>(), nnz, uoff, ctx->vinfo.as<uint64_t>(), ctx->pmodel,
+            ctx->t32, ctx->toff(), nullptr, nullptr, ctx->tm1.as<uint32_t>(), nullptr);
+      }
+    } else if (up) {  // lane per upper edge of the upper CSR
       const bool vrow = ucsr != 2 && ucsr != 3;
       if (ctx->ucsr) {
         pc_ensure(ctx, ctx->ud16, m * 2);
@@ -736,11 +753,12 @@ static void derive_lean(pacim_ctx *ctx) {
 
 // lean when asked (PACIM_LEAN=1) or when the edge lists (keys + ckeys, 16 B
 // per upper edge) would take more than a third of the device
+// (round 2, late: no longer by default — graphs whose edge lists do not fit
+// take the CSR-direct form of the edge stream, which keeps the store-row
+// compaction: c5's batch passes then skip the isolated vertices' rows)
 static bool want_lean(pacim_ctx *ctx) {
   if (const char *e = getenv("PACIM_LEAN")) return atoi(e) != 0;
-  size_t fr = 0, tot = 0;
-  pc_mem_info(ctx, &fr, &tot);
-  return ctx->pmodel == PACIM_P_CONST && 16 * ctx->m > tot / 3;
+  return false;
 }
 
 void pc_graph_finish_load(pacim_ctx *ctx, int validate) {

@@ -276,6 +276,7 @@ struct pacim_ctx {
   bool tcsr_ok = false;
   bool elist_ok = false;
   bool ucsr = false;      // the build streams the upper edges (UpperCsr), derive_edges
+  bool ucsr_direct = false;  // ... without per-edge arrays (UpperCsr's CSR-direct form)
   // graphs loaded as an upper CSR (pacim_load_graph_upper[_async]): the upper
   // CSR stays in uoff / unbr, off holds the symmetric offsets (from the
   // degrees), and the symmetric neighbour lists nbr are built only when
@@ -519,8 +520,15 @@ struct EdgeSet {
 // store row uvrow[e] (or, PACIM_UCSR=2, the rank map).  10 B per edge (+ 4 B
 // tm1) instead of keys + ckeys' 16, and no load depends on another: a
 // dependent rank-map gather in k_edges' front end cost 22.8 -> 31.5 ms at c4.
+// CSR-direct form (k_edges LEAN = 4, `ucsr_direct`: graphs for which even
+// the stream does not fit — c5): no per-edge array at all; the row by the
+// chunk table and pc_row_of, the neighbour at the row's upper part of the
+// symmetric CSR (off, nbr; or unbr[e] for an upper-loaded graph), both store
+// rows by the rank map, the threshold t32 or tm1[e]
 struct UpperCsr {
   uint32_t nv = 0;  // vertices
+  const uint64_t *off = nullptr;  // LEAN = 4: the symmetric offsets
+  const uint32_t *nbr = nullptr;  // LEAN = 4: the symmetric lists (null: unbr)
   const uint64_t *uoff = nullptr;
   const uint32_t *unbr = nullptr, *ucrow = nullptr, *uvrow = nullptr, *ucrowr = nullptr;
   const uint16_t *ud16 = nullptr;

@@ -168,6 +168,14 @@ def test_c5_shape_scale16_lean_bucketed(orc, ctx, monkeypatch):
     assert ctx.pacim_get_stats()["rows"] == 1 << 16
 
 
+@pytest.mark.parametrize("i", [0, 1, 3, 9, 10])
+def test_compressed_csr_direct(orc, ctx, i, monkeypatch):
+    """Compressed builds over the CSR-direct edge form (PACIM_UCSR=4: c5's
+    default at full scale — store rows compacted, no edge lists, no HLA)."""
+    monkeypatch.setenv("PACIM_UCSR", "4")
+    run_case(orc, ctx, i, check_sketches=True)
+
+
 @pytest.mark.parametrize("upper", ["1", "0"])
 @pytest.mark.parametrize("i", [0, 1, 3, 9])
 def test_compressed_lean(orc, ctx, i, upper, monkeypatch):

@@ -100,6 +100,14 @@ def test_tiny_corpus_parity(orc, ctx, i):
     full_parity(orc, ctx, g, model, t32, R, 1000 + i, min(k, g.n))
 
 
+@pytest.mark.parametrize("i", [0, 2, 3, 7, 10])
+def test_compact_store_csr_direct(orc, ctx, i, monkeypatch):
+    """The compact store's mask and union passes over the CSR-direct edge
+    form (PACIM_UCSR=4, no edge lists derived): the oracle's parity."""
+    monkeypatch.setenv("PACIM_UCSR", "4")
+    test_tiny_corpus_parity_compact_store(orc, ctx, i, monkeypatch)
+
+
 @pytest.mark.parametrize("i", range(len(CASES)))
 def test_tiny_corpus_parity_compact_store(orc, ctx, i, monkeypatch):
     """The compact store forced (PACIM_STORE=compact; by default a one-GPU
@@ -131,14 +139,16 @@ def gapped_graph(nv, m, gap, seed):
     return inputs.csr_from_edges(nv * gap, e)
 
 
-@pytest.mark.parametrize("ucsr", ["1", "0", "2", "3"])
+@pytest.mark.parametrize("ucsr", ["1", "0", "2", "3", "4"])
 @pytest.mark.parametrize("i", [0, 2, 3, 7, 10, 12, -1])
 def test_dense_store_edge_streams(orc, ctx, i, ucsr, monkeypatch):
     """The dense store's upper-edge stream (UpperCsr: neighbours, row deltas
     and the neighbours' rows per edge; 1, the default when the edge lists
     would take more than a fifth of the device), the edge lists
     keys / ckeys (0), the neighbours' rows from the rank map (2), every delta
-    capped so the offsets walk and the rank map serve every edge (3): the
+    capped so the offsets walk and the rank map serve every edge (3), the
+    CSR-direct form (4: no per-edge array, the default when not even the
+    stream fits — c5): the
     same oracle parity (labels, gain0, seeds, gains).  i = -1: a graph whose
     runs of isolated vertices exceed a byte (deltas overflow naturally)."""
     monkeypatch.setenv("PACIM_STORE", "dense")
@@ -382,7 +392,7 @@ def test_upper_csr_load(orc, ctx, i, mode):
     assert np.array_equal(ctx.pacim_get_gain0(), eg0)
 
 
-@pytest.mark.parametrize("ucsr", ["0", "1"])
+@pytest.mark.parametrize("ucsr", ["0", "1", "4"])
 @pytest.mark.parametrize("sel", [0, 1, 2])
 @pytest.mark.parametrize("i", [0, 3, 7, 10, 12])
 def test_upper_load_deferred_sym(orc, ctx, i, sel, ucsr, monkeypatch):
