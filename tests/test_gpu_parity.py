@@ -724,20 +724,23 @@ def test_c4_full_scale_certified(orc, ctx):
     assert info[3] == sg[-1]          # Σ_r |∪_i C_r(s_i)| = N(S_k)
 
 
-@pytest.mark.parametrize("lean", [True])
-def test_c5_shape_scale25_certified(orc, ctx, lean, monkeypatch):
+@pytest.mark.parametrize("form", ["direct"])
+def test_c5_shape_scale25_certified(orc, ctx, form, monkeypatch):
     """BASELINE.json configs[4]'s generator and method (web R-MAT .6/.15/.15/.1,
     ef 32, p = 0.01, R = 256, compressed alpha = 1/16, k = 100) at scale 25
     (n = 2^25): the full-size c5 CSR (58 GB) does not fit the oracle's host,
     so SURVEY 8(c)'s fallback scale is used.  The GPU's CSR equals the
     oracle generator's (golden digest, tests/golden/c5_s25_graph.json), and
     the GPU's seeds and gains are certified by the oracle's verify mode.
-    lean: the path c5 takes at full scale (no edge lists, k_edges over the
-    CSR, source-bucketed generator)."""
+    form "direct": the path c5 takes at full scale (the CSR-direct edge form
+    — no edge lists, rows by the rank map — and the source-bucketed
+    generator); the lean layout (rows = vertex ids) is covered by the small
+    lean tests."""
     path = os.path.join(GOLD, "c5_s25_graph.json")
     gold = json.load(open(path))
-    if lean:
-        monkeypatch.setenv("PACIM_LEAN", "1")
+    lean = False
+    if form == "direct":
+        monkeypatch.setenv("PACIM_UCSR", "4")
         monkeypatch.setenv("PACIM_GEN_BUCKETS", "8")
     from oracle.oracle import Graph
     from paper_2311_07554_b200 import pipeline
