@@ -585,6 +585,10 @@ void pc_build_compressed(pacim_ctx *ctx) {
   // and so is the HLA of an earlier build; its batch parent arrays are kept
   // for reuse (choose_batch counts them as free)
   pc_cs_free(ctx);  // a compact store of an earlier build
+  // the selection's Get-center probes read the symmetric lists and the
+  // per-entry thresholds: derived before the batch takes the free memory
+  // (derived lazily after it, c4 at alpha = 1/2 ran out of memory)
+  pc_ensure_tcsr(ctx);
   ctx->ep = Ep{};   // batch stores are reset in line (no slot epochs)
   ctx->skip_init = false;
   for (DevBuf *d : {&ctx->L, &ctx->bfs, &ctx->pkeys, &ctx->hla_off, &ctx->hla_row, &ctx->hla_raw})
