@@ -375,6 +375,7 @@ def main():
     # Lean graphs and compressed builds (c5) send the symmetric CSR: their
     # build or Get-center probes read it, and the device-side transpose of an
     # upper CSR needs 16 B of scratch per edge (133 GB at c5)
+    out_dev = out  # the resident path's result: the e2e path must reproduce it
     off, nbr = ctx.pacim_get_graph()
     _full = (bool(os.environ.get("PACIM_E2E_FULL")) or bool(st.get("lean"))
              or a32 < (1 << 32))
@@ -454,6 +455,12 @@ def main():
     torch.cuda.synchronize(dev)
     barrier()
     ms_e2e = f0.elapsed_time(f1)
+    # the e2e path (host CSR, another load and derivation) must give the
+    # resident path's seeds and gains bit for bit
+    e2e_same = (np.array_equal(np.asarray(out[0]), np.asarray(out_dev[0]))
+                and np.array_equal(np.asarray(out[1]), np.asarray(out_dev[1])))
+    if not e2e_same:
+        print("ERROR: the e2e seeds/gains differ from the resident path's", file=sys.stderr)
     if world > 1:
         t = torch.tensor([ms_e2e], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
@@ -523,6 +530,7 @@ def main():
         "build_tests_per_s": R * m / (avg["t_build_ms"] / 1000.0),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": ms_e2e / args.e2e_steps,
+                "same_seeds_and_gains_as_resident": bool(e2e_same),
                 "mode": e2e_mode},
         "gpu_launches": launches,
         "roofline": roofline,

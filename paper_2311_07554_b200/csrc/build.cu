@@ -22,6 +22,7 @@
 //   k_gain_scatter    gain0[v] = sum_j |C_j(v)| (H7) and the member index
 //                     perm grouped by component (H6u); hot-component cursor
 //                     reservations aggregated per tile in shared memory
+#include <type_traits>
 #include <chrono>
 #include <algorithm>
 #include <cstdlib>
@@ -656,6 +657,76 @@ __global__ void __launch_bounds__(256, 8) k_compress_list(uint32_t *L, uint32_t 
   for (uint32_t j = threadIdx.x; j < H; j += blockDim.x)
     if (hcnt[j]) add_to_root(L, B, j, hroot[j], hcnt[j], ep, ld_cg(L + (size_t)hroot[j] * B + j));
   add_count(ctr + 1, nnr);
+}
+
+// ------------------------------------------------------- k_gain0_narrow
+// k_gain0 for narrow stores (B <= 32 S slots, S = 1, 2, 4: a rank's shard of
+// a sharded build, P >= 2 at R = 256): S slots per lane and 32 / S rows per warp
+// iteration (32 loads in flight per lane, as k_gain0's 8 slots x 4 rows); the
+// per-row sums through shared memory (lane r adds row r's 32 partials) —
+// k_gain0 kept 8 slot loads per lane of which B = 32 used one (c4 shard at
+// P = 8: 7.7 ms for an eighth of the one-GPU store)
+template <bool EP, int S>
+__global__ void __launch_bounds__(256) k_gain0_narrow(const uint32_t *__restrict__ L, uint32_t n,
+                                                      uint32_t B, const uint32_t *rmap,
+                                                      int64_t *gain0, int acc,
+                                                      unsigned long long *ncc_ctr, Ep ep_in) {
+  const Ep ep = EP ? ep_in : Ep{};
+  constexpr int GR = 32 / S;
+  using part_t = typename std::conditional<(S <= 2), uint32_t, unsigned long long>::type;
+  __shared__ part_t red[8][GR][33];
+  unsigned long long ncc = 0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t szm = PACIM_LOW & ~ep.mask;
+  for (size_t v0 = warp * GR; v0 < n; v0 += nw * GR) {
+    uint32_t sv[GR][S];
+#pragma unroll
+    for (int r = 0; r < GR; r++)
+#pragma unroll
+      for (int i = 0; i < S; i++) {
+        const uint32_t j = lane + 32 * i;
+        sv[r][i] = (j < B && v0 + r < n) ? L[(v0 + r) * B + j] : NONE;
+      }
+#pragma unroll
+    for (int r = 0; r < GR; r++)
+#pragma unroll
+      for (int i = 0; i < S; i++) {
+        const uint32_t j = lane + 32 * i, raw = sv[r][i];
+        if (raw == NONE) continue;
+        const bool cur = (raw & ep.mask) == ep.tag;
+        const uint32_t s = raw & ~ep.mask;
+        if (!cur || (raw & PACIM_HIGH)) {
+          ncc += cur && (s & PACIM_LOW) >= 2;
+          if (!cur) sv[r][i] = (PACIM_HIGH | 1u) | ep.tag;
+        } else {
+          sv[r][i] = __ldg(L + (size_t)s * B + j);  // the root's word (of this epoch)
+        }
+      }
+#pragma unroll
+    for (int r = 0; r < GR; r++) {
+      part_t p = 0;  // S <= 2: at most two sizes below 2^31 fit 32 bits
+#pragma unroll
+      for (int i = 0; i < S; i++)
+        if (sv[r][i] != NONE) p += sv[r][i] & szm;
+      red[wid][r][lane] = p;
+    }
+    __syncwarp();
+    if (lane < GR && v0 + lane < n) {
+      long long t = 0;
+#pragma unroll 8
+      for (int l = 0; l < 32; l++) t += red[wid][lane][l];
+      const uint32_t v = rmap[v0 + lane];
+      if (acc) {
+        if (t != (long long)B) gain0[v] += t - (long long)B;
+      } else {
+        gain0[v] = t;
+      }
+    }
+    __syncwarp();
+  }
+  add_count(ncc_ctr, ncc);
 }
 
 // ---------------------------------------------------------------- k_gain0
@@ -1779,6 +1850,13 @@ void pc_build(pacim_ctx *ctx) {
                                          ctx->d_hot.as<uint32_t>(), ctx->d_hot_size.as<uint32_t>(),
                                          big_t, ctx->hotsum.as<int64_t>(), ctx->ep);
         }
+      } else if (c <= 128 && !(getenv("PACIM_GAIN_NARROW") && !atoi(getenv("PACIM_GAIN_NARROW")))) {
+        const int S = c <= 32 ? 1 : c <= 64 ? 2 : 4;
+        auto kg = S == 1 ? (ep_on ? k_gain0_narrow<true, 1> : k_gain0_narrow<false, 1>)
+                : S == 2 ? (ep_on ? k_gain0_narrow<true, 2> : k_gain0_narrow<false, 2>)
+                         : (ep_on ? k_gain0_narrow<true, 4> : k_gain0_narrow<false, 4>);
+        kg<<<pc_grid(ctx, (size_t)n * S, 256, 8), 256, 0, ctx->stream>>>(
+            Lw, n, c, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>(), 0, ctr, ctx->ep);
       } else {
         auto kg = ep_on ? k_gain0<false, true> : k_gain0<false, false>;
         kg<<<rows_grid, 256, 0, ctx->stream>>>(Lw, n, c, ctx->rmap.as<uint32_t>(),

@@ -164,6 +164,21 @@ def test_dense_store_edge_streams(orc, ctx, i, ucsr, monkeypatch):
     assert ctx.pacim_get_stats()["store"] == 0
 
 
+@pytest.mark.parametrize("narrow", ["1", "0"])
+@pytest.mark.parametrize("R", [1, 31, 32, 33, 64, 65, 100, 128, 129])
+def test_gain_narrow_store(orc, ctx, R, narrow, monkeypatch):
+    """gain0 of narrow dense stores (B <= 128 slots: S = 1, 2, 4 slots per
+    lane, 32 / S rows per warp iteration, row sums through shared memory)
+    against the oracle, and the generic kernel (PACIM_GAIN_NARROW=0)."""
+    from oracle.oracle import Graph
+    monkeypatch.setenv("PACIM_STORE", "dense")
+    monkeypatch.setenv("PACIM_GAIN_NARROW", narrow)
+    off, nbr = inputs.random_powerlaw_graph(3000, 20000, 61)
+    g = Graph(len(off) - 1, off, nbr)
+    model, t32 = model_of(orc, 0.1)
+    full_parity(orc, ctx, g, model, t32, R, 900 + R, 8)
+
+
 @pytest.mark.parametrize("hl", ["1", "0", "40"])
 @pytest.mark.parametrize("bits", ["1", "2", "6"])
 @pytest.mark.parametrize("i", [0, 3, 7, 9, 10, 12])
