@@ -461,13 +461,15 @@ __device__ __forceinline__ void add_to_root(uint32_t *L, uint32_t B, uint32_t j,
                                             uint32_t cnt, Ep ep = Ep{}, uint32_t root_raw = 0) {
   uint32_t *a = L + (size_t)root * B + j;
   if ((root_raw & ep.mask) != ep.tag) {
-    // a stale root slot (a singleton until this build): HIGH | 1 of this
-    // epoch first (racing members: the first CAS wins, the others see a
-    // current word)
+    // a stale root slot (a singleton until this build): the claim writes
+    // HIGH | (1 + cnt) of this epoch in one CAS (the claimer's count rides
+    // on it: one random atomic per CC fewer); racing members: the first CAS
+    // wins, the others see a current word and add
     uint32_t x = root_raw;
     for (;;) {
-      const uint32_t y = atomicCAS(a, x, (PACIM_HIGH | 1u) | ep.tag);
-      if (y == x || (y & ep.mask) == ep.tag) break;
+      const uint32_t y = atomicCAS(a, x, ((PACIM_HIGH | 1u) | ep.tag) + cnt);
+      if (y == x) return;
+      if ((y & ep.mask) == ep.tag) break;
       x = y;
     }
   }
