@@ -252,11 +252,17 @@ PACIM_API int pacim_load_graph_async(pacim_ctx *ctx, uint32_t n, uint64_t nnz,
 /* H0 from the UPPER CSR: each undirected edge {u, v} given once, in row
  * min(u, v) — uoffsets[n+1] (host, uoffsets[0] = 0, uoffsets[n] = m), and
  * uneighbors[m] (host): row u lists its neighbours v > u in increasing order.
- * Half the bytes of the symmetric CSR cross PCIe; the device builds the
- * symmetric CSR (lower lists by a transpose: target histogram, scan, atomic
- * cursors, per-vertex segmented sort; rows = sorted lower ++ upper), so the
- * graph is exactly the one pacim_load_graph would load from the symmetric
- * CSR of the same edge set ("symmetrize", R14).  validate: 0 = trust
+ * Half the bytes of the symmetric CSR cross PCIe.  The upper CSR stays on the
+ * device (SURVEY H0's build input: the dense store's build and the Win-Tree
+ * selection read only the upper edges); the symmetric offsets come from the
+ * degrees at once, and the symmetric neighbour lists (lower lists by a
+ * transpose: stable radix sort of the upper pairs by target; rows = sorted
+ * lower ++ upper) are built on the device only when something reads them
+ * (traversal selections, Get-center probes, Monte Carlo, pacim_get_graph) —
+ * the graph is exactly the one pacim_load_graph would load from the
+ * symmetric CSR of the same edge set ("symmetrize", R14).  The
+ * transpose needs 16 B of device scratch per edge (ENOMEM beyond: send the
+ * symmetric CSR instead).  validate: 0 = trust
  * the caller; != 0 = check offsets, 0 <= u < v < n and strictly increasing
  * rows on the device (EINVAL naming the first bad vertex).  Other EINVAL and
  * the model as for pacim_load_graph; m = 0 is allowed (n isolated vertices).
@@ -266,9 +272,9 @@ PACIM_API int pacim_load_graph_upper(pacim_ctx *ctx, uint32_t n, uint64_t m,
                                      int pmodel, uint64_t t32, int validate);
 
 /* Pipelined pacim_load_graph_upper (validate = 0): the copies of the upper
- * CSR are enqueued on the copy stream like pacim_load_graph_async, and the
- * symmetrization runs on the ctx stream when the next pacim_build_sketches
- * commits the load.  Same rules as pacim_load_graph_async (at most two
+ * CSR are enqueued on the copy stream like pacim_load_graph_async; the next
+ * pacim_build_sketches commits the load (degrees, symmetric offsets, the
+ * build's edge form; the symmetric lists on first read, as above).  Same rules as pacim_load_graph_async (at most two
  * pending loads, host arrays valid and unmodified until committed, pinned
  * for overlap). */
 PACIM_API int pacim_load_graph_upper_async(pacim_ctx *ctx, uint32_t n, uint64_t m,
