@@ -42,6 +42,17 @@ import time
 
 import numpy as np
 
+# stdout carries only the JSON line: native output (the image sets
+# NCCL_DEBUG=VERSION, whose banner NCCL prints to stdout at communicator
+# init) goes to stderr — fd 1 is pointed at stderr and the JSON line is
+# written to the saved original stdout
+_JSON_FD = os.dup(1)
+os.dup2(2, 1)
+
+
+def emit(line: dict) -> None:
+    os.write(_JSON_FD, (json.dumps(line) + "\n").encode())
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -229,7 +240,7 @@ def run_reference(args, cfg):
                          "sample": sample, **host_info()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 # ------------------------------------------------------------------- ours
@@ -562,7 +573,7 @@ def main():
                         "labellings at the sampled rate (the selection of c4 adds seconds)"},
             **host_info()}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     ctx.close()
     if use_dist:
         torch.distributed.destroy_process_group()
