@@ -451,11 +451,15 @@ def test_upper_load_deferred_sym(orc, ctx, i, sel, ucsr, monkeypatch):
     assert np.array_equal(o2, np.asarray(off, np.uint64)) and np.array_equal(n2, np.asarray(nbr, np.uint32))
 
 
-def test_upper_csr_load_edge_cases(orc, ctx, pc):
+@pytest.mark.parametrize("ucsr", [None, "1", "4"])
+def test_upper_csr_load_edge_cases(orc, ctx, pc, ucsr, monkeypatch):
     """Upper loads: no edges, isolated vertices between and after the edges,
     a hub whose lower list spans many chunks, and invalid upper CSRs (an entry
-    v <= u, unsorted rows, v >= n, offsets[n] != m) raise."""
+    v <= u, unsorted rows, v >= n, offsets[n] != m) raise — with each form of
+    the build's edge stream."""
     from oracle.oracle import Graph
+    if ucsr:
+        monkeypatch.setenv("PACIM_UCSR", ucsr)
     ctx.pacim_load_graph_upper(np.zeros(9, np.uint64), np.zeros(0, np.uint32), 0, 1 << 31, 1)
     o2, n2 = ctx.pacim_get_graph()
     assert list(o2) == [0] * 9 and len(n2) == 0
@@ -498,15 +502,19 @@ def test_upper_csr_load_c2(ctx):
     assert (sha(o2), sha(n2)) == h
 
 
+@pytest.mark.parametrize("ucsr", [None, "1", "4"])
 @pytest.mark.parametrize("p", [0.4, "wic", ("unif", 0.2, 0.6)])
-def test_load_derivation_shapes(orc, ctx, p):
+def test_load_derivation_shapes(orc, ctx, p, ucsr, monkeypatch):
     """The load's edge pass (rows of CSR entries from the 32-entry chunk
     table, one packed (degree, row + hub flag) gather per entry) on shapes
     that stress it: isolated vertices between and after the edges, a hub whose
     list spans several chunks next to degree-1 rows, a chunk starting inside a
     row; and an edgeless graph.  Labels, gain0 and the greedy equal the
-    oracle's under the constant, WIC and Uniform models."""
+    oracle's under the constant, WIC and Uniform models — with each form of
+    the build's edge stream (ucsr: default lists, the stream, CSR-direct)."""
     from oracle.oracle import Graph
+    if ucsr:
+        monkeypatch.setenv("PACIM_UCSR", ucsr)
     model, t32 = model_of(orc, p)
     n = 300
     edges = [(0, v) for v in range(5, 300, 2)] + [(7, 9), (11, 13), (250, 251), (3, 290)]
@@ -517,15 +525,17 @@ def test_load_derivation_shapes(orc, ctx, p):
     full_parity(orc, ctx, Graph(40, off, nbr), model, t32, 5, 78, 4)
 
 
-@pytest.mark.parametrize("big_t", [None, "8"])
+@pytest.mark.parametrize("big_t,ucsr", [(None, None), ("8", None), (None, "1"), (None, "4")])
 @pytest.mark.parametrize("R,p", [(1000, 0.02), (1023, 0.1), (520, "wic")])
-def test_many_sketches(orc, ctx, R, p, big_t, monkeypatch):
+def test_many_sketches(orc, ctx, R, p, big_t, ucsr, monkeypatch):
     """R above 256 on one GPU (several 256-slot blocks per store row, up to
     1024 slots, odd counts): labels of sampled sketches, gain0 and the greedy
     equal the oracle's, also with the dense pass forced."""
     from oracle.oracle import Graph
     if big_t:
         monkeypatch.setenv("PACIM_BIG_T", big_t)
+    if ucsr:
+        monkeypatch.setenv("PACIM_UCSR", ucsr)
     off, nbr = inputs.random_powerlaw_graph(600, 2400, 31)
     g = Graph(600, off, nbr)
     model, t32 = model_of(orc, p)
