@@ -108,6 +108,80 @@ __global__ void k_gain_sizes(const uint32_t *Lb, uint32_t nr, uint32_t Bb, const
   if (lane == 0 && ncc) atomicAdd(ncc_ctr, ncc);
 }
 
+// k_gain_sizes for narrow batches (Bb <= 32 S slots): S slots per lane and
+// 16 / S rows per warp iteration, every row's slot words and then every
+// non-root's root word in flight together, the per-row sums through shared
+// memory (lane r adds row r's 32 partials).  The warp-per-row kernel kept one
+// dependent pair of loads in flight per lane and spent 20 shuffles per row
+// (c5: ~37-slot batches, 27 ms of gain pass per batch)
+template <int S>
+__global__ void __launch_bounds__(256) k_gain_sizes_n(const uint32_t *Lb, uint32_t nr, uint32_t Bb,
+                                                      const uint32_t *rmap, int64_t *gain0,
+                                                      unsigned long long *ncc_ctr,
+                                                      const uint32_t *hot, uint32_t j0,
+                                                      uint32_t big_t, uint32_t *hot_size,
+                                                      int64_t *hotsum) {
+  constexpr int GR = 16 / S;
+  __shared__ uint32_t redg[8][GR][33], redh[8][GR][33];
+  unsigned long long ncc = 0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const size_t warp = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const size_t nw = ((size_t)gridDim.x * blockDim.x) >> 5;
+  if (warp == 0)
+    for (uint32_t j = lane; j < Bb; j += 32)
+      hot_size[j0 + j] = hot[j] < nr ? (Lb[(size_t)hot[j] * Bb + j] & PACIM_LOW) : 0u;
+  uint32_t hj[S];
+#pragma unroll
+  for (int i = 0; i < S; i++) hj[i] = (lane + 32 * i < Bb) ? hot[lane + 32 * i] : NONE;
+  for (size_t v0 = warp * GR; v0 < nr; v0 += nw * GR) {
+    uint32_t sv[GR][S], rt[GR][S];
+#pragma unroll
+    for (int r = 0; r < GR; r++)
+#pragma unroll
+      for (int i = 0; i < S; i++) {
+        const uint32_t j = lane + 32 * i;
+        sv[r][i] = (j < Bb && v0 + r < nr) ? Lb[(v0 + r) * Bb + j] : (PACIM_HIGH | 1u);
+      }
+#pragma unroll
+    for (int r = 0; r < GR; r++)
+#pragma unroll
+      for (int i = 0; i < S; i++) {
+        const uint32_t s = sv[r][i];
+        rt[r][i] = (s & PACIM_HIGH) ? s : Lb[(size_t)s * Bb + lane + 32 * i];  // the root's word
+      }
+#pragma unroll
+    for (int r = 0; r < GR; r++) {
+      uint32_t g = 0, h = 0;  // < 2^32: at most two sizes below 2^31 (S <= 2)
+#pragma unroll
+      for (int i = 0; i < S; i++) {
+        const uint32_t s = sv[r][i];
+        if (s == (PACIM_HIGH | 1u)) continue;  // singleton: size 1, already counted
+        ncc += (s & PACIM_HIGH) != 0;
+        const uint32_t sz = rt[r][i] & PACIM_LOW;
+        g += sz - 1;
+        const uint32_t root = (s & PACIM_HIGH) ? (uint32_t)(v0 + r) : s;
+        if (root == hj[i] && sz > big_t) h += sz;
+      }
+      redg[wid][r][lane] = g;
+      redh[wid][r][lane] = h;
+    }
+    __syncwarp();
+    if (lane < GR && v0 + lane < nr) {
+      long long g = 0, h = 0;
+#pragma unroll 8
+      for (int l = 0; l < 32; l++) {
+        g += redg[wid][lane][l];
+        h += redh[wid][lane][l];
+      }
+      if (g) gain0[rmap[v0 + lane]] += g;
+      if (h) hotsum[rmap[v0 + lane]] += h;
+    }
+    __syncwarp();
+  }
+  for (int d = 16; d; d >>= 1) ncc += __shfl_xor_sync(0xffffffffu, ncc, d);
+  if (lane == 0 && ncc) atomicAdd(ncc_ctr, ncc);
+}
+
 // center i, batch slot jj: its CC's root row (NONE: singleton) and CC size
 __global__ void k_center_a(const uint32_t *Lb, uint32_t Bb, uint32_t rho, const uint32_t *centers,
                            const uint32_t *cid, uint32_t *croot, uint32_t *csz, uint32_t B,
@@ -665,10 +739,18 @@ void pc_build_compressed(pacim_ctx *ctx) {
     cudaEvent_t *ev = bev.data() + 5 * (size_t)(j0 / Bb);
     PC_CUDA(cudaEventRecord(ev[0], ctx->stream));
     pc_sketch_pass(ctx, Lb, j0, bb, ctr, ev + 1, rec_hla ? &hla : nullptr);
-    k_gain_sizes<<<pc_grid(ctx, (size_t)nr * 32, 256, 16), 256, 0, ctx->stream>>>(
-        Lb, nr, bb, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>(), ctr,
-        ctx->d_hot.as<uint32_t>(), j0, ctx->cbig_t, ctx->d_hot_size.as<uint32_t>(),
-        ctx->hotsum.as<int64_t>());
+    if (bb <= 64 && !(getenv("PACIM_GAIN_NARROW") && !atoi(getenv("PACIM_GAIN_NARROW")))) {
+      auto kg = bb <= 32 ? k_gain_sizes_n<1> : k_gain_sizes_n<2>;
+      kg<<<pc_grid(ctx, (size_t)nr * (bb <= 32 ? 2 : 4), 256, 8), 256, 0, ctx->stream>>>(
+          Lb, nr, bb, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>(), ctr,
+          ctx->d_hot.as<uint32_t>(), j0, ctx->cbig_t, ctx->d_hot_size.as<uint32_t>(),
+          ctx->hotsum.as<int64_t>());
+    } else {
+      k_gain_sizes<<<pc_grid(ctx, (size_t)nr * 32, 256, 16), 256, 0, ctx->stream>>>(
+          Lb, nr, bb, ctx->rmap.as<uint32_t>(), ctx->gain0.as<int64_t>(), ctr,
+          ctx->d_hot.as<uint32_t>(), j0, ctx->cbig_t, ctx->d_hot_size.as<uint32_t>(),
+          ctx->hotsum.as<int64_t>());
+    }
     PC_CHECK_LAUNCH();
     PC_CUDA(cudaEventRecord(ev[4], ctx->stream));
     const size_t tot = (size_t)rho * bb;
