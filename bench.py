@@ -509,6 +509,10 @@ def main():
                 "share_of_step": round(dur[dom] / ms_step, 3),
                 "kernel_ms": {kk: round(v, 4) for kk, v in dur.items()},
                 "kernel_bytes": kb,
+                "kernel_bytes_note": ("§8(d) terms per kernel (k_init 4 B, k_compress_count 8 B, k_gain0 4 B "
+                                      "per (row, sketch)); a dense epoch build with the hook list "
+                                      "(stats.build_hook_list = 1) compresses only the hooked slots, so "
+                                      "k_compress_count's bytes / ms may exceed the HBM peak"),
                 "build": {"model": "SURVEY 8(d): ceil(R_g/B)*(CSR_upper [+4m WIC/Uniform]) + 16*rows*R_g, "
                                    "CSR_upper = 4m + 8(n+1); rows = store rows (non-isolated vertices); "
                                    "'frac_n' counts 16*n*R_g as the formula is written",
@@ -552,7 +556,7 @@ def main():
         "roofline": roofline,
         "clocks": clk,
         "stats": {kk: st[kk] for kk in ("rows", "ncomp", "nnonsingle", "live_pairs", "device_bytes",
-                                        "select_member_updates",
+                                        "select_member_updates", "build_hook_list",
                                         "select_dense_steps", "select_warp_slots",
                                         "select_deferred_slots", "select_row_items",
                                         "select_chunk_items", "select_edges")},
