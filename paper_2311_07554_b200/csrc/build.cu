@@ -38,6 +38,9 @@ constexpr uint32_t HOT_MAX = 1024;  // slots with a shared-memory hot-root cache
 // warp-per-row kernels win from ~16 slots up, e.g. c4's 23-slot batch)
 constexpr uint32_t NARROW_W = 16;
 constexpr uint32_t NONE = 0xFFFFFFFFu;
+#ifndef PACIM_UF_KEEP
+#define PACIM_UF_KEEP 1  // uf_unite keeps the unmoved side's word (A/B: -DPACIM_UF_KEEP=0)
+#endif
 
 __device__ __forceinline__ uint32_t ld_cg(const uint32_t *p) { return __ldcg(p); }
 
@@ -82,6 +85,45 @@ __device__ __forceinline__ void uf_unite(uint32_t *L, uint32_t B, uint32_t j, ui
   // ep: slot epochs (a stale slot is a root; every write carries ep.tag and
   // every CAS expects the raw word it read)
   uint32_t *Lj = L + j;
+#if PACIM_UF_KEEP
+  // the side that did not move keeps the word it read: parents only
+  // decrease, so a stale word names an ancestor (same set, smaller id) and
+  // every hook is still a CAS against the word read; a failed CAS returns
+  // the current word, which replaces the re-read
+  uint32_t ru = ld_cg(Lj + (size_t)u * B), rv = ld_cg(Lj + (size_t)v * B);
+  for (;;) {
+    uint32_t pu = ep_rd(ru, ep), pv = ep_rd(rv, ep);
+    if (pu & PACIM_HIGH) pu = u;
+    if (pv & PACIM_HIGH) pv = v;
+    if (pu == pv) return;
+    if (pu < pv) {
+      uint32_t t = u;
+      u = v;
+      v = t;
+      t = pu;
+      pu = pv;
+      pv = t;
+      t = ru;
+      ru = rv;
+      rv = t;
+    }
+    if (u == pu) {
+      const uint32_t got = atomicCAS(Lj + (size_t)u * B, ru, pv | ep.tag);
+      if (got == ru) {  // hooked root u under pv
+        if (hu) {
+          *hu = u;
+          *hp = pv;
+        }
+        return;
+      }
+      ru = got;
+    } else {
+      atomicCAS(Lj + (size_t)u * B, ru, pv | ep.tag);  // splice (may lose a race harmlessly)
+      u = pu;
+      ru = ld_cg(Lj + (size_t)u * B);
+    }
+  }
+#endif
   for (;;) {
     const uint32_t ru = ld_cg(Lj + (size_t)u * B), rv = ld_cg(Lj + (size_t)v * B);
     uint32_t pu = ep_rd(ru, ep), pv = ep_rd(rv, ep);
